@@ -1,0 +1,176 @@
+"""CPU oracle for TPGen's hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_2210_16998_b200``) never imports it and shares no code
+with it.
+
+Contents
+  * ``oracle.c`` (tier 1): DFS prime-path enumerator following Def. 1
+     with the operational maximality test, E_canon counter,
+    digest, lexmin-shortest prefix/suffix tables for test paths.
+  * ``brute.py`` (tier 0): the definition itself -- all simple paths, minus the
+    proper contiguous subpaths of other simple paths -- for tiny graphs.
+  * this module: ctypes wrappers + test-path assembly (a plain loop).
+
+Parity status: PP set, E_canon, digest and the TP
+prefix/suffix tables are pinned by tests/test_oracle.py (worked example P:230-255,
+closed forms P:626-643, DAG = Npath P:604, tier-0 brute force, brute-force
+lexmin walks, invariants).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain C, -O2)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.POINTER
+        lib.oracle_prime_paths.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32),
+                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           P(P(ctypes.c_int64)), P(P(ctypes.c_int32)),
+                                           P(ctypes.c_int64), P(ctypes.c_int64)]
+        lib.oracle_prime_paths.restype = ctypes.c_int
+        lib.oracle_free.argtypes = [ctypes.c_void_p]
+        lib.oracle_ext_count.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32),
+                                         ctypes.c_int32, ctypes.c_int32]
+        lib.oracle_ext_count.restype = ctypes.c_int64
+        lib.oracle_scc_labels.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32),
+                                          P(ctypes.c_int32)]
+        lib.oracle_digest.argtypes = [ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int32),
+                                      P(ctypes.c_uint64)]
+        lib.oracle_tp_tables.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32),
+                                         ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int32),
+                                         P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)]
+        _lib = lib
+    return _lib
+
+
+def _csr(g):
+    so = np.ascontiguousarray(g.offsets, dtype=np.int64)
+    st = np.ascontiguousarray(g.targets, dtype=np.int32)
+    if st.size == 0:
+        st = np.zeros(1, dtype=np.int32)
+    return so, st
+
+
+def _p64(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def _p32(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def prime_paths(g, v_lo: int = 0, v_hi: Optional[int] = None, prunes: bool = True
+                ) -> Tuple[np.ndarray, np.ndarray]:
+    """Prime paths with first vertex in [v_lo, v_hi), lexicographic order.
+
+    Returns (offsets int64[n_paths+1] starting at 0, vertices int32)."""
+    lib = _load()
+    so, st = _csr(g)
+    v_hi = g.n if v_hi is None else v_hi
+    po = ctypes.POINTER(ctypes.c_int64)()
+    pv = ctypes.POINTER(ctypes.c_int32)()
+    npaths = ctypes.c_int64()
+    nvert = ctypes.c_int64()
+    rc = lib.oracle_prime_paths(g.n, _p64(so), _p32(st), v_lo, v_hi, int(prunes), ctypes.byref(po),
+                                ctypes.byref(pv), ctypes.byref(npaths), ctypes.byref(nvert))
+    if rc != 0:
+        raise MemoryError("oracle_prime_paths failed")
+    try:
+        off = np.ctypeslib.as_array(po, shape=(npaths.value + 1,)).copy()
+        vert = (np.ctypeslib.as_array(pv, shape=(nvert.value,)).copy() if nvert.value
+                else np.zeros(0, dtype=np.int32))
+    finally:
+        lib.oracle_free(ctypes.cast(po, ctypes.c_void_p))
+        lib.oracle_free(ctypes.cast(pv, ctypes.c_void_p))
+    return off, vert
+
+
+def ext_count(g, v_lo: int = 0, v_hi: Optional[int] = None) -> int:
+    """E_canon restricted to start vertices in [v_lo, v_hi)."""
+    lib = _load()
+    so, st = _csr(g)
+    return int(lib.oracle_ext_count(g.n, _p64(so), _p32(st), v_lo, g.n if v_hi is None else v_hi))
+
+
+def scc_labels(g) -> np.ndarray:
+    lib = _load()
+    so, st = _csr(g)
+    lab = np.zeros(max(g.n, 1), dtype=np.int32)
+    lib.oracle_scc_labels(g.n, _p64(so), _p32(st), _p32(lab))
+    return lab[:g.n]
+
+
+def digest(offsets: np.ndarray, vertices: np.ndarray) -> Tuple[int, int]:
+    lib = _load()
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    vert = np.ascontiguousarray(vertices, dtype=np.int32)
+    if vert.size == 0:
+        vert = np.zeros(1, dtype=np.int32)
+    out = (ctypes.c_uint64 * 2)()
+    lib.oracle_digest(off.shape[0] - 1, _p64(off), _p32(vert), out)
+    return int(out[0]), int(out[1])
+
+
+def tp_tables(g, entry: int, exit: int):
+    """Lexmin-shortest prefix (entry->v) and suffix (v->exit) walks per vertex.
+
+    Returns (pre: list[list[int] | None], suf: list[list[int] | None])."""
+    lib = _load()
+    so, st = _csr(g)
+    n = g.n
+    pre_len = np.zeros(n, dtype=np.int32)
+    suf_len = np.zeros(n, dtype=np.int32)
+    pre_tab = np.zeros(n * n, dtype=np.int32)
+    suf_tab = np.zeros(n * n, dtype=np.int32)
+    lib.oracle_tp_tables(n, _p64(so), _p32(st), entry, exit, _p32(pre_len), _p32(pre_tab),
+                         _p32(suf_len), _p32(suf_tab))
+    pre = [None if pre_len[v] < 0 else pre_tab[v * n: v * n + pre_len[v]].tolist() for v in range(n)]
+    suf = [None if suf_len[v] < 0 else suf_tab[v * n: v * n + suf_len[v]].tolist() for v in range(n)]
+    return pre, suf
+
+
+def test_paths(g, offsets: np.ndarray, vertices: np.ndarray, entry: int, exit: int
+               ) -> Tuple[np.ndarray, np.ndarray]:
+    """TP_i = prefix[first_i][:-1] + PP_i + suffix[last_i][1:], aligned with the PP list
+    (reading R15).  Raises ValueError if an endpoint is unreachable."""
+    pre, suf = tp_tables(g, entry, exit)
+    out_off = [0]
+    out_v = []
+    for i in range(len(offsets) - 1):
+        p = vertices[offsets[i]:offsets[i + 1]].tolist()
+        a, b = pre[p[0]], suf[p[-1]]
+        if a is None or b is None:
+            raise ValueError(f"PP {i} endpoints unreachable from entry / to exit")
+        tp = a[:-1] + p + b[1:]
+        out_v.extend(tp)
+        out_off.append(len(out_v))
+    return np.asarray(out_off, dtype=np.int64), np.asarray(out_v, dtype=np.int32)
+
+
+def as_list(offsets: np.ndarray, vertices: np.ndarray):
+    return [tuple(vertices[offsets[i]:offsets[i + 1]].tolist()) for i in range(len(offsets) - 1)]

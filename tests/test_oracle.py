@@ -1,0 +1,312 @@
+"""Pins for the CPU oracle (oracle/) against things other than itself.
+
+Every expected value here comes from the paper (cited), a closed form, a
+textbook special case, or brute force on tiny inputs -- never from the oracle
+under test or from the CUDA path.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import brute
+from tests.conftest import load_golden
+from workloads import generators as gen
+
+
+def _pp_list(g, **kw):
+    off, vert = oracle.prime_paths(g, **kw)
+    return oracle.as_list(off, vert)
+
+
+# --------------------------------------------------------------- worked example
+def test_fig1b_prime_paths_equal_paper():
+    """the 19 PPs quoted in the paper."""
+    rows = load_golden("fig1b_prime_paths.txt")
+    paper = sorted(p for _, p in rows)
+    assert len(paper) == 19  # P:255 "we reach 19 PPs"
+    got = _pp_list(gen.fig1b())
+    assert got == paper  # same set, and oracle order is lexicographic
+    assert got == sorted(got)
+
+
+def test_fig1b_class_counts():
+    """11 internal, 2 complete, 4 exit, 2 entry."""
+    rows = load_golden("fig1b_prime_paths.txt")
+    counts = {}
+    for tag, _ in rows:
+        counts[tag] = counts.get(tag, 0) + 1
+    assert counts == {"internal": 11, "complete": 2, "exit": 4, "entry": 2}
+
+
+def test_fig1b_tier0_equals_paper():
+    rows = load_golden("fig1b_prime_paths.txt")
+    g = gen.fig1b()
+    assert brute.prime_paths(g.n, brute.graph_succ(g)) == sorted(p for _, p in rows)
+
+
+def test_fig1b_graph_matches_paper_counts():
+    """E = 13, V = 11, CC = 13 - 11 + 2 = 4."""
+    g = gen.fig1b()
+    assert (g.n, g.m, g.m - g.n + 2) == (11, 13, 4)
+
+
+def test_fig1b_scc():
+    """Fig. 2(a) / P:150: the one nontrivial SCC is {2,3,4,5,6,8}."""
+    lab = oracle.scc_labels(gen.fig1b())
+    members = [v for v in range(11) if lab[v] == lab[2]]
+    assert members == [2, 3, 4, 5, 6, 8]
+    assert len(set(lab.tolist())) == 6  # that SCC + 5 singletons
+
+
+def test_fig1b_ext_count():
+    """E_canon on Fig. 1(b) = 42: the per-start counts 8,9,6,6,6,7 are brute-forced here."""
+    g = gen.fig1b()
+    scc = {2, 3, 4, 5, 6, 8}
+    succ = brute.graph_succ(g)
+    sp = brute.simple_paths(g.n, [[w for w in succ[v] if w in scc and v in scc] for v in range(g.n)])
+    per = {s: sum(1 for p in sp if p[0] == s and len(p) >= 2) for s in scc}
+    assert per == {2: 8, 3: 9, 4: 6, 5: 6, 6: 6, 8: 7}
+    assert oracle.ext_count(g) == 42 == sum(per.values())
+
+
+def test_fig1b_segments_reading(golden):
+    """DESIGN.md reading R8/R9 reproduce the paper's intermediate path sets:
+    head = non-entry first, pred(first) within path, last an exit;
+    transit = entry first, exit last (all acyclic simple paths, Def. 6);
+    tail = entry first, succ(last) within path."""
+    g = gen.fig1b()
+    rows = golden("fig1b_segments.txt")
+    scc = set(dict(rows)["scc"])
+    succ = brute.graph_succ(g)
+    pred = [[u for u in range(g.n) if v in succ[u]] for v in range(g.n)]
+    entries = {v for v in scc if any(u not in scc for u in pred[v])}
+    exits = {v for v in scc if any(w not in scc for w in succ[v])}
+    assert sorted(entries) == list(dict(rows)["entries"])
+    assert sorted(exits) == list(dict(rows)["exits"])
+    inner = [[w for w in succ[v] if w in scc] if v in scc else [] for v in range(g.n)]
+    paths = [p for p in brute.simple_paths(g.n, inner)
+             if p[0] in scc and not (len(p) > 1 and p[0] == p[-1])]
+    head = sorted(p for p in paths if p[0] not in entries and set(pred[p[0]]) <= set(p) and p[-1] in exits)
+    transit = sorted(p for p in paths if p[0] in entries and p[-1] in exits)
+    tail = sorted(p for p in paths if p[0] in entries and set(succ[p[-1]]) <= set(p))
+    assert head == sorted(p for t, p in rows if t == "head")
+    assert transit == sorted(p for t, p in rows if t == "transit")
+    assert tail == sorted(p for t, p in rows if t == "tail")
+
+
+# ---------------------------------------------------------- closed forms
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
+def test_nested_if_closed_form(K):
+    """K nested if-then -> K+1 prime paths."""
+    assert len(_pp_list(gen.k_nested_if(K))) == K + 1
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 6, 8])
+def test_seq_if_closed_form(K):
+    """K if-then in sequence -> 2^K prime paths."""
+    assert len(_pp_list(gen.k_seq_if(K))) == 2 ** K
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 9])
+def test_single_loop_closed_form(K):
+    """a single loop of length K -> K prime paths (one rotation per vertex);
+    E_canon = K^2 (K starts x K-1 acyclic extensions + 1 closure)."""
+    g = gen.single_loop(K)
+    pps = _pp_list(g)
+    assert len(pps) == K
+    assert all(p[0] == p[-1] and len(p) == K + 1 for p in pps)
+    assert oracle.ext_count(g) == K * K
+
+
+@pytest.mark.parametrize("K,N,expect", [(1, 3, 6), (2, 3, 12), (3, 3, 19), (3, 2, 16), (4, 3, 27)])
+def test_seq_loops_count(K, N, expect):
+    """K loops in sequence: 1 complete + K*N internal + K exit + K entry + K(K-1)/2 SCC->SCC.
+    (The paper's K((N+1)+(K-1)/2) at P:636 is wrong -- DESIGN.md reading R7.)
+    Cross-checked against tier-0 brute force where it is small enough."""
+    g = gen.k_seq_loops(K, N)
+    assert 1 + K * N + 2 * K + K * (K - 1) // 2 == expect
+    pps = _pp_list(g)
+    assert len(pps) == expect
+    if g.n <= 11:
+        assert pps == brute.prime_paths(g.n, brute.graph_succ(g))
+
+
+def _count_st_paths(g):
+    """#Start->End paths of a DAG by memoised recursion (Npath for DAGs)."""
+    memo = {}
+
+    def f(v):
+        if v == g.exit:
+            return 1
+        if v not in memo:
+            memo[v] = sum(f(int(w)) for w in g.succ(v))
+        return memo[v]
+
+    return f(g.entry)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_dag_pp_equals_npath(seed):
+    """for acyclic CFGs the PP count equals the Npath complexity (= #Start->End paths
+    when every vertex lies on such a path), and every PP is a Start->End path."""
+    g = gen.random_dag_cfg(8 + seed, seed)
+    pps = _pp_list(g)
+    assert len(pps) == _count_st_paths(g)
+    assert all(p[0] == g.entry and p[-1] == g.exit for p in pps)
+
+
+# ------------------------------------------------------- tier-0 equivalence corpus
+def _corpus(count, seed0=1000):
+    rng = np.random.default_rng(seed0)
+    for i in range(count):
+        n = int(rng.integers(1, 9))
+        p = float(rng.choice([0.12, 0.2, 0.3, 0.4]))
+        yield gen.random_digraph(n, p, seed0 + i, self_loops=bool(rng.random() < 0.5))
+
+
+def test_tier1_equals_tier0_random_corpus():
+    """Def. 1 brute force vs the DFS oracle (with and without the exact prunes A', B)."""
+    total = 0
+    for g in _corpus(700):
+        ref = brute.prime_paths(g.n, brute.graph_succ(g))
+        assert _pp_list(g, prunes=True) == ref, g.name
+        assert _pp_list(g, prunes=False) == ref, g.name
+        total += len(ref)
+    assert total > 3000
+
+
+def test_tier1_equals_tier0_multi_scc():
+    """Chains of small SCCs (exercise SCC->SCC prime paths and prunes)."""
+    for seed in range(60):
+        parts = [gen.random_digraph(3, 0.5, 7 * seed + j) for j in range(3)]
+        u = gen.disjoint_union(parts)
+        arcs = u.arcs() + [(2, 3), (5, 6), (1, 4), (0, 7)]
+        g = gen.from_arcs(u.n, arcs)
+        assert _pp_list(g) == brute.prime_paths(g.n, brute.graph_succ(g))
+
+
+def test_ext_count_matches_bruteforce():
+    for g in _corpus(200, seed0=5000):
+        lab = oracle.scc_labels(g)
+        succ = brute.graph_succ(g)
+        cnt = 0
+        for s in range(g.n):
+            comp = {v for v in range(g.n) if lab[v] == lab[s]}
+            nontriv = len(comp) > 1 or s in succ[s]
+            if not nontriv:
+                continue
+            inner = [[w for w in succ[v] if w in comp] if v in comp else [] for v in range(g.n)]
+            cnt += sum(1 for p in brute.simple_paths(g.n, inner) if p[0] == s and len(p) >= 2)
+        assert oracle.ext_count(g) == cnt
+
+
+def test_scc_labels_mutual_reachability():
+    for g in _corpus(100, seed0=9000):
+        lab = oracle.scc_labels(g)
+        succ = brute.graph_succ(g)
+        reach = []
+        for a in range(g.n):
+            seen, st = {a}, [a]
+            while st:
+                v = st.pop()
+                for w in succ[v]:
+                    if w not in seen:
+                        seen.add(w)
+                        st.append(w)
+            reach.append(seen)
+        for a, b in itertools.product(range(g.n), repeat=2):
+            assert (lab[a] == lab[b]) == (b in reach[a] and a in reach[b])
+
+
+# ------------------------------------------------------------------ invariants
+def test_invariants_simple_antichain_coverage():
+    """Every PP is simple; no PP is a proper subpath of another; every simple path is a
+    contiguous subpath of some PP (north_star invariants)."""
+    for g in _corpus(150, seed0=7000):
+        pps = _pp_list(g)
+        pset = set(pps)
+        for p in pps:
+            body = p[:-1] if len(p) > 1 and p[0] == p[-1] else p
+            assert len(set(body)) == len(body)
+            for i in range(len(p)):
+                for j in range(i + 1, len(p) + 1):
+                    if j - i < len(p):
+                        assert p[i:j] not in pset
+        subs = set()
+        for p in pps:
+            for i in range(len(p)):
+                for j in range(i + 1, len(p) + 1):
+                    subs.add(p[i:j])
+        for sp in brute.simple_paths(g.n, brute.graph_succ(g)):
+            assert sp in subs
+
+
+def test_lexicographic_order_and_blocks():
+    g = gen.config2()
+    off, vert = oracle.prime_paths(g)
+    pps = oracle.as_list(off, vert)
+    assert pps == sorted(pps)
+    # per-start-vertex blocks concatenate to the whole list
+    parts = []
+    for lo, hi in [(0, 10), (10, 31), (31, g.n)]:
+        parts += _pp_list(g, v_lo=lo, v_hi=hi)
+    assert parts == pps
+
+
+# ---------------------------------------------------------------------- digest
+def test_digest_order_independent_and_sensitive():
+    g = gen.fig1b()
+    off, vert = oracle.prime_paths(g)
+    d = oracle.digest(off, vert)
+    pps = oracle.as_list(off, vert)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(len(pps))
+    pv = [pps[i] for i in perm]
+    off2 = np.cumsum([0] + [len(p) for p in pv]).astype(np.int64)
+    vert2 = np.asarray([v for p in pv for v in p], dtype=np.int32)
+    assert oracle.digest(off2, vert2) == d
+    vert3 = vert2.copy()
+    vert3[3] ^= 1
+    assert oracle.digest(off2, vert3) != d
+    # splitting one path differently changes the digest (length is hashed)
+    off4 = off2.copy()
+    off4[1] += 1
+    assert oracle.digest(off4, vert2) != d
+
+
+# ------------------------------------------------------------------ test paths
+def test_tp_tables_are_lexmin_shortest_walks():
+    """The prefix/suffix rule (R15) equals 'lexicographically smallest among
+    minimum-hop walks', checked by brute force on tiny graphs."""
+    checks = 0
+    for g in _corpus(150, seed0=3000):
+        if g.n < 2:
+            continue
+        succ = brute.graph_succ(g)
+        entry, exit_ = 0, g.n - 1
+        pre, suf = oracle.tp_tables(g, entry, exit_)
+        for v in range(g.n):
+            assert pre[v] == brute.lexmin_shortest_walk(succ, entry, v)
+            assert suf[v] == brute.lexmin_shortest_walk(succ, v, exit_)
+            checks += 2
+    assert checks > 1000
+
+
+def test_fig1b_test_paths():
+    """S:536 example: PP <8,2,3,4,8> -> TP <S,1,2,3,4,8,2,3,4,8,2,9,E>; every TP runs
+    entry->exit along arcs and contains its PP; 19 aligned, 10 distinct."""
+    g = gen.fig1b()
+    off, vert = oracle.prime_paths(g)
+    toff, tvert = oracle.test_paths(g, off, vert, g.entry, g.exit)
+    pps = oracle.as_list(off, vert)
+    tps = oracle.as_list(toff, tvert)
+    assert len(tps) == 19
+    assert tps[pps.index((8, 2, 3, 4, 8))] == (0, 1, 2, 3, 4, 8, 2, 3, 4, 8, 2, 9, 10)
+    arcs = set(g.arcs())
+    for p, t in zip(pps, tps):
+        assert t[0] == g.entry and t[-1] == g.exit
+        assert all((a, b) in arcs for a, b in zip(t[:-1], t[1:]))
+        assert any(t[i:i + len(p)] == p for i in range(len(t) - len(p) + 1))
+    assert len(set(tps)) == 10
