@@ -1,0 +1,177 @@
+/*
+ * tpgen.h -- C ABI of the B200-native prime-path / test-path engine.
+ *
+ * Reference: "TPGen: A Self-Stabilizing GPU-Based Method for Prime and Test
+ * Paths Generation" (arXiv 2210.16998), cited as PAPER.md line numbers (P:n).
+ *
+ * Problem 1: input a CFG G = (V, E), start s, end e; output the
+ * prime paths of G and a set of test paths covering them.  The prime-path set
+ * does not depend on s and e (Def. 1), so the ABI has two calls:
+ *   tpgen_prime_paths -- all prime paths (maximal simple paths, simple cycles
+ *                        included), canonical order;
+ *   tpgen_test_paths  -- one entry->exit test path per prime path.
+ *
+ * Conventions (all calls)
+ *   - Graph input is a SUCCESSOR CSR in HOST memory, borrowed for the call:
+ *     csr_offsets int64[n_vertices+1] (offsets[0] = 0, non-decreasing),
+ *     csr_targets int32[offsets[n]] (each in [0, n_vertices)).  Rows need not be
+ *     sorted; duplicate arcs in a row are rejected (TPGEN_ERR_INVALID_GRAPH);
+ *     self-loops are allowed.  (The paper's CSR is predecessor-oriented, P:300;
+ *     predecessor masks are derived internally.)
+ *   - Vertex ids are int32, path offsets int64, counts uint64 internally
+ *     (overflow -> TPGEN_ERR_LIMIT_EXCEEDED, detected before any output
+ *     allocation).
+ *   - Canonical output order: lexicographic on int32 sequences.  Prime-path
+ *     sets are prefix-free, so the order is total.  Output arrays:
+ *       offsets  int64[n_paths + 1], offsets[0] = 0, non-decreasing;
+ *       vertices int32[offsets[n_paths]] (global vertex ids).
+ *     A cyclic prime path v1..vk repeats v1 at the end (v1 = vk).
+ *   - Outputs are allocated by the library, on the device (opt->device) through
+ *     opt->device_alloc (or cudaMallocAsync on opt->stream when NULL), or in
+ *     pinned host memory when output_on_device = 0.  Release with
+ *     tpgen_paths_free.  On any error *out is zeroed.
+ *   - Work is enqueued on opt->stream (a cudaStream_t; NULL = legacy default
+ *     stream) and the call returns after the stream has been synchronised.
+ *   - Errors: a tpgen_status; tpgen_status_string gives a static message and
+ *     tpgen_last_error_message a thread-local detail string.
+ *   - There is no CPU fallback: without a usable CUDA device every call that
+ *     computes returns TPGEN_ERR_CUDA.
+ */
+#ifndef TPGEN_H
+#define TPGEN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TPGEN_OK = 0,
+    TPGEN_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, n < 0, bad entry/exit, bad shard spec */
+    TPGEN_ERR_INVALID_GRAPH = 2,    /* offsets[0] != 0, decreasing offsets, target out of range, duplicate arc */
+    TPGEN_ERR_LIMIT_EXCEEDED = 3,   /* n_paths > max_paths, extensions > max_extensions, or a count >= 2^62 */
+    TPGEN_ERR_OUT_OF_MEMORY = 4,    /* host or device allocation failed */
+    TPGEN_ERR_UNREACHABLE = 5,      /* tpgen_test_paths: a PP's first vertex is not reachable from entry,
+                                       or its last vertex cannot reach exit */
+    TPGEN_ERR_CUDA = 6,             /* CUDA runtime error (no device, launch failure, ...) */
+    TPGEN_ERR_INTERNAL = 7,         /* invariant violated inside the library */
+    TPGEN_ERR_UNSUPPORTED = 8       /* a strongly connected component with more than 64 vertices */
+} tpgen_status;
+
+enum { TPGEN_OUT_MATERIALIZE = 0, TPGEN_OUT_COUNT_HASH = 1 };
+enum { TPGEN_TP_PER_PP = 0 };
+
+/* Canonical flat path array (see conventions). */
+typedef struct {
+    int64_t n_paths;
+    int64_t *offsets;   /* n_paths + 1 entries */
+    int32_t *vertices;  /* offsets[n_paths] entries */
+    int32_t on_device;  /* 1: device pointers on `device`; 0: pinned host pointers */
+    int32_t device;
+    void *_owner;       /* library-private */
+} tpgen_paths;
+
+typedef void *(*tpgen_alloc_fn)(size_t bytes, void *stream, void *ctx);
+typedef void (*tpgen_free_fn)(void *ptr, void *stream, void *ctx);
+
+typedef struct {
+    int32_t device;            /* CUDA ordinal; -1 = current device */
+    void *stream;              /* cudaStream_t; NULL = legacy default stream */
+    int32_t output_on_device;  /* 1 (default): device output; 0: pinned host output */
+    int32_t output_mode;       /* TPGEN_OUT_MATERIALIZE (default) | TPGEN_OUT_COUNT_HASH (counts + digest only) */
+    int32_t shard_rank;        /* start-vertex shard (0-based); with shard_count = 1 the whole graph */
+    int32_t shard_count;       /* >= 1 */
+    int64_t max_paths;         /* 0 = unlimited */
+    int64_t max_extensions;    /* 0 = unlimited */
+    int32_t tp_mode;           /* TPGEN_TP_PER_PP */
+    int32_t compute_digest;    /* 1: fill stats->hash_lo/hi (extra pass over the output) */
+    tpgen_alloc_fn device_alloc;  /* output allocator; NULL -> cudaMallocAsync */
+    tpgen_free_fn device_free;
+    void *alloc_ctx;
+    void *host_out;            /* optional caller-owned (ideally pinned) host buffer for output_on_device = 0:
+                                  offsets are placed at host_out, vertices right after them; used when
+                                  host_out_bytes >= 8*(n_paths+1) + 4*n_vertices, else pinned memory is
+                                  allocated by the library.  The caller keeps ownership. */
+    size_t host_out_bytes;
+} tpgen_options;
+
+typedef struct {
+    int64_t n_paths;         /* paths returned (this shard) */
+    int64_t total_vertices;  /* offsets[n_paths] */
+    int64_t n_extensions;    /* E_canon of this shard's start vertices */
+    int64_t n_cross;         /* prime paths spanning >= 2 SCCs */
+    int64_t n_units;         /* work units of the final write pass */
+    int64_t n_heads;         /* head segments (cross-PP blocks) */
+    int64_t n_segments;      /* transit + tail segment items */
+    uint64_t hash_lo, hash_hi;  /* order-independent multiset digest */
+    int32_t n_scc, n_scc_nontrivial, max_scc, n_count_rounds;
+    int64_t gpu_launches;    /* kernels this call launched */
+    int32_t shard_lo, shard_hi;  /* start-vertex range of this shard */
+    double ms_plan;          /* host planning (Tarjan, tables) */
+    double ms_count;         /* device: count + refine rounds */
+    double ms_write;         /* device: write pass (K1 write) */
+    double ms_stitch;        /* device: segment scan + stitch writer */
+    double ms_device;        /* device time of the whole pipeline (CUDA events) */
+    double ms_total;         /* wall clock of the call */
+    double ms_dfs_write;     /* device time of the dominant kernel (DFS write pass) */
+    double ms_dfs_count;     /* device time summed over the DFS count launches */
+} tpgen_stats;
+
+void tpgen_options_init(tpgen_options *opt);
+const char *tpgen_status_string(tpgen_status s);
+const char *tpgen_last_error_message(void);
+const char *tpgen_version(void);
+
+/*
+ * All prime paths of G (Def. 1) whose first vertex lies in this
+ * shard's start-vertex range, in canonical order.  Shards partition the global
+ * canonical list into contiguous blocks in rank order.
+ */
+tpgen_status tpgen_prime_paths(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                               const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats);
+
+/*
+ * Test paths ("the set of TPs covering all PPs"; "extends every PP
+ * to visit initial and final nodes"): TP_i = prefix[first_i] (minus its last
+ * vertex) ++ PP_i ++ suffix[last_i] (minus its first vertex), aligned 1:1 with
+ * the prime-path list.  prefix[v] is the lexicographically smallest
+ * minimum-hop walk entry -> v, suffix[v] the one v -> exit (R15).
+ * prime_paths: a canonical list (host or device), or NULL to compute it.
+ */
+tpgen_status tpgen_test_paths(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                              const tpgen_paths *prime_paths, int32_t entry, int32_t exit,
+                              const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats);
+
+/*
+ * Component graph (host only, no device needed): Tarjan SCCs of G.
+ * comp[v] = SCC id of v, ids in reverse topological order of the component
+ * DAG (Def. 3): every arc between two SCCs goes from a larger id to
+ * a smaller one.  flags[v] = 1 if v is an SccEntryVertex (Def. 4),
+ * | 2 if an SccExitVertex (Def. 5), | 4 if its SCC is nontrivial
+ * (more than one vertex or a self-loop).  comp and flags are caller-owned
+ * int32[n_vertices]; *n_scc receives the number of SCCs.  Same validation and
+ * error codes as tpgen_prime_paths (TPGEN_ERR_UNSUPPORTED is not raised here).
+ */
+tpgen_status tpgen_components(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                              int32_t *comp, int32_t *flags, int32_t *n_scc);
+
+/* Stream-ordered release; safe on a zeroed struct. */
+void tpgen_paths_free(tpgen_paths *p);
+
+/*
+ * Plan API: host planning + host->device upload of the graph tables once, then
+ * device-resident calls (what bench.py times as `value`).
+ */
+typedef struct tpgen_plan tpgen_plan;
+tpgen_status tpgen_plan_create(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                               const tpgen_options *opt, tpgen_plan **plan);
+tpgen_status tpgen_plan_prime_paths(tpgen_plan *plan, const tpgen_options *opt, tpgen_paths *out,
+                                    tpgen_stats *stats);
+void tpgen_plan_destroy(tpgen_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPGEN_H */

@@ -1,0 +1,262 @@
+"""B200-native prime-path / test-path engine (TPGen hot path, arXiv 2210.16998).
+
+Thin Python binding over the C ABI in ``include/tpgen.h`` (``libtpgen.so``):
+argument marshalling only -- every step of the path runs in the library's
+CUDA kernels.  PyTorch supplies device memory (output buffers come from the
+caching allocator), streams and, in bench.py, process groups.  There is no
+CPU fallback: without the built library or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any, Dict, Optional, Tuple
+
+import numpy as np
+
+from . import _abi
+
+__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "library", "version"]
+
+
+class TpgenError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.status_name = _abi.STATUS_NAMES.get(status, str(status))
+        super().__init__(f"{self.status_name}: {msg}")
+
+
+def library():
+    return _abi.load()
+
+
+def version() -> str:
+    return library().tpgen_version().decode()
+
+
+@dataclass
+class PathSet:
+    """Canonical flat path array: ``offsets[n_paths+1]`` (int64), ``vertices`` (int32).
+
+    On device these are torch CUDA tensors, on the host numpy arrays."""
+
+    offsets: Any
+    vertices: Any
+    n_paths: int
+    on_device: bool
+    stats: Dict[str, Any] = field(default_factory=dict)
+
+    def to_numpy(self) -> Tuple[np.ndarray, np.ndarray]:
+        if self.on_device:
+            return self.offsets.cpu().numpy(), self.vertices.cpu().numpy()
+        return np.asarray(self.offsets), np.asarray(self.vertices)
+
+    def as_list(self):
+        off, vert = self.to_numpy()
+        return [tuple(vert[off[i]:off[i + 1]].tolist()) for i in range(len(off) - 1)]
+
+
+def _csr(graph) -> Tuple[np.ndarray, np.ndarray, int]:
+    if hasattr(graph, "offsets") and hasattr(graph, "targets"):
+        so, st, n = graph.offsets, graph.targets, graph.n
+    else:
+        so, st = graph[0], graph[1]
+        n = len(so) - 1
+    so = np.ascontiguousarray(so, dtype=np.int64)
+    st = np.ascontiguousarray(st, dtype=np.int32)
+    if st.size == 0:
+        st = np.zeros(1, dtype=np.int32)  # valid pointer for an arc-free graph
+    return so, st, int(n)
+
+
+def _p64(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def _p32(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+class _TorchAllocator:
+    """Output allocator backed by torch's caching allocator (device memory only)."""
+
+    def __init__(self, device: int):
+        import torch
+
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.live: Dict[int, Any] = {}
+        self.alloc_fn = _abi.ALLOC_FN(self._alloc)
+        self.free_fn = _abi.FREE_FN(self._free)
+
+    def _alloc(self, nbytes, stream, ctx):
+        t = self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.device)
+        p = t.data_ptr()
+        self.live[p] = t
+        return p
+
+    def _free(self, ptr, stream, ctx):
+        self.live.pop(int(ptr or 0), None)
+
+    def take(self, ptr: int):
+        return self.live.pop(ptr)
+
+
+def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest: bool, max_paths: int,
+             max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None) -> _abi.Options:
+    lib = library()
+    o = _abi.Options()
+    lib.tpgen_options_init(ctypes.byref(o))
+    o.device = device
+    o.stream = stream
+    o.output_on_device = 1 if output == "device" else 0
+    o.output_mode = _abi.OUT_COUNT_HASH if mode == "count" else _abi.OUT_MATERIALIZE
+    o.shard_rank, o.shard_count = shard
+    o.max_paths = max_paths
+    o.max_extensions = max_extensions
+    o.compute_digest = 1 if digest else 0
+    if alloc is not None:
+        o.device_alloc = alloc.alloc_fn
+        o.device_free = alloc.free_fn
+    if host_out is not None:
+        o.host_out = host_out.data_ptr()
+        o.host_out_bytes = host_out.numel() * host_out.element_size()
+    return o
+
+
+def _stream_handle(device: int, stream):
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check(status: int):
+    if status != _abi.TPGEN_OK:
+        raise TpgenError(status, library().tpgen_last_error_message().decode())
+
+
+def _wrap(paths: _abi.Paths, stats: _abi.Stats, alloc: Optional[_TorchAllocator], host_out=None) -> PathSet:
+    lib = library()
+    n = int(paths.n_paths)
+    st = stats.as_dict()
+    nv = int(st.get("total_vertices", 0))
+    if not ctypes.cast(paths.offsets, ctypes.c_void_p).value:  # count-only mode: stats, no arrays
+        return PathSet(None, None, int(st.get("n_paths", 0)), False, st)
+    if paths.on_device:
+        p_off = ctypes.cast(paths.offsets, ctypes.c_void_p).value
+        p_v = ctypes.cast(paths.vertices, ctypes.c_void_p).value
+        if alloc is None:
+            raise RuntimeError("device output requires the torch allocator")
+        off = alloc.take(p_off).view(alloc.torch.int64)[: n + 1]
+        vert = alloc.take(p_v).view(alloc.torch.int32)[:nv]
+        lib.tpgen_paths_free(ctypes.byref(paths))
+        return PathSet(off, vert, n, True, st)
+    if host_out is not None and ctypes.cast(paths.offsets, ctypes.c_void_p).value == host_out.data_ptr():
+        import torch
+
+        off = host_out[: 8 * (n + 1)].view(torch.int64)
+        vert = host_out[8 * (n + 1): 8 * (n + 1) + 4 * nv].view(torch.int32)
+        lib.tpgen_paths_free(ctypes.byref(paths))
+        return PathSet(off, vert, n, False, st)
+    off = np.ctypeslib.as_array(paths.offsets, shape=(n + 1,)).copy()
+    vert = (np.ctypeslib.as_array(paths.vertices, shape=(nv,)).copy() if nv else np.zeros(0, dtype=np.int32))
+    lib.tpgen_paths_free(ctypes.byref(paths))
+    return PathSet(off, vert, n, False, st)
+
+
+def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "materialize",
+                shard: Tuple[int, int] = (0, 1), digest: bool = False, max_paths: int = 0,
+                max_extensions: int = 0, stream=None, host_out=None) -> PathSet:
+    """All prime paths of ``graph`` (Def. 1), canonical order.
+
+    ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host)."""
+    lib = library()
+    so, st, n = _csr(graph)
+    alloc = _TorchAllocator(device) if output == "device" else None
+    o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
+                 alloc, host_out)
+    paths, stats = _abi.Paths(), _abi.Stats()
+    _check(lib.tpgen_prime_paths(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
+    return _wrap(paths, stats, alloc, host_out)
+
+
+def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *, device: int = 0,
+               output: str = "device", stream=None) -> PathSet:
+    """One entry->exit test path per prime path (R15)."""
+    lib = library()
+    so, st, n = _csr(graph)
+    alloc = _TorchAllocator(device) if output == "device" else None
+    o = _options(device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(device, stream), alloc)
+    pin = None
+    keep = []
+    if prime is not None:
+        pin = _abi.Paths()
+        pin.n_paths = prime.n_paths
+        if prime.on_device:
+            pin.offsets = ctypes.cast(prime.offsets.data_ptr(), ctypes.POINTER(ctypes.c_int64))
+            pin.vertices = ctypes.cast(prime.vertices.data_ptr(), ctypes.POINTER(ctypes.c_int32))
+            pin.on_device = 1
+        else:
+            a = np.ascontiguousarray(prime.offsets, dtype=np.int64)
+            b = np.ascontiguousarray(prime.vertices, dtype=np.int32)
+            if b.size == 0:
+                b = np.zeros(1, dtype=np.int32)
+            keep += [a, b]
+            pin.offsets = _p64(a)
+            pin.vertices = _p32(b)
+            pin.on_device = 0
+        pin.device = device
+    paths, stats = _abi.Paths(), _abi.Stats()
+    _check(lib.tpgen_test_paths(_p64(so), _p32(st), n, ctypes.byref(pin) if pin is not None else None, entry, exit,
+                                ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
+    return _wrap(paths, stats, alloc)
+
+
+def components(graph):
+    """Component graph on the host (``tpgen_components``): (comp[v], flags[v], n_scc).
+    flags: 1 = SCC entry vertex (Def. 4), 2 = SCC exit vertex (Def. 5), 4 = nontrivial SCC."""
+    lib = library()
+    so, st, n = _csr(graph)
+    comp = np.zeros(max(n, 1), dtype=np.int32)
+    flags = np.zeros(max(n, 1), dtype=np.int32)
+    nscc = ctypes.c_int32()
+    _check(lib.tpgen_components(_p64(so), _p32(st), n, _p32(comp), _p32(flags), ctypes.byref(nscc)))
+    return comp[:n], flags[:n], int(nscc.value)
+
+
+class Plan:
+    """Host plan + device-resident graph tables (``tpgen_plan_create``); ``prime_paths()``
+    then runs device-only (what bench.py times as ``value``)."""
+
+    def __init__(self, graph, device: int = 0, stream=None):
+        lib = library()
+        so, st, n = _csr(graph)
+        self.device = device
+        self.n = n
+        o = _options(device, "device", "materialize", (0, 1), False, 0, 0, _stream_handle(device, stream), None)
+        h = ctypes.c_void_p()
+        _check(lib.tpgen_plan_create(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+
+    def prime_paths(self, *, output: str = "device", mode: str = "materialize", shard: Tuple[int, int] = (0, 1),
+                    digest: bool = False, max_paths: int = 0, stream=None, host_out=None) -> PathSet:
+        lib = library()
+        alloc = _TorchAllocator(self.device) if output == "device" else None
+        o = _options(self.device, output, mode, shard, digest, max_paths, 0, _stream_handle(self.device, stream),
+                     alloc, host_out)
+        paths, stats = _abi.Paths(), _abi.Stats()
+        _check(lib.tpgen_plan_prime_paths(self._h, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
+        return _wrap(paths, stats, alloc, host_out)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            library().tpgen_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

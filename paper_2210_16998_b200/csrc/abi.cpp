@@ -1,0 +1,216 @@
+// abi.cpp -- extern "C" entry points of libtpgen (declared in include/tpgen.h).
+#include <chrono>
+#include <cstring>
+#include <new>
+
+#include "engine.h"
+
+struct tpgen_plan {
+    tpg::PlanImpl impl;
+};
+
+namespace {
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+tpgen_status check_options(const tpgen_options &o) {
+    if (o.shard_count < 1 || o.shard_rank < 0 || o.shard_rank >= o.shard_count) {
+        tpg::set_error("bad shard spec");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (o.output_mode != TPGEN_OUT_MATERIALIZE && o.output_mode != TPGEN_OUT_COUNT_HASH) {
+        tpg::set_error("bad output_mode");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    return TPGEN_OK;
+}
+
+tpgen_options resolve(const tpgen_options *opt) {
+    tpgen_options o;
+    tpgen_options_init(&o);
+    if (opt) o = *opt;
+    return o;
+}
+
+tpgen_status make_plan(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options &o, tpgen_plan **out) {
+    *out = nullptr;
+    tpgen_plan *p = new (std::nothrow) tpgen_plan();
+    if (!p) return TPGEN_ERR_OUT_OF_MEMORY;
+    tpgen_status s = tpg::init_device(p->impl, o);
+    if (s == TPGEN_OK) {
+        const double t0 = now_ms();
+        std::string msg;
+        s = tpg::build_plan(so, st, n, p->impl.hp, msg);
+        if (s != TPGEN_OK) tpg::set_error(msg);
+        p->impl.ms_plan = now_ms() - t0;
+    }
+    if (s == TPGEN_OK) s = tpg::plan_upload(p->impl, (cudaStream_t)o.stream);
+    if (s != TPGEN_OK) {
+        delete p;
+        return s;
+    }
+    *out = p;
+    return TPGEN_OK;
+}
+
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+void tpgen_options_init(tpgen_options *o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->device = -1;
+    o->output_on_device = 1;
+    o->output_mode = TPGEN_OUT_MATERIALIZE;
+    o->shard_rank = 0;
+    o->shard_count = 1;
+}
+
+const char *tpgen_status_string(tpgen_status s) {
+    switch (s) {
+        case TPGEN_OK: return "ok";
+        case TPGEN_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case TPGEN_ERR_INVALID_GRAPH: return "invalid graph";
+        case TPGEN_ERR_LIMIT_EXCEEDED: return "limit exceeded";
+        case TPGEN_ERR_OUT_OF_MEMORY: return "out of memory";
+        case TPGEN_ERR_UNREACHABLE: return "unreachable endpoint";
+        case TPGEN_ERR_CUDA: return "CUDA error";
+        case TPGEN_ERR_INTERNAL: return "internal error";
+        case TPGEN_ERR_UNSUPPORTED: return "unsupported input";
+    }
+    return "unknown status";
+}
+
+const char *tpgen_last_error_message(void) { return tpg::last_error(); }
+
+const char *tpgen_version(void) { return "tpgen-b200 0.1 (sm_100a; DFS units + warp-cooperative writer)"; }
+
+tpgen_status tpgen_plan_create(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options *opt,
+                               tpgen_plan **plan) {
+    if (!plan) return TPGEN_ERR_INVALID_ARGUMENT;
+    *plan = nullptr;
+    tpgen_options o = resolve(opt);
+    tpgen_status s = check_options(o);
+    if (s != TPGEN_OK) return s;
+    tpgen_status r = make_plan(so, st, n, o, plan);
+    if (r == TPGEN_OK && cudaStreamSynchronize((cudaStream_t)o.stream) != cudaSuccess) {
+        tpgen_plan_destroy(*plan);
+        *plan = nullptr;
+        return TPGEN_ERR_CUDA;
+    }
+    return r;
+}
+
+tpgen_status tpgen_plan_prime_paths(tpgen_plan *plan, const tpgen_options *opt, tpgen_paths *out,
+                                    tpgen_stats *stats) {
+    if (!plan || !out) return TPGEN_ERR_INVALID_ARGUMENT;
+    memset(out, 0, sizeof(*out));
+    tpgen_options o = resolve(opt);
+    tpgen_status s = check_options(o);
+    if (s != TPGEN_OK) return s;
+    DeviceScope ds(plan->impl.device);
+    s = tpg::run_prime_paths(plan->impl, o, out, stats);
+    if (s != TPGEN_OK) memset(out, 0, sizeof(*out));
+    return s;
+}
+
+void tpgen_plan_destroy(tpgen_plan *plan) { delete plan; }
+
+tpgen_status tpgen_prime_paths(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options *opt,
+                               tpgen_paths *out, tpgen_stats *stats) {
+    if (!out) return TPGEN_ERR_INVALID_ARGUMENT;
+    memset(out, 0, sizeof(*out));
+    const double t0 = now_ms();
+    tpgen_options o = resolve(opt);
+    tpgen_status s = check_options(o);
+    if (s != TPGEN_OK) return s;
+    tpgen_plan *p = nullptr;
+    s = make_plan(so, st, n, o, &p);
+    if (s != TPGEN_OK) return s;
+    {
+        DeviceScope ds(p->impl.device);
+        s = tpg::run_prime_paths(p->impl, o, out, stats);
+    }
+    tpgen_plan_destroy(p);
+    if (s != TPGEN_OK) memset(out, 0, sizeof(*out));
+    if (s == TPGEN_OK && stats) stats->ms_total = now_ms() - t0;
+    return s;
+}
+
+tpgen_status tpgen_test_paths(const int64_t *so, const int32_t *st, int32_t n, const tpgen_paths *prime_paths,
+                              int32_t entry, int32_t exit, const tpgen_options *opt, tpgen_paths *out,
+                              tpgen_stats *stats) {
+    if (!out) return TPGEN_ERR_INVALID_ARGUMENT;
+    memset(out, 0, sizeof(*out));
+    const double t0 = now_ms();
+    tpgen_options o = resolve(opt);
+    tpgen_status s = check_options(o);
+    if (s != TPGEN_OK) return s;
+    if (entry < 0 || entry >= n || exit < 0 || exit >= n) {
+        tpg::set_error("entry/exit out of range");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (prime_paths && prime_paths->n_paths > 0 && (!prime_paths->offsets || !prime_paths->vertices)) {
+        tpg::set_error("prime_paths has NULL arrays");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    tpgen_plan *p = nullptr;
+    s = make_plan(so, st, n, o, &p);
+    if (s != TPGEN_OK) return s;
+    {
+        DeviceScope ds(p->impl.device);
+        s = tpg::run_test_paths(p->impl, prime_paths, entry, exit, o, out, stats);
+    }
+    tpgen_plan_destroy(p);
+    if (s != TPGEN_OK) memset(out, 0, sizeof(*out));
+    if (s == TPGEN_OK && stats) stats->ms_total = now_ms() - t0;
+    return s;
+}
+
+void tpgen_paths_free(tpgen_paths *p) { tpg::free_paths(p); }
+
+tpgen_status tpgen_components(const int64_t *so, const int32_t *st, int32_t n, int32_t *comp, int32_t *flags,
+                              int32_t *n_scc) {
+    if (n < 0 || (n > 0 && (!comp || !flags)) || !n_scc) {
+        tpg::set_error("NULL output pointer or n < 0");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    tpg::HostPlan P;
+    std::string msg;
+    tpgen_status s = tpg::build_plan(so, st, n, P, msg, false);
+    if (s != TPGEN_OK) {
+        tpg::set_error(msg);
+        return s;
+    }
+    std::vector<int32_t> size(P.n_scc, 0);
+    std::vector<char> loop(P.n_scc, 0);
+    for (int32_t v = 0; v < n; v++) {
+        size[P.comp[v]]++;
+        for (int64_t e = P.so[v]; e < P.so[v + 1]; e++)
+            if (P.st[e] == v) loop[P.comp[v]] = 1;
+    }
+    for (int32_t v = 0; v < n; v++) {
+        comp[v] = P.comp[v];
+        int32_t f = P.slots[v].flags;
+        if (size[P.comp[v]] > 1 || loop[P.comp[v]]) f |= 4;
+        flags[v] = f;
+    }
+    *n_scc = P.n_scc;
+    return TPGEN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+// aux_kernels.cuh -- scans, refinement scatter, segment tables, cross-SCC
+// stitch writer (K5), test-path writer (K6) and digest (K8) for libtpgen.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace tpg {
+
+// ------------------------------------------------------------------- scan
+// Exclusive prefix sums of up to 8 uint64 arrays of the same length, in place.
+constexpr int kScanThreads = 256;
+constexpr int kScanIpt = 8;
+constexpr int kScanTile = kScanThreads * kScanIpt;
+
+struct ScanArrays {
+    uint64_t *a[8];
+    int na;
+};
+
+__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t t = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread (kScanThreads threads).
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *sm, uint64_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t inc = warp_incl_scan(v);
+    if (lane == 31) sm[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint64_t w = (lane < kScanThreads / 32) ? sm[lane] : 0;
+        const uint64_t wi = warp_incl_scan(w);
+        if (lane < kScanThreads / 32) sm[lane] = wi - w;
+        if (lane == kScanThreads / 32 - 1) sm[16] = wi;
+    }
+    __syncthreads();
+    const uint64_t r = inc - v + sm[wid];
+    total = sm[16];
+    __syncthreads();
+    return r;
+}
+
+__global__ void scan_reduce_kernel(ScanArrays S, int64_t n, uint64_t *bsum, int nb) {
+    __shared__ uint64_t sm[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanIpt;
+    for (int a = 0; a < S.na; a++) {
+        uint64_t s = 0;
+#pragma unroll
+        for (int i = 0; i < kScanIpt; i++)
+            if (base + i < n) s += S.a[a][base + i];
+        uint64_t tot;
+        block_excl_scan(s, sm, tot);
+        if (threadIdx.x == 0) bsum[(int64_t)a * nb + blockIdx.x] = tot;
+    }
+}
+
+__global__ void scan_bsum_kernel(uint64_t *bsum, int nb, int na, uint64_t *totals) {
+    __shared__ uint64_t sm[32];
+    for (int a = 0; a < na; a++) {
+        uint64_t carry = 0;
+        for (int b0 = 0; b0 < nb; b0 += kScanThreads) {
+            const int b = b0 + threadIdx.x;
+            const uint64_t v = (b < nb) ? bsum[(int64_t)a * nb + b] : 0;
+            uint64_t tot;
+            const uint64_t ex = block_excl_scan(v, sm, tot);
+            if (b < nb) bsum[(int64_t)a * nb + b] = ex + carry;
+            carry += tot;
+        }
+        if (threadIdx.x == 0) totals[a] = carry;
+    }
+}
+
+__global__ void scan_down_kernel(ScanArrays S, int64_t n, const uint64_t *bsum, int nb) {
+    __shared__ uint64_t sm[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanIpt;
+    for (int a = 0; a < S.na; a++) {
+        uint64_t v[kScanIpt];
+        uint64_t s = 0;
+#pragma unroll
+        for (int i = 0; i < kScanIpt; i++) {
+            v[i] = (base + i < n) ? S.a[a][base + i] : 0;
+            s += v[i];
+        }
+        uint64_t tot;
+        uint64_t run = block_excl_scan(s, sm, tot) + bsum[(int64_t)a * nb + blockIdx.x];
+#pragma unroll
+        for (int i = 0; i < kScanIpt; i++) {
+            if (base + i < n) S.a[a][base + i] = run;
+            run += v[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------- refinement
+__global__ void build_worklist_kernel(DevGraph G, const Unit *units, const uint8_t *status, int64_t n, int seg_phase,
+                                      int64_t *work, unsigned long long *nwork) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (status[i] != ST_PENDING) continue;
+        const int32_t scc = units[i].scc;
+        const int s = units[i].path[0];
+        const int flags = __ldg(&G.slots[__ldg(G.scc_vbase + scc) + s].flags);
+        if (((flags & F_ENTRY) != 0) == (seg_phase != 0)) work[atomicAdd(nwork, 1ull)] = i;
+    }
+}
+
+__global__ void refine_count_kernel(DevGraph G, const uint8_t *status, const Unit *stop, int64_t n, uint64_t *r) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (status[i] != ST_TRUNC) {
+            r[i] = 1;
+        } else {
+            Unit S = stop[i];
+            r[i] = 1 + (uint64_t)remainder_events<false>(G, S, nullptr);
+        }
+    }
+}
+
+struct RefineBufs {
+    const Unit *units;
+    const uint8_t *status;
+    const Unit *stop;
+    const uint64_t *cnt[C_NUM];
+    const uint64_t *ext;
+    Unit *nunits;
+    uint8_t *nstatus;
+    uint64_t *ncnt[C_NUM];
+    uint64_t *next;
+};
+
+__global__ void refine_scatter_kernel(DevGraph G, RefineBufs B, int64_t n, const uint64_t *off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = (int64_t)off[i];
+        Unit U = B.units[i];
+        const uint8_t st = B.status[i];
+        if (st == ST_TRUNC) U.nsteps = B.stop[i].nsteps;
+        B.nunits[p] = U;
+        B.nstatus[p] = (st == ST_TRUNC) ? ST_DONE : st;
+#pragma unroll
+        for (int c = 0; c < C_NUM; c++) B.ncnt[c][p] = B.cnt[c][i];
+        B.next[p] = B.ext[i];
+        if (st == ST_TRUNC) {
+            Unit S = B.stop[i];
+            const int m = remainder_events<true>(G, S, B.nunits + p + 1);
+            for (int q = 1; q <= m; q++) {
+                B.nstatus[p + q] = ST_PENDING;
+#pragma unroll
+                for (int c = 0; c < C_NUM; c++) B.ncnt[c][p + q] = 0;
+                B.next[p + q] = 0;
+            }
+        }
+    }
+}
+
+// --------------------------------------------------- segment tables (a5)
+__global__ void item_bounds_kernel(DevGraph G, const Unit *units, int64_t n, const uint64_t *off_items,
+                                   uint64_t total_items, int64_t *ibeg, int64_t *iend) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int vb = __ldg(G.scc_vbase + units[i].scc);
+        const Slot ss = ld_slot(G.slots + vb + units[i].path[0]);
+        if (!(ss.flags & F_ENTRY)) continue;
+        const int32_t g = ss.gid;
+        int32_t gp = -1, gn = -1;
+        if (i > 0) gp = __ldg(G.slot_gid + __ldg(G.scc_vbase + units[i - 1].scc) + units[i - 1].path[0]);
+        if (i + 1 < n) gn = __ldg(G.slot_gid + __ldg(G.scc_vbase + units[i + 1].scc) + units[i + 1].path[0]);
+        if (gp != g) ibeg[g] = (int64_t)off_items[i];
+        if (gn != g) iend[g] = (i + 1 < n) ? (int64_t)off_items[i + 1] : (int64_t)total_items;
+    }
+}
+
+__global__ void item_weight_kernel(DevGraph G, const ItemRec *items, int64_t n, uint64_t *cw, uint64_t *vw) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const ItemRec it = items[i];
+        if (it.y < 0) {
+            cw[i] = 1;
+            vw[i] = (uint64_t)it.len;
+        } else {
+            const uint64_t W = __ldg(G.Wc + it.y), V = __ldg(G.Wv + it.y);
+            cw[i] = W;
+            vw[i] = (uint64_t)it.len * W + V;
+        }
+    }
+}
+
+__global__ void head_weight_kernel(DevGraph G, const HeadRec *heads, int64_t n, uint64_t *hw) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        hw[i] = __ldg(G.Wc + heads[i].x);
+}
+
+struct StitchArgs {
+    const HeadRec *heads;
+    int64_t n_heads;
+    const uint64_t *comp_off;  // exclusive scan of W(x_h) over heads
+    uint64_t n_comp;
+    const ItemRec *items;
+    const uint64_t *cum, *vcum;  // global exclusive scans of item weights
+    const int64_t *ibeg, *iend;  // per entry vertex (global id)
+    const int32_t *head_pool, *item_pool;
+    int64_t *out_off;
+    int32_t *out_vert;
+};
+
+__device__ __forceinline__ int64_t upper_bound_u64(const uint64_t *a, int64_t lo, int64_t hi, uint64_t key) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// K5: one warp per cross prime path h (+) completion_k(x).  The k-th
+// completion is unranked through the entry tables (mixed radix over the DP
+// counts), its output position follows from the per-item vertex prefix sums.
+__global__ void stitch_kernel(StitchArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t g = (uint64_t)wg; g < A.n_comp; g += (uint64_t)nw) {
+        const int64_t h = upper_bound_u64(A.comp_off, 0, A.n_heads, g) - 1;
+        const HeadRec H = A.heads[h];
+        const uint64_t k = g - A.comp_off[h];
+        // pass 1: vertex offset of completion k inside the block
+        uint64_t vrel = 0, kk = k;
+        int32_t x = H.x;
+        while (true) {
+            const int64_t b = A.ibeg[x], e = A.iend[x];
+            const uint64_t bc = A.cum[b], bv = A.vcum[b];
+            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            const uint64_t k2 = kk - (A.cum[i] - bc);
+            const ItemRec it = A.items[i];
+            vrel += A.vcum[i] - bv;
+            if (it.y < 0) break;
+            vrel += k2 * (uint64_t)it.len;
+            x = it.y;
+            kk = k2;
+        }
+        const uint64_t vstart = H.v_off + k * (uint64_t)H.len + vrel;
+        if (lane == 0) A.out_off[H.pp_off + k] = (int64_t)vstart;
+        int32_t *dst = A.out_vert + vstart;
+        for (int j = lane; j < H.len; j += 32) dst[j] = A.head_pool[H.hv_off + j];
+        dst += H.len;
+        // pass 2: copy the segments
+        kk = k;
+        x = H.x;
+        while (true) {
+            const int64_t b = A.ibeg[x], e = A.iend[x];
+            const uint64_t bc = A.cum[b];
+            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            const uint64_t k2 = kk - (A.cum[i] - bc);
+            const ItemRec it = A.items[i];
+            const int32_t *src = A.item_pool + it.pool_off;
+            for (int j = lane; j < it.len; j += 32) dst[j] = src[j];
+            dst += it.len;
+            if (it.y < 0) break;
+            x = it.y;
+            kk = k2;
+        }
+    }
+}
+
+__global__ void set_last_offset_kernel(int64_t *off, int64_t n_paths, int64_t total) { off[n_paths] = total; }
+
+// ------------------------------------------------------------- digest (K8)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return z;
+}
+
+__global__ void digest_kernel(const int64_t *off, const int32_t *vert, int64_t n, unsigned long long *acc) {
+    uint64_t a = 0, b = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = off[i], e = off[i + 1];
+        uint64_t za = mix64(0x9E3779B97F4A7C15ull ^ (uint64_t)(e - s));
+        uint64_t zb = mix64(0xD1B54A32D192ED03ull ^ (uint64_t)(e - s));
+        for (int64_t j = s; j < e; j++) {
+            const uint64_t v = (uint64_t)(uint32_t)__ldg(vert + j);
+            za = mix64(za ^ v);
+            zb = mix64(zb ^ v);
+        }
+        a += za;
+        b += zb;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        a += __shfl_xor_sync(kFull, a, d);
+        b += __shfl_xor_sync(kFull, b, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc, (unsigned long long)a);
+        atomicAdd(acc + 1, (unsigned long long)b);
+    }
+}
+
+// --------------------------------------------------------- test paths (K6)
+struct TpArgs {
+    const int64_t *pp_off;
+    const int32_t *pp_vert;
+    int64_t n;
+    const int64_t *pre_off, *suf_off;
+    const int32_t *pre_len, *suf_len;
+    const int32_t *pre_flat, *suf_flat;
+    uint64_t *tp_len;  // then scanned into offsets
+    int64_t *tp_off;
+    int32_t *tp_vert;
+    unsigned int *unreachable;
+};
+
+__global__ void tp_len_kernel(TpArgs A) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = A.pp_off[i], e = A.pp_off[i + 1];
+        const int32_t f = A.pp_vert[s], l = A.pp_vert[e - 1];
+        const int32_t pl = A.pre_len[f], sl = A.suf_len[l];
+        if (pl < 0 || sl < 0) {
+            atomicOr(A.unreachable, 1u);
+            A.tp_len[i] = 0;
+        } else {
+            A.tp_len[i] = (uint64_t)(pl - 1) + (uint64_t)(e - s) + (uint64_t)(sl - 1);
+        }
+    }
+}
+
+__global__ void tp_write_kernel(TpArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = wg; i < A.n; i += nw) {
+        const int64_t s = A.pp_off[i], e = A.pp_off[i + 1];
+        const int32_t f = A.pp_vert[s], l = A.pp_vert[e - 1];
+        const int32_t pl = A.pre_len[f] - 1, sl = A.suf_len[l] - 1;
+        const int64_t t0 = (int64_t)A.tp_len[i];
+        if (lane == 0) A.tp_off[i] = t0;
+        int32_t *d = A.tp_vert + t0;
+        const int32_t *pre = A.pre_flat + A.pre_off[f];
+        for (int j = lane; j < pl; j += 32) d[j] = pre[j];
+        d += pl;
+        for (int64_t j = lane; j < e - s; j += 32) d[j] = A.pp_vert[s + j];
+        d += e - s;
+        const int32_t *suf = A.suf_flat + A.suf_off[l] + 1;
+        for (int j = lane; j < sl; j += 32) d[j] = suf[j];
+    }
+}
+
+}  // namespace tpg

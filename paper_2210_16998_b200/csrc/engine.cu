@@ -1,0 +1,760 @@
+// engine.cu -- host orchestration of the device pipeline of libtpgen.
+//
+// tpgen_prime_paths (SURVEY.md §3 "Build 1"):
+//   plan (host)  -> roots (one unit per start vertex, canonical order)
+//   segment phase (entry starts): count rounds [dfs_kernel<COUNT> + refine]
+//   completion DP over the component DAG (host, KBs)
+//   prime-path phase (non-entry starts): count rounds
+//   scan of the per-unit counts -> exact output offsets
+//   dfs_kernel<WRITE> (all units)         -- the dominant kernel
+//   segment-table scans + stitch_kernel (cross-SCC prime paths)
+//   optional digest, optional D2H
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "aux_kernels.cuh"
+#include "engine.h"
+
+namespace tpg {
+
+#define TPG_CK(x)                                                                                      \
+    do {                                                                                               \
+        cudaError_t _e = (x);                                                                          \
+        if (_e != cudaSuccess) {                                                                       \
+            set_error(std::string("CUDA error ") + cudaGetErrorString(_e) + " at " #x);                \
+            return _e == cudaErrorMemoryAllocation ? TPGEN_ERR_OUT_OF_MEMORY : TPGEN_ERR_CUDA;         \
+        }                                                                                              \
+    } while (0)
+
+#define TPG_TRY(x)                        \
+    do {                                  \
+        tpgen_status _s = (x);            \
+        if (_s != TPGEN_OK) return _s;    \
+    } while (0)
+
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------ buffers
+tpgen_status DevBuf::ensure(size_t bytes, cudaStream_t s) {
+    if (bytes <= cap) return TPGEN_OK;
+    size_t nc = std::max(bytes, (size_t)(cap * 3 / 2));
+    nc = (nc + 255) & ~(size_t)255;
+    if (p) TPG_CK(cudaFreeAsync(p, s));
+    p = nullptr;
+    cap = 0;
+    TPG_CK(cudaMallocAsync(&p, nc, s));
+    cap = nc;
+    return TPGEN_OK;
+}
+void DevBuf::release(cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    cap = 0;
+}
+
+template <class T>
+static tpgen_status upload(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
+    size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+    TPG_TRY(b.ensure(bytes, s));
+    if (!v.empty()) TPG_CK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return TPGEN_OK;
+}
+
+// ------------------------------------------------------------ plan
+PlanImpl::~PlanImpl() {
+    if (!dev_ok) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaStream_t s = 0;
+    for (DevBuf *b : all_bufs()) b->release(s);
+    cudaStreamSynchronize(s);
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+std::vector<DevBuf *> PlanImpl::all_bufs() {
+    std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &stop, &work,
+                               &rbuf, &scan_b, &scan_tot, &ctr, &agg, &heads, &head_pool, &items, &item_pool,
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs};
+    for (int i = 0; i < 2; i++) {
+        v.push_back(&units[i]);
+        v.push_back(&status[i]);
+        v.push_back(&ext[i]);
+        for (int c = 0; c < C_NUM; c++) v.push_back(&cnt[i][c]);
+    }
+    return v;
+}
+
+tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
+    const HostPlan &H = P.hp;
+    TPG_TRY(upload(P.d_slots, H.slots, s));
+    std::vector<int32_t> gid(H.n);
+    for (int32_t i = 0; i < H.n; i++) gid[i] = H.slots[i].gid;
+    TPG_TRY(upload(P.d_slot_gid, gid, s));
+    TPG_TRY(upload(P.d_out_gid, H.out_gid, s));
+    TPG_TRY(upload(P.d_out_pos, H.out_pos, s));
+    TPG_TRY(upload(P.d_scc_vbase, H.scc_vbase, s));
+    TPG_TRY(upload(P.d_scc_out_base, H.scc_out_base, s));
+    TPG_TRY(upload(P.d_scc_nout, H.scc_nout, s));
+    TPG_TRY(upload(P.d_scc_pair_base, H.scc_pair_base, s));
+    TPG_TRY(upload(P.d_slot_eidx, H.slot_eidx, s));
+    TPG_TRY(P.d_Wc.ensure(std::max<size_t>(H.n, 1) * 8, s));
+    TPG_TRY(P.d_Wv.ensure(std::max<size_t>(H.n, 1) * 8, s));
+    TPG_CK(cudaMemsetAsync(P.d_Wc.p, 0, std::max<size_t>(H.n, 1) * 8, s));
+    TPG_CK(cudaMemsetAsync(P.d_Wv.p, 0, std::max<size_t>(H.n, 1) * 8, s));
+    P.dev_ok = true;
+    return TPGEN_OK;
+}
+
+static DevGraph dev_graph(PlanImpl &P, int32_t lo, int32_t hi) {
+    DevGraph G;
+    G.slots = P.d_slots.as<Slot>();
+    G.slot_gid = P.d_slot_gid.as<int32_t>();
+    G.out_gid = P.d_out_gid.as<int32_t>();
+    G.out_pos = P.d_out_pos.as<int32_t>();
+    G.scc_vbase = P.d_scc_vbase.as<int32_t>();
+    G.scc_out_base = P.d_scc_out_base.as<int32_t>();
+    G.scc_nout = P.d_scc_nout.as<int32_t>();
+    G.scc_pair_base = P.d_scc_pair_base.as<int64_t>();
+    G.slot_eidx = P.d_slot_eidx.as<int32_t>();
+    G.Wc = P.d_Wc.as<uint64_t>();
+    G.Wv = P.d_Wv.as<uint64_t>();
+    G.shard_lo = lo;
+    G.shard_hi = hi;
+    return G;
+}
+
+// ------------------------------------------------------------ scan helper
+static tpgen_status scan_multi(PlanImpl &P, uint64_t *const *arrs, int na, int64_t n, uint64_t *totals_host,
+                               cudaStream_t s, int64_t &launches) {
+    if (n <= 0) {
+        for (int a = 0; a < na; a++) totals_host[a] = 0;
+        return TPGEN_OK;
+    }
+    ScanArrays S;
+    for (int a = 0; a < na; a++) S.a[a] = arrs[a];
+    S.na = na;
+    const int nb = (int)((n + kScanTile - 1) / kScanTile);
+    TPG_TRY(P.scan_b.ensure((size_t)nb * na * 8, s));
+    TPG_TRY(P.scan_tot.ensure(8 * 8, s));
+    scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(S, n, P.scan_b.as<uint64_t>(), nb);
+    scan_bsum_kernel<<<1, kScanThreads, 0, s>>>(P.scan_b.as<uint64_t>(), nb, na, P.scan_tot.as<uint64_t>());
+    scan_down_kernel<<<nb, kScanThreads, 0, s>>>(S, n, P.scan_b.as<uint64_t>(), nb);
+    launches += 3;
+    TPG_CK(cudaGetLastError());
+    if (totals_host) {
+        TPG_CK(cudaMemcpyAsync(totals_host, P.scan_tot.p, na * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+    }
+    return TPGEN_OK;
+}
+
+static int grid_for(int64_t n, int threads, int cap) {
+    int64_t b = (n + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+// ------------------------------------------------------------ output memory
+struct OutOwner {
+    tpgen_free_fn free_fn = nullptr;
+    void *ctx = nullptr;
+    void *stream = nullptr;
+    int kind = 0;  // 0 cudaMallocAsync, 1 callback, 2 pinned host (library), 3 caller host buffer
+    void *p_off = nullptr, *p_vert = nullptr;
+    int device = 0;
+};
+
+static tpgen_status out_alloc_device(const tpgen_options &o, OutOwner *ow, size_t bytes, void **p, cudaStream_t s) {
+    bytes = std::max<size_t>(bytes, 16);
+    if (o.device_alloc) {
+        *p = o.device_alloc(bytes, o.stream, o.alloc_ctx);
+        if (!*p) {
+            set_error("device_alloc callback returned NULL");
+            return TPGEN_ERR_OUT_OF_MEMORY;
+        }
+        ow->kind = 1;
+        ow->free_fn = o.device_free;
+        ow->ctx = o.alloc_ctx;
+        ow->stream = o.stream;
+    } else {
+        TPG_CK(cudaMallocAsync(p, bytes, s));
+        ow->kind = 0;
+        ow->stream = (void *)s;
+    }
+    return TPGEN_OK;
+}
+
+void free_paths(tpgen_paths *p) {
+    if (!p) return;
+    OutOwner *ow = (OutOwner *)p->_owner;
+    if (ow) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(ow->device);
+        void *ptrs[2] = {ow->p_off, ow->p_vert};
+        for (void *q : ptrs) {
+            if (!q) continue;
+            if (ow->kind == 0) cudaFreeAsync(q, (cudaStream_t)ow->stream);
+            else if (ow->kind == 1) {
+                if (ow->free_fn) ow->free_fn(q, ow->stream, ow->ctx);
+            } else if (ow->kind == 2) cudaFreeHost(q);
+        }
+        if (ow->kind == 0) cudaStreamSynchronize((cudaStream_t)ow->stream);
+        if (prev >= 0) cudaSetDevice(prev);
+        delete ow;
+    }
+    memset(p, 0, sizeof(*p));
+}
+
+// Places device arrays (off, vert) into *out according to the options.
+static tpgen_status finish_output(const tpgen_options &o, OutOwner *ow, int64_t n_paths, int64_t n_vert, int64_t *d_off,
+                                  int32_t *d_vert, cudaStream_t s, tpgen_paths *out) {
+    out->n_paths = n_paths;
+    out->device = ow->device;
+    if (o.output_on_device) {
+        out->offsets = d_off;
+        out->vertices = d_vert;
+        out->on_device = 1;
+        ow->p_off = d_off;
+        ow->p_vert = d_vert;
+        out->_owner = ow;
+        return TPGEN_OK;
+    }
+    size_t boff = (size_t)(n_paths + 1) * 8, bv = (size_t)n_vert * 4;
+    OutOwner *hw = new OutOwner();
+    hw->device = ow->device;
+    char *h = nullptr;
+    if (o.host_out && o.host_out_bytes >= boff + bv) {
+        h = (char *)o.host_out;
+        hw->kind = 3;
+    } else {
+        cudaError_t e = cudaHostAlloc((void **)&h, std::max<size_t>(boff + bv, 16), cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            delete hw;
+            set_error("pinned host allocation failed");
+            return TPGEN_ERR_OUT_OF_MEMORY;
+        }
+        hw->kind = 2;
+        hw->p_off = h;
+    }
+    cudaMemcpyAsync(h, d_off, boff, cudaMemcpyDeviceToHost, s);
+    if (bv) cudaMemcpyAsync(h + boff, d_vert, bv, cudaMemcpyDeviceToHost, s);
+    TPG_CK(cudaStreamSynchronize(s));
+    // release the device copies
+    ow->p_off = d_off;
+    ow->p_vert = d_vert;
+    tpgen_paths tmp;
+    memset(&tmp, 0, sizeof(tmp));
+    tmp._owner = ow;
+    free_paths(&tmp);
+    out->offsets = (int64_t *)h;
+    out->vertices = (int32_t *)(h + boff);
+    out->on_device = 0;
+    out->_owner = hw;
+    return TPGEN_OK;
+}
+
+// ------------------------------------------------------------ pipeline
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timer() {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+static uint32_t choose_budget(int64_t nwork, int64_t lanes) {
+    const uint32_t big = 4096;
+    if (nwork >= lanes) return big;
+    double f = (double)nwork / (double)lanes;
+    uint32_t b = (uint32_t)(big * f);
+    return std::max<uint32_t>(32, std::min(big, b));
+}
+
+static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStream_t s, tpgen_stats &st,
+                                int64_t &launches, double &ms_count_kernel) {
+    Timer t;
+    const int64_t lanes = (int64_t)P.num_sms * 4 * kDfsThreads;
+    for (int round = 0; round < 4096; round++) {
+        const int cur = P.cur;
+        const int64_t n = P.n_units;
+        if (n == 0) return TPGEN_OK;
+        TPG_TRY(P.work.ensure((size_t)n * 8, s));
+        unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0]=nwork [1]=next [2]=ntrunc
+        TPG_CK(cudaMemsetAsync(ctr, 0, 4 * 8, s));
+        build_worklist_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit>(),
+                                                                     P.status[cur].as<uint8_t>(), n, seg,
+                                                                     P.work.as<int64_t>(), ctr + 0);
+        launches++;
+        unsigned long long hctr[4];
+        TPG_CK(cudaMemcpyAsync(hctr, ctr, 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        const int64_t nwork = (int64_t)hctr[0];
+        if (nwork == 0) return TPGEN_OK;
+        DfsArgs A;
+        memset(&A, 0, sizeof(A));
+        A.G = G;
+        A.units = P.units[cur].as<Unit>();
+        A.n_units = n;
+        A.work = P.work.as<int64_t>();
+        A.n_work = ctr + 0;
+        A.next = ctr + 1;
+        for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.cnt[cur][c].as<uint64_t>();
+        A.ext = P.ext[cur].as<uint64_t>();
+        A.status = P.status[cur].as<uint8_t>();
+        A.stop = P.stop.as<Unit>();
+        A.budget = choose_budget(nwork, lanes);
+        A.n_trunc = ctr + 2;
+        unsigned long long *agg = P.agg.as<unsigned long long>();
+        A.agg_tail_cnt = agg;
+        A.agg_tail_len = agg + P.hp.n;
+        A.agg_pair_cnt = agg + 2 * (int64_t)P.hp.n;
+        A.agg_pair_len = agg + 2 * (int64_t)P.hp.n + P.hp.n_pairs;
+        A.overflow = reinterpret_cast<unsigned int *>(ctr + 3);
+        const int grid = grid_for(nwork, kDfsThreads, P.num_sms * 4);
+        cudaEventRecord(t.a, s);
+        dfs_kernel<PASS_COUNT><<<grid, kDfsThreads, 0, s>>>(A);
+        cudaEventRecord(t.b, s);
+        launches++;
+        TPG_CK(cudaGetLastError());
+        TPG_CK(cudaMemcpyAsync(hctr, ctr, 4 * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        ms_count_kernel += ms;
+        st.n_count_rounds++;
+        if ((unsigned)hctr[3] & 1u) P.overflow = true;
+        if (hctr[2] == 0) return TPGEN_OK;
+        // ---- refine: truncated units -> counted piece + remainder units
+        TPG_TRY(P.rbuf.ensure((size_t)n * 8, s));
+        refine_count_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.status[cur].as<uint8_t>(),
+                                                                    P.stop.as<Unit>(), n, P.rbuf.as<uint64_t>());
+        launches++;
+        uint64_t *arr[1] = {P.rbuf.as<uint64_t>()};
+        uint64_t total = 0;
+        TPG_TRY(scan_multi(P, arr, 1, n, &total, s, launches));
+        const int nx = cur ^ 1;
+        const int64_t nn = (int64_t)total;
+        TPG_TRY(P.units[nx].ensure((size_t)nn * sizeof(Unit), s));
+        TPG_TRY(P.status[nx].ensure((size_t)nn, s));
+        TPG_TRY(P.ext[nx].ensure((size_t)nn * 8, s));
+        for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[nx][c].ensure((size_t)nn * 8, s));
+        RefineBufs B;
+        B.units = P.units[cur].as<Unit>();
+        B.status = P.status[cur].as<uint8_t>();
+        B.stop = P.stop.as<Unit>();
+        for (int c = 0; c < C_NUM; c++) {
+            B.cnt[c] = P.cnt[cur][c].as<uint64_t>();
+            B.ncnt[c] = P.cnt[nx][c].as<uint64_t>();
+        }
+        B.ext = P.ext[cur].as<uint64_t>();
+        B.nunits = P.units[nx].as<Unit>();
+        B.nstatus = P.status[nx].as<uint8_t>();
+        B.next = P.ext[nx].as<uint64_t>();
+        refine_scatter_kernel<<<grid_for(n, 128, 8192), 128, 0, s>>>(G, B, n, P.rbuf.as<uint64_t>());
+        launches++;
+        TPG_CK(cudaGetLastError());
+        P.cur = nx;
+        P.n_units = nn;
+        TPG_TRY(P.stop.ensure((size_t)nn * sizeof(Unit), s));
+    }
+    set_error("count phase did not converge");
+    return TPGEN_ERR_INTERNAL;
+}
+
+tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    memset(out, 0, sizeof(*out));
+    int64_t launches = 0;
+    const HostPlan &H = P.hp;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    int32_t lo = 0, hi = H.n;
+    shard_range(H, o.shard_rank, o.shard_count, lo, hi);
+    st.shard_lo = lo;
+    st.shard_hi = hi;
+    st.n_scc = H.n_scc;
+    st.n_scc_nontrivial = H.n_nontrivial;
+    st.max_scc = H.max_scc;
+    st.ms_plan = P.ms_plan;
+    P.overflow = false;
+
+    Timer tall, tw, tst;
+    cudaEventRecord(tall.a, s);
+    const DevGraph G = dev_graph(P, lo, hi);
+
+    // ---- roots: one K_NODE unit per start vertex, ascending global id
+    std::vector<Unit> roots;
+    roots.reserve(H.n);
+    for (int32_t v = 0; v < H.n; v++) {
+        const int32_t slot = H.v_slot[v];
+        const bool entry = (H.slots[slot].flags & F_ENTRY) != 0;
+        const bool mine = v >= lo && v < hi;
+        if (!entry && !mine) continue;
+        Unit u;
+        memset(&u, 0, sizeof(u));
+        const int32_t c = H.comp[v];
+        const int loc = slot - H.scc_vbase[c];
+        u.M = 1ull << loc;
+        u.scc = c;
+        u.e = -1;
+        u.kind = K_NODE;
+        u.path[0] = (uint8_t)loc;
+        roots.push_back(u);
+    }
+    P.cur = 0;
+    P.n_units = (int64_t)roots.size();
+    const size_t nr = std::max<size_t>(roots.size(), 1);
+    TPG_TRY(P.units[0].ensure(nr * sizeof(Unit), s));
+    TPG_TRY(P.status[0].ensure(nr, s));
+    TPG_TRY(P.ext[0].ensure(nr * 8, s));
+    for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[0][c].ensure(nr * 8, s));
+    TPG_TRY(P.stop.ensure(nr * sizeof(Unit), s));
+    TPG_TRY(P.ctr.ensure(8 * 8, s));
+    if (!roots.empty()) {
+        TPG_CK(cudaMemcpyAsync(P.units[0].p, roots.data(), roots.size() * sizeof(Unit), cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemsetAsync(P.status[0].p, ST_PENDING, roots.size(), s));
+    }
+    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
+    TPG_TRY(P.agg.ensure(agg_n * 8, s));
+    TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
+
+    double ms_count_kernel = 0;
+    // ---- segment phase (SCC entries) -> completion DP
+    if (H.has_entries) {
+        TPG_TRY(count_phase(P, G, 1, s, st, launches, ms_count_kernel));
+        std::vector<uint64_t> aggh(agg_n);
+        TPG_CK(cudaMemcpyAsync(aggh.data(), P.agg.p, agg_n * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        std::vector<uint64_t> tail_cnt(aggh.begin(), aggh.begin() + H.n);
+        std::vector<uint64_t> tail_len(aggh.begin() + H.n, aggh.begin() + 2 * H.n);
+        std::vector<uint64_t> pair_cnt(aggh.begin() + 2 * H.n, aggh.begin() + 2 * H.n + H.n_pairs);
+        std::vector<uint64_t> pair_len(aggh.begin() + 2 * H.n + H.n_pairs, aggh.begin() + 2 * H.n + 2 * H.n_pairs);
+        std::vector<uint64_t> W, V;
+        if (!completion_dp(H, tail_cnt, tail_len, pair_cnt, pair_len, W, V)) {
+            set_error("cross-SCC prime-path count exceeds 2^62");
+            return TPGEN_ERR_LIMIT_EXCEEDED;
+        }
+        TPG_CK(cudaMemcpyAsync(P.d_Wc.p, W.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemcpyAsync(P.d_Wv.p, V.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+    }
+    // ---- prime-path phase
+    TPG_TRY(count_phase(P, G, 0, s, st, launches, ms_count_kernel));
+    if (P.overflow) {
+        set_error("prime-path count exceeds 2^62");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    const int cur = P.cur;
+    const int64_t nu = P.n_units;
+    st.n_units = nu;
+
+    // ---- exact offsets: scan of the per-unit counts
+    const size_t nu1 = (size_t)std::max<int64_t>(nu, 1);
+    TPG_TRY(P.offs.ensure(nu1 * 8 * (C_NUM + 1), s));
+    uint64_t *off[C_NUM + 1];
+    for (int c = 0; c <= C_NUM; c++) {
+        off[c] = P.offs.as<uint64_t>() + (size_t)c * nu1;
+        const void *src = (c < C_NUM) ? P.cnt[cur][c].p : P.ext[cur].p;
+        if (nu) TPG_CK(cudaMemcpyAsync(off[c], src, (size_t)nu * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    uint64_t tot[C_NUM + 1] = {0};
+    TPG_TRY(scan_multi(P, off, C_NUM + 1, nu, tot, s, launches));
+    const int64_t n_pp = (int64_t)tot[C_PP], n_vert = (int64_t)tot[C_VERT];
+    st.n_extensions = (int64_t)tot[C_NUM];
+    st.n_heads = (int64_t)tot[C_HEADS];
+    st.n_segments = (int64_t)tot[C_ITEMS];
+    if ((o.max_paths > 0 && n_pp > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
+        set_error("result exceeds max_paths / max_extensions");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    st.n_paths = n_pp;
+    st.total_vertices = n_vert;
+
+    if (o.output_mode == TPGEN_OUT_COUNT_HASH) {
+        cudaEventRecord(tall.b, s);
+        TPG_CK(cudaStreamSynchronize(s));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, tall.a, tall.b);
+        st.ms_device = ms;
+        st.ms_count = ms_count_kernel;
+        st.gpu_launches = launches;
+        st.ms_total = now_ms() - t0;
+        if (stp) *stp = st;
+        return TPGEN_OK;
+    }
+
+    // ---- allocations (exact sizes)
+    OutOwner *ow = new OutOwner();
+    ow->device = P.device;
+    std::unique_ptr<OutOwner> ow_guard(ow);
+    void *d_off = nullptr, *d_vert = nullptr;
+    TPG_TRY(out_alloc_device(o, ow, (size_t)(n_pp + 1) * 8, &d_off, s));
+    ow->p_off = d_off;
+    TPG_TRY(out_alloc_device(o, ow, (size_t)n_vert * 4, &d_vert, s));
+    ow->p_vert = d_vert;
+    const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = (int64_t)tot[C_HEADS];
+    TPG_TRY(P.heads.ensure(std::max<int64_t>(n_heads, 1) * sizeof(HeadRec), s));
+    TPG_TRY(P.head_pool.ensure(std::max<uint64_t>(tot[C_HEADV], 1) * 4, s));
+    TPG_TRY(P.items.ensure(std::max<int64_t>(n_items, 1) * sizeof(ItemRec), s));
+    TPG_TRY(P.item_pool.ensure(std::max<uint64_t>(tot[C_ITEMV], 1) * 4, s));
+
+    // ---- write pass
+    DfsArgs A;
+    memset(&A, 0, sizeof(A));
+    A.G = G;
+    A.units = P.units[cur].as<Unit>();
+    A.n_units = nu;
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();
+    TPG_CK(cudaMemsetAsync(ctr, 0, 4 * 8, s));
+    A.next = ctr + 1;
+    for (int c = 0; c < C_NUM; c++) A.off[c] = off[c];
+    A.out_off = (int64_t *)d_off;
+    A.out_vert = (int32_t *)d_vert;
+    A.heads = P.heads.as<HeadRec>();
+    A.head_pool = P.head_pool.as<int32_t>();
+    A.items = P.items.as<ItemRec>();
+    A.item_pool = P.item_pool.as<int32_t>();
+    cudaEventRecord(tw.a, s);
+    if (nu > 0) {
+        dfs_kernel<PASS_WRITE><<<grid_for(nu, kDfsThreads, P.num_sms * 4), kDfsThreads, 0, s>>>(A);
+        launches++;
+    }
+    cudaEventRecord(tw.b, s);
+    TPG_CK(cudaGetLastError());
+
+    // ---- cross-SCC stitching
+    cudaEventRecord(tst.a, s);
+    if (n_heads > 0) {
+        TPG_TRY(P.hcomp.ensure((size_t)n_heads * 8, s));
+        head_weight_kernel<<<grid_for(n_heads, 256, 4096), 256, 0, s>>>(G, P.heads.as<HeadRec>(), n_heads,
+                                                                         P.hcomp.as<uint64_t>());
+        launches++;
+        uint64_t *ha[1] = {P.hcomp.as<uint64_t>()};
+        uint64_t ncomp = 0;
+        TPG_TRY(scan_multi(P, ha, 1, n_heads, &ncomp, s, launches));
+        st.n_cross = (int64_t)ncomp;
+        TPG_TRY(P.icum.ensure((size_t)std::max<int64_t>(n_items, 1) * 8, s));
+        TPG_TRY(P.ivcum.ensure((size_t)std::max<int64_t>(n_items, 1) * 8, s));
+        TPG_TRY(P.ibeg.ensure((size_t)std::max(H.n, 1) * 8, s));
+        TPG_TRY(P.iend.ensure((size_t)std::max(H.n, 1) * 8, s));
+        if (n_items > 0) {
+            item_weight_kernel<<<grid_for(n_items, 256, 4096), 256, 0, s>>>(G, P.items.as<ItemRec>(), n_items,
+                                                                             P.icum.as<uint64_t>(),
+                                                                             P.ivcum.as<uint64_t>());
+            launches++;
+            uint64_t *ia[2] = {P.icum.as<uint64_t>(), P.ivcum.as<uint64_t>()};
+            TPG_TRY(scan_multi(P, ia, 2, n_items, nullptr, s, launches));
+        }
+        item_bounds_kernel<<<grid_for(nu, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit>(), nu, off[C_ITEMS],
+                                                                    tot[C_ITEMS], P.ibeg.as<int64_t>(),
+                                                                    P.iend.as<int64_t>());
+        launches++;
+        StitchArgs SA;
+        SA.heads = P.heads.as<HeadRec>();
+        SA.n_heads = n_heads;
+        SA.comp_off = P.hcomp.as<uint64_t>();
+        SA.n_comp = ncomp;
+        SA.items = P.items.as<ItemRec>();
+        SA.cum = P.icum.as<uint64_t>();
+        SA.vcum = P.ivcum.as<uint64_t>();
+        SA.ibeg = P.ibeg.as<int64_t>();
+        SA.iend = P.iend.as<int64_t>();
+        SA.head_pool = P.head_pool.as<int32_t>();
+        SA.item_pool = P.item_pool.as<int32_t>();
+        SA.out_off = (int64_t *)d_off;
+        SA.out_vert = (int32_t *)d_vert;
+        if (ncomp > 0) {
+            stitch_kernel<<<grid_for((int64_t)ncomp * 32, 256, P.num_sms * 8), 256, 0, s>>>(SA);
+            launches++;
+        }
+    }
+    set_last_offset_kernel<<<1, 1, 0, s>>>((int64_t *)d_off, n_pp, n_vert);
+    launches++;
+    cudaEventRecord(tst.b, s);
+    cudaEventRecord(tall.b, s);
+    TPG_CK(cudaGetLastError());
+
+    if (o.compute_digest && n_pp > 0) {
+        unsigned long long *acc = ctr + 4;
+        TPG_CK(cudaMemsetAsync(acc, 0, 16, s));
+        digest_kernel<<<grid_for(n_pp, 256, P.num_sms * 8), 256, 0, s>>>((int64_t *)d_off, (int32_t *)d_vert, n_pp,
+                                                                           acc);
+        launches++;
+        unsigned long long hd[2];
+        TPG_CK(cudaMemcpyAsync(hd, acc, 16, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        st.hash_lo = hd[0];
+        st.hash_hi = hd[1];
+    }
+    TPG_CK(cudaStreamSynchronize(s));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tall.a, tall.b);
+    st.ms_device = ms;
+    cudaEventElapsedTime(&ms, tw.a, tw.b);
+    st.ms_dfs_write = ms;
+    st.ms_write = ms;
+    cudaEventElapsedTime(&ms, tst.a, tst.b);
+    st.ms_stitch = ms;
+    st.ms_count = st.ms_device - st.ms_write - st.ms_stitch;
+    st.ms_dfs_count = ms_count_kernel;
+    st.gpu_launches = launches;
+
+    ow_guard.release();
+    TPG_TRY(finish_output(o, ow, n_pp, n_vert, (int64_t *)d_off, (int32_t *)d_vert, s, out));
+    st.ms_total = now_ms() - t0;
+    if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
+// ------------------------------------------------------------ test paths
+tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry, int32_t exit,
+                            const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    memset(out, 0, sizeof(*out));
+    const HostPlan &H = P.hp;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    tpgen_paths own;
+    memset(&own, 0, sizeof(own));
+    const tpgen_paths *pp = pp_in;
+    if (!pp) {
+        tpgen_options o2 = o;
+        o2.output_on_device = 1;
+        o2.device_alloc = nullptr;
+        o2.device_free = nullptr;
+        o2.host_out = nullptr;
+        TPG_TRY(run_prime_paths(P, o2, &own, &st));
+        pp = &own;
+    }
+    struct Guard {
+        tpgen_paths *p;
+        ~Guard() { free_paths(p); }
+    } g{&own};
+    const int64_t n = pp->n_paths;
+    // PP arrays on device
+    const int64_t *d_ppo = pp->offsets;
+    const int32_t *d_ppv = pp->vertices;
+    DevBuf tmp_o, tmp_v;
+    struct BufGuard {
+        DevBuf *a, *b;
+        cudaStream_t s;
+        ~BufGuard() {
+            a->release(s);
+            b->release(s);
+        }
+    } bg{&tmp_o, &tmp_v, s};
+    if (n > 0 && !pp->on_device) {
+        int64_t nv = pp->offsets[n];
+        TPG_TRY(tmp_o.ensure((size_t)(n + 1) * 8, s));
+        TPG_TRY(tmp_v.ensure((size_t)std::max<int64_t>(nv, 1) * 4, s));
+        TPG_CK(cudaMemcpyAsync(tmp_o.p, pp->offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (nv) TPG_CK(cudaMemcpyAsync(tmp_v.p, pp->vertices, (size_t)nv * 4, cudaMemcpyHostToDevice, s));
+        d_ppo = tmp_o.as<int64_t>();
+        d_ppv = tmp_v.as<int32_t>();
+    }
+    TpTables T;
+    build_tp_tables(H, entry, exit, T);
+    // one buffer: pre_off, suf_off (int64 n each), pre_len, suf_len (int32 n each), flats
+    const size_t nn = std::max<int32_t>(H.n, 1);
+    const size_t bytes = nn * 8 * 2 + nn * 4 * 2 + (T.pre_flat.size() + T.suf_flat.size() + 2) * 4 + 64;
+    TPG_TRY(P.tp_tabs.ensure(bytes, s));
+    char *b = (char *)P.tp_tabs.p;
+    int64_t *d_pre_off = (int64_t *)b;
+    int64_t *d_suf_off = d_pre_off + nn;
+    int32_t *d_pre_len = (int32_t *)(d_suf_off + nn);
+    int32_t *d_suf_len = d_pre_len + nn;
+    int32_t *d_pre_flat = d_suf_len + nn;
+    int32_t *d_suf_flat = d_pre_flat + T.pre_flat.size() + 1;
+    TPG_CK(cudaMemcpyAsync(d_pre_off, T.pre_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(d_suf_off, T.suf_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(d_pre_len, T.pre_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(d_suf_len, T.suf_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    if (!T.pre_flat.empty())
+        TPG_CK(cudaMemcpyAsync(d_pre_flat, T.pre_flat.data(), T.pre_flat.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!T.suf_flat.empty())
+        TPG_CK(cudaMemcpyAsync(d_suf_flat, T.suf_flat.data(), T.suf_flat.size() * 4, cudaMemcpyHostToDevice, s));
+
+    DevBuf lenb;
+    struct LGuard {
+        DevBuf *a;
+        cudaStream_t s;
+        ~LGuard() { a->release(s); }
+    } lg{&lenb, s};
+    TPG_TRY(lenb.ensure((size_t)std::max<int64_t>(n, 1) * 8 + 16, s));
+    unsigned int *d_unr = (unsigned int *)(lenb.as<char>() + (size_t)std::max<int64_t>(n, 1) * 8);
+    TPG_CK(cudaMemsetAsync(d_unr, 0, 4, s));
+    TpArgs A;
+    A.pp_off = d_ppo;
+    A.pp_vert = d_ppv;
+    A.n = n;
+    A.pre_off = d_pre_off;
+    A.suf_off = d_suf_off;
+    A.pre_len = d_pre_len;
+    A.suf_len = d_suf_len;
+    A.pre_flat = d_pre_flat;
+    A.suf_flat = d_suf_flat;
+    A.tp_len = lenb.as<uint64_t>();
+    A.unreachable = d_unr;
+    int64_t launches = st.gpu_launches;
+    uint64_t total = 0;
+    if (n > 0) {
+        tp_len_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(A);
+        launches++;
+        uint64_t *arr[1] = {A.tp_len};
+        TPG_TRY(scan_multi(P, arr, 1, n, &total, s, launches));
+        unsigned int unr = 0;
+        TPG_CK(cudaMemcpyAsync(&unr, d_unr, 4, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        if (unr) {
+            set_error("a prime path's first vertex is unreachable from entry or its last cannot reach exit");
+            return TPGEN_ERR_UNREACHABLE;
+        }
+    }
+    OutOwner *ow = new OutOwner();
+    ow->device = P.device;
+    std::unique_ptr<OutOwner> ow_guard(ow);
+    void *d_off = nullptr, *d_vert = nullptr;
+    TPG_TRY(out_alloc_device(o, ow, (size_t)(n + 1) * 8, &d_off, s));
+    ow->p_off = d_off;
+    TPG_TRY(out_alloc_device(o, ow, (size_t)total * 4, &d_vert, s));
+    ow->p_vert = d_vert;
+    A.tp_off = (int64_t *)d_off;
+    A.tp_vert = (int32_t *)d_vert;
+    if (n > 0) {
+        tp_write_kernel<<<grid_for(n * 32, 256, P.num_sms * 8), 256, 0, s>>>(A);
+        launches++;
+    }
+    set_last_offset_kernel<<<1, 1, 0, s>>>((int64_t *)d_off, n, (int64_t)total);
+    launches++;
+    TPG_CK(cudaGetLastError());
+    ow_guard.release();
+    TPG_TRY(finish_output(o, ow, n, (int64_t)total, (int64_t *)d_off, (int32_t *)d_vert, s, out));
+    st.gpu_launches = launches;
+    st.ms_total = now_ms() - t0;
+    if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
+tpgen_status init_device(PlanImpl &P, const tpgen_options &o) {
+    int dev = o.device;
+    if (dev < 0) TPG_CK(cudaGetDevice(&dev));
+    TPG_CK(cudaSetDevice(dev));
+    P.device = dev;
+    TPG_CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    return TPGEN_OK;
+}
+
+}  // namespace tpg

@@ -1,0 +1,55 @@
+// engine.h -- host-side engine interface of libtpgen (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "internal.h"
+
+namespace tpg {
+
+// Grow-only, stream-ordered device buffer.
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    tpgen_status ensure(size_t bytes, cudaStream_t s);
+    void release(cudaStream_t s);
+    template <class T>
+    T *as() const {
+        return reinterpret_cast<T *>(p);
+    }
+};
+
+constexpr int kCnt = 6;
+
+// A plan: the host plan plus its device tables and the reusable workspace.
+struct PlanImpl {
+    HostPlan hp;
+    int device = 0;
+    int num_sms = 148;
+    bool dev_ok = false;
+    double ms_plan = 0;
+    // device tables
+    DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
+        d_slot_eidx, d_Wc, d_Wv;
+    // workspace (double-buffered unit arrays for refinement)
+    DevBuf units[2], status[2], ext[2], cnt[2][kCnt];
+    DevBuf stop, work, rbuf, scan_b, scan_tot, ctr, agg, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend,
+        hcomp, offs, tp_tabs;
+    int cur = 0;
+    int64_t n_units = 0;
+    bool overflow = false;
+    ~PlanImpl();
+    std::vector<DevBuf *> all_bufs();
+};
+
+tpgen_status init_device(PlanImpl &P, const tpgen_options &o);
+tpgen_status plan_upload(PlanImpl &P, cudaStream_t s);
+tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st);
+tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp, int32_t entry, int32_t exit, const tpgen_options &o,
+                            tpgen_paths *out, tpgen_stats *st);
+void free_paths(tpgen_paths *p);
+const char *last_error();
+
+}  // namespace tpg

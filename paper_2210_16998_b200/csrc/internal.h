@@ -1,0 +1,105 @@
+// internal.h -- structures shared by the host planner, the CUDA engine and the
+// C-ABI layer of libtpgen.  Not part of the public ABI (see include/tpgen.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tpgen.h"
+
+#if defined(__CUDACC__)
+#define TPG_HD __host__ __device__
+#define TPG_ALIGN(n) __align__(n)
+#else
+#define TPG_HD
+#define TPG_ALIGN(n) alignas(n)
+#endif
+
+namespace tpg {
+
+constexpr int kMaxScc = 64;  // one 64-bit visited mask per path (W = 1)
+
+enum SlotFlags : int32_t { F_ENTRY = 1, F_EXIT = 2 };
+
+// One vertex of an SCC in SCC-local order (local ids ascend with global ids,
+// so lexicographic order on local ids == order on global ids inside an SCC).
+struct TPG_ALIGN(16) Slot {
+    uint64_t sin;     // in-SCC successors (local bits; a self-loop sets the own bit)
+    uint64_t pin;     // in-SCC predecessors (local bits)
+    int32_t gid;      // global vertex id
+    int32_t out_off;  // first out-of-SCC arc (index into out_gid/out_pos)
+    int32_t out_cnt;  // number of out-of-SCC successors (sorted by global id)
+    int32_t flags;    // F_ENTRY (has a predecessor outside, Def. 4) | F_EXIT (Def. 5)
+};
+static_assert(sizeof(Slot) == 32, "Slot layout");
+
+// Head segment record: a cross-SCC block h (+) completions(x) reserved in the output.
+struct TPG_ALIGN(16) HeadRec {
+    uint64_t pp_off;   // first prime-path index of the block
+    uint64_t v_off;    // first output vertex of the block
+    uint64_t hv_off;   // head vertices in the head pool
+    int32_t len;       // |h|
+    int32_t x;         // global id of the successor outside h's SCC (an SCC entry)
+};
+static_assert(sizeof(HeadRec) == 32, "HeadRec layout");
+
+// Segment item of an entry vertex's completion table: a tail segment (y < 0) or
+// a transit segment followed by the arc to y (y = entry of a downstream SCC).
+struct TPG_ALIGN(16) ItemRec {
+    int64_t pool_off;  // vertices in the item pool
+    int32_t len;
+    int32_t y;         // -1 for a tail segment
+    int32_t ent;       // global id of the entry vertex whose table holds the item
+    int32_t pad;
+};
+static_assert(sizeof(ItemRec) == 24 || sizeof(ItemRec) == 32, "ItemRec layout");
+
+// ------------------------------------------------------------------ host plan
+struct HostPlan {
+    int32_t n = 0;
+    int64_t m = 0;
+    std::vector<int64_t> so;    // sorted successor CSR
+    std::vector<int32_t> st;
+    std::vector<int64_t> po;    // predecessor CSR
+    std::vector<int32_t> pt;
+    std::vector<int32_t> comp;  // SCC id per vertex; ids in reverse topological order (sinks first)
+    int32_t n_scc = 0, n_nontrivial = 0, max_scc = 0;
+    std::vector<int32_t> scc_vbase, scc_size, scc_out_base, scc_nout, scc_nentries;
+    std::vector<int64_t> scc_pair_base;
+    int64_t n_pairs = 0;
+    std::vector<int32_t> v_slot;     // vertex -> slot
+    std::vector<Slot> slots;         // n slots
+    std::vector<int32_t> slot_eidx;  // entry index inside its SCC, -1 if not an entry
+    std::vector<int32_t> out_gid, out_pos;
+    bool has_entries = false;        // some vertex is an SCC entry (segment phase needed)
+    std::vector<double> cost;        // per-vertex work estimate (shard balancing)
+};
+
+// Validates the CSR and builds the plan.  Returns TPGEN_OK or an error (msg set).
+tpgen_status build_plan(const int64_t *so, const int32_t *st, int32_t n, HostPlan &plan, std::string &msg,
+                        bool enforce_limit = true);
+
+// Start-vertex range [lo, hi) of a shard (contiguous, cost balanced).
+void shard_range(const HostPlan &plan, int32_t rank, int32_t count, int32_t &lo, int32_t &hi);
+
+// Completion-count DP over the component DAG:
+//   W(x) = #tails(x) + sum_arcs cnt(x,e) W(y_e),  V(x) = vertices of all completions.
+// Inputs are the per-entry tail aggregates and per-(entry, out-arc) transit
+// aggregates of the segment phase.  Returns false on overflow (>= 2^62).
+bool completion_dp(const HostPlan &plan, const std::vector<uint64_t> &tail_cnt, const std::vector<uint64_t> &tail_len,
+                   const std::vector<uint64_t> &pair_cnt, const std::vector<uint64_t> &pair_len,
+                   std::vector<uint64_t> &W, std::vector<uint64_t> &V);
+
+// Test-path tables (R15): lexmin-shortest walks.
+struct TpTables {
+    std::vector<int64_t> pre_off, suf_off;  // per vertex, -1 if unreachable
+    std::vector<int32_t> pre_len, suf_len;
+    std::vector<int32_t> pre_flat, suf_flat;
+};
+void build_tp_tables(const HostPlan &plan, int32_t entry, int32_t exit, TpTables &tp);
+
+void set_error(const std::string &msg);
+
+}  // namespace tpg

@@ -1,0 +1,351 @@
+// planner.cpp -- host side of libtpgen: CSR validation, Tarjan SCCs + the
+// component graph ("first generates the component graph of the input CFG
+// on the CPU", Def. 3), SCC-local tables for the CUDA
+// kernels, the completion-count DP over the component DAG, shard ranges and
+// the test-path prefix/suffix tables.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace tpg {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+const char *last_error() { return g_err.c_str(); }
+
+// Iterative Tarjan ("Tarjan presents an algorithm with O(|V|+|E|)").
+// SCC ids are assigned in completion order, which is a reverse topological
+// order of the component DAG: every arc between SCCs goes from a larger id to
+// a smaller id.
+static int32_t tarjan(int32_t n, const std::vector<int64_t> &so, const std::vector<int32_t> &st,
+                      std::vector<int32_t> &comp) {
+    std::vector<int32_t> index(n, -1), low(n, 0), stack;
+    std::vector<char> on(n, 0);
+    std::vector<std::pair<int32_t, int64_t>> call;  // (vertex, next arc)
+    comp.assign(n, -1);
+    int32_t next_index = 0, n_scc = 0;
+    stack.reserve(n);
+    for (int32_t r = 0; r < n; r++) {
+        if (index[r] >= 0) continue;
+        call.push_back({r, so[r]});
+        index[r] = low[r] = next_index++;
+        stack.push_back(r);
+        on[r] = 1;
+        while (!call.empty()) {
+            int32_t v = call.back().first;
+            int64_t &e = call.back().second;
+            if (e < so[v + 1]) {
+                int32_t w = st[e++];
+                if (index[w] < 0) {
+                    index[w] = low[w] = next_index++;
+                    stack.push_back(w);
+                    on[w] = 1;
+                    call.push_back({w, so[w]});
+                } else if (on[w]) {
+                    low[v] = std::min(low[v], index[w]);
+                }
+            } else {
+                if (low[v] == index[v]) {
+                    int32_t w;
+                    do {
+                        w = stack.back();
+                        stack.pop_back();
+                        on[w] = 0;
+                        comp[w] = n_scc;
+                    } while (w != v);
+                    n_scc++;
+                }
+                call.pop_back();
+                if (!call.empty()) {
+                    int32_t p = call.back().first;
+                    low[p] = std::min(low[p], low[v]);
+                }
+            }
+        }
+    }
+    return n_scc;
+}
+
+tpgen_status build_plan(const int64_t *so_in, const int32_t *st_in, int32_t n, HostPlan &P, std::string &msg,
+                        bool enforce_limit) {
+    P = HostPlan();
+    if (n < 0) { msg = "n_vertices < 0"; return TPGEN_ERR_INVALID_ARGUMENT; }
+    if (n > 0 && (!so_in || (!st_in && so_in[n] > 0))) { msg = "NULL CSR pointer"; return TPGEN_ERR_INVALID_ARGUMENT; }
+    P.n = n;
+    if (n == 0) return TPGEN_OK;
+    if (so_in[0] != 0) { msg = "csr_offsets[0] != 0"; return TPGEN_ERR_INVALID_GRAPH; }
+    for (int32_t v = 0; v < n; v++)
+        if (so_in[v + 1] < so_in[v]) { msg = "csr_offsets decreasing at row " + std::to_string(v); return TPGEN_ERR_INVALID_GRAPH; }
+    P.m = so_in[n];
+    P.so.assign(so_in, so_in + n + 1);
+    P.st.assign(st_in, st_in + P.m);
+    for (int32_t v = 0; v < n; v++) {
+        auto b = P.st.begin() + P.so[v], e = P.st.begin() + P.so[v + 1];
+        for (auto it = b; it != e; ++it)
+            if (*it < 0 || *it >= n) { msg = "target out of range in row " + std::to_string(v); return TPGEN_ERR_INVALID_GRAPH; }
+        std::sort(b, e);
+        if (std::adjacent_find(b, e) != e) { msg = "duplicate arc in row " + std::to_string(v); return TPGEN_ERR_INVALID_GRAPH; }
+    }
+    // predecessor CSR (sources ascending)
+    P.po.assign(n + 1, 0);
+    P.pt.resize(P.m);
+    for (int64_t e = 0; e < P.m; e++) P.po[P.st[e] + 1]++;
+    for (int32_t v = 0; v < n; v++) P.po[v + 1] += P.po[v];
+    {
+        std::vector<int64_t> fill(P.po.begin(), P.po.end() - 1);
+        for (int32_t v = 0; v < n; v++)
+            for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) P.pt[fill[P.st[e]]++] = v;
+    }
+
+    P.n_scc = tarjan(n, P.so, P.st, P.comp);
+    if (!enforce_limit) {  // component graph only (tpgen_components)
+        P.slots.assign(n, Slot{});
+        for (int32_t v = 0; v < n; v++) {
+            for (int64_t e = P.so[v]; e < P.so[v + 1]; e++)
+                if (P.comp[P.st[e]] != P.comp[v]) P.slots[v].flags |= F_EXIT;
+            for (int64_t e = P.po[v]; e < P.po[v + 1]; e++)
+                if (P.comp[P.pt[e]] != P.comp[v]) P.slots[v].flags |= F_ENTRY;
+        }
+        return TPGEN_OK;
+    }
+    std::vector<std::vector<int32_t>> members(P.n_scc);
+    for (int32_t v = 0; v < n; v++) members[P.comp[v]].push_back(v);  // ascending v
+    P.scc_vbase.resize(P.n_scc);
+    P.scc_size.resize(P.n_scc);
+    P.scc_out_base.resize(P.n_scc);
+    P.scc_nout.resize(P.n_scc);
+    P.scc_nentries.resize(P.n_scc);
+    P.scc_pair_base.resize(P.n_scc);
+    P.v_slot.resize(n);
+    P.slots.resize(n);
+    P.slot_eidx.assign(n, -1);
+    std::vector<int32_t> local(n);
+    int32_t base = 0;
+    for (int32_t c = 0; c < P.n_scc; c++) {
+        const auto &mem = members[c];
+        if ((int)mem.size() > kMaxScc) {
+            msg = "strongly connected component with " + std::to_string(mem.size()) +
+                  " vertices exceeds the 64-vertex limit of this build";
+            return TPGEN_ERR_UNSUPPORTED;
+        }
+        P.scc_vbase[c] = base;
+        P.scc_size[c] = (int32_t)mem.size();
+        P.max_scc = std::max<int32_t>(P.max_scc, (int32_t)mem.size());
+        for (size_t i = 0; i < mem.size(); i++) {
+            local[mem[i]] = (int32_t)i;
+            P.v_slot[mem[i]] = base + (int32_t)i;
+        }
+        base += (int32_t)mem.size();
+    }
+    int64_t pair_base = 0;
+    for (int32_t c = 0; c < P.n_scc; c++) {
+        const auto &mem = members[c];
+        P.scc_out_base[c] = (int32_t)P.out_gid.size();
+        int32_t nent = 0;
+        bool nontriv = mem.size() > 1;
+        for (int32_t v : mem) {
+            Slot &s = P.slots[P.v_slot[v]];
+            s = Slot{};
+            s.gid = v;
+            s.out_off = (int32_t)P.out_gid.size();
+            for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) {
+                int32_t w = P.st[e];
+                if (P.comp[w] == c) {
+                    s.sin |= 1ull << local[w];
+                    if (w == v) nontriv = true;
+                } else {
+                    s.flags |= F_EXIT;
+                    P.out_gid.push_back(w);
+                    // out_pos: number of SCC members with a smaller global id
+                    P.out_pos.push_back((int32_t)(std::lower_bound(mem.begin(), mem.end(), w) - mem.begin()));
+                    s.out_cnt++;
+                }
+            }
+            for (int64_t e = P.po[v]; e < P.po[v + 1]; e++) {
+                int32_t u = P.pt[e];
+                if (P.comp[u] == c) s.pin |= 1ull << local[u];
+                else s.flags |= F_ENTRY;
+            }
+            if (s.flags & F_ENTRY) {
+                P.slot_eidx[P.v_slot[v]] = nent++;
+                P.has_entries = true;
+            }
+        }
+        P.scc_nout[c] = (int32_t)P.out_gid.size() - P.scc_out_base[c];
+        P.scc_nentries[c] = nent;
+        P.scc_pair_base[c] = pair_base;
+        pair_base += (int64_t)nent * P.scc_nout[c];
+        if (nontriv) P.n_nontrivial++;
+    }
+    P.n_pairs = pair_base;
+
+    // Work estimate per start vertex for shard balancing: Knuth's random-probe
+    // estimator of the number of simple paths inside the start's SCC
+    // (deterministic seed so every rank computes the same ranges).
+    P.cost.assign(n, 1.0);
+    uint64_t rng = 0x243F6A8885A308D3ull;
+    auto next = [&rng]() {
+        rng ^= rng << 13;
+        rng ^= rng >> 7;
+        rng ^= rng << 17;
+        return rng;
+    };
+    for (int32_t v = 0; v < n; v++) {
+        int32_t c = P.comp[v];
+        if (P.scc_size[c] <= 1) continue;
+        const Slot *S = &P.slots[P.scc_vbase[c]];
+        int32_t s = local[v];
+        const int probes = 48;
+        double acc = 0;
+        for (int p = 0; p < probes; p++) {
+            uint64_t M = 1ull << s;
+            int32_t u = s;
+            double prod = 1, est = 1;
+            while (true) {
+                uint64_t cand = S[u].sin & ~M;
+                int d = __builtin_popcountll(cand);
+                if (!d) break;
+                prod *= d;
+                est += prod;
+                int pick = (int)(next() % (uint64_t)d);
+                for (int i = 0; i < pick; i++) cand &= cand - 1;
+                u = __builtin_ctzll(cand);
+                M |= 1ull << u;
+            }
+            acc += est;
+        }
+        P.cost[v] = 1.0 + acc / probes;
+    }
+    return TPGEN_OK;
+}
+
+void shard_range(const HostPlan &P, int32_t rank, int32_t count, int32_t &lo, int32_t &hi) {
+    if (count <= 1 || P.n == 0) { lo = 0; hi = P.n; return; }
+    double total = 0;
+    for (int32_t v = 0; v < P.n; v++) total += P.cost[v];
+    // boundary b_r = first vertex whose prefix cost reaches r/count of the total
+    auto boundary = [&](int32_t r) -> int32_t {
+        if (r <= 0) return 0;
+        if (r >= count) return P.n;
+        double target = total * r / count, acc = 0;
+        for (int32_t v = 0; v < P.n; v++) {
+            if (acc + 0.5 * P.cost[v] >= target) return v;
+            acc += P.cost[v];
+        }
+        return P.n;
+    };
+    lo = boundary(rank);
+    hi = boundary(rank + 1);
+    if (hi < lo) hi = lo;
+}
+
+static inline bool add_ov(uint64_t a, uint64_t b, uint64_t &r) {
+    r = a + b;
+    return r < a || r >= (1ull << 62);
+}
+static inline bool mul_ov(uint64_t a, uint64_t b, uint64_t &r) {
+    unsigned __int128 p = (unsigned __int128)a * b;
+    r = (uint64_t)p;
+    return p >= ((unsigned __int128)1 << 62);
+}
+
+bool completion_dp(const HostPlan &P, const std::vector<uint64_t> &tail_cnt, const std::vector<uint64_t> &tail_len,
+                   const std::vector<uint64_t> &pair_cnt, const std::vector<uint64_t> &pair_len,
+                   std::vector<uint64_t> &W, std::vector<uint64_t> &V) {
+    W.assign(P.n, 0);
+    V.assign(P.n, 0);
+    bool ok = true;
+    // SCC ids are reverse topological: every y reached over an out-arc of SCC c
+    // lives in an SCC with a smaller id, already final when c is processed.
+    for (int32_t c = 0; c < P.n_scc; c++) {
+        int32_t vb = P.scc_vbase[c], L = P.scc_size[c];
+        int32_t nout = P.scc_nout[c], ob = P.scc_out_base[c];
+        for (int32_t i = 0; i < L; i++) {
+            int32_t slot = vb + i;
+            int32_t ei = P.slot_eidx[slot];
+            if (ei < 0) continue;
+            int32_t x = P.slots[slot].gid;
+            uint64_t w = tail_cnt[slot], vv = tail_len[slot];
+            for (int32_t a = 0; a < nout; a++) {
+                int64_t pi = P.scc_pair_base[c] + (int64_t)ei * nout + a;
+                uint64_t cnt = pair_cnt[pi], len = pair_len[pi];
+                if (!cnt) continue;
+                int32_t y = P.out_gid[ob + a];
+                uint64_t t1, t2, t3;
+                // W += cnt * W(y); V += len * W(y) + cnt * V(y)
+                ok &= !mul_ov(cnt, W[y], t1);
+                ok &= !add_ov(w, t1, w);
+                ok &= !mul_ov(len, W[y], t2);
+                ok &= !mul_ov(cnt, V[y], t3);
+                ok &= !add_ov(vv, t2, vv);
+                ok &= !add_ov(vv, t3, vv);
+            }
+            W[x] = w;
+            V[x] = vv;
+        }
+    }
+    return ok;
+}
+
+void build_tp_tables(const HostPlan &P, int32_t entry, int32_t exit, TpTables &T) {
+    int32_t n = P.n;
+    T.pre_off.assign(n, -1);
+    T.suf_off.assign(n, -1);
+    T.pre_len.assign(n, -1);
+    T.suf_len.assign(n, -1);
+    T.pre_flat.clear();
+    T.suf_flat.clear();
+    // BFS from entry, successors ascending, first discoverer becomes the parent:
+    // the tree path is the lexicographically smallest minimum-hop walk.
+    std::vector<int32_t> parent(n, -2), order;
+    order.reserve(n);
+    parent[entry] = -1;
+    order.push_back(entry);
+    for (size_t h = 0; h < order.size(); h++) {
+        int32_t v = order[h];
+        for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) {
+            int32_t w = P.st[e];
+            if (parent[w] == -2) { parent[w] = v; order.push_back(w); }
+        }
+    }
+    std::vector<int32_t> tmp;
+    for (int32_t v = 0; v < n; v++) {
+        if (parent[v] == -2) continue;
+        tmp.clear();
+        for (int32_t c = v; c != -1; c = parent[c]) tmp.push_back(c);
+        T.pre_off[v] = (int64_t)T.pre_flat.size();
+        T.pre_len[v] = (int32_t)tmp.size();
+        T.pre_flat.insert(T.pre_flat.end(), tmp.rbegin(), tmp.rend());
+    }
+    // reverse BFS distances to exit; suffix = greedy smallest successor one hop closer
+    std::vector<int32_t> dist(n, -1);
+    order.clear();
+    dist[exit] = 0;
+    order.push_back(exit);
+    for (size_t h = 0; h < order.size(); h++) {
+        int32_t v = order[h];
+        for (int64_t e = P.po[v]; e < P.po[v + 1]; e++) {
+            int32_t u = P.pt[e];
+            if (dist[u] < 0) { dist[u] = dist[v] + 1; order.push_back(u); }
+        }
+    }
+    for (int32_t v = 0; v < n; v++) {
+        if (dist[v] < 0) continue;
+        T.suf_off[v] = (int64_t)T.suf_flat.size();
+        int32_t cur = v, len = 1;
+        T.suf_flat.push_back(cur);
+        while (cur != exit) {
+            int32_t best = -1;
+            for (int64_t e = P.so[cur]; e < P.so[cur + 1]; e++)  // successors ascending
+                if (dist[P.st[e]] == dist[cur] - 1) { best = P.st[e]; break; }
+            cur = best;
+            T.suf_flat.push_back(cur);
+            len++;
+        }
+        T.suf_len[v] = len;
+    }
+}
+
+}  // namespace tpg

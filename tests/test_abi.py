@@ -1,0 +1,120 @@
+"""CPU-side checks of the C-ABI library (no GPU needed): it loads, exports every
+symbol include/tpgen.h declares, and its host-only component-graph entry point
+(tpgen_components) matches the definitions (Defs. 3-5 P:137-156)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import brute
+from tests.conftest import ROOT
+from workloads import generators as gen
+
+import paper_2210_16998_b200 as tp
+from paper_2210_16998_b200 import _abi
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "tpgen.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(tpgen_[a-z_]+)\s*\(", src))
+    return {n for n in names if not n.endswith("_fn")}
+
+
+def test_library_exports_every_declared_symbol():
+    lib = tp.library()
+    declared = _declared_functions()
+    assert declared == set(_abi.SYMBOLS), declared ^ set(_abi.SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (tpgen_\w+)", out))
+    assert declared <= exported
+
+
+def test_version_and_status_strings():
+    lib = tp.library()
+    assert b"sm_100a" in lib.tpgen_version()
+    for code in range(9):
+        assert lib.tpgen_status_string(code)
+
+
+def test_abi_struct_sizes_match_header():
+    """The ctypes mirror must match the C layout (compiled probe, no GPU)."""
+    probe = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "tpgen.h"
+int main(void){printf("%zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
+ offsetof(tpgen_stats, ms_plan), offsetof(tpgen_options, host_out));return 0;}
+'''
+    tmpd = os.path.join(ROOT, "build")
+    os.makedirs(tmpd, exist_ok=True)
+    c = os.path.join(tmpd, "abi_probe.c")
+    exe = os.path.join(tmpd, "abi_probe")
+    open(c, "w").write(probe)
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+    vals = [int(x) for x in subprocess.check_output([exe]).split()]
+    assert vals == [ctypes.sizeof(_abi.Options), ctypes.sizeof(_abi.Stats), ctypes.sizeof(_abi.Paths),
+                    _abi.Stats.ms_plan.offset, _abi.Options.host_out.offset]
+
+
+def _corpus(count, seed0):
+    rng = np.random.default_rng(seed0)
+    for i in range(count):
+        n = int(rng.integers(1, 12))
+        yield gen.random_digraph(n, float(rng.choice([0.1, 0.2, 0.35])), seed0 + i)
+
+
+def test_components_match_definitions():
+    graphs = list(_corpus(200, 11)) + [gen.fig1b(), gen.config2(), gen.config4()]
+    for g in graphs:
+        comp, flags, nscc = tp.components(g)
+        lab = oracle.scc_labels(g)
+        # same partition as mutual reachability
+        for a in range(g.n):
+            for b in range(g.n):
+                assert (comp[a] == comp[b]) == (lab[a] == lab[b])
+        assert nscc == len(set(comp.tolist()))
+        succ = brute.graph_succ(g)
+        for v in range(g.n):
+            size = int((comp == comp[v]).sum())
+            entry = any(comp[u] != comp[v] for u in range(g.n) if v in succ[u])
+            exit_ = any(comp[w] != comp[v] for w in succ[v])
+            nontriv = size > 1 or v in succ[v]
+            assert flags[v] == (1 if entry else 0) | (2 if exit_ else 0) | (4 if nontriv else 0)
+            for w in succ[v]:  # reverse topological ids
+                assert comp[w] <= comp[v]
+
+
+def test_components_fig1b():
+    comp, flags, nscc = tp.components(gen.fig1b())
+    scc = [v for v in range(11) if comp[v] == comp[2]]
+    assert scc == [2, 3, 4, 5, 6, 8] and nscc == 6
+    assert [v for v in scc if flags[v] & 1] == [2]
+    assert [v for v in scc if flags[v] & 2] == [2, 5]
+
+
+@pytest.mark.parametrize("so,st,n,code", [
+    ([1, 1], [0], 1, 2),             # offsets[0] != 0
+    ([0, 2, 1], [1, 0], 2, 2),       # decreasing
+    ([0, 1], [5], 1, 2),             # target out of range
+    ([0, 2, 2], [1, 1], 2, 2),       # duplicate arc
+])
+def test_components_rejects_invalid_graphs(so, st, n, code):
+    with pytest.raises(tp.TpgenError) as ei:
+        tp.components((np.asarray(so), np.asarray(st)))
+    assert ei.value.status == code
+
+
+def test_compute_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(Exception):
+        tp.prime_paths(gen.fig1b())

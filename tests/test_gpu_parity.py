@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Expected values come only from oracle/ (itself pinned by tests/test_oracle.py)."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import generators as gen
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2210_16998_b200")
+
+
+def _gpu(g, **kw):
+    ps = tp.prime_paths(g, digest=True, **kw)
+    off, vert = ps.to_numpy()
+    return off, vert, ps.stats
+
+
+def _assert_same(g, **kw):
+    off, vert, st = _gpu(g, **kw)
+    ro, rv = oracle.prime_paths(g)
+    assert off.shape == ro.shape, (g.name, off.shape, ro.shape)
+    np.testing.assert_array_equal(off, ro, err_msg=g.name)
+    np.testing.assert_array_equal(vert, rv, err_msg=g.name)
+    assert (st["hash_lo"], st["hash_hi"]) == oracle.digest(ro, rv)
+    assert st["n_extensions"] == oracle.ext_count(g), g.name
+    return st
+
+
+def test_fig1b_bit_exact():
+    st = _assert_same(gen.fig1b())
+    assert st["n_paths"] == 19 and st["total_vertices"] == 114
+    assert st["n_extensions"] == 42
+    assert st["n_cross"] == 8  # 2 complete + 4 exit + 2 entry
+
+
+def test_random_corpus_individual():
+    rng = np.random.default_rng(42)
+    for i in range(120):
+        n = int(rng.integers(1, 12))
+        g = gen.random_digraph(n, float(rng.choice([0.1, 0.2, 0.3, 0.45])), 100 + i,
+                               self_loops=bool(rng.random() < 0.5))
+        _assert_same(g)
+
+
+def test_random_corpus_batched_union():
+    """Many small graphs as disjoint components of one call: many SCCs per launch."""
+    rng = np.random.default_rng(7)
+    parts = []
+    for i in range(300):
+        n = int(rng.integers(1, 10))
+        parts.append(gen.random_digraph(n, float(rng.choice([0.15, 0.25, 0.4])), 5000 + i))
+    g = gen.disjoint_union(parts, name="union300")
+    _assert_same(g)
+
+
+def test_multi_scc_chains():
+    for seed in range(40):
+        parts = [gen.random_digraph(4, 0.5, 11 * seed + j) for j in range(4)]
+        u = gen.disjoint_union(parts)
+        arcs = u.arcs() + [(3, 4), (7, 8), (11, 12), (1, 6), (0, 9), (5, 14)]
+        _assert_same(gen.from_arcs(u.n, arcs))
+
+
+@pytest.mark.parametrize("K,N", [(1, 3), (3, 3), (6, 4), (20, 5)])
+def test_seq_loops(K, N):
+    st = _assert_same(gen.k_seq_loops(K, N))
+    assert st["n_paths"] == 1 + K * N + 2 * K + K * (K - 1) // 2
+
+
+def test_config2_structured():
+    _assert_same(gen.config2())
+
+
+def test_config4_loop_chain():
+    st = _assert_same(gen.config4())
+    assert st["n_cross"] > 0.9 * st["n_paths"]
+
+
+@pytest.mark.parametrize("n,d,seed", [(12, 3, 1), (16, 3, 2), (18, 3, 3), (14, 4, 4)])
+def test_dense_scc_medium(n, d, seed):
+    """Dense SCCs big enough to force truncation/refinement rounds."""
+    st = _assert_same(gen.dense_scc(n, d, seed))
+    assert st["n_count_rounds"] >= 2
+
+
+def test_cycle_64_and_limit():
+    st = _assert_same(gen.single_loop(64))
+    assert st["n_paths"] == 64
+    with pytest.raises(tp.TpgenError) as ei:
+        tp.prime_paths(gen.single_loop(65))
+    assert ei.value.status_name == "TPGEN_ERR_UNSUPPORTED"
+
+
+def test_edge_cases():
+    empty = gen.from_arcs(0, [])
+    ps = tp.prime_paths(empty)
+    assert ps.n_paths == 0 and ps.offsets.cpu().tolist() == [0]
+    _assert_same(gen.from_arcs(1, []))            # isolated vertex -> <v>
+    _assert_same(gen.from_arcs(1, [(0, 0)]))      # self-loop -> <v,v>
+    _assert_same(gen.from_arcs(5, []))            # no arcs
+    _assert_same(gen.from_arcs(3, [(0, 0), (0, 1), (1, 1), (1, 2), (2, 2)]))
+
+
+def test_invalid_graph_errors():
+    with pytest.raises(tp.TpgenError) as ei:
+        tp.prime_paths((np.array([0, 2, 2]), np.array([1, 1])))
+    assert ei.value.status_name == "TPGEN_ERR_INVALID_GRAPH"
+    with pytest.raises(tp.TpgenError):
+        tp.prime_paths((np.array([0, 1]), np.array([3])))
+
+
+def test_shards_concatenate_to_whole():
+    g = gen.disjoint_union([gen.dense_scc(12, 3, s) for s in range(4)] + [gen.config2()], name="shards")
+    ro, rv = oracle.prime_paths(g)
+    offs, verts = [], []
+    lo_prev = 0
+    for r in range(3):
+        ps = tp.prime_paths(g, shard=(r, 3))
+        o, v = ps.to_numpy()
+        assert ps.stats["shard_lo"] == lo_prev
+        lo_prev = ps.stats["shard_hi"]
+        offs.append(o)
+        verts.append(v)
+    assert lo_prev == g.n
+    cat_v = np.concatenate(verts)
+    np.testing.assert_array_equal(cat_v, rv)
+    cat_o = [0]
+    for o in offs:
+        cat_o += (o[1:] + cat_o[-1]).tolist()
+    np.testing.assert_array_equal(np.asarray(cat_o), ro)
+
+
+def test_host_output_and_plan_reuse():
+    g = gen.config2()
+    ro, rv = oracle.prime_paths(g)
+    ps = tp.prime_paths(g, output="host")
+    o, v = ps.to_numpy()
+    np.testing.assert_array_equal(o, ro)
+    np.testing.assert_array_equal(v, rv)
+    plan = tp.Plan(g)
+    for _ in range(3):
+        o2, v2 = plan.prime_paths().to_numpy()
+        np.testing.assert_array_equal(o2, ro)
+        np.testing.assert_array_equal(v2, rv)
+    plan.close()
+
+
+def test_config3_sampled_blocks():
+    """Full config 3 in the bench's launch configuration; blocks of sampled start
+    vertices compared element by element, totals against the oracle's counters."""
+    g = gen.config3()
+    plan = tp.Plan(g)
+    ps = plan.prime_paths(digest=True)
+    off = ps.offsets
+    vert = ps.vertices
+    st = ps.stats
+    assert st["n_extensions"] == oracle.ext_count(g)
+    first = vert[off[:-1]].cpu().numpy()
+    assert np.all(np.diff(first) >= 0)
+    for s in (0, 11, 21):
+        ro, rv = oracle.prime_paths(g, v_lo=s, v_hi=s + 1)
+        idx = np.nonzero(first == s)[0]
+        a, b = int(idx[0]), int(idx[-1]) + 1
+        o = off[a:b + 1].cpu().numpy()
+        np.testing.assert_array_equal(o - o[0], ro)
+        np.testing.assert_array_equal(vert[o[0]:o[-1]].cpu().numpy(), rv)
+    plan.close()
+
+
+def test_test_paths_fig1b_and_config2():
+    for g in (gen.fig1b(), gen.config2()):
+        ro, rv = oracle.prime_paths(g)
+        to, tv = oracle.test_paths(g, ro, rv, g.entry, g.exit)
+        pp = tp.prime_paths(g)
+        ts = tp.test_paths(g, g.entry, g.exit, pp)
+        o, v = ts.to_numpy()
+        np.testing.assert_array_equal(o, to)
+        np.testing.assert_array_equal(v, tv)
+        ts2 = tp.test_paths(g, g.entry, g.exit)  # computes the PPs itself
+        o2, v2 = ts2.to_numpy()
+        np.testing.assert_array_equal(o2, to)
+        np.testing.assert_array_equal(v2, tv)
+
+
+def test_test_paths_unreachable():
+    g = gen.from_arcs(4, [(0, 1), (1, 0), (2, 3)])
+    with pytest.raises(tp.TpgenError) as ei:
+        tp.test_paths(g, 0, 1)
+    assert ei.value.status_name == "TPGEN_ERR_UNREACHABLE"
