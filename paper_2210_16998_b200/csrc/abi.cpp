@@ -205,7 +205,7 @@ tpgen_status tpgen_components(const int64_t *so, const int32_t *st, int32_t n, i
     }
     for (int32_t v = 0; v < n; v++) {
         comp[v] = P.comp[v];
-        int32_t f = P.slots[v].flags;
+        int32_t f = P.slot_flags[v];
         if (size[P.comp[v]] > 1 || loop[P.comp[v]]) f |= 4;
         flags[v] = f;
     }

@@ -98,44 +98,49 @@ __global__ void scan_down_kernel(ScanArrays S, int64_t n, const uint64_t *bsum, 
 }
 
 // ------------------------------------------------------------- refinement
-__global__ void build_worklist_kernel(DevGraph G, const Unit *units, const uint8_t *status, int64_t n, int seg_phase,
-                                      int64_t *work, unsigned long long *nwork) {
+template <int W>
+__global__ void build_worklist_kernel(DevGraph G, const Unit<W> *units, const uint8_t *status, int64_t n,
+                                      int seg_phase, int64_t *work, unsigned long long *nwork) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (status[i] != ST_PENDING) continue;
         const int32_t scc = units[i].scc;
         const int s = units[i].path[0];
-        const int flags = __ldg(&G.slots[__ldg(G.scc_vbase + scc) + s].flags);
+        const int flags = __ldg(&slot_ptr<W>(G, __ldg(G.scc_vbase + scc) + s)->flags);
         if (((flags & F_ENTRY) != 0) == (seg_phase != 0)) work[atomicAdd(nwork, 1ull)] = i;
     }
 }
 
-__global__ void refine_count_kernel(DevGraph G, const uint8_t *status, const Unit *stop, int64_t n, uint64_t *r) {
+template <int W>
+__global__ void refine_count_kernel(DevGraph G, const uint8_t *status, const Unit<W> *stop, int64_t n,
+                                    uint64_t *r) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (status[i] != ST_TRUNC) {
             r[i] = 1;
         } else {
-            Unit S = stop[i];
-            r[i] = 1 + (uint64_t)remainder_events<false>(G, S, nullptr);
+            const Unit<W> S = stop[i];
+            r[i] = 1 + (uint64_t)remainder_events<W, false>(G, S, nullptr);
         }
     }
 }
 
+template <int W>
 struct RefineBufs {
-    const Unit *units;
+    const Unit<W> *units;
     const uint8_t *status;
-    const Unit *stop;
+    const Unit<W> *stop;
     const uint64_t *cnt[C_NUM];
     const uint64_t *ext;
-    Unit *nunits;
+    Unit<W> *nunits;
     uint8_t *nstatus;
     uint64_t *ncnt[C_NUM];
     uint64_t *next;
 };
 
-__global__ void refine_scatter_kernel(DevGraph G, RefineBufs B, int64_t n, const uint64_t *off) {
+template <int W>
+__global__ void refine_scatter_kernel(DevGraph G, RefineBufs<W> B, int64_t n, const uint64_t *off) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = (int64_t)off[i];
-        Unit U = B.units[i];
+        Unit<W> U = B.units[i];
         const uint8_t st = B.status[i];
         if (st == ST_TRUNC) U.nsteps = B.stop[i].nsteps;
         B.nunits[p] = U;
@@ -144,8 +149,8 @@ __global__ void refine_scatter_kernel(DevGraph G, RefineBufs B, int64_t n, const
         for (int c = 0; c < C_NUM; c++) B.ncnt[c][p] = B.cnt[c][i];
         B.next[p] = B.ext[i];
         if (st == ST_TRUNC) {
-            Unit S = B.stop[i];
-            const int m = remainder_events<true>(G, S, B.nunits + p + 1);
+            const Unit<W> S = B.stop[i];
+            const int m = remainder_events<W, true>(G, S, B.nunits + p + 1);
             for (int q = 1; q <= m; q++) {
                 B.nstatus[p + q] = ST_PENDING;
 #pragma unroll
@@ -157,13 +162,14 @@ __global__ void refine_scatter_kernel(DevGraph G, RefineBufs B, int64_t n, const
 }
 
 // --------------------------------------------------- segment tables (a5)
-__global__ void item_bounds_kernel(DevGraph G, const Unit *units, int64_t n, const uint64_t *off_items,
+template <int W>
+__global__ void item_bounds_kernel(DevGraph G, const Unit<W> *units, int64_t n, const uint64_t *off_items,
                                    uint64_t total_items, int64_t *ibeg, int64_t *iend) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int vb = __ldg(G.scc_vbase + units[i].scc);
-        const Slot ss = ld_slot(G.slots + vb + units[i].path[0]);
-        if (!(ss.flags & F_ENTRY)) continue;
-        const int32_t g = ss.gid;
+        const int4 sm = ld_meta(slot_ptr<W>(G, vb + units[i].path[0]));
+        if (!(sm.w & F_ENTRY)) continue;
+        const int32_t g = sm.x;
         int32_t gp = -1, gn = -1;
         if (i > 0) gp = __ldg(G.slot_gid + __ldg(G.scc_vbase + units[i - 1].scc) + units[i - 1].path[0]);
         if (i + 1 < n) gn = __ldg(G.slot_gid + __ldg(G.scc_vbase + units[i + 1].scc) + units[i + 1].path[0]);

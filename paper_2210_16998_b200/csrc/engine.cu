@@ -94,10 +94,19 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
 
 tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     const HostPlan &H = P.hp;
-    TPG_TRY(upload(P.d_slots, H.slots, s));
-    std::vector<int32_t> gid(H.n);
-    for (int32_t i = 0; i < H.n; i++) gid[i] = H.slots[i].gid;
-    TPG_TRY(upload(P.d_slot_gid, gid, s));
+    // pack Slot<W> records (sin[W], pin[W], gid, out_off, out_cnt, flags)
+    const int W = H.W;
+    const size_t rec = 16 * (size_t)W + 16;
+    std::vector<uint8_t> packed(std::max<size_t>((size_t)H.n * rec, 16), 0);
+    for (int32_t i = 0; i < H.n; i++) {
+        uint8_t *r = packed.data() + (size_t)i * rec;
+        memcpy(r, &H.sin[(size_t)i * W], 8 * W);
+        memcpy(r + 8 * W, &H.pin[(size_t)i * W], 8 * W);
+        const int32_t meta[4] = {H.slot_gid[i], H.slot_out_off[i], H.slot_out_cnt[i], H.slot_flags[i]};
+        memcpy(r + 16 * W, meta, 16);
+    }
+    TPG_TRY(upload(P.d_slots, packed, s));
+    TPG_TRY(upload(P.d_slot_gid, H.slot_gid, s));
     TPG_TRY(upload(P.d_out_gid, H.out_gid, s));
     TPG_TRY(upload(P.d_out_pos, H.out_pos, s));
     TPG_TRY(upload(P.d_scc_vbase, H.scc_vbase, s));
@@ -115,7 +124,7 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
 
 static DevGraph dev_graph(PlanImpl &P, int32_t lo, int32_t hi) {
     DevGraph G;
-    G.slots = P.d_slots.as<Slot>();
+    G.slots = P.d_slots.p;
     G.slot_gid = P.d_slot_gid.as<int32_t>();
     G.out_gid = P.d_out_gid.as<int32_t>();
     G.out_pos = P.d_out_pos.as<int32_t>();
@@ -282,10 +291,11 @@ static uint32_t choose_budget(int64_t nwork, int64_t lanes) {
     return std::max<uint32_t>(32, std::min(big, b));
 }
 
+template <int W>
 static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStream_t s, tpgen_stats &st,
                                 int64_t &launches, double &ms_count_kernel) {
     Timer t;
-    const int64_t lanes = (int64_t)P.num_sms * 4 * kDfsThreads;
+    const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
     for (int round = 0; round < 4096; round++) {
         const int cur = P.cur;
         const int64_t n = P.n_units;
@@ -293,7 +303,7 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         TPG_TRY(P.work.ensure((size_t)n * 8, s));
         unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0]=nwork [1]=next [2]=ntrunc
         TPG_CK(cudaMemsetAsync(ctr, 0, 4 * 8, s));
-        build_worklist_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit>(),
+        build_worklist_kernel<W><<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit<W>>(),
                                                                      P.status[cur].as<uint8_t>(), n, seg,
                                                                      P.work.as<int64_t>(), ctr + 0);
         launches++;
@@ -305,7 +315,7 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         DfsArgs A;
         memset(&A, 0, sizeof(A));
         A.G = G;
-        A.units = P.units[cur].as<Unit>();
+        A.units = P.units[cur].as<Unit<W>>();
         A.n_units = n;
         A.work = P.work.as<int64_t>();
         A.n_work = ctr + 0;
@@ -313,7 +323,7 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.cnt[cur][c].as<uint64_t>();
         A.ext = P.ext[cur].as<uint64_t>();
         A.status = P.status[cur].as<uint8_t>();
-        A.stop = P.stop.as<Unit>();
+        A.stop = P.stop.as<Unit<W>>();
         A.budget = choose_budget(nwork, lanes);
         A.n_trunc = ctr + 2;
         unsigned long long *agg = P.agg.as<unsigned long long>();
@@ -322,9 +332,9 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         A.agg_pair_cnt = agg + 2 * (int64_t)P.hp.n;
         A.agg_pair_len = agg + 2 * (int64_t)P.hp.n + P.hp.n_pairs;
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 3);
-        const int grid = grid_for(nwork, kDfsThreads, P.num_sms * 4);
+        const int grid = grid_for(nwork, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks);
         cudaEventRecord(t.a, s);
-        dfs_kernel<PASS_COUNT><<<grid, kDfsThreads, 0, s>>>(A);
+        dfs_kernel<W, PASS_COUNT><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
         cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
@@ -338,42 +348,43 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         if (hctr[2] == 0) return TPGEN_OK;
         // ---- refine: truncated units -> counted piece + remainder units
         TPG_TRY(P.rbuf.ensure((size_t)n * 8, s));
-        refine_count_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.status[cur].as<uint8_t>(),
-                                                                    P.stop.as<Unit>(), n, P.rbuf.as<uint64_t>());
+        refine_count_kernel<W><<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.status[cur].as<uint8_t>(),
+                                                                    P.stop.as<Unit<W>>(), n, P.rbuf.as<uint64_t>());
         launches++;
         uint64_t *arr[1] = {P.rbuf.as<uint64_t>()};
         uint64_t total = 0;
         TPG_TRY(scan_multi(P, arr, 1, n, &total, s, launches));
         const int nx = cur ^ 1;
         const int64_t nn = (int64_t)total;
-        TPG_TRY(P.units[nx].ensure((size_t)nn * sizeof(Unit), s));
+        TPG_TRY(P.units[nx].ensure((size_t)nn * sizeof(Unit<W>), s));
         TPG_TRY(P.status[nx].ensure((size_t)nn, s));
         TPG_TRY(P.ext[nx].ensure((size_t)nn * 8, s));
         for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[nx][c].ensure((size_t)nn * 8, s));
-        RefineBufs B;
-        B.units = P.units[cur].as<Unit>();
+        RefineBufs<W> B;
+        B.units = P.units[cur].as<Unit<W>>();
         B.status = P.status[cur].as<uint8_t>();
-        B.stop = P.stop.as<Unit>();
+        B.stop = P.stop.as<Unit<W>>();
         for (int c = 0; c < C_NUM; c++) {
             B.cnt[c] = P.cnt[cur][c].as<uint64_t>();
             B.ncnt[c] = P.cnt[nx][c].as<uint64_t>();
         }
         B.ext = P.ext[cur].as<uint64_t>();
-        B.nunits = P.units[nx].as<Unit>();
+        B.nunits = P.units[nx].as<Unit<W>>();
         B.nstatus = P.status[nx].as<uint8_t>();
         B.next = P.ext[nx].as<uint64_t>();
-        refine_scatter_kernel<<<grid_for(n, 128, 8192), 128, 0, s>>>(G, B, n, P.rbuf.as<uint64_t>());
+        refine_scatter_kernel<W><<<grid_for(n, 128, 8192), 128, 0, s>>>(G, B, n, P.rbuf.as<uint64_t>());
         launches++;
         TPG_CK(cudaGetLastError());
         P.cur = nx;
         P.n_units = nn;
-        TPG_TRY(P.stop.ensure((size_t)nn * sizeof(Unit), s));
+        TPG_TRY(P.stop.ensure((size_t)nn * sizeof(Unit<W>), s));
     }
     set_error("count phase did not converge");
     return TPGEN_ERR_INTERNAL;
 }
 
-tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
+template <int W>
+static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
@@ -396,18 +407,18 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
     const DevGraph G = dev_graph(P, lo, hi);
 
     // ---- roots: one K_NODE unit per start vertex, ascending global id
-    std::vector<Unit> roots;
+    std::vector<Unit<W>> roots;
     roots.reserve(H.n);
     for (int32_t v = 0; v < H.n; v++) {
         const int32_t slot = H.v_slot[v];
-        const bool entry = (H.slots[slot].flags & F_ENTRY) != 0;
+        const bool entry = (H.slot_flags[slot] & F_ENTRY) != 0;
         const bool mine = v >= lo && v < hi;
         if (!entry && !mine) continue;
-        Unit u;
+        Unit<W> u;
         memset(&u, 0, sizeof(u));
         const int32_t c = H.comp[v];
         const int loc = slot - H.scc_vbase[c];
-        u.M = 1ull << loc;
+        u.M[loc >> 6] = 1ull << (loc & 63);
         u.scc = c;
         u.e = -1;
         u.kind = K_NODE;
@@ -417,14 +428,14 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
     P.cur = 0;
     P.n_units = (int64_t)roots.size();
     const size_t nr = std::max<size_t>(roots.size(), 1);
-    TPG_TRY(P.units[0].ensure(nr * sizeof(Unit), s));
+    TPG_TRY(P.units[0].ensure(nr * sizeof(Unit<W>), s));
     TPG_TRY(P.status[0].ensure(nr, s));
     TPG_TRY(P.ext[0].ensure(nr * 8, s));
     for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[0][c].ensure(nr * 8, s));
-    TPG_TRY(P.stop.ensure(nr * sizeof(Unit), s));
+    TPG_TRY(P.stop.ensure(nr * sizeof(Unit<W>), s));
     TPG_TRY(P.ctr.ensure(8 * 8, s));
     if (!roots.empty()) {
-        TPG_CK(cudaMemcpyAsync(P.units[0].p, roots.data(), roots.size() * sizeof(Unit), cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemcpyAsync(P.units[0].p, roots.data(), roots.size() * sizeof(Unit<W>), cudaMemcpyHostToDevice, s));
         TPG_CK(cudaMemsetAsync(P.status[0].p, ST_PENDING, roots.size(), s));
     }
     const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
@@ -434,7 +445,7 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
     double ms_count_kernel = 0;
     // ---- segment phase (SCC entries) -> completion DP
     if (H.has_entries) {
-        TPG_TRY(count_phase(P, G, 1, s, st, launches, ms_count_kernel));
+        TPG_TRY(count_phase<W>(P, G, 1, s, st, launches, ms_count_kernel));
         std::vector<uint64_t> aggh(agg_n);
         TPG_CK(cudaMemcpyAsync(aggh.data(), P.agg.p, agg_n * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
@@ -451,7 +462,7 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
         TPG_CK(cudaMemcpyAsync(P.d_Wv.p, V.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     }
     // ---- prime-path phase
-    TPG_TRY(count_phase(P, G, 0, s, st, launches, ms_count_kernel));
+    TPG_TRY(count_phase<W>(P, G, 0, s, st, launches, ms_count_kernel));
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
@@ -514,7 +525,7 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
     DfsArgs A;
     memset(&A, 0, sizeof(A));
     A.G = G;
-    A.units = P.units[cur].as<Unit>();
+    A.units = P.units[cur].as<Unit<W>>();
     A.n_units = nu;
     unsigned long long *ctr = P.ctr.as<unsigned long long>();
     TPG_CK(cudaMemsetAsync(ctr, 0, 4 * 8, s));
@@ -528,7 +539,8 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
     A.item_pool = P.item_pool.as<int32_t>();
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        dfs_kernel<PASS_WRITE><<<grid_for(nu, kDfsThreads, P.num_sms * 4), kDfsThreads, 0, s>>>(A);
+        dfs_kernel<W, PASS_WRITE><<<grid_for(nu, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks), DfsCfg<W>::threads,
+                                   0, s>>>(A);
         launches++;
     }
     cudaEventRecord(tw.b, s);
@@ -557,7 +569,7 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
             uint64_t *ia[2] = {P.icum.as<uint64_t>(), P.ivcum.as<uint64_t>()};
             TPG_TRY(scan_multi(P, ia, 2, n_items, nullptr, s, launches));
         }
-        item_bounds_kernel<<<grid_for(nu, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit>(), nu, off[C_ITEMS],
+        item_bounds_kernel<W><<<grid_for(nu, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit<W>>(), nu, off[C_ITEMS],
                                                                     tot[C_ITEMS], P.ibeg.as<int64_t>(),
                                                                     P.iend.as<int64_t>());
         launches++;
@@ -616,6 +628,16 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
     st.ms_total = now_ms() - t0;
     if (stp) *stp = st;
     return TPGEN_OK;
+}
+
+tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st) {
+    switch (P.hp.W) {
+        case 1: return run_pp<1>(P, o, out, st);
+        case 2: return run_pp<2>(P, o, out, st);
+        case 4: return run_pp<4>(P, o, out, st);
+    }
+    set_error("bad mask width");
+    return TPGEN_ERR_INTERNAL;
 }
 
 // ------------------------------------------------------------ test paths
@@ -743,6 +765,8 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
     ow_guard.release();
     TPG_TRY(finish_output(o, ow, n, (int64_t)total, (int64_t *)d_off, (int32_t *)d_vert, s, out));
     st.gpu_launches = launches;
+    st.n_paths = n;                  // stats describe the returned test paths
+    st.total_vertices = (int64_t)total;
     st.ms_total = now_ms() - t0;
     if (stp) *stp = st;
     return TPGEN_OK;

@@ -19,21 +19,10 @@
 
 namespace tpg {
 
-constexpr int kMaxScc = 64;  // one 64-bit visited mask per path (W = 1)
+constexpr int kMaxW = 4;              // visited mask words per path (W in {1, 2, 4})
+constexpr int kMaxScc = 64 * kMaxW;   // largest SCC this build enumerates
 
 enum SlotFlags : int32_t { F_ENTRY = 1, F_EXIT = 2 };
-
-// One vertex of an SCC in SCC-local order (local ids ascend with global ids,
-// so lexicographic order on local ids == order on global ids inside an SCC).
-struct TPG_ALIGN(16) Slot {
-    uint64_t sin;     // in-SCC successors (local bits; a self-loop sets the own bit)
-    uint64_t pin;     // in-SCC predecessors (local bits)
-    int32_t gid;      // global vertex id
-    int32_t out_off;  // first out-of-SCC arc (index into out_gid/out_pos)
-    int32_t out_cnt;  // number of out-of-SCC successors (sorted by global id)
-    int32_t flags;    // F_ENTRY (has a predecessor outside, Def. 4) | F_EXIT (Def. 5)
-};
-static_assert(sizeof(Slot) == 32, "Slot layout");
 
 // Head segment record: a cross-SCC block h (+) completions(x) reserved in the output.
 struct TPG_ALIGN(16) HeadRec {
@@ -70,8 +59,15 @@ struct HostPlan {
     std::vector<int64_t> scc_pair_base;
     int64_t n_pairs = 0;
     std::vector<int32_t> v_slot;     // vertex -> slot
-    std::vector<Slot> slots;         // n slots
-    std::vector<int32_t> slot_eidx;  // entry index inside its SCC, -1 if not an entry
+    // Slots: the vertices of each SCC in SCC-local order (local ids ascend with
+    // global ids, so lexicographic order on local ids == order on global ids).
+    int32_t W = 1;                        // mask words: ceil(max_scc / 64) rounded to 1, 2, 4
+    std::vector<uint64_t> sin, pin;       // [slot*W + word]: in-SCC successor / predecessor local bits
+    std::vector<int32_t> slot_gid;        // global vertex id
+    std::vector<int32_t> slot_out_off;    // first out-of-SCC arc (index into out_gid/out_pos)
+    std::vector<int32_t> slot_out_cnt;    // number of out-of-SCC successors (ascending global id)
+    std::vector<int32_t> slot_flags;      // F_ENTRY (Def. 4) | F_EXIT (Def. 5)
+    std::vector<int32_t> slot_eidx;       // entry index inside its SCC, -1 if not an entry
     std::vector<int32_t> out_gid, out_pos;
     bool has_entries = false;        // some vertex is an SCC entry (segment phase needed)
     std::vector<double> cost;        // per-vertex work estimate (shard balancing)

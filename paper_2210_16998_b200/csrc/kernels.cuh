@@ -1,23 +1,23 @@
-// kernels.cuh -- device code of libtpgen (sm_100a).
+// kernels.cuh -- device code of libtpgen (sm_100a): the DFS enumerator.
 //
 // Hot path: per start vertex s, depth-first
 // enumeration of the simple paths inside SCC(s) (tail extension along CSR
-// arcs, one 64-bit visited mask per path, cycle closure back to s -- PAPER.md
+// arcs, a W-word visited mask per path, cycle closure back to s -- PAPER.md
 // Alg. 4 "ExtendPath" P:459-472, Ammann-Offutt generation P:865), fused with
 // the maximality / segment classification (Def. 1, Defs. 6-9
 // P:158-176 under DESIGN.md readings R8/R9) and the canonical writer.
 //
 // Design: one lane owns one work unit (a subtree of the
 // per-start trie, or a terminal event) and walks it depth-first; the lane's
-// path lives in shared memory ([level][lane] bytes), its visited set in a
-// register.  Lanes refill from a global unit counter (warp-aggregated atomic).
-// Emission is warp-cooperative: every emitting lane's path is written by the
-// whole warp as one coalesced store stream.  Exact output offsets come from a
-// count pass with the same step function, a scan, and the write pass.  Units
-// that exceed a step budget in the count pass are split into a counted piece
-// (replayed for exactly that many steps by the write pass) plus the untried
-// sibling subtrees on its stack, which keeps lexicographic order and bounds
-// every unit's work.
+// path lives in shared memory ([level][lane] bytes), its visited set in
+// registers.  Lanes refill from a global unit counter (warp-aggregated
+// atomic).  Emission is warp-cooperative: every emitting lane's path is
+// written by the whole warp as one coalesced store stream.  Exact output
+// offsets come from a count pass with the same step function, a scan, and the
+// write pass.  Units that exceed a step budget in the count pass are split into
+// a counted piece (replayed for exactly that many steps by the write pass) plus
+// the untried sibling subtrees on its stack, which keeps lexicographic order
+// and bounds every unit's work.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,25 +33,87 @@ enum EvType : int { EV_NONE = 0, EV_PP = 1, EV_HEAD = 2, EV_TAIL = 3, EV_TRANSIT
 enum Pass : int { PASS_COUNT = 0, PASS_WRITE = 1 };
 enum Cnt : int { C_PP = 0, C_VERT = 1, C_ITEMS = 2, C_ITEMV = 3, C_HEADS = 4, C_HEADV = 5, C_NUM = 6 };
 
-// A work unit: a trie node (K_NODE: the whole subtree under it), or one
-// terminal event of a trie node (K_SELF: the node's own leaf/tail event,
-// K_CLOSURE: the cycle path(+)s, K_OUT: the arc to an out-of-SCC successor).
-struct __align__(16) Unit {
-    uint64_t M;       // visited mask of path[0..depth] (local bits)
-    int32_t scc;
-    int32_t e;        // K_OUT: out-arc index
-    uint32_t nsteps;  // write pass: replay exactly this many steps (0 = to completion)
-    uint8_t depth;    // path = path[0..depth]
-    uint8_t kind;
-    uint8_t k, o;     // stop states only: cursor at level `depth`
-    uint8_t rdepth;   // stop states only: root depth of the unit
-    uint8_t pad[7];
-    uint8_t path[64]; // local vertex ids
+// ------------------------------------------------------------------ masks
+template <int W>
+struct Mask {
+    uint64_t w[W];
 };
-static_assert(sizeof(Unit) == 96, "Unit layout");
+
+template <int W>
+__device__ __forceinline__ Mask<W> mzero() {
+    Mask<W> m;
+#pragma unroll
+    for (int i = 0; i < W; i++) m.w[i] = 0;
+    return m;
+}
+template <int W>
+__device__ __forceinline__ void mset(Mask<W> &m, int b) {
+#pragma unroll
+    for (int i = 0; i < W; i++)
+        if (i == (b >> 6)) m.w[i] |= 1ull << (b & 63);
+}
+template <int W>
+__device__ __forceinline__ void mclr(Mask<W> &m, int b) {
+#pragma unroll
+    for (int i = 0; i < W; i++)
+        if (i == (b >> 6)) m.w[i] &= ~(1ull << (b & 63));
+}
+template <int W>
+__device__ __forceinline__ Mask<W> mbit(int b) {
+    Mask<W> m = mzero<W>();
+    mset(m, b);
+    return m;
+}
+// (a & ~b) == 0
+template <int W>
+__device__ __forceinline__ bool msubset(const Mask<W> &a, const Mask<W> &b) {
+    uint64_t r = 0;
+#pragma unroll
+    for (int i = 0; i < W; i++) r |= a.w[i] & ~b.w[i];
+    return r == 0;
+}
+// lowest set bit >= k of (sin & (~M | sbit)); 64*W if none
+template <int W>
+__device__ __forceinline__ int mnext(const Mask<W> &sin, const Mask<W> &M, const Mask<W> &sbit, int k) {
+    int res = 64 * W;
+#pragma unroll
+    for (int i = W - 1; i >= 0; i--) {
+        uint64_t c = sin.w[i] & (~M.w[i] | sbit.w[i]);
+        const int lo = i * 64;
+        if (k >= lo + 64) c = 0;
+        else if (k > lo) c = (c >> (k - lo)) << (k - lo);
+        if (c) res = lo + __ffsll((long long)c) - 1;
+    }
+    return res;
+}
+
+// ------------------------------------------------------------------ tables
+// One vertex of an SCC in SCC-local order (device copy of the HostPlan slot).
+template <int W>
+struct __align__(16) Slot {
+    uint64_t sin[W];  // in-SCC successors (local bits; a self-loop sets the own bit)
+    uint64_t pin[W];  // in-SCC predecessors
+    int32_t gid, out_off, out_cnt, flags;
+};
+
+// A work unit: a trie node (K_NODE: the whole subtree under it), or one
+// terminal event of a trie node (K_CLOSURE: the cycle path(+)s, K_OUT: the arc
+// to an out-of-SCC successor).  Stop states of truncated units use the same
+// record (k, o, rdepth).
+template <int W>
+struct __align__(16) Unit {
+    uint8_t path[64 * W];  // local vertex ids, path[0..depth]
+    int32_t scc;           // (16-byte aligned: read as one int4)
+    int32_t e;             // K_OUT: out-arc index
+    uint32_t nsteps;       // write pass: replay exactly this many steps (0 = to completion)
+    uint8_t depth, kind, k, o;
+    uint64_t M[W];         // visited mask of path[0..depth]
+    uint8_t rdepth;        // stop states: root depth of the unit
+    uint8_t pad[3];
+};
 
 struct DevGraph {
-    const Slot *slots;
+    const void *slots;  // Slot<W>[n]
     const int32_t *slot_gid;
     const int32_t *out_gid;
     const int32_t *out_pos;
@@ -67,7 +129,7 @@ struct DevGraph {
 
 struct DfsArgs {
     DevGraph G;
-    const Unit *units;
+    const void *units;  // Unit<W>[n_units]
     int64_t n_units;
     const int64_t *work;  // count pass: indices of the units to process
     const unsigned long long *n_work;
@@ -76,7 +138,7 @@ struct DfsArgs {
     uint64_t *cnt[C_NUM];
     uint64_t *ext;
     uint8_t *status;
-    Unit *stop;
+    void *stop;  // Unit<W>[n_units]
     uint32_t budget;
     unsigned long long *n_trunc;
     unsigned long long *agg_tail_cnt, *agg_tail_len, *agg_pair_cnt, *agg_pair_len;
@@ -91,14 +153,20 @@ struct DfsArgs {
     int32_t *item_pool;
 };
 
-constexpr int kDfsThreads = 256;
-constexpr int kDfsWarps = kDfsThreads / 32;
+// 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
+template <int W>
+struct DfsCfg {
+    static constexpr int threads = (W <= 2) ? 256 : 128;
+    static constexpr int warps = threads / 32;
+    static constexpr int min_blocks = (W == 1) ? 4 : ((W == 2) ? 2 : 3);
+};
 constexpr unsigned kFull = 0xffffffffu;
 
 enum LanePhase : int { PH_IDLE = 0, PH_ROOT = 1, PH_RUN = 2, PH_DONE = 3, PH_EXHAUSTED = 4 };
 
+template <int W>
 struct Lane {
-    uint64_t M, sbit, ps;
+    Mask<W> M, sbit, ps;
     int32_t vb, sgid, s, u, l, r, k, o, kind, e, phase;
     uint32_t steps, limit;
     bool seg, emit;
@@ -108,44 +176,62 @@ struct Event {
     int type, len, clo, e;
 };
 
-__device__ __forceinline__ Slot ld_slot(const Slot *p) {
-    Slot s;
-    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2 *>(p));
-    const int4 b = __ldg(reinterpret_cast<const int4 *>(p) + 1);
-    s.sin = a.x;
-    s.pin = a.y;
-    s.gid = b.x;
-    s.out_off = b.y;
-    s.out_cnt = b.z;
-    s.flags = b.w;
-    return s;
+template <int W>
+__device__ __forceinline__ const Slot<W> *slot_ptr(const DevGraph &G, int i) {
+    return reinterpret_cast<const Slot<W> *>(G.slots) + i;
+}
+template <int W>
+__device__ __forceinline__ Mask<W> ld_sin(const Slot<W> *p) {
+    Mask<W> m;
+#pragma unroll
+    for (int i = 0; i < W; i++) m.w[i] = __ldg(&p->sin[i]);
+    return m;
+}
+template <int W>
+__device__ __forceinline__ Mask<W> ld_pin(const Slot<W> *p) {
+    Mask<W> m;
+#pragma unroll
+    for (int i = 0; i < W; i++) m.w[i] = __ldg(&p->pin[i]);
+    return m;
+}
+template <int W>
+__device__ __forceinline__ int4 ld_meta(const Slot<W> *p) {
+    return __ldg(reinterpret_cast<const int4 *>(&p->gid));
 }
 
 // Own event of the node whose last vertex is w (called on creation).
 //  PP mode (s not an SCC entry): internal acyclic prime path iff
 //    succ(w) within {v2..vk} and pred(s) within {v1..v(k-1)}    (Def. 1 / Def. 9)
 //  segment mode (s an SCC entry): tail segment iff succ(w) within the path  (R8)
-__device__ __forceinline__ void node_event(const DevGraph &G, const Lane &L, int w, Event &ev) {
-    const Slot sw = ld_slot(G.slots + L.vb + w);
-    if (sw.flags & F_EXIT) return;
+template <int W>
+__device__ __forceinline__ void node_event(const DevGraph &G, const Lane<W> &L, int w, Event &ev) {
+    const Slot<W> *sp = slot_ptr<W>(G, L.vb + w);
+    const int flags = __ldg(&sp->flags);
+    if (flags & F_EXIT) return;
+    const Mask<W> sw = ld_sin(sp);
     if (L.seg) {
-        if ((sw.sin & ~L.M) == 0) ev = Event{EV_TAIL, L.l + 1, 0, -1};
-    } else if (L.emit && (sw.sin & ~(L.M & ~L.sbit)) == 0 && (L.ps & ~(L.M & ~(1ull << w))) == 0) {
-        ev = Event{EV_PP, L.l + 1, 0, -1};
+        if (msubset(sw, L.M)) ev = Event{EV_TAIL, L.l + 1, 0, -1};
+    } else if (L.emit) {
+        Mask<W> inner_t = L.M, inner_h = L.M;
+#pragma unroll
+        for (int i = 0; i < W; i++) inner_t.w[i] &= ~L.sbit.w[i];
+        mclr(inner_h, w);
+        if (msubset(sw, inner_t) && msubset(L.ps, inner_h)) ev = Event{EV_PP, L.l + 1, 0, -1};
     }
 }
 
 // Arc to an out-of-SCC successor (out-arc e) from the current node.
 //  segment mode: transit segment item (Def. 6, all entry->exit paths, R9)
 //  PP mode: a head segment iff pred(s) lies on the path (R8) -> cross block
-__device__ __forceinline__ void out_event(const Lane &L, int e, Event &ev) {
+template <int W>
+__device__ __forceinline__ void out_event(const Lane<W> &L, int e, Event &ev) {
     if (L.seg) ev = Event{EV_TRANSIT, L.l + 1, 0, e};
-    else if ((L.ps & ~L.M) == 0) ev = Event{EV_HEAD, L.l + 1, 0, e};
+    else if (msubset(L.ps, L.M)) ev = Event{EV_HEAD, L.l + 1, 0, e};
 }
 
-__device__ __forceinline__ int count_out_le(const DevGraph &G, const Slot &su, int w) {
+__device__ __forceinline__ int count_out_le(const DevGraph &G, int out_off, int out_cnt, int w) {
     int o = 0;
-    while (o < su.out_cnt && __ldg(G.out_pos + su.out_off + o) <= w) o++;
+    while (o < out_cnt && __ldg(G.out_pos + out_off + o) <= w) o++;
     return o;
 }
 
@@ -153,7 +239,8 @@ __device__ __forceinline__ int count_out_le(const DevGraph &G, const Slot &su, i
 // ascending global id: in-SCC successors (local bits, ascending local id ==
 // ascending global id), the closing arc back to s, and out-of-SCC successors
 // (merged by their rank out_pos among the SCC members).
-__device__ __forceinline__ void dfs_step(const DevGraph &G, Lane &L, uint8_t *mypath, Event &ev, uint64_t &ext) {
+template <int W>
+__device__ __forceinline__ void dfs_step(const DevGraph &G, Lane<W> &L, uint8_t *mypath, Event &ev, uint64_t &ext) {
     if (L.phase == PH_ROOT) {
         switch (L.kind) {
             case K_NODE:
@@ -178,19 +265,18 @@ __device__ __forceinline__ void dfs_step(const DevGraph &G, Lane &L, uint8_t *my
                 return;
         }
     }
-    const Slot su = ld_slot(G.slots + L.vb + L.u);
-    uint64_t cand = su.sin & (~L.M | L.sbit);
-    cand = (L.k >= 64) ? 0ull : (cand >> L.k) << L.k;
-    const int w = cand ? (__ffsll((long long)cand) - 1) : 64;
-    if (L.o < su.out_cnt) {
-        const int e = su.out_off + L.o;
+    const Slot<W> *su = slot_ptr<W>(G, L.vb + L.u);
+    const int4 meta = ld_meta(su);  // gid, out_off, out_cnt, flags
+    const int w = mnext(ld_sin(su), L.M, L.sbit, L.k);
+    if (L.o < meta.z) {
+        const int e = meta.y + L.o;
         if (__ldg(G.out_pos + e) <= w) {
             L.o++;
             out_event(L, e, ev);
             return;
         }
     }
-    if (w < 64) {
+    if (w < 64 * W) {
         L.k = w + 1;
         if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
             if (L.emit) {
@@ -201,7 +287,7 @@ __device__ __forceinline__ void dfs_step(const DevGraph &G, Lane &L, uint8_t *my
         }
         L.l++;
         mypath[L.l * 32] = (uint8_t)w;
-        L.M |= 1ull << w;
+        mset(L.M, w);
         L.u = w;
         L.k = 0;
         L.o = 0;
@@ -214,12 +300,12 @@ __device__ __forceinline__ void dfs_step(const DevGraph &G, Lane &L, uint8_t *my
         return;
     }
     const int wold = L.u;
-    L.M &= ~(1ull << wold);
+    mclr(L.M, wold);
     L.l--;
     L.u = mypath[L.l * 32];
     L.k = wold + 1;
-    const Slot sp = ld_slot(G.slots + L.vb + L.u);
-    L.o = count_out_le(G, sp, wold);
+    const int4 pm = ld_meta(slot_ptr<W>(G, L.vb + L.u));
+    L.o = count_out_le(G, pm.y, pm.z, wold);
 }
 
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b, unsigned int *ovf) {
@@ -239,18 +325,20 @@ __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b, unsigned int
     return lo;
 }
 
-template <int PASS>
-__global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
-    __shared__ uint8_t spath[kDfsWarps * 64 * 32];
+template <int W, int PASS>
+__global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs_kernel(DfsArgs A) {
+    __shared__ uint8_t spath[DfsCfg<W>::warps * 64 * W * 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t *wpath = spath + wid * 64 * 32;  // [level][lane]
+    uint8_t *wpath = spath + wid * 64 * W * 32;  // [level][lane]
     uint8_t *mypath = wpath + lane;
     const DevGraph &G = A.G;
+    const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
     const int64_t nwork = (PASS == PASS_COUNT) ? (int64_t)*A.n_work : A.n_units;
 
-    Lane L;
+    Lane<W> L;
     L.phase = PH_IDLE;
     int64_t uidx = -1;
+    int32_t uscc = 0;
     uint64_t c[C_NUM];
     uint64_t ext = 0;
     int64_t pair_row = 0;
@@ -269,15 +357,15 @@ __global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
                 const int64_t my = (int64_t)base + __popc(idle & ((1u << lane) - 1));
                 if (my < nwork) {
                     uidx = (PASS == PASS_COUNT) ? A.work[my] : my;
-                    const Unit *U = A.units + uidx;
-                    const uint4 h0 = *reinterpret_cast<const uint4 *>(U);
-                    const uint4 h1 = *(reinterpret_cast<const uint4 *>(U) + 1);
-                    L.M = ((uint64_t)h0.y << 32) | h0.x;
-                    const int32_t scc = (int32_t)h0.z;
-                    L.e = (int32_t)h0.w;
-                    const uint32_t nsteps = h1.x;
-                    const int depth = h1.y & 0xff;
-                    L.kind = (h1.y >> 8) & 0xff;
+                    const Unit<W> *U = units + uidx;
+#pragma unroll
+                    for (int i = 0; i < W; i++) L.M.w[i] = U->M[i];
+                    const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
+                    uscc = h.x;
+                    L.e = h.y;
+                    const uint32_t nsteps = (uint32_t)h.z;
+                    const int depth = h.w & 0xff;
+                    L.kind = (h.w >> 8) & 0xff;
                     L.l = L.r = depth;
                     const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
                     int s = 0, u = 0;
@@ -298,14 +386,15 @@ __global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
                     }
                     L.s = s;
                     L.u = u;
-                    L.sbit = 1ull << s;
-                    L.vb = __ldg(G.scc_vbase + scc);
+                    L.sbit = mbit<W>(s);
+                    L.vb = __ldg(G.scc_vbase + uscc);
                     s_slot = L.vb + s;
-                    const Slot ss = ld_slot(G.slots + s_slot);
-                    L.ps = ss.pin;
-                    L.seg = (ss.flags & F_ENTRY) != 0;
-                    L.sgid = ss.gid;
-                    L.emit = ss.gid >= G.shard_lo && ss.gid < G.shard_hi;
+                    const Slot<W> *ss = slot_ptr<W>(G, s_slot);
+                    L.ps = ld_pin(ss);
+                    const int4 sm = ld_meta(ss);
+                    L.seg = (sm.w & F_ENTRY) != 0;
+                    L.sgid = sm.x;
+                    L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
                     L.k = 0;
                     L.o = 0;
                     L.steps = 0;
@@ -316,9 +405,9 @@ __global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
                         for (int i = 0; i < C_NUM; i++) c[i] = 0;
                         ext = 0;
                         if (L.seg) {
-                            const int32_t nout = __ldg(G.scc_nout + scc);
-                            pair_row = __ldg(G.scc_pair_base + scc) +
-                                       (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + scc);
+                            const int32_t nout = __ldg(G.scc_nout + uscc);
+                            pair_row = __ldg(G.scc_pair_base + uscc) +
+                                       (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
                         }
                     } else {
                         L.limit = nsteps ? nsteps : 0xffffffffu;
@@ -336,7 +425,7 @@ __global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
         Event ev;
         ev.type = EV_NONE;
         if (active) {
-            dfs_step(G, L, mypath, ev, ext);
+            dfs_step<W>(G, L, mypath, ev, ext);
             L.steps++;
         }
 
@@ -424,18 +513,16 @@ __global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
                     A.ext[uidx] = ext;
                     A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
                     if (trunc) {
-                        Unit *S = A.stop + uidx;
-                        uint4 h0, h1;
-                        h0.x = (uint32_t)L.M;
-                        h0.y = (uint32_t)(L.M >> 32);
-                        h0.z = (uint32_t)A.units[uidx].scc;
-                        h0.w = 0;
-                        h1.x = L.steps;
-                        h1.y = (uint32_t)L.l | ((uint32_t)K_NODE << 8) | ((uint32_t)L.k << 16) | ((uint32_t)L.o << 24);
-                        h1.z = (uint32_t)L.r;
-                        h1.w = 0;
-                        reinterpret_cast<uint4 *>(S)[0] = h0;
-                        reinterpret_cast<uint4 *>(S)[1] = h1;
+                        Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
+#pragma unroll
+                        for (int i = 0; i < W; i++) S->M[i] = L.M.w[i];
+                        int4 h;
+                        h.x = uscc;
+                        h.y = -1;
+                        h.z = (int)L.steps;
+                        h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
+                        *reinterpret_cast<int4 *>(&S->scc) = h;
+                        S->rdepth = (uint8_t)L.r;
                         for (int j = 0; j <= L.l; j++) S->path[j] = mypath[j * 32];
                         atomicAdd(A.n_trunc, 1ull);
                     }
@@ -449,41 +536,44 @@ __global__ void __launch_bounds__(kDfsThreads, 4) dfs_kernel(DfsArgs A) {
 // ------------------------------------------------------------- refinement
 // Remainder of a truncated unit: the untried events of every node on its stop
 // stack, deepest level first (lexicographic order of the rest of the walk).
-template <bool WRITE>
-__device__ int remainder_events(const DevGraph &G, const Unit &S, Unit *out) {
+template <int W, bool WRITE>
+__device__ int remainder_events(const DevGraph &G, const Unit<W> &S, Unit<W> *out) {
     const int vb = __ldg(G.scc_vbase + S.scc);
     const int s = S.path[0];
-    const uint64_t sbit = 1ull << s;
-    const Slot ss = ld_slot(G.slots + vb + s);
-    const bool seg = (ss.flags & F_ENTRY) != 0;
-    const uint64_t ps = ss.pin;
-    uint64_t M = S.M;
+    const Mask<W> sbit = mbit<W>(s);
+    const Slot<W> *ss = slot_ptr<W>(G, vb + s);
+    const bool seg = (__ldg(&ss->flags) & F_ENTRY) != 0;
+    const Mask<W> ps = ld_pin(ss);
+    Mask<W> M;
+#pragma unroll
+    for (int i = 0; i < W; i++) M.w[i] = S.M[i];
     int n = 0;
     for (int j = S.depth; j >= (int)S.rdepth; j--) {
         const int u = S.path[j];
-        const Slot su = ld_slot(G.slots + vb + u);
+        const Slot<W> *su = slot_ptr<W>(G, vb + u);
+        const int4 meta = ld_meta(su);
+        const Mask<W> sin = ld_sin(su);
         int k, o;
         if (j == S.depth) {
             k = S.k;
             o = S.o;
         } else {
             const int wc = S.path[j + 1];
-            M &= ~(1ull << wc);
+            mclr(M, wc);
             k = wc + 1;
-            o = count_out_le(G, su, wc);
+            o = count_out_le(G, meta.y, meta.z, wc);
         }
-        uint64_t cand = su.sin & (~M | sbit);
-        cand = (k >= 64) ? 0ull : (cand >> k) << k;
         while (true) {
-            const int w = cand ? (__ffsll((long long)cand) - 1) : 64;
-            if (o < su.out_cnt && __ldg(G.out_pos + su.out_off + o) <= w) {
-                const int e = su.out_off + o;
+            const int w = mnext(sin, M, sbit, k);
+            if (o < meta.z && __ldg(G.out_pos + meta.y + o) <= w) {
+                const int e = meta.y + o;
                 o++;
-                if (seg || (ps & ~M) == 0) {
+                if (seg || msubset(ps, M)) {
                     if (WRITE) {
-                        Unit &U = out[n];
+                        Unit<W> &U = out[n];
                         U = S;
-                        U.M = M;
+#pragma unroll
+                        for (int i = 0; i < W; i++) U.M[i] = M.w[i];
                         U.e = e;
                         U.nsteps = 0;
                         U.depth = (uint8_t)j;
@@ -494,20 +584,21 @@ __device__ int remainder_events(const DevGraph &G, const Unit &S, Unit *out) {
                 }
                 continue;
             }
-            if (w == 64) break;
-            cand &= cand - 1;
+            if (w >= 64 * W) break;
+            k = w + 1;
             if (WRITE) {
-                Unit &U = out[n];
+                Unit<W> &U = out[n];
                 U = S;
                 U.nsteps = 0;
                 U.k = U.o = U.rdepth = 0;
                 U.e = -1;
+#pragma unroll
+                for (int i = 0; i < W; i++) U.M[i] = M.w[i];
                 if (w == s) {
-                    U.M = M;
                     U.depth = (uint8_t)j;
                     U.kind = K_CLOSURE;
                 } else {
-                    U.M = M | (1ull << w);
+                    U.M[w >> 6] |= 1ull << (w & 63);
                     U.depth = (uint8_t)(j + 1);
                     U.path[j + 1] = (uint8_t)w;
                     U.kind = K_NODE;

@@ -101,12 +101,12 @@ tpgen_status build_plan(const int64_t *so_in, const int32_t *st_in, int32_t n, H
 
     P.n_scc = tarjan(n, P.so, P.st, P.comp);
     if (!enforce_limit) {  // component graph only (tpgen_components)
-        P.slots.assign(n, Slot{});
+        P.slot_flags.assign(n, 0);  // indexed by vertex here
         for (int32_t v = 0; v < n; v++) {
             for (int64_t e = P.so[v]; e < P.so[v + 1]; e++)
-                if (P.comp[P.st[e]] != P.comp[v]) P.slots[v].flags |= F_EXIT;
+                if (P.comp[P.st[e]] != P.comp[v]) P.slot_flags[v] |= F_EXIT;
             for (int64_t e = P.po[v]; e < P.po[v + 1]; e++)
-                if (P.comp[P.pt[e]] != P.comp[v]) P.slots[v].flags |= F_ENTRY;
+                if (P.comp[P.pt[e]] != P.comp[v]) P.slot_flags[v] |= F_ENTRY;
         }
         return TPGEN_OK;
     }
@@ -119,15 +119,18 @@ tpgen_status build_plan(const int64_t *so_in, const int32_t *st_in, int32_t n, H
     P.scc_nentries.resize(P.n_scc);
     P.scc_pair_base.resize(P.n_scc);
     P.v_slot.resize(n);
-    P.slots.resize(n);
+    P.slot_gid.assign(n, 0);
+    P.slot_out_off.assign(n, 0);
+    P.slot_out_cnt.assign(n, 0);
+    P.slot_flags.assign(n, 0);
     P.slot_eidx.assign(n, -1);
     std::vector<int32_t> local(n);
     int32_t base = 0;
     for (int32_t c = 0; c < P.n_scc; c++) {
         const auto &mem = members[c];
         if ((int)mem.size() > kMaxScc) {
-            msg = "strongly connected component with " + std::to_string(mem.size()) +
-                  " vertices exceeds the 64-vertex limit of this build";
+            msg = "strongly connected component with " + std::to_string(mem.size()) + " vertices exceeds the " +
+                  std::to_string(kMaxScc) + "-vertex limit of this build";
             return TPGEN_ERR_UNSUPPORTED;
         }
         P.scc_vbase[c] = base;
@@ -139,6 +142,10 @@ tpgen_status build_plan(const int64_t *so_in, const int32_t *st_in, int32_t n, H
         }
         base += (int32_t)mem.size();
     }
+    P.W = P.max_scc <= 64 ? 1 : (P.max_scc <= 128 ? 2 : 4);
+    const int W = P.W;
+    P.sin.assign((size_t)n * W, 0);
+    P.pin.assign((size_t)n * W, 0);
     int64_t pair_base = 0;
     for (int32_t c = 0; c < P.n_scc; c++) {
         const auto &mem = members[c];
@@ -146,30 +153,30 @@ tpgen_status build_plan(const int64_t *so_in, const int32_t *st_in, int32_t n, H
         int32_t nent = 0;
         bool nontriv = mem.size() > 1;
         for (int32_t v : mem) {
-            Slot &s = P.slots[P.v_slot[v]];
-            s = Slot{};
-            s.gid = v;
-            s.out_off = (int32_t)P.out_gid.size();
+            const int32_t sl = P.v_slot[v];
+            uint64_t *sin = &P.sin[(size_t)sl * W], *pin = &P.pin[(size_t)sl * W];
+            P.slot_gid[sl] = v;
+            P.slot_out_off[sl] = (int32_t)P.out_gid.size();
             for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) {
                 int32_t w = P.st[e];
                 if (P.comp[w] == c) {
-                    s.sin |= 1ull << local[w];
+                    sin[local[w] >> 6] |= 1ull << (local[w] & 63);
                     if (w == v) nontriv = true;
                 } else {
-                    s.flags |= F_EXIT;
+                    P.slot_flags[sl] |= F_EXIT;
                     P.out_gid.push_back(w);
                     // out_pos: number of SCC members with a smaller global id
                     P.out_pos.push_back((int32_t)(std::lower_bound(mem.begin(), mem.end(), w) - mem.begin()));
-                    s.out_cnt++;
+                    P.slot_out_cnt[sl]++;
                 }
             }
             for (int64_t e = P.po[v]; e < P.po[v + 1]; e++) {
                 int32_t u = P.pt[e];
-                if (P.comp[u] == c) s.pin |= 1ull << local[u];
-                else s.flags |= F_ENTRY;
+                if (P.comp[u] == c) pin[local[u] >> 6] |= 1ull << (local[u] & 63);
+                else P.slot_flags[sl] |= F_ENTRY;
             }
-            if (s.flags & F_ENTRY) {
-                P.slot_eidx[P.v_slot[v]] = nent++;
+            if (P.slot_flags[sl] & F_ENTRY) {
+                P.slot_eidx[sl] = nent++;
                 P.has_entries = true;
             }
         }
@@ -195,24 +202,34 @@ tpgen_status build_plan(const int64_t *so_in, const int32_t *st_in, int32_t n, H
     for (int32_t v = 0; v < n; v++) {
         int32_t c = P.comp[v];
         if (P.scc_size[c] <= 1) continue;
-        const Slot *S = &P.slots[P.scc_vbase[c]];
+        const uint64_t *S = &P.sin[(size_t)P.scc_vbase[c] * W];
         int32_t s = local[v];
         const int probes = 48;
         double acc = 0;
         for (int p = 0; p < probes; p++) {
-            uint64_t M = 1ull << s;
+            uint64_t M[kMaxW] = {0, 0, 0, 0};
+            M[s >> 6] |= 1ull << (s & 63);
             int32_t u = s;
             double prod = 1, est = 1;
             while (true) {
-                uint64_t cand = S[u].sin & ~M;
-                int d = __builtin_popcountll(cand);
+                int d = 0;
+                for (int i = 0; i < W; i++) d += __builtin_popcountll(S[(size_t)u * W + i] & ~M[i]);
                 if (!d) break;
                 prod *= d;
                 est += prod;
                 int pick = (int)(next() % (uint64_t)d);
-                for (int i = 0; i < pick; i++) cand &= cand - 1;
-                u = __builtin_ctzll(cand);
-                M |= 1ull << u;
+                for (int i = 0; i < W; i++) {
+                    uint64_t cand = S[(size_t)u * W + i] & ~M[i];
+                    int cw = __builtin_popcountll(cand);
+                    if (pick >= cw) {
+                        pick -= cw;
+                        continue;
+                    }
+                    for (int q = 0; q < pick; q++) cand &= cand - 1;
+                    u = i * 64 + __builtin_ctzll(cand);
+                    break;
+                }
+                M[u >> 6] |= 1ull << (u & 63);
             }
             acc += est;
         }
@@ -266,7 +283,7 @@ bool completion_dp(const HostPlan &P, const std::vector<uint64_t> &tail_cnt, con
             int32_t slot = vb + i;
             int32_t ei = P.slot_eidx[slot];
             if (ei < 0) continue;
-            int32_t x = P.slots[slot].gid;
+            int32_t x = P.slot_gid[slot];
             uint64_t w = tail_cnt[slot], vv = tail_len[slot];
             for (int32_t a = 0; a < nout; a++) {
                 int64_t pi = P.scc_pair_base[c] + (int64_t)ei * nout + a;
