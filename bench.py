@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark of the TPGen hot path on B200 (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs): at N=1 the largest single-GPU configuration,
+config 3 -- one dense SCC of 22 vertices, exact out-degree 4 (seed 1):
+E_canon = 2.34e8 path extensions, 6.0e7 prime paths, 1.1e9 output vertices.
+For N > 1 the job is weak-scaled: N disjoint copies of that SCC, rank r owns
+the start vertices of copy r (no data-path collective; counts and times are
+reduced over NCCL at the end).
+
+A "step" is one full tpgen_plan_prime_paths call: count rounds + completion DP
++ scan + DFS write pass + stitching, output materialised in HBM (canonical
+offsets + vertices).  `value` = prime paths / s over all ranks (device time,
+CUDA events, max over ranks); `e2e` = the same through tpgen_prime_paths with
+the CSR in host memory and the result copied into pinned host memory.
+
+--impl reference runs the CPU oracle (oracle/, single core) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from workloads import generators as gen  # noqa: E402
+
+HBM_FALLBACK = 6650.0
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def workload(n_ranks: int):
+    base = gen.config3()
+    if n_ranks == 1:
+        return base, [(0, base.n)]
+    g = gen.disjoint_union([base] * n_ranks, name=f"{n_ranks}x_{base.name}")
+    return g, [(r * base.n, (r + 1) * base.n) for r in range(n_ranks)]
+
+
+# algorithmic bytes per unit of the hot path --
+# 2 x (8W + 1 + 4) B per extension (frontier record written + read, W = 1)
+# + (4 len + 8) B per prime path (int32 vertices + int64 offset).
+def algorithmic_bytes(ext: int, n_pp: int, n_vert: int) -> float:
+    return 2.0 * 13.0 * ext + 4.0 * n_vert + 8.0 * n_pp
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for nm, v in zip(names, r[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args):
+    """The CPU oracle as it stands, single core, bounded sample per step."""
+    import oracle
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    g, _ = workload(1)
+    starts = list(range(0, 4))  # bounded sample: start vertices 0..3 of config 3 (~2.5 s per step)
+    times, npp = [], 0
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        off, _ = oracle.prime_paths(g, v_lo=starts[0], v_hi=starts[-1] + 1)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+            npp = len(off) - 1
+    total = sum(times)
+    value = npp * len(times) / total
+    sample = f"config3 start vertices {starts[0]}..{starts[-1]} ({npp} prime paths per step), oracle/oracle.c DFS"
+    print(json.dumps({
+        "impl": "reference", "metric": "prime_paths_per_sec", "value": value, "unit": "PP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": g.name, "n_vertices": g.n, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "PP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "PP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline_leg():
+    import oracle
+
+    g, _ = workload(1)
+    t = time.perf_counter()
+    off, _ = oracle.prime_paths(g, v_lo=0, v_hi=4)
+    dt = time.perf_counter() - t
+    npp = len(off) - 1
+    return {"value": npp / dt, "unit": "PP/s", "cores": 1, "kind": "oracle",
+            "sample": f"config3 start vertices 0..3: {npp} prime paths in {dt:.2f} s (single core, oracle/oracle.c)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2210_16998_b200 as tp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    g, ranges = workload(world)
+    rng = ranges[rank]
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    plan = tp.Plan(g, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
+
+    # ---------------- device-resident timing (value)
+    for _ in range(args.warmup):
+        ps = plan.prime_paths(start_range=rng)
+        del ps
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stats = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)  # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            ps = plan.prime_paths(start_range=rng)
+            ev[k][1].record(stream)
+            stats.append(ps.stats)
+            del ps
+        torch.cuda.synchronize()
+    barrier()
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms_total = float(sum(ms_steps))
+    st = stats[-1]
+    n_pp, n_vert, ext = st["n_paths"], st["total_vertices"], st["n_extensions"]
+    ms_write = float(np.mean([s["ms_dfs_write"] for s in stats]))
+    launches = int(sum(s["gpu_launches"] for s in stats))
+
+    # ---------------- end-to-end through the public C ABI (host CSR in, pinned host result out)
+    e2e = None
+    if not args.no_e2e:
+        host_out = torch.empty(8 * (n_pp + 1) + 4 * n_vert, dtype=torch.uint8, pin_memory=True)
+        h2d = int(g.offsets.nbytes + g.targets.nbytes)
+        d2h = 8 * (n_pp + 1) + 4 * n_vert
+        e2e_steps = max(1, min(args.steps, 3))
+        ps = tp.prime_paths(g, device=dev, output="host", host_out=host_out, start_range=rng)
+        del ps
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ps = tp.prime_paths(g, device=dev, output="host", host_out=host_out, start_range=rng)
+            del ps
+        torch.cuda.synchronize()
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
+        e2e = {"value": None, "unit": "PP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_ms, "steps": e2e_steps}
+
+    # ---------------- reduce over ranks
+    vals = torch.tensor([float(n_pp) * args.steps, float(ext) * args.steps, ms_total,
+                         e2e["ms_per_step"] if e2e else 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        sums = vals.clone()
+        dist.all_reduce(sums[:2], op=dist.ReduceOp.SUM)
+        mx = vals.clone()
+        dist.all_reduce(mx[2:], op=dist.ReduceOp.MAX)
+        vals = torch.cat([sums[:2], mx[2:]])
+    tot_pp, tot_ext, ms_max, e2e_ms_max = vals.tolist()
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        a_bytes = algorithmic_bytes(ext, n_pp, n_vert)
+        achieved = a_bytes / (ms_write * 1e-3) / 1e9
+        value = tot_pp / (ms_max * 1e-3)
+        if e2e is not None:
+            e2e["value"] = (tot_pp / args.steps) / (e2e_ms_max * 1e-3)
+            e2e["ms_per_step"] = e2e_ms_max
+        out = {
+            "metric": "prime_paths_per_sec",
+            "value": value,
+            "unit": "PP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": "config3: dense SCC n=22 out-degree 4 seed 1" +
+                       (f" x{world} disjoint copies, one per rank" if world > 1 else ""),
+                       "n_vertices": g.n, "prime_paths_per_rank": n_pp, "output_vertices_per_rank": n_vert,
+                       "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",
+                       "parallelism": f"start-vertex shards x{world}"},
+            "extensions_per_sec": tot_ext / (ms_max * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "dfs_kernel<1,PASS_WRITE>",
+                         "algorithmic_bytes_per_launch": a_bytes, "ms_per_launch": ms_write,
+                         "peak_kind": peak_kind,
+                         "model": "SURVEY 8(d): 26 B/extension + (4 len + 8) B/prime path"},
+            "breakdown_ms": {k: float(np.mean([s[k] for s in stats]))
+                             for k in ("ms_count", "ms_dfs_count", "ms_write", "ms_stitch", "ms_device")},
+            "count_rounds": st["n_count_rounds"],
+            "n_units": st["n_units"],
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_leg()
+        print(json.dumps(out))
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

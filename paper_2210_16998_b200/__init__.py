@@ -103,7 +103,8 @@ class _TorchAllocator:
 
 
 def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest: bool, max_paths: int,
-             max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None) -> _abi.Options:
+             max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None,
+             start_range: Optional[Tuple[int, int]] = None) -> _abi.Options:
     lib = library()
     o = _abi.Options()
     lib.tpgen_options_init(ctypes.byref(o))
@@ -112,6 +113,8 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
     o.output_on_device = 1 if output == "device" else 0
     o.output_mode = _abi.OUT_COUNT_HASH if mode == "count" else _abi.OUT_MATERIALIZE
     o.shard_rank, o.shard_count = shard
+    if start_range is not None:
+        o.start_lo, o.start_hi = start_range
     o.max_paths = max_paths
     o.max_extensions = max_extensions
     o.compute_digest = 1 if digest else 0
@@ -168,7 +171,8 @@ def _wrap(paths: _abi.Paths, stats: _abi.Stats, alloc: Optional[_TorchAllocator]
 
 def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "materialize",
                 shard: Tuple[int, int] = (0, 1), digest: bool = False, max_paths: int = 0,
-                max_extensions: int = 0, stream=None, host_out=None) -> PathSet:
+                max_extensions: int = 0, stream=None, host_out=None,
+                start_range: Optional[Tuple[int, int]] = None) -> PathSet:
     """All prime paths of ``graph`` (Def. 1), canonical order.
 
     ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host)."""
@@ -176,7 +180,7 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
     so, st, n = _csr(graph)
     alloc = _TorchAllocator(device) if output == "device" else None
     o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
-                 alloc, host_out)
+                 alloc, host_out, start_range)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_prime_paths(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc, host_out)
@@ -241,11 +245,12 @@ class Plan:
         self._h = h
 
     def prime_paths(self, *, output: str = "device", mode: str = "materialize", shard: Tuple[int, int] = (0, 1),
-                    digest: bool = False, max_paths: int = 0, stream=None, host_out=None) -> PathSet:
+                    digest: bool = False, max_paths: int = 0, stream=None, host_out=None,
+                    start_range: Optional[Tuple[int, int]] = None) -> PathSet:
         lib = library()
         alloc = _TorchAllocator(self.device) if output == "device" else None
         o = _options(self.device, output, mode, shard, digest, max_paths, 0, _stream_handle(self.device, stream),
-                     alloc, host_out)
+                     alloc, host_out, start_range)
         paths, stats = _abi.Paths(), _abi.Stats()
         _check(lib.tpgen_plan_prime_paths(self._h, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
         return _wrap(paths, stats, alloc, host_out)

@@ -31,6 +31,7 @@ class Paths(Structure):
 class Options(Structure):
     _fields_ = [("device", c_int32), ("stream", c_void_p), ("output_on_device", c_int32),
                 ("output_mode", c_int32), ("shard_rank", c_int32), ("shard_count", c_int32),
+                ("start_lo", c_int32), ("start_hi", c_int32),
                 ("max_paths", c_int64), ("max_extensions", c_int64), ("tp_mode", c_int32),
                 ("compute_digest", c_int32), ("device_alloc", ALLOC_FN), ("device_free", FREE_FN),
                 ("alloc_ctx", c_void_p), ("host_out", c_void_p), ("host_out_bytes", c_size_t)]

@@ -394,6 +394,10 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaStream_t s = (cudaStream_t)o.stream;
     int32_t lo = 0, hi = H.n;
     shard_range(H, o.shard_rank, o.shard_count, lo, hi);
+    if (o.start_hi > o.start_lo) {
+        lo = std::max(0, o.start_lo);
+        hi = std::min(H.n, o.start_hi);
+    }
     st.shard_lo = lo;
     st.shard_hi = hi;
     st.n_scc = H.n_scc;
@@ -453,13 +457,13 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         std::vector<uint64_t> tail_len(aggh.begin() + H.n, aggh.begin() + 2 * H.n);
         std::vector<uint64_t> pair_cnt(aggh.begin() + 2 * H.n, aggh.begin() + 2 * H.n + H.n_pairs);
         std::vector<uint64_t> pair_len(aggh.begin() + 2 * H.n + H.n_pairs, aggh.begin() + 2 * H.n + 2 * H.n_pairs);
-        std::vector<uint64_t> W, V;
-        if (!completion_dp(H, tail_cnt, tail_len, pair_cnt, pair_len, W, V)) {
+        std::vector<uint64_t> Wd, Vd;
+        if (!completion_dp(H, tail_cnt, tail_len, pair_cnt, pair_len, Wd, Vd)) {
             set_error("cross-SCC prime-path count exceeds 2^62");
             return TPGEN_ERR_LIMIT_EXCEEDED;
         }
-        TPG_CK(cudaMemcpyAsync(P.d_Wc.p, W.data(), H.n * 8, cudaMemcpyHostToDevice, s));
-        TPG_CK(cudaMemcpyAsync(P.d_Wv.p, V.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemcpyAsync(P.d_Wc.p, Wd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemcpyAsync(P.d_Wv.p, Vd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     }
     // ---- prime-path phase
     TPG_TRY(count_phase<W>(P, G, 0, s, st, launches, ms_count_kernel));
