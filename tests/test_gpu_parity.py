@@ -90,7 +90,7 @@ def test_cycle_64_and_limit():
     st = _assert_same(gen.single_loop(64))
     assert st["n_paths"] == 64
     with pytest.raises(tp.TpgenError) as ei:
-        tp.prime_paths(gen.single_loop(65))
+        tp.prime_paths(gen.single_loop(257))
     assert ei.value.status_name == "TPGEN_ERR_UNSUPPORTED"
 
 
