@@ -80,7 +80,7 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &stop, &work,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &stop, &work,
                                &rbuf, &scan_b, &scan_tot, &ctr, &agg, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs};
     for (int i = 0; i < 2; i++) {
@@ -107,6 +107,12 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     }
     TPG_TRY(upload(P.d_slots, packed, s));
     TPG_TRY(upload(P.d_slot_gid, H.slot_gid, s));
+    std::vector<int32_t> gbase(std::max(H.n_scc, 1), -1);
+    for (int32_t c = 0; c < H.n_scc; c++) {
+        const int32_t vb = H.scc_vbase[c], L = H.scc_size[c];
+        if (L > 0 && H.slot_gid[vb + L - 1] - H.slot_gid[vb] == L - 1) gbase[c] = H.slot_gid[vb];
+    }
+    TPG_TRY(upload(P.d_scc_gbase, gbase, s));
     TPG_TRY(upload(P.d_out_gid, H.out_gid, s));
     TPG_TRY(upload(P.d_out_pos, H.out_pos, s));
     TPG_TRY(upload(P.d_scc_vbase, H.scc_vbase, s));
@@ -135,6 +141,7 @@ static DevGraph dev_graph(PlanImpl &P, int32_t lo, int32_t hi) {
     G.slot_eidx = P.d_slot_eidx.as<int32_t>();
     G.Wc = P.d_Wc.as<uint64_t>();
     G.Wv = P.d_Wv.as<uint64_t>();
+    G.scc_gbase = P.d_scc_gbase.as<int32_t>();
     G.shard_lo = lo;
     G.shard_hi = hi;
     return G;

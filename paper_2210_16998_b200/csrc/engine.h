@@ -32,7 +32,7 @@ struct PlanImpl {
     double ms_plan = 0;
     // device tables
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
-        d_slot_eidx, d_Wc, d_Wv;
+        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase;
     // workspace (double-buffered unit arrays for refinement)
     DevBuf units[2], status[2], ext[2], cnt[2][kCnt];
     DevBuf stop, work, rbuf, scan_b, scan_tot, ctr, agg, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend,

@@ -124,6 +124,7 @@ struct DevGraph {
     const int32_t *slot_eidx;
     const uint64_t *Wc;  // completions per entry vertex (global id)
     const uint64_t *Wv;  // total vertices of those completions
+    const int32_t *scc_gbase;  // global id of local 0 when an SCC's ids are contiguous, else -1
     int32_t shard_lo, shard_hi;
 };
 
@@ -162,19 +163,18 @@ struct DfsCfg {
 };
 constexpr unsigned kFull = 0xffffffffu;
 
-enum LanePhase : int { PH_IDLE = 0, PH_ROOT = 1, PH_RUN = 2, PH_DONE = 3, PH_EXHAUSTED = 4 };
-
 template <int W>
 struct Lane {
-    Mask<W> M, sbit, ps;
-    int32_t vb, sgid, s, u, l, r, k, o, kind, e, phase;
+    Mask<W> M, sbit, ps, sin;  // visited set, bit of s, pred(s) in SCC, succ(u) in SCC
+    int32_t vb, gadd, sgid, s, u, l, r, k, o, ooff, ocnt, flags;
     uint32_t steps, limit;
-    bool seg, emit;
+    bool active, done, seg, emit;
 };
 
-struct Event {
-    int type, len, clo, e;
-};
+// Event codes: type in bits 0-2, closure flag bit 3, path length in bits 8+.
+constexpr int EV_CLO = 8;
+__device__ __forceinline__ int ev_type(int ev) { return ev & 7; }
+__device__ __forceinline__ int ev_len(int ev) { return ev >> 8; }
 
 template <int W>
 __device__ __forceinline__ const Slot<W> *slot_ptr(const DevGraph &G, int i) {
@@ -183,8 +183,16 @@ __device__ __forceinline__ const Slot<W> *slot_ptr(const DevGraph &G, int i) {
 template <int W>
 __device__ __forceinline__ Mask<W> ld_sin(const Slot<W> *p) {
     Mask<W> m;
+    if (W == 1) {
+        m.w[0] = __ldg(&p->sin[0]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < W; i++) m.w[i] = __ldg(&p->sin[i]);
+        for (int i = 0; i < W; i += 2) {
+            const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(&p->sin[i]));
+            m.w[i] = v.x;
+            m.w[i + 1] = v.y;
+        }
+    }
     return m;
 }
 template <int W>
@@ -199,34 +207,31 @@ __device__ __forceinline__ int4 ld_meta(const Slot<W> *p) {
     return __ldg(reinterpret_cast<const int4 *>(&p->gid));
 }
 
-// Own event of the node whose last vertex is w (called on creation).
+// Own event of a node whose last vertex is w (evaluated when the node is created).
 //  PP mode (s not an SCC entry): internal acyclic prime path iff
-//    succ(w) within {v2..vk} and pred(s) within {v1..v(k-1)}    (Def. 1 / Def. 9)
-//  segment mode (s an SCC entry): tail segment iff succ(w) within the path  (R8)
+//    succ(w) within {v2..vk} and pred(s) within {v1..v(k-1)}    (Def. 1 / Def. 9, P:127-130, P:173-176)
+//  segment mode (s an SCC entry): tail segment iff succ(w) within the path  (DESIGN.md R8)
 template <int W>
-__device__ __forceinline__ void node_event(const DevGraph &G, const Lane<W> &L, int w, Event &ev) {
-    const Slot<W> *sp = slot_ptr<W>(G, L.vb + w);
-    const int flags = __ldg(&sp->flags);
-    if (flags & F_EXIT) return;
-    const Mask<W> sw = ld_sin(sp);
-    if (L.seg) {
-        if (msubset(sw, L.M)) ev = Event{EV_TAIL, L.l + 1, 0, -1};
-    } else if (L.emit) {
-        Mask<W> inner_t = L.M, inner_h = L.M;
+__device__ __forceinline__ int node_event(const Lane<W> &L, int w) {
+    if (L.flags & F_EXIT) return 0;
+    const int len = (L.l + 1) << 8;
+    if (L.seg) return msubset(L.sin, L.M) ? (EV_TAIL | len) : 0;
+    if (!L.emit) return 0;
+    Mask<W> inner_t = L.M, inner_h = L.M;
 #pragma unroll
-        for (int i = 0; i < W; i++) inner_t.w[i] &= ~L.sbit.w[i];
-        mclr(inner_h, w);
-        if (msubset(sw, inner_t) && msubset(L.ps, inner_h)) ev = Event{EV_PP, L.l + 1, 0, -1};
-    }
+    for (int i = 0; i < W; i++) inner_t.w[i] &= ~L.sbit.w[i];
+    mclr(inner_h, w);
+    return (msubset(L.sin, inner_t) && msubset(L.ps, inner_h)) ? (EV_PP | len) : 0;
 }
 
-// Arc to an out-of-SCC successor (out-arc e) from the current node.
-//  segment mode: transit segment item (Def. 6, all entry->exit paths, R9)
+// Arc to an out-of-SCC successor from the current node.
+//  segment mode: transit segment item (Def. 6 -- all entry->exit paths, R9)
 //  PP mode: a head segment iff pred(s) lies on the path (R8) -> cross block
 template <int W>
-__device__ __forceinline__ void out_event(const Lane<W> &L, int e, Event &ev) {
-    if (L.seg) ev = Event{EV_TRANSIT, L.l + 1, 0, e};
-    else if (msubset(L.ps, L.M)) ev = Event{EV_HEAD, L.l + 1, 0, e};
+__device__ __forceinline__ int out_event(const Lane<W> &L) {
+    const int len = (L.l + 1) << 8;
+    if (L.seg) return EV_TRANSIT | len;
+    return msubset(L.ps, L.M) ? (EV_HEAD | len) : 0;
 }
 
 __device__ __forceinline__ int count_out_le(const DevGraph &G, int out_off, int out_cnt, int w) {
@@ -235,77 +240,62 @@ __device__ __forceinline__ int count_out_le(const DevGraph &G, int out_off, int 
     return o;
 }
 
-// One step of the depth-first walk.  Children of a node are visited in
-// ascending global id: in-SCC successors (local bits, ascending local id ==
-// ascending global id), the closing arc back to s, and out-of-SCC successors
-// (merged by their rank out_pos among the SCC members).
 template <int W>
-__device__ __forceinline__ void dfs_step(const DevGraph &G, Lane<W> &L, uint8_t *mypath, Event &ev, uint64_t &ext) {
-    if (L.phase == PH_ROOT) {
-        switch (L.kind) {
-            case K_NODE:
-                L.phase = PH_RUN;
-                if (L.l > 0 && L.emit) ext++;
-                node_event(G, L, L.u, ev);
-                return;
-            case K_SELF:
-                L.phase = PH_DONE;
-                node_event(G, L, L.u, ev);
-                return;
-            case K_CLOSURE:
-                L.phase = PH_DONE;
-                if (L.emit) {
-                    ext++;
-                    ev = Event{EV_PP, L.l + 2, 1, -1};
-                }
-                return;
-            default:
-                L.phase = PH_DONE;
-                out_event(L, L.e, ev);
-                return;
-        }
-    }
-    const Slot<W> *su = slot_ptr<W>(G, L.vb + L.u);
-    const int4 meta = ld_meta(su);  // gid, out_off, out_cnt, flags
-    const int w = mnext(ld_sin(su), L.M, L.sbit, L.k);
-    if (L.o < meta.z) {
-        const int e = meta.y + L.o;
+__device__ __forceinline__ void load_slot(const DevGraph &G, Lane<W> &L, int u) {
+    const Slot<W> *sp = slot_ptr<W>(G, L.vb + u);
+    L.sin = ld_sin(sp);
+    const int4 m = ld_meta(sp);
+    L.ooff = m.y;
+    L.ocnt = m.z;
+    L.flags = m.w;
+}
+
+// One step of the depth-first walk (branch-light: push, closure and pop share
+// one predicated update).  Children of a node are visited in ascending global
+// id: in-SCC successors (local bits; ascending local id == ascending global
+// id), the closing arc back to s, and out-of-SCC successors (merged by their
+// rank out_pos among the SCC members).  Returns the event of this step.
+template <int W>
+__device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<W> &L, uint8_t *mypath, int &e_out, uint64_t &ext) {
+    const int w = mnext(L.sin, L.M, L.sbit, L.k);
+    if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
+        const int e = L.ooff + L.o;
         if (__ldg(G.out_pos + e) <= w) {
             L.o++;
-            out_event(L, e, ev);
-            return;
+            e_out = e;
+            return out_event(L);
         }
     }
-    if (w < 64 * W) {
-        L.k = w + 1;
-        if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
-            if (L.emit) {
-                ext++;
-                ev = Event{EV_PP, L.l + 2, 1, -1};
-            }
-            return;
+    const bool has = w < 64 * W;
+    if (!has && L.l == L.r) {
+        L.done = true;
+        return 0;
+    }
+    const bool clo = has && (w == L.s);
+    const bool push = has && !clo;
+    const int wold = L.u;
+    const int parent = mypath[(L.l > 0 ? L.l - 1 : 0) * 32];
+    if (push) mypath[(L.l + 1) * 32] = (uint8_t)w;
+    if (push) mset(L.M, w);
+    if (!has) mclr(L.M, wold);
+    L.k = push ? 0 : (has ? w + 1 : wold + 1);
+    L.l += push ? 1 : (has ? 0 : -1);
+    if (clo) {  // cycle closure: always prime (Alg. 4 l.4-6)
+        if (L.emit) {
+            ext++;
+            return EV_PP | EV_CLO | ((L.l + 2) << 8);
         }
-        L.l++;
-        mypath[L.l * 32] = (uint8_t)w;
-        mset(L.M, w);
-        L.u = w;
-        L.k = 0;
+        return 0;
+    }
+    L.u = push ? w : parent;
+    load_slot(G, L, L.u);
+    if (push) {
         L.o = 0;
         if (L.emit) ext++;
-        node_event(G, L, w, ev);
-        return;
+        return node_event(L, w);
     }
-    if (L.l == L.r) {
-        L.phase = PH_DONE;
-        return;
-    }
-    const int wold = L.u;
-    mclr(L.M, wold);
-    L.l--;
-    L.u = mypath[L.l * 32];
-    L.k = wold + 1;
-    const int4 pm = ld_meta(slot_ptr<W>(G, L.vb + L.u));
-    L.o = count_out_le(G, pm.y, pm.z, wold);
+    L.o = count_out_le(G, L.ooff, L.ocnt, wold);
+    return 0;
 }
 
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b, unsigned int *ovf) {
@@ -336,7 +326,9 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
     const int64_t nwork = (PASS == PASS_COUNT) ? (int64_t)*A.n_work : A.n_units;
 
     Lane<W> L;
-    L.phase = PH_IDLE;
+    L.active = false;
+    L.done = false;
+    bool exhausted = false;
     int64_t uidx = -1;
     int32_t uscc = 0;
     uint64_t c[C_NUM];
@@ -347,25 +339,27 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
     for (int i = 0; i < C_NUM; i++) c[i] = 0;
 
     while (true) {
-        const unsigned idle = __ballot_sync(kFull, L.phase == PH_IDLE);
+        int ev = 0, e = -1;
+        // ---------------- refill idle lanes (warp-aggregated grab)
+        const unsigned idle = __ballot_sync(kFull, !L.active && !exhausted);
         if (idle) {
             const int leader = __ffs(idle) - 1;
             unsigned long long base = 0;
             if (lane == leader) base = atomicAdd(A.next, (unsigned long long)__popc(idle));
             base = __shfl_sync(kFull, base, leader);
-            if (L.phase == PH_IDLE) {
+            if (!L.active && !exhausted) {
                 const int64_t my = (int64_t)base + __popc(idle & ((1u << lane) - 1));
-                if (my < nwork) {
+                if (my >= nwork) {
+                    exhausted = true;
+                } else {
                     uidx = (PASS == PASS_COUNT) ? A.work[my] : my;
                     const Unit<W> *U = units + uidx;
+                    const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
 #pragma unroll
                     for (int i = 0; i < W; i++) L.M.w[i] = U->M[i];
-                    const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
                     uscc = h.x;
-                    L.e = h.y;
-                    const uint32_t nsteps = (uint32_t)h.z;
+                    const int kind = (h.w >> 8) & 0xff;
                     const int depth = h.w & 0xff;
-                    L.kind = (h.w >> 8) & 0xff;
                     L.l = L.r = depth;
                     const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
                     int s = 0, u = 0;
@@ -388,6 +382,7 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
                     L.u = u;
                     L.sbit = mbit<W>(s);
                     L.vb = __ldg(G.scc_vbase + uscc);
+                    L.gadd = __ldg(G.scc_gbase + uscc);
                     s_slot = L.vb + s;
                     const Slot<W> *ss = slot_ptr<W>(G, s_slot);
                     L.ps = ld_pin(ss);
@@ -398,7 +393,8 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
                     L.k = 0;
                     L.o = 0;
                     L.steps = 0;
-                    L.phase = PH_ROOT;
+                    L.done = false;
+                    L.active = true;
                     if (PASS == PASS_COUNT) {
                         L.limit = A.budget;
 #pragma unroll
@@ -410,125 +406,152 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
                                        (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
                         }
                     } else {
+                        const uint32_t nsteps = (uint32_t)h.z;
                         L.limit = nsteps ? nsteps : 0xffffffffu;
 #pragma unroll
                         for (int i = 0; i < C_NUM; i++) c[i] = A.off[i][uidx];
                     }
-                } else {
-                    L.phase = PH_EXHAUSTED;
+                    // the unit's root event (no step is counted for it)
+                    if (kind == K_NODE) {
+                        load_slot(G, L, u);
+                        if (depth > 0 && L.emit) ext++;
+                        ev = node_event(L, u);
+                    } else if (kind == K_CLOSURE) {
+                        L.done = true;
+                        if (L.emit) {
+                            ext++;
+                            ev = EV_PP | EV_CLO | ((depth + 2) << 8);
+                        }
+                    } else {  // K_OUT
+                        L.done = true;
+                        e = h.y;
+                        ev = out_event(L);
+                    }
                 }
             }
         }
-        const bool active = (L.phase == PH_ROOT || L.phase == PH_RUN);
-        if (__ballot_sync(kFull, active) == 0) break;
+        if (__ballot_sync(kFull, L.active) == 0) break;
 
-        Event ev;
-        ev.type = EV_NONE;
-        if (active) {
-            dfs_step<W>(G, L, mypath, ev, ext);
-            L.steps++;
+        // ---------------- steps until some lane has an event, finishes or hits its budget
+        if (__ballot_sync(kFull, ev != 0 || L.done) == 0) {
+            while (true) {
+                if (L.active) {
+                    ev = dfs_step<W>(G, L, mypath, e, ext);
+                    L.steps++;
+                }
+                if (__ballot_sync(kFull, ev != 0 || L.done || (L.active && L.steps >= L.limit))) break;
+            }
         }
 
+        // ---------------- events
         if (PASS == PASS_COUNT) {
-            if (ev.type == EV_PP) {
-                c[C_PP] += 1;
-                c[C_VERT] += (uint64_t)ev.len;
-            } else if (ev.type == EV_HEAD) {
-                const int32_t x = __ldg(G.out_gid + ev.e);
-                const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
-                c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul((uint64_t)ev.len, Wx, A.overflow), Vx, A.overflow),
-                                    A.overflow);
-                c[C_HEADS] += 1;
-                c[C_HEADV] += (uint64_t)ev.len;
-            } else if (ev.type == EV_TAIL) {
-                c[C_ITEMS] += 1;
-                c[C_ITEMV] += (uint64_t)ev.len;
-                atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
-                atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)ev.len);
-            } else if (ev.type == EV_TRANSIT) {
-                c[C_ITEMS] += 1;
-                c[C_ITEMV] += (uint64_t)ev.len;
-                atomicAdd(A.agg_pair_cnt + pair_row + ev.e, 1ull);
-                atomicAdd(A.agg_pair_len + pair_row + ev.e, (unsigned long long)ev.len);
+            if (ev) {
+                const int ty = ev_type(ev);
+                const uint64_t len = (uint64_t)ev_len(ev);
+                if (ty == EV_PP) {
+                    c[C_PP] += 1;
+                    c[C_VERT] += len;
+                } else if (ty == EV_HEAD) {
+                    const int32_t x = __ldg(G.out_gid + e);
+                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                    c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
+                    c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow),
+                                        A.overflow);
+                    c[C_HEADS] += 1;
+                    c[C_HEADV] += len;
+                } else if (ty == EV_TAIL) {
+                    c[C_ITEMS] += 1;
+                    c[C_ITEMV] += len;
+                    atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
+                    atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
+                } else {  // EV_TRANSIT
+                    c[C_ITEMS] += 1;
+                    c[C_ITEMV] += len;
+                    atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
+                    atomicAdd(A.agg_pair_len + pair_row + e, (unsigned long long)len);
+                }
             }
         } else {
-            // ---- warp-cooperative emission ----
             int32_t *dst = nullptr;
-            if (ev.type == EV_PP) {
-                dst = A.out_vert + c[C_VERT];
-                A.out_off[c[C_PP]] = (int64_t)c[C_VERT];
-                c[C_PP] += 1;
-                c[C_VERT] += (uint64_t)ev.len;
-            } else if (ev.type == EV_HEAD) {
-                const int32_t x = __ldg(G.out_gid + ev.e);
-                dst = A.head_pool + c[C_HEADV];
-                HeadRec h;
-                h.pp_off = c[C_PP];
-                h.v_off = c[C_VERT];
-                h.hv_off = c[C_HEADV];
-                h.len = ev.len;
-                h.x = x;
-                A.heads[c[C_HEADS]] = h;
-                const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                c[C_PP] += Wx;
-                c[C_VERT] += (uint64_t)ev.len * Wx + Vx;
-                c[C_HEADS] += 1;
-                c[C_HEADV] += (uint64_t)ev.len;
-            } else if (ev.type == EV_TAIL || ev.type == EV_TRANSIT) {
-                dst = A.item_pool + c[C_ITEMV];
-                ItemRec it;
-                it.pool_off = (int64_t)c[C_ITEMV];
-                it.len = ev.len;
-                it.y = (ev.type == EV_TRANSIT) ? __ldg(G.out_gid + ev.e) : -1;
-                it.ent = L.sgid;
-                it.pad = 0;
-                A.items[c[C_ITEMS]] = it;
-                c[C_ITEMS] += 1;
-                c[C_ITEMV] += (uint64_t)ev.len;
+            if (ev) {
+                const int ty = ev_type(ev);
+                const uint64_t len = (uint64_t)ev_len(ev);
+                if (ty == EV_PP) {
+                    dst = A.out_vert + c[C_VERT];
+                    A.out_off[c[C_PP]] = (int64_t)c[C_VERT];
+                    c[C_PP] += 1;
+                    c[C_VERT] += len;
+                } else if (ty == EV_HEAD) {
+                    const int32_t x = __ldg(G.out_gid + e);
+                    dst = A.head_pool + c[C_HEADV];
+                    HeadRec hr;
+                    hr.pp_off = c[C_PP];
+                    hr.v_off = c[C_VERT];
+                    hr.hv_off = c[C_HEADV];
+                    hr.len = (int32_t)len;
+                    hr.x = x;
+                    A.heads[c[C_HEADS]] = hr;
+                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                    c[C_PP] += Wx;
+                    c[C_VERT] += len * Wx + Vx;
+                    c[C_HEADS] += 1;
+                    c[C_HEADV] += len;
+                } else {  // EV_TAIL / EV_TRANSIT
+                    dst = A.item_pool + c[C_ITEMV];
+                    ItemRec it;
+                    it.pool_off = (int64_t)c[C_ITEMV];
+                    it.len = (int32_t)len;
+                    it.y = (ty == EV_TRANSIT) ? __ldg(G.out_gid + e) : -1;
+                    it.ent = L.sgid;
+                    it.pad = 0;
+                    A.items[c[C_ITEMS]] = it;
+                    c[C_ITEMS] += 1;
+                    c[C_ITEMV] += len;
+                }
             }
-            unsigned em = __ballot_sync(kFull, ev.type != EV_NONE);
+            // warp-cooperative copy: each emitting lane's path is written by the whole warp
+            unsigned em = __ballot_sync(kFull, ev != 0);
             while (em) {
                 const int src = __ffs(em) - 1;
                 em &= em - 1;
                 int32_t *d = reinterpret_cast<int32_t *>(__shfl_sync(kFull, (unsigned long long)dst, src));
-                const int len = __shfl_sync(kFull, ev.len, src);
-                const int clo = __shfl_sync(kFull, ev.clo, src);
+                const int evs = __shfl_sync(kFull, ev, src);
                 const int vb = __shfl_sync(kFull, L.vb, src);
+                const int ga = __shfl_sync(kFull, L.gadd, src);
                 const uint8_t *sp = wpath + src;
-                const int plen = len - clo;
+                const int len = ev_len(evs);
+                const int plen = len - ((evs & EV_CLO) ? 1 : 0);
                 for (int j = lane; j < len; j += 32) {
                     const int loc = sp[(j < plen ? j : 0) * 32];
-                    d[j] = __ldg(G.slot_gid + vb + loc);
+                    d[j] = (ga >= 0) ? ga + loc : __ldg(G.slot_gid + vb + loc);
                 }
             }
         }
 
-        if (active) {
-            if (L.phase == PH_DONE || L.steps >= L.limit) {
-                if (PASS == PASS_COUNT) {
-                    const bool trunc = (L.phase != PH_DONE);
+        // ---------------- unit completion / budget
+        if (L.active && (L.done || L.steps >= L.limit)) {
+            if (PASS == PASS_COUNT) {
+                const bool trunc = !L.done;
 #pragma unroll
-                    for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
-                    A.ext[uidx] = ext;
-                    A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
-                    if (trunc) {
-                        Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
+                for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
+                A.ext[uidx] = ext;
+                A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
+                if (trunc) {
+                    Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
 #pragma unroll
-                        for (int i = 0; i < W; i++) S->M[i] = L.M.w[i];
-                        int4 h;
-                        h.x = uscc;
-                        h.y = -1;
-                        h.z = (int)L.steps;
-                        h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
-                        *reinterpret_cast<int4 *>(&S->scc) = h;
-                        S->rdepth = (uint8_t)L.r;
-                        for (int j = 0; j <= L.l; j++) S->path[j] = mypath[j * 32];
-                        atomicAdd(A.n_trunc, 1ull);
-                    }
+                    for (int i = 0; i < W; i++) S->M[i] = L.M.w[i];
+                    int4 h;
+                    h.x = uscc;
+                    h.y = -1;
+                    h.z = (int)L.steps;
+                    h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
+                    *reinterpret_cast<int4 *>(&S->scc) = h;
+                    S->rdepth = (uint8_t)L.r;
+                    for (int j = 0; j <= L.l; j++) S->path[j] = mypath[j * 32];
+                    atomicAdd(A.n_trunc, 1ull);
                 }
-                L.phase = PH_IDLE;
             }
+            L.active = false;
         }
     }
 }
