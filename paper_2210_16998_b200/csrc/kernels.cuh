@@ -433,13 +433,13 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
         if (__ballot_sync(kFull, L.active) == 0) break;
 
         // ---------------- steps until some lane has an event, finishes or hits its budget
-        if (__ballot_sync(kFull, ev != 0 || L.done) == 0) {
+        if (__ballot_sync(kFull, ev != 0 || (L.active && L.done)) == 0) {
             while (true) {
                 if (L.active) {
                     ev = dfs_step<W>(G, L, mypath, e, ext);
                     L.steps++;
                 }
-                if (__ballot_sync(kFull, ev != 0 || L.done || (L.active && L.steps >= L.limit))) break;
+                if (__ballot_sync(kFull, L.active && (ev != 0 || L.done || L.steps >= L.limit))) break;
             }
         }
 
@@ -552,6 +552,7 @@ __global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs
                 }
             }
             L.active = false;
+            L.done = false;
         }
     }
 }
