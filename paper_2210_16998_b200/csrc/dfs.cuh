@@ -1,0 +1,474 @@
+// dfs.cuh -- the DFS enumerator kernel (K1 count / K1 write) of libtpgen.
+//
+// Hot path: per start vertex s, depth-first
+// enumeration of the simple paths inside SCC(s) (tail extension along CSR
+// arcs, a visited bit mask per path, cycle closure back to s -- PAPER.md
+// Alg. 4 "ExtendPath" P:459-472, Ammann-Offutt generation P:865), fused with
+// the maximality / segment classification (Def. 1, Defs. 6-9
+// P:158-176 under DESIGN.md readings R8/R9) and the canonical writer.
+//
+// One lane owns one work unit (a subtree of the per-start trie, or a terminal
+// event) and walks it depth-first.  Its path lives in shared memory, laid out
+// [level/4][lane][level%4] so that the 32 lanes of a warp touching their own
+// path never conflict on a bank; its visited set lives in a register (32-bit
+// when the largest SCC has <= 32 vertices).  Lanes refill from a global unit
+// counter (warp-aggregated atomic).  Emission is warp-cooperative: every
+// emitting lane publishes a descriptor in shared memory and the whole warp
+// writes that lane's path as one coalesced store stream.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace tpg {
+
+// ---------------------------------------------------------------- mask traits
+template <class T>
+struct MT;
+
+template <>
+struct MT<uint32_t> {
+    static constexpr int W = 1, BITS = 32;
+    static __device__ __forceinline__ uint32_t bit(int b) { return 1u << b; }
+    static __device__ __forceinline__ void set(uint32_t &m, int b) { m |= 1u << b; }
+    static __device__ __forceinline__ void clr(uint32_t &m, int b) { m &= ~(1u << b); }
+    static __device__ __forceinline__ bool subset(uint32_t a, uint32_t b) { return (a & ~b) == 0u; }
+    static __device__ __forceinline__ uint32_t andnot(uint32_t a, uint32_t b) { return a & ~b; }
+    // lowest set bit >= k of (sin & (~M | sbit)), BITS if none
+    static __device__ __forceinline__ int next(uint32_t sin, uint32_t M, uint32_t sbit, int k) {
+        uint32_t c = sin & (~M | sbit);
+        c = (k < 32) ? (c & (0xffffffffu << k)) : 0u;
+        return c ? (__ffs((int)c) - 1) : 32;
+    }
+    static __device__ __forceinline__ uint32_t load(const uint64_t *w) { return (uint32_t)__ldg(w); }
+    static __device__ __forceinline__ uint32_t from(const uint64_t *w) { return (uint32_t)w[0]; }
+    static __device__ __forceinline__ void store(uint32_t m, uint64_t *w) { w[0] = m; }
+};
+
+template <>
+struct MT<uint64_t> {
+    static constexpr int W = 1, BITS = 64;
+    static __device__ __forceinline__ uint64_t bit(int b) { return 1ull << b; }
+    static __device__ __forceinline__ void set(uint64_t &m, int b) { m |= 1ull << b; }
+    static __device__ __forceinline__ void clr(uint64_t &m, int b) { m &= ~(1ull << b); }
+    static __device__ __forceinline__ bool subset(uint64_t a, uint64_t b) { return (a & ~b) == 0ull; }
+    static __device__ __forceinline__ uint64_t andnot(uint64_t a, uint64_t b) { return a & ~b; }
+    static __device__ __forceinline__ int next(uint64_t sin, uint64_t M, uint64_t sbit, int k) {
+        uint64_t c = sin & (~M | sbit);
+        c = (k < 64) ? (c & (~0ull << k)) : 0ull;
+        return c ? (__ffsll((long long)c) - 1) : 64;
+    }
+    static __device__ __forceinline__ uint64_t load(const uint64_t *w) { return __ldg(w); }
+    static __device__ __forceinline__ uint64_t from(const uint64_t *w) { return w[0]; }
+    static __device__ __forceinline__ void store(uint64_t m, uint64_t *w) { w[0] = m; }
+};
+
+template <int WW>
+struct MT<Mask<WW>> {
+    using T = Mask<WW>;
+    static constexpr int W = WW, BITS = 64 * WW;
+    static __device__ __forceinline__ T bit(int b) { return mbit<WW>(b); }
+    static __device__ __forceinline__ void set(T &m, int b) { mset(m, b); }
+    static __device__ __forceinline__ void clr(T &m, int b) { mclr(m, b); }
+    static __device__ __forceinline__ bool subset(const T &a, const T &b) { return msubset(a, b); }
+    static __device__ __forceinline__ T andnot(const T &a, const T &b) {
+        T r;
+#pragma unroll
+        for (int i = 0; i < WW; i++) r.w[i] = a.w[i] & ~b.w[i];
+        return r;
+    }
+    static __device__ __forceinline__ int next(const T &sin, const T &M, const T &sbit, int k) {
+        return mnext(sin, M, sbit, k);
+    }
+    static __device__ __forceinline__ T load(const uint64_t *w) {
+        T m;
+#pragma unroll
+        for (int i = 0; i < WW; i++) m.w[i] = __ldg(w + i);
+        return m;
+    }
+    static __device__ __forceinline__ T from(const uint64_t *w) {
+        T m;
+#pragma unroll
+        for (int i = 0; i < WW; i++) m.w[i] = w[i];
+        return m;
+    }
+    static __device__ __forceinline__ void store(const T &m, uint64_t *w) {
+#pragma unroll
+        for (int i = 0; i < WW; i++) w[i] = m.w[i];
+    }
+};
+
+// Event codes: type in bits 0-2, closure flag bit 3, path length in bits 8+.
+constexpr int EV_CLO = 8;
+__device__ __forceinline__ int ev_type(int ev) { return ev & 7; }
+__device__ __forceinline__ int ev_len(int ev) { return ev >> 8; }
+
+// shared-memory path layout: byte of level l of lane q at ((l>>2)*32 + q)*4 + (l&3)
+__device__ __forceinline__ int pidx(int l) { return ((l >> 2) << 7) | (l & 3); }
+
+template <class T>
+struct Lane {
+    T M, sbit, ps, sin;  // visited set, bit of s, pred(s) in SCC, succ(u) in SCC
+    int32_t vb, sgid, s, u, l, r, k, o, ooff, ocnt, flags;
+    uint32_t steps, limit;
+    bool active, done, seg, emit;
+};
+
+template <class T>
+__device__ __forceinline__ void load_slot(const DevGraph &G, Lane<T> &L, int u) {
+    constexpr int W = MT<T>::W;
+    const Slot<W> *sp = slot_ptr<W>(G, L.vb + u);
+    L.sin = MT<T>::load(sp->sin);
+    const int4 m = ld_meta(sp);
+    L.ooff = m.y;
+    L.ocnt = m.z;
+    L.flags = m.w;
+}
+
+// Own event of a node whose last vertex is w (evaluated when the node is created).
+//  PP mode (s not an SCC entry): internal acyclic prime path iff
+//    succ(w) within {v2..vk} and pred(s) within {v1..v(k-1)}   (Def. 1 / Def. 9)
+//  segment mode (s an SCC entry): tail segment iff succ(w) within the path  (R8)
+template <class T>
+__device__ __forceinline__ int node_event(const Lane<T> &L, int w) {
+    using O = MT<T>;
+    if (L.flags & F_EXIT) return 0;
+    const int len = (L.l + 1) << 8;
+    if (L.seg) return O::subset(L.sin, L.M) ? (EV_TAIL | len) : 0;
+    if (!L.emit) return 0;
+    T inner_h = L.M;
+    O::clr(inner_h, w);
+    return (O::subset(L.sin, O::andnot(L.M, L.sbit)) && O::subset(L.ps, inner_h)) ? (EV_PP | len) : 0;
+}
+
+// Arc to an out-of-SCC successor from the current node.
+//  segment mode: transit segment item (Def. 6 -- all entry->exit paths, R9)
+//  PP mode: a head segment iff pred(s) lies on the path (R8) -> cross block
+template <class T>
+__device__ __forceinline__ int out_event(const Lane<T> &L) {
+    const int len = (L.l + 1) << 8;
+    if (L.seg) return EV_TRANSIT | len;
+    return MT<T>::subset(L.ps, L.M) ? (EV_HEAD | len) : 0;
+}
+
+// One step of the depth-first walk.  Children of a node are visited in
+// ascending global id: in-SCC successors (local bits; ascending local id ==
+// ascending global id), the closing arc back to s, and out-of-SCC successors
+// (merged by their rank out_pos among the SCC members).  Returns the event.
+template <class T>
+__device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint8_t *mypath, int &e_out, uint64_t &ext) {
+    using O = MT<T>;
+    const int w = O::next(L.sin, L.M, L.sbit, L.k);
+    if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
+        const int e = L.ooff + L.o;
+        if (__ldg(G.out_pos + e) <= w) {
+            L.o++;
+            e_out = e;
+            return out_event(L);
+        }
+    }
+    if (w < O::BITS) {
+        L.k = w + 1;
+        if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
+            if (L.emit) {
+                ext++;
+                return EV_PP | EV_CLO | ((L.l + 2) << 8);
+            }
+            return 0;
+        }
+        L.l++;  // push
+        mypath[pidx(L.l)] = (uint8_t)w;
+        O::set(L.M, w);
+        L.u = w;
+        L.k = 0;
+        L.o = 0;
+        load_slot(G, L, w);
+        if (L.emit) ext++;
+        return node_event(L, w);
+    }
+    if (L.l == L.r) {
+        L.done = true;
+        return 0;
+    }
+    const int wold = L.u;  // pop
+    O::clr(L.M, wold);
+    L.l--;
+    L.u = mypath[pidx(L.l)];
+    L.k = wold + 1;
+    load_slot(G, L, L.u);
+    L.o = (L.ocnt > 0) ? count_out_le(G, L.ooff, L.ocnt, wold) : 0;
+    return 0;
+}
+
+template <class T>
+struct DfsTraits {
+    static constexpr int W = MT<T>::W;
+    static constexpr int threads = DfsCfg<W>::threads;
+    static constexpr int warps = DfsCfg<W>::warps;
+    static constexpr int min_blocks = DfsCfg<W>::min_blocks;
+};
+
+template <class T, int PASS>
+__global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
+    using O = MT<T>;
+    constexpr int W = O::W;
+    constexpr int WARPS = DfsTraits<T>::warps;
+    __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32];
+    __shared__ int4 sdesc[(PASS == PASS_WRITE) ? WARPS * 32 : 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint8_t *wpath = spath + wid * 64 * W * 32;
+    uint8_t *mypath = wpath + lane * 4;
+    int4 *wdesc = sdesc + ((PASS == PASS_WRITE) ? wid * 32 : 0);
+    const DevGraph &G = A.G;
+    const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
+    const int64_t nwork = (PASS == PASS_COUNT) ? (int64_t)*A.n_work : A.n_units;
+
+    Lane<T> L;
+    L.active = false;
+    L.done = false;
+    bool exhausted = false;
+    int64_t uidx = -1;
+    int32_t uscc = 0, tr = 0;
+    uint64_t c[C_NUM];
+    uint64_t ext = 0;
+    int64_t pair_row = 0;
+    int32_t s_slot = 0;
+#pragma unroll
+    for (int i = 0; i < C_NUM; i++) c[i] = 0;
+    unsigned long long d_outer = 0, d_inner = 0, d_steps = 0, d_emit = 0;
+    const long long t_start = clock64();
+
+    while (true) {
+        int ev = 0, e = -1;
+        d_outer++;
+        // ---------------- refill idle lanes (warp-aggregated grab)
+        const unsigned idle = __ballot_sync(kFull, !L.active && !exhausted);
+        if (idle) {
+            const int leader = __ffs(idle) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(A.next, (unsigned long long)__popc(idle));
+            base = __shfl_sync(kFull, base, leader);
+            if (!L.active && !exhausted) {
+                const int64_t my = (int64_t)base + __popc(idle & ((1u << lane) - 1));
+                if (my >= nwork) {
+                    exhausted = true;
+                } else {
+                    uidx = (PASS == PASS_COUNT) ? A.work[my] : my;
+                    const Unit<W> *U = units + uidx;
+                    const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
+                    L.M = O::from(U->M);
+                    uscc = h.x;
+                    const int kind = (h.w >> 8) & 0xff;
+                    const int depth = h.w & 0xff;
+                    L.l = L.r = depth;
+                    const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
+#pragma unroll 1
+                    for (int q = 0; q * 16 <= depth; q++) {
+                        const uint4 v = p4[q];
+                        // 4 levels per word: one 32-bit smem store per 4 levels
+                        uint32_t *wp = reinterpret_cast<uint32_t *>(mypath + pidx(q * 16));
+                        wp[0] = v.x;
+                        if (q * 16 + 4 <= depth) wp[32] = v.y;
+                        if (q * 16 + 8 <= depth) wp[64] = v.z;
+                        if (q * 16 + 12 <= depth) wp[96] = v.w;
+                    }
+                    const int s = mypath[0];
+                    const int u = mypath[pidx(depth)];
+                    L.s = s;
+                    L.u = u;
+                    L.sbit = O::bit(s);
+                    L.vb = __ldg(G.scc_vbase + uscc);
+                    const int ga = __ldg(G.scc_gbase + uscc);
+                    tr = (ga >= 0) ? ga : -(L.vb + 1);
+                    s_slot = L.vb + s;
+                    const Slot<W> *ss = slot_ptr<W>(G, s_slot);
+                    L.ps = O::load(ss->pin);
+                    const int4 sm = ld_meta(ss);
+                    L.seg = (sm.w & F_ENTRY) != 0;
+                    L.sgid = sm.x;
+                    L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
+                    L.k = 0;
+                    L.o = 0;
+                    L.steps = 0;
+                    L.done = false;
+                    L.active = true;
+                    if (PASS == PASS_COUNT) {
+                        L.limit = A.budget;
+#pragma unroll
+                        for (int i = 0; i < C_NUM; i++) c[i] = 0;
+                        ext = 0;
+                        if (L.seg) {
+                            const int32_t nout = __ldg(G.scc_nout + uscc);
+                            pair_row = __ldg(G.scc_pair_base + uscc) +
+                                       (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
+                        }
+                    } else {
+                        const uint32_t nsteps = (uint32_t)h.z;
+                        L.limit = nsteps ? nsteps : 0xffffffffu;
+#pragma unroll
+                        for (int i = 0; i < C_NUM; i++) c[i] = A.off[i][uidx];
+                    }
+                    // the unit's root event (no step is counted for it)
+                    if (kind == K_NODE) {
+                        load_slot(G, L, u);
+                        if (depth > 0 && L.emit) ext++;
+                        ev = node_event(L, u);
+                    } else if (kind == K_CLOSURE) {
+                        L.done = true;
+                        if (L.emit) {
+                            ext++;
+                            ev = EV_PP | EV_CLO | ((depth + 2) << 8);
+                        }
+                    } else {  // K_OUT
+                        L.done = true;
+                        e = h.y;
+                        ev = out_event(L);
+                    }
+                }
+            }
+        }
+        if (__ballot_sync(kFull, L.active) == 0) break;
+
+        // ---------------- steps until some lane has an event, finishes or hits its budget
+        if (__ballot_sync(kFull, ev != 0 || (L.active && L.done)) == 0) {
+            while (true) {
+                if (A.dbg) {
+                    d_inner++;
+                    d_steps += __popc(__ballot_sync(kFull, L.active));
+                }
+                if (L.active) {
+                    ev = dfs_step<T>(G, L, mypath, e, ext);
+                    L.steps++;
+                }
+                if (__ballot_sync(kFull, L.active && (ev != 0 || L.done || L.steps >= L.limit))) break;
+            }
+        }
+
+        // ---------------- events
+        if (PASS == PASS_COUNT) {
+            if (ev) {
+                const int ty = ev_type(ev);
+                const uint64_t len = (uint64_t)ev_len(ev);
+                if (ty == EV_PP) {
+                    c[C_PP] += 1;
+                    c[C_VERT] += len;
+                } else if (ty == EV_HEAD) {
+                    const int32_t x = __ldg(G.out_gid + e);
+                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                    c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
+                    c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow),
+                                        A.overflow);
+                    c[C_HEADS] += 1;
+                    c[C_HEADV] += len;
+                } else if (ty == EV_TAIL) {
+                    c[C_ITEMS] += 1;
+                    c[C_ITEMV] += len;
+                    atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
+                    atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
+                } else {  // EV_TRANSIT
+                    c[C_ITEMS] += 1;
+                    c[C_ITEMV] += len;
+                    atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
+                    atomicAdd(A.agg_pair_len + pair_row + e, (unsigned long long)len);
+                }
+            }
+        } else {
+            const unsigned em = __ballot_sync(kFull, ev != 0);
+            if (em) {
+                if (ev) {
+                    const int ty = ev_type(ev);
+                    const uint64_t len = (uint64_t)ev_len(ev);
+                    int32_t *dst;
+                    if (ty == EV_PP) {
+                        dst = A.out_vert + c[C_VERT];
+                        A.out_off[c[C_PP]] = (int64_t)c[C_VERT];
+                        c[C_PP] += 1;
+                        c[C_VERT] += len;
+                    } else if (ty == EV_HEAD) {
+                        const int32_t x = __ldg(G.out_gid + e);
+                        dst = A.head_pool + c[C_HEADV];
+                        HeadRec hr;
+                        hr.pp_off = c[C_PP];
+                        hr.v_off = c[C_VERT];
+                        hr.hv_off = c[C_HEADV];
+                        hr.len = (int32_t)len;
+                        hr.x = x;
+                        A.heads[c[C_HEADS]] = hr;
+                        const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                        c[C_PP] += Wx;
+                        c[C_VERT] += len * Wx + Vx;
+                        c[C_HEADS] += 1;
+                        c[C_HEADV] += len;
+                    } else {  // EV_TAIL / EV_TRANSIT
+                        dst = A.item_pool + c[C_ITEMV];
+                        ItemRec it;
+                        it.pool_off = (int64_t)c[C_ITEMV];
+                        it.len = (int32_t)len;
+                        it.y = (ty == EV_TRANSIT) ? __ldg(G.out_gid + e) : -1;
+                        it.ent = L.sgid;
+                        it.pad = 0;
+                        A.items[c[C_ITEMS]] = it;
+                        c[C_ITEMS] += 1;
+                        c[C_ITEMV] += len;
+                    }
+                    const unsigned long long p = reinterpret_cast<unsigned long long>(dst);
+                    wdesc[lane] = make_int4((int)(uint32_t)p, (int)(uint32_t)(p >> 32), ev, tr);
+                }
+                if (A.dbg) d_emit += __popc(em);
+                __syncwarp();
+                // warp-cooperative copy: each emitting lane's path is written by the whole warp
+                unsigned m = em;
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int4 d = wdesc[src];
+                    int32_t *dd = reinterpret_cast<int32_t *>(((unsigned long long)(uint32_t)d.y << 32) |
+                                                              (unsigned long long)(uint32_t)d.x);
+                    const int len = ev_len(d.z);
+                    const int plen = len - ((d.z & EV_CLO) ? 1 : 0);
+                    const uint8_t *sp = wpath + src * 4;
+                    for (int j = lane; j < len; j += 32) {
+                        const int loc = sp[pidx(j < plen ? j : 0)];
+                        dd[j] = (d.w >= 0) ? d.w + loc : __ldg(G.slot_gid + (-d.w - 1) + loc);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+
+        // ---------------- unit completion / budget
+        if (L.active && (L.done || L.steps >= L.limit)) {
+            if (PASS == PASS_COUNT) {
+                const bool trunc = !L.done;
+#pragma unroll
+                for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
+                A.ext[uidx] = ext;
+                A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
+                if (trunc) {
+                    Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
+                    O::store(L.M, S->M);
+                    int4 h;
+                    h.x = uscc;
+                    h.y = -1;
+                    h.z = (int)L.steps;
+                    h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
+                    *reinterpret_cast<int4 *>(&S->scc) = h;
+                    S->rdepth = (uint8_t)L.r;
+                    for (int j = 0; j <= L.l; j++) S->path[j] = mypath[pidx(j)];
+                    atomicAdd(A.n_trunc, 1ull);
+                }
+            }
+            L.active = false;
+            L.done = false;
+        }
+    }
+    if (A.dbg && lane == 0) {
+        atomicAdd(A.dbg + 0, d_outer);
+        atomicAdd(A.dbg + 1, d_inner);
+        atomicAdd(A.dbg + 2, d_steps);
+        atomicAdd(A.dbg + 3, d_emit);
+        atomicAdd(A.dbg + 4, (unsigned long long)(clock64() - t_start));
+        atomicMax(A.dbg + 5, (unsigned long long)(clock64() - t_start));
+    }
+}
+
+}  // namespace tpg

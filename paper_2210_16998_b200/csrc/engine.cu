@@ -10,6 +10,7 @@
 //   segment-table scans + stitch_kernel (cross-SCC prime paths)
 //   optional digest, optional D2H
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include <mutex>
 
 #include "aux_kernels.cuh"
+#include "dfs.cuh"
 #include "engine.h"
 
 namespace tpg {
@@ -298,9 +300,10 @@ static uint32_t choose_budget(int64_t nwork, int64_t lanes) {
     return std::max<uint32_t>(32, std::min(big, b));
 }
 
-template <int W>
+template <class T>
 static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStream_t s, tpgen_stats &st,
                                 int64_t &launches, double &ms_count_kernel) {
+    constexpr int W = MT<T>::W;
     Timer t;
     const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
     for (int round = 0; round < 4096; round++) {
@@ -341,7 +344,7 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 3);
         const int grid = grid_for(nwork, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks);
         cudaEventRecord(t.a, s);
-        dfs_kernel<W, PASS_COUNT><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
+        dfs_kernel<T, PASS_COUNT><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
         cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
@@ -390,8 +393,9 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
     return TPGEN_ERR_INTERNAL;
 }
 
-template <int W>
+template <class T>
 static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
+    constexpr int W = MT<T>::W;
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
@@ -444,7 +448,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     TPG_TRY(P.ext[0].ensure(nr * 8, s));
     for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[0][c].ensure(nr * 8, s));
     TPG_TRY(P.stop.ensure(nr * sizeof(Unit<W>), s));
-    TPG_TRY(P.ctr.ensure(8 * 8, s));
+    TPG_TRY(P.ctr.ensure(16 * 8, s));
     if (!roots.empty()) {
         TPG_CK(cudaMemcpyAsync(P.units[0].p, roots.data(), roots.size() * sizeof(Unit<W>), cudaMemcpyHostToDevice, s));
         TPG_CK(cudaMemsetAsync(P.status[0].p, ST_PENDING, roots.size(), s));
@@ -456,7 +460,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     double ms_count_kernel = 0;
     // ---- segment phase (SCC entries) -> completion DP
     if (H.has_entries) {
-        TPG_TRY(count_phase<W>(P, G, 1, s, st, launches, ms_count_kernel));
+        TPG_TRY(count_phase<T>(P, G, 1, s, st, launches, ms_count_kernel));
         std::vector<uint64_t> aggh(agg_n);
         TPG_CK(cudaMemcpyAsync(aggh.data(), P.agg.p, agg_n * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
@@ -473,7 +477,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         TPG_CK(cudaMemcpyAsync(P.d_Wv.p, Vd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     }
     // ---- prime-path phase
-    TPG_TRY(count_phase<W>(P, G, 0, s, st, launches, ms_count_kernel));
+    TPG_TRY(count_phase<T>(P, G, 0, s, st, launches, ms_count_kernel));
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
@@ -548,14 +552,26 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     A.head_pool = P.head_pool.as<int32_t>();
     A.items = P.items.as<ItemRec>();
     A.item_pool = P.item_pool.as<int32_t>();
+    const bool dbg = getenv("TPGEN_DEBUG") != nullptr;
+    if (dbg) {
+        A.dbg = ctr + 8;
+        TPG_CK(cudaMemsetAsync(A.dbg, 0, 8 * 8, s));
+    }
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        dfs_kernel<W, PASS_WRITE><<<grid_for(nu, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks), DfsCfg<W>::threads,
+        dfs_kernel<T, PASS_WRITE><<<grid_for(nu, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks), DfsCfg<W>::threads,
                                    0, s>>>(A);
         launches++;
     }
     cudaEventRecord(tw.b, s);
     TPG_CK(cudaGetLastError());
+    if (dbg) {
+        unsigned long long h[8];
+        TPG_CK(cudaMemcpyAsync(h, A.dbg, 64, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "[tpgen dbg write] outer=%llu inner=%llu lane_steps=%llu emits=%llu warp_cycles_sum=%llu max=%llu\n",
+                h[0], h[1], h[2], h[3], h[4], h[5]);
+    }
 
     // ---- cross-SCC stitching
     cudaEventRecord(tst.a, s);
@@ -642,10 +658,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
 }
 
 tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st) {
+    if (P.hp.max_scc <= 32) return run_pp<uint32_t>(P, o, out, st);
     switch (P.hp.W) {
-        case 1: return run_pp<1>(P, o, out, st);
-        case 2: return run_pp<2>(P, o, out, st);
-        case 4: return run_pp<4>(P, o, out, st);
+        case 1: return run_pp<uint64_t>(P, o, out, st);
+        case 2: return run_pp<Mask<2>>(P, o, out, st);
+        case 4: return run_pp<Mask<4>>(P, o, out, st);
     }
     set_error("bad mask width");
     return TPGEN_ERR_INTERNAL;

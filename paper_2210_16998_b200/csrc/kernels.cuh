@@ -152,6 +152,7 @@ struct DfsArgs {
     int32_t *head_pool;
     ItemRec *items;
     int32_t *item_pool;
+    unsigned long long *dbg;  // optional counters: outer iters, inner iters, lane-steps, emissions, warp cycles
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
@@ -162,19 +163,6 @@ struct DfsCfg {
     static constexpr int min_blocks = (W == 1) ? 4 : ((W == 2) ? 2 : 3);
 };
 constexpr unsigned kFull = 0xffffffffu;
-
-template <int W>
-struct Lane {
-    Mask<W> M, sbit, ps, sin;  // visited set, bit of s, pred(s) in SCC, succ(u) in SCC
-    int32_t vb, gadd, sgid, s, u, l, r, k, o, ooff, ocnt, flags;
-    uint32_t steps, limit;
-    bool active, done, seg, emit;
-};
-
-// Event codes: type in bits 0-2, closure flag bit 3, path length in bits 8+.
-constexpr int EV_CLO = 8;
-__device__ __forceinline__ int ev_type(int ev) { return ev & 7; }
-__device__ __forceinline__ int ev_len(int ev) { return ev >> 8; }
 
 template <int W>
 __device__ __forceinline__ const Slot<W> *slot_ptr(const DevGraph &G, int i) {
@@ -207,95 +195,10 @@ __device__ __forceinline__ int4 ld_meta(const Slot<W> *p) {
     return __ldg(reinterpret_cast<const int4 *>(&p->gid));
 }
 
-// Own event of a node whose last vertex is w (evaluated when the node is created).
-//  PP mode (s not an SCC entry): internal acyclic prime path iff
-//    succ(w) within {v2..vk} and pred(s) within {v1..v(k-1)}    (Def. 1 / Def. 9)
-//  segment mode (s an SCC entry): tail segment iff succ(w) within the path  (R8)
-template <int W>
-__device__ __forceinline__ int node_event(const Lane<W> &L, int w) {
-    if (L.flags & F_EXIT) return 0;
-    const int len = (L.l + 1) << 8;
-    if (L.seg) return msubset(L.sin, L.M) ? (EV_TAIL | len) : 0;
-    if (!L.emit) return 0;
-    Mask<W> inner_t = L.M, inner_h = L.M;
-#pragma unroll
-    for (int i = 0; i < W; i++) inner_t.w[i] &= ~L.sbit.w[i];
-    mclr(inner_h, w);
-    return (msubset(L.sin, inner_t) && msubset(L.ps, inner_h)) ? (EV_PP | len) : 0;
-}
-
-// Arc to an out-of-SCC successor from the current node.
-//  segment mode: transit segment item (Def. 6 -- all entry->exit paths, R9)
-//  PP mode: a head segment iff pred(s) lies on the path (R8) -> cross block
-template <int W>
-__device__ __forceinline__ int out_event(const Lane<W> &L) {
-    const int len = (L.l + 1) << 8;
-    if (L.seg) return EV_TRANSIT | len;
-    return msubset(L.ps, L.M) ? (EV_HEAD | len) : 0;
-}
-
 __device__ __forceinline__ int count_out_le(const DevGraph &G, int out_off, int out_cnt, int w) {
     int o = 0;
     while (o < out_cnt && __ldg(G.out_pos + out_off + o) <= w) o++;
     return o;
-}
-
-template <int W>
-__device__ __forceinline__ void load_slot(const DevGraph &G, Lane<W> &L, int u) {
-    const Slot<W> *sp = slot_ptr<W>(G, L.vb + u);
-    L.sin = ld_sin(sp);
-    const int4 m = ld_meta(sp);
-    L.ooff = m.y;
-    L.ocnt = m.z;
-    L.flags = m.w;
-}
-
-// One step of the depth-first walk (branch-light: push, closure and pop share
-// one predicated update).  Children of a node are visited in ascending global
-// id: in-SCC successors (local bits; ascending local id == ascending global
-// id), the closing arc back to s, and out-of-SCC successors (merged by their
-// rank out_pos among the SCC members).  Returns the event of this step.
-template <int W>
-__device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<W> &L, uint8_t *mypath, int &e_out, uint64_t &ext) {
-    const int w = mnext(L.sin, L.M, L.sbit, L.k);
-    if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
-        const int e = L.ooff + L.o;
-        if (__ldg(G.out_pos + e) <= w) {
-            L.o++;
-            e_out = e;
-            return out_event(L);
-        }
-    }
-    const bool has = w < 64 * W;
-    if (!has && L.l == L.r) {
-        L.done = true;
-        return 0;
-    }
-    const bool clo = has && (w == L.s);
-    const bool push = has && !clo;
-    const int wold = L.u;
-    const int parent = mypath[(L.l > 0 ? L.l - 1 : 0) * 32];
-    if (push) mypath[(L.l + 1) * 32] = (uint8_t)w;
-    if (push) mset(L.M, w);
-    if (!has) mclr(L.M, wold);
-    L.k = push ? 0 : (has ? w + 1 : wold + 1);
-    L.l += push ? 1 : (has ? 0 : -1);
-    if (clo) {  // cycle closure: always prime (Alg. 4 l.4-6)
-        if (L.emit) {
-            ext++;
-            return EV_PP | EV_CLO | ((L.l + 2) << 8);
-        }
-        return 0;
-    }
-    L.u = push ? w : parent;
-    load_slot(G, L, L.u);
-    if (push) {
-        L.o = 0;
-        if (L.emit) ext++;
-        return node_event(L, w);
-    }
-    L.o = count_out_le(G, L.ooff, L.ocnt, wold);
-    return 0;
 }
 
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b, unsigned int *ovf) {
@@ -313,248 +216,6 @@ __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b, unsigned int
         return (1ull << 62);
     }
     return lo;
-}
-
-template <int W, int PASS>
-__global__ void __launch_bounds__(DfsCfg<W>::threads, DfsCfg<W>::min_blocks) dfs_kernel(DfsArgs A) {
-    __shared__ uint8_t spath[DfsCfg<W>::warps * 64 * W * 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t *wpath = spath + wid * 64 * W * 32;  // [level][lane]
-    uint8_t *mypath = wpath + lane;
-    const DevGraph &G = A.G;
-    const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
-    const int64_t nwork = (PASS == PASS_COUNT) ? (int64_t)*A.n_work : A.n_units;
-
-    Lane<W> L;
-    L.active = false;
-    L.done = false;
-    bool exhausted = false;
-    int64_t uidx = -1;
-    int32_t uscc = 0;
-    uint64_t c[C_NUM];
-    uint64_t ext = 0;
-    int64_t pair_row = 0;
-    int32_t s_slot = 0;
-#pragma unroll
-    for (int i = 0; i < C_NUM; i++) c[i] = 0;
-
-    while (true) {
-        int ev = 0, e = -1;
-        // ---------------- refill idle lanes (warp-aggregated grab)
-        const unsigned idle = __ballot_sync(kFull, !L.active && !exhausted);
-        if (idle) {
-            const int leader = __ffs(idle) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(A.next, (unsigned long long)__popc(idle));
-            base = __shfl_sync(kFull, base, leader);
-            if (!L.active && !exhausted) {
-                const int64_t my = (int64_t)base + __popc(idle & ((1u << lane) - 1));
-                if (my >= nwork) {
-                    exhausted = true;
-                } else {
-                    uidx = (PASS == PASS_COUNT) ? A.work[my] : my;
-                    const Unit<W> *U = units + uidx;
-                    const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
-#pragma unroll
-                    for (int i = 0; i < W; i++) L.M.w[i] = U->M[i];
-                    uscc = h.x;
-                    const int kind = (h.w >> 8) & 0xff;
-                    const int depth = h.w & 0xff;
-                    L.l = L.r = depth;
-                    const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
-                    int s = 0, u = 0;
-#pragma unroll 1
-                    for (int q = 0; q * 16 <= depth; q++) {
-                        const uint4 v = p4[q];
-                        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                        for (int b = 0; b < 16; b++) {
-                            const int j = q * 16 + b;
-                            if (j <= depth) {
-                                const uint8_t byte = (uint8_t)(wv[b >> 2] >> ((b & 3) * 8));
-                                mypath[j * 32] = byte;
-                                if (j == 0) s = byte;
-                                if (j == depth) u = byte;
-                            }
-                        }
-                    }
-                    L.s = s;
-                    L.u = u;
-                    L.sbit = mbit<W>(s);
-                    L.vb = __ldg(G.scc_vbase + uscc);
-                    L.gadd = __ldg(G.scc_gbase + uscc);
-                    s_slot = L.vb + s;
-                    const Slot<W> *ss = slot_ptr<W>(G, s_slot);
-                    L.ps = ld_pin(ss);
-                    const int4 sm = ld_meta(ss);
-                    L.seg = (sm.w & F_ENTRY) != 0;
-                    L.sgid = sm.x;
-                    L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
-                    L.k = 0;
-                    L.o = 0;
-                    L.steps = 0;
-                    L.done = false;
-                    L.active = true;
-                    if (PASS == PASS_COUNT) {
-                        L.limit = A.budget;
-#pragma unroll
-                        for (int i = 0; i < C_NUM; i++) c[i] = 0;
-                        ext = 0;
-                        if (L.seg) {
-                            const int32_t nout = __ldg(G.scc_nout + uscc);
-                            pair_row = __ldg(G.scc_pair_base + uscc) +
-                                       (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
-                        }
-                    } else {
-                        const uint32_t nsteps = (uint32_t)h.z;
-                        L.limit = nsteps ? nsteps : 0xffffffffu;
-#pragma unroll
-                        for (int i = 0; i < C_NUM; i++) c[i] = A.off[i][uidx];
-                    }
-                    // the unit's root event (no step is counted for it)
-                    if (kind == K_NODE) {
-                        load_slot(G, L, u);
-                        if (depth > 0 && L.emit) ext++;
-                        ev = node_event(L, u);
-                    } else if (kind == K_CLOSURE) {
-                        L.done = true;
-                        if (L.emit) {
-                            ext++;
-                            ev = EV_PP | EV_CLO | ((depth + 2) << 8);
-                        }
-                    } else {  // K_OUT
-                        L.done = true;
-                        e = h.y;
-                        ev = out_event(L);
-                    }
-                }
-            }
-        }
-        if (__ballot_sync(kFull, L.active) == 0) break;
-
-        // ---------------- steps until some lane has an event, finishes or hits its budget
-        if (__ballot_sync(kFull, ev != 0 || (L.active && L.done)) == 0) {
-            while (true) {
-                if (L.active) {
-                    ev = dfs_step<W>(G, L, mypath, e, ext);
-                    L.steps++;
-                }
-                if (__ballot_sync(kFull, L.active && (ev != 0 || L.done || L.steps >= L.limit))) break;
-            }
-        }
-
-        // ---------------- events
-        if (PASS == PASS_COUNT) {
-            if (ev) {
-                const int ty = ev_type(ev);
-                const uint64_t len = (uint64_t)ev_len(ev);
-                if (ty == EV_PP) {
-                    c[C_PP] += 1;
-                    c[C_VERT] += len;
-                } else if (ty == EV_HEAD) {
-                    const int32_t x = __ldg(G.out_gid + e);
-                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                    c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
-                    c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow),
-                                        A.overflow);
-                    c[C_HEADS] += 1;
-                    c[C_HEADV] += len;
-                } else if (ty == EV_TAIL) {
-                    c[C_ITEMS] += 1;
-                    c[C_ITEMV] += len;
-                    atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
-                    atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
-                } else {  // EV_TRANSIT
-                    c[C_ITEMS] += 1;
-                    c[C_ITEMV] += len;
-                    atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
-                    atomicAdd(A.agg_pair_len + pair_row + e, (unsigned long long)len);
-                }
-            }
-        } else {
-            int32_t *dst = nullptr;
-            if (ev) {
-                const int ty = ev_type(ev);
-                const uint64_t len = (uint64_t)ev_len(ev);
-                if (ty == EV_PP) {
-                    dst = A.out_vert + c[C_VERT];
-                    A.out_off[c[C_PP]] = (int64_t)c[C_VERT];
-                    c[C_PP] += 1;
-                    c[C_VERT] += len;
-                } else if (ty == EV_HEAD) {
-                    const int32_t x = __ldg(G.out_gid + e);
-                    dst = A.head_pool + c[C_HEADV];
-                    HeadRec hr;
-                    hr.pp_off = c[C_PP];
-                    hr.v_off = c[C_VERT];
-                    hr.hv_off = c[C_HEADV];
-                    hr.len = (int32_t)len;
-                    hr.x = x;
-                    A.heads[c[C_HEADS]] = hr;
-                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                    c[C_PP] += Wx;
-                    c[C_VERT] += len * Wx + Vx;
-                    c[C_HEADS] += 1;
-                    c[C_HEADV] += len;
-                } else {  // EV_TAIL / EV_TRANSIT
-                    dst = A.item_pool + c[C_ITEMV];
-                    ItemRec it;
-                    it.pool_off = (int64_t)c[C_ITEMV];
-                    it.len = (int32_t)len;
-                    it.y = (ty == EV_TRANSIT) ? __ldg(G.out_gid + e) : -1;
-                    it.ent = L.sgid;
-                    it.pad = 0;
-                    A.items[c[C_ITEMS]] = it;
-                    c[C_ITEMS] += 1;
-                    c[C_ITEMV] += len;
-                }
-            }
-            // warp-cooperative copy: each emitting lane's path is written by the whole warp
-            unsigned em = __ballot_sync(kFull, ev != 0);
-            while (em) {
-                const int src = __ffs(em) - 1;
-                em &= em - 1;
-                int32_t *d = reinterpret_cast<int32_t *>(__shfl_sync(kFull, (unsigned long long)dst, src));
-                const int evs = __shfl_sync(kFull, ev, src);
-                const int vb = __shfl_sync(kFull, L.vb, src);
-                const int ga = __shfl_sync(kFull, L.gadd, src);
-                const uint8_t *sp = wpath + src;
-                const int len = ev_len(evs);
-                const int plen = len - ((evs & EV_CLO) ? 1 : 0);
-                for (int j = lane; j < len; j += 32) {
-                    const int loc = sp[(j < plen ? j : 0) * 32];
-                    d[j] = (ga >= 0) ? ga + loc : __ldg(G.slot_gid + vb + loc);
-                }
-            }
-        }
-
-        // ---------------- unit completion / budget
-        if (L.active && (L.done || L.steps >= L.limit)) {
-            if (PASS == PASS_COUNT) {
-                const bool trunc = !L.done;
-#pragma unroll
-                for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
-                A.ext[uidx] = ext;
-                A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
-                if (trunc) {
-                    Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
-#pragma unroll
-                    for (int i = 0; i < W; i++) S->M[i] = L.M.w[i];
-                    int4 h;
-                    h.x = uscc;
-                    h.y = -1;
-                    h.z = (int)L.steps;
-                    h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
-                    *reinterpret_cast<int4 *>(&S->scc) = h;
-                    S->rdepth = (uint8_t)L.r;
-                    for (int j = 0; j <= L.l; j++) S->path[j] = mypath[j * 32];
-                    atomicAdd(A.n_trunc, 1ull);
-                }
-            }
-            L.active = false;
-            L.done = false;
-        }
-    }
 }
 
 // ------------------------------------------------------------- refinement
