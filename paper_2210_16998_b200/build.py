@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+    dbg = ["-DTPGEN_KERNEL_DEBUG"] if os.environ.get("TPGEN_KERNEL_DEBUG") else []
+    cmd = [NVCC] + FLAGS + dbg + (["-Xptxas", "-v"] if verbose else []) + \
         [os.path.join(CSRC, f) for f in SOURCES] + ["-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -105,6 +105,11 @@ __device__ __forceinline__ int ev_len(int ev) { return ev >> 8; }
 // shared-memory path layout: byte of level l of lane q at ((l>>2)*32 + q)*4 + (l&3)
 __device__ __forceinline__ int pidx(int l) { return ((l >> 2) << 7) | (l & 3); }
 
+// output pointers travel through shared memory; keep the store in the global window
+__device__ __forceinline__ void st_global(int32_t *p, int v) {
+    asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <class T>
 struct Lane {
     T M, sbit, ps, sin;  // visited set, bit of s, pred(s) in SCC, succ(u) in SCC
@@ -166,37 +171,30 @@ __device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint8_t *
             return out_event(L);
         }
     }
-    if (w < O::BITS) {
-        L.k = w + 1;
-        if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
-            if (L.emit) {
-                ext++;
-                return EV_PP | EV_CLO | ((L.l + 2) << 8);
-            }
-            return 0;
-        }
-        L.l++;  // push
-        mypath[pidx(L.l)] = (uint8_t)w;
-        O::set(L.M, w);
-        L.u = w;
-        L.k = 0;
-        L.o = 0;
-        load_slot(G, L, w);
-        if (L.emit) ext++;
-        return node_event(L, w);
-    }
-    if (L.l == L.r) {
+    const bool has = w < O::BITS;
+    if (!has && L.l == L.r) {  // subtree of the unit's root exhausted
         L.done = true;
         return 0;
     }
-    const int wold = L.u;  // pop
-    O::clr(L.M, wold);
-    L.l--;
-    L.u = mypath[pidx(L.l)];
-    L.k = wold + 1;
+    // push / cycle closure / pop share one predicated update (no divergent paths)
+    const bool clo = has && (w == L.s);  // cycle closure: always prime (Alg. 4 l.4-6)
+    const bool push = has && !clo;
+    const bool pop = !has;
+    const int wold = L.u;
+    const int parent = mypath[pidx(L.l > 0 ? L.l - 1 : 0)];
+    if (push) mypath[pidx(L.l + 1)] = (uint8_t)w;
+    const T bw = O::bit(push ? w : wold);
+    if (push) L.M = L.M | bw;
+    if (pop) L.M = O::andnot(L.M, bw);
+    L.k = push ? 0 : (has ? w + 1 : wold + 1);
+    L.l += push ? 1 : (pop ? -1 : 0);
+    L.u = push ? w : (pop ? parent : wold);
     load_slot(G, L, L.u);
-    L.o = (L.ocnt > 0) ? count_out_le(G, L.ooff, L.ocnt, wold) : 0;
-    return 0;
+    if (pop && L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: exit vertices only
+    else if (push) L.o = 0;
+    if (L.emit && has) ext++;
+    if (clo) return L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
+    return push ? node_event(L, w) : 0;
 }
 
 template <class T>
@@ -218,6 +216,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     uint8_t *wpath = spath + wid * 64 * W * 32;
     uint8_t *mypath = wpath + lane * 4;
     int4 *wdesc = sdesc + ((PASS == PASS_WRITE) ? wid * 32 : 0);
+    const int plane = pidx(lane);
     const DevGraph &G = A.G;
     const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
     const int64_t nwork = (PASS == PASS_COUNT) ? (int64_t)*A.n_work : A.n_units;
@@ -234,12 +233,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     int32_t s_slot = 0;
 #pragma unroll
     for (int i = 0; i < C_NUM; i++) c[i] = 0;
+#ifdef TPGEN_KERNEL_DEBUG
     unsigned long long d_outer = 0, d_inner = 0, d_steps = 0, d_emit = 0;
     const long long t_start = clock64();
+#endif
 
     while (true) {
         int ev = 0, e = -1;
+        bool fresh = false;
+#ifdef TPGEN_KERNEL_DEBUG
         d_outer++;
+#endif
         // ---------------- refill idle lanes (warp-aggregated grab)
         const unsigned idle = __ballot_sync(kFull, !L.active && !exhausted);
         if (idle) {
@@ -291,6 +295,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     L.steps = 0;
                     L.done = false;
                     L.active = true;
+                    fresh = true;
                     if (PASS == PASS_COUNT) {
                         L.limit = A.budget;
 #pragma unroll
@@ -326,22 +331,19 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 }
             }
         }
-        if (__ballot_sync(kFull, L.active) == 0) break;
-
-        // ---------------- steps until some lane has an event, finishes or hits its budget
-        if (__ballot_sync(kFull, ev != 0 || (L.active && L.done)) == 0) {
-            while (true) {
-                if (A.dbg) {
-                    d_inner++;
-                    d_steps += __popc(__ballot_sync(kFull, L.active));
-                }
-                if (L.active) {
-                    ev = dfs_step<T>(G, L, mypath, e, ext);
-                    L.steps++;
-                }
-                if (__ballot_sync(kFull, L.active && (ev != 0 || L.done || L.steps >= L.limit))) break;
-            }
+        // ---------------- one step for every running lane (lanes that just loaded emit their root event)
+        const bool run = L.active && !L.done && !(fresh && ev != 0);
+        #ifdef TPGEN_KERNEL_DEBUG
+        if (A.dbg) {
+            d_inner++;
+            d_steps += __popc(__ballot_sync(kFull, run));
         }
+#endif
+        if (run) {
+            ev = dfs_step<T>(G, L, mypath, e, ext);
+            L.steps++;
+        }
+        if (__ballot_sync(kFull, L.active) == 0) break;
 
         // ---------------- events
         if (PASS == PASS_COUNT) {
@@ -413,7 +415,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     const unsigned long long p = reinterpret_cast<unsigned long long>(dst);
                     wdesc[lane] = make_int4((int)(uint32_t)p, (int)(uint32_t)(p >> 32), ev, tr);
                 }
+#ifdef TPGEN_KERNEL_DEBUG
                 if (A.dbg) d_emit += __popc(em);
+#endif
                 __syncwarp();
                 // warp-cooperative copy: each emitting lane's path is written by the whole warp
                 unsigned m = em;
@@ -426,9 +430,11 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     const int len = ev_len(d.z);
                     const int plen = len - ((d.z & EV_CLO) ? 1 : 0);
                     const uint8_t *sp = wpath + src * 4;
-                    for (int j = lane; j < len; j += 32) {
-                        const int loc = sp[pidx(j < plen ? j : 0)];
-                        dd[j] = (d.w >= 0) ? d.w + loc : __ldg(G.slot_gid + (-d.w - 1) + loc);
+                    // element j = lane + 32 r lives at pidx(lane) + 1024 r; the closing vertex is path[0]
+                    for (int j = lane, pj = plane; j < len; j += 32, pj += 1024) {
+                        const int loc = sp[j < plen ? pj : 0];
+                        const int g = (d.w >= 0) ? d.w + loc : __ldg(G.slot_gid + (-d.w - 1) + loc);
+                        st_global(dd + j, g);
                     }
                 }
                 __syncwarp();
@@ -461,6 +467,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             L.done = false;
         }
     }
+#ifdef TPGEN_KERNEL_DEBUG
     if (A.dbg && lane == 0) {
         atomicAdd(A.dbg + 0, d_outer);
         atomicAdd(A.dbg + 1, d_inner);
@@ -469,6 +476,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         atomicAdd(A.dbg + 4, (unsigned long long)(clock64() - t_start));
         atomicMax(A.dbg + 5, (unsigned long long)(clock64() - t_start));
     }
+#endif
 }
 
 }  // namespace tpg

@@ -72,6 +72,13 @@ __device__ __forceinline__ bool msubset(const Mask<W> &a, const Mask<W> &b) {
     for (int i = 0; i < W; i++) r |= a.w[i] & ~b.w[i];
     return r == 0;
 }
+template <int W>
+__device__ __forceinline__ Mask<W> operator|(const Mask<W> &a, const Mask<W> &b) {
+    Mask<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = a.w[i] | b.w[i];
+    return r;
+}
 // lowest set bit >= k of (sin & (~M | sbit)); 64*W if none
 template <int W>
 __device__ __forceinline__ int mnext(const Mask<W> &sin, const Mask<W> &M, const Mask<W> &sbit, int k) {
