@@ -109,6 +109,18 @@ __device__ __forceinline__ int pidx(int l) { return ((l >> 2) << 7) | (l & 3); }
 __device__ __forceinline__ void st_global(int32_t *p, int v) {
     asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// path bytes are addressed with 32-bit shared-window addresses (no generic->shared conversion per access)
+__device__ __forceinline__ int lds_u8(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, int v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 
 template <class T>
 struct Lane {
@@ -160,7 +172,7 @@ __device__ __forceinline__ int out_event(const Lane<T> &L) {
 // ascending global id), the closing arc back to s, and out-of-SCC successors
 // (merged by their rank out_pos among the SCC members).  Returns the event.
 template <class T>
-__device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint8_t *mypath, int &e_out, uint64_t &ext) {
+__device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint32_t mp, int &e_out, uint64_t &ext) {
     using O = MT<T>;
     const int w = O::next(L.sin, L.M, L.sbit, L.k);
     if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
@@ -181,8 +193,8 @@ __device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint8_t *
     const bool push = has && !clo;
     const bool pop = !has;
     const int wold = L.u;
-    const int parent = mypath[pidx(L.l > 0 ? L.l - 1 : 0)];
-    if (push) mypath[pidx(L.l + 1)] = (uint8_t)w;
+    const int parent = lds_u8(mp + pidx(L.l > 0 ? L.l - 1 : 0));
+    if (push) sts_u8(mp + pidx(L.l + 1), w);
     const T bw = O::bit(push ? w : wold);
     if (push) L.M = L.M | bw;
     if (pop) L.M = O::andnot(L.M, bw);
@@ -213,8 +225,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32];
     __shared__ int4 sdesc[(PASS == PASS_WRITE) ? WARPS * 32 : 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t *wpath = spath + wid * 64 * W * 32;
-    uint8_t *mypath = wpath + lane * 4;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32);
+    const uint32_t mp = wbase + lane * 4;
     int4 *wdesc = sdesc + ((PASS == PASS_WRITE) ? wid * 32 : 0);
     const int plane = pidx(lane);
     const DevGraph &G = A.G;
@@ -269,14 +281,14 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     for (int q = 0; q * 16 <= depth; q++) {
                         const uint4 v = p4[q];
                         // 4 levels per word: one 32-bit smem store per 4 levels
-                        uint32_t *wp = reinterpret_cast<uint32_t *>(mypath + pidx(q * 16));
-                        wp[0] = v.x;
-                        if (q * 16 + 4 <= depth) wp[32] = v.y;
-                        if (q * 16 + 8 <= depth) wp[64] = v.z;
-                        if (q * 16 + 12 <= depth) wp[96] = v.w;
+                        const uint32_t wa = mp + pidx(q * 16);
+                        sts_u32(wa, v.x);
+                        if (q * 16 + 4 <= depth) sts_u32(wa + 128, v.y);
+                        if (q * 16 + 8 <= depth) sts_u32(wa + 256, v.z);
+                        if (q * 16 + 12 <= depth) sts_u32(wa + 384, v.w);
                     }
-                    const int s = mypath[0];
-                    const int u = mypath[pidx(depth)];
+                    const int s = lds_u8(mp);
+                    const int u = lds_u8(mp + pidx(depth));
                     L.s = s;
                     L.u = u;
                     L.sbit = O::bit(s);
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         }
 #endif
         if (run) {
-            ev = dfs_step<T>(G, L, mypath, e, ext);
+            ev = dfs_step<T>(G, L, mp, e, ext);
             L.steps++;
         }
         if (__ballot_sync(kFull, L.active) == 0) break;
@@ -429,12 +441,15 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                                                               (unsigned long long)(uint32_t)d.x);
                     const int len = ev_len(d.z);
                     const int plen = len - ((d.z & EV_CLO) ? 1 : 0);
-                    const uint8_t *sp = wpath + src * 4;
+                    const uint32_t sp = wbase + src * 4;
                     // element j = lane + 32 r lives at pidx(lane) + 1024 r; the closing vertex is path[0]
-                    for (int j = lane, pj = plane; j < len; j += 32, pj += 1024) {
-                        const int loc = sp[j < plen ? pj : 0];
-                        const int g = (d.w >= 0) ? d.w + loc : __ldg(G.slot_gid + (-d.w - 1) + loc);
-                        st_global(dd + j, g);
+                    if (d.w >= 0) {  // SCC with contiguous global ids: gid = base + local
+                        for (int j = lane, pj = plane; j < len; j += 32, pj += 1024)
+                            st_global(dd + j, d.w + lds_u8(sp + (j < plen ? pj : 0)));
+                    } else {
+                        const int32_t *gt = G.slot_gid + (-d.w - 1);
+                        for (int j = lane, pj = plane; j < len; j += 32, pj += 1024)
+                            st_global(dd + j, __ldg(gt + lds_u8(sp + (j < plen ? pj : 0))));
                     }
                 }
                 __syncwarp();
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
                     *reinterpret_cast<int4 *>(&S->scc) = h;
                     S->rdepth = (uint8_t)L.r;
-                    for (int j = 0; j <= L.l; j++) S->path[j] = mypath[pidx(j)];
+                    for (int j = 0; j <= L.l; j++) S->path[j] = (uint8_t)lds_u8(mp + pidx(j));
                     atomicAdd(A.n_trunc, 1ull);
                 }
             }
