@@ -130,10 +130,12 @@ struct RefineBufs {
     const Unit<W> *stop;
     const uint64_t *cnt[C_NUM];
     const uint64_t *ext;
+    const int64_t *rfirst, *rcount;
     Unit<W> *nunits;
     uint8_t *nstatus;
     uint64_t *ncnt[C_NUM];
     uint64_t *next;
+    int64_t *nrfirst, *nrcount;
 };
 
 template <int W>
@@ -148,6 +150,8 @@ __global__ void refine_scatter_kernel(DevGraph G, RefineBufs<W> B, int64_t n, co
 #pragma unroll
         for (int c = 0; c < C_NUM; c++) B.ncnt[c][p] = B.cnt[c][i];
         B.next[p] = B.ext[i];
+        B.nrfirst[p] = B.rfirst[i];
+        B.nrcount[p] = B.rcount[i];
         if (st == ST_TRUNC) {
             const Unit<W> S = B.stop[i];
             const int m = remainder_events<W, true>(G, S, B.nunits + p + 1);
@@ -156,9 +160,18 @@ __global__ void refine_scatter_kernel(DevGraph G, RefineBufs<W> B, int64_t n, co
 #pragma unroll
                 for (int c = 0; c < C_NUM; c++) B.ncnt[c][p + q] = 0;
                 B.next[p + q] = 0;
+                B.nrfirst[p + q] = -1;
+                B.nrcount[p + q] = 0;
             }
         }
     }
+}
+
+// Undo a DFS round whose record pool overflowed: its units become pending again.
+__global__ void reset_status_kernel(const int64_t *work, const unsigned long long *nwork, uint8_t *status) {
+    const int64_t n = (int64_t)*nwork;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        status[work[i]] = ST_PENDING;
 }
 
 // --------------------------------------------------- segment tables (a5)

@@ -1,20 +1,27 @@
-// dfs.cuh -- the DFS enumerator kernel (K1 count / K1 write) of libtpgen.
+// dfs.cuh -- the DFS enumerator kernel (K1) of libtpgen.
 //
-// Hot path (SURVEY.md §8(a) a2/a3/a4): per start vertex s, depth-first
+// Hot path (SURVEY.md §8(a) a2/a3): per start vertex s, depth-first
 // enumeration of the simple paths inside SCC(s) (tail extension along CSR
 // arcs, a visited bit mask per path, cycle closure back to s -- PAPER.md
 // Alg. 4 "ExtendPath" P:459-472, Ammann-Offutt generation P:865), fused with
 // the maximality / segment classification (Def. 1, Defs. 6-9
-// P:158-176 under DESIGN.md readings R8/R9) and the canonical writer.
+// P:158-176 under DESIGN.md readings R8/R9).
 //
 // One lane owns one work unit (a subtree of the per-start trie, or a terminal
 // event) and walks it depth-first.  Its path lives in shared memory, laid out
 // [level/4][lane][level%4] so that the 32 lanes of a warp touching their own
 // path never conflict on a bank; its visited set lives in a register (32-bit
 // when the largest SCC has <= 32 vertices).  Lanes refill from a global unit
-// counter (warp-aggregated atomic).  Emission is warp-cooperative: every
-// emitting lane publishes a descriptor in shared memory and the whole warp
-// writes that lane's path as one coalesced store stream.
+// counter (warp-aggregated atomic).
+//
+// Output is a per-unit stream of 64-bit *path-delta records* (lane-local
+// stores, no warp cooperation): "truncate the path to c vertices, append n
+// bytes, then emit" -- consecutive prime paths of a DFS share long prefixes,
+// so a record carries only the few vertices pushed since the previous one.
+// Records live in 512-byte chunks linked through their last word, allocated
+// from a pool by atomic bump.  The expand kernel (expand.cuh) replays the
+// streams into the canonical offsets/vertices arrays at exact offsets obtained
+// from the per-unit counters this kernel also produces.
 #pragma once
 
 #include "kernels.cuh"
@@ -97,7 +104,17 @@ struct MT<Mask<WW>> {
     }
 };
 
-// Event codes: type in bits 0-2, closure flag bit 3, path length in bits 8+.
+// ---------------------------------------------------------------- records
+// 64-bit path-delta record:
+//   bits 0-2 type, bit 3 closure flag, bits 4-11 c (truncate the path to c
+//   vertices), bits 12-14 n (number of appended vertices, <= 5),
+//   bits 16-55 the n appended local vertex ids (one byte each).
+// R_ARG carries the out-arc index of the preceding HEAD / TRANSIT in bits 32-63.
+enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAIL, R_TRANSIT = EV_TRANSIT, R_ARG = 6 };
+constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
+constexpr int kRecBytes = 5;    // appended vertices carried by one record
+
+// Event codes inside the DFS: type in bits 0-2, closure flag bit 3, path length in bits 8+.
 constexpr int EV_CLO = 8;
 __device__ __forceinline__ int ev_type(int ev) { return ev & 7; }
 __device__ __forceinline__ int ev_len(int ev) { return ev >> 8; }
@@ -105,11 +122,7 @@ __device__ __forceinline__ int ev_len(int ev) { return ev >> 8; }
 // shared-memory path layout: byte of level l of lane q at ((l>>2)*32 + q)*4 + (l&3)
 __device__ __forceinline__ int pidx(int l) { return ((l >> 2) << 7) | (l & 3); }
 
-// output pointers travel through shared memory; keep the store in the global window
-__device__ __forceinline__ void st_global(int32_t *p, int v) {
-    asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// path bytes are addressed with 32-bit shared-window addresses (no generic->shared conversion per access)
+// path bytes are addressed with 32-bit shared-window addresses
 __device__ __forceinline__ int lds_u8(uint32_t a) {
     int v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -125,9 +138,12 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 template <class T>
 struct Lane {
     T M, sbit, ps, sin;  // visited set, bit of s, pred(s) in SCC, succ(u) in SCC
-    int32_t vb, sgid, s, u, l, r, k, o, ooff, ocnt, flags;
+    int32_t vb, s, u, l, r, k, o, ooff, ocnt, flags;
     uint32_t steps, limit;
     bool active, done, seg, emit;
+    // record stream state: the decoder knows path[0..base); pend holds path[base..l] (pn bytes)
+    int32_t base, pn;
+    uint64_t pend;
 };
 
 template <class T>
@@ -167,12 +183,36 @@ __device__ __forceinline__ int out_event(const Lane<T> &L) {
     return MT<T>::subset(L.ps, L.M) ? (EV_HEAD | len) : 0;
 }
 
+struct RecWriter {
+    uint64_t *cur;  // current chunk
+    int fill;       // records used in it
+    int64_t first;  // first chunk index of the unit
+    int64_t count;  // records of the unit
+};
+
+__device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t rec) {
+    if (R.fill == kChunkRecs - 1) {
+        const unsigned long long nc = atomicAdd(A.chunk_next, 1ull);
+        if (nc >= A.chunk_cap) {
+            atomicOr(A.overflow, 2u);
+            R.fill = 0;  // keep writing into the current chunk (result is discarded)
+        } else {
+            R.cur[kChunkRecs - 1] = nc;
+            R.cur = A.chunks + nc * kChunkRecs;
+            R.fill = 0;
+        }
+    }
+    R.cur[R.fill++] = rec;
+    R.count++;
+}
+
 // One step of the depth-first walk.  Children of a node are visited in
 // ascending global id: in-SCC successors (local bits; ascending local id ==
 // ascending global id), the closing arc back to s, and out-of-SCC successors
 // (merged by their rank out_pos among the SCC members).  Returns the event.
 template <class T>
-__device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint32_t mp, int &e_out, uint64_t &ext) {
+__device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, Lane<T> &L, RecWriter &R, uint32_t mp,
+                                        int &e_out, uint64_t &ext) {
     using O = MT<T>;
     const int w = O::next(L.sin, L.M, L.sbit, L.k);
     if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
@@ -204,6 +244,25 @@ __device__ __forceinline__ int dfs_step(const DevGraph &G, Lane<T> &L, uint32_t 
     load_slot(G, L, L.u);
     if (pop && L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: exit vertices only
     else if (push) L.o = 0;
+    // record-stream bookkeeping: pending bytes follow pushes and pops
+    if (push) {
+        if (L.pn == kRecBytes) {  // flush a continuation record
+            rec_put(A, R, (uint64_t)R_PATH | ((uint64_t)L.base << 4) | ((uint64_t)kRecBytes << 12) |
+                              (L.pend << 16));
+            L.base += kRecBytes;
+            L.pn = 0;
+            L.pend = 0;
+        }
+        L.pend |= (uint64_t)w << (8 * L.pn);
+        L.pn++;
+    } else if (pop) {
+        if (L.pn > 0) {
+            L.pn--;
+            L.pend &= ~(0xffull << (8 * L.pn));
+        } else {
+            L.base--;
+        }
+    }
     if (L.emit && has) ext++;
     if (clo) return L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
     return push ? node_event(L, w) : 0;
@@ -217,58 +276,57 @@ struct DfsTraits {
     static constexpr int min_blocks = DfsCfg<W>::min_blocks;
 };
 
-template <class T, int PASS>
+template <class T>
 __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
     using O = MT<T>;
     constexpr int W = O::W;
     constexpr int WARPS = DfsTraits<T>::warps;
     __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32];
-    __shared__ int4 sdesc[(PASS == PASS_WRITE) ? WARPS * 32 : 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32);
-    const uint32_t mp = wbase + lane * 4;
-    int4 *wdesc = sdesc + ((PASS == PASS_WRITE) ? wid * 32 : 0);
-    const int plane = pidx(lane);
+    const uint32_t mp = (uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32) + lane * 4;
     const DevGraph &G = A.G;
     const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
-    const int64_t nwork = (PASS == PASS_COUNT) ? (int64_t)*A.n_work : A.n_units;
+    const int64_t nwork = (int64_t)*A.n_work;
 
     Lane<T> L;
     L.active = false;
     L.done = false;
     bool exhausted = false;
     int64_t uidx = -1;
-    int32_t uscc = 0, tr = 0;
+    int32_t uscc = 0;
     uint64_t c[C_NUM];
     uint64_t ext = 0;
     int64_t pair_row = 0;
     int32_t s_slot = 0;
+    RecWriter R;
+    R.cur = A.chunks;
+    R.fill = 0;
+    R.first = 0;
+    R.count = 0;
 #pragma unroll
     for (int i = 0; i < C_NUM; i++) c[i] = 0;
-#ifdef TPGEN_KERNEL_DEBUG
-    unsigned long long d_outer = 0, d_inner = 0, d_steps = 0, d_emit = 0;
-    const long long t_start = clock64();
-#endif
 
     while (true) {
         int ev = 0, e = -1;
         bool fresh = false;
-#ifdef TPGEN_KERNEL_DEBUG
-        d_outer++;
-#endif
         // ---------------- refill idle lanes (warp-aggregated grab)
         const unsigned idle = __ballot_sync(kFull, !L.active && !exhausted);
         if (idle) {
             const int leader = __ffs(idle) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(A.next, (unsigned long long)__popc(idle));
+            unsigned long long base = 0, cbase = 0;
+            if (lane == leader) {
+                base = atomicAdd(A.next, (unsigned long long)__popc(idle));
+                cbase = atomicAdd(A.chunk_next, (unsigned long long)__popc(idle));
+            }
             base = __shfl_sync(kFull, base, leader);
+            cbase = __shfl_sync(kFull, cbase, leader);
             if (!L.active && !exhausted) {
-                const int64_t my = (int64_t)base + __popc(idle & ((1u << lane) - 1));
+                const int rank = __popc(idle & ((1u << lane) - 1));
+                const int64_t my = (int64_t)base + rank;
                 if (my >= nwork) {
                     exhausted = true;
                 } else {
-                    uidx = (PASS == PASS_COUNT) ? A.work[my] : my;
+                    uidx = A.work[my];
                     const Unit<W> *U = units + uidx;
                     const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
                     L.M = O::from(U->M);
@@ -293,36 +351,40 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     L.u = u;
                     L.sbit = O::bit(s);
                     L.vb = __ldg(G.scc_vbase + uscc);
-                    const int ga = __ldg(G.scc_gbase + uscc);
-                    tr = (ga >= 0) ? ga : -(L.vb + 1);
                     s_slot = L.vb + s;
                     const Slot<W> *ss = slot_ptr<W>(G, s_slot);
                     L.ps = O::load(ss->pin);
                     const int4 sm = ld_meta(ss);
                     L.seg = (sm.w & F_ENTRY) != 0;
-                    L.sgid = sm.x;
                     L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
                     L.k = 0;
                     L.o = 0;
                     L.steps = 0;
                     L.done = false;
                     L.active = true;
+                    L.limit = A.budget;
+                    L.base = depth + 1;
+                    L.pn = 0;
+                    L.pend = 0;
                     fresh = true;
-                    if (PASS == PASS_COUNT) {
-                        L.limit = A.budget;
 #pragma unroll
-                        for (int i = 0; i < C_NUM; i++) c[i] = 0;
-                        ext = 0;
-                        if (L.seg) {
-                            const int32_t nout = __ldg(G.scc_nout + uscc);
-                            pair_row = __ldg(G.scc_pair_base + uscc) +
-                                       (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
-                        }
+                    for (int i = 0; i < C_NUM; i++) c[i] = 0;
+                    ext = 0;
+                    const unsigned long long ch = cbase + rank;
+                    if (ch >= A.chunk_cap) {
+                        atomicOr(A.overflow, 2u);
+                        R.cur = A.chunks;
+                        R.first = 0;
                     } else {
-                        const uint32_t nsteps = (uint32_t)h.z;
-                        L.limit = nsteps ? nsteps : 0xffffffffu;
-#pragma unroll
-                        for (int i = 0; i < C_NUM; i++) c[i] = A.off[i][uidx];
+                        R.cur = A.chunks + ch * kChunkRecs;
+                        R.first = (int64_t)ch;
+                    }
+                    R.fill = 0;
+                    R.count = 0;
+                    if (L.seg) {
+                        const int32_t nout = __ldg(G.scc_nout + uscc);
+                        pair_row = __ldg(G.scc_pair_base + uscc) +
+                                   (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
                     }
                     // the unit's root event (no step is counted for it)
                     if (kind == K_NODE) {
@@ -343,155 +405,74 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 }
             }
         }
+
         // ---------------- one step for every running lane (lanes that just loaded emit their root event)
-        const bool run = L.active && !L.done && !(fresh && ev != 0);
-        #ifdef TPGEN_KERNEL_DEBUG
-        if (A.dbg) {
-            d_inner++;
-            d_steps += __popc(__ballot_sync(kFull, run));
-        }
-#endif
-        if (run) {
-            ev = dfs_step<T>(G, L, mp, e, ext);
+        if (L.active && !L.done && !(fresh && ev != 0)) {
+            ev = dfs_step<T>(A, G, L, R, mp, e, ext);
             L.steps++;
         }
         if (__ballot_sync(kFull, L.active) == 0) break;
 
-        // ---------------- events
-        if (PASS == PASS_COUNT) {
-            if (ev) {
-                const int ty = ev_type(ev);
-                const uint64_t len = (uint64_t)ev_len(ev);
-                if (ty == EV_PP) {
-                    c[C_PP] += 1;
-                    c[C_VERT] += len;
-                } else if (ty == EV_HEAD) {
-                    const int32_t x = __ldg(G.out_gid + e);
-                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                    c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
-                    c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow),
-                                        A.overflow);
-                    c[C_HEADS] += 1;
-                    c[C_HEADV] += len;
-                } else if (ty == EV_TAIL) {
-                    c[C_ITEMS] += 1;
-                    c[C_ITEMV] += len;
-                    atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
-                    atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
-                } else {  // EV_TRANSIT
-                    c[C_ITEMS] += 1;
-                    c[C_ITEMV] += len;
-                    atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
-                    atomicAdd(A.agg_pair_len + pair_row + e, (unsigned long long)len);
-                }
-            }
-        } else {
-            const unsigned em = __ballot_sync(kFull, ev != 0);
-            if (em) {
-                if (ev) {
-                    const int ty = ev_type(ev);
-                    const uint64_t len = (uint64_t)ev_len(ev);
-                    int32_t *dst;
-                    if (ty == EV_PP) {
-                        dst = A.out_vert + c[C_VERT];
-                        A.out_off[c[C_PP]] = (int64_t)c[C_VERT];
-                        c[C_PP] += 1;
-                        c[C_VERT] += len;
-                    } else if (ty == EV_HEAD) {
-                        const int32_t x = __ldg(G.out_gid + e);
-                        dst = A.head_pool + c[C_HEADV];
-                        HeadRec hr;
-                        hr.pp_off = c[C_PP];
-                        hr.v_off = c[C_VERT];
-                        hr.hv_off = c[C_HEADV];
-                        hr.len = (int32_t)len;
-                        hr.x = x;
-                        A.heads[c[C_HEADS]] = hr;
-                        const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                        c[C_PP] += Wx;
-                        c[C_VERT] += len * Wx + Vx;
-                        c[C_HEADS] += 1;
-                        c[C_HEADV] += len;
-                    } else {  // EV_TAIL / EV_TRANSIT
-                        dst = A.item_pool + c[C_ITEMV];
-                        ItemRec it;
-                        it.pool_off = (int64_t)c[C_ITEMV];
-                        it.len = (int32_t)len;
-                        it.y = (ty == EV_TRANSIT) ? __ldg(G.out_gid + e) : -1;
-                        it.ent = L.sgid;
-                        it.pad = 0;
-                        A.items[c[C_ITEMS]] = it;
-                        c[C_ITEMS] += 1;
-                        c[C_ITEMV] += len;
-                    }
-                    const unsigned long long p = reinterpret_cast<unsigned long long>(dst);
-                    wdesc[lane] = make_int4((int)(uint32_t)p, (int)(uint32_t)(p >> 32), ev, tr);
-                }
-#ifdef TPGEN_KERNEL_DEBUG
-                if (A.dbg) d_emit += __popc(em);
-#endif
-                __syncwarp();
-                // warp-cooperative copy: each emitting lane's path is written by the whole warp
-                unsigned m = em;
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int4 d = wdesc[src];
-                    int32_t *dd = reinterpret_cast<int32_t *>(((unsigned long long)(uint32_t)d.y << 32) |
-                                                              (unsigned long long)(uint32_t)d.x);
-                    const int len = ev_len(d.z);
-                    const int plen = len - ((d.z & EV_CLO) ? 1 : 0);
-                    const uint32_t sp = wbase + src * 4;
-                    // element j = lane + 32 r lives at pidx(lane) + 1024 r; the closing vertex is path[0]
-                    if (d.w >= 0) {  // SCC with contiguous global ids: gid = base + local
-                        for (int j = lane, pj = plane; j < len; j += 32, pj += 1024)
-                            st_global(dd + j, d.w + lds_u8(sp + (j < plen ? pj : 0)));
-                    } else {
-                        const int32_t *gt = G.slot_gid + (-d.w - 1);
-                        for (int j = lane, pj = plane; j < len; j += 32, pj += 1024)
-                            st_global(dd + j, __ldg(gt + lds_u8(sp + (j < plen ? pj : 0))));
-                    }
-                }
-                __syncwarp();
+        // ---------------- event: counters + one record (lane-local)
+        if (ev) {
+            const int ty = ev_type(ev);
+            const uint64_t len = (uint64_t)ev_len(ev);
+            rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 12) |
+                              (L.pend << 16));
+            L.base += L.pn;
+            L.pn = 0;
+            L.pend = 0;
+            if (ty == EV_PP) {
+                c[C_PP] += 1;
+                c[C_VERT] += len;
+            } else if (ty == EV_HEAD) {
+                rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
+                const int32_t x = __ldg(G.out_gid + e);
+                const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
+                c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow), A.overflow);
+                c[C_HEADS] += 1;
+                c[C_HEADV] += len;
+            } else if (ty == EV_TAIL) {
+                c[C_ITEMS] += 1;
+                c[C_ITEMV] += len;
+                atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
+                atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
+            } else {  // EV_TRANSIT
+                rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
+                c[C_ITEMS] += 1;
+                c[C_ITEMV] += len;
+                atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
+                atomicAdd(A.agg_pair_len + pair_row + e, (unsigned long long)len);
             }
         }
 
         // ---------------- unit completion / budget
         if (L.active && (L.done || L.steps >= L.limit)) {
-            if (PASS == PASS_COUNT) {
-                const bool trunc = !L.done;
+            const bool trunc = !L.done;
 #pragma unroll
-                for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
-                A.ext[uidx] = ext;
-                A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
-                if (trunc) {
-                    Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
-                    O::store(L.M, S->M);
-                    int4 h;
-                    h.x = uscc;
-                    h.y = -1;
-                    h.z = (int)L.steps;
-                    h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
-                    *reinterpret_cast<int4 *>(&S->scc) = h;
-                    S->rdepth = (uint8_t)L.r;
-                    for (int j = 0; j <= L.l; j++) S->path[j] = (uint8_t)lds_u8(mp + pidx(j));
-                    atomicAdd(A.n_trunc, 1ull);
-                }
+            for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
+            A.ext[uidx] = ext;
+            A.rfirst[uidx] = R.first;
+            A.rcount[uidx] = R.count;
+            A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
+            if (trunc) {
+                Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
+                O::store(L.M, S->M);
+                int4 h;
+                h.x = uscc;
+                h.y = -1;
+                h.z = (int)L.steps;
+                h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
+                *reinterpret_cast<int4 *>(&S->scc) = h;
+                S->rdepth = (uint8_t)L.r;
+                for (int j = 0; j <= L.l; j++) S->path[j] = (uint8_t)lds_u8(mp + pidx(j));
+                atomicAdd(A.n_trunc, 1ull);
             }
             L.active = false;
             L.done = false;
         }
     }
-#ifdef TPGEN_KERNEL_DEBUG
-    if (A.dbg && lane == 0) {
-        atomicAdd(A.dbg + 0, d_outer);
-        atomicAdd(A.dbg + 1, d_inner);
-        atomicAdd(A.dbg + 2, d_steps);
-        atomicAdd(A.dbg + 3, d_emit);
-        atomicAdd(A.dbg + 4, (unsigned long long)(clock64() - t_start));
-        atomicMax(A.dbg + 5, (unsigned long long)(clock64() - t_start));
-    }
-#endif
 }
 
 }  // namespace tpg

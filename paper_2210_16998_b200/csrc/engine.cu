@@ -2,11 +2,11 @@
 //
 // tpgen_prime_paths (SURVEY.md §3 "Build 1"):
 //   plan (host)  -> roots (one unit per start vertex, canonical order)
-//   segment phase (entry starts): count rounds [dfs_kernel<COUNT> + refine]
+//   segment phase (entry starts): DFS rounds [dfs_kernel + refine]
 //   completion DP over the component DAG (host, KBs)
-//   prime-path phase (non-entry starts): count rounds
+//   prime-path phase (non-entry starts): DFS rounds  -- the dominant kernel
 //   scan of the per-unit counts -> exact output offsets
-//   dfs_kernel<WRITE> (all units)         -- the dominant kernel
+//   expand_kernel: record streams -> canonical offsets/vertices
 //   segment-table scans + stitch_kernel (cross-SCC prime paths)
 //   optional digest, optional D2H
 #include <algorithm>
@@ -18,7 +18,7 @@
 #include <mutex>
 
 #include "aux_kernels.cuh"
-#include "dfs.cuh"
+#include "expand.cuh"
 #include "engine.h"
 
 namespace tpg {
@@ -84,11 +84,13 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &stop, &work,
                                &rbuf, &scan_b, &scan_tot, &ctr, &agg, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs};
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &agg_bak};
     for (int i = 0; i < 2; i++) {
         v.push_back(&units[i]);
         v.push_back(&status[i]);
         v.push_back(&ext[i]);
+        v.push_back(&rfirst[i]);
+        v.push_back(&rcount[i]);
         for (int c = 0; c < C_NUM; c++) v.push_back(&cnt[i][c]);
     }
     return v;
@@ -300,28 +302,51 @@ static uint32_t choose_budget(int64_t nwork, int64_t lanes) {
     return std::max<uint32_t>(32, std::min(big, b));
 }
 
+// Grows the record pool to hold at least `need` chunks, keeping the first `used` chunks.
+static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
+    if (need <= P.chunk_cap) return TPGEN_OK;
+    uint64_t cap = std::max<uint64_t>(need, P.chunk_cap * 2);
+    void *np = nullptr;
+    TPG_CK(cudaMallocAsync(&np, cap * kChunkRecs * 8, s));
+    if (P.chunk_used && P.chunks.p)
+        TPG_CK(cudaMemcpyAsync(np, P.chunks.p, P.chunk_used * kChunkRecs * 8, cudaMemcpyDeviceToDevice, s));
+    if (P.chunks.p) TPG_CK(cudaFreeAsync(P.chunks.p, s));
+    P.chunks.p = np;
+    P.chunks.cap = cap * kChunkRecs * 8;
+    P.chunk_cap = cap;
+    return TPGEN_OK;
+}
+
+// Rounds of the DFS kernel over the pending units of one phase (seg = SCC-entry
+// starts, else prime-path starts).  Each round walks every pending unit for at
+// most `budget` steps, writing its records and counters; truncated units are
+// split into the walked piece plus the untried siblings on its stack (refine).
 template <class T>
-static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStream_t s, tpgen_stats &st,
-                                int64_t &launches, double &ms_count_kernel) {
+static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStream_t s, tpgen_stats &st,
+                              int64_t &launches, double &ms_dfs) {
     constexpr int W = MT<T>::W;
     Timer t;
     const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
+    const HostPlan &H = P.hp;
+    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
     for (int round = 0; round < 4096; round++) {
         const int cur = P.cur;
         const int64_t n = P.n_units;
         if (n == 0) return TPGEN_OK;
         TPG_TRY(P.work.ensure((size_t)n * 8, s));
-        unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0]=nwork [1]=next [2]=ntrunc
-        TPG_CK(cudaMemsetAsync(ctr, 0, 4 * 8, s));
+        unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0]=nwork [1]=next [2]=ntrunc [3]=ovf [4]=chunk_next
+        TPG_CK(cudaMemsetAsync(ctr, 0, 8, s));
         build_worklist_kernel<W><<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit<W>>(),
                                                                      P.status[cur].as<uint8_t>(), n, seg,
                                                                      P.work.as<int64_t>(), ctr + 0);
         launches++;
-        unsigned long long hctr[4];
+        unsigned long long hctr[5];
         TPG_CK(cudaMemcpyAsync(hctr, ctr, 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
         const int64_t nwork = (int64_t)hctr[0];
         if (nwork == 0) return TPGEN_OK;
+        if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
+        TPG_TRY(grow_pool(P, P.chunk_used + (uint64_t)nwork * 2 + 1024, s));
         DfsArgs A;
         memset(&A, 0, sizeof(A));
         A.G = G;
@@ -333,33 +358,51 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.cnt[cur][c].as<uint64_t>();
         A.ext = P.ext[cur].as<uint64_t>();
         A.status = P.status[cur].as<uint8_t>();
+        A.rfirst = P.rfirst[cur].as<int64_t>();
+        A.rcount = P.rcount[cur].as<int64_t>();
         A.stop = P.stop.as<Unit<W>>();
         A.budget = choose_budget(nwork, lanes);
         A.n_trunc = ctr + 2;
         unsigned long long *agg = P.agg.as<unsigned long long>();
         A.agg_tail_cnt = agg;
-        A.agg_tail_len = agg + P.hp.n;
-        A.agg_pair_cnt = agg + 2 * (int64_t)P.hp.n;
-        A.agg_pair_len = agg + 2 * (int64_t)P.hp.n + P.hp.n_pairs;
+        A.agg_tail_len = agg + H.n;
+        A.agg_pair_cnt = agg + 2 * (int64_t)H.n;
+        A.agg_pair_len = agg + 2 * (int64_t)H.n + H.n_pairs;
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 3);
+        A.chunk_next = ctr + 4;
         const int grid = grid_for(nwork, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks);
-        cudaEventRecord(t.a, s);
-        dfs_kernel<T, PASS_COUNT><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
-        cudaEventRecord(t.b, s);
-        launches++;
-        TPG_CK(cudaGetLastError());
-        TPG_CK(cudaMemcpyAsync(hctr, ctr, 4 * 8, cudaMemcpyDeviceToHost, s));
-        TPG_CK(cudaStreamSynchronize(s));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, t.a, t.b);
-        ms_count_kernel += ms;
-        st.n_count_rounds++;
+        while (true) {  // retried only if the record pool overflows
+            A.chunks = P.chunks.as<uint64_t>();
+            A.chunk_cap = P.chunk_cap;
+            unsigned long long init[4] = {0, 0, 0, P.chunk_used};
+            TPG_CK(cudaMemcpyAsync(ctr + 1, init, 4 * 8, cudaMemcpyHostToDevice, s));
+            cudaEventRecord(t.a, s);
+            dfs_kernel<T><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
+            cudaEventRecord(t.b, s);
+            launches++;
+            TPG_CK(cudaGetLastError());
+            TPG_CK(cudaMemcpyAsync(hctr, ctr, 5 * 8, cudaMemcpyDeviceToHost, s));
+            TPG_CK(cudaStreamSynchronize(s));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, t.a, t.b);
+            ms_dfs += ms;
+            st.n_count_rounds++;
+            if (!((unsigned)hctr[3] & 2u)) break;
+            // record pool exhausted: undo the round and retry with a larger pool
+            reset_status_kernel<<<grid_for(nwork, 256, 4096), 256, 0, s>>>(P.work.as<int64_t>(), ctr + 0,
+                                                                           P.status[cur].as<uint8_t>());
+            launches++;
+            if (seg) TPG_CK(cudaMemcpyAsync(P.agg.p, P.agg_bak.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
+            TPG_TRY(grow_pool(P, std::max<uint64_t>(hctr[4], P.chunk_cap) * 2, s));
+        }
+        P.chunk_used = hctr[4];
         if ((unsigned)hctr[3] & 1u) P.overflow = true;
         if (hctr[2] == 0) return TPGEN_OK;
-        // ---- refine: truncated units -> counted piece + remainder units
+        // ---- refine: truncated units -> walked piece + remainder units
         TPG_TRY(P.rbuf.ensure((size_t)n * 8, s));
         refine_count_kernel<W><<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.status[cur].as<uint8_t>(),
-                                                                    P.stop.as<Unit<W>>(), n, P.rbuf.as<uint64_t>());
+                                                                       P.stop.as<Unit<W>>(), n,
+                                                                       P.rbuf.as<uint64_t>());
         launches++;
         uint64_t *arr[1] = {P.rbuf.as<uint64_t>()};
         uint64_t total = 0;
@@ -369,6 +412,8 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         TPG_TRY(P.units[nx].ensure((size_t)nn * sizeof(Unit<W>), s));
         TPG_TRY(P.status[nx].ensure((size_t)nn, s));
         TPG_TRY(P.ext[nx].ensure((size_t)nn * 8, s));
+        TPG_TRY(P.rfirst[nx].ensure((size_t)nn * 8, s));
+        TPG_TRY(P.rcount[nx].ensure((size_t)nn * 8, s));
         for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[nx][c].ensure((size_t)nn * 8, s));
         RefineBufs<W> B;
         B.units = P.units[cur].as<Unit<W>>();
@@ -379,9 +424,13 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
             B.ncnt[c] = P.cnt[nx][c].as<uint64_t>();
         }
         B.ext = P.ext[cur].as<uint64_t>();
+        B.rfirst = P.rfirst[cur].as<int64_t>();
+        B.rcount = P.rcount[cur].as<int64_t>();
         B.nunits = P.units[nx].as<Unit<W>>();
         B.nstatus = P.status[nx].as<uint8_t>();
         B.next = P.ext[nx].as<uint64_t>();
+        B.nrfirst = P.rfirst[nx].as<int64_t>();
+        B.nrcount = P.rcount[nx].as<int64_t>();
         refine_scatter_kernel<W><<<grid_for(n, 128, 8192), 128, 0, s>>>(G, B, n, P.rbuf.as<uint64_t>());
         launches++;
         TPG_CK(cudaGetLastError());
@@ -389,7 +438,7 @@ static tpgen_status count_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStr
         P.n_units = nn;
         TPG_TRY(P.stop.ensure((size_t)nn * sizeof(Unit<W>), s));
     }
-    set_error("count phase did not converge");
+    set_error("DFS phase did not converge");
     return TPGEN_ERR_INTERNAL;
 }
 
@@ -416,6 +465,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     st.max_scc = H.max_scc;
     st.ms_plan = P.ms_plan;
     P.overflow = false;
+    P.chunk_used = 0;
 
     Timer tall, tw, tst;
     cudaEventRecord(tall.a, s);
@@ -446,6 +496,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     TPG_TRY(P.units[0].ensure(nr * sizeof(Unit<W>), s));
     TPG_TRY(P.status[0].ensure(nr, s));
     TPG_TRY(P.ext[0].ensure(nr * 8, s));
+    TPG_TRY(P.rfirst[0].ensure(nr * 8, s));
+    TPG_TRY(P.rcount[0].ensure(nr * 8, s));
     for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[0][c].ensure(nr * 8, s));
     TPG_TRY(P.stop.ensure(nr * sizeof(Unit<W>), s));
     TPG_TRY(P.ctr.ensure(16 * 8, s));
@@ -455,12 +507,14 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     }
     const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
     TPG_TRY(P.agg.ensure(agg_n * 8, s));
+    TPG_TRY(P.agg_bak.ensure(agg_n * 8, s));
     TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
+    TPG_TRY(grow_pool(P, std::max<uint64_t>((64ull << 20) / (kChunkRecs * 8), nr * 4), s));
 
-    double ms_count_kernel = 0;
+    double ms_dfs = 0;
     // ---- segment phase (SCC entries) -> completion DP
     if (H.has_entries) {
-        TPG_TRY(count_phase<T>(P, G, 1, s, st, launches, ms_count_kernel));
+        TPG_TRY(dfs_phase<T>(P, G, 1, s, st, launches, ms_dfs));
         std::vector<uint64_t> aggh(agg_n);
         TPG_CK(cudaMemcpyAsync(aggh.data(), P.agg.p, agg_n * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
@@ -477,7 +531,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         TPG_CK(cudaMemcpyAsync(P.d_Wv.p, Vd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     }
     // ---- prime-path phase
-    TPG_TRY(count_phase<T>(P, G, 0, s, st, launches, ms_count_kernel));
+    TPG_TRY(dfs_phase<T>(P, G, 0, s, st, launches, ms_dfs));
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
@@ -514,7 +568,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         float ms = 0;
         cudaEventElapsedTime(&ms, tall.a, tall.b);
         st.ms_device = ms;
-        st.ms_count = ms_count_kernel;
+        st.ms_count = ms;
+        st.ms_dfs_count = ms_dfs;
         st.gpu_launches = launches;
         st.ms_total = now_ms() - t0;
         if (stp) *stp = st;
@@ -536,42 +591,29 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     TPG_TRY(P.items.ensure(std::max<int64_t>(n_items, 1) * sizeof(ItemRec), s));
     TPG_TRY(P.item_pool.ensure(std::max<uint64_t>(tot[C_ITEMV], 1) * 4, s));
 
-    // ---- write pass
-    DfsArgs A;
-    memset(&A, 0, sizeof(A));
-    A.G = G;
-    A.units = P.units[cur].as<Unit<W>>();
-    A.n_units = nu;
-    unsigned long long *ctr = P.ctr.as<unsigned long long>();
-    TPG_CK(cudaMemsetAsync(ctr, 0, 4 * 8, s));
-    A.next = ctr + 1;
-    for (int c = 0; c < C_NUM; c++) A.off[c] = off[c];
-    A.out_off = (int64_t *)d_off;
-    A.out_vert = (int32_t *)d_vert;
-    A.heads = P.heads.as<HeadRec>();
-    A.head_pool = P.head_pool.as<int32_t>();
-    A.items = P.items.as<ItemRec>();
-    A.item_pool = P.item_pool.as<int32_t>();
-    const bool dbg = getenv("TPGEN_DEBUG") != nullptr;
-    if (dbg) {
-        A.dbg = ctr + 8;
-        TPG_CK(cudaMemsetAsync(A.dbg, 0, 8 * 8, s));
-    }
+    // ---- canonical writer: replay the record streams at their exact offsets
+    ExpandArgs E;
+    memset(&E, 0, sizeof(E));
+    E.G = G;
+    E.units = P.units[cur].as<Unit<W>>();
+    E.n_units = nu;
+    E.rfirst = P.rfirst[cur].as<int64_t>();
+    E.rcount = P.rcount[cur].as<int64_t>();
+    for (int c = 0; c < C_NUM; c++) E.off[c] = off[c];
+    E.chunks = P.chunks.as<uint64_t>();
+    E.out_off = (int64_t *)d_off;
+    E.out_vert = (int32_t *)d_vert;
+    E.heads = P.heads.as<HeadRec>();
+    E.head_pool = P.head_pool.as<int32_t>();
+    E.items = P.items.as<ItemRec>();
+    E.item_pool = P.item_pool.as<int32_t>();
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        dfs_kernel<T, PASS_WRITE><<<grid_for(nu, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks), DfsCfg<W>::threads,
-                                   0, s>>>(A);
+        expand_kernel<W><<<grid_for(nu * 32, kExpandThreads, P.num_sms * 8), kExpandThreads, 0, s>>>(E);
         launches++;
     }
     cudaEventRecord(tw.b, s);
     TPG_CK(cudaGetLastError());
-    if (dbg) {
-        unsigned long long h[8];
-        TPG_CK(cudaMemcpyAsync(h, A.dbg, 64, cudaMemcpyDeviceToHost, s));
-        TPG_CK(cudaStreamSynchronize(s));
-        fprintf(stderr, "[tpgen dbg write] outer=%llu inner=%llu lane_steps=%llu emits=%llu warp_cycles_sum=%llu max=%llu\n",
-                h[0], h[1], h[2], h[3], h[4], h[5]);
-    }
 
     // ---- cross-SCC stitching
     cudaEventRecord(tst.a, s);
@@ -625,8 +667,9 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventRecord(tall.b, s);
     TPG_CK(cudaGetLastError());
 
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();
     if (o.compute_digest && n_pp > 0) {
-        unsigned long long *acc = ctr + 4;
+        unsigned long long *acc = ctr + 8;
         TPG_CK(cudaMemsetAsync(acc, 0, 16, s));
         digest_kernel<<<grid_for(n_pp, 256, P.num_sms * 8), 256, 0, s>>>((int64_t *)d_off, (int32_t *)d_vert, n_pp,
                                                                            acc);
@@ -642,12 +685,12 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventElapsedTime(&ms, tall.a, tall.b);
     st.ms_device = ms;
     cudaEventElapsedTime(&ms, tw.a, tw.b);
-    st.ms_dfs_write = ms;
     st.ms_write = ms;
     cudaEventElapsedTime(&ms, tst.a, tst.b);
     st.ms_stitch = ms;
     st.ms_count = st.ms_device - st.ms_write - st.ms_stitch;
-    st.ms_dfs_count = ms_count_kernel;
+    st.ms_dfs_count = ms_dfs;   // DFS kernel time (all rounds)
+    st.ms_dfs_write = ms_dfs;   // the dominant kernel is the DFS enumerator
     st.gpu_launches = launches;
 
     ow_guard.release();

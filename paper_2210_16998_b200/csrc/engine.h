@@ -34,7 +34,10 @@ struct PlanImpl {
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
         d_slot_eidx, d_Wc, d_Wv, d_scc_gbase;
     // workspace (double-buffered unit arrays for refinement)
-    DevBuf units[2], status[2], ext[2], cnt[2][kCnt];
+    DevBuf units[2], status[2], ext[2], rfirst[2], rcount[2], cnt[2][kCnt];
+    DevBuf chunks, agg_bak;      // path-delta record pool (chunks of kChunkRecs words); aggregate backup
+    uint64_t chunk_cap = 0;      // pool capacity in chunks
+    uint64_t chunk_used = 0;     // chunks handed out so far in this call
     DevBuf stop, work, rbuf, scan_b, scan_tot, ctr, agg, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend,
         hcomp, offs, tp_tabs;
     int cur = 0;

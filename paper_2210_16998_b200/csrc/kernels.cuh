@@ -139,27 +139,24 @@ struct DfsArgs {
     DevGraph G;
     const void *units;  // Unit<W>[n_units]
     int64_t n_units;
-    const int64_t *work;  // count pass: indices of the units to process
+    const int64_t *work;  // indices of the units to process
     const unsigned long long *n_work;
     unsigned long long *next;  // grab counter (zeroed before launch)
-    // count pass
+    // per-unit results
     uint64_t *cnt[C_NUM];
     uint64_t *ext;
     uint8_t *status;
-    void *stop;  // Unit<W>[n_units]
+    int64_t *rfirst;  // first record chunk of the unit
+    int64_t *rcount;  // records of the unit
+    void *stop;       // Unit<W>[n_units]: stop states of truncated units
     uint32_t budget;
     unsigned long long *n_trunc;
     unsigned long long *agg_tail_cnt, *agg_tail_len, *agg_pair_cnt, *agg_pair_len;
-    unsigned int *overflow;
-    // write pass
-    const uint64_t *off[C_NUM];
-    int64_t *out_off;
-    int32_t *out_vert;
-    HeadRec *heads;
-    int32_t *head_pool;
-    ItemRec *items;
-    int32_t *item_pool;
-    unsigned long long *dbg;  // optional counters: outer iters, inner iters, lane-steps, emissions, warp cycles
+    unsigned int *overflow;  // bit 0: count overflow, bit 1: record pool exhausted
+    // record pool
+    uint64_t *chunks;
+    unsigned long long *chunk_next;
+    unsigned long long chunk_cap;
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
