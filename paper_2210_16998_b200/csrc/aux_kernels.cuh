@@ -97,97 +97,91 @@ __global__ void scan_down_kernel(ScanArrays S, int64_t n, const uint64_t *bsum, 
     }
 }
 
-// ------------------------------------------------------------- refinement
-template <int W>
-__global__ void build_worklist_kernel(DevGraph G, const Unit<W> *units, const uint8_t *status, int64_t n,
-                                      int seg_phase, int64_t *work, unsigned long long *nwork) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (status[i] != ST_PENDING) continue;
-        const int32_t scc = units[i].scc;
-        const int s = units[i].path[0];
-        const int flags = __ldg(&slot_ptr<W>(G, __ldg(G.scc_vbase + scc) + s)->flags);
-        if (((flags & F_ENTRY) != 0) == (seg_phase != 0)) work[atomicAdd(nwork, 1ull)] = i;
-    }
-}
+// ---------------------------------------------------------- linearization
+// The units form a forest: roots are the start vertices (canonical order =
+// ascending global id), and a split unit's children are its remainder units,
+// which follow it in lexicographic order.  Canonical output order is the
+// preorder of that forest, so each unit's output offsets are obtained by a
+// bottom-up pass (subtree totals, generation by generation) and a top-down pass
+// (children placed after their parent, in order).
+struct LinArgs {
+    const uint64_t *cnt[C_NUM];  // own counts
+    uint64_t *sub[C_NUM];        // subtree totals
+    uint64_t *off[C_NUM];        // exclusive offsets in canonical order
+    const int64_t *child_first;
+    const int32_t *child_count;
+    const int32_t *gen;
+    int64_t n;
+    const int64_t *roots;        // root units in canonical order
+    int64_t n_roots;
+    uint64_t *totals;            // [C_NUM]
+};
 
-template <int W>
-__global__ void refine_count_kernel(DevGraph G, const uint8_t *status, const Unit<W> *stop, int64_t n,
-                                    uint64_t *r) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (status[i] != ST_TRUNC) {
-            r[i] = 1;
-        } else {
-            const Unit<W> S = stop[i];
-            r[i] = 1 + (uint64_t)remainder_events<W, false>(G, S, nullptr);
+__global__ void lin_up_kernel(LinArgs A, int g) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (A.gen[i] != g) continue;
+        const int32_t cc = A.child_count[i];
+        const int64_t cf = A.child_first[i];
+#pragma unroll
+        for (int c = 0; c < C_NUM; c++) {
+            uint64_t s = A.cnt[c][i];
+            for (int32_t k = 0; k < cc; k++) s += A.sub[c][cf + k];
+            A.sub[c][i] = s;
         }
     }
 }
 
-template <int W>
-struct RefineBufs {
-    const Unit<W> *units;
-    const uint8_t *status;
-    const Unit<W> *stop;
-    const uint64_t *cnt[C_NUM];
-    const uint64_t *ext;
-    const int64_t *rfirst, *rcount;
-    Unit<W> *nunits;
-    uint8_t *nstatus;
-    uint64_t *ncnt[C_NUM];
-    uint64_t *next;
-    int64_t *nrfirst, *nrcount;
-};
+// One block: exclusive scan of the root subtree totals in canonical root order.
+__global__ void lin_roots_kernel(LinArgs A) {
+    __shared__ uint64_t sm[32];
+    for (int c = 0; c < C_NUM; c++) {
+        uint64_t carry = 0;
+        for (int64_t b0 = 0; b0 < A.n_roots; b0 += kScanThreads) {
+            const int64_t j = b0 + threadIdx.x;
+            const uint64_t v = (j < A.n_roots) ? A.sub[c][A.roots[j]] : 0;
+            uint64_t tot;
+            const uint64_t ex = block_excl_scan(v, sm, tot);
+            if (j < A.n_roots) A.off[c][A.roots[j]] = ex + carry;
+            carry += tot;
+        }
+        if (threadIdx.x == 0) A.totals[c] = carry;
+    }
+}
 
-template <int W>
-__global__ void refine_scatter_kernel(DevGraph G, RefineBufs<W> B, int64_t n, const uint64_t *off) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = (int64_t)off[i];
-        Unit<W> U = B.units[i];
-        const uint8_t st = B.status[i];
-        if (st == ST_TRUNC) U.nsteps = B.stop[i].nsteps;
-        B.nunits[p] = U;
-        B.nstatus[p] = (st == ST_TRUNC) ? ST_DONE : st;
+__global__ void lin_down_kernel(LinArgs A, int g) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (A.gen[i] != g) continue;
+        const int32_t cc = A.child_count[i];
+        if (cc == 0) continue;
+        const int64_t cf = A.child_first[i];
 #pragma unroll
-        for (int c = 0; c < C_NUM; c++) B.ncnt[c][p] = B.cnt[c][i];
-        B.next[p] = B.ext[i];
-        B.nrfirst[p] = B.rfirst[i];
-        B.nrcount[p] = B.rcount[i];
-        if (st == ST_TRUNC) {
-            const Unit<W> S = B.stop[i];
-            const int m = remainder_events<W, true>(G, S, B.nunits + p + 1);
-            for (int q = 1; q <= m; q++) {
-                B.nstatus[p + q] = ST_PENDING;
-#pragma unroll
-                for (int c = 0; c < C_NUM; c++) B.ncnt[c][p + q] = 0;
-                B.next[p + q] = 0;
-                B.nrfirst[p + q] = -1;
-                B.nrcount[p + q] = 0;
+        for (int c = 0; c < C_NUM; c++) {
+            uint64_t base = A.off[c][i] + A.cnt[c][i];
+            for (int32_t k = 0; k < cc; k++) {
+                A.off[c][cf + k] = base;
+                base += A.sub[c][cf + k];
             }
         }
     }
 }
 
-// Undo a DFS round whose record pool overflowed: its units become pending again.
-__global__ void reset_status_kernel(const int64_t *work, const unsigned long long *nwork, uint8_t *status) {
-    const int64_t n = (int64_t)*nwork;
+__global__ void sum_kernel(const uint64_t *a, int64_t n, unsigned long long *out) {
+    uint64_t s = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        status[work[i]] = ST_PENDING;
+        s += a[i];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, (unsigned long long)s);
 }
 
 // --------------------------------------------------- segment tables (a5)
-template <int W>
-__global__ void item_bounds_kernel(DevGraph G, const Unit<W> *units, int64_t n, const uint64_t *off_items,
-                                   uint64_t total_items, int64_t *ibeg, int64_t *iend) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int vb = __ldg(G.scc_vbase + units[i].scc);
-        const int4 sm = ld_meta(slot_ptr<W>(G, vb + units[i].path[0]));
-        if (!(sm.w & F_ENTRY)) continue;
-        const int32_t g = sm.x;
-        int32_t gp = -1, gn = -1;
-        if (i > 0) gp = __ldg(G.slot_gid + __ldg(G.scc_vbase + units[i - 1].scc) + units[i - 1].path[0]);
-        if (i + 1 < n) gn = __ldg(G.slot_gid + __ldg(G.scc_vbase + units[i + 1].scc) + units[i + 1].path[0]);
-        if (gp != g) ibeg[g] = (int64_t)off_items[i];
-        if (gn != g) iend[g] = (i + 1 < n) ? (int64_t)off_items[i + 1] : (int64_t)total_items;
+// Items of entry vertex x are the items of the subtree of x's root unit.
+__global__ void item_bounds_kernel(const int64_t *roots, const int32_t *root_gid, int64_t n_roots,
+                                   const uint64_t *off_items, const uint64_t *sub_items, int64_t *ibeg, int64_t *iend) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_roots; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = roots[j];
+        ibeg[root_gid[j]] = (int64_t)off_items[r];
+        iend[root_gid[j]] = (int64_t)(off_items[r] + sub_items[r]);
     }
 }
 

@@ -276,6 +276,78 @@ struct DfsTraits {
     static constexpr int min_blocks = DfsCfg<W>::min_blocks;
 };
 
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+__device__ __forceinline__ int lds_u32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
+// Remainder of a running unit: the untried events of every node on the lane's
+// stack, deepest level first -- exactly the rest of the walk, in lexicographic
+// order.  Pass WRITE=false counts them, WRITE=true writes them as units.
+template <class T, bool WRITE>
+__device__ int lane_remainder(const DevGraph &G, const Lane<T> &L, uint32_t mp, int uscc, Unit<MT<T>::W> *out) {
+    using O = MT<T>;
+    constexpr int W = O::W;
+    T M = L.M;
+    int n = 0;
+    for (int j = L.l; j >= L.r; j--) {
+        const int u = lds_u8(mp + pidx(j));
+        const Slot<W> *su = slot_ptr<W>(G, L.vb + u);
+        const T sin = O::load(su->sin);
+        const int4 meta = ld_meta(su);
+        int k, o;
+        if (j == L.l) {
+            k = L.k;
+            o = L.o;
+        } else {
+            const int wc = lds_u8(mp + pidx(j + 1));
+            O::clr(M, wc);
+            k = wc + 1;
+            o = count_out_le(G, meta.y, meta.z, wc);
+        }
+        while (true) {
+            const int w = O::next(sin, M, L.sbit, k);
+            int kind = -1, e = -1;
+            if (o < meta.z && __ldg(G.out_pos + meta.y + o) <= w) {
+                e = meta.y + o;
+                o++;
+                if (L.seg || O::subset(L.ps, M)) kind = K_OUT;
+            } else {
+                if (w >= O::BITS) break;
+                k = w + 1;
+                kind = (w == L.s) ? K_CLOSURE : K_NODE;
+            }
+            if (kind < 0) continue;
+            if (WRITE) {
+                Unit<W> &U = out[n];
+                const int depth = (kind == K_NODE) ? j + 1 : j;
+                uint32_t *pw = reinterpret_cast<uint32_t *>(U.path);
+                for (int q = 0; q <= (j >> 2); q++) pw[q] = (uint32_t)lds_u32(mp + (q << 7));
+                T Mu = M;
+                if (kind == K_NODE) {
+                    U.path[j + 1] = (uint8_t)w;
+                    O::set(Mu, w);
+                }
+                O::store(Mu, U.M);
+                *reinterpret_cast<int4 *>(&U.scc) = make_int4(uscc, e, 0, depth | (kind << 8));
+            }
+            n++;
+        }
+    }
+    return n;
+}
+
+// Persistent DFS kernel with an in-kernel work queue.  Idle lanes claim queue
+// slots (warp-aggregated atomic on the head) and wait for them to be filled;
+// a running lane whose unit has taken at least split_min steps splits it when
+// claims outrun the queue tail (some lane is starving): its walk so far becomes
+// a finished piece and the untried siblings on its stack are pushed as new
+// units (children of the piece in the unit tree).  The kernel ends when every
+// pushed unit has finished (done == tail).
 template <class T>
 __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
     using O = MT<T>;
@@ -285,15 +357,14 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t mp = (uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32) + lane * 4;
     const DevGraph &G = A.G;
-    const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
-    const int64_t nwork = (int64_t)*A.n_work;
+    Unit<W> *units = reinterpret_cast<Unit<W> *>(A.units);
 
     Lane<T> L;
     L.active = false;
     L.done = false;
-    bool exhausted = false;
-    int64_t uidx = -1;
-    int32_t uscc = 0;
+    bool waiting = false, exited = false;
+    int64_t slot = -1;
+    int32_t uscc = 0, ugen = 0;
     uint64_t c[C_NUM];
     uint64_t ext = 0;
     int64_t pair_row = 0;
@@ -309,114 +380,132 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     while (true) {
         int ev = 0, e = -1;
         bool fresh = false;
-        // ---------------- refill idle lanes (warp-aggregated grab)
-        const unsigned idle = __ballot_sync(kFull, !L.active && !exhausted);
-        if (idle) {
-            const int leader = __ffs(idle) - 1;
-            unsigned long long base = 0, cbase = 0;
-            if (lane == leader) {
-                base = atomicAdd(A.next, (unsigned long long)__popc(idle));
-                cbase = atomicAdd(A.chunk_next, (unsigned long long)__popc(idle));
-            }
+        // ---------------- idle lanes claim a queue slot (warp-aggregated)
+        const unsigned need = __ballot_sync(kFull, !L.active && !waiting && !exited);
+        if (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(A.q + 0, (unsigned long long)__popc(need));
             base = __shfl_sync(kFull, base, leader);
-            cbase = __shfl_sync(kFull, cbase, leader);
-            if (!L.active && !exhausted) {
-                const int rank = __popc(idle & ((1u << lane) - 1));
-                const int64_t my = (int64_t)base + rank;
-                if (my >= nwork) {
-                    exhausted = true;
-                } else {
-                    uidx = A.work[my];
-                    const Unit<W> *U = units + uidx;
-                    const int4 h = *reinterpret_cast<const int4 *>(&U->scc);  // scc, e, nsteps, depth|kind|k|o
-                    L.M = O::from(U->M);
-                    uscc = h.x;
-                    const int kind = (h.w >> 8) & 0xff;
-                    const int depth = h.w & 0xff;
-                    L.l = L.r = depth;
-                    const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
-#pragma unroll 1
-                    for (int q = 0; q * 16 <= depth; q++) {
-                        const uint4 v = p4[q];
-                        // 4 levels per word: one 32-bit smem store per 4 levels
-                        const uint32_t wa = mp + pidx(q * 16);
-                        sts_u32(wa, v.x);
-                        if (q * 16 + 4 <= depth) sts_u32(wa + 128, v.y);
-                        if (q * 16 + 8 <= depth) sts_u32(wa + 256, v.z);
-                        if (q * 16 + 12 <= depth) sts_u32(wa + 384, v.w);
-                    }
-                    const int s = lds_u8(mp);
-                    const int u = lds_u8(mp + pidx(depth));
-                    L.s = s;
-                    L.u = u;
-                    L.sbit = O::bit(s);
-                    L.vb = __ldg(G.scc_vbase + uscc);
-                    s_slot = L.vb + s;
-                    const Slot<W> *ss = slot_ptr<W>(G, s_slot);
-                    L.ps = O::load(ss->pin);
-                    const int4 sm = ld_meta(ss);
-                    L.seg = (sm.w & F_ENTRY) != 0;
-                    L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
-                    L.k = 0;
-                    L.o = 0;
-                    L.steps = 0;
-                    L.done = false;
-                    L.active = true;
-                    L.limit = A.budget;
-                    L.base = depth + 1;
-                    L.pn = 0;
-                    L.pend = 0;
-                    fresh = true;
+            if (!L.active && !waiting && !exited) {
+                slot = (int64_t)base + __popc(need & ((1u << lane) - 1));
+                waiting = true;
+            }
+        }
+        // ---------------- waiting lanes: start the unit once written, or stop when all work is done
+        if (waiting) {
+            if (slot < (int64_t)A.qcap &&
+                *reinterpret_cast<const volatile unsigned int *>(A.ready + slot) != 0u) {
+                waiting = false;
+                __threadfence();
+                // queue slots are written by other SMs during this launch: read them at L2 (ld.cg)
+                const Unit<W> *U = units + slot;
+                const int4 h = __ldcg(reinterpret_cast<const int4 *>(&U->scc));  // scc, e, -, depth|kind
+                {
+                    uint64_t mw[W];
 #pragma unroll
-                    for (int i = 0; i < C_NUM; i++) c[i] = 0;
-                    ext = 0;
-                    const unsigned long long ch = cbase + rank;
-                    if (ch >= A.chunk_cap) {
-                        atomicOr(A.overflow, 2u);
-                        R.cur = A.chunks;
-                        R.first = 0;
-                    } else {
-                        R.cur = A.chunks + ch * kChunkRecs;
-                        R.first = (int64_t)ch;
+                    for (int i = 0; i < W; i++) mw[i] = __ldcg(reinterpret_cast<const unsigned long long *>(U->M) + i);
+                    L.M = O::from(mw);
+                }
+                uscc = h.x;
+                ugen = __ldcg(A.gen + slot);
+                const int kind = (h.w >> 8) & 0xff;
+                const int depth = h.w & 0xff;
+                L.l = L.r = depth;
+                const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
+#pragma unroll 1
+                for (int q = 0; q * 16 <= depth; q++) {
+                    const uint4 v = __ldcg(p4 + q);
+                    const uint32_t wa = mp + pidx(q * 16);  // 4 levels per 32-bit smem word
+                    sts_u32(wa, v.x);
+                    if (q * 16 + 4 <= depth) sts_u32(wa + 128, v.y);
+                    if (q * 16 + 8 <= depth) sts_u32(wa + 256, v.z);
+                    if (q * 16 + 12 <= depth) sts_u32(wa + 384, v.w);
+                }
+                const int s = lds_u8(mp);
+                const int u = lds_u8(mp + pidx(depth));
+                L.s = s;
+                L.u = u;
+                L.sbit = O::bit(s);
+                L.vb = __ldg(G.scc_vbase + uscc);
+                s_slot = L.vb + s;
+                const Slot<W> *ss = slot_ptr<W>(G, s_slot);
+                L.ps = O::load(ss->pin);
+                const int4 sm = ld_meta(ss);
+                L.seg = (sm.w & F_ENTRY) != 0;
+                L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
+                L.k = 0;
+                L.o = 0;
+                L.steps = 0;
+                L.done = false;
+                L.active = true;
+                L.base = depth + 1;
+                L.pn = 0;
+                L.pend = 0;
+                fresh = true;
+#pragma unroll
+                for (int i = 0; i < C_NUM; i++) c[i] = 0;
+                ext = 0;
+                const unsigned long long ch = atomicAdd(A.chunk_next, 1ull);
+                if (ch >= A.chunk_cap) {
+                    atomicOr(A.overflow, 2u);
+                    R.cur = A.chunks;
+                    R.first = 0;
+                } else {
+                    R.cur = A.chunks + ch * kChunkRecs;
+                    R.first = (int64_t)ch;
+                }
+                R.fill = 0;
+                R.count = 0;
+                if (L.seg) {
+                    const int32_t nout = __ldg(G.scc_nout + uscc);
+                    pair_row = __ldg(G.scc_pair_base + uscc) + (int64_t)__ldg(G.slot_eidx + s_slot) * nout -
+                               __ldg(G.scc_out_base + uscc);
+                }
+                // the unit's root event (no step is counted for it)
+                if (kind == K_NODE) {
+                    load_slot(G, L, u);
+                    if (depth > 0 && L.emit) ext++;
+                    ev = node_event(L, u);
+                } else if (kind == K_CLOSURE) {
+                    L.done = true;
+                    if (L.emit) {
+                        ext++;
+                        ev = EV_PP | EV_CLO | ((depth + 2) << 8);
                     }
-                    R.fill = 0;
-                    R.count = 0;
-                    if (L.seg) {
-                        const int32_t nout = __ldg(G.scc_nout + uscc);
-                        pair_row = __ldg(G.scc_pair_base + uscc) +
-                                   (int64_t)__ldg(G.slot_eidx + s_slot) * nout - __ldg(G.scc_out_base + uscc);
-                    }
-                    // the unit's root event (no step is counted for it)
-                    if (kind == K_NODE) {
-                        load_slot(G, L, u);
-                        if (depth > 0 && L.emit) ext++;
-                        ev = node_event(L, u);
-                    } else if (kind == K_CLOSURE) {
-                        L.done = true;
-                        if (L.emit) {
-                            ext++;
-                            ev = EV_PP | EV_CLO | ((depth + 2) << 8);
-                        }
-                    } else {  // K_OUT
-                        L.done = true;
-                        e = h.y;
-                        ev = out_event(L);
-                    }
+                } else {  // K_OUT
+                    L.done = true;
+                    e = h.y;
+                    ev = out_event(L);
+                }
+            } else {
+                const unsigned long long dn = ld_volatile(A.q + 2);
+                __threadfence();
+                const unsigned long long tl = ld_volatile(A.q + 1);
+                if (dn == tl || (*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u)) {
+                    waiting = false;
+                    exited = true;
                 }
             }
         }
+        if (__ballot_sync(kFull, L.active) == 0) {
+            if (__ballot_sync(kFull, !exited) == 0) break;
+            __nanosleep(256);
+            continue;
+        }
 
-        // ---------------- one step for every running lane (lanes that just loaded emit their root event)
+        // ---------------- one step for every running lane (lanes that just started emit their root event)
         if (L.active && !L.done && !(fresh && ev != 0)) {
             ev = dfs_step<T>(A, G, L, R, mp, e, ext);
             L.steps++;
         }
-        if (__ballot_sync(kFull, L.active) == 0) break;
 
         // ---------------- event: counters + one record (lane-local)
         if (ev) {
             const int ty = ev_type(ev);
             const uint64_t len = (uint64_t)ev_len(ev);
+            // HEAD / TRANSIT carry their out-arc in an R_ARG record written just before them
+            if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
             rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 12) |
                               (L.pend << 16));
             L.base += L.pn;
@@ -426,7 +515,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 c[C_PP] += 1;
                 c[C_VERT] += len;
             } else if (ty == EV_HEAD) {
-                rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
                 const int32_t x = __ldg(G.out_gid + e);
                 const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
                 c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
@@ -439,7 +527,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
                 atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
             } else {  // EV_TRANSIT
-                rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
                 c[C_ITEMS] += 1;
                 c[C_ITEMV] += len;
                 atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
@@ -447,28 +534,40 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             }
         }
 
-        // ---------------- unit completion / budget
-        if (L.active && (L.done || L.steps >= L.limit)) {
-            const bool trunc = !L.done;
-#pragma unroll
-            for (int i = 0; i < C_NUM; i++) A.cnt[i][uidx] = c[i];
-            A.ext[uidx] = ext;
-            A.rfirst[uidx] = R.first;
-            A.rcount[uidx] = R.count;
-            A.status[uidx] = trunc ? ST_TRUNC : ST_DONE;
-            if (trunc) {
-                Unit<W> *S = reinterpret_cast<Unit<W> *>(A.stop) + uidx;
-                O::store(L.M, S->M);
-                int4 h;
-                h.x = uscc;
-                h.y = -1;
-                h.z = (int)L.steps;
-                h.w = L.l | ((int)K_NODE << 8) | (L.k << 16) | (L.o << 24);
-                *reinterpret_cast<int4 *>(&S->scc) = h;
-                S->rdepth = (uint8_t)L.r;
-                for (int j = 0; j <= L.l; j++) S->path[j] = (uint8_t)lds_u8(mp + pidx(j));
-                atomicAdd(A.n_trunc, 1ull);
+        // ---------------- split on demand: some lane is starving and this unit has run long enough
+        if (L.active && !L.done && L.steps >= A.split_min && (L.steps & 31u) == 0u) {
+            if (ld_volatile(A.q + 0) > ld_volatile(A.q + 1)) {
+                const int m = lane_remainder<T, false>(G, L, mp, uscc, nullptr);
+                if (m > 0) {
+                    const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m);
+                    if (base + m > A.qcap) {
+                        atomicOr(A.overflow, 4u);
+                    } else {
+                        lane_remainder<T, true>(G, L, mp, uscc, units + base);
+                        for (int i = 0; i < m; i++) {
+                            A.gen[base + i] = ugen + 1;
+                            A.child_count[base + i] = 0;
+                        }
+                        A.child_first[slot] = (int64_t)base;
+                        A.child_count[slot] = m;
+                        atomicMax(A.maxgen, ugen + 1);
+                        __threadfence();
+                        for (int i = 0; i < m; i++) atomicExch(A.ready + base + i, 1u);
+                    }
+                }
+                L.done = true;  // the walked part is a finished piece
             }
+        }
+
+        // ---------------- unit completion
+        if (L.active && L.done) {
+#pragma unroll
+            for (int i = 0; i < C_NUM; i++) A.cnt[i][slot] = c[i];
+            A.ext[slot] = ext;
+            A.rfirst[slot] = R.first;
+            A.rcount[slot] = R.count;
+            __threadfence();
+            atomicAdd(A.q + 2, 1ull);
             L.active = false;
             L.done = false;
         }

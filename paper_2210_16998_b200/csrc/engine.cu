@@ -82,17 +82,11 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &stop, &work,
-                               &rbuf, &scan_b, &scan_tot, &ctr, &agg, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &agg_bak};
-    for (int i = 0; i < 2; i++) {
-        v.push_back(&units[i]);
-        v.push_back(&status[i]);
-        v.push_back(&ext[i]);
-        v.push_back(&rfirst[i]);
-        v.push_back(&rcount[i]);
-        for (int c = 0; c < C_NUM; c++) v.push_back(&cnt[i][c]);
-    }
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
+                               &qunits, &qready, &qext, &qrfirst, &qrcount, &qcfirst, &qccount, &qgen, &roots,
+                               &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks};
+    for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
 
@@ -294,14 +288,6 @@ struct Timer {
     }
 };
 
-static uint32_t choose_budget(int64_t nwork, int64_t lanes) {
-    const uint32_t big = 4096;
-    if (nwork >= lanes) return big;
-    double f = (double)nwork / (double)lanes;
-    uint32_t b = (uint32_t)(big * f);
-    return std::max<uint32_t>(32, std::min(big, b));
-}
-
 // Grows the record pool to hold at least `need` chunks, keeping the first `used` chunks.
 static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
     if (need <= P.chunk_cap) return TPGEN_OK;
@@ -317,129 +303,123 @@ static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
     return TPGEN_OK;
 }
 
-// Rounds of the DFS kernel over the pending units of one phase (seg = SCC-entry
-// starts, else prime-path starts).  Each round walks every pending unit for at
-// most `budget` steps, writing its records and counters; truncated units are
-// split into the walked piece plus the untried siblings on its stack (refine).
+// Grows a per-slot array to `cap` elements of `es` bytes keeping the first `used`.
+static tpgen_status grow_keep(DevBuf &b, size_t used, size_t cap, size_t es, cudaStream_t s) {
+    if (cap * es <= b.cap) return TPGEN_OK;
+    void *np = nullptr;
+    TPG_CK(cudaMallocAsync(&np, cap * es, s));
+    if (used && b.p) TPG_CK(cudaMemcpyAsync(np, b.p, used * es, cudaMemcpyDeviceToDevice, s));
+    if (b.p) TPG_CK(cudaFreeAsync(b.p, s));
+    b.p = np;
+    b.cap = cap * es;
+    return TPGEN_OK;
+}
+
+template <int W>
+static tpgen_status grow_queue(PlanImpl &P, uint64_t used, uint64_t cap, cudaStream_t s) {
+    if (cap <= P.qcap) return TPGEN_OK;
+    TPG_TRY(grow_keep(P.qunits, used, cap, sizeof(Unit<W>), s));
+    TPG_TRY(grow_keep(P.qready, used, cap, 4, s));
+    for (int c = 0; c < C_NUM; c++) TPG_TRY(grow_keep(P.qcnt[c], used, cap, 8, s));
+    TPG_TRY(grow_keep(P.qext, used, cap, 8, s));
+    TPG_TRY(grow_keep(P.qrfirst, used, cap, 8, s));
+    TPG_TRY(grow_keep(P.qrcount, used, cap, 8, s));
+    TPG_TRY(grow_keep(P.qcfirst, used, cap, 8, s));
+    TPG_TRY(grow_keep(P.qccount, used, cap, 4, s));
+    TPG_TRY(grow_keep(P.qgen, used, cap, 4, s));
+    P.qcap = cap;
+    return TPGEN_OK;
+}
+
+// Writes `roots` into the queue at slots [qbase, qbase + roots.size()).
+template <int W>
+static tpgen_status put_roots(PlanImpl &P, const std::vector<Unit<W>> &roots, uint64_t qbase, cudaStream_t s) {
+    const size_t n = roots.size();
+    if (!n) return TPGEN_OK;
+    TPG_CK(cudaMemcpyAsync(P.qunits.as<Unit<W>>() + qbase, roots.data(), n * sizeof(Unit<W>), cudaMemcpyHostToDevice,
+                           s));
+    std::vector<uint32_t> ones(n, 1u);
+    TPG_CK(cudaMemcpyAsync(P.qready.as<uint32_t>() + qbase, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemsetAsync(P.qgen.as<int32_t>() + qbase, 0, n * 4, s));
+    TPG_CK(cudaMemsetAsync(P.qccount.as<int32_t>() + qbase, 0, n * 4, s));
+    return TPGEN_OK;
+}
+
+// One phase of the persistent DFS (seg = SCC-entry starts, else prime-path
+// starts) over the roots already placed at [qbase, qbase + nroots).  Retried
+// with a larger record pool or queue if either overflows.  Returns the new tail.
 template <class T>
-static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, int seg, cudaStream_t s, tpgen_stats &st,
-                              int64_t &launches, double &ms_dfs) {
+static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<Unit<MT<T>::W>> &roots, int seg,
+                              uint64_t qbase, cudaStream_t s, tpgen_stats &st, int64_t &launches, double &ms_dfs,
+                              uint64_t &tail_out) {
     constexpr int W = MT<T>::W;
     Timer t;
-    const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
     const HostPlan &H = P.hp;
     const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
-    for (int round = 0; round < 4096; round++) {
-        const int cur = P.cur;
-        const int64_t n = P.n_units;
-        if (n == 0) return TPGEN_OK;
-        TPG_TRY(P.work.ensure((size_t)n * 8, s));
-        unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0]=nwork [1]=next [2]=ntrunc [3]=ovf [4]=chunk_next
-        TPG_CK(cudaMemsetAsync(ctr, 0, 8, s));
-        build_worklist_kernel<W><<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit<W>>(),
-                                                                     P.status[cur].as<uint8_t>(), n, seg,
-                                                                     P.work.as<int64_t>(), ctr + 0);
-        launches++;
-        unsigned long long hctr[5];
-        TPG_CK(cudaMemcpyAsync(hctr, ctr, 8, cudaMemcpyDeviceToHost, s));
-        TPG_CK(cudaStreamSynchronize(s));
-        const int64_t nwork = (int64_t)hctr[0];
-        if (nwork == 0) return TPGEN_OK;
-        if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
-        TPG_TRY(grow_pool(P, P.chunk_used + (uint64_t)nwork * 2 + 1024, s));
+    const uint64_t nroots = roots.size();
+    tail_out = qbase + nroots;
+    if (nroots == 0) return TPGEN_OK;
+    const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
+    TPG_TRY(grow_queue<W>(P, qbase, std::max<uint64_t>(qbase + nroots + 8 * (uint64_t)lanes, 1u << 21), s));
+    if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0..2] head/tail/done [3] ovf [4] chunk_next [5] maxgen
+    for (int attempt = 0; attempt < 32; attempt++) {
+        TPG_TRY(put_roots<W>(P, roots, qbase, s));
+        TPG_CK(cudaMemsetAsync(P.qready.as<uint32_t>() + qbase + nroots, 0, (P.qcap - qbase - nroots) * 4, s));
+        unsigned long long init[6] = {qbase, qbase + nroots, qbase, 0, P.chunk_used, (unsigned long long)P.maxgen};
+        TPG_CK(cudaMemcpyAsync(ctr, init, 6 * 8, cudaMemcpyHostToDevice, s));
         DfsArgs A;
         memset(&A, 0, sizeof(A));
         A.G = G;
-        A.units = P.units[cur].as<Unit<W>>();
-        A.n_units = n;
-        A.work = P.work.as<int64_t>();
-        A.n_work = ctr + 0;
-        A.next = ctr + 1;
-        for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.cnt[cur][c].as<uint64_t>();
-        A.ext = P.ext[cur].as<uint64_t>();
-        A.status = P.status[cur].as<uint8_t>();
-        A.rfirst = P.rfirst[cur].as<int64_t>();
-        A.rcount = P.rcount[cur].as<int64_t>();
-        A.stop = P.stop.as<Unit<W>>();
-        A.budget = choose_budget(nwork, lanes);
-        A.n_trunc = ctr + 2;
+        A.units = P.qunits.p;
+        A.ready = P.qready.as<unsigned int>();
+        A.q = ctr;
+        A.qcap = P.qcap;
+        for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.qcnt[c].as<uint64_t>();
+        A.ext = P.qext.as<uint64_t>();
+        A.rfirst = P.qrfirst.as<int64_t>();
+        A.rcount = P.qrcount.as<int64_t>();
+        A.child_first = P.qcfirst.as<int64_t>();
+        A.child_count = P.qccount.as<int32_t>();
+        A.gen = P.qgen.as<int32_t>();
+        A.maxgen = reinterpret_cast<int *>(ctr + 5);
         unsigned long long *agg = P.agg.as<unsigned long long>();
         A.agg_tail_cnt = agg;
         A.agg_tail_len = agg + H.n;
         A.agg_pair_cnt = agg + 2 * (int64_t)H.n;
         A.agg_pair_len = agg + 2 * (int64_t)H.n + H.n_pairs;
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 3);
+        A.chunks = P.chunks.as<uint64_t>();
         A.chunk_next = ctr + 4;
-        const int grid = grid_for(nwork, DfsCfg<W>::threads, P.num_sms * DfsCfg<W>::min_blocks);
-        while (true) {  // retried only if the record pool overflows
-            A.chunks = P.chunks.as<uint64_t>();
-            A.chunk_cap = P.chunk_cap;
-            unsigned long long init[4] = {0, 0, 0, P.chunk_used};
-            TPG_CK(cudaMemcpyAsync(ctr + 1, init, 4 * 8, cudaMemcpyHostToDevice, s));
-            cudaEventRecord(t.a, s);
-            dfs_kernel<T><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
-            cudaEventRecord(t.b, s);
-            launches++;
-            TPG_CK(cudaGetLastError());
-            TPG_CK(cudaMemcpyAsync(hctr, ctr, 5 * 8, cudaMemcpyDeviceToHost, s));
-            TPG_CK(cudaStreamSynchronize(s));
-            float ms = 0;
-            cudaEventElapsedTime(&ms, t.a, t.b);
-            ms_dfs += ms;
-            st.n_count_rounds++;
-            if (!((unsigned)hctr[3] & 2u)) break;
-            // record pool exhausted: undo the round and retry with a larger pool
-            reset_status_kernel<<<grid_for(nwork, 256, 4096), 256, 0, s>>>(P.work.as<int64_t>(), ctr + 0,
-                                                                           P.status[cur].as<uint8_t>());
-            launches++;
-            if (seg) TPG_CK(cudaMemcpyAsync(P.agg.p, P.agg_bak.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
-            TPG_TRY(grow_pool(P, std::max<uint64_t>(hctr[4], P.chunk_cap) * 2, s));
-        }
-        P.chunk_used = hctr[4];
-        if ((unsigned)hctr[3] & 1u) P.overflow = true;
-        if (hctr[2] == 0) return TPGEN_OK;
-        // ---- refine: truncated units -> walked piece + remainder units
-        TPG_TRY(P.rbuf.ensure((size_t)n * 8, s));
-        refine_count_kernel<W><<<grid_for(n, 256, 4096), 256, 0, s>>>(G, P.status[cur].as<uint8_t>(),
-                                                                       P.stop.as<Unit<W>>(), n,
-                                                                       P.rbuf.as<uint64_t>());
-        launches++;
-        uint64_t *arr[1] = {P.rbuf.as<uint64_t>()};
-        uint64_t total = 0;
-        TPG_TRY(scan_multi(P, arr, 1, n, &total, s, launches));
-        const int nx = cur ^ 1;
-        const int64_t nn = (int64_t)total;
-        TPG_TRY(P.units[nx].ensure((size_t)nn * sizeof(Unit<W>), s));
-        TPG_TRY(P.status[nx].ensure((size_t)nn, s));
-        TPG_TRY(P.ext[nx].ensure((size_t)nn * 8, s));
-        TPG_TRY(P.rfirst[nx].ensure((size_t)nn * 8, s));
-        TPG_TRY(P.rcount[nx].ensure((size_t)nn * 8, s));
-        for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[nx][c].ensure((size_t)nn * 8, s));
-        RefineBufs<W> B;
-        B.units = P.units[cur].as<Unit<W>>();
-        B.status = P.status[cur].as<uint8_t>();
-        B.stop = P.stop.as<Unit<W>>();
-        for (int c = 0; c < C_NUM; c++) {
-            B.cnt[c] = P.cnt[cur][c].as<uint64_t>();
-            B.ncnt[c] = P.cnt[nx][c].as<uint64_t>();
-        }
-        B.ext = P.ext[cur].as<uint64_t>();
-        B.rfirst = P.rfirst[cur].as<int64_t>();
-        B.rcount = P.rcount[cur].as<int64_t>();
-        B.nunits = P.units[nx].as<Unit<W>>();
-        B.nstatus = P.status[nx].as<uint8_t>();
-        B.next = P.ext[nx].as<uint64_t>();
-        B.nrfirst = P.rfirst[nx].as<int64_t>();
-        B.nrcount = P.rcount[nx].as<int64_t>();
-        refine_scatter_kernel<W><<<grid_for(n, 128, 8192), 128, 0, s>>>(G, B, n, P.rbuf.as<uint64_t>());
+        A.chunk_cap = P.chunk_cap;
+        A.split_min = P.split_min;
+        cudaEventRecord(t.a, s);
+        dfs_kernel<T><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, 0, s>>>(A);
+        cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
-        P.cur = nx;
-        P.n_units = nn;
-        TPG_TRY(P.stop.ensure((size_t)nn * sizeof(Unit<W>), s));
+        unsigned long long h[6];
+        TPG_CK(cudaMemcpyAsync(h, ctr, 6 * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        ms_dfs += ms;
+        st.n_count_rounds++;
+        const unsigned ovf = (unsigned)h[3];
+        if (ovf & 6u) {  // record pool or queue exhausted: undo and retry bigger
+            if (seg) TPG_CK(cudaMemcpyAsync(P.agg.p, P.agg_bak.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
+            if (ovf & 2u) TPG_TRY(grow_pool(P, std::max<uint64_t>(h[4], P.chunk_cap) * 2, s));
+            if (ovf & 4u) TPG_TRY(grow_queue<W>(P, qbase, P.qcap * 2, s));
+            continue;
+        }
+        if (ovf & 1u) P.overflow = true;
+        P.chunk_used = h[4];
+        P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
+        tail_out = h[1];
+        return TPGEN_OK;
     }
-    set_error("DFS phase did not converge");
-    return TPGEN_ERR_INTERNAL;
+    set_error("DFS phase: work queue / record pool could not be sized");
+    return TPGEN_ERR_OUT_OF_MEMORY;
 }
 
 template <class T>
@@ -466,19 +446,19 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     st.ms_plan = P.ms_plan;
     P.overflow = false;
     P.chunk_used = 0;
+    P.maxgen = 0;
 
     Timer tall, tw, tst;
     cudaEventRecord(tall.a, s);
     const DevGraph G = dev_graph(P, lo, hi);
 
-    // ---- roots: one K_NODE unit per start vertex, ascending global id
-    std::vector<Unit<W>> roots;
-    roots.reserve(H.n);
+    // ---- roots: one K_NODE unit per start vertex (segment phase: SCC entries; PP phase: the rest)
+    std::vector<Unit<W>> seg_roots, pp_roots;
+    std::vector<int32_t> seg_gid, pp_gid;
     for (int32_t v = 0; v < H.n; v++) {
         const int32_t slot = H.v_slot[v];
         const bool entry = (H.slot_flags[slot] & F_ENTRY) != 0;
-        const bool mine = v >= lo && v < hi;
-        if (!entry && !mine) continue;
+        if (!entry && !(v >= lo && v < hi)) continue;
         Unit<W> u;
         memset(&u, 0, sizeof(u));
         const int32_t c = H.comp[v];
@@ -488,33 +468,26 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         u.e = -1;
         u.kind = K_NODE;
         u.path[0] = (uint8_t)loc;
-        roots.push_back(u);
+        (entry ? seg_roots : pp_roots).push_back(u);
+        (entry ? seg_gid : pp_gid).push_back(v);
     }
-    P.cur = 0;
-    P.n_units = (int64_t)roots.size();
-    const size_t nr = std::max<size_t>(roots.size(), 1);
-    TPG_TRY(P.units[0].ensure(nr * sizeof(Unit<W>), s));
-    TPG_TRY(P.status[0].ensure(nr, s));
-    TPG_TRY(P.ext[0].ensure(nr * 8, s));
-    TPG_TRY(P.rfirst[0].ensure(nr * 8, s));
-    TPG_TRY(P.rcount[0].ensure(nr * 8, s));
-    for (int c = 0; c < C_NUM; c++) TPG_TRY(P.cnt[0][c].ensure(nr * 8, s));
-    TPG_TRY(P.stop.ensure(nr * sizeof(Unit<W>), s));
-    TPG_TRY(P.ctr.ensure(16 * 8, s));
-    if (!roots.empty()) {
-        TPG_CK(cudaMemcpyAsync(P.units[0].p, roots.data(), roots.size() * sizeof(Unit<W>), cudaMemcpyHostToDevice, s));
-        TPG_CK(cudaMemsetAsync(P.status[0].p, ST_PENDING, roots.size(), s));
-    }
+    TPG_TRY(P.ctr.ensure(32 * 8, s));
     const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
     TPG_TRY(P.agg.ensure(agg_n * 8, s));
     TPG_TRY(P.agg_bak.ensure(agg_n * 8, s));
     TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
-    TPG_TRY(grow_pool(P, std::max<uint64_t>((64ull << 20) / (kChunkRecs * 8), nr * 4), s));
+    {
+        double est = 0;  // Knuth estimates of the trie sizes -> initial record pool
+        for (int32_t v = 0; v < H.n; v++) est += P.hp.cost[v];
+        TPG_TRY(grow_pool(P, std::max<uint64_t>((64ull << 20) / (kChunkRecs * 8),
+                                                (uint64_t)(est * 0.75 / (kChunkRecs - 1)) + 4 * H.n), s));
+    }
 
     double ms_dfs = 0;
+    uint64_t tail_seg = 0, tail = 0;
     // ---- segment phase (SCC entries) -> completion DP
-    if (H.has_entries) {
-        TPG_TRY(dfs_phase<T>(P, G, 1, s, st, launches, ms_dfs));
+    if (!seg_roots.empty()) {
+        TPG_TRY(dfs_phase<T>(P, G, seg_roots, 1, 0, s, st, launches, ms_dfs, tail_seg));
         std::vector<uint64_t> aggh(agg_n);
         TPG_CK(cudaMemcpyAsync(aggh.data(), P.agg.p, agg_n * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
@@ -531,26 +504,70 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         TPG_CK(cudaMemcpyAsync(P.d_Wv.p, Vd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     }
     // ---- prime-path phase
-    TPG_TRY(dfs_phase<T>(P, G, 0, s, st, launches, ms_dfs));
+    TPG_TRY(dfs_phase<T>(P, G, pp_roots, 0, tail_seg, s, st, launches, ms_dfs, tail));
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
     }
-    const int cur = P.cur;
-    const int64_t nu = P.n_units;
+    const int64_t nu = (int64_t)tail;
     st.n_units = nu;
 
-    // ---- exact offsets: scan of the per-unit counts
-    const size_t nu1 = (size_t)std::max<int64_t>(nu, 1);
-    TPG_TRY(P.offs.ensure(nu1 * 8 * (C_NUM + 1), s));
-    uint64_t *off[C_NUM + 1];
-    for (int c = 0; c <= C_NUM; c++) {
-        off[c] = P.offs.as<uint64_t>() + (size_t)c * nu1;
-        const void *src = (c < C_NUM) ? P.cnt[cur][c].p : P.ext[cur].p;
-        if (nu) TPG_CK(cudaMemcpyAsync(off[c], src, (size_t)nu * 8, cudaMemcpyDeviceToDevice, s));
+    // ---- canonical order: roots by global id, then preorder of the split forest
+    std::vector<int64_t> root_order;
+    std::vector<int32_t> root_gid;
+    root_order.reserve(seg_roots.size() + pp_roots.size());
+    {
+        size_t a = 0, b = 0;
+        while (a < seg_gid.size() || b < pp_gid.size()) {
+            if (b >= pp_gid.size() || (a < seg_gid.size() && seg_gid[a] < pp_gid[b])) {
+                root_order.push_back((int64_t)a);
+                root_gid.push_back(seg_gid[a++]);
+            } else {
+                root_order.push_back((int64_t)(tail_seg + b));
+                root_gid.push_back(pp_gid[b++]);
+            }
+        }
     }
+    const int64_t n_roots = (int64_t)root_order.size();
+    const size_t nu1 = (size_t)std::max<int64_t>(nu, 1);
+    TPG_TRY(P.offs.ensure(nu1 * 8 * 2 * C_NUM + 64, s));
+    TPG_TRY(P.roots.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
+    if (n_roots) {
+        TPG_CK(cudaMemcpyAsync(P.roots.p, root_order.data(), n_roots * 8, cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemcpyAsync(P.roots.as<char>() + n_roots * 8, root_gid.data(), n_roots * 4, cudaMemcpyHostToDevice,
+                               s));
+    }
+    uint64_t *off[C_NUM], *sub[C_NUM];
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();
+    uint64_t *tot_d = reinterpret_cast<uint64_t *>(ctr + 8);
+    LinArgs LA;
+    for (int c = 0; c < C_NUM; c++) {
+        sub[c] = P.offs.as<uint64_t>() + (size_t)c * nu1;
+        off[c] = P.offs.as<uint64_t>() + (size_t)(C_NUM + c) * nu1;
+        LA.cnt[c] = P.qcnt[c].as<uint64_t>();
+        LA.sub[c] = sub[c];
+        LA.off[c] = off[c];
+    }
+    LA.child_first = P.qcfirst.as<int64_t>();
+    LA.child_count = P.qccount.as<int32_t>();
+    LA.gen = P.qgen.as<int32_t>();
+    LA.n = nu;
+    LA.roots = P.roots.as<int64_t>();
+    LA.n_roots = n_roots;
+    LA.totals = tot_d;
     uint64_t tot[C_NUM + 1] = {0};
-    TPG_TRY(scan_multi(P, off, C_NUM + 1, nu, tot, s, launches));
+    if (nu > 0) {
+        const int lg = grid_for(nu, 256, P.num_sms * 8);
+        for (int g = P.maxgen; g >= 0; g--) lin_up_kernel<<<lg, 256, 0, s>>>(LA, g);
+        lin_roots_kernel<<<1, kScanThreads, 0, s>>>(LA);
+        for (int g = 0; g <= P.maxgen; g++) lin_down_kernel<<<lg, 256, 0, s>>>(LA, g);
+        TPG_CK(cudaMemsetAsync(ctr + 14, 0, 8, s));
+        sum_kernel<<<lg, 256, 0, s>>>(P.qext.as<uint64_t>(), nu, ctr + 14);
+        launches += 2 * (P.maxgen + 1) + 2;
+        TPG_CK(cudaMemcpyAsync(tot, tot_d, C_NUM * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaMemcpyAsync(tot + C_NUM, ctr + 14, 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+    }
     const int64_t n_pp = (int64_t)tot[C_PP], n_vert = (int64_t)tot[C_VERT];
     st.n_extensions = (int64_t)tot[C_NUM];
     st.n_heads = (int64_t)tot[C_HEADS];
@@ -570,6 +587,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         st.ms_device = ms;
         st.ms_count = ms;
         st.ms_dfs_count = ms_dfs;
+        st.ms_dfs_write = ms_dfs;
         st.gpu_launches = launches;
         st.ms_total = now_ms() - t0;
         if (stp) *stp = st;
@@ -595,10 +613,10 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     ExpandArgs E;
     memset(&E, 0, sizeof(E));
     E.G = G;
-    E.units = P.units[cur].as<Unit<W>>();
+    E.units = P.qunits.p;
     E.n_units = nu;
-    E.rfirst = P.rfirst[cur].as<int64_t>();
-    E.rcount = P.rcount[cur].as<int64_t>();
+    E.rfirst = P.qrfirst.as<int64_t>();
+    E.rcount = P.qrcount.as<int64_t>();
     for (int c = 0; c < C_NUM; c++) E.off[c] = off[c];
     E.chunks = P.chunks.as<uint64_t>();
     E.out_off = (int64_t *)d_off;
@@ -638,9 +656,9 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             uint64_t *ia[2] = {P.icum.as<uint64_t>(), P.ivcum.as<uint64_t>()};
             TPG_TRY(scan_multi(P, ia, 2, n_items, nullptr, s, launches));
         }
-        item_bounds_kernel<W><<<grid_for(nu, 256, 4096), 256, 0, s>>>(G, P.units[cur].as<Unit<W>>(), nu, off[C_ITEMS],
-                                                                    tot[C_ITEMS], P.ibeg.as<int64_t>(),
-                                                                    P.iend.as<int64_t>());
+        item_bounds_kernel<<<grid_for(n_roots, 256, 4096), 256, 0, s>>>(
+            P.roots.as<int64_t>(), reinterpret_cast<const int32_t *>(P.roots.as<char>() + n_roots * 8), n_roots,
+            off[C_ITEMS], sub[C_ITEMS], P.ibeg.as<int64_t>(), P.iend.as<int64_t>());
         launches++;
         StitchArgs SA;
         SA.heads = P.heads.as<HeadRec>();
@@ -667,9 +685,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventRecord(tall.b, s);
     TPG_CK(cudaGetLastError());
 
-    unsigned long long *ctr = P.ctr.as<unsigned long long>();
     if (o.compute_digest && n_pp > 0) {
-        unsigned long long *acc = ctr + 8;
+        unsigned long long *acc = ctr + 16;
         TPG_CK(cudaMemsetAsync(acc, 0, 16, s));
         digest_kernel<<<grid_for(n_pp, 256, P.num_sms * 8), 256, 0, s>>>((int64_t *)d_off, (int32_t *)d_vert, n_pp,
                                                                            acc);
@@ -689,8 +706,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventElapsedTime(&ms, tst.a, tst.b);
     st.ms_stitch = ms;
     st.ms_count = st.ms_device - st.ms_write - st.ms_stitch;
-    st.ms_dfs_count = ms_dfs;   // DFS kernel time (all rounds)
-    st.ms_dfs_write = ms_dfs;   // the dominant kernel is the DFS enumerator
+    st.ms_dfs_count = ms_dfs;  // DFS kernel time (both phases)
+    st.ms_dfs_write = ms_dfs;  // the dominant kernel is the DFS enumerator
     st.gpu_launches = launches;
 
     ow_guard.release();

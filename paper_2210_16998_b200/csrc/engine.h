@@ -33,15 +33,15 @@ struct PlanImpl {
     // device tables
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
         d_slot_eidx, d_Wc, d_Wv, d_scc_gbase;
-    // workspace (double-buffered unit arrays for refinement)
-    DevBuf units[2], status[2], ext[2], rfirst[2], rcount[2], cnt[2][kCnt];
-    DevBuf chunks, agg_bak;      // path-delta record pool (chunks of kChunkRecs words); aggregate backup
-    uint64_t chunk_cap = 0;      // pool capacity in chunks
-    uint64_t chunk_used = 0;     // chunks handed out so far in this call
-    DevBuf stop, work, rbuf, scan_b, scan_tot, ctr, agg, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend,
-        hcomp, offs, tp_tabs;
-    int cur = 0;
-    int64_t n_units = 0;
+    // DFS work queue (one slot per unit) and its per-unit results
+    DevBuf qunits, qready, qcnt[kCnt], qext, qrfirst, qrcount, qcfirst, qccount, qgen, roots;
+    uint64_t qcap = 0;
+    DevBuf chunks, agg, agg_bak;  // path-delta record pool (chunks of kChunkRecs words); SEG aggregates + backup
+    uint64_t chunk_cap = 0;       // pool capacity in chunks
+    uint64_t chunk_used = 0;      // chunks handed out so far in this call
+    int maxgen = 0;               // deepest split generation so far in this call
+    uint32_t split_min = 256;     // steps before a unit may be split
+    DevBuf scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     bool overflow = false;
     ~PlanImpl();
     std::vector<DevBuf *> all_bufs();

@@ -105,8 +105,7 @@ struct __align__(16) Slot {
 
 // A work unit: a trie node (K_NODE: the whole subtree under it), or one
 // terminal event of a trie node (K_CLOSURE: the cycle path(+)s, K_OUT: the arc
-// to an out-of-SCC successor).  Stop states of truncated units use the same
-// record (k, o, rdepth).
+// to an out-of-SCC successor).
 template <int W>
 struct __align__(16) Unit {
     uint8_t path[64 * W];  // local vertex ids, path[0..depth]
@@ -137,26 +136,26 @@ struct DevGraph {
 
 struct DfsArgs {
     DevGraph G;
-    const void *units;  // Unit<W>[n_units]
-    int64_t n_units;
-    const int64_t *work;  // indices of the units to process
-    const unsigned long long *n_work;
-    unsigned long long *next;  // grab counter (zeroed before launch)
-    // per-unit results
+    void *units;              // Unit<W>[qcap]: the work queue (roots pre-filled by the host)
+    unsigned int *ready;      // per queue slot: 1 once the unit record is written
+    unsigned long long *q;    // [0] head (claims), [1] tail (pushed), [2] done (finished)
+    unsigned long long qcap;  // queue capacity (slots)
+    // per-unit results, indexed by queue slot
     uint64_t *cnt[C_NUM];
     uint64_t *ext;
-    uint8_t *status;
-    int64_t *rfirst;  // first record chunk of the unit
-    int64_t *rcount;  // records of the unit
-    void *stop;       // Unit<W>[n_units]: stop states of truncated units
-    uint32_t budget;
-    unsigned long long *n_trunc;
+    int64_t *rfirst;          // first record chunk of the unit
+    int64_t *rcount;          // records of the unit
+    int64_t *child_first;     // split units: first remainder unit
+    int32_t *child_count;     // split units: number of remainder units (0 otherwise)
+    int32_t *gen;             // split generation (roots 0)
+    int *maxgen;
     unsigned long long *agg_tail_cnt, *agg_tail_len, *agg_pair_cnt, *agg_pair_len;
-    unsigned int *overflow;  // bit 0: count overflow, bit 1: record pool exhausted
+    unsigned int *overflow;   // bit 0: count overflow, bit 1: record pool exhausted, bit 2: queue full
     // record pool
     uint64_t *chunks;
     unsigned long long *chunk_next;
     unsigned long long chunk_cap;
+    uint32_t split_min;       // steps a unit runs before it may be split
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
@@ -220,83 +219,6 @@ __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b, unsigned int
         return (1ull << 62);
     }
     return lo;
-}
-
-// ------------------------------------------------------------- refinement
-// Remainder of a truncated unit: the untried events of every node on its stop
-// stack, deepest level first (lexicographic order of the rest of the walk).
-template <int W, bool WRITE>
-__device__ int remainder_events(const DevGraph &G, const Unit<W> &S, Unit<W> *out) {
-    const int vb = __ldg(G.scc_vbase + S.scc);
-    const int s = S.path[0];
-    const Mask<W> sbit = mbit<W>(s);
-    const Slot<W> *ss = slot_ptr<W>(G, vb + s);
-    const bool seg = (__ldg(&ss->flags) & F_ENTRY) != 0;
-    const Mask<W> ps = ld_pin(ss);
-    Mask<W> M;
-#pragma unroll
-    for (int i = 0; i < W; i++) M.w[i] = S.M[i];
-    int n = 0;
-    for (int j = S.depth; j >= (int)S.rdepth; j--) {
-        const int u = S.path[j];
-        const Slot<W> *su = slot_ptr<W>(G, vb + u);
-        const int4 meta = ld_meta(su);
-        const Mask<W> sin = ld_sin(su);
-        int k, o;
-        if (j == S.depth) {
-            k = S.k;
-            o = S.o;
-        } else {
-            const int wc = S.path[j + 1];
-            mclr(M, wc);
-            k = wc + 1;
-            o = count_out_le(G, meta.y, meta.z, wc);
-        }
-        while (true) {
-            const int w = mnext(sin, M, sbit, k);
-            if (o < meta.z && __ldg(G.out_pos + meta.y + o) <= w) {
-                const int e = meta.y + o;
-                o++;
-                if (seg || msubset(ps, M)) {
-                    if (WRITE) {
-                        Unit<W> &U = out[n];
-                        U = S;
-#pragma unroll
-                        for (int i = 0; i < W; i++) U.M[i] = M.w[i];
-                        U.e = e;
-                        U.nsteps = 0;
-                        U.depth = (uint8_t)j;
-                        U.kind = K_OUT;
-                        U.k = U.o = U.rdepth = 0;
-                    }
-                    n++;
-                }
-                continue;
-            }
-            if (w >= 64 * W) break;
-            k = w + 1;
-            if (WRITE) {
-                Unit<W> &U = out[n];
-                U = S;
-                U.nsteps = 0;
-                U.k = U.o = U.rdepth = 0;
-                U.e = -1;
-#pragma unroll
-                for (int i = 0; i < W; i++) U.M[i] = M.w[i];
-                if (w == s) {
-                    U.depth = (uint8_t)j;
-                    U.kind = K_CLOSURE;
-                } else {
-                    U.M[w >> 6] |= 1ull << (w & 63);
-                    U.depth = (uint8_t)(j + 1);
-                    U.path[j + 1] = (uint8_t)w;
-                    U.kind = K_NODE;
-                }
-            }
-            n++;
-        }
-    }
-    return n;
 }
 
 }  // namespace tpg
