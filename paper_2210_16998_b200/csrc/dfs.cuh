@@ -341,12 +341,12 @@ __device__ int lane_remainder(const DevGraph &G, const Lane<T> &L, uint32_t mp, 
     return n;
 }
 
-// Persistent DFS kernel with an in-kernel work queue.  Idle lanes claim queue
-// slots (warp-aggregated atomic on the head) and wait for them to be filled;
-// a running lane whose unit has taken at least split_min steps splits it when
-// claims outrun the queue tail (some lane is starving): its walk so far becomes
-// a finished piece and the untried siblings on its stack are pushed as new
-// units (children of the piece in the unit tree).  The kernel ends when every
+// Persistent DFS kernel with an in-kernel work queue.  Idle lanes claim the
+// units that are queued (warp-aggregated atomic on the head); a running lane
+// whose unit has taken at least split_min steps splits it when the backlog of
+// queued, unclaimed units falls below low_water: its walk so far becomes a
+// finished piece and the untried siblings on its stack are pushed as new units
+// (children of the piece in the unit forest).  The kernel ends when every
 // pushed unit has finished (done == tail).
 template <class T>
 __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
@@ -377,19 +377,40 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
 #pragma unroll
     for (int i = 0; i < C_NUM; i++) c[i] = 0;
 
+    int backoff = 0;  // idle lanes poll the queue every few iterations
     while (true) {
         int ev = 0, e = -1;
         bool fresh = false;
-        // ---------------- idle lanes claim a queue slot (warp-aggregated)
-        const unsigned need = __ballot_sync(kFull, !L.active && !waiting && !exited);
+        // ---------------- idle lanes claim queued units (warp-aggregated, only what is available)
+        if (backoff > 0) backoff--;
+        const unsigned need = __ballot_sync(kFull, !L.active && !waiting && !exited && backoff == 0);
         if (need) {
             const int leader = __ffs(need) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(A.q + 0, (unsigned long long)__popc(need));
+            long long base = -1, k = 0;
+            int fin = 0;
+            if (lane == leader) {
+                const unsigned long long dn = ld_volatile(A.q + 2);
+                __threadfence();
+                const unsigned long long tl = ld_volatile(A.q + 1);
+                const unsigned long long hd = ld_volatile(A.q + 0);
+                const long long avail = (long long)tl - (long long)hd;
+                k = min((long long)__popc(need), avail);
+                if (k > 0) base = (long long)atomicAdd(A.q + 0, (unsigned long long)k);
+                fin = (dn == tl) || ((*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u) != 0u);
+            }
             base = __shfl_sync(kFull, base, leader);
-            if (!L.active && !waiting && !exited) {
-                slot = (int64_t)base + __popc(need & ((1u << lane) - 1));
-                waiting = true;
+            k = __shfl_sync(kFull, k, leader);
+            fin = __shfl_sync(kFull, fin, leader);
+            if (!L.active && !waiting && !exited && backoff == 0) {
+                const int rank = __popc(need & ((1u << lane) - 1));
+                if (rank < k) {
+                    slot = base + rank;  // may lie beyond the tail if another warp raced us: wait for it
+                    waiting = true;
+                } else if (fin) {
+                    exited = true;
+                } else {
+                    backoff = 8;
+                }
             }
         }
         // ---------------- waiting lanes: start the unit once written, or stop when all work is done
@@ -536,7 +557,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
 
         // ---------------- split on demand: some lane is starving and this unit has run long enough
         if (L.active && !L.done && L.steps >= A.split_min && (L.steps & 31u) == 0u) {
-            if (ld_volatile(A.q + 0) > ld_volatile(A.q + 1)) {
+            // backlog of queued, unclaimed units below the low-water mark: feed the queue
+            if ((long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water) {
                 const int m = lane_remainder<T, false>(G, L, mp, uscc, nullptr);
                 if (m > 0) {
                     const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m);

@@ -393,6 +393,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.chunk_next = ctr + 4;
         A.chunk_cap = P.chunk_cap;
         A.split_min = P.split_min;
+        A.low_water = (uint32_t)std::max<int64_t>(64, lanes / 8);
         cudaEventRecord(t.a, s);
         dfs_kernel<T><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, 0, s>>>(A);
         cudaEventRecord(t.b, s);

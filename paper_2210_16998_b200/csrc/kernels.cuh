@@ -156,6 +156,7 @@ struct DfsArgs {
     unsigned long long *chunk_next;
     unsigned long long chunk_cap;
     uint32_t split_min;       // steps a unit runs before it may be split
+    uint32_t low_water;       // split when fewer queued units than this are waiting to be claimed
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)

@@ -83,7 +83,7 @@ def test_config4_loop_chain():
 def test_dense_scc_medium(n, d, seed):
     """Dense SCCs big enough to force truncation/refinement rounds."""
     st = _assert_same(gen.dense_scc(n, d, seed))
-    assert st["n_count_rounds"] >= 2
+    assert st["n_units"] >= 2  # the work was split across lanes
 
 
 def test_cycle_64_and_limit():
