@@ -106,8 +106,8 @@ struct MT<Mask<WW>> {
 
 // ---------------------------------------------------------------- records
 // 64-bit path-delta record:
-//   bits 0-2 type, bit 3 closure flag, bits 4-11 c (truncate the path to c
-//   vertices), bits 12-14 n (number of appended vertices, <= 5),
+//   bits 0-2 type, bit 3 closure flag, bits 4-12 c (truncate the path to c
+//   vertices), bits 13-15 n (number of appended vertices, <= 5),
 //   bits 16-55 the n appended local vertex ids (one byte each).
 // R_ARG carries the out-arc index of the preceding HEAD / TRANSIT in bits 32-63.
 enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAIL, R_TRANSIT = EV_TRANSIT, R_ARG = 6 };
@@ -247,7 +247,7 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, Lan
     // record-stream bookkeeping: pending bytes follow pushes and pops
     if (push) {
         if (L.pn == kRecBytes) {  // flush a continuation record
-            rec_put(A, R, (uint64_t)R_PATH | ((uint64_t)L.base << 4) | ((uint64_t)kRecBytes << 12) |
+            rec_put(A, R, (uint64_t)R_PATH | ((uint64_t)L.base << 4) | ((uint64_t)kRecBytes << 13) |
                               (L.pend << 16));
             L.base += kRecBytes;
             L.pn = 0;
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     for (int i = 0; i < C_NUM; i++) c[i] = 0;
 
     int backoff = 0;  // idle lanes poll the queue every few iterations
+    uint32_t iter = 0;
     while (true) {
         int ev = 0, e = -1;
         bool fresh = false;
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 } else if (fin) {
                     exited = true;
                 } else {
-                    backoff = 8;
+                    backoff = 16;
                 }
             }
         }
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             const uint64_t len = (uint64_t)ev_len(ev);
             // HEAD / TRANSIT carry their out-arc in an R_ARG record written just before them
             if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
-            rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 12) |
+            rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 13) |
                               (L.pend << 16));
             L.base += L.pn;
             L.pn = 0;
@@ -556,9 +557,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         }
 
         // ---------------- split on demand: some lane is starving and this unit has run long enough
-        if (L.active && !L.done && L.steps >= A.split_min && (L.steps & 31u) == 0u) {
+        // (one lane per warp samples the queue every 64 iterations: the counters are a hot line)
+        bool feed = false;
+        if (((++iter) & 63u) == 0u) {
+            int f = 0;
+            if (lane == 0)
+                f = (long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water;
+            feed = __shfl_sync(kFull, f, 0) != 0;
+        }
+        if (feed && L.active && !L.done && L.steps >= A.split_min) {
             // backlog of queued, unclaimed units below the low-water mark: feed the queue
-            if ((long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water) {
+            {
                 const int m = lane_remainder<T, false>(G, L, mp, uscc, nullptr);
                 if (m > 0) {
                     const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m);

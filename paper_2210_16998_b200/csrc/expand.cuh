@@ -39,7 +39,7 @@ __device__ __forceinline__ void st_global_cs(int32_t *p, int v) {
 
 template <int W>
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
-    constexpr int NP = 2 * W;  // path registers per lane (64*W positions / 32 lanes)
+    constexpr int NP = 2 * W + 1;  // path registers per lane (64*W positions + the closing vertex)
     const int lane = threadIdx.x & 31;
     const DevGraph &G = A.G;
     const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
                     arg = (int)(rec >> 32);
                     continue;
                 }
-                const int cc = (int)((rec >> 4) & 0xff);
-                const int n = (int)((rec >> 12) & 7);
+                const int cc = (int)((rec >> 4) & 0x1ff);
+                const int n = (int)((rec >> 13) & 7);
 #pragma unroll
                 for (int r = 0; r < NP; r++) {
                     const int d = lane + 32 * r - cc;
