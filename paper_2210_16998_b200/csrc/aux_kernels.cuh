@@ -99,17 +99,20 @@ __global__ void scan_down_kernel(ScanArrays S, int64_t n, const uint64_t *bsum, 
 
 // ---------------------------------------------------------- linearization
 // The units form a forest: roots are the start vertices (canonical order =
-// ascending global id), and a split unit's children are its remainder units,
-// which follow it in lexicographic order.  Canonical output order is the
-// preorder of that forest, so each unit's output offsets are obtained by a
-// bottom-up pass (subtree totals, generation by generation) and a top-down pass
-// (children placed after their parent, in order).
+// ascending global id), and a unit's children are the units it donated, which
+// follow all of its own output in lexicographic order -- blocks donated later
+// come from deeper levels and so come first (the block list is newest-first).
+// Canonical output order is the preorder of that forest, so each unit's output
+// offsets are obtained by a bottom-up pass (subtree totals, generation by
+// generation) and a top-down pass (children placed after their parent).
 struct LinArgs {
     const uint64_t *cnt[C_NUM];  // own counts
     uint64_t *sub[C_NUM];        // subtree totals
     uint64_t *off[C_NUM];        // exclusive offsets in canonical order
-    const int64_t *child_first;
-    const int32_t *child_count;
+    const int64_t *child_head;
+    const int64_t *blk_first;
+    const int32_t *blk_count;
+    const int64_t *blk_next;
     const int32_t *gen;
     int64_t n;
     const int64_t *roots;        // root units in canonical order
@@ -120,14 +123,19 @@ struct LinArgs {
 __global__ void lin_up_kernel(LinArgs A, int g) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
         if (A.gen[i] != g) continue;
-        const int32_t cc = A.child_count[i];
-        const int64_t cf = A.child_first[i];
+        uint64_t s[C_NUM];
 #pragma unroll
-        for (int c = 0; c < C_NUM; c++) {
-            uint64_t s = A.cnt[c][i];
-            for (int32_t k = 0; k < cc; k++) s += A.sub[c][cf + k];
-            A.sub[c][i] = s;
+        for (int c = 0; c < C_NUM; c++) s[c] = A.cnt[c][i];
+        for (int64_t b = A.child_head[i]; b >= 0; b = A.blk_next[b]) {
+            const int64_t cf = A.blk_first[b];
+            const int32_t cc = A.blk_count[b];
+            for (int32_t k = 0; k < cc; k++) {
+#pragma unroll
+                for (int c = 0; c < C_NUM; c++) s[c] += A.sub[c][cf + k];
+            }
         }
+#pragma unroll
+        for (int c = 0; c < C_NUM; c++) A.sub[c][i] = s[c];
     }
 }
 
@@ -150,16 +158,19 @@ __global__ void lin_roots_kernel(LinArgs A) {
 
 __global__ void lin_down_kernel(LinArgs A, int g) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (A.gen[i] != g) continue;
-        const int32_t cc = A.child_count[i];
-        if (cc == 0) continue;
-        const int64_t cf = A.child_first[i];
+        if (A.gen[i] != g || A.child_head[i] < 0) continue;
+        uint64_t base[C_NUM];
 #pragma unroll
-        for (int c = 0; c < C_NUM; c++) {
-            uint64_t base = A.off[c][i] + A.cnt[c][i];
+        for (int c = 0; c < C_NUM; c++) base[c] = A.off[c][i] + A.cnt[c][i];
+        for (int64_t b = A.child_head[i]; b >= 0; b = A.blk_next[b]) {
+            const int64_t cf = A.blk_first[b];
+            const int32_t cc = A.blk_count[b];
             for (int32_t k = 0; k < cc; k++) {
-                A.off[c][cf + k] = base;
-                base += A.sub[c][cf + k];
+#pragma unroll
+                for (int c = 0; c < C_NUM; c++) {
+                    A.off[c][cf + k] = base[c];
+                    base[c] += A.sub[c][cf + k];
+                }
             }
         }
     }

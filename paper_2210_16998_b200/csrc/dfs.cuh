@@ -285,15 +285,19 @@ __device__ __forceinline__ int lds_u32(uint32_t a) {
     return v;
 }
 
-// Remainder of a running unit: the untried events of every node on the lane's
-// stack, deepest level first -- exactly the rest of the walk, in lexicographic
-// order.  Pass WRITE=false counts them, WRITE=true writes them as units.
+// Donation: the untried events (children in ascending global id) of the
+// shallowest node on the lane's stack that still has any -- the largest
+// subtrees left in the unit.  WRITE=false finds that level (j0) and counts the
+// events; WRITE=true writes them as units.  The lane keeps everything below
+// level j0 and stops when its walk returns to depth j0+1, so its remaining
+// output precedes the donated units in lexicographic order.
 template <class T, bool WRITE>
-__device__ int lane_remainder(const DevGraph &G, const Lane<T> &L, uint32_t mp, int uscc, Unit<MT<T>::W> *out) {
+__device__ int lane_donate(const DevGraph &G, const Lane<T> &L, uint32_t mp, int uscc, int &j0,
+                           Unit<MT<T>::W> *out) {
     using O = MT<T>;
     constexpr int W = O::W;
     T M = L.M;
-    int n = 0;
+    int best = 0;
     for (int j = L.l; j >= L.r; j--) {
         const int u = lds_u8(mp + pidx(j));
         const Slot<W> *su = slot_ptr<W>(G, L.vb + u);
@@ -309,6 +313,8 @@ __device__ int lane_remainder(const DevGraph &G, const Lane<T> &L, uint32_t mp, 
             k = wc + 1;
             o = count_out_le(G, meta.y, meta.z, wc);
         }
+        if (WRITE && j != j0) continue;
+        int n = 0;
         while (true) {
             const int w = O::next(sin, M, L.sbit, k);
             int kind = -1, e = -1;
@@ -337,8 +343,13 @@ __device__ int lane_remainder(const DevGraph &G, const Lane<T> &L, uint32_t mp, 
             }
             n++;
         }
+        if (WRITE) return n;
+        if (n > 0) {
+            best = n;
+            j0 = j;
+        }
     }
-    return n;
+    return best;
 }
 
 // Persistent DFS kernel with an in-kernel work queue.  Idle lanes claim the
@@ -377,6 +388,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
 #pragma unroll
     for (int i = 0; i < C_NUM; i++) c[i] = 0;
 
+    int64_t child_head = -1;  // latest donated block of the running unit
+    uint32_t last_split = 0;
     int backoff = 0;  // idle lanes poll the queue every few iterations
     uint32_t iter = 0;
     while (true) {
@@ -390,14 +403,16 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             long long base = -1, k = 0;
             int fin = 0;
             if (lane == leader) {
-                const unsigned long long dn = ld_volatile(A.q + 2);
-                __threadfence();
-                const unsigned long long tl = ld_volatile(A.q + 1);
-                const unsigned long long hd = ld_volatile(A.q + 0);
-                const long long avail = (long long)tl - (long long)hd;
+                const long long avail = (long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0);
                 k = min((long long)__popc(need), avail);
-                if (k > 0) base = (long long)atomicAdd(A.q + 0, (unsigned long long)k);
-                fin = (dn == tl) || ((*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u) != 0u);
+                if (k > 0) {
+                    base = (long long)atomicAdd(A.q + 0, (unsigned long long)k);
+                } else {  // nothing queued: has every pushed unit finished?
+                    const unsigned long long dn = ld_volatile(A.q + 2);
+                    __threadfence();
+                    const unsigned long long tl = ld_volatile(A.q + 1);
+                    fin = (dn == tl) || ((*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u) != 0u);
+                }
             }
             base = __shfl_sync(kFull, base, leader);
             k = __shfl_sync(kFull, k, leader);
@@ -461,6 +476,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 L.steps = 0;
                 L.done = false;
                 L.active = true;
+                child_head = -1;
+                last_split = 0;
                 L.base = depth + 1;
                 L.pn = 0;
                 L.pend = 0;
@@ -556,8 +573,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             }
         }
 
-        // ---------------- split on demand: some lane is starving and this unit has run long enough
-        // (one lane per warp samples the queue every 64 iterations: the counters are a hot line)
+        // ---------------- donate on demand (one lane per warp samples the queue every 64 iterations)
         bool feed = false;
         if (((++iter) & 63u) == 0u) {
             int f = 0;
@@ -565,28 +581,32 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 f = (long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water;
             feed = __shfl_sync(kFull, f, 0) != 0;
         }
-        if (feed && L.active && !L.done && L.steps >= A.split_min) {
-            // backlog of queued, unclaimed units below the low-water mark: feed the queue
-            {
-                const int m = lane_remainder<T, false>(G, L, mp, uscc, nullptr);
-                if (m > 0) {
-                    const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m);
-                    if (base + m > A.qcap) {
-                        atomicOr(A.overflow, 4u);
-                    } else {
-                        lane_remainder<T, true>(G, L, mp, uscc, units + base);
-                        for (int i = 0; i < m; i++) {
-                            A.gen[base + i] = ugen + 1;
-                            A.child_count[base + i] = 0;
-                        }
-                        A.child_first[slot] = (int64_t)base;
-                        A.child_count[slot] = m;
-                        atomicMax(A.maxgen, ugen + 1);
-                        __threadfence();
-                        for (int i = 0; i < m; i++) atomicExch(A.ready + base + i, 1u);
+        if (feed && L.active && !L.done && L.steps - last_split >= A.split_min) {
+            // backlog of queued, unclaimed units below the low-water mark: donate the shallowest siblings
+            int j0 = -1;
+            const int m = lane_donate<T, false>(G, L, mp, uscc, j0, nullptr);
+            if (m > 0) {
+                const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m);
+                const unsigned long long b = atomicAdd(A.blk_ctr, 1ull);
+                if (base + m > A.qcap || b >= A.qcap) {
+                    atomicOr(A.overflow, 4u);
+                } else {
+                    lane_donate<T, true>(G, L, mp, uscc, j0, units + base);
+                    for (int i = 0; i < m; i++) {
+                        A.gen[base + i] = ugen + 1;
+                        A.child_head[base + i] = -1;
                     }
+                    A.blk_first[b] = (int64_t)base;
+                    A.blk_count[b] = m;
+                    A.blk_next[b] = child_head;
+                    child_head = (int64_t)b;
+                    atomicMax(A.maxgen, ugen + 1);
+                    __threadfence();
+                    for (int i = 0; i < m; i++) atomicExch(A.ready + base + i, 1u);
+                    if (j0 == L.l) L.done = true;  // nothing left below the donated level
+                    else L.r = j0 + 1;             // the walk now ends when it returns to depth j0+1
+                    last_split = L.steps;
                 }
-                L.done = true;  // the walked part is a finished piece
             }
         }
 
@@ -597,6 +617,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             A.ext[slot] = ext;
             A.rfirst[slot] = R.first;
             A.rcount[slot] = R.count;
+            A.child_head[slot] = child_head;
             __threadfence();
             atomicAdd(A.q + 2, 1ull);
             L.active = false;

@@ -83,7 +83,7 @@ PlanImpl::~PlanImpl() {
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
-                               &qunits, &qready, &qext, &qrfirst, &qrcount, &qcfirst, &qccount, &qgen, &roots,
+                               &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
@@ -324,8 +324,10 @@ static tpgen_status grow_queue(PlanImpl &P, uint64_t used, uint64_t cap, cudaStr
     TPG_TRY(grow_keep(P.qext, used, cap, 8, s));
     TPG_TRY(grow_keep(P.qrfirst, used, cap, 8, s));
     TPG_TRY(grow_keep(P.qrcount, used, cap, 8, s));
-    TPG_TRY(grow_keep(P.qcfirst, used, cap, 8, s));
-    TPG_TRY(grow_keep(P.qccount, used, cap, 4, s));
+    TPG_TRY(grow_keep(P.qchead, used, cap, 8, s));
+    TPG_TRY(grow_keep(P.blk_first, P.blk_used, cap, 8, s));
+    TPG_TRY(grow_keep(P.blk_count, P.blk_used, cap, 4, s));
+    TPG_TRY(grow_keep(P.blk_next, P.blk_used, cap, 8, s));
     TPG_TRY(grow_keep(P.qgen, used, cap, 4, s));
     P.qcap = cap;
     return TPGEN_OK;
@@ -341,7 +343,7 @@ static tpgen_status put_roots(PlanImpl &P, const std::vector<Unit<W>> &roots, ui
     std::vector<uint32_t> ones(n, 1u);
     TPG_CK(cudaMemcpyAsync(P.qready.as<uint32_t>() + qbase, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
     TPG_CK(cudaMemsetAsync(P.qgen.as<int32_t>() + qbase, 0, n * 4, s));
-    TPG_CK(cudaMemsetAsync(P.qccount.as<int32_t>() + qbase, 0, n * 4, s));
+    TPG_CK(cudaMemsetAsync(P.qchead.as<int64_t>() + qbase, 0xff, n * 8, s));  // -1: no donated block
     return TPGEN_OK;
 }
 
@@ -366,8 +368,9 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
     for (int attempt = 0; attempt < 32; attempt++) {
         TPG_TRY(put_roots<W>(P, roots, qbase, s));
         TPG_CK(cudaMemsetAsync(P.qready.as<uint32_t>() + qbase + nroots, 0, (P.qcap - qbase - nroots) * 4, s));
-        unsigned long long init[6] = {qbase, qbase + nroots, qbase, 0, P.chunk_used, (unsigned long long)P.maxgen};
-        TPG_CK(cudaMemcpyAsync(ctr, init, 6 * 8, cudaMemcpyHostToDevice, s));
+        unsigned long long init[7] = {qbase, qbase + nroots, qbase, 0, P.chunk_used, (unsigned long long)P.maxgen,
+                                      P.blk_used};
+        TPG_CK(cudaMemcpyAsync(ctr, init, 7 * 8, cudaMemcpyHostToDevice, s));
         DfsArgs A;
         memset(&A, 0, sizeof(A));
         A.G = G;
@@ -379,8 +382,11 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.ext = P.qext.as<uint64_t>();
         A.rfirst = P.qrfirst.as<int64_t>();
         A.rcount = P.qrcount.as<int64_t>();
-        A.child_first = P.qcfirst.as<int64_t>();
-        A.child_count = P.qccount.as<int32_t>();
+        A.child_head = P.qchead.as<int64_t>();
+        A.blk_first = P.blk_first.as<int64_t>();
+        A.blk_count = P.blk_count.as<int32_t>();
+        A.blk_next = P.blk_next.as<int64_t>();
+        A.blk_ctr = ctr + 6;
         A.gen = P.qgen.as<int32_t>();
         A.maxgen = reinterpret_cast<int *>(ctr + 5);
         unsigned long long *agg = P.agg.as<unsigned long long>();
@@ -399,8 +405,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
-        unsigned long long h[6];
-        TPG_CK(cudaMemcpyAsync(h, ctr, 6 * 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long h[7];
+        TPG_CK(cudaMemcpyAsync(h, ctr, 7 * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
         float ms = 0;
         cudaEventElapsedTime(&ms, t.a, t.b);
@@ -416,6 +422,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         if (ovf & 1u) P.overflow = true;
         P.chunk_used = h[4];
         P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
+        P.blk_used = h[6];
         tail_out = h[1];
         return TPGEN_OK;
     }
@@ -448,6 +455,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     P.overflow = false;
     P.chunk_used = 0;
     P.maxgen = 0;
+    P.blk_used = 0;
 
     Timer tall, tw, tst;
     cudaEventRecord(tall.a, s);
@@ -549,8 +557,10 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         LA.sub[c] = sub[c];
         LA.off[c] = off[c];
     }
-    LA.child_first = P.qcfirst.as<int64_t>();
-    LA.child_count = P.qccount.as<int32_t>();
+    LA.child_head = P.qchead.as<int64_t>();
+    LA.blk_first = P.blk_first.as<int64_t>();
+    LA.blk_count = P.blk_count.as<int32_t>();
+    LA.blk_next = P.blk_next.as<int64_t>();
     LA.gen = P.qgen.as<int32_t>();
     LA.n = nu;
     LA.roots = P.roots.as<int64_t>();

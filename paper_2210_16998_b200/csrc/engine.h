@@ -34,8 +34,10 @@ struct PlanImpl {
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
         d_slot_eidx, d_Wc, d_Wv, d_scc_gbase;
     // DFS work queue (one slot per unit) and its per-unit results
-    DevBuf qunits, qready, qcnt[kCnt], qext, qrfirst, qrcount, qcfirst, qccount, qgen, roots;
+    DevBuf qunits, qready, qcnt[kCnt], qext, qrfirst, qrcount, qchead, qgen, roots;
+    DevBuf blk_first, blk_count, blk_next;  // donated blocks (one per donation)
     uint64_t qcap = 0;
+    uint64_t blk_used = 0;
     DevBuf chunks, agg, agg_bak;  // path-delta record pool (chunks of kChunkRecs words); SEG aggregates + backup
     uint64_t chunk_cap = 0;       // pool capacity in chunks
     uint64_t chunk_used = 0;      // chunks handed out so far in this call

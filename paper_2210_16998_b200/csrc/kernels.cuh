@@ -145,9 +145,12 @@ struct DfsArgs {
     uint64_t *ext;
     int64_t *rfirst;          // first record chunk of the unit
     int64_t *rcount;          // records of the unit
-    int64_t *child_first;     // split units: first remainder unit
-    int32_t *child_count;     // split units: number of remainder units (0 otherwise)
-    int32_t *gen;             // split generation (roots 0)
+    int64_t *child_head;      // latest block of units donated by the unit (-1: none)
+    int64_t *blk_first;       // donated block: first unit
+    int32_t *blk_count;       // donated block: number of units
+    int64_t *blk_next;        // donated block: the unit's previous block (-1: none)
+    unsigned long long *blk_ctr;
+    int32_t *gen;             // donation generation (roots 0)
     int *maxgen;
     unsigned long long *agg_tail_cnt, *agg_tail_len, *agg_pair_cnt, *agg_pair_len;
     unsigned int *overflow;   // bit 0: count overflow, bit 1: record pool exhausted, bit 2: queue full
