@@ -139,7 +139,7 @@ template <class T>
 struct Lane {
     T M, sbit, ps, sin;  // visited set, bit of s, pred(s) in SCC, succ(u) in SCC
     int32_t vb, s, u, l, r, k, o, ooff, ocnt, flags;
-    uint32_t steps, limit;
+    uint32_t steps;
     bool active, done, seg, emit;
     // record stream state: the decoder knows path[0..base); pend holds path[base..l] (pn bytes)
     int32_t base, pn;
@@ -186,7 +186,6 @@ __device__ __forceinline__ int out_event(const Lane<T> &L) {
 struct RecWriter {
     uint64_t *cur;  // current chunk
     int fill;       // records used in it
-    int64_t first;  // first chunk index of the unit
     int64_t count;  // records of the unit
 };
 
@@ -212,7 +211,7 @@ __device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t
 // (merged by their rank out_pos among the SCC members).  Returns the event.
 template <class T>
 __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, Lane<T> &L, RecWriter &R, uint32_t mp,
-                                        int &e_out, uint64_t &ext) {
+                                        int &e_out, uint32_t &ext) {
     using O = MT<T>;
     const int w = O::next(L.sin, L.M, L.sbit, L.k);
     if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
@@ -376,19 +375,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     bool waiting = false, exited = false;
     int64_t slot = -1;
     int32_t uscc = 0, ugen = 0;
-    uint64_t c[C_NUM];
-    uint64_t ext = 0;
-    int64_t pair_row = 0;
-    int32_t s_slot = 0;
+    uint64_t c_pp = 0, c_vert = 0;                          // per-unit counters (C_PP, C_VERT)
+    uint32_t c_it = 0, c_itv = 0, c_hd = 0, c_hdv = 0, ext = 0;  // C_ITEMS, C_ITEMV, C_HEADS, C_HEADV, E_canon
     RecWriter R;
     R.cur = A.chunks;
     R.fill = 0;
-    R.first = 0;
     R.count = 0;
-#pragma unroll
-    for (int i = 0; i < C_NUM; i++) c[i] = 0;
 
     int64_t child_head = -1;  // latest donated block of the running unit
+#ifdef TPGEN_KERNEL_DEBUG
+    unsigned long long d_it = 0, d_act = 0, d_don = 0;
+#endif
     uint32_t last_split = 0;
     int backoff = 0;  // idle lanes poll the queue every few iterations
     uint32_t iter = 0;
@@ -465,8 +462,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 L.u = u;
                 L.sbit = O::bit(s);
                 L.vb = __ldg(G.scc_vbase + uscc);
-                s_slot = L.vb + s;
-                const Slot<W> *ss = slot_ptr<W>(G, s_slot);
+                const Slot<W> *ss = slot_ptr<W>(G, L.vb + s);
                 L.ps = O::load(ss->pin);
                 const int4 sm = ld_meta(ss);
                 L.seg = (sm.w & F_ENTRY) != 0;
@@ -482,25 +478,20 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 L.pn = 0;
                 L.pend = 0;
                 fresh = true;
-#pragma unroll
-                for (int i = 0; i < C_NUM; i++) c[i] = 0;
                 ext = 0;
+                c_pp = c_vert = 0;
+                c_it = c_itv = c_hd = c_hdv = 0;
                 const unsigned long long ch = atomicAdd(A.chunk_next, 1ull);
                 if (ch >= A.chunk_cap) {
                     atomicOr(A.overflow, 2u);
                     R.cur = A.chunks;
-                    R.first = 0;
+                    A.rfirst[slot] = 0;
                 } else {
                     R.cur = A.chunks + ch * kChunkRecs;
-                    R.first = (int64_t)ch;
+                    A.rfirst[slot] = (int64_t)ch;
                 }
                 R.fill = 0;
                 R.count = 0;
-                if (L.seg) {
-                    const int32_t nout = __ldg(G.scc_nout + uscc);
-                    pair_row = __ldg(G.scc_pair_base + uscc) + (int64_t)__ldg(G.slot_eidx + s_slot) * nout -
-                               __ldg(G.scc_out_base + uscc);
-                }
                 // the unit's root event (no step is counted for it)
                 if (kind == K_NODE) {
                     load_slot(G, L, u);
@@ -527,6 +518,10 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 }
             }
         }
+#ifdef TPGEN_KERNEL_DEBUG
+        d_it++;
+        d_act += __popc(__ballot_sync(kFull, L.active));
+#endif
         if (__ballot_sync(kFull, L.active) == 0) {
             if (__ballot_sync(kFull, !exited) == 0) break;
             __nanosleep(256);
@@ -551,25 +546,28 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             L.pn = 0;
             L.pend = 0;
             if (ty == EV_PP) {
-                c[C_PP] += 1;
-                c[C_VERT] += len;
+                c_pp += 1;
+                c_vert += len;
             } else if (ty == EV_HEAD) {
                 const int32_t x = __ldg(G.out_gid + e);
                 const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                c[C_PP] = sat_add(c[C_PP], Wx, A.overflow);
-                c[C_VERT] = sat_add(c[C_VERT], sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow), A.overflow);
-                c[C_HEADS] += 1;
-                c[C_HEADV] += len;
+                c_pp = sat_add(c_pp, Wx, A.overflow);
+                c_vert = sat_add(c_vert, sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow), A.overflow);
+                c_hd += 1;
+                c_hdv += (uint32_t)len;
             } else if (ty == EV_TAIL) {
-                c[C_ITEMS] += 1;
-                c[C_ITEMV] += len;
-                atomicAdd(A.agg_tail_cnt + s_slot, 1ull);
-                atomicAdd(A.agg_tail_len + s_slot, (unsigned long long)len);
+                c_it += 1;
+                c_itv += (uint32_t)len;
+                atomicAdd(A.agg_tail_cnt + L.vb + L.s, 1ull);
+                atomicAdd(A.agg_tail_len + L.vb + L.s, (unsigned long long)len);
             } else {  // EV_TRANSIT
-                c[C_ITEMS] += 1;
-                c[C_ITEMV] += len;
-                atomicAdd(A.agg_pair_cnt + pair_row + e, 1ull);
-                atomicAdd(A.agg_pair_len + pair_row + e, (unsigned long long)len);
+                c_it += 1;
+                c_itv += (uint32_t)len;
+                const int32_t nout = __ldg(G.scc_nout + uscc);
+                const int64_t pair = __ldg(G.scc_pair_base + uscc) +
+                                     (int64_t)__ldg(G.slot_eidx + L.vb + L.s) * nout - __ldg(G.scc_out_base + uscc) + e;
+                atomicAdd(A.agg_pair_cnt + pair, 1ull);
+                atomicAdd(A.agg_pair_len + pair, (unsigned long long)len);
             }
         }
 
@@ -606,16 +604,22 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     if (j0 == L.l) L.done = true;  // nothing left below the donated level
                     else L.r = j0 + 1;             // the walk now ends when it returns to depth j0+1
                     last_split = L.steps;
+#ifdef TPGEN_KERNEL_DEBUG
+                    d_don++;
+#endif
                 }
             }
         }
 
         // ---------------- unit completion
         if (L.active && L.done) {
-#pragma unroll
-            for (int i = 0; i < C_NUM; i++) A.cnt[i][slot] = c[i];
+            A.cnt[C_PP][slot] = c_pp;
+            A.cnt[C_VERT][slot] = c_vert;
+            A.cnt[C_ITEMS][slot] = c_it;
+            A.cnt[C_ITEMV][slot] = c_itv;
+            A.cnt[C_HEADS][slot] = c_hd;
+            A.cnt[C_HEADV][slot] = c_hdv;
             A.ext[slot] = ext;
-            A.rfirst[slot] = R.first;
             A.rcount[slot] = R.count;
             A.child_head[slot] = child_head;
             __threadfence();
@@ -624,6 +628,15 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             L.done = false;
         }
     }
+#ifdef TPGEN_KERNEL_DEBUG
+    if (A.dbg) {
+        if (lane == 0) {
+            atomicAdd(A.dbg + 0, d_it);
+            atomicAdd(A.dbg + 1, d_act);
+        }
+        atomicAdd(A.dbg + 2, d_don);
+    }
+#endif
 }
 
 }  // namespace tpg

@@ -399,6 +399,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.chunk_next = ctr + 4;
         A.chunk_cap = P.chunk_cap;
         A.split_min = P.split_min;
+        A.dbg = getenv("TPGEN_DEBUG") ? ctr + 24 : nullptr;
+        if (A.dbg) TPG_CK(cudaMemsetAsync(A.dbg, 0, 8 * 8, s));
         A.low_water = (uint32_t)std::max<int64_t>(64, lanes / 8);
         cudaEventRecord(t.a, s);
         dfs_kernel<T><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, 0, s>>>(A);
@@ -418,6 +420,13 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
             if (ovf & 2u) TPG_TRY(grow_pool(P, std::max<uint64_t>(h[4], P.chunk_cap) * 2, s));
             if (ovf & 4u) TPG_TRY(grow_queue<W>(P, qbase, P.qcap * 2, s));
             continue;
+        }
+        if (A.dbg) {
+            unsigned long long d[4];
+            TPG_CK(cudaMemcpyAsync(d, A.dbg, 32, cudaMemcpyDeviceToHost, s));
+            TPG_CK(cudaStreamSynchronize(s));
+            fprintf(stderr, "[tpgen dfs] ms=%.3f iters=%llu active_lane_iters=%llu (%.2f/warp-iter) donations=%llu units=%llu\n",
+                    ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], h[1] - qbase);
         }
         if (ovf & 1u) P.overflow = true;
         P.chunk_used = h[4];

@@ -160,6 +160,7 @@ struct DfsArgs {
     unsigned long long chunk_cap;
     uint32_t split_min;       // steps a unit runs before it may be split
     uint32_t low_water;       // split when fewer queued units than this are waiting to be claimed
+    unsigned long long *dbg;  // TPGEN_KERNEL_DEBUG builds: iterations, idle iterations, lane-steps, donations
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
@@ -167,7 +168,7 @@ template <int W>
 struct DfsCfg {
     static constexpr int threads = (W <= 2) ? 256 : 128;
     static constexpr int warps = threads / 32;
-    static constexpr int min_blocks = (W == 1) ? 4 : ((W == 2) ? 2 : 3);
+    static constexpr int min_blocks = (W == 1) ? 3 : ((W == 2) ? 2 : 3);
 };
 constexpr unsigned kFull = 0xffffffffu;
 
