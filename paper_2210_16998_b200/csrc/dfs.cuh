@@ -146,12 +146,27 @@ struct Lane {
     uint64_t pend;
 };
 
-template <class T>
-__device__ __forceinline__ void load_slot(const DevGraph &G, Lane<T> &L, int u) {
-    constexpr int W = MT<T>::W;
-    const Slot<W> *sp = slot_ptr<W>(G, L.vb + u);
-    L.sin = MT<T>::load(sp->sin);
-    const int4 m = ld_meta(sp);
+// View of the slot table: staged in shared memory (TS) when it fits, else read through L1.
+template <int W, bool TS>
+struct TabView {
+    const Slot<W> *p;
+    template <class T>
+    __device__ __forceinline__ T sin(int i) const {
+        return TS ? MT<T>::from(p[i].sin) : MT<T>::load(p[i].sin);
+    }
+    template <class T>
+    __device__ __forceinline__ T pin(int i) const {
+        return TS ? MT<T>::from(p[i].pin) : MT<T>::load(p[i].pin);
+    }
+    __device__ __forceinline__ int4 meta(int i) const {
+        return TS ? *reinterpret_cast<const int4 *>(&p[i].gid) : ld_meta(p + i);
+    }
+};
+
+template <class T, bool TS>
+__device__ __forceinline__ void load_slot(const TabView<MT<T>::W, TS> &tab, Lane<T> &L, int u) {
+    L.sin = tab.template sin<T>(L.vb + u);
+    const int4 m = tab.meta(L.vb + u);
     L.ooff = m.y;
     L.ocnt = m.z;
     L.flags = m.w;
@@ -209,9 +224,9 @@ __device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t
 // ascending global id: in-SCC successors (local bits; ascending local id ==
 // ascending global id), the closing arc back to s, and out-of-SCC successors
 // (merged by their rank out_pos among the SCC members).  Returns the event.
-template <class T>
-__device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, Lane<T> &L, RecWriter &R, uint32_t mp,
-                                        int &e_out, uint32_t &ext) {
+template <class T, bool TS>
+__device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, const TabView<MT<T>::W, TS> &tab,
+                                        Lane<T> &L, RecWriter &R, uint32_t mp, int &e_out, uint32_t &ext) {
     using O = MT<T>;
     const int w = O::next(L.sin, L.M, L.sbit, L.k);
     if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
@@ -240,7 +255,7 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, Lan
     L.k = push ? 0 : (has ? w + 1 : wold + 1);
     L.l += push ? 1 : (pop ? -1 : 0);
     L.u = push ? w : (pop ? parent : wold);
-    load_slot(G, L, L.u);
+    load_slot(tab, L, L.u);
     if (pop && L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: exit vertices only
     else if (push) L.o = 0;
     // record-stream bookkeeping: pending bytes follow pushes and pops
@@ -278,6 +293,19 @@ struct DfsTraits {
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
     return *reinterpret_cast<const volatile unsigned long long *>(p);
 }
+// hand-off of queued units between lanes of different SMs: release store / acquire load of the ready flag
+__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// The consumer polls the flag with a relaxed load and only then issues its
+// (L2, .cg) loads of the unit payload: the payload was made visible at L2 by
+// the producer's release before the flag, and the payload loads are control
+// dependent on the flag value -- no acquire, so no L1 invalidation per claim.
+__device__ __forceinline__ unsigned int ld_relaxed(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ int lds_u32(uint32_t a) {
     int v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -290,18 +318,17 @@ __device__ __forceinline__ int lds_u32(uint32_t a) {
 // events; WRITE=true writes them as units.  The lane keeps everything below
 // level j0 and stops when its walk returns to depth j0+1, so its remaining
 // output precedes the donated units in lexicographic order.
-template <class T, bool WRITE>
-__device__ int lane_donate(const DevGraph &G, const Lane<T> &L, uint32_t mp, int uscc, int &j0,
-                           Unit<MT<T>::W> *out) {
+template <class T, bool TS, bool WRITE>
+__device__ int lane_donate(const DevGraph &G, const TabView<MT<T>::W, TS> &tab, const Lane<T> &L, uint32_t mp,
+                           int uscc, int &j0, Unit<MT<T>::W> *out) {
     using O = MT<T>;
     constexpr int W = O::W;
     T M = L.M;
     int best = 0;
     for (int j = L.l; j >= L.r; j--) {
         const int u = lds_u8(mp + pidx(j));
-        const Slot<W> *su = slot_ptr<W>(G, L.vb + u);
-        const T sin = O::load(su->sin);
-        const int4 meta = ld_meta(su);
+        const T sin = tab.template sin<T>(L.vb + u);
+        const int4 meta = tab.meta(L.vb + u);
         int k, o;
         if (j == L.l) {
             k = L.k;
@@ -357,16 +384,28 @@ __device__ int lane_donate(const DevGraph &G, const Lane<T> &L, uint32_t mp, int
 // queued, unclaimed units falls below low_water: its walk so far becomes a
 // finished piece and the untried siblings on its stack are pushed as new units
 // (children of the piece in the unit forest).  The kernel ends when every
-// pushed unit has finished (done == tail).
-template <class T>
+// pushed unit has finished (done == tail; both live in one 64-bit word so a
+// single load gives a consistent snapshot).
+template <class T, bool TS>
 __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
     using O = MT<T>;
     constexpr int W = O::W;
     constexpr int WARPS = DfsTraits<T>::warps;
     __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32];
+    extern __shared__ __align__(16) uint8_t stab[];  // slot table copy (TS)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t mp = (uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32) + lane * 4;
     const DevGraph &G = A.G;
+    TabView<W, TS> tab;
+    if (TS) {
+        const int4 *src = reinterpret_cast<const int4 *>(G.slots);
+        int4 *dst = reinterpret_cast<int4 *>(stab);
+        for (int i = threadIdx.x; i < A.n_slots * (int)(sizeof(Slot<W>) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+        __syncthreads();
+        tab.p = reinterpret_cast<const Slot<W> *>(stab);
+    } else {
+        tab.p = reinterpret_cast<const Slot<W> *>(G.slots);
+    }
     Unit<W> *units = reinterpret_cast<Unit<W> *>(A.units);
 
     Lane<T> L;
@@ -385,6 +424,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     int64_t child_head = -1;  // latest donated block of the running unit
 #ifdef TPGEN_KERNEL_DEBUG
     unsigned long long d_it = 0, d_act = 0, d_don = 0;
+    const unsigned long long t0 = A.dbg ? A.dbg[7] : 0;
 #endif
     uint32_t last_split = 0;
     int backoff = 0;  // idle lanes poll the queue every few iterations
@@ -400,15 +440,14 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             long long base = -1, k = 0;
             int fin = 0;
             if (lane == leader) {
-                const long long avail = (long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0);
+                const unsigned long long td = ld_volatile(A.q + 1);  // tail << 32 | done
+                const long long avail = (long long)(td >> 32) - (long long)ld_volatile(A.q + 0);
                 k = min((long long)__popc(need), avail);
                 if (k > 0) {
                     base = (long long)atomicAdd(A.q + 0, (unsigned long long)k);
                 } else {  // nothing queued: has every pushed unit finished?
-                    const unsigned long long dn = ld_volatile(A.q + 2);
-                    __threadfence();
-                    const unsigned long long tl = ld_volatile(A.q + 1);
-                    fin = (dn == tl) || ((*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u) != 0u);
+                    fin = ((td >> 32) == (td & 0xffffffffull)) ||
+                          ((*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u) != 0u);
                 }
             }
             base = __shfl_sync(kFull, base, leader);
@@ -422,16 +461,15 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 } else if (fin) {
                     exited = true;
                 } else {
-                    backoff = 16;
+                    backoff = 4;
                 }
             }
         }
         // ---------------- waiting lanes: start the unit once written, or stop when all work is done
         if (waiting) {
             if (slot < (int64_t)A.qcap &&
-                *reinterpret_cast<const volatile unsigned int *>(A.ready + slot) != 0u) {
+                ld_relaxed(A.ready + slot) != 0u) {
                 waiting = false;
-                __threadfence();
                 // queue slots are written by other SMs during this launch: read them at L2 (ld.cg)
                 const Unit<W> *U = units + slot;
                 const int4 h = __ldcg(reinterpret_cast<const int4 *>(&U->scc));  // scc, e, -, depth|kind
@@ -462,9 +500,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 L.u = u;
                 L.sbit = O::bit(s);
                 L.vb = __ldg(G.scc_vbase + uscc);
-                const Slot<W> *ss = slot_ptr<W>(G, L.vb + s);
-                L.ps = O::load(ss->pin);
-                const int4 sm = ld_meta(ss);
+                L.ps = tab.template pin<T>(L.vb + s);
+                const int4 sm = tab.meta(L.vb + s);
                 L.seg = (sm.w & F_ENTRY) != 0;
                 L.emit = sm.x >= G.shard_lo && sm.x < G.shard_hi;
                 L.k = 0;
@@ -494,7 +531,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 R.count = 0;
                 // the unit's root event (no step is counted for it)
                 if (kind == K_NODE) {
-                    load_slot(G, L, u);
+                    load_slot(tab, L, u);
                     if (depth > 0 && L.emit) ext++;
                     ev = node_event(L, u);
                 } else if (kind == K_CLOSURE) {
@@ -509,10 +546,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     ev = out_event(L);
                 }
             } else {
-                const unsigned long long dn = ld_volatile(A.q + 2);
-                __threadfence();
-                const unsigned long long tl = ld_volatile(A.q + 1);
-                if (dn == tl || (*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u)) {
+                const unsigned long long td = ld_volatile(A.q + 1);
+                if ((td >> 32) == (td & 0xffffffffull) ||
+                    (*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u)) {
                     waiting = false;
                     exited = true;
                 }
@@ -520,7 +556,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         }
 #ifdef TPGEN_KERNEL_DEBUG
         d_it++;
-        d_act += __popc(__ballot_sync(kFull, L.active));
+        {
+            const int na = __popc(__ballot_sync(kFull, L.active));
+            d_act += na;
+            if (A.dbg && lane == 0 && (d_it & 15) == 0) {  // timeline: 64 buckets of 0.5 ms
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                const unsigned long long bkt = min((now - t0) / 500000ull, 63ull);
+                atomicAdd(A.dbg + 8 + 2 * bkt, (unsigned long long)na);
+                atomicAdd(A.dbg + 9 + 2 * bkt, 1ull);
+            }
+        }
 #endif
         if (__ballot_sync(kFull, L.active) == 0) {
             if (__ballot_sync(kFull, !exited) == 0) break;
@@ -530,7 +576,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
 
         // ---------------- one step for every running lane (lanes that just started emit their root event)
         if (L.active && !L.done && !(fresh && ev != 0)) {
-            ev = dfs_step<T>(A, G, L, R, mp, e, ext);
+            ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
             L.steps++;
         }
 
@@ -571,25 +617,25 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             }
         }
 
-        // ---------------- donate on demand (one lane per warp samples the queue every 64 iterations)
+        // ---------------- donate on demand (one lane per warp samples the queue every 16 iterations)
         bool feed = false;
-        if (((++iter) & 63u) == 0u) {
+        if (((++iter) & 15u) == 0u) {
             int f = 0;
             if (lane == 0)
-                f = (long long)ld_volatile(A.q + 1) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water;
+                f = (long long)(ld_volatile(A.q + 1) >> 32) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water;
             feed = __shfl_sync(kFull, f, 0) != 0;
         }
         if (feed && L.active && !L.done && L.steps - last_split >= A.split_min) {
             // backlog of queued, unclaimed units below the low-water mark: donate the shallowest siblings
             int j0 = -1;
-            const int m = lane_donate<T, false>(G, L, mp, uscc, j0, nullptr);
+            const int m = lane_donate<T, TS, false>(G, tab, L, mp, uscc, j0, nullptr);
             if (m > 0) {
-                const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m);
+                const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m << 32) >> 32;
                 const unsigned long long b = atomicAdd(A.blk_ctr, 1ull);
                 if (base + m > A.qcap || b >= A.qcap) {
                     atomicOr(A.overflow, 4u);
                 } else {
-                    lane_donate<T, true>(G, L, mp, uscc, j0, units + base);
+                    lane_donate<T, TS, true>(G, tab, L, mp, uscc, j0, units + base);
                     for (int i = 0; i < m; i++) {
                         A.gen[base + i] = ugen + 1;
                         A.child_head[base + i] = -1;
@@ -599,8 +645,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     A.blk_next[b] = child_head;
                     child_head = (int64_t)b;
                     atomicMax(A.maxgen, ugen + 1);
-                    __threadfence();
-                    for (int i = 0; i < m; i++) atomicExch(A.ready + base + i, 1u);
+                    for (int i = 0; i < m; i++) st_release(A.ready + base + i, 1u);  // publish after the unit data
                     if (j0 == L.l) L.done = true;  // nothing left below the donated level
                     else L.r = j0 + 1;             // the walk now ends when it returns to depth j0+1
                     last_split = L.steps;
@@ -622,8 +667,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             A.ext[slot] = ext;
             A.rcount[slot] = R.count;
             A.child_head[slot] = child_head;
-            __threadfence();
-            atomicAdd(A.q + 2, 1ull);
+            atomicAdd(A.q + 1, 1ull);  // done += 1 (same word as the tail: termination needs no fence)
             L.active = false;
             L.done = false;
         }

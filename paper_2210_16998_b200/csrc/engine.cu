@@ -85,7 +85,7 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks};
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
@@ -288,6 +288,14 @@ struct Timer {
     }
 };
 
+constexpr size_t kSmemTabMax = 40 * 1024;  // slot tables up to this size are staged in shared memory
+
+__global__ void set_t0_kernel(unsigned long long *p) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    *p = now;
+}
+
 // Grows the record pool to hold at least `need` chunks, keeping the first `used` chunks.
 static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
     if (need <= P.chunk_cap) return TPGEN_OK;
@@ -368,8 +376,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
     for (int attempt = 0; attempt < 32; attempt++) {
         TPG_TRY(put_roots<W>(P, roots, qbase, s));
         TPG_CK(cudaMemsetAsync(P.qready.as<uint32_t>() + qbase + nroots, 0, (P.qcap - qbase - nroots) * 4, s));
-        unsigned long long init[7] = {qbase, qbase + nroots, qbase, 0, P.chunk_used, (unsigned long long)P.maxgen,
-                                      P.blk_used};
+        unsigned long long init[7] = {qbase, ((qbase + nroots) << 32) | qbase, 0, 0, P.chunk_used,
+                                      (unsigned long long)P.maxgen, P.blk_used};
         TPG_CK(cudaMemcpyAsync(ctr, init, 7 * 8, cudaMemcpyHostToDevice, s));
         DfsArgs A;
         memset(&A, 0, sizeof(A));
@@ -399,11 +407,24 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.chunk_next = ctr + 4;
         A.chunk_cap = P.chunk_cap;
         A.split_min = P.split_min;
-        A.dbg = getenv("TPGEN_DEBUG") ? ctr + 24 : nullptr;
-        if (A.dbg) TPG_CK(cudaMemsetAsync(A.dbg, 0, 8 * 8, s));
+        A.dbg = nullptr;
+        if (getenv("TPGEN_DEBUG")) {
+            TPG_TRY(P.dbgbuf.ensure(160 * 8, s));
+            A.dbg = P.dbgbuf.as<unsigned long long>();
+            TPG_CK(cudaMemsetAsync(A.dbg, 0, 160 * 8, s));
+            set_t0_kernel<<<1, 1, 0, s>>>(A.dbg + 7);
+        }
         A.low_water = (uint32_t)std::max<int64_t>(64, lanes / 8);
         cudaEventRecord(t.a, s);
-        dfs_kernel<T><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, 0, s>>>(A);
+        A.n_slots = H.n;
+        const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
+        if (tab_bytes <= kSmemTabMax) {
+            TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kSmemTabMax));
+            dfs_kernel<T, true><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, tab_bytes, s>>>(A);
+        } else {
+            dfs_kernel<T, false><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, 0, s>>>(A);
+        }
         cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
@@ -422,17 +443,21 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
             continue;
         }
         if (A.dbg) {
-            unsigned long long d[4];
-            TPG_CK(cudaMemcpyAsync(d, A.dbg, 32, cudaMemcpyDeviceToHost, s));
+            unsigned long long d[160];
+            TPG_CK(cudaMemcpyAsync(d, A.dbg, 160 * 8, cudaMemcpyDeviceToHost, s));
             TPG_CK(cudaStreamSynchronize(s));
+            fprintf(stderr, "[tpgen dfs timeline] avg active lanes per warp-iteration per 0.5 ms:");
+            for (int b = 0; b < 64; b++)
+                if (d[9 + 2 * b]) fprintf(stderr, " %.1f", (double)d[8 + 2 * b] / d[9 + 2 * b]);
+            fprintf(stderr, "\n");
             fprintf(stderr, "[tpgen dfs] ms=%.3f iters=%llu active_lane_iters=%llu (%.2f/warp-iter) donations=%llu units=%llu\n",
-                    ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], h[1] - qbase);
+                    ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], (h[1] >> 32) - qbase);
         }
         if (ovf & 1u) P.overflow = true;
         P.chunk_used = h[4];
         P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
         P.blk_used = h[6];
-        tail_out = h[1];
+        tail_out = h[1] >> 32;
         return TPGEN_OK;
     }
     set_error("DFS phase: work queue / record pool could not be sized");

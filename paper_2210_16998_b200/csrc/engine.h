@@ -42,8 +42,8 @@ struct PlanImpl {
     uint64_t chunk_cap = 0;       // pool capacity in chunks
     uint64_t chunk_used = 0;      // chunks handed out so far in this call
     int maxgen = 0;               // deepest split generation so far in this call
-    uint32_t split_min = 256;     // steps before a unit may be split
-    DevBuf scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
+    uint32_t split_min = 32;      // steps between two donations of a unit
+    DevBuf dbgbuf, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     bool overflow = false;
     ~PlanImpl();
     std::vector<DevBuf *> all_bufs();

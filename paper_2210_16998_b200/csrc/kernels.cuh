@@ -138,7 +138,7 @@ struct DfsArgs {
     DevGraph G;
     void *units;              // Unit<W>[qcap]: the work queue (roots pre-filled by the host)
     unsigned int *ready;      // per queue slot: 1 once the unit record is written
-    unsigned long long *q;    // [0] head (claims), [1] tail (pushed), [2] done (finished)
+    unsigned long long *q;    // [0] head (claims), [1] tail (pushed) << 32 | done (finished)
     unsigned long long qcap;  // queue capacity (slots)
     // per-unit results, indexed by queue slot
     uint64_t *cnt[C_NUM];
@@ -161,6 +161,7 @@ struct DfsArgs {
     uint32_t split_min;       // steps a unit runs before it may be split
     uint32_t low_water;       // split when fewer queued units than this are waiting to be claimed
     unsigned long long *dbg;  // TPGEN_KERNEL_DEBUG builds: iterations, idle iterations, lane-steps, donations
+    int n_slots;              // slot table size (copied to shared memory by the TS kernels)
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
