@@ -290,8 +290,16 @@ struct DfsTraits {
     static constexpr int min_blocks = DfsCfg<W>::min_blocks;
 };
 
+// queue counters are polled with GPU-scope relaxed loads (a volatile load would be system scope)
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
-    return *reinterpret_cast<const volatile unsigned long long *>(p);
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int ld_flags(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 // hand-off of queued units between lanes of different SMs: release store / acquire load of the ready flag
 __device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
@@ -440,14 +448,14 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             long long base = -1, k = 0;
             int fin = 0;
             if (lane == leader) {
-                const unsigned long long td = ld_volatile(A.q + 1);  // tail << 32 | done
-                const long long avail = (long long)(td >> 32) - (long long)ld_volatile(A.q + 0);
+                const unsigned long long td = ld_volatile(A.qtd);  // tail << 32 | done
+                const long long avail = (long long)(td >> 32) - (long long)ld_volatile(A.qhead);
                 k = min((long long)__popc(need), avail);
                 if (k > 0) {
-                    base = (long long)atomicAdd(A.q + 0, (unsigned long long)k);
+                    base = (long long)atomicAdd(A.qhead, (unsigned long long)k);
                 } else {  // nothing queued: has every pushed unit finished?
                     fin = ((td >> 32) == (td & 0xffffffffull)) ||
-                          ((*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u) != 0u);
+                          ((ld_flags(A.overflow) & 6u) != 0u);
                 }
             }
             base = __shfl_sync(kFull, base, leader);
@@ -546,9 +554,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     ev = out_event(L);
                 }
             } else {
-                const unsigned long long td = ld_volatile(A.q + 1);
+                const unsigned long long td = ld_volatile(A.qtd);
                 if ((td >> 32) == (td & 0xffffffffull) ||
-                    (*reinterpret_cast<const volatile unsigned int *>(A.overflow) & 6u)) {
+                    (ld_flags(A.overflow) & 6u)) {
                     waiting = false;
                     exited = true;
                 }
@@ -622,7 +630,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         if (((++iter) & 15u) == 0u) {
             int f = 0;
             if (lane == 0)
-                f = (long long)(ld_volatile(A.q + 1) >> 32) - (long long)ld_volatile(A.q + 0) < (long long)A.low_water;
+                f = (long long)(ld_volatile(A.qtd) >> 32) - (long long)ld_volatile(A.qhead) < (long long)A.low_water;
             feed = __shfl_sync(kFull, f, 0) != 0;
         }
         if (feed && L.active && !L.done && L.steps - last_split >= A.split_min) {
@@ -630,7 +638,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             int j0 = -1;
             const int m = lane_donate<T, TS, false>(G, tab, L, mp, uscc, j0, nullptr);
             if (m > 0) {
-                const unsigned long long base = atomicAdd(A.q + 1, (unsigned long long)m << 32) >> 32;
+                const unsigned long long base = atomicAdd(A.qtd, (unsigned long long)m << 32) >> 32;
                 const unsigned long long b = atomicAdd(A.blk_ctr, 1ull);
                 if (base + m > A.qcap || b >= A.qcap) {
                     atomicOr(A.overflow, 4u);
@@ -667,7 +675,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             A.ext[slot] = ext;
             A.rcount[slot] = R.count;
             A.child_head[slot] = child_head;
-            atomicAdd(A.q + 1, 1ull);  // done += 1 (same word as the tail: termination needs no fence)
+            atomicAdd(A.qtd, 1ull);  // done += 1 (same word as the tail: termination needs no fence)
             L.active = false;
             L.done = false;
         }

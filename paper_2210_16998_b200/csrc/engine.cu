@@ -85,7 +85,7 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf};
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
@@ -372,19 +372,27 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
     const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
     TPG_TRY(grow_queue<W>(P, qbase, std::max<uint64_t>(qbase + nroots + 8 * (uint64_t)lanes, 1u << 21), s));
     if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
-    unsigned long long *ctr = P.ctr.as<unsigned long long>();  // [0..2] head/tail/done [3] ovf [4] chunk_next [5] maxgen
+    TPG_TRY(P.qctr.ensure(7 * 16 * 8, s));
+    unsigned long long *qc = P.qctr.as<unsigned long long>();
     for (int attempt = 0; attempt < 32; attempt++) {
         TPG_TRY(put_roots<W>(P, roots, qbase, s));
         TPG_CK(cudaMemsetAsync(P.qready.as<uint32_t>() + qbase + nroots, 0, (P.qcap - qbase - nroots) * 4, s));
-        unsigned long long init[7] = {qbase, ((qbase + nroots) << 32) | qbase, 0, 0, P.chunk_used,
-                                      (unsigned long long)P.maxgen, P.blk_used};
-        TPG_CK(cudaMemcpyAsync(ctr, init, 7 * 8, cudaMemcpyHostToDevice, s));
+        // queue counters, one per 128-byte line: head, tail<<32|done, overflow, chunk_next, maxgen, blk_ctr
+        unsigned long long init[7 * 16];
+        memset(init, 0, sizeof(init));
+        init[0] = qbase;
+        init[16] = ((qbase + nroots) << 32) | qbase;
+        init[48] = P.chunk_used;
+        init[64] = (unsigned long long)P.maxgen;
+        init[80] = P.blk_used;
+        TPG_CK(cudaMemcpyAsync(qc, init, sizeof(init), cudaMemcpyHostToDevice, s));
         DfsArgs A;
         memset(&A, 0, sizeof(A));
         A.G = G;
         A.units = P.qunits.p;
         A.ready = P.qready.as<unsigned int>();
-        A.q = ctr;
+        A.qhead = qc;
+        A.qtd = qc + 16;
         A.qcap = P.qcap;
         for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.qcnt[c].as<uint64_t>();
         A.ext = P.qext.as<uint64_t>();
@@ -394,17 +402,17 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.blk_first = P.blk_first.as<int64_t>();
         A.blk_count = P.blk_count.as<int32_t>();
         A.blk_next = P.blk_next.as<int64_t>();
-        A.blk_ctr = ctr + 6;
+        A.blk_ctr = qc + 80;
         A.gen = P.qgen.as<int32_t>();
-        A.maxgen = reinterpret_cast<int *>(ctr + 5);
+        A.maxgen = reinterpret_cast<int *>(qc + 64);
         unsigned long long *agg = P.agg.as<unsigned long long>();
         A.agg_tail_cnt = agg;
         A.agg_tail_len = agg + H.n;
         A.agg_pair_cnt = agg + 2 * (int64_t)H.n;
         A.agg_pair_len = agg + 2 * (int64_t)H.n + H.n_pairs;
-        A.overflow = reinterpret_cast<unsigned int *>(ctr + 3);
+        A.overflow = reinterpret_cast<unsigned int *>(qc + 32);
         A.chunks = P.chunks.as<uint64_t>();
-        A.chunk_next = ctr + 4;
+        A.chunk_next = qc + 48;
         A.chunk_cap = P.chunk_cap;
         A.split_min = P.split_min;
         A.dbg = nullptr;
@@ -428,9 +436,11 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
-        unsigned long long h[7];
-        TPG_CK(cudaMemcpyAsync(h, ctr, 7 * 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long hq[7 * 16], h[7];
+        TPG_CK(cudaMemcpyAsync(hq, qc, sizeof(hq), cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
+        const int hidx[7] = {0, 16, 0, 32, 48, 64, 80};  // old layout: head, td, -, ovf, chunk, maxgen, blk
+        for (int i = 0; i < 7; i++) h[i] = hq[hidx[i]];
         float ms = 0;
         cudaEventElapsedTime(&ms, t.a, t.b);
         ms_dfs += ms;

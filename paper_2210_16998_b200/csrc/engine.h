@@ -43,7 +43,7 @@ struct PlanImpl {
     uint64_t chunk_used = 0;      // chunks handed out so far in this call
     int maxgen = 0;               // deepest split generation so far in this call
     uint32_t split_min = 32;      // steps between two donations of a unit
-    DevBuf dbgbuf, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
+    DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     bool overflow = false;
     ~PlanImpl();
     std::vector<DevBuf *> all_bufs();

@@ -138,7 +138,8 @@ struct DfsArgs {
     DevGraph G;
     void *units;              // Unit<W>[qcap]: the work queue (roots pre-filled by the host)
     unsigned int *ready;      // per queue slot: 1 once the unit record is written
-    unsigned long long *q;    // [0] head (claims), [1] tail (pushed) << 32 | done (finished)
+    unsigned long long *qhead;  // claims (own 128-byte line)
+    unsigned long long *qtd;    // tail (pushed) << 32 | done (finished) (own 128-byte line)
     unsigned long long qcap;  // queue capacity (slots)
     // per-unit results, indexed by queue slot
     uint64_t *cnt[C_NUM];
