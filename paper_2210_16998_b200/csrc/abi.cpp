@@ -1,6 +1,8 @@
 // abi.cpp -- extern "C" entry points of libtpgen (declared in include/tpgen.h).
 #include <chrono>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 
 #include "engine.h"
@@ -51,6 +53,47 @@ tpgen_status make_plan(const int64_t *so, const int32_t *st, int32_t n, const tp
         delete p;
         return s;
     }
+    *out = p;
+    return TPGEN_OK;
+}
+
+// One-shot calls (tpgen_prime_paths / tpgen_test_paths) reuse a per-device
+// plan object so device workspaces (work queue, record pool, scan buffers)
+// persist across calls; calls are serialised per process by the mutex.
+std::mutex g_cache_mu;
+std::map<int, tpgen_plan *> g_cache;
+
+tpgen_status cached_plan(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options &o, tpgen_plan **out) {
+    *out = nullptr;
+    int dev = o.device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+        tpg::set_error("no CUDA device");
+        return TPGEN_ERR_CUDA;
+    }
+    tpgen_plan *&p = g_cache[dev];
+    if (!p) {
+        p = new (std::nothrow) tpgen_plan();
+        if (!p) return TPGEN_ERR_OUT_OF_MEMORY;
+        tpgen_options od = o;
+        od.device = dev;
+        tpgen_status s = tpg::init_device(p->impl, od);
+        if (s != TPGEN_OK) {
+            delete p;
+            p = nullptr;
+            return s;
+        }
+    }
+    if (cudaSetDevice(dev) != cudaSuccess) return TPGEN_ERR_CUDA;
+    const double t0 = now_ms();
+    std::string msg;
+    tpgen_status s = tpg::build_plan(so, st, n, p->impl.hp, msg);
+    if (s != TPGEN_OK) {
+        tpg::set_error(msg);
+        return s;
+    }
+    p->impl.ms_plan = now_ms() - t0;
+    s = tpg::plan_upload(p->impl, (cudaStream_t)o.stream);
+    if (s != TPGEN_OK) return s;
     *out = p;
     return TPGEN_OK;
 }
@@ -138,14 +181,14 @@ tpgen_status tpgen_prime_paths(const int64_t *so, const int32_t *st, int32_t n, 
     tpgen_options o = resolve(opt);
     tpgen_status s = check_options(o);
     if (s != TPGEN_OK) return s;
+    std::lock_guard<std::mutex> lock(g_cache_mu);
     tpgen_plan *p = nullptr;
-    s = make_plan(so, st, n, o, &p);
+    s = cached_plan(so, st, n, o, &p);
     if (s != TPGEN_OK) return s;
     {
         DeviceScope ds(p->impl.device);
         s = tpg::run_prime_paths(p->impl, o, out, stats);
     }
-    tpgen_plan_destroy(p);
     if (s != TPGEN_OK) memset(out, 0, sizeof(*out));
     if (s == TPGEN_OK && stats) stats->ms_total = now_ms() - t0;
     return s;
@@ -168,14 +211,14 @@ tpgen_status tpgen_test_paths(const int64_t *so, const int32_t *st, int32_t n, c
         tpg::set_error("prime_paths has NULL arrays");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
+    std::lock_guard<std::mutex> lock(g_cache_mu);
     tpgen_plan *p = nullptr;
-    s = make_plan(so, st, n, o, &p);
+    s = cached_plan(so, st, n, o, &p);
     if (s != TPGEN_OK) return s;
     {
         DeviceScope ds(p->impl.device);
         s = tpg::run_test_paths(p->impl, prime_paths, entry, exit, o, out, stats);
     }
-    tpgen_plan_destroy(p);
     if (s != TPGEN_OK) memset(out, 0, sizeof(*out));
     if (s == TPGEN_OK && stats) stats->ms_total = now_ms() - t0;
     return s;

@@ -682,7 +682,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     E.item_pool = P.item_pool.as<int32_t>();
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        expand_kernel<W><<<grid_for(nu * 32, kExpandThreads, P.num_sms * 8), kExpandThreads, 0, s>>>(E);
+        const int eg = grid_for(nu * 32, kExpandThreads, P.num_sms * 8);
+        const int np = (H.max_scc + 1 + 31) / 32;  // registers per lane for the longest emitted path
+        if (W == 1 && np <= 1) expand_kernel<W, 1><<<eg, kExpandThreads, 0, s>>>(E);
+        else if (W == 1 && np <= 2) expand_kernel<W, 2><<<eg, kExpandThreads, 0, s>>>(E);
+        else expand_kernel<W, 2 * W + 1><<<eg, kExpandThreads, 0, s>>>(E);
         launches++;
     }
     cudaEventRecord(tw.b, s);

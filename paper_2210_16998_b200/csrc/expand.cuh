@@ -37,9 +37,9 @@ __device__ __forceinline__ void st_global_cs(int32_t *p, int v) {
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int W>
+// NP = path registers per lane: ceil((longest emitted path + closing vertex) / 32).
+template <int W, int NP>
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
-    constexpr int NP = 2 * W + 1;  // path registers per lane (64*W positions + the closing vertex)
     const int lane = threadIdx.x & 31;
     const DevGraph &G = A.G;
     const Unit<W> *units = reinterpret_cast<const Unit<W> *>(A.units);
@@ -138,12 +138,17 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
                     itv += (uint64_t)len;
                 }
                 const int s0 = __shfl_sync(kFull, P[0], 0);  // closing vertex of a cycle
+                if (ga >= 0) {  // SCC with contiguous global ids (warp-uniform branch)
 #pragma unroll
-                for (int r = 0; r < NP; r++) {
-                    const int pos = lane + 32 * r;
-                    if (pos < tot) {
-                        const int loc = (pos < len) ? P[r] : s0;
-                        st_global_cs(dst + pos, (ga >= 0) ? ga + loc : __ldg(G.slot_gid + vb + loc));
+                    for (int r = 0; r < NP; r++) {
+                        const int pos = lane + 32 * r;
+                        if (pos < tot) st_global_cs(dst + pos, ga + ((pos < len) ? P[r] : s0));
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < NP; r++) {
+                        const int pos = lane + 32 * r;
+                        if (pos < tot) st_global_cs(dst + pos, __ldg(G.slot_gid + vb + ((pos < len) ? P[r] : s0)));
                     }
                 }
             }
