@@ -77,6 +77,35 @@ def _p32(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
 
 
+class _PathsOwner:
+    """Owns a library-allocated tpgen_paths (device pool memory); frees it when the
+    last tensor view is gone."""
+
+    def __init__(self, paths: _abi.Paths):
+        self.paths = paths
+
+    def __del__(self):
+        try:
+            library().tpgen_paths_free(ctypes.byref(self.paths))
+        except Exception:
+            pass
+
+
+class _DeviceArray:
+    """Zero-copy view of library device memory for torch (``__cuda_array_interface__``)."""
+
+    def __init__(self, owner: _PathsOwner, ptr: int, n: int, typestr: str):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 2, "strides": None}
+
+
+def _as_tensor(owner: _PathsOwner, ptr: int, n: int, typestr: str, device: int):
+    import torch
+
+    return torch.as_tensor(_DeviceArray(owner, ptr, n, typestr), device=torch.device("cuda", device))
+
+
 class _TorchAllocator:
     """Output allocator backed by torch's caching allocator (device memory only)."""
 
@@ -150,8 +179,11 @@ def _wrap(paths: _abi.Paths, stats: _abi.Stats, alloc: Optional[_TorchAllocator]
     if paths.on_device:
         p_off = ctypes.cast(paths.offsets, ctypes.c_void_p).value
         p_v = ctypes.cast(paths.vertices, ctypes.c_void_p).value
-        if alloc is None:
-            raise RuntimeError("device output requires the torch allocator")
+        if alloc is None:  # library pool memory, viewed zero-copy; freed with the last view
+            owner = _PathsOwner(paths)
+            off = _as_tensor(owner, p_off, n + 1, "<i8", int(paths.device))
+            vert = _as_tensor(owner, p_v, nv, "<i4", int(paths.device))
+            return PathSet(off, vert, n, True, st)
         off = alloc.take(p_off).view(alloc.torch.int64)[: n + 1]
         vert = alloc.take(p_v).view(alloc.torch.int32)[:nv]
         lib.tpgen_paths_free(ctypes.byref(paths))
@@ -178,7 +210,7 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
     ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host)."""
     lib = library()
     so, st, n = _csr(graph)
-    alloc = _TorchAllocator(device) if output == "device" else None
+    alloc = None  # outputs come from the library's device memory pool (no Python callback while timing)
     o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
                  alloc, host_out, start_range)
     paths, stats = _abi.Paths(), _abi.Stats()
@@ -191,7 +223,7 @@ def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *,
     """One entry->exit test path per prime path (R15)."""
     lib = library()
     so, st, n = _csr(graph)
-    alloc = _TorchAllocator(device) if output == "device" else None
+    alloc = None
     o = _options(device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(device, stream), alloc)
     pin = None
     keep = []
@@ -248,7 +280,7 @@ class Plan:
                     digest: bool = False, max_paths: int = 0, stream=None, host_out=None,
                     start_range: Optional[Tuple[int, int]] = None) -> PathSet:
         lib = library()
-        alloc = _TorchAllocator(self.device) if output == "device" else None
+        alloc = None
         o = _options(self.device, output, mode, shard, digest, max_paths, 0, _stream_handle(self.device, stream),
                      alloc, host_out, start_range)
         paths, stats = _abi.Paths(), _abi.Stats()

@@ -500,6 +500,15 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     P.chunk_used = 0;
     P.maxgen = 0;
     P.blk_used = 0;
+    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;
+    double hprev = now_ms();
+    auto HT = [&](const char *what) {
+        if (!hdbg) return;
+        cudaStreamSynchronize(s);
+        const double t = now_ms();
+        fprintf(stderr, "[tpgen host] %-24s %8.3f ms\n", what, t - hprev);
+        hprev = t;
+    };
 
     Timer tall, tw, tst;
     cudaEventRecord(tall.a, s);
@@ -557,6 +566,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         TPG_CK(cudaMemcpyAsync(P.d_Wv.p, Vd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     }
     // ---- prime-path phase
+    HT("before pp phase");
     TPG_TRY(dfs_phase<T>(P, G, pp_roots, 0, tail_seg, s, st, launches, ms_dfs, tail));
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
@@ -565,6 +575,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     const int64_t nu = (int64_t)tail;
     st.n_units = nu;
 
+    HT("after dfs phases");
     // ---- canonical order: roots by global id, then preorder of the split forest
     std::vector<int64_t> root_order;
     std::vector<int32_t> root_gid;
@@ -649,6 +660,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         return TPGEN_OK;
     }
 
+    HT("after linearize");
     // ---- allocations (exact sizes)
     OutOwner *ow = new OutOwner();
     ow->device = P.device;
@@ -664,6 +676,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     TPG_TRY(P.items.ensure(std::max<int64_t>(n_items, 1) * sizeof(ItemRec), s));
     TPG_TRY(P.item_pool.ensure(std::max<uint64_t>(tot[C_ITEMV], 1) * 4, s));
 
+    HT("after alloc");
     // ---- canonical writer: replay the record streams at their exact offsets
     ExpandArgs E;
     memset(&E, 0, sizeof(E));
@@ -692,6 +705,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventRecord(tw.b, s);
     TPG_CK(cudaGetLastError());
 
+    HT("before stitch");
     // ---- cross-SCC stitching
     cudaEventRecord(tst.a, s);
     if (n_heads > 0) {
@@ -769,6 +783,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     st.ms_dfs_write = ms_dfs;  // the dominant kernel is the DFS enumerator
     st.gpu_launches = launches;
 
+    HT("before finish_output");
     ow_guard.release();
     TPG_TRY(finish_output(o, ow, n_pp, n_vert, (int64_t *)d_off, (int32_t *)d_vert, s, out));
     st.ms_total = now_ms() - t0;
@@ -924,6 +939,12 @@ tpgen_status init_device(PlanImpl &P, const tpgen_options &o) {
     if (dev < 0) TPG_CK(cudaGetDevice(&dev));
     TPG_CK(cudaSetDevice(dev));
     P.device = dev;
+    // keep freed pool memory cached: outputs and workspaces are recycled call after call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     TPG_CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
     return TPGEN_OK;
 }
