@@ -103,39 +103,73 @@ __global__ void scan_down_kernel(ScanArrays S, int64_t n, const uint64_t *bsum, 
 // follow all of its own output in lexicographic order -- blocks donated later
 // come from deeper levels and so come first (the block list is newest-first).
 // Canonical output order is the preorder of that forest, so each unit's output
-// offsets are obtained by a bottom-up pass (subtree totals, generation by
-// generation) and a top-down pass (children placed after their parent).
+// offset is  off(root) + sum over the edges on its root path of the position of
+// the child inside its parent's output.  Three steps, independent of the
+// forest depth in launches:
+//   lin_init + lin_up_flow: subtree totals bottom-up as a dataflow (the last
+//     child to finish folds its parent; one launch, one atomic per edge);
+//   lin_roots + lin_rel: the position of every unit relative to its parent
+//     (the roots: their canonical offset);
+//   lin_jump: pointer jumping along parent links (ceil(log2(depth+1))
+//     launches), which sums the relative positions along each root path.
 struct LinArgs {
     const uint64_t *cnt[C_NUM];  // own counts
     uint64_t *sub[C_NUM];        // subtree totals
-    uint64_t *off[C_NUM];        // exclusive offsets in canonical order
+    LinNode *node;               // relative offsets / jump links (input of the first jump round)
+    int64_t *parent;             // donor of each unit (-1: a root)
+    int32_t *pending;            // children whose subtree totals are not yet folded
     const int64_t *child_head;
     const int64_t *blk_first;
     const int32_t *blk_count;
     const int64_t *blk_next;
-    const int32_t *gen;
     int64_t n;
     const int64_t *roots;        // root units in canonical order
     int64_t n_roots;
     uint64_t *totals;            // [C_NUM]
 };
 
-__global__ void lin_up_kernel(LinArgs A, int g) {
+__global__ void lin_init_kernel(LinArgs A) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (A.gen[i] != g) continue;
-        uint64_t s[C_NUM];
 #pragma unroll
-        for (int c = 0; c < C_NUM; c++) s[c] = A.cnt[c][i];
+        for (int c = 0; c < C_NUM; c++) A.sub[c][i] = A.cnt[c][i];
+        int32_t nc = 0;
         for (int64_t b = A.child_head[i]; b >= 0; b = A.blk_next[b]) {
             const int64_t cf = A.blk_first[b];
             const int32_t cc = A.blk_count[b];
-            for (int32_t k = 0; k < cc; k++) {
-#pragma unroll
-                for (int c = 0; c < C_NUM; c++) s[c] += A.sub[c][cf + k];
-            }
+            for (int32_t k = 0; k < cc; k++) A.parent[cf + k] = i;
+            nc += cc;
         }
+        A.pending[i] = nc;
+    }
+}
+
+// Leaves start; a unit whose last pending child just finished is folded by
+// that child's thread, which then continues upward.
+__global__ void lin_up_flow_kernel(LinArgs A) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (A.child_head[i] >= 0) continue;
+        int64_t cur = i;
+        for (;;) {
+            const int64_t p = A.parent[cur];
+            if (p < 0) break;
+            __threadfence();  // cur's subtree totals before the decrement
+            if (atomicSub(A.pending + p, 1) != 1) break;
+            __threadfence();
+            uint64_t s[C_NUM];
 #pragma unroll
-        for (int c = 0; c < C_NUM; c++) A.sub[c][i] = s[c];
+            for (int c = 0; c < C_NUM; c++) s[c] = A.cnt[c][p];
+            for (int64_t b = A.child_head[p]; b >= 0; b = A.blk_next[b]) {
+                const int64_t cf = A.blk_first[b];
+                const int32_t cc = A.blk_count[b];
+                for (int32_t k = 0; k < cc; k++) {
+#pragma unroll
+                    for (int c = 0; c < C_NUM; c++) s[c] += __ldcg(A.sub[c] + cf + k);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < C_NUM; c++) A.sub[c][p] = s[c];
+            cur = p;
+        }
     }
 }
 
@@ -149,30 +183,52 @@ __global__ void lin_roots_kernel(LinArgs A) {
             const uint64_t v = (j < A.n_roots) ? A.sub[c][A.roots[j]] : 0;
             uint64_t tot;
             const uint64_t ex = block_excl_scan(v, sm, tot);
-            if (j < A.n_roots) A.off[c][A.roots[j]] = ex + carry;
+            if (j < A.n_roots) {
+                A.node[A.roots[j]].v[c] = ex + carry;
+                if (c == 0) A.node[A.roots[j]].jmp = -1;
+            }
             carry += tot;
         }
         if (threadIdx.x == 0) A.totals[c] = carry;
     }
 }
 
-__global__ void lin_down_kernel(LinArgs A, int g) {
+// Children placed after their parent's own output, newest block first.
+__global__ void lin_rel_kernel(LinArgs A) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (A.gen[i] != g || A.child_head[i] < 0) continue;
+        if (A.child_head[i] < 0) continue;
         uint64_t base[C_NUM];
 #pragma unroll
-        for (int c = 0; c < C_NUM; c++) base[c] = A.off[c][i] + A.cnt[c][i];
+        for (int c = 0; c < C_NUM; c++) base[c] = A.cnt[c][i];
         for (int64_t b = A.child_head[i]; b >= 0; b = A.blk_next[b]) {
             const int64_t cf = A.blk_first[b];
             const int32_t cc = A.blk_count[b];
             for (int32_t k = 0; k < cc; k++) {
+                LinNode nd;
 #pragma unroll
                 for (int c = 0; c < C_NUM; c++) {
-                    A.off[c][cf + k] = base[c];
+                    nd.v[c] = base[c];
                     base[c] += A.sub[c][cf + k];
                 }
+                nd.jmp = i;
+                nd.pad = 0;
+                A.node[cf + k] = nd;
             }
         }
+    }
+}
+
+// One round of pointer jumping (Wyllie): v += v[jmp], jmp = jmp[jmp].
+__global__ void lin_jump_kernel(const LinNode *in, LinNode *out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        LinNode a = in[i];
+        if (a.jmp >= 0) {
+            const LinNode b = in[a.jmp];
+#pragma unroll
+            for (int c = 0; c < C_NUM; c++) a.v[c] += b.v[c];
+            a.jmp = b.jmp;
+        }
+        out[i] = a;
     }
 }
 
@@ -188,11 +244,11 @@ __global__ void sum_kernel(const uint64_t *a, int64_t n, unsigned long long *out
 // --------------------------------------------------- segment tables (a5)
 // Items of entry vertex x are the items of the subtree of x's root unit.
 __global__ void item_bounds_kernel(const int64_t *roots, const int32_t *root_gid, int64_t n_roots,
-                                   const uint64_t *off_items, const uint64_t *sub_items, int64_t *ibeg, int64_t *iend) {
+                                   const LinNode *off, const uint64_t *sub_items, int64_t *ibeg, int64_t *iend) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_roots; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = roots[j];
-        ibeg[root_gid[j]] = (int64_t)off_items[r];
-        iend[root_gid[j]] = (int64_t)(off_items[r] + sub_items[r]);
+        ibeg[root_gid[j]] = (int64_t)off[r].v[C_ITEMS];
+        iend[root_gid[j]] = (int64_t)(off[r].v[C_ITEMS] + sub_items[r]);
     }
 }
 

@@ -594,42 +594,60 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     }
     const int64_t n_roots = (int64_t)root_order.size();
     const size_t nu1 = (size_t)std::max<int64_t>(nu, 1);
-    TPG_TRY(P.offs.ensure(nu1 * 8 * 2 * C_NUM + 64, s));
+    // scratch: sub[C_NUM] | node ping | node pong | parent | pending
+    const size_t lin_bytes = nu1 * (8 * C_NUM + 2 * sizeof(LinNode) + 8 + 4) + 256;
+    TPG_TRY(P.offs.ensure(lin_bytes, s));
     TPG_TRY(P.roots.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
     if (n_roots) {
         TPG_CK(cudaMemcpyAsync(P.roots.p, root_order.data(), n_roots * 8, cudaMemcpyHostToDevice, s));
         TPG_CK(cudaMemcpyAsync(P.roots.as<char>() + n_roots * 8, root_gid.data(), n_roots * 4, cudaMemcpyHostToDevice,
                                s));
     }
-    uint64_t *off[C_NUM], *sub[C_NUM];
+    uint64_t *sub[C_NUM];
     unsigned long long *ctr = P.ctr.as<unsigned long long>();
     uint64_t *tot_d = reinterpret_cast<uint64_t *>(ctr + 8);
     LinArgs LA;
+    char *lp = P.offs.as<char>();
     for (int c = 0; c < C_NUM; c++) {
-        sub[c] = P.offs.as<uint64_t>() + (size_t)c * nu1;
-        off[c] = P.offs.as<uint64_t>() + (size_t)(C_NUM + c) * nu1;
+        sub[c] = reinterpret_cast<uint64_t *>(lp) + (size_t)c * nu1;
         LA.cnt[c] = P.qcnt[c].as<uint64_t>();
         LA.sub[c] = sub[c];
-        LA.off[c] = off[c];
     }
+    lp += nu1 * 8 * C_NUM;
+    LinNode *node[2] = {reinterpret_cast<LinNode *>(lp), reinterpret_cast<LinNode *>(lp) + nu1};
+    lp += nu1 * 2 * sizeof(LinNode);
+    LA.node = node[0];
+    LA.parent = reinterpret_cast<int64_t *>(lp);
+    LA.pending = reinterpret_cast<int32_t *>(lp + nu1 * 8);
     LA.child_head = P.qchead.as<int64_t>();
     LA.blk_first = P.blk_first.as<int64_t>();
     LA.blk_count = P.blk_count.as<int32_t>();
     LA.blk_next = P.blk_next.as<int64_t>();
-    LA.gen = P.qgen.as<int32_t>();
     LA.n = nu;
     LA.roots = P.roots.as<int64_t>();
     LA.n_roots = n_roots;
     LA.totals = tot_d;
+    const LinNode *off = node[0];  // final canonical offsets
     uint64_t tot[C_NUM + 1] = {0};
     if (nu > 0) {
         const int lg = grid_for(nu, 256, P.num_sms * 8);
-        for (int g = P.maxgen; g >= 0; g--) lin_up_kernel<<<lg, 256, 0, s>>>(LA, g);
+        TPG_CK(cudaMemsetAsync(LA.parent, 0xff, (size_t)nu * 8, s));
+        lin_init_kernel<<<lg, 256, 0, s>>>(LA);
+        lin_up_flow_kernel<<<lg, 256, 0, s>>>(LA);
         lin_roots_kernel<<<1, kScanThreads, 0, s>>>(LA);
-        for (int g = 0; g <= P.maxgen; g++) lin_down_kernel<<<lg, 256, 0, s>>>(LA, g);
+        lin_rel_kernel<<<lg, 256, 0, s>>>(LA);
+        launches += 4;
+        // rounds: after r rounds a unit has summed its 2^r nearest ancestors' relative offsets
+        int rounds = 0;
+        while ((1ll << rounds) < (long long)P.maxgen + 1) rounds++;
+        for (int r = 0; r < rounds; r++) {
+            lin_jump_kernel<<<lg, 256, 0, s>>>(node[r & 1], node[(r + 1) & 1], nu);
+            launches++;
+        }
+        off = node[rounds & 1];
         TPG_CK(cudaMemsetAsync(ctr + 14, 0, 8, s));
         sum_kernel<<<lg, 256, 0, s>>>(P.qext.as<uint64_t>(), nu, ctr + 14);
-        launches += 2 * (P.maxgen + 1) + 2;
+        launches++;
         TPG_CK(cudaMemcpyAsync(tot, tot_d, C_NUM * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaMemcpyAsync(tot + C_NUM, ctr + 14, 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
@@ -685,7 +703,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     E.n_units = nu;
     E.rfirst = P.qrfirst.as<int64_t>();
     E.rcount = P.qrcount.as<int64_t>();
-    for (int c = 0; c < C_NUM; c++) E.off[c] = off[c];
+    E.off = off;
     E.chunks = P.chunks.as<uint64_t>();
     E.out_off = (int64_t *)d_off;
     E.out_vert = (int32_t *)d_vert;
@@ -731,7 +749,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         }
         item_bounds_kernel<<<grid_for(n_roots, 256, 4096), 256, 0, s>>>(
             P.roots.as<int64_t>(), reinterpret_cast<const int32_t *>(P.roots.as<char>() + n_roots * 8), n_roots,
-            off[C_ITEMS], sub[C_ITEMS], P.ibeg.as<int64_t>(), P.iend.as<int64_t>());
+            off, sub[C_ITEMS], P.ibeg.as<int64_t>(), P.iend.as<int64_t>());
         launches++;
         StitchArgs SA;
         SA.heads = P.heads.as<HeadRec>();

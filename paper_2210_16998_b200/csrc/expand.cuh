@@ -21,7 +21,7 @@ struct ExpandArgs {
     int64_t n_units;
     const int64_t *rfirst;
     const int64_t *rcount;
-    const uint64_t *off[C_NUM];  // canonical exclusive offsets of each unit's outputs
+    const LinNode *off;  // canonical exclusive offsets of each unit's outputs
     const uint64_t *chunks;
     int64_t *out_off;
     int32_t *out_vert;
@@ -59,9 +59,10 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
         const int vb = __ldg(G.scc_vbase + h.x);
         const int ga = __ldg(G.scc_gbase + h.x);
         const int sgid = __ldg(G.slot_gid + vb + __shfl_sync(kFull, P[0], 0));
-        uint64_t pp = A.off[C_PP][u], vv = A.off[C_VERT][u];
-        uint64_t it = A.off[C_ITEMS][u], itv = A.off[C_ITEMV][u];
-        uint64_t hd = A.off[C_HEADS][u], hdv = A.off[C_HEADV][u];
+        const LinNode *on = A.off + u;
+        uint64_t pp = on->v[C_PP], vv = on->v[C_VERT];
+        uint64_t it = on->v[C_ITEMS], itv = on->v[C_ITEMV];
+        uint64_t hd = on->v[C_HEADS], hdv = on->v[C_HEADV];
         const int64_t nrec = A.rcount[u];
         const uint64_t *ch = A.chunks + A.rfirst[u] * kChunkRecs;
         int slot = 0;  // next record slot in chunk `ch`

@@ -118,6 +118,13 @@ struct __align__(16) Unit {
     uint8_t pad[3];
 };
 
+// Canonical offsets of one units outputs (linearization, aux_kernels.cuh).
+struct __align__(16) LinNode {
+    uint64_t v[C_NUM];  // offsets (relative to the jump target until the jumping ends)
+    int64_t jmp;        // ancestor still to be added (-1: none)
+    int64_t pad;
+};
+
 struct DevGraph {
     const void *slots;  // Slot<W>[n]
     const int32_t *slot_gid;
