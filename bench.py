@@ -79,6 +79,11 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (NVML init) stalls the device: let it finish before the timed region
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.02)
+            time.sleep(0.3)
         except Exception:
             self.proc = None
         return self

@@ -106,8 +106,8 @@ __global__ void scan_down_kernel(ScanArrays S, int64_t n, const uint64_t *bsum, 
 // offset is  off(root) + sum over the edges on its root path of the position of
 // the child inside its parent's output.  Three steps, independent of the
 // forest depth in launches:
-//   lin_init + lin_up_flow: subtree totals bottom-up as a dataflow (the last
-//     child to finish folds its parent; one launch, one atomic per edge);
+//   lin_up_flow: subtree totals bottom-up as a dataflow (the last child to
+//     finish closes its parent; one launch, one decrement per edge);
 //   lin_roots + lin_rel: the position of every unit relative to its parent
 //     (the roots: their canonical offset);
 //   lin_jump: pointer jumping along parent links (ceil(log2(depth+1))
@@ -116,8 +116,9 @@ struct LinArgs {
     const uint64_t *cnt[C_NUM];  // own counts
     uint64_t *sub[C_NUM];        // subtree totals
     LinNode *node;               // relative offsets / jump links (input of the first jump round)
-    int64_t *parent;             // donor of each unit (-1: a root)
-    int32_t *pending;            // children whose subtree totals are not yet folded
+    uint64_t *acc[C_NUM];        // sums of the children's subtree totals (zeroed before lin_up_flow)
+    const int64_t *parent;       // donor of each unit (-1: a root)
+    int32_t *pending;            // children whose subtree totals are still open (consumed)
     const int64_t *child_head;
     const int64_t *blk_first;
     const int32_t *blk_count;
@@ -128,47 +129,29 @@ struct LinArgs {
     uint64_t *totals;            // [C_NUM]
 };
 
-__global__ void lin_init_kernel(LinArgs A) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-        for (int c = 0; c < C_NUM; c++) A.sub[c][i] = A.cnt[c][i];
-        int32_t nc = 0;
-        for (int64_t b = A.child_head[i]; b >= 0; b = A.blk_next[b]) {
-            const int64_t cf = A.blk_first[b];
-            const int32_t cc = A.blk_count[b];
-            for (int32_t k = 0; k < cc; k++) A.parent[cf + k] = i;
-            nc += cc;
-        }
-        A.pending[i] = nc;
-    }
-}
-
-// Leaves start; a unit whose last pending child just finished is folded by
-// that child's thread, which then continues upward.
+// Leaves start; every unit passes its subtree total to its donor with plain
+// atomic adds, then decrements the donor's open-children count -- whoever
+// closes the donor continues with it.  One launch; the critical path is one
+// atomic round trip per level of the deepest donation chain.
 __global__ void lin_up_flow_kernel(LinArgs A) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
         if (A.child_head[i] >= 0) continue;
         int64_t cur = i;
+        uint64_t t[C_NUM];
+#pragma unroll
+        for (int c = 0; c < C_NUM; c++) t[c] = A.cnt[c][cur];
         for (;;) {
+#pragma unroll
+            for (int c = 0; c < C_NUM; c++) A.sub[c][cur] = t[c];
             const int64_t p = A.parent[cur];
             if (p < 0) break;
-            __threadfence();  // cur's subtree totals before the decrement
-            if (atomicSub(A.pending + p, 1) != 1) break;
-            __threadfence();
-            uint64_t s[C_NUM];
 #pragma unroll
-            for (int c = 0; c < C_NUM; c++) s[c] = A.cnt[c][p];
-            for (int64_t b = A.child_head[p]; b >= 0; b = A.blk_next[b]) {
-                const int64_t cf = A.blk_first[b];
-                const int32_t cc = A.blk_count[b];
-                for (int32_t k = 0; k < cc; k++) {
-#pragma unroll
-                    for (int c = 0; c < C_NUM; c++) s[c] += __ldcg(A.sub[c] + cf + k);
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < C_NUM; c++) A.sub[c][p] = s[c];
+            for (int c = 0; c < C_NUM; c++)
+                if (t[c]) atomicAdd(reinterpret_cast<unsigned long long *>(A.acc[c] + p), (unsigned long long)t[c]);
+            if (atom_dec_acq_rel(A.pending + p) != 1) break;
             cur = p;
+#pragma unroll
+            for (int c = 0; c < C_NUM; c++) t[c] = A.cnt[c][cur] + ld_relaxed_u64(A.acc[c] + cur);
         }
     }
 }

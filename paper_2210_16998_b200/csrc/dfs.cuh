@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     R.count = 0;
 
     int64_t child_head = -1;  // latest donated block of the running unit
+    int nchild = 0;           // units donated by the running unit
 #ifdef TPGEN_KERNEL_DEBUG
     unsigned long long d_it = 0, d_act = 0, d_don = 0;
     const unsigned long long t0 = A.dbg ? A.dbg[7] : 0;
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 L.done = false;
                 L.active = true;
                 child_head = -1;
+                nchild = 0;
                 last_split = 0;
                 L.base = depth + 1;
                 L.pn = 0;
@@ -647,11 +649,13 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     for (int i = 0; i < m; i++) {
                         A.gen[base + i] = ugen + 1;
                         A.child_head[base + i] = -1;
+                        A.parent[base + i] = slot;
                     }
                     A.blk_first[b] = (int64_t)base;
                     A.blk_count[b] = m;
                     A.blk_next[b] = child_head;
                     child_head = (int64_t)b;
+                    nchild += m;
                     atomicMax(A.maxgen, ugen + 1);
                     for (int i = 0; i < m; i++) st_release(A.ready + base + i, 1u);  // publish after the unit data
                     if (j0 == L.l) L.done = true;  // nothing left below the donated level
@@ -675,6 +679,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             A.ext[slot] = ext;
             A.rcount[slot] = R.count;
             A.child_head[slot] = child_head;
+            A.nchild[slot] = nchild;
             atomicAdd(A.qtd, 1ull);  // done += 1 (same word as the tail: termination needs no fence)
             L.active = false;
             L.done = false;

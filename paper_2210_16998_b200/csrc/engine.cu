@@ -83,7 +83,7 @@ PlanImpl::~PlanImpl() {
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
-                               &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots,
+                               &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
@@ -337,6 +337,8 @@ static tpgen_status grow_queue(PlanImpl &P, uint64_t used, uint64_t cap, cudaStr
     TPG_TRY(grow_keep(P.blk_count, P.blk_used, cap, 4, s));
     TPG_TRY(grow_keep(P.blk_next, P.blk_used, cap, 8, s));
     TPG_TRY(grow_keep(P.qgen, used, cap, 4, s));
+    TPG_TRY(grow_keep(P.qparent, used, cap, 8, s));
+    TPG_TRY(grow_keep(P.qnchild, used, cap, 4, s));
     P.qcap = cap;
     return TPGEN_OK;
 }
@@ -352,6 +354,7 @@ static tpgen_status put_roots(PlanImpl &P, const std::vector<Unit<W>> &roots, ui
     TPG_CK(cudaMemcpyAsync(P.qready.as<uint32_t>() + qbase, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
     TPG_CK(cudaMemsetAsync(P.qgen.as<int32_t>() + qbase, 0, n * 4, s));
     TPG_CK(cudaMemsetAsync(P.qchead.as<int64_t>() + qbase, 0xff, n * 8, s));  // -1: no donated block
+    TPG_CK(cudaMemsetAsync(P.qparent.as<int64_t>() + qbase, 0xff, n * 8, s));  // -1: a root
     return TPGEN_OK;
 }
 
@@ -404,6 +407,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.blk_next = P.blk_next.as<int64_t>();
         A.blk_ctr = qc + 80;
         A.gen = P.qgen.as<int32_t>();
+        A.parent = P.qparent.as<int64_t>();
+        A.nchild = P.qnchild.as<int32_t>();
         A.maxgen = reinterpret_cast<int *>(qc + 64);
         unsigned long long *agg = P.agg.as<unsigned long long>();
         A.agg_tail_cnt = agg;
@@ -594,9 +599,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     }
     const int64_t n_roots = (int64_t)root_order.size();
     const size_t nu1 = (size_t)std::max<int64_t>(nu, 1);
-    // scratch: sub[C_NUM] | node ping | node pong | parent | pending
-    const size_t lin_bytes = nu1 * (8 * C_NUM + 2 * sizeof(LinNode) + 8 + 4) + 256;
-    TPG_TRY(P.offs.ensure(lin_bytes, s));
+    // scratch: sub[C_NUM] | acc[C_NUM] | node ping | node pong
+    TPG_TRY(P.offs.ensure(nu1 * (16 * C_NUM + 2 * sizeof(LinNode)) + 256, s));
     TPG_TRY(P.roots.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
     if (n_roots) {
         TPG_CK(cudaMemcpyAsync(P.roots.p, root_order.data(), n_roots * 8, cudaMemcpyHostToDevice, s));
@@ -607,18 +611,18 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     unsigned long long *ctr = P.ctr.as<unsigned long long>();
     uint64_t *tot_d = reinterpret_cast<uint64_t *>(ctr + 8);
     LinArgs LA;
-    char *lp = P.offs.as<char>();
+    uint64_t *lp = P.offs.as<uint64_t>();
     for (int c = 0; c < C_NUM; c++) {
-        sub[c] = reinterpret_cast<uint64_t *>(lp) + (size_t)c * nu1;
+        sub[c] = lp + (size_t)c * nu1;
         LA.cnt[c] = P.qcnt[c].as<uint64_t>();
         LA.sub[c] = sub[c];
+        LA.acc[c] = lp + (size_t)(C_NUM + c) * nu1;
     }
-    lp += nu1 * 8 * C_NUM;
-    LinNode *node[2] = {reinterpret_cast<LinNode *>(lp), reinterpret_cast<LinNode *>(lp) + nu1};
-    lp += nu1 * 2 * sizeof(LinNode);
+    LinNode *node[2] = {reinterpret_cast<LinNode *>(lp + 2 * C_NUM * nu1),
+                        reinterpret_cast<LinNode *>(lp + 2 * C_NUM * nu1) + nu1};
     LA.node = node[0];
-    LA.parent = reinterpret_cast<int64_t *>(lp);
-    LA.pending = reinterpret_cast<int32_t *>(lp + nu1 * 8);
+    LA.parent = P.qparent.as<int64_t>();
+    LA.pending = P.qnchild.as<int32_t>();
     LA.child_head = P.qchead.as<int64_t>();
     LA.blk_first = P.blk_first.as<int64_t>();
     LA.blk_count = P.blk_count.as<int32_t>();
@@ -631,12 +635,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     uint64_t tot[C_NUM + 1] = {0};
     if (nu > 0) {
         const int lg = grid_for(nu, 256, P.num_sms * 8);
-        TPG_CK(cudaMemsetAsync(LA.parent, 0xff, (size_t)nu * 8, s));
-        lin_init_kernel<<<lg, 256, 0, s>>>(LA);
+        TPG_CK(cudaMemsetAsync(LA.acc[0], 0, (size_t)C_NUM * nu1 * 8, s));
         lin_up_flow_kernel<<<lg, 256, 0, s>>>(LA);
         lin_roots_kernel<<<1, kScanThreads, 0, s>>>(LA);
         lin_rel_kernel<<<lg, 256, 0, s>>>(LA);
-        launches += 4;
+        launches += 3;
         // rounds: after r rounds a unit has summed its 2^r nearest ancestors' relative offsets
         int rounds = 0;
         while ((1ll << rounds) < (long long)P.maxgen + 1) rounds++;

@@ -35,6 +35,7 @@ struct PlanImpl {
         d_slot_eidx, d_Wc, d_Wv, d_scc_gbase;
     // DFS work queue (one slot per unit) and its per-unit results
     DevBuf qunits, qready, qcnt[kCnt], qext, qrfirst, qrcount, qchead, qgen, roots;
+    DevBuf qparent, qnchild;  // donor / number of donated units, per unit
     DevBuf blk_first, blk_count, blk_next;  // donated blocks (one per donation)
     uint64_t qcap = 0;
     uint64_t blk_used = 0;

@@ -159,6 +159,8 @@ struct DfsArgs {
     int64_t *blk_next;        // donated block: the unit's previous block (-1: none)
     unsigned long long *blk_ctr;
     int32_t *gen;             // donation generation (roots 0)
+    int64_t *parent;          // donor of the unit (roots: -1, set by the host)
+    int32_t *nchild;          // number of units the unit donated
     int *maxgen;
     unsigned long long *agg_tail_cnt, *agg_tail_len, *agg_pair_cnt, *agg_pair_len;
     unsigned int *overflow;   // bit 0: count overflow, bit 1: record pool exhausted, bit 2: queue full
@@ -216,6 +218,19 @@ __device__ __forceinline__ int count_out_le(const DevGraph &G, int out_off, int 
     int o = 0;
     while (o < out_cnt && __ldg(G.out_pos + out_off + o) <= w) o++;
     return o;
+}
+
+// dataflow hand-off: the decrement releases the caller's earlier additions and
+// acquires those of every earlier decrementer
+__device__ __forceinline__ int atom_dec_acq_rel(int *p) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b, unsigned int *ovf) {
