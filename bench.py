@@ -46,19 +46,60 @@ def measured_peaks():
         return HBM_FALLBACK, "fallback"
 
 
-def workload(n_ranks: int):
-    base = gen.config3()
+def workload(n_ranks: int, base=None):
+    """Weak scaling: rank r enumerates the r-th of n_ranks disjoint
+    copies of the config-3 graph, i.e. the start-vertex range [r*n, (r+1)*n) of
+    their union; its output is that contiguous block of the union's canonical list."""
+    base = gen.config3() if base is None else base
     if n_ranks == 1:
         return base, [(0, base.n)]
     g = gen.disjoint_union([base] * n_ranks, name=f"{n_ranks}x_{base.name}")
     return g, [(r * base.n, (r + 1) * base.n) for r in range(n_ranks)]
 
 
+def rank_reduce(dist, world: int, n_pp: float, ext: float, ms_total: float, e2e_ms: float, device):
+    """Whole-job totals: PP and extension counts summed over ranks, times maxed
+    (the slowest rank defines the job time)."""
+    import torch
+
+    vals = torch.tensor([n_pp, ext, ms_total, e2e_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        sums = vals[:2].clone()
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        mx = vals[2:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        vals = torch.cat([sums, mx])
+    return vals.tolist()
+
+
 # SURVEY.md §8(d): algorithmic bytes per unit of the hot path --
 # 2 x (8W + 1 + 4) B per extension (frontier record written + read, W = 1)
 # + (4 len + 8) B per prime path (int32 vertices + int64 offset).
 def algorithmic_bytes(ext: int, n_pp: int, n_vert: int) -> float:
+    """A = 2*(8W+1+4)*E_canon + sum_PP (4 len + 8)  (W = 1 here)."""
     return 2.0 * 13.0 * ext + 4.0 * n_vert + 8.0 * n_pp
+
+
+def output_bytes(n_pp: int, n_vert: int) -> float:
+    """What expand_kernel must write: int32 vertices + int64 offsets."""
+    return 4.0 * n_vert + 8.0 * (n_pp + 1)
+
+
+# ALU ceiling of the DFS enumerator (DESIGN.md "Rooflines"): 148 SMs x 128 INT32
+# lanes x SM clock / 30 lane-ops per extension (SURVEY.md 8(d): "K1 does ~10-30
+# int ops per extension"; the upper figure, so the ceiling is not overstated).
+ALU_LANES = 148 * 128
+OPS_PER_EXT = 30.0
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) from the
+    committed ncu --set full summary of this round (profiles/), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 class ClockSampler:
@@ -242,24 +283,51 @@ def main():
                "ms_per_step": e2e_ms, "steps": e2e_steps}
 
     # ---------------- reduce over ranks
-    vals = torch.tensor([float(n_pp) * args.steps, float(ext) * args.steps, ms_total,
-                         e2e["ms_per_step"] if e2e else 0.0], dtype=torch.float64, device=dev)
-    if world > 1:
-        sums = vals.clone()
-        dist.all_reduce(sums[:2], op=dist.ReduceOp.SUM)
-        mx = vals.clone()
-        dist.all_reduce(mx[2:], op=dist.ReduceOp.MAX)
-        vals = torch.cat([sums[:2], mx[2:]])
-    tot_pp, tot_ext, ms_max, e2e_ms_max = vals.tolist()
+    tot_pp, tot_ext, ms_max, e2e_ms_max = rank_reduce(dist, world, float(n_pp) * args.steps, float(ext) * args.steps,
+                                                      ms_total, e2e["ms_per_step"] if e2e else 0.0, dev)
 
     if rank == 0:
         peak, peak_kind = measured_peaks()
         a_bytes = algorithmic_bytes(ext, n_pp, n_vert)
-        achieved = a_bytes / (ms_write * 1e-3) / 1e9
+        o_bytes = output_bytes(n_pp, n_vert)
         value = tot_pp / (ms_max * 1e-3)
         if e2e is not None:
             e2e["value"] = (tot_pp / args.steps) / (e2e_ms_max * 1e-3)
             e2e["ms_per_step"] = e2e_ms_max
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                sm_max = float(json.load(f).get("sm_max_mhz", 1965.0))
+        except Exception:
+            sm_max = 1965.0
+        ms_dfs = float(np.mean([s["ms_dfs_write"] for s in stats]))
+        ms_expand = float(np.mean([s["ms_write"] for s in stats]))
+        ms_dev = float(np.mean([s["ms_device"] for s in stats]))
+        alu_peak = ALU_LANES * sm_max * 1e6 / OPS_PER_EXT / 1e9  # Gext/s
+        dfs_ach = ext / (ms_dfs * 1e-3) / 1e9
+        traffic = ncu_traffic()
+        roofline = {
+            "bound": "alu", "kernel": "dfs_kernel<uint32_t,TS=1>",
+            "achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak,
+            "traffic": traffic.get("dfs_kernel", {}).get("dram_bytes_per_launch"),
+            "ms_per_launch": ms_dfs, "units_per_launch": ext,
+            "peak_model": f"148 SM x 128 INT32 lanes x {sm_max:.0f} MHz / {OPS_PER_EXT:.0f} lane-ops per extension "
+                          "(SURVEY 8(d)); DESIGN.md Rooflines",
+            "share_of_step": ms_dfs / ms_dev,
+            "second": {
+                "bound": "hbm", "kernel": "expand_kernel<1,1>",
+                "achieved": o_bytes / (ms_expand * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": o_bytes / (ms_expand * 1e-3) / 1e9 / peak,
+                "traffic": traffic.get("expand_kernel", {}).get("dram_bytes_per_launch"),
+                "algorithmic_bytes_per_launch": o_bytes, "ms_per_launch": ms_expand,
+                "share_of_step": ms_expand / ms_dev,
+                "model": "4 B per output vertex + 8 B per offset (written once)"},
+            "path_hbm": {
+                "achieved": a_bytes / (ms_dev * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": a_bytes / (ms_dev * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,
+                "model": "SURVEY 8(d): 26 B/extension + (4 len + 8) B/prime path, over the whole step"},
+            "peak_kind": peak_kind,
+            "traffic_source": traffic.get("source"),
+        }
         out = {
             "metric": "prime_paths_per_sec",
             "value": value,
@@ -279,14 +347,11 @@ def main():
                        "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",
                        "parallelism": f"start-vertex shards x{world}"},
             "extensions_per_sec": tot_ext / (ms_max * 1e-3),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "dfs_kernel<1,PASS_WRITE>",
-                         "algorithmic_bytes_per_launch": a_bytes, "ms_per_launch": ms_write,
-                         "peak_kind": peak_kind,
-                         "model": "SURVEY 8(d): 26 B/extension + (4 len + 8) B/prime path"},
-            "breakdown_ms": {k: float(np.mean([s[k] for s in stats]))
-                             for k in ("ms_count", "ms_dfs_count", "ms_write", "ms_stitch", "ms_device")},
+            "roofline": roofline,
+            "breakdown_ms": {"dfs_kernel": ms_dfs, "linearize": float(np.mean([s["ms_count"] - s["ms_dfs_count"]
+                                                                                for s in stats])),
+                             "expand_kernel": ms_expand,
+                             "stitch": float(np.mean([s["ms_stitch"] for s in stats])), "device": ms_dev},
             "count_rounds": st["n_count_rounds"],
             "n_units": st["n_units"],
             "gpu_launches": launches,

@@ -57,7 +57,7 @@ typedef enum {
                                        or its last vertex cannot reach exit */
     TPGEN_ERR_CUDA = 6,             /* CUDA runtime error (no device, launch failure, ...) */
     TPGEN_ERR_INTERNAL = 7,         /* invariant violated inside the library */
-    TPGEN_ERR_UNSUPPORTED = 8       /* a strongly connected component with more than 64 vertices */
+    TPGEN_ERR_UNSUPPORTED = 8       /* a strongly connected component with more than 256 vertices */
 } tpgen_status;
 
 enum { TPGEN_OUT_MATERIALIZE = 0, TPGEN_OUT_COUNT_HASH = 1 };
@@ -104,7 +104,7 @@ typedef struct {
     int64_t total_vertices;  /* offsets[n_paths] */
     int64_t n_extensions;    /* E_canon of this shard's start vertices */
     int64_t n_cross;         /* prime paths spanning >= 2 SCCs */
-    int64_t n_units;         /* work units of the final write pass */
+    int64_t n_units;         /* DFS work units (roots + donated) */
     int64_t n_heads;         /* head segments (cross-PP blocks) */
     int64_t n_segments;      /* transit + tail segment items */
     uint64_t hash_lo, hash_hi;  /* order-independent multiset digest */
@@ -112,13 +112,13 @@ typedef struct {
     int64_t gpu_launches;    /* kernels this call launched */
     int32_t shard_lo, shard_hi;  /* start-vertex range of this shard */
     double ms_plan;          /* host planning (Tarjan, tables) */
-    double ms_count;         /* device: count + refine rounds */
-    double ms_write;         /* device: write pass (K1 write) */
-    double ms_stitch;        /* device: segment scan + stitch writer */
+    double ms_count;         /* device: DFS phases + linearization (ms_device - ms_write - ms_stitch) */
+    double ms_write;         /* device: canonical writer (expand_kernel) */
+    double ms_stitch;        /* device: segment scans + stitch writer */
     double ms_device;        /* device time of the whole pipeline (CUDA events) */
     double ms_total;         /* wall clock of the call */
-    double ms_dfs_write;     /* device time of the dominant kernel (DFS write pass) */
-    double ms_dfs_count;     /* device time summed over the DFS count launches */
+    double ms_dfs_write;     /* device time of the dominant kernel (dfs_kernel, both phases) */
+    double ms_dfs_count;     /* same as ms_dfs_write (kept for ABI stability) */
 } tpgen_stats;
 
 void tpgen_options_init(tpgen_options *opt);

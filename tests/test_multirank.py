@@ -1,0 +1,108 @@
+"""World-size-2 `gloo` test of the multi-rank path, CPU only.
+
+bench.py's N>1 run gives rank r the start-vertex range of the r-th disjoint
+copy of the workload graph and reduces counts (sum) and times (max) over the
+ranks.  Here each rank computes its block with the ORACLE (no GPU on this box)
+and the test checks, across two real processes talking over gloo:
+  * the rank blocks concatenate to the canonical list of the whole union graph
+    (shards are contiguous blocks of the global order);
+  * bench.rank_reduce sums the counts and maxes the times;
+  * the order-independent digests of the blocks add up to the whole digest.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank: int, world: int, port: int, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import oracle
+    from workloads import generators as gen
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        base = gen.dense_scc(9, 3, 2)
+        g, ranges = bench.workload(world, base=base)
+        lo, hi = ranges[rank]
+        off, vert = oracle.prime_paths(g, v_lo=lo, v_hi=hi)
+        n_pp = len(off) - 1
+        ext = oracle.ext_count(g, v_lo=lo, v_hi=hi)
+        tot_pp, tot_ext, ms_max, e2e_max = bench.rank_reduce(dist, world, float(n_pp), float(ext),
+                                                             1.0 + rank, 10.0 * (rank + 1), "cpu")
+        # gather the blocks to rank 0 (object collective over gloo)
+        blocks = [None] * world
+        dist.all_gather_object(blocks, (off.tolist(), vert.tolist()))
+        h = oracle.digest(off, vert)
+        hs = torch.tensor([h[0] & 0xFFFFFFFF, h[0] >> 32, h[1] & 0xFFFFFFFF, h[1] >> 32], dtype=torch.float64)
+        parts = [torch.zeros_like(hs) for _ in range(world)]
+        dist.all_gather(parts, hs)
+        if rank == 0:
+            q.put(dict(tot_pp=tot_pp, tot_ext=tot_ext, ms_max=ms_max, e2e_max=e2e_max, blocks=blocks,
+                       parts=[p.tolist() for p in parts], n=g.n))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_shards_and_reduce():
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    from workloads import generators as gen
+    import bench
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+
+    base = gen.dense_scc(9, 3, 2)
+    g, _ = bench.workload(world, base=base)
+    off, vert = oracle.prime_paths(g)
+    # concatenation of the rank blocks == the whole canonical list
+    cat_off, cat_vert = [0], []
+    for bo, bv in res["blocks"]:
+        shift = cat_off[-1]
+        cat_off.extend(shift + np.asarray(bo[1:], dtype=np.int64))
+        cat_vert.extend(bv)
+    assert np.array_equal(np.asarray(cat_off, dtype=np.int64), off)
+    assert np.array_equal(np.asarray(cat_vert, dtype=np.int32), vert)
+    # reductions: counts summed, times maxed
+    assert res["tot_pp"] == float(len(off) - 1)
+    assert res["tot_ext"] == float(oracle.ext_count(g))
+    assert res["ms_max"] == 2.0 and res["e2e_max"] == 20.0
+    # digest is additive over shards (mod 2^64)
+    lo = sum(int(p[0]) | (int(p[1]) << 32) for p in res["parts"]) % (1 << 64)
+    hi = sum(int(p[2]) | (int(p[3]) << 32) for p in res["parts"]) % (1 << 64)
+    assert (lo, hi) == oracle.digest(off, vert)
+    # each copy contributes the same block (weak scaling: equal work per rank)
+    assert len(res["blocks"][0][1]) == len(res["blocks"][1][1])
