@@ -348,8 +348,11 @@ def main():
                        "parallelism": f"start-vertex shards x{world}"},
             "extensions_per_sec": tot_ext / (ms_max * 1e-3),
             "roofline": roofline,
-            "breakdown_ms": {"dfs_kernel": ms_dfs, "linearize": float(np.mean([s["ms_count"] - s["ms_dfs_count"]
-                                                                                for s in stats])),
+            "ms_steps": {"min": float(np.min(ms_steps)), "median": float(np.median(ms_steps)),
+                         "max": float(np.max(ms_steps))},
+            "breakdown_ms": {"dfs_kernel": ms_dfs, "linearize": float(np.mean([s["ms_linearize"] for s in stats])),
+                             "other_count": float(np.mean([s["ms_count"] - s["ms_dfs_count"] - s["ms_linearize"]
+                                                           for s in stats])),
                              "expand_kernel": ms_expand,
                              "stitch": float(np.mean([s["ms_stitch"] for s in stats])), "device": ms_dev},
             "count_rounds": st["n_count_rounds"],

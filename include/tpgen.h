@@ -119,6 +119,7 @@ typedef struct {
     double ms_total;         /* wall clock of the call */
     double ms_dfs_write;     /* device time of the dominant kernel (dfs_kernel, both phases) */
     double ms_dfs_count;     /* same as ms_dfs_write (kept for ABI stability) */
+    double ms_linearize;     /* device: linearization of the unit forest (canonical offsets) */
 } tpgen_stats;
 
 void tpgen_options_init(tpgen_options *opt);

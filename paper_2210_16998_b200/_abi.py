@@ -45,7 +45,7 @@ class Stats(Structure):
                 ("gpu_launches", c_int64), ("shard_lo", c_int32), ("shard_hi", c_int32),
                 ("ms_plan", c_double), ("ms_count", c_double), ("ms_write", c_double), ("ms_stitch", c_double),
                 ("ms_device", c_double), ("ms_total", c_double), ("ms_dfs_write", c_double),
-                ("ms_dfs_count", c_double)]
+                ("ms_dfs_count", c_double), ("ms_linearize", c_double)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

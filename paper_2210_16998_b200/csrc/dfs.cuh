@@ -109,7 +109,7 @@ struct MT<Mask<WW>> {
 //   bits 0-2 type, bit 3 closure flag, bits 4-12 c (truncate the path to c
 //   vertices), bits 13-15 n (number of appended vertices, <= 5),
 //   bits 16-55 the n appended local vertex ids (one byte each).
-// R_ARG carries the out-arc index of the preceding HEAD / TRANSIT in bits 32-63.
+// R_ARG carries the out-arc index of the HEAD / TRANSIT record that follows it, in bits 32-63.
 enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAIL, R_TRANSIT = EV_TRANSIT, R_ARG = 6 };
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record

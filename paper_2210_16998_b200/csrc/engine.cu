@@ -505,17 +505,20 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     P.chunk_used = 0;
     P.maxgen = 0;
     P.blk_used = 0;
-    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;
+    // TPGEN_DEBUG=1: host time per stage with a sync before each mark; =2: no syncs (enqueue times)
+    const char *hdbg_env = getenv("TPGEN_DEBUG");
+    const bool hdbg = hdbg_env != nullptr;
+    const bool hsync = hdbg && strcmp(hdbg_env, "2") != 0;
     double hprev = now_ms();
     auto HT = [&](const char *what) {
         if (!hdbg) return;
-        cudaStreamSynchronize(s);
+        if (hsync) cudaStreamSynchronize(s);
         const double t = now_ms();
         fprintf(stderr, "[tpgen host] %-24s %8.3f ms\n", what, t - hprev);
         hprev = t;
     };
 
-    Timer tall, tw, tst;
+    Timer tall, tw, tst, tlin;
     cudaEventRecord(tall.a, s);
     const DevGraph G = dev_graph(P, lo, hi);
 
@@ -633,6 +636,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     LA.totals = tot_d;
     const LinNode *off = node[0];  // final canonical offsets
     uint64_t tot[C_NUM + 1] = {0};
+    cudaEventRecord(tlin.a, s);
     if (nu > 0) {
         const int lg = grid_for(nu, 256, P.num_sms * 8);
         TPG_CK(cudaMemsetAsync(LA.acc[0], 0, (size_t)C_NUM * nu1 * 8, s));
@@ -651,9 +655,13 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         TPG_CK(cudaMemsetAsync(ctr + 14, 0, 8, s));
         sum_kernel<<<lg, 256, 0, s>>>(P.qext.as<uint64_t>(), nu, ctr + 14);
         launches++;
+        cudaEventRecord(tlin.b, s);
         TPG_CK(cudaMemcpyAsync(tot, tot_d, C_NUM * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaMemcpyAsync(tot + C_NUM, ctr + 14, 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
+        float lms = 0;
+        cudaEventElapsedTime(&lms, tlin.a, tlin.b);
+        st.ms_linearize = lms;
     }
     const int64_t n_pp = (int64_t)tot[C_PP], n_vert = (int64_t)tot[C_VERT];
     st.n_extensions = (int64_t)tot[C_NUM];
@@ -718,7 +726,19 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     if (nu > 0) {
         const int eg = grid_for(nu * 32, kExpandThreads, P.num_sms * 8);
         const int np = (H.max_scc + 1 + 31) / 32;  // registers per lane for the longest emitted path
-        if (W == 1 && np <= 1) expand_kernel<W, 1><<<eg, kExpandThreads, 0, s>>>(E);
+        const int npw = (H.max_scc + 3) / 4;         // 32-bit words of local ids for the longest path
+        if (W == 1 && H.max_scc <= kFastMaxScc && !getenv("TPGEN_SLOW_EXPAND")) {
+            switch (npw) {
+                case 1: expand_fast_kernel<1><<<eg, kExpandThreads, 0, s>>>(E); break;
+                case 2: expand_fast_kernel<2><<<eg, kExpandThreads, 0, s>>>(E); break;
+                case 3: expand_fast_kernel<3><<<eg, kExpandThreads, 0, s>>>(E); break;
+                case 4: expand_fast_kernel<4><<<eg, kExpandThreads, 0, s>>>(E); break;
+                case 5: expand_fast_kernel<5><<<eg, kExpandThreads, 0, s>>>(E); break;
+                case 6: expand_fast_kernel<6><<<eg, kExpandThreads, 0, s>>>(E); break;
+                case 7: expand_fast_kernel<7><<<eg, kExpandThreads, 0, s>>>(E); break;
+                default: expand_fast_kernel<8><<<eg, kExpandThreads, 0, s>>>(E); break;
+            }
+        } else if (W == 1 && np <= 1) expand_kernel<W, 1><<<eg, kExpandThreads, 0, s>>>(E);
         else if (W == 1 && np <= 2) expand_kernel<W, 2><<<eg, kExpandThreads, 0, s>>>(E);
         else expand_kernel<W, 2 * W + 1><<<eg, kExpandThreads, 0, s>>>(E);
         launches++;

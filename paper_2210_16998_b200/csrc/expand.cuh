@@ -3,12 +3,23 @@
 // offsets/vertices arrays, head records (cross-SCC
 // blocks, filled later by stitch_kernel) and segment items (a5).
 //
-// One warp per unit.  The current path lives in registers, distributed over
-// the warp (lane q holds positions q, q+32, ...); records are fetched 32 at a
-// time (one coalesced load, then broadcast by shuffle), so the replay has no
-// dependent global loads and no shared-memory round trips.  Emitting records
-// are written as one coalesced streaming store per 32 vertices at the exact
-// offsets produced by the linearization of the per-unit counters.
+// One warp per unit.  Two kernels:
+//
+//  expand_fast_kernel<NPW> (every SCC has at most 31 vertices, so a path fits
+//  in NPW <= 8 32-bit words of local ids): the warp takes 32 records at a time,
+//  lane j owning record j.  Each lane turns its record into the bytes it writes
+//  (positions c..c+n-1) plus a byte mask, and an inclusive warp scan whose
+//  operator is "later record overwrites earlier bytes" gives every lane the full
+//  path of its record (bytes no record of the batch wrote come from the path the
+//  previous batch ended with).  Emitting lanes place their paths in a per-warp
+//  shared-memory stage at offsets from a warp scan of their lengths, and the
+//  warp streams the stage to HBM with coalesced stores.  Batches that contain
+//  other record kinds (segment items, head blocks; they occur only at SCC exits)
+//  fall back to the sequential replay below.
+//
+//  expand_kernel<W, NP> (any SCC size): sequential replay, the current path
+//  distributed over the lanes' registers (lane q holds positions q, q+32, ...);
+//  records are fetched 32 at a time and broadcast by shuffle.
 #pragma once
 
 #include "dfs.cuh"
@@ -37,6 +48,122 @@ __device__ __forceinline__ void st_global_cs(int32_t *p, int v) {
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Output cursors of one unit (canonical exclusive offsets, advanced as records are replayed).
+struct Cursor {
+    uint64_t pp, vv, it, itv, hd, hdv;
+    int arg;  // out-arc of the pending HEAD / TRANSIT (from the R_ARG record before it)
+};
+
+__device__ __forceinline__ Cursor unit_cursor(const ExpandArgs &A, int64_t u) {
+    const LinNode *on = A.off + u;
+    Cursor cu;
+    cu.pp = on->v[C_PP];
+    cu.vv = on->v[C_VERT];
+    cu.it = on->v[C_ITEMS];
+    cu.itv = on->v[C_ITEMV];
+    cu.hd = on->v[C_HEADS];
+    cu.hdv = on->v[C_HEADV];
+    cu.arg = -1;
+    return cu;
+}
+
+// Record stream reader: 32 records per fetch (lane j gets record r0 + j).
+struct RecReader {
+    const uint64_t *ch;  // current chunk
+    int slot;            // next record slot in it
+};
+
+__device__ __forceinline__ uint64_t fetch32(const ExpandArgs &A, RecReader &rd, int nb, int lane) {
+    // link word of a full chunk (read, but only followed when the unit has records beyond it)
+    const uint64_t *nxt = (rd.slot + nb >= kChunkRecs - 1) ? A.chunks + rd.ch[kChunkRecs - 1] * kChunkRecs : rd.ch;
+    uint64_t myrec = 0;
+    if (lane < nb) {
+        const int sj = rd.slot + lane;
+        myrec = (sj < kChunkRecs - 1) ? rd.ch[sj] : nxt[sj - (kChunkRecs - 1)];
+    }
+    if (rd.slot + nb >= kChunkRecs - 1) {
+        rd.slot = rd.slot + nb - (kChunkRecs - 1);
+        rd.ch = nxt;
+    } else {
+        rd.slot += nb;
+    }
+    return myrec;
+}
+
+// Sequential replay of one record (warp-uniform `rec`); P = the current path
+// distributed over the lanes (lane q holds positions q + 32 r).
+template <int NP>
+__device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, int (&P)[NP], Cursor &cu, int lane,
+                                           int ga, int vb, int sgid) {
+    const DevGraph &G = A.G;
+    const int ty = (int)(rec & 7);
+    if (ty == R_ARG) {
+        cu.arg = (int)(rec >> 32);
+        return;
+    }
+    const int cc = (int)((rec >> 4) & 0x1ff);
+    const int n = (int)((rec >> 13) & 7);
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const int d = lane + 32 * r - cc;
+        if (d >= 0 && d < n) P[r] = (int)((rec >> (16 + 8 * d)) & 0xff);
+    }
+    if (ty == R_PATH) return;
+    const int len = cc + n;
+    const int tot = len + (int)((rec >> 3) & 1);
+    int32_t *dst;
+    if (ty == R_PP) {
+        dst = A.out_vert + cu.vv;
+        if (lane == 0) A.out_off[cu.pp] = (int64_t)cu.vv;
+        cu.pp += 1;
+        cu.vv += (uint64_t)tot;
+    } else if (ty == R_HEAD) {
+        const int32_t x = __ldg(G.out_gid + cu.arg);
+        dst = A.head_pool + cu.hdv;
+        if (lane == 0) {
+            HeadRec hr;
+            hr.pp_off = cu.pp;
+            hr.v_off = cu.vv;
+            hr.hv_off = cu.hdv;
+            hr.len = len;
+            hr.x = x;
+            A.heads[cu.hd] = hr;
+        }
+        const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+        cu.pp += Wx;
+        cu.vv += (uint64_t)len * Wx + Vx;
+        cu.hd += 1;
+        cu.hdv += (uint64_t)len;
+    } else {  // R_TAIL / R_TRANSIT
+        dst = A.item_pool + cu.itv;
+        if (lane == 0) {
+            ItemRec ir;
+            ir.pool_off = (int64_t)cu.itv;
+            ir.len = len;
+            ir.y = (ty == R_TRANSIT) ? __ldg(G.out_gid + cu.arg) : -1;
+            ir.ent = sgid;
+            ir.pad = 0;
+            A.items[cu.it] = ir;
+        }
+        cu.it += 1;
+        cu.itv += (uint64_t)len;
+    }
+    const int s0 = __shfl_sync(kFull, P[0], 0);  // closing vertex of a cycle
+    if (ga >= 0) {  // SCC with contiguous global ids (warp-uniform branch)
+#pragma unroll
+        for (int r = 0; r < NP; r++) {
+            const int pos = lane + 32 * r;
+            if (pos < tot) st_global_cs(dst + pos, ga + ((pos < len) ? P[r] : s0));
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < NP; r++) {
+            const int pos = lane + 32 * r;
+            if (pos < tot) st_global_cs(dst + pos, __ldg(G.slot_gid + vb + ((pos < len) ? P[r] : s0)));
+        }
+    }
+}
+
 // NP = path registers per lane: ceil((longest emitted path + closing vertex) / 32).
 template <int W, int NP>
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
@@ -59,98 +186,144 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
         const int vb = __ldg(G.scc_vbase + h.x);
         const int ga = __ldg(G.scc_gbase + h.x);
         const int sgid = __ldg(G.slot_gid + vb + __shfl_sync(kFull, P[0], 0));
-        const LinNode *on = A.off + u;
-        uint64_t pp = on->v[C_PP], vv = on->v[C_VERT];
-        uint64_t it = on->v[C_ITEMS], itv = on->v[C_ITEMV];
-        uint64_t hd = on->v[C_HEADS], hdv = on->v[C_HEADV];
+        Cursor cu = unit_cursor(A, u);
         const int64_t nrec = A.rcount[u];
-        const uint64_t *ch = A.chunks + A.rfirst[u] * kChunkRecs;
-        int slot = 0;  // next record slot in chunk `ch`
-        int arg = -1;
+        RecReader rd{A.chunks + A.rfirst[u] * kChunkRecs, 0};
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
-            // ---- fetch the next (up to) 32 records: lane j takes record r0 + j
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
-            // link word of a full chunk (read, but only followed when the unit has records beyond it)
-            const uint64_t *nxt = (slot + nb >= kChunkRecs - 1) ? A.chunks + ch[kChunkRecs - 1] * kChunkRecs : ch;
-            uint64_t myrec = 0;
-            if (lane < nb) {
-                const int sj = slot + lane;
-                myrec = (sj < kChunkRecs - 1) ? ch[sj] : nxt[sj - (kChunkRecs - 1)];
-            }
-            if (slot + nb >= kChunkRecs - 1) {
-                slot = slot + nb - (kChunkRecs - 1);
-                ch = nxt;
-            } else {
-                slot += nb;
-            }
-            // ---- replay them in order
-            for (int i = 0; i < nb; i++) {
-                const uint64_t rec = __shfl_sync(kFull, myrec, i);
-                const int ty = (int)(rec & 7);
-                if (ty == R_ARG) {
-                    arg = (int)(rec >> 32);
-                    continue;
-                }
-                const int cc = (int)((rec >> 4) & 0x1ff);
-                const int n = (int)((rec >> 13) & 7);
+            const uint64_t myrec = fetch32(A, rd, nb, lane);
+            for (int i = 0; i < nb; i++) replay_one<NP>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, sgid);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- fast path
+constexpr int kFastMaxScc = 31;      // a path + its closing vertex fits one 32-lane row
+constexpr int kStageInts = 32 * 32;  // one batch: 32 paths of at most 32 output vertices
+
+__device__ __forceinline__ uint32_t lop_merge(uint32_t mine, uint32_t other, uint32_t mask) {
+    return (mine & mask) | (other & ~mask);  // one LOP3
+}
+
+template <int NPW>
+__global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs A) {
+    __shared__ __align__(16) int32_t stage_all[kExpandThreads / 32][kStageInts];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *stage = stage_all[wid];
+    const DevGraph &G = A.G;
+    const Unit<1> *units = reinterpret_cast<const Unit<1> *>(A.units);
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    for (int64_t u = gw; u < A.n_units; u += nw) {
+        const Unit<1> *U = units + u;
+        const int4 h = *reinterpret_cast<const int4 *>(&U->scc);
+        // carry = the current path as bytes (positions 0..depth valid; the others are
+        // always written by a record before an emitted path reads them)
+        uint32_t carry[NPW];
+        {
+            const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
+            const uint4 a = p4[0];
+            const uint4 b = (NPW > 4) ? p4[1] : make_uint4(0, 0, 0, 0);
+            const uint32_t w8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-                for (int r = 0; r < NP; r++) {
-                    const int d = lane + 32 * r - cc;
-                    if (d >= 0 && d < n) P[r] = (int)((rec >> (16 + 8 * d)) & 0xff);
+            for (int w = 0; w < NPW; w++) carry[w] = w8[w];
+        }
+        const int vb = __ldg(G.scc_vbase + h.x);
+        const int ga = __ldg(G.scc_gbase + h.x);
+        const int s0 = (int)(carry[0] & 0xff);
+        const int s0g = (ga >= 0) ? ga + s0 : __ldg(G.slot_gid + vb + s0);  // global id of the start vertex
+        Cursor cu = unit_cursor(A, u);
+        const int64_t nrec = A.rcount[u];
+        RecReader rd{A.chunks + A.rfirst[u] * kChunkRecs, 0};
+        for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
+            const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
+            const uint64_t myrec = fetch32(A, rd, nb, lane);  // lanes >= nb: 0 = an empty R_PATH
+            const int ty = (int)(myrec & 7);
+            if (__all_sync(kFull, ty == R_PP || ty == R_PATH)) {
+                // ---- this lane's bytes: positions cc .. cc+n-1 of the path
+                const int cc = (int)((myrec >> 4) & 0x1ff);
+                const int n = (int)((myrec >> 13) & 7);
+                const int sh = 8 * (cc & 3);
+                const uint64_t nm = (1ull << (8 * n)) - 1ull;
+                const uint64_t pay = ((myrec >> 16) & nm) << sh;
+                const uint64_t pm = nm << sh;
+                const int w0 = cc >> 2;
+                uint32_t D[NPW], M[NPW];
+#pragma unroll
+                for (int w = 0; w < NPW; w++) {
+                    D[w] = (w == w0) ? (uint32_t)pay : ((w == w0 + 1) ? (uint32_t)(pay >> 32) : 0u);
+                    M[w] = (w == w0) ? (uint32_t)pm : ((w == w0 + 1) ? (uint32_t)(pm >> 32) : 0u);
                 }
-                if (ty == R_PATH) continue;
+                // ---- inclusive scan: later records overwrite earlier bytes
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                    for (int w = 0; w < NPW; w++) {
+                        const uint32_t dn = __shfl_up_sync(kFull, D[w], o);
+                        const uint32_t mn = __shfl_up_sync(kFull, M[w], o);
+                        if (lane >= o) {
+                            D[w] = lop_merge(D[w], dn, M[w]);
+                            M[w] |= mn;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int w = 0; w < NPW; w++) D[w] = lop_merge(D[w], carry[w], M[w]);
+#pragma unroll
+                for (int w = 0; w < NPW; w++) carry[w] = __shfl_sync(kFull, D[w], 31);
+                // ---- emitting lanes: offsets by a warp scan of the path lengths
+                const bool emit = (ty == R_PP);
                 const int len = cc + n;
-                const int tot = len + (int)((rec >> 3) & 1);
-                int32_t *dst;
-                if (ty == R_PP) {
-                    dst = A.out_vert + vv;
-                    if (lane == 0) A.out_off[pp] = (int64_t)vv;
-                    pp += 1;
-                    vv += (uint64_t)tot;
-                } else if (ty == R_HEAD) {
-                    const int32_t x = __ldg(G.out_gid + arg);
-                    dst = A.head_pool + hdv;
-                    if (lane == 0) {
-                        HeadRec hr;
-                        hr.pp_off = pp;
-                        hr.v_off = vv;
-                        hr.hv_off = hdv;
-                        hr.len = len;
-                        hr.x = x;
-                        A.heads[hd] = hr;
-                    }
-                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                    pp += Wx;
-                    vv += (uint64_t)len * Wx + Vx;
-                    hd += 1;
-                    hdv += (uint64_t)len;
-                } else {  // R_TAIL / R_TRANSIT
-                    dst = A.item_pool + itv;
-                    if (lane == 0) {
-                        ItemRec ir;
-                        ir.pool_off = (int64_t)itv;
-                        ir.len = len;
-                        ir.y = (ty == R_TRANSIT) ? __ldg(G.out_gid + arg) : -1;
-                        ir.ent = sgid;
-                        ir.pad = 0;
-                        A.items[it] = ir;
-                    }
-                    it += 1;
-                    itv += (uint64_t)len;
-                }
-                const int s0 = __shfl_sync(kFull, P[0], 0);  // closing vertex of a cycle
-                if (ga >= 0) {  // SCC with contiguous global ids (warp-uniform branch)
+                const int tot = emit ? len + (int)((myrec >> 3) & 1) : 0;
+                int ex = tot;
 #pragma unroll
-                    for (int r = 0; r < NP; r++) {
-                        const int pos = lane + 32 * r;
-                        if (pos < tot) st_global_cs(dst + pos, ga + ((pos < len) ? P[r] : s0));
-                    }
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(kFull, ex, o);
+                    if (lane >= o) ex += t;
+                }
+                const int T = __shfl_sync(kFull, ex, 31);
+                ex -= tot;
+                const unsigned em = __ballot_sync(kFull, emit);
+                if (emit) A.out_off[cu.pp + __popc(em & lt_mask)] = (int64_t)(cu.vv + (uint64_t)ex);
+                // ---- stage the vertices (global ids), then stream them out coalesced
+                if (ga >= 0) {
+#pragma unroll
+                    for (int p = 0; p < 4 * NPW; p++)
+                        if (p < tot) stage[ex + p] = ga + (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
                 } else {
 #pragma unroll
-                    for (int r = 0; r < NP; r++) {
-                        const int pos = lane + 32 * r;
-                        if (pos < tot) st_global_cs(dst + pos, __ldg(G.slot_gid + vb + ((pos < len) ? P[r] : s0)));
-                    }
+                    for (int p = 0; p < 4 * NPW; p++)
+                        if (p < tot) stage[ex + p] = __ldg(G.slot_gid + vb + (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff));
+                }
+                if (len < tot) stage[ex + len] = s0g;  // closing vertex of a cycle (after the byte loop)
+                __syncwarp();
+                int32_t *dst = A.out_vert + cu.vv;
+                for (int i = lane; i < T; i += 32) st_global_cs(dst + i, stage[i]);
+                __syncwarp();
+                cu.pp += (uint64_t)__popc(em);
+                cu.vv += (uint64_t)T;
+            } else {
+                // ---- segment items / head blocks in this batch: sequential replay
+                int P[1];
+                {
+                    const int w = lane >> 2;
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int k = 0; k < NPW; k++)
+                        if (k == w) x = carry[k];
+                    P[0] = (int)((x >> (8 * (lane & 3))) & 0xff);
+                }
+                for (int i = 0; i < nb; i++)
+                    replay_one<1>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, s0g);
+                // back to bytes: word w = lanes 4w..4w+3
+#pragma unroll
+                for (int w = 0; w < NPW; w++) {
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; b++) x |= ((uint32_t)__shfl_sync(kFull, P[0], 4 * w + b) & 0xffu) << (8 * b);
+                    carry[w] = x;
                 }
             }
         }
