@@ -301,9 +301,10 @@ __device__ __forceinline__ unsigned int ld_flags(const unsigned int *p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-// hand-off of queued units between lanes of different SMs: release store / acquire load of the ready flag
-__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// hand-off of queued units between lanes of different SMs: the producer fences once after
+// writing a block of units, then sets their ready flags with relaxed stores
+__device__ __forceinline__ void st_relaxed(unsigned int *p, unsigned int v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // The consumer polls the flag with a relaxed load and only then issues its
 // (L2, .cg) loads of the unit payload: the payload was made visible at L2 by
@@ -436,48 +437,37 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     const unsigned long long t0 = A.dbg ? A.dbg[7] : 0;
 #endif
     uint32_t last_split = 0;
-    int backoff = 0;  // idle lanes poll the queue every few iterations
     uint32_t iter = 0;
+    // Queue traffic is software-pipelined: every global load or atomic whose
+    // result the warp needs is issued in one iteration and consumed in the next,
+    // so its L2 round trip overlaps a DFS step instead of stalling the warp.
+    unsigned rdy = 0;                       // waiting lanes: ready flag of `slot`, loaded last iteration
+    bool claim_pending = false;             // warp-uniform: a claim atomic is in flight
+    unsigned claim_mask = 0;                // lanes the claim is for
+    int claim_leader = 0;
+    unsigned long long claim_res = 0;       // leader: first claimed slot
+    bool snap_pending = false;              // warp-uniform: lane 0 loaded the queue words last iteration
+    unsigned long long snap_td = 0, snap_head = 0;
+    unsigned snap_ov = 0;
+    bool qdone = false;                     // every pushed unit finished (or the pool/queue overflowed)
     while (true) {
         int ev = 0, e = -1;
         bool fresh = false;
-        // ---------------- idle lanes claim queued units (warp-aggregated, only what is available)
-        if (backoff > 0) backoff--;
-        const unsigned need = __ballot_sync(kFull, !L.active && !waiting && !exited && backoff == 0);
-        if (need) {
-            const int leader = __ffs(need) - 1;
-            long long base = -1, k = 0;
-            int fin = 0;
-            if (lane == leader) {
-                const unsigned long long td = ld_volatile(A.qtd);  // tail << 32 | done
-                const long long avail = (long long)(td >> 32) - (long long)ld_volatile(A.qhead);
-                k = min((long long)__popc(need), avail);
-                if (k > 0) {
-                    base = (long long)atomicAdd(A.qhead, (unsigned long long)k);
-                } else {  // nothing queued: has every pushed unit finished?
-                    fin = ((td >> 32) == (td & 0xffffffffull)) ||
-                          ((ld_flags(A.overflow) & 6u) != 0u);
-                }
-            }
-            base = __shfl_sync(kFull, base, leader);
-            k = __shfl_sync(kFull, k, leader);
-            fin = __shfl_sync(kFull, fin, leader);
-            if (!L.active && !waiting && !exited && backoff == 0) {
-                const int rank = __popc(need & ((1u << lane) - 1));
-                if (rank < k) {
-                    slot = base + rank;  // may lie beyond the tail if another warp raced us: wait for it
-                    waiting = true;
-                } else if (fin) {
-                    exited = true;
-                } else {
-                    backoff = 4;
-                }
-            }
+        iter++;
+        // ---------------- consume last iteration's queue snapshot / claim
+        bool feed = false;
+        if (snap_pending) {
+            const unsigned long long td = __shfl_sync(kFull, snap_td, 0);
+            const unsigned long long hd = __shfl_sync(kFull, snap_head, 0);
+            const unsigned ov = __shfl_sync(kFull, snap_ov, 0);
+            qdone = ((td >> 32) == (td & 0xffffffffull)) || ((ov & 6u) != 0u);
+            // donate when the backlog of queued, unclaimed units is below the low-water mark
+            feed = (long long)(td >> 32) - (long long)hd < (long long)A.low_water;
+            snap_pending = false;
         }
         // ---------------- waiting lanes: start the unit once written, or stop when all work is done
         if (waiting) {
-            if (slot < (int64_t)A.qcap &&
-                ld_relaxed(A.ready + slot) != 0u) {
+            if (rdy != 0u) {
                 waiting = false;
                 // queue slots are written by other SMs during this launch: read them at L2 (ld.cg)
                 const Unit<W> *U = units + slot;
@@ -555,14 +545,43 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     e = h.y;
                     ev = out_event(L);
                 }
-            } else {
-                const unsigned long long td = ld_volatile(A.qtd);
-                if ((td >> 32) == (td & 0xffffffffull) ||
-                    (ld_flags(A.overflow) & 6u)) {
-                    waiting = false;
-                    exited = true;
-                }
+            } else if (qdone) {
+                // nothing is running that could still push this slot (done == tail implies slot >= tail)
+                waiting = false;
+                exited = true;
+            } else if (slot < (int64_t)A.qcap) {
+                rdy = ld_relaxed(A.ready + slot);  // consumed next iteration
             }
+        }
+        // ---------------- the claim issued last iteration: take the slots, poll their flags next iteration
+        if (claim_pending) {
+            const unsigned long long base = __shfl_sync(kFull, claim_res, claim_leader);
+            if ((claim_mask >> lane) & 1u) {
+                slot = (int64_t)(base + __popc(claim_mask & ((1u << lane) - 1u)));
+                waiting = true;  // the slot may lie beyond the tail: wait until it is pushed
+                rdy = (slot < (int64_t)A.qcap) ? ld_relaxed(A.ready + slot) : 0u;
+            }
+            claim_pending = false;
+        }
+        // ---------------- idle lanes claim the next slots (one atomic per warp, consumed next iteration)
+        {
+            const unsigned need = __ballot_sync(kFull, !L.active && !waiting && !exited);
+            if (need && !claim_pending) {
+                claim_leader = __ffs(need) - 1;
+                claim_mask = need;
+                claim_pending = true;
+                if (lane == claim_leader) claim_res = atomicAdd(A.qhead, (unsigned long long)__popc(need));
+            }
+        }
+        // ---------------- queue snapshot for donation / termination (lane 0, consumed next iteration)
+        const bool any_active = __ballot_sync(kFull, L.active) != 0;
+        if (!snap_pending && (((iter & 15u) == 0u) || !any_active)) {
+            if (lane == 0) {
+                snap_td = ld_volatile(A.qtd);
+                snap_head = ld_volatile(A.qhead);
+                snap_ov = ld_flags(A.overflow);
+            }
+            snap_pending = true;
         }
 #ifdef TPGEN_KERNEL_DEBUG
         d_it++;
@@ -578,9 +597,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             }
         }
 #endif
-        if (__ballot_sync(kFull, L.active) == 0) {
+        if (!any_active) {
             if (__ballot_sync(kFull, !exited) == 0) break;
-            __nanosleep(256);
+            __nanosleep(128);
             continue;
         }
 
@@ -627,22 +646,15 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             }
         }
 
-        // ---------------- donate on demand (one lane per warp samples the queue every 16 iterations)
-        bool feed = false;
-        if (((++iter) & 15u) == 0u) {
-            int f = 0;
-            if (lane == 0)
-                f = (long long)(ld_volatile(A.qtd) >> 32) - (long long)ld_volatile(A.qhead) < (long long)A.low_water;
-            feed = __shfl_sync(kFull, f, 0) != 0;
-        }
+        // ---------------- donate on demand (feed: set by this iteration's queue snapshot)
         if (feed && L.active && !L.done && L.steps - last_split >= A.split_min) {
             // backlog of queued, unclaimed units below the low-water mark: donate the shallowest siblings
             int j0 = -1;
             const int m = lane_donate<T, TS, false>(G, tab, L, mp, uscc, j0, nullptr);
             if (m > 0) {
                 const unsigned long long base = atomicAdd(A.qtd, (unsigned long long)m << 32) >> 32;
-                const unsigned long long b = atomicAdd(A.blk_ctr, 1ull);
-                if (base + m > A.qcap || b >= A.qcap) {
+                const unsigned long long b = base;  // a block is named by its first slot
+                if (base + m > A.qcap) {
                     atomicOr(A.overflow, 4u);
                 } else {
                     lane_donate<T, TS, true>(G, tab, L, mp, uscc, j0, units + base);
@@ -657,7 +669,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     child_head = (int64_t)b;
                     nchild += m;
                     atomicMax(A.maxgen, ugen + 1);
-                    for (int i = 0; i < m; i++) st_release(A.ready + base + i, 1u);  // publish after the unit data
+                    __threadfence();  // unit data before the ready flags
+                    for (int i = 0; i < m; i++) st_relaxed(A.ready + base + i, 1u);
                     if (j0 == L.l) L.done = true;  // nothing left below the donated level
                     else L.r = j0 + 1;             // the walk now ends when it returns to depth j0+1
                     last_split = L.steps;
