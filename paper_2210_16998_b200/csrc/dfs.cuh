@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     // result the warp needs is issued in one iteration and consumed in the next,
     // so its L2 round trip overlaps a DFS step instead of stalling the warp.
     unsigned rdy = 0;                       // waiting lanes: ready flag of `slot`, loaded last iteration
+    unsigned long long pre_ch = 0;          // waiting lanes: record chunk reserved for the claimed unit
     bool claim_pending = false;             // warp-uniform: a claim atomic is in flight
     unsigned claim_mask = 0;                // lanes the claim is for
     int claim_leader = 0;
@@ -450,20 +451,52 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     unsigned long long snap_td = 0, snap_head = 0;
     unsigned snap_ov = 0;
     bool qdone = false;                     // every pushed unit finished (or the pool/queue overflowed)
+    bool prev_active = true;
+    __shared__ unsigned long long s_td, s_head;  // warp 0's latest queue snapshot
+    __shared__ unsigned s_ov;
+    if (threadIdx.x == 0) {
+        s_td = 0xffffffffull << 32;  // "work pending, no backlog need" until warp 0's first snapshot
+        s_head = 0;
+        s_ov = 0;
+    }
+    __syncthreads();
     while (true) {
         int ev = 0, e = -1;
         bool fresh = false;
         iter++;
         // ---------------- consume last iteration's queue snapshot / claim
+        // The queue words are polled by warp 0 of each block only (the lines they live on are
+        // hot: every claim, push and completion is an atomic on them); it publishes its
+        // snapshot in shared memory, where the other warps read it.
         bool feed = false;
-        if (snap_pending) {
-            const unsigned long long td = __shfl_sync(kFull, snap_td, 0);
-            const unsigned long long hd = __shfl_sync(kFull, snap_head, 0);
-            const unsigned ov = __shfl_sync(kFull, snap_ov, 0);
-            qdone = ((td >> 32) == (td & 0xffffffffull)) || ((ov & 6u) != 0u);
-            // donate when the backlog of queued, unclaimed units is below the low-water mark
-            feed = (long long)(td >> 32) - (long long)hd < (long long)A.low_water;
-            snap_pending = false;
+        {
+            bool have = false;
+            unsigned long long td = 0, hd = 0;
+            unsigned ov = 0;
+            if (wid == 0) {
+                if (snap_pending) {
+                    td = __shfl_sync(kFull, snap_td, 0);
+                    hd = __shfl_sync(kFull, snap_head, 0);
+                    ov = __shfl_sync(kFull, snap_ov, 0);
+                    if (lane == 0) {
+                        *reinterpret_cast<volatile unsigned long long *>(&s_td) = td;
+                        *reinterpret_cast<volatile unsigned long long *>(&s_head) = hd;
+                        *reinterpret_cast<volatile unsigned *>(&s_ov) = ov;
+                    }
+                    snap_pending = false;
+                    have = true;
+                }
+            } else if (((iter & 15u) == 0u) || !prev_active) {
+                td = *reinterpret_cast<volatile unsigned long long *>(&s_td);
+                hd = *reinterpret_cast<volatile unsigned long long *>(&s_head);
+                ov = *reinterpret_cast<volatile unsigned *>(&s_ov);
+                have = true;
+            }
+            if (have) {
+                qdone = ((td >> 32) == (td & 0xffffffffull)) || ((ov & 6u) != 0u);
+                // donate when the backlog of queued, unclaimed units is below the low-water mark
+                feed = (long long)(td >> 32) - (long long)hd < (long long)A.low_water;
+            }
         }
         // ---------------- waiting lanes: start the unit once written, or stop when all work is done
         if (waiting) {
@@ -518,7 +551,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 ext = 0;
                 c_pp = c_vert = 0;
                 c_it = c_itv = c_hd = c_hdv = 0;
-                const unsigned long long ch = atomicAdd(A.chunk_next, 1ull);
+                const unsigned long long ch = pre_ch;  // allocated when the slot was claimed
                 if (ch >= A.chunk_cap) {
                     atomicOr(A.overflow, 2u);
                     R.cur = A.chunks;
@@ -560,6 +593,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 slot = (int64_t)(base + __popc(claim_mask & ((1u << lane) - 1u)));
                 waiting = true;  // the slot may lie beyond the tail: wait until it is pushed
                 rdy = (slot < (int64_t)A.qcap) ? ld_relaxed(A.ready + slot) : 0u;
+                pre_ch = atomicAdd(A.chunk_next, 1ull);  // first record chunk of that unit (consumed later)
             }
             claim_pending = false;
         }
@@ -575,7 +609,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         }
         // ---------------- queue snapshot for donation / termination (lane 0, consumed next iteration)
         const bool any_active = __ballot_sync(kFull, L.active) != 0;
-        if (!snap_pending && (((iter & 15u) == 0u) || !any_active)) {
+        prev_active = any_active;
+        if (wid == 0 && !snap_pending && (((iter & 15u) == 0u) || !any_active)) {
             if (lane == 0) {
                 snap_td = ld_volatile(A.qtd);
                 snap_head = ld_volatile(A.qhead);

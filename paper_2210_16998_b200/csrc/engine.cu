@@ -45,7 +45,9 @@ static double now_ms() {
 // ------------------------------------------------------------ buffers
 tpgen_status DevBuf::ensure(size_t bytes, cudaStream_t s) {
     if (bytes <= cap) return TPGEN_OK;
-    size_t nc = std::max(bytes, (size_t)(cap * 3 / 2));
+    // 25 % headroom: per-call sizes (units, records) vary with the dynamic donation pattern,
+    // and a regrowth inside a later call costs a fresh mapping from the pool
+    size_t nc = std::max(bytes + bytes / 4, (size_t)(cap * 3 / 2));
     nc = (nc + 255) & ~(size_t)255;
     if (p) TPG_CK(cudaFreeAsync(p, s));
     p = nullptr;
@@ -373,7 +375,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
     tail_out = qbase + nroots;
     if (nroots == 0) return TPGEN_OK;
     const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
-    TPG_TRY(grow_queue<W>(P, qbase, std::max<uint64_t>(qbase + nroots + 8 * (uint64_t)lanes, 1u << 21), s));
+    TPG_TRY(grow_queue<W>(P, qbase, std::max<uint64_t>(std::max<uint64_t>(qbase + nroots + 8 * (uint64_t)lanes, 1u << 21),
+                                                       P.q_hwm * 3 / 2), s));
     if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
     TPG_TRY(P.qctr.ensure(7 * 16 * 8, s));
     unsigned long long *qc = P.qctr.as<unsigned long long>();
@@ -470,6 +473,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         }
         if (ovf & 1u) P.overflow = true;
         P.chunk_used = h[4];
+        P.chunk_hwm = std::max<uint64_t>(P.chunk_hwm, h[4]);
+        P.q_hwm = std::max<uint64_t>(P.q_hwm, h[1] >> 32);
         P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
         P.blk_used = h[6];
         tail_out = h[1] >> 32;
@@ -549,8 +554,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     {
         double est = 0;  // Knuth estimates of the trie sizes -> initial record pool
         for (int32_t v = 0; v < H.n; v++) est += P.hp.cost[v];
-        TPG_TRY(grow_pool(P, std::max<uint64_t>((64ull << 20) / (kChunkRecs * 8),
-                                                (uint64_t)(est * 0.75 / (kChunkRecs - 1)) + 4 * H.n), s));
+        // ... or 1.5x the most this plan has used: record counts vary from call to call (the
+        // donation pattern is dynamic), and a retry inside a call costs a second DFS launch
+        TPG_TRY(grow_pool(P, std::max<uint64_t>(std::max<uint64_t>((64ull << 20) / (kChunkRecs * 8),
+                                                                   (uint64_t)(est * 0.75 / (kChunkRecs - 1)) + 4 * H.n),
+                                                P.chunk_hwm * 3 / 2), s));
     }
 
     double ms_dfs = 0;

@@ -42,6 +42,8 @@ struct PlanImpl {
     DevBuf chunks, agg, agg_bak;  // path-delta record pool (chunks of kChunkRecs words); SEG aggregates + backup
     uint64_t chunk_cap = 0;       // pool capacity in chunks
     uint64_t chunk_used = 0;      // chunks handed out so far in this call
+    uint64_t chunk_hwm = 0;       // most chunks any call of this plan used (sizes the pool with headroom)
+    uint64_t q_hwm = 0;           // most queue slots any call of this plan used
     int maxgen = 0;               // deepest split generation so far in this call
     uint32_t split_min = 32;      // steps between two donations of a unit
     DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
