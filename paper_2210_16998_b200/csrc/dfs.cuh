@@ -198,24 +198,32 @@ __device__ __forceinline__ int out_event(const Lane<T> &L) {
     return MT<T>::subset(L.ps, L.M) ? (EV_HEAD | len) : 0;
 }
 
+// A lane writes the records of all its units into one chain of chunks: a unit
+// starts wherever the previous one ended (rfirst = global record index), so
+// starting a unit costs no allocation.  The next chunk is reserved (atomic
+// issued) when the current one is half full and consumed when it fills.
 struct RecWriter {
-    uint64_t *cur;  // current chunk
-    int fill;       // records used in it
-    int64_t count;  // records of the unit
+    uint64_t *cur;   // current chunk
+    int fill;        // records used in it (kChunkRecs - 1: full, the next record needs a new chunk)
+    long long next;  // chunk reserved for when this one fills (-1: none)
+    int64_t count;   // records of the current unit
 };
 
-__device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t rec) {
-    if (R.fill == kChunkRecs - 1) {
-        const unsigned long long nc = atomicAdd(A.chunk_next, 1ull);
-        if (nc >= A.chunk_cap) {
-            atomicOr(A.overflow, 2u);
-            R.fill = 0;  // keep writing into the current chunk (result is discarded)
-        } else {
-            R.cur[kChunkRecs - 1] = nc;
-            R.cur = A.chunks + nc * kChunkRecs;
-            R.fill = 0;
-        }
+__device__ __forceinline__ void rec_switch(const DfsArgs &A, RecWriter &R) {
+    unsigned long long nc = (R.next >= 0) ? (unsigned long long)R.next : atomicAdd(A.chunk_next, 1ull);
+    R.next = -1;
+    if (nc >= A.chunk_cap) {  // pool exhausted: the phase is retried with a bigger pool;
+        atomicOr(A.overflow, 2u);  // meanwhile write into the sink chunk past the end
+        nc = A.chunk_cap;
     }
+    R.cur[kChunkRecs - 1] = nc;  // link
+    R.cur = A.chunks + nc * kChunkRecs;
+    R.fill = 0;
+}
+
+__device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t rec) {
+    if (R.fill == kChunkRecs - 1) rec_switch(A, R);
+    else if (R.fill == kChunkRecs / 2 && R.next < 0) R.next = (long long)atomicAdd(A.chunk_next, 1ull);
     R.cur[R.fill++] = rec;
     R.count++;
 }
@@ -426,8 +434,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     uint64_t c_pp = 0, c_vert = 0;                          // per-unit counters (C_PP, C_VERT)
     uint32_t c_it = 0, c_itv = 0, c_hd = 0, c_hdv = 0, ext = 0;  // C_ITEMS, C_ITEMV, C_HEADS, C_HEADV, E_canon
     RecWriter R;
-    R.cur = A.chunks;
-    R.fill = 0;
+    R.cur = A.chunks + A.chunk_cap * kChunkRecs;  // the sink chunk, marked full: the first record allocates
+    R.fill = kChunkRecs - 1;
+    R.next = -1;
     R.count = 0;
 
     int64_t child_head = -1;  // latest donated block of the running unit
@@ -442,7 +451,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     // result the warp needs is issued in one iteration and consumed in the next,
     // so its L2 round trip overlaps a DFS step instead of stalling the warp.
     unsigned rdy = 0;                       // waiting lanes: ready flag of `slot`, loaded last iteration
-    unsigned long long pre_ch = 0;          // waiting lanes: record chunk reserved for the claimed unit
     bool claim_pending = false;             // warp-uniform: a claim atomic is in flight
     unsigned claim_mask = 0;                // lanes the claim is for
     int claim_leader = 0;
@@ -551,16 +559,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 ext = 0;
                 c_pp = c_vert = 0;
                 c_it = c_itv = c_hd = c_hdv = 0;
-                const unsigned long long ch = pre_ch;  // allocated when the slot was claimed
-                if (ch >= A.chunk_cap) {
-                    atomicOr(A.overflow, 2u);
-                    R.cur = A.chunks;
-                    A.rfirst[slot] = 0;
-                } else {
-                    R.cur = A.chunks + ch * kChunkRecs;
-                    A.rfirst[slot] = (int64_t)ch;
-                }
-                R.fill = 0;
+                if (R.fill == kChunkRecs - 1) rec_switch(A, R);
+                A.rfirst[slot] = (int64_t)(R.cur - A.chunks) + R.fill;  // global record index
                 R.count = 0;
                 // the unit's root event (no step is counted for it)
                 if (kind == K_NODE) {
@@ -593,7 +593,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 slot = (int64_t)(base + __popc(claim_mask & ((1u << lane) - 1u)));
                 waiting = true;  // the slot may lie beyond the tail: wait until it is pushed
                 rdy = (slot < (int64_t)A.qcap) ? ld_relaxed(A.ready + slot) : 0u;
-                pre_ch = atomicAdd(A.chunk_next, 1ull);  // first record chunk of that unit (consumed later)
             }
             claim_pending = false;
         }

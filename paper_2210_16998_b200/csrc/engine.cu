@@ -182,10 +182,97 @@ struct OutOwner {
     tpgen_free_fn free_fn = nullptr;
     void *ctx = nullptr;
     void *stream = nullptr;
-    int kind = 0;  // 0 cudaMallocAsync, 1 callback, 2 pinned host (library), 3 caller host buffer
+    int kind = 0;  // 0 library pool block (offsets + vertices), 1 callback, 2 pinned host (library), 3 caller host buffer
     void *p_off = nullptr, *p_vert = nullptr;
+    void *block = nullptr;  // kind 0: the one block holding both arrays
+    size_t block_bytes = 0;
     int device = 0;
 };
+
+// Output blocks of the library pool are recycled through a small per-device
+// cache: an output is one block (offsets, then vertices), and a block of the
+// same size class is handed to the next call.  Without it the stream-ordered
+// pool may carve a freed multi-GB block for smaller workspaces and then map
+// fresh memory for the next output (hundreds of ms).
+namespace {
+struct OutCache {
+    std::mutex mu;
+    std::vector<std::pair<void *, size_t>> blocks;  // free blocks (their last use has completed)
+};
+OutCache g_outcache[64];
+constexpr size_t kOutCacheMin = 1u << 20;  // smaller outputs go straight to the pool
+constexpr size_t kOutCacheBlocks = 4;
+}  // namespace
+
+static void *out_cache_get(int dev, size_t bytes, size_t *got) {
+    if (bytes < kOutCacheMin || dev < 0 || dev >= 64) return nullptr;
+    OutCache &C = g_outcache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    int best = -1;
+    for (int i = 0; i < (int)C.blocks.size(); i++) {
+        const size_t sz = C.blocks[i].second;
+        if (sz >= bytes && sz <= bytes + bytes / 2 && (best < 0 || sz < C.blocks[best].second)) best = i;
+    }
+    if (best < 0) return nullptr;
+    void *p = C.blocks[best].first;
+    *got = C.blocks[best].second;
+    C.blocks.erase(C.blocks.begin() + best);
+    return p;
+}
+
+// Takes a block whose last use has completed; false: not cached (caller frees it).
+static bool out_cache_put(int dev, void *p, size_t bytes) {
+    if (bytes < kOutCacheMin || dev < 0 || dev >= 64) return false;
+    OutCache &C = g_outcache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    C.blocks.emplace_back(p, bytes);
+    while (C.blocks.size() > kOutCacheBlocks) {
+        cudaFree(C.blocks.front().first);
+        C.blocks.erase(C.blocks.begin());
+    }
+    return true;
+}
+
+static void out_cache_clear(int dev) {
+    if (dev < 0 || dev >= 64) return;
+    OutCache &C = g_outcache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    for (auto &b : C.blocks) cudaFree(b.first);
+    C.blocks.clear();
+}
+
+static tpgen_status out_alloc_device(const tpgen_options &o, OutOwner *ow, size_t bytes, void **p, cudaStream_t s);
+
+// Offsets (int64[n+1]) and vertices (int32[...]) of one output.
+static tpgen_status out_alloc_pair(const tpgen_options &o, OutOwner *ow, size_t b_off, size_t b_vert, void **d_off,
+                                   void **d_vert, cudaStream_t s) {
+    if (o.device_alloc) {
+        TPG_TRY(out_alloc_device(o, ow, b_off, d_off, s));
+        ow->p_off = *d_off;
+        TPG_TRY(out_alloc_device(o, ow, b_vert, d_vert, s));
+        ow->p_vert = *d_vert;
+        return TPGEN_OK;
+    }
+    const size_t a_off = (b_off + 255) & ~(size_t)255;
+    const size_t bytes = std::max<size_t>(a_off + b_vert, 256);
+    size_t got = bytes;
+    void *p = out_cache_get(ow->device, bytes, &got);
+    if (!p) {
+        cudaError_t e = cudaMallocAsync(&p, bytes, s);
+        if (e != cudaSuccess) {  // release the cached blocks and try once more
+            cudaGetLastError();
+            out_cache_clear(ow->device);
+            TPG_CK(cudaMallocAsync(&p, bytes, s));
+        }
+    }
+    ow->kind = 0;
+    ow->stream = (void *)s;
+    ow->block = p;
+    ow->block_bytes = p ? got : 0;
+    *d_off = p;
+    *d_vert = (char *)p + a_off;
+    return TPGEN_OK;
+}
 
 static tpgen_status out_alloc_device(const tpgen_options &o, OutOwner *ow, size_t bytes, void **p, cudaStream_t s) {
     bytes = std::max<size_t>(bytes, 16);
@@ -214,15 +301,23 @@ void free_paths(tpgen_paths *p) {
         int prev = -1;
         cudaGetDevice(&prev);
         cudaSetDevice(ow->device);
-        void *ptrs[2] = {ow->p_off, ow->p_vert};
-        for (void *q : ptrs) {
-            if (!q) continue;
-            if (ow->kind == 0) cudaFreeAsync(q, (cudaStream_t)ow->stream);
-            else if (ow->kind == 1) {
-                if (ow->free_fn) ow->free_fn(q, ow->stream, ow->ctx);
-            } else if (ow->kind == 2) cudaFreeHost(q);
+        if (ow->kind == 0) {
+            if (ow->block) {
+                cudaStreamSynchronize((cudaStream_t)ow->stream);  // last use complete: reusable on any stream
+                if (!out_cache_put(ow->device, ow->block, ow->block_bytes)) {
+                    cudaFreeAsync(ow->block, (cudaStream_t)ow->stream);
+                    cudaStreamSynchronize((cudaStream_t)ow->stream);
+                }
+            }
+        } else {
+            void *ptrs[2] = {ow->p_off, ow->p_vert};
+            for (void *q : ptrs) {
+                if (!q) continue;
+                if (ow->kind == 1) {
+                    if (ow->free_fn) ow->free_fn(q, ow->stream, ow->ctx);
+                } else if (ow->kind == 2) cudaFreeHost(q);
+            }
         }
-        if (ow->kind == 0) cudaStreamSynchronize((cudaStream_t)ow->stream);
         if (prev >= 0) cudaSetDevice(prev);
         delete ow;
     }
@@ -303,12 +398,12 @@ static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
     if (need <= P.chunk_cap) return TPGEN_OK;
     uint64_t cap = std::max<uint64_t>(need, P.chunk_cap * 2);
     void *np = nullptr;
-    TPG_CK(cudaMallocAsync(&np, cap * kChunkRecs * 8, s));
+    TPG_CK(cudaMallocAsync(&np, (cap + 1) * kChunkRecs * 8, s));  // + the overflow sink chunk
     if (P.chunk_used && P.chunks.p)
         TPG_CK(cudaMemcpyAsync(np, P.chunks.p, P.chunk_used * kChunkRecs * 8, cudaMemcpyDeviceToDevice, s));
     if (P.chunks.p) TPG_CK(cudaFreeAsync(P.chunks.p, s));
     P.chunks.p = np;
-    P.chunks.cap = cap * kChunkRecs * 8;
+    P.chunks.cap = (cap + 1) * kChunkRecs * 8;
     P.chunk_cap = cap;
     return TPGEN_OK;
 }
@@ -472,8 +567,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
                     ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], (h[1] >> 32) - qbase);
         }
         if (ovf & 1u) P.overflow = true;
-        P.chunk_used = h[4];
-        P.chunk_hwm = std::max<uint64_t>(P.chunk_hwm, h[4]);
+        P.chunk_used = std::min<uint64_t>(h[4], P.chunk_cap);  // (reserved-but-unused chunks may overshoot)
+        P.chunk_hwm = std::max<uint64_t>(P.chunk_hwm, P.chunk_used);
         P.q_hwm = std::max<uint64_t>(P.q_hwm, h[1] >> 32);
         P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
         P.blk_used = h[6];
@@ -703,10 +798,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     ow->device = P.device;
     std::unique_ptr<OutOwner> ow_guard(ow);
     void *d_off = nullptr, *d_vert = nullptr;
-    TPG_TRY(out_alloc_device(o, ow, (size_t)(n_pp + 1) * 8, &d_off, s));
-    ow->p_off = d_off;
-    TPG_TRY(out_alloc_device(o, ow, (size_t)n_vert * 4, &d_vert, s));
-    ow->p_vert = d_vert;
+    TPG_TRY(out_alloc_pair(o, ow, (size_t)(n_pp + 1) * 8, (size_t)n_vert * 4, &d_off, &d_vert, s));
     const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = (int64_t)tot[C_HEADS];
     TPG_TRY(P.heads.ensure(std::max<int64_t>(n_heads, 1) * sizeof(HeadRec), s));
     TPG_TRY(P.head_pool.ensure(std::max<uint64_t>(tot[C_HEADV], 1) * 4, s));
@@ -960,10 +1052,7 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
     ow->device = P.device;
     std::unique_ptr<OutOwner> ow_guard(ow);
     void *d_off = nullptr, *d_vert = nullptr;
-    TPG_TRY(out_alloc_device(o, ow, (size_t)(n + 1) * 8, &d_off, s));
-    ow->p_off = d_off;
-    TPG_TRY(out_alloc_device(o, ow, (size_t)total * 4, &d_vert, s));
-    ow->p_vert = d_vert;
+    TPG_TRY(out_alloc_pair(o, ow, (size_t)(n + 1) * 8, (size_t)total * 4, &d_off, &d_vert, s));
     A.tp_off = (int64_t *)d_off;
     A.tp_vert = (int32_t *)d_vert;
     if (n > 0) {

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
         const int sgid = __ldg(G.slot_gid + vb + __shfl_sync(kFull, P[0], 0));
         Cursor cu = unit_cursor(A, u);
         const int64_t nrec = A.rcount[u];
-        RecReader rd{A.chunks + A.rfirst[u] * kChunkRecs, 0};
+        RecReader rd{A.chunks + (A.rfirst[u] & ~(int64_t)(kChunkRecs - 1)), (int)(A.rfirst[u] & (kChunkRecs - 1))};
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
             const uint64_t myrec = fetch32(A, rd, nb, lane);
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs 
         const int s0g = (ga >= 0) ? ga + s0 : __ldg(G.slot_gid + vb + s0);  // global id of the start vertex
         Cursor cu = unit_cursor(A, u);
         const int64_t nrec = A.rcount[u];
-        RecReader rd{A.chunks + A.rfirst[u] * kChunkRecs, 0};
+        RecReader rd{A.chunks + (A.rfirst[u] & ~(int64_t)(kChunkRecs - 1)), (int)(A.rfirst[u] & (kChunkRecs - 1))};
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
             const uint64_t myrec = fetch32(A, rd, nb, lane);  // lanes >= nb: 0 = an empty R_PATH
