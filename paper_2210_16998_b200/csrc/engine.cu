@@ -423,6 +423,7 @@ static tpgen_status grow_keep(DevBuf &b, size_t used, size_t cap, size_t es, cud
 template <int W>
 static tpgen_status grow_queue(PlanImpl &P, uint64_t used, uint64_t cap, cudaStream_t s) {
     if (cap <= P.qcap) return TPGEN_OK;
+    cap = std::max<uint64_t>(cap, P.qcap * 2);  // geometric: creeping high-water marks must not regrow every call
     TPG_TRY(grow_keep(P.qunits, used, cap, sizeof(Unit<W>), s));
     TPG_TRY(grow_keep(P.qready, used, cap, 4, s));
     for (int c = 0; c < C_NUM; c++) TPG_TRY(grow_keep(P.qcnt[c], used, cap, 8, s));
