@@ -113,6 +113,7 @@ struct MT<Mask<WW>> {
 enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAIL, R_TRANSIT = EV_TRANSIT, R_ARG = 6 };
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
+constexpr int kStepsPerIter = 8; // DFS steps per pass of the persistent loop
 
 // Event codes inside the DFS: type in bits 0-2, closure flag bit 3, path length in bits 8+.
 constexpr int EV_CLO = 8;
@@ -494,7 +495,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     snap_pending = false;
                     have = true;
                 }
-            } else if (((iter & 15u) == 0u) || !prev_active) {
+            } else if (((iter & 1u) == 0u) || !prev_active) {
                 td = *reinterpret_cast<volatile unsigned long long *>(&s_td);
                 hd = *reinterpret_cast<volatile unsigned long long *>(&s_head);
                 ov = *reinterpret_cast<volatile unsigned *>(&s_ov);
@@ -609,7 +610,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         // ---------------- queue snapshot for donation / termination (lane 0, consumed next iteration)
         const bool any_active = __ballot_sync(kFull, L.active) != 0;
         prev_active = any_active;
-        if (wid == 0 && !snap_pending && (((iter & 15u) == 0u) || !any_active)) {
+        if (wid == 0 && !snap_pending && (((iter & 1u) == 0u) || !any_active)) {
             if (lane == 0) {
                 snap_td = ld_volatile(A.qtd);
                 snap_head = ld_volatile(A.qhead);
@@ -637,47 +638,53 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             continue;
         }
 
-        // ---------------- one step for every running lane (lanes that just started emit their root event)
-        if (L.active && !L.done && !(fresh && ev != 0)) {
-            ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
-            L.steps++;
-        }
-
-        // ---------------- event: counters + one record (lane-local)
-        if (ev) {
-            const int ty = ev_type(ev);
-            const uint64_t len = (uint64_t)ev_len(ev);
-            // HEAD / TRANSIT carry their out-arc in an R_ARG record written just before them
-            if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
-            rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 13) |
-                              (L.pend << 16));
-            L.base += L.pn;
-            L.pn = 0;
-            L.pend = 0;
-            if (ty == EV_PP) {
-                c_pp += 1;
-                c_vert += len;
-            } else if (ty == EV_HEAD) {
-                const int32_t x = __ldg(G.out_gid + e);
-                const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
-                c_pp = sat_add(c_pp, Wx, A.overflow);
-                c_vert = sat_add(c_vert, sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow), A.overflow);
-                c_hd += 1;
-                c_hdv += (uint32_t)len;
-            } else if (ty == EV_TAIL) {
-                c_it += 1;
-                c_itv += (uint32_t)len;
-                atomicAdd(A.agg_tail_cnt + L.vb + L.s, 1ull);
-                atomicAdd(A.agg_tail_len + L.vb + L.s, (unsigned long long)len);
-            } else {  // EV_TRANSIT
-                c_it += 1;
-                c_itv += (uint32_t)len;
-                const int32_t nout = __ldg(G.scc_nout + uscc);
-                const int64_t pair = __ldg(G.scc_pair_base + uscc) +
-                                     (int64_t)__ldg(G.slot_eidx + L.vb + L.s) * nout - __ldg(G.scc_out_base + uscc) + e;
-                atomicAdd(A.agg_pair_cnt + pair, 1ull);
-                atomicAdd(A.agg_pair_len + pair, (unsigned long long)len);
+        // ---------------- kStepsPerIter DFS steps for every running lane; the queue housekeeping
+        // above runs once per kStepsPerIter steps (lanes that just started emit their root event first)
+#pragma unroll 1
+        for (int t = 0; t < kStepsPerIter; t++) {
+            if (L.active && !L.done && !(fresh && ev != 0)) {
+                ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
+                L.steps++;
             }
+
+            // ---------------- event: counters + one record (lane-local)
+            if (ev) {
+                const int ty = ev_type(ev);
+                const uint64_t len = (uint64_t)ev_len(ev);
+                // HEAD / TRANSIT carry their out-arc in an R_ARG record written just before them
+                if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
+                rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 13) |
+                                  (L.pend << 16));
+                L.base += L.pn;
+                L.pn = 0;
+                L.pend = 0;
+                if (ty == EV_PP) {
+                    c_pp += 1;
+                    c_vert += len;
+                } else if (ty == EV_HEAD) {
+                    const int32_t x = __ldg(G.out_gid + e);
+                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                    c_pp = sat_add(c_pp, Wx, A.overflow);
+                    c_vert = sat_add(c_vert, sat_add(sat_mul(len, Wx, A.overflow), Vx, A.overflow), A.overflow);
+                    c_hd += 1;
+                    c_hdv += (uint32_t)len;
+                } else if (ty == EV_TAIL) {
+                    c_it += 1;
+                    c_itv += (uint32_t)len;
+                    atomicAdd(A.agg_tail_cnt + L.vb + L.s, 1ull);
+                    atomicAdd(A.agg_tail_len + L.vb + L.s, (unsigned long long)len);
+                } else {  // EV_TRANSIT
+                    c_it += 1;
+                    c_itv += (uint32_t)len;
+                    const int32_t nout = __ldg(G.scc_nout + uscc);
+                    const int64_t pair = __ldg(G.scc_pair_base + uscc) +
+                                         (int64_t)__ldg(G.slot_eidx + L.vb + L.s) * nout - __ldg(G.scc_out_base + uscc) + e;
+                    atomicAdd(A.agg_pair_cnt + pair, 1ull);
+                    atomicAdd(A.agg_pair_len + pair, (unsigned long long)len);
+                }
+            }
+            ev = 0;
+            fresh = false;
         }
 
         // ---------------- donate on demand (feed: set by this iteration's queue snapshot)
