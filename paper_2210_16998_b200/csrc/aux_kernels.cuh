@@ -326,31 +326,74 @@ __global__ void stitch_kernel(StitchArgs A) {
     }
 }
 
+// COUNT_HASH mode: the digest of every cross-SCC prime path without writing it;
+// one thread per path (completion), vertices absorbed in path order.
+__global__ void stitch_hash_kernel(StitchArgs A, unsigned long long *acc) {
+    uint64_t sa = 0, sb = 0;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < A.n_comp;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t h = upper_bound_u64(A.comp_off, 0, A.n_heads, g) - 1;
+        const HeadRec H = A.heads[h];
+        const uint64_t k = g - A.comp_off[h];
+        // pass 1: length of completion k
+        uint64_t len = (uint64_t)H.len, kk = k;
+        int32_t x = H.x;
+        while (true) {
+            const int64_t b = A.ibeg[x], e = A.iend[x];
+            const uint64_t bc = A.cum[b];
+            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            const uint64_t k2 = kk - (A.cum[i] - bc);
+            const ItemRec it = A.items[i];
+            len += (uint64_t)it.len;
+            if (it.y < 0) break;
+            x = it.y;
+            kk = k2;
+        }
+        // pass 2: absorb head, transits, tail
+        PathHash hs;
+        hs.init(len);
+        for (int j = 0; j < H.len; j++) hs.add(A.head_pool[H.hv_off + j]);
+        kk = k;
+        x = H.x;
+        while (true) {
+            const int64_t b = A.ibeg[x], e = A.iend[x];
+            const uint64_t bc = A.cum[b];
+            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            const uint64_t k2 = kk - (A.cum[i] - bc);
+            const ItemRec it = A.items[i];
+            const int32_t *src = A.item_pool + it.pool_off;
+            for (int j = 0; j < it.len; j++) hs.add(src[j]);
+            if (it.y < 0) break;
+            x = it.y;
+            kk = k2;
+        }
+        sa += hs.a;
+        sb += hs.b;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        sa += __shfl_xor_sync(kFull, sa, d);
+        sb += __shfl_xor_sync(kFull, sb, d);
+    }
+    if ((threadIdx.x & 31) == 0 && (sa | sb)) {
+        atomicAdd(acc, (unsigned long long)sa);
+        atomicAdd(acc + 1, (unsigned long long)sb);
+    }
+}
+
 __global__ void set_last_offset_kernel(int64_t *off, int64_t n_paths, int64_t total) { off[n_paths] = total; }
 
 // ------------------------------------------------------------- digest (K8)
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    z ^= z >> 30;
-    z *= 0xbf58476d1ce4e5b9ull;
-    z ^= z >> 27;
-    z *= 0x94d049bb133111ebull;
-    z ^= z >> 31;
-    return z;
-}
 
 __global__ void digest_kernel(const int64_t *off, const int32_t *vert, int64_t n, unsigned long long *acc) {
     uint64_t a = 0, b = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = off[i], e = off[i + 1];
-        uint64_t za = mix64(0x9E3779B97F4A7C15ull ^ (uint64_t)(e - s));
-        uint64_t zb = mix64(0xD1B54A32D192ED03ull ^ (uint64_t)(e - s));
-        for (int64_t j = s; j < e; j++) {
-            const uint64_t v = (uint64_t)(uint32_t)__ldg(vert + j);
-            za = mix64(za ^ v);
-            zb = mix64(zb ^ v);
-        }
-        a += za;
-        b += zb;
+        PathHash h;
+        h.init((uint64_t)(e - s));
+        for (int64_t j = s; j < e; j++) h.add(__ldg(vert + j));
+        a += h.a;
+        b += h.b;
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) {

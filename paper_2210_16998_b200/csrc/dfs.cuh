@@ -135,6 +135,17 @@ __device__ __forceinline__ void sts_u8(uint32_t a, int v) {
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// n <= 5 consecutive path bytes starting at position p (shared-memory layout of pidx):
+// two 32-bit words of the lane's column, funnel-shifted.
+template <int W>
+__device__ __forceinline__ uint64_t path_bytes(uint32_t mp, int p, int n) {
+    const int q = p >> 2;
+    uint32_t lo, hi = 0u;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(mp + (q << 7)) : "memory");
+    if (q + 1 < 16 * W) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(mp + ((q + 1) << 7)) : "memory");
+    const uint64_t v = (((uint64_t)hi << 32) | lo) >> (8 * (p & 3));
+    return v & ((1ull << (8 * n)) - 1ull);
+}
 
 template <class T>
 struct Lane {
@@ -142,9 +153,9 @@ struct Lane {
     int32_t vb, s, u, l, r, k, o, ooff, ocnt, flags;
     uint32_t steps;
     bool active, done, seg, emit;
-    // record stream state: the decoder knows path[0..base); pend holds path[base..l] (pn bytes)
-    int32_t base, pn;
-    uint64_t pend;
+    // record stream state: the decoder knows path[0..base) (base <= l+1); the bytes
+    // path[base..l] are read from the shared-memory path when the next record is written
+    int32_t base;
 };
 
 // View of the slot table: staged in shared memory (TS) when it fits, else read through L1.
@@ -267,25 +278,8 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
     load_slot(tab, L, L.u);
     if (pop && L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: exit vertices only
     else if (push) L.o = 0;
-    // record-stream bookkeeping: pending bytes follow pushes and pops
-    if (push) {
-        if (L.pn == kRecBytes) {  // flush a continuation record
-            rec_put(A, R, (uint64_t)R_PATH | ((uint64_t)L.base << 4) | ((uint64_t)kRecBytes << 13) |
-                              (L.pend << 16));
-            L.base += kRecBytes;
-            L.pn = 0;
-            L.pend = 0;
-        }
-        L.pend |= (uint64_t)w << (8 * L.pn);
-        L.pn++;
-    } else if (pop) {
-        if (L.pn > 0) {
-            L.pn--;
-            L.pend &= ~(0xffull << (8 * L.pn));
-        } else {
-            L.base--;
-        }
-    }
+    // record stream: a pop below the decoder's known prefix shortens it
+    if (pop) L.base = min(L.base, L.l + 1);
     if (L.emit && has) ext++;
     if (clo) return L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
     return push ? node_event(L, w) : 0;
@@ -554,8 +548,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 nchild = 0;
                 last_split = 0;
                 L.base = depth + 1;
-                L.pn = 0;
-                L.pend = 0;
                 fresh = true;
                 ext = 0;
                 c_pp = c_vert = 0;
@@ -653,11 +645,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 const uint64_t len = (uint64_t)ev_len(ev);
                 // HEAD / TRANSIT carry their out-arc in an R_ARG record written just before them
                 if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
-                rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)L.pn << 13) |
-                                  (L.pend << 16));
-                L.base += L.pn;
-                L.pn = 0;
-                L.pend = 0;
+                // the bytes path[base..l] the decoder lacks, <= kRecBytes per record
+                int nb = L.l + 1 - L.base;
+                while (nb > kRecBytes) {  // continuation records
+                    rec_put(A, R, (uint64_t)R_PATH | ((uint64_t)L.base << 4) | ((uint64_t)kRecBytes << 13) |
+                                      (path_bytes<MT<T>::W>(mp, L.base, kRecBytes) << 16));
+                    L.base += kRecBytes;
+                    nb -= kRecBytes;
+                }
+                rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)nb << 13) |
+                                  (path_bytes<MT<T>::W>(mp, L.base, nb) << 16));
+                L.base = L.l + 1;
                 if (ty == EV_PP) {
                     c_pp += 1;
                     c_vert += len;

@@ -431,9 +431,9 @@ static tpgen_status grow_queue(PlanImpl &P, uint64_t used, uint64_t cap, cudaStr
     TPG_TRY(grow_keep(P.qrfirst, used, cap, 8, s));
     TPG_TRY(grow_keep(P.qrcount, used, cap, 8, s));
     TPG_TRY(grow_keep(P.qchead, used, cap, 8, s));
-    TPG_TRY(grow_keep(P.blk_first, P.blk_used, cap, 8, s));
-    TPG_TRY(grow_keep(P.blk_count, P.blk_used, cap, 4, s));
-    TPG_TRY(grow_keep(P.blk_next, P.blk_used, cap, 8, s));
+    TPG_TRY(grow_keep(P.blk_first, used, cap, 8, s));  // blocks are named by their first slot
+    TPG_TRY(grow_keep(P.blk_count, used, cap, 4, s));
+    TPG_TRY(grow_keep(P.blk_next, used, cap, 8, s));
     TPG_TRY(grow_keep(P.qgen, used, cap, 4, s));
     TPG_TRY(grow_keep(P.qparent, used, cap, 8, s));
     TPG_TRY(grow_keep(P.qnchild, used, cap, 4, s));
@@ -476,17 +476,23 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
     if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
     TPG_TRY(P.qctr.ensure(7 * 16 * 8, s));
     unsigned long long *qc = P.qctr.as<unsigned long long>();
-    for (int attempt = 0; attempt < 32; attempt++) {
+    // Test hooks: TPGEN_TEST_QCAP / TPGEN_TEST_POOL cap the queue slots / record chunks this
+    // phase may use (doubling after each overflow), so small graphs exercise the retry path.
+    uint64_t qlim = P.qcap, plim = P.chunk_cap;
+    if (const char *ev = getenv("TPGEN_TEST_QCAP"))
+        qlim = std::min<uint64_t>(qlim, qbase + nroots + std::max<uint64_t>(1, strtoull(ev, nullptr, 10)));
+    if (const char *ev = getenv("TPGEN_TEST_POOL"))
+        plim = std::min<uint64_t>(plim, P.chunk_used + std::max<uint64_t>(1, strtoull(ev, nullptr, 10)));
+    for (int attempt = 0; attempt < 48; attempt++) {
         TPG_TRY(put_roots<W>(P, roots, qbase, s));
         TPG_CK(cudaMemsetAsync(P.qready.as<uint32_t>() + qbase + nroots, 0, (P.qcap - qbase - nroots) * 4, s));
-        // queue counters, one per 128-byte line: head, tail<<32|done, overflow, chunk_next, maxgen, blk_ctr
+        // queue counters, one per 128-byte line: head, tail<<32|done, overflow, chunk_next, maxgen
         unsigned long long init[7 * 16];
         memset(init, 0, sizeof(init));
         init[0] = qbase;
         init[16] = ((qbase + nroots) << 32) | qbase;
         init[48] = P.chunk_used;
         init[64] = (unsigned long long)P.maxgen;
-        init[80] = P.blk_used;
         TPG_CK(cudaMemcpyAsync(qc, init, sizeof(init), cudaMemcpyHostToDevice, s));
         DfsArgs A;
         memset(&A, 0, sizeof(A));
@@ -495,7 +501,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.ready = P.qready.as<unsigned int>();
         A.qhead = qc;
         A.qtd = qc + 16;
-        A.qcap = P.qcap;
+        A.qcap = qlim;
         for (int c = 0; c < C_NUM; c++) A.cnt[c] = P.qcnt[c].as<uint64_t>();
         A.ext = P.qext.as<uint64_t>();
         A.rfirst = P.qrfirst.as<int64_t>();
@@ -504,7 +510,6 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.blk_first = P.blk_first.as<int64_t>();
         A.blk_count = P.blk_count.as<int32_t>();
         A.blk_next = P.blk_next.as<int64_t>();
-        A.blk_ctr = qc + 80;
         A.gen = P.qgen.as<int32_t>();
         A.parent = P.qparent.as<int64_t>();
         A.nchild = P.qnchild.as<int32_t>();
@@ -517,7 +522,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.overflow = reinterpret_cast<unsigned int *>(qc + 32);
         A.chunks = P.chunks.as<uint64_t>();
         A.chunk_next = qc + 48;
-        A.chunk_cap = P.chunk_cap;
+        A.chunk_cap = plim;  // (the sink chunk is chunk plim: inside the allocation)
         A.split_min = P.split_min;
         A.dbg = nullptr;
         if (getenv("TPGEN_DEBUG")) {
@@ -552,8 +557,22 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         const unsigned ovf = (unsigned)h[3];
         if (ovf & 6u) {  // record pool or queue exhausted: undo and retry bigger
             if (seg) TPG_CK(cudaMemcpyAsync(P.agg.p, P.agg_bak.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
-            if (ovf & 2u) TPG_TRY(grow_pool(P, std::max<uint64_t>(h[4], P.chunk_cap) * 2, s));
-            if (ovf & 4u) TPG_TRY(grow_queue<W>(P, qbase, P.qcap * 2, s));
+            if (ovf & 2u) {
+                if (plim < P.chunk_cap) {
+                    plim = std::min<uint64_t>(P.chunk_cap, plim * 2);
+                } else {
+                    TPG_TRY(grow_pool(P, std::max<uint64_t>(h[4], P.chunk_cap) * 2, s));
+                    plim = P.chunk_cap;
+                }
+            }
+            if (ovf & 4u) {
+                if (qlim < P.qcap) {
+                    qlim = std::min<uint64_t>(P.qcap, qlim * 2);
+                } else {
+                    TPG_TRY(grow_queue<W>(P, qbase, P.qcap * 2, s));
+                    qlim = P.qcap;
+                }
+            }
             continue;
         }
         if (A.dbg) {
@@ -572,12 +591,59 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         P.chunk_hwm = std::max<uint64_t>(P.chunk_hwm, P.chunk_used);
         P.q_hwm = std::max<uint64_t>(P.q_hwm, h[1] >> 32);
         P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
-        P.blk_used = h[6];
         tail_out = h[1] >> 32;
         return TPGEN_OK;
     }
     set_error("DFS phase: work queue / record pool could not be sized");
     return TPGEN_ERR_OUT_OF_MEMORY;
+}
+
+// Canonical writer launch: the lane-parallel kernel when every SCC has at most
+// kFastMaxScc vertices (one mask word), else the sequential replay.  HASH: digest only.
+template <int NPW, bool HASH>
+static void launch_fast(const ExpandArgs &E, int64_t nu, int num_sms, cudaStream_t s) {
+    constexpr int th = FastCfg<NPW>::threads;
+    expand_fast_kernel<NPW, HASH><<<grid_for(nu * 32, th, num_sms * 2048 / th), th, 0, s>>>(E);
+}
+template <bool HASH>
+static void launch_fast_npw(int npw, const ExpandArgs &E, int64_t nu, int num_sms, cudaStream_t s) {
+    switch (npw) {
+        case 1: launch_fast<1, HASH>(E, nu, num_sms, s); break;
+        case 2: launch_fast<2, HASH>(E, nu, num_sms, s); break;
+        case 3: launch_fast<3, HASH>(E, nu, num_sms, s); break;
+        case 4: launch_fast<4, HASH>(E, nu, num_sms, s); break;
+        case 5: launch_fast<5, HASH>(E, nu, num_sms, s); break;
+        case 6: launch_fast<6, HASH>(E, nu, num_sms, s); break;
+        case 7: launch_fast<7, HASH>(E, nu, num_sms, s); break;
+        case 8: launch_fast<8, HASH>(E, nu, num_sms, s); break;
+        case 9: launch_fast<9, HASH>(E, nu, num_sms, s); break;
+        case 10: launch_fast<10, HASH>(E, nu, num_sms, s); break;
+        case 11: launch_fast<11, HASH>(E, nu, num_sms, s); break;
+        case 12: launch_fast<12, HASH>(E, nu, num_sms, s); break;
+        case 13: launch_fast<13, HASH>(E, nu, num_sms, s); break;
+        case 14: launch_fast<14, HASH>(E, nu, num_sms, s); break;
+        case 15: launch_fast<15, HASH>(E, nu, num_sms, s); break;
+        default: launch_fast<16, HASH>(E, nu, num_sms, s); break;
+    }
+}
+template <int W, bool HASH>
+static void launch_seq(int np, const ExpandArgs &E, int64_t nu, int num_sms, cudaStream_t s) {
+    const int eg = grid_for(nu * 32, kExpandThreads, num_sms * 8);
+    if (W == 1 && np <= 1) expand_kernel<W, 1, HASH><<<eg, kExpandThreads, 0, s>>>(E);
+    else if (W == 1 && np <= 2) expand_kernel<W, 2, HASH><<<eg, kExpandThreads, 0, s>>>(E);
+    else expand_kernel<W, 2 * W + 1, HASH><<<eg, kExpandThreads, 0, s>>>(E);
+}
+template <int W>
+static void launch_expand(const HostPlan &H, const ExpandArgs &E, int64_t nu, int num_sms, bool hash, cudaStream_t s) {
+    const int np = (H.max_scc + 1 + 31) / 32;  // registers per lane for the longest emitted path
+    const int npw = std::max(1, (H.max_scc + 3) / 4);  // 32-bit words of local ids for the longest path
+    if (W == 1 && H.max_scc <= kFastMaxScc && !getenv("TPGEN_SLOW_EXPAND")) {
+        if (hash) launch_fast_npw<true>(npw, E, nu, num_sms, s);
+        else launch_fast_npw<false>(npw, E, nu, num_sms, s);
+    } else {
+        if (hash) launch_seq<W, true>(np, E, nu, num_sms, s);
+        else launch_seq<W, false>(np, E, nu, num_sms, s);
+    }
 }
 
 template <class T>
@@ -605,7 +671,6 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     P.overflow = false;
     P.chunk_used = 0;
     P.maxgen = 0;
-    P.blk_used = 0;
     // TPGEN_DEBUG=1: host time per stage with a sync before each mark; =2: no syncs (enqueue times)
     const char *hdbg_env = getenv("TPGEN_DEBUG");
     const bool hdbg = hdbg_env != nullptr;
@@ -778,7 +843,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     st.n_paths = n_pp;
     st.total_vertices = n_vert;
 
-    if (o.output_mode == TPGEN_OUT_COUNT_HASH) {
+    const bool hash_only = (o.output_mode == TPGEN_OUT_COUNT_HASH);
+    if (hash_only && !o.compute_digest) {  // counts only: no writer at all
         cudaEventRecord(tall.b, s);
         TPG_CK(cudaStreamSynchronize(s));
         float ms = 0;
@@ -799,7 +865,9 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     ow->device = P.device;
     std::unique_ptr<OutOwner> ow_guard(ow);
     void *d_off = nullptr, *d_vert = nullptr;
-    TPG_TRY(out_alloc_pair(o, ow, (size_t)(n_pp + 1) * 8, (size_t)n_vert * 4, &d_off, &d_vert, s));
+    if (!hash_only) TPG_TRY(out_alloc_pair(o, ow, (size_t)(n_pp + 1) * 8, (size_t)n_vert * 4, &d_off, &d_vert, s));
+    unsigned long long *hacc = ctr + 16;  // digest accumulators (COUNT_HASH: filled by the writers)
+    TPG_CK(cudaMemsetAsync(hacc, 0, 16, s));
     const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = (int64_t)tot[C_HEADS];
     TPG_TRY(P.heads.ensure(std::max<int64_t>(n_heads, 1) * sizeof(HeadRec), s));
     TPG_TRY(P.head_pool.ensure(std::max<uint64_t>(tot[C_HEADV], 1) * 4, s));
@@ -823,25 +891,10 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     E.head_pool = P.head_pool.as<int32_t>();
     E.items = P.items.as<ItemRec>();
     E.item_pool = P.item_pool.as<int32_t>();
+    E.hash_acc = hacc;
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        const int eg = grid_for(nu * 32, kExpandThreads, P.num_sms * 8);
-        const int np = (H.max_scc + 1 + 31) / 32;  // registers per lane for the longest emitted path
-        const int npw = (H.max_scc + 3) / 4;         // 32-bit words of local ids for the longest path
-        if (W == 1 && H.max_scc <= kFastMaxScc && !getenv("TPGEN_SLOW_EXPAND")) {
-            switch (npw) {
-                case 1: expand_fast_kernel<1><<<eg, kExpandThreads, 0, s>>>(E); break;
-                case 2: expand_fast_kernel<2><<<eg, kExpandThreads, 0, s>>>(E); break;
-                case 3: expand_fast_kernel<3><<<eg, kExpandThreads, 0, s>>>(E); break;
-                case 4: expand_fast_kernel<4><<<eg, kExpandThreads, 0, s>>>(E); break;
-                case 5: expand_fast_kernel<5><<<eg, kExpandThreads, 0, s>>>(E); break;
-                case 6: expand_fast_kernel<6><<<eg, kExpandThreads, 0, s>>>(E); break;
-                case 7: expand_fast_kernel<7><<<eg, kExpandThreads, 0, s>>>(E); break;
-                default: expand_fast_kernel<8><<<eg, kExpandThreads, 0, s>>>(E); break;
-            }
-        } else if (W == 1 && np <= 1) expand_kernel<W, 1><<<eg, kExpandThreads, 0, s>>>(E);
-        else if (W == 1 && np <= 2) expand_kernel<W, 2><<<eg, kExpandThreads, 0, s>>>(E);
-        else expand_kernel<W, 2 * W + 1><<<eg, kExpandThreads, 0, s>>>(E);
+        launch_expand<W>(H, E, nu, P.num_sms, hash_only, s);
         launches++;
     }
     cudaEventRecord(tw.b, s);
@@ -890,22 +943,27 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         SA.out_off = (int64_t *)d_off;
         SA.out_vert = (int32_t *)d_vert;
         if (ncomp > 0) {
-            stitch_kernel<<<grid_for((int64_t)ncomp * 32, 256, P.num_sms * 8), 256, 0, s>>>(SA);
+            if (hash_only) stitch_hash_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(SA, hacc);
+            else stitch_kernel<<<grid_for((int64_t)ncomp * 32, 256, P.num_sms * 8), 256, 0, s>>>(SA);
             launches++;
         }
     }
-    set_last_offset_kernel<<<1, 1, 0, s>>>((int64_t *)d_off, n_pp, n_vert);
-    launches++;
+    if (!hash_only) {
+        set_last_offset_kernel<<<1, 1, 0, s>>>((int64_t *)d_off, n_pp, n_vert);
+        launches++;
+    }
     cudaEventRecord(tst.b, s);
     cudaEventRecord(tall.b, s);
     TPG_CK(cudaGetLastError());
 
     if (o.compute_digest && n_pp > 0) {
-        unsigned long long *acc = ctr + 16;
-        TPG_CK(cudaMemsetAsync(acc, 0, 16, s));
-        digest_kernel<<<grid_for(n_pp, 256, P.num_sms * 8), 256, 0, s>>>((int64_t *)d_off, (int32_t *)d_vert, n_pp,
-                                                                           acc);
-        launches++;
+        unsigned long long *acc = hacc;
+        if (!hash_only) {
+            TPG_CK(cudaMemsetAsync(acc, 0, 16, s));
+            digest_kernel<<<grid_for(n_pp, 256, P.num_sms * 8), 256, 0, s>>>((int64_t *)d_off, (int32_t *)d_vert,
+                                                                               n_pp, acc);
+            launches++;
+        }
         unsigned long long hd[2];
         TPG_CK(cudaMemcpyAsync(hd, acc, 16, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
@@ -926,8 +984,10 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     st.gpu_launches = launches;
 
     HT("before finish_output");
-    ow_guard.release();
-    TPG_TRY(finish_output(o, ow, n_pp, n_vert, (int64_t *)d_off, (int32_t *)d_vert, s, out));
+    if (!hash_only) {
+        ow_guard.release();
+        TPG_TRY(finish_output(o, ow, n_pp, n_vert, (int64_t *)d_off, (int32_t *)d_vert, s, out));
+    }
     st.ms_total = now_ms() - t0;
     if (stp) *stp = st;
     return TPGEN_OK;

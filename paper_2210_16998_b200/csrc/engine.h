@@ -38,7 +38,6 @@ struct PlanImpl {
     DevBuf qparent, qnchild;  // donor / number of donated units, per unit
     DevBuf blk_first, blk_count, blk_next;  // donated blocks (one per donation)
     uint64_t qcap = 0;
-    uint64_t blk_used = 0;
     DevBuf chunks, agg, agg_bak;  // path-delta record pool (chunks of kChunkRecs words); SEG aggregates + backup
     uint64_t chunk_cap = 0;       // pool capacity in chunks
     uint64_t chunk_used = 0;      // chunks handed out so far in this call

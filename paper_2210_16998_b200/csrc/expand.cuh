@@ -40,6 +40,7 @@ struct ExpandArgs {
     int32_t *head_pool;
     ItemRec *items;
     int32_t *item_pool;
+    unsigned long long *hash_acc;  // HASH kernels: digest of the prime paths instead of writing them
 };
 
 constexpr int kExpandThreads = 256;
@@ -92,9 +93,9 @@ __device__ __forceinline__ uint64_t fetch32(const ExpandArgs &A, RecReader &rd, 
 
 // Sequential replay of one record (warp-uniform `rec`); P = the current path
 // distributed over the lanes (lane q holds positions q + 32 r).
-template <int NP>
+template <int NP, bool HASH>
 __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, int (&P)[NP], Cursor &cu, int lane,
-                                           int ga, int vb, int sgid) {
+                                           int ga, int vb, int sgid, PathHash &acc) {
     const DevGraph &G = A.G;
     const int ty = (int)(rec & 7);
     if (ty == R_ARG) {
@@ -112,6 +113,26 @@ __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, in
     const int len = cc + n;
     const int tot = len + (int)((rec >> 3) & 1);
     int32_t *dst;
+    if (HASH && ty == R_PP) {  // digest only: absorb the vertices in order (lane q holds position q + 32 r)
+        const int s0 = __shfl_sync(kFull, P[0], 0);
+        PathHash hs;
+        hs.init((uint64_t)tot);
+        for (int pos = 0; pos < tot; pos++) {
+            int xq = 0;
+#pragma unroll
+            for (int r = 0; r < NP; r++)
+                if (r == (pos >> 5)) xq = P[r];
+            const int loc = (pos < len) ? __shfl_sync(kFull, xq, pos & 31) : s0;
+            hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
+        }
+        if (lane == 0) {
+            acc.a += hs.a;
+            acc.b += hs.b;
+        }
+        cu.pp += 1;
+        cu.vv += (uint64_t)tot;
+        return;
+    }
     if (ty == R_PP) {
         dst = A.out_vert + cu.vv;
         if (lane == 0) A.out_off[cu.pp] = (int64_t)cu.vv;
@@ -165,7 +186,19 @@ __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, in
 }
 
 // NP = path registers per lane: ceil((longest emitted path + closing vertex) / 32).
-template <int W, int NP>
+__device__ __forceinline__ void flush_hash(const ExpandArgs &A, PathHash &acc) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        acc.a += __shfl_xor_sync(kFull, acc.a, d);
+        acc.b += __shfl_xor_sync(kFull, acc.b, d);
+    }
+    if ((threadIdx.x & 31) == 0 && (acc.a | acc.b)) {
+        atomicAdd(A.hash_acc, (unsigned long long)acc.a);
+        atomicAdd(A.hash_acc + 1, (unsigned long long)acc.b);
+    }
+}
+
+template <int W, int NP, bool HASH>
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
     const int lane = threadIdx.x & 31;
     const DevGraph &G = A.G;
@@ -173,6 +206,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
 
+    PathHash acc{0, 0};
     for (int64_t u = gw; u < A.n_units; u += nw) {
         const Unit<W> *U = units + u;
         const int4 h = *reinterpret_cast<const int4 *>(&U->scc);
@@ -192,22 +226,31 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
             const uint64_t myrec = fetch32(A, rd, nb, lane);
-            for (int i = 0; i < nb; i++) replay_one<NP>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, sgid);
+            for (int i = 0; i < nb; i++)
+                replay_one<NP, HASH>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, sgid, acc);
         }
     }
+    if (HASH) flush_hash(A, acc);
 }
 
 // ---------------------------------------------------------------- fast path
-constexpr int kFastMaxScc = 31;      // a path + its closing vertex fits one 32-lane row
-constexpr int kStageInts = 32 * 32;  // one batch: 32 paths of at most 32 output vertices
+constexpr int kFastMaxScc = 63;  // a path of local ids fits NPW <= 16 32-bit words (W = 1 masks)
+
+template <int NPW>
+struct FastCfg {
+    static constexpr int threads = (NPW > 8) ? 128 : 256;
+    static constexpr int max_out = 4 * NPW + 1;  // output vertices per path (incl. the closing vertex)
+};
 
 __device__ __forceinline__ uint32_t lop_merge(uint32_t mine, uint32_t other, uint32_t mask) {
     return (mine & mask) | (other & ~mask);  // one LOP3
 }
 
-template <int NPW>
-__global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs A) {
-    __shared__ __align__(16) int32_t stage_all[kExpandThreads / 32][kStageInts];
+template <int NPW, bool HASH>
+__global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(ExpandArgs A) {
+    constexpr int kWarps = FastCfg<NPW>::threads / 32;
+    constexpr int kStage = HASH ? 1 : 32 * FastCfg<NPW>::max_out;  // one batch of paths
+    __shared__ __align__(16) int32_t stage_all[kWarps][kStage];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int32_t *stage = stage_all[wid];
     const DevGraph &G = A.G;
@@ -215,6 +258,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs 
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
+    PathHash acc{0, 0};
 
     for (int64_t u = gw; u < A.n_units; u += nw) {
         const Unit<1> *U = units + u;
@@ -224,11 +268,14 @@ __global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs 
         uint32_t carry[NPW];
         {
             const uint4 *p4 = reinterpret_cast<const uint4 *>(U->path);
-            const uint4 a = p4[0];
-            const uint4 b = (NPW > 4) ? p4[1] : make_uint4(0, 0, 0, 0);
-            const uint32_t w8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int w = 0; w < NPW; w++) carry[w] = w8[w];
+            for (int q = 0; q < (NPW + 3) / 4; q++) {
+                const uint4 v = p4[q];
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (4 * q + j < NPW) carry[4 * q + j] = w4[j];
+            }
         }
         const int vb = __ldg(G.scc_vbase + h.x);
         const int ga = __ldg(G.scc_gbase + h.x);
@@ -273,10 +320,34 @@ __global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs 
                 for (int w = 0; w < NPW; w++) D[w] = lop_merge(D[w], carry[w], M[w]);
 #pragma unroll
                 for (int w = 0; w < NPW; w++) carry[w] = __shfl_sync(kFull, D[w], 31);
-                // ---- emitting lanes: offsets by a warp scan of the path lengths
                 const bool emit = (ty == R_PP);
                 const int len = cc + n;
                 const int tot = emit ? len + (int)((myrec >> 3) & 1) : 0;
+                const unsigned em = __ballot_sync(kFull, emit);
+                if (HASH) {
+                    // ---- digest only: every emitting lane hashes its own path
+                    if (emit) {
+                        PathHash hs;
+                        hs.init((uint64_t)tot);
+#pragma unroll
+                        for (int p = 0; p < 4 * NPW; p++) {
+                            if (p < len) {
+                                const int loc = (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
+                                hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
+                            }
+                        }
+                        if (len < tot) hs.add(s0g);
+                        acc.a += hs.a;
+                        acc.b += hs.b;
+                    }
+                    int T = tot;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) T += __shfl_xor_sync(kFull, T, o);
+                    cu.pp += (uint64_t)__popc(em);
+                    cu.vv += (uint64_t)T;
+                    continue;
+                }
+                // ---- emitting lanes: offsets by a warp scan of the path lengths
                 int ex = tot;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -285,7 +356,6 @@ __global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs 
                 }
                 const int T = __shfl_sync(kFull, ex, 31);
                 ex -= tot;
-                const unsigned em = __ballot_sync(kFull, emit);
                 if (emit) A.out_off[cu.pp + __popc(em & lt_mask)] = (int64_t)(cu.vv + (uint64_t)ex);
                 // ---- stage the vertices (global ids), then stream them out coalesced
                 if (ga >= 0) {
@@ -306,28 +376,35 @@ __global__ void __launch_bounds__(kExpandThreads) expand_fast_kernel(ExpandArgs 
                 cu.vv += (uint64_t)T;
             } else {
                 // ---- segment items / head blocks in this batch: sequential replay
-                int P[1];
-                {
-                    const int w = lane >> 2;
-                    uint32_t x = 0;
+                constexpr int NP = (4 * NPW + 1 + 31) / 32;
+                int P[NP];
 #pragma unroll
-                    for (int k = 0; k < NPW; k++)
-                        if (k == w) x = carry[k];
-                    P[0] = (int)((x >> (8 * (lane & 3))) & 0xff);
+                for (int r = 0; r < NP; r++) {
+                    const int pos = lane + 32 * r;
+                    const int w = pos >> 2;
+                    uint32_t xw = 0;
+#pragma unroll
+                    for (int k2 = 0; k2 < NPW; k2++)
+                        if (k2 == w) xw = carry[k2];
+                    P[r] = (int)((xw >> (8 * (pos & 3))) & 0xff);
                 }
                 for (int i = 0; i < nb; i++)
-                    replay_one<1>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, s0g);
-                // back to bytes: word w = lanes 4w..4w+3
+                    replay_one<NP, HASH>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, s0g, acc);
+                // back to bytes: word w = positions 4w..4w+3 (lane (4w+b) & 31 of register (4w+b) >> 5)
 #pragma unroll
                 for (int w = 0; w < NPW; w++) {
-                    uint32_t x = 0;
+                    uint32_t xw = 0;
 #pragma unroll
-                    for (int b = 0; b < 4; b++) x |= ((uint32_t)__shfl_sync(kFull, P[0], 4 * w + b) & 0xffu) << (8 * b);
-                    carry[w] = x;
+                    for (int b = 0; b < 4; b++) {
+                        const int pos = 4 * w + b;
+                        xw |= ((uint32_t)__shfl_sync(kFull, P[pos >> 5], pos & 31) & 0xffu) << (8 * b);
+                    }
+                    carry[w] = xw;
                 }
             }
         }
     }
+    if (HASH) flush_hash(A, acc);
 }
 
 }  // namespace tpg

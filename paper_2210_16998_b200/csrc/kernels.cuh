@@ -157,7 +157,6 @@ struct DfsArgs {
     int64_t *blk_first;       // donated block: first unit
     int32_t *blk_count;       // donated block: number of units
     int64_t *blk_next;        // donated block: the unit's previous block (-1: none)
-    unsigned long long *blk_ctr;
     int32_t *gen;             // donation generation (roots 0)
     int64_t *parent;          // donor of the unit (roots: -1, set by the host)
     int32_t *nchild;          // number of units the unit donated
@@ -232,6 +231,28 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+
+// Digest: per path z = mix(seed ^ len), then z = mix(z ^ v)
+// for each vertex, under two seeds; the set digest is the sum over paths mod 2^64.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finalizer
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return z;
+}
+struct PathHash {
+    uint64_t a, b;
+    __device__ __forceinline__ void init(uint64_t len) {
+        a = mix64(0x9E3779B97F4A7C15ull ^ len);
+        b = mix64(0xD1B54A32D192ED03ull ^ len);
+    }
+    __device__ __forceinline__ void add(int32_t v) {
+        a = mix64(a ^ (uint64_t)(uint32_t)v);
+        b = mix64(b ^ (uint64_t)(uint32_t)v);
+    }
+};
 
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b, unsigned int *ovf) {
     uint64_t r = a + b;

@@ -190,3 +190,56 @@ def test_test_paths_unreachable():
     with pytest.raises(tp.TpgenError) as ei:
         tp.test_paths(g, 0, 1)
     assert ei.value.status_name == "TPGEN_ERR_UNREACHABLE"
+
+
+@pytest.mark.timeout(900)
+def test_config5_sampled_blocks_and_shards():
+    """Config 5 (16 parallel 56-vertex SCCs, ~1.3e10 extensions) at full size on one GPU.
+
+    * blocks of sampled start vertices (an SCC entry, interior vertices, an SCC
+      exit, a trivial vertex with an empty block) vs the oracle, element by
+      element, with their E_canon and digest;
+    * COUNT_HASH over the whole graph (the one-GPU configuration: the full output
+      is ~200 GB) equals the sum of 8 materialized start-vertex shards, whose
+      digests add up to the count-mode digest."""
+    g = gen.config5()
+    plan = tp.Plan(g)
+    for s in (5, 17, 205, 464, 887):
+        ps = plan.prime_paths(start_range=(s, s + 1), digest=True)
+        o, v = ps.to_numpy()
+        ro, rv = oracle.prime_paths(g, v_lo=s, v_hi=s + 1)
+        np.testing.assert_array_equal(o, ro, err_msg=f"start {s}")
+        np.testing.assert_array_equal(v, rv, err_msg=f"start {s}")
+        assert ps.stats["n_extensions"] == oracle.ext_count(g, v_lo=s, v_hi=s + 1)
+        assert (ps.stats["hash_lo"], ps.stats["hash_hi"]) == oracle.digest(ro, rv)
+        del ps
+    whole = plan.prime_paths(mode="count", digest=True).stats
+    tot_pp = tot_v = tot_e = 0
+    h_lo = h_hi = 0
+    for r in range(8):
+        ps = plan.prime_paths(shard=(r, 8), digest=True)
+        st = ps.stats
+        tot_pp += st["n_paths"]
+        tot_v += st["total_vertices"]
+        tot_e += st["n_extensions"]
+        h_lo = (h_lo + st["hash_lo"]) % (1 << 64)
+        h_hi = (h_hi + st["hash_hi"]) % (1 << 64)
+        del ps
+    assert whole["n_paths"] == tot_pp and whole["total_vertices"] == tot_v
+    assert whole["n_extensions"] == tot_e > 10 ** 10
+    assert (whole["hash_lo"], whole["hash_hi"]) == (h_lo, h_hi)
+    plan.close()
+
+
+@pytest.mark.parametrize("qcap,pool", [(16, 4), (200, 64), (4096, 2)])
+def test_overflow_retry_paths(monkeypatch, qcap, pool):
+    """The work queue and the record pool overflow and are retried bigger (test
+    hooks cap what a DFS phase may use); results stay bit-exact, including graphs
+    whose segment phase and prime-path phase both overflow."""
+    monkeypatch.setenv("TPGEN_TEST_QCAP", str(qcap))
+    monkeypatch.setenv("TPGEN_TEST_POOL", str(pool))
+    rounds = 0
+    for g in (gen.fig1b(), gen.config2(), gen.config4(K=40), gen.dense_scc(14, 3, 1), gen.k_seq_loops(4, 5)):
+        st = _assert_same(g)
+        rounds += st["n_count_rounds"]
+    assert rounds > 10  # the caps forced retries
