@@ -244,11 +244,14 @@ __device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t
 // ascending global id: in-SCC successors (local bits; ascending local id ==
 // ascending global id), the closing arc back to s, and out-of-SCC successors
 // (merged by their rank out_pos among the SCC members).  Returns the event.
+// A step that exhausts a node pops it and, unless the parent still has
+// out-of-SCC arcs to merge, moves on to the parent's next child in the same
+// step (a pop costs no step of its own).
 template <class T, bool TS>
 __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, const TabView<MT<T>::W, TS> &tab,
                                         Lane<T> &L, RecWriter &R, uint32_t mp, int &e_out, uint32_t &ext) {
     using O = MT<T>;
-    const int w = O::next(L.sin, L.M, L.sbit, L.k);
+    int w = O::next(L.sin, L.M, L.sbit, L.k);
     if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
         const int e = L.ooff + L.o;
         if (__ldg(G.out_pos + e) <= w) {
@@ -257,32 +260,41 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
             return out_event(L);
         }
     }
-    const bool has = w < O::BITS;
-    if (!has && L.l == L.r) {  // subtree of the unit's root exhausted
-        L.done = true;
-        return 0;
+    if (w >= O::BITS) {
+        if (L.l == L.r) {  // subtree of the unit's root exhausted
+            L.done = true;
+            return 0;
+        }
+        // pop
+        const int wold = L.u;
+        const int parent = lds_u8(mp + pidx(L.l - 1));
+        L.M = O::andnot(L.M, O::bit(wold));
+        L.l -= 1;
+        L.u = parent;
+        load_slot(tab, L, parent);
+        L.k = wold + 1;
+        L.base = min(L.base, L.l + 1);  // the record decoder's known prefix shortens
+        if (L.ocnt > 0) {  // rare: an exit vertex, whose out-of-SCC arcs merge with its children
+            L.o = count_out_le(G, L.ooff, L.ocnt, wold);
+            return 0;
+        }
+        w = O::next(L.sin, L.M, L.sbit, L.k);
+        if (w >= O::BITS) return 0;
     }
-    // push / cycle closure / pop share one predicated update (no divergent paths)
-    const bool clo = has && (w == L.s);  // cycle closure: always prime (Alg. 4 l.4-6)
-    const bool push = has && !clo;
-    const bool pop = !has;
-    const int wold = L.u;
-    const int parent = lds_u8(mp + pidx(L.l > 0 ? L.l - 1 : 0));
-    if (push) sts_u8(mp + pidx(L.l + 1), w);
-    const T bw = O::bit(push ? w : wold);
-    if (push) L.M = L.M | bw;
-    if (pop) L.M = O::andnot(L.M, bw);
-    L.k = push ? 0 : (has ? w + 1 : wold + 1);
-    L.l += push ? 1 : (pop ? -1 : 0);
-    L.u = push ? w : (pop ? parent : wold);
-    load_slot(tab, L, L.u);
-    if (pop && L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: exit vertices only
-    else if (push) L.o = 0;
-    // record stream: a pop below the decoder's known prefix shortens it
-    if (pop) L.base = min(L.base, L.l + 1);
-    if (L.emit && has) ext++;
-    if (clo) return L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
-    return push ? node_event(L, w) : 0;
+    if (L.emit) ext++;
+    if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
+        L.k = w + 1;
+        return L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
+    }
+    // push
+    sts_u8(mp + pidx(L.l + 1), w);
+    L.M = L.M | O::bit(w);
+    L.k = 0;
+    L.l += 1;
+    L.u = w;
+    load_slot(tab, L, w);
+    L.o = 0;
+    return node_event(L, w);
 }
 
 template <class T>
