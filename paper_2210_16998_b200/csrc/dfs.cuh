@@ -114,6 +114,7 @@ enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAI
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
 constexpr int kStepsPerIter = 8; // DFS steps per pass of the persistent loop
+constexpr int kEagerGens = 4;    // donation generations that split without waiting split_min steps
 
 // Event codes inside the DFS: type in bits 0-2, closure flag bit 3, path length in bits 8+.
 constexpr int EV_CLO = 8;
@@ -470,8 +471,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     __shared__ unsigned long long s_td, s_head;  // warp 0's latest queue snapshot
     __shared__ unsigned s_ov;
     if (threadIdx.x == 0) {
-        s_td = 0xffffffffull << 32;  // "work pending, no backlog need" until warp 0's first snapshot
-        s_head = 0;
+        s_td = 1ull << 32;  // until warp 0's first snapshot: work pending (tail 1, done 0) and lanes
+        s_head = 1ull << 20;  // waiting for it (backlog negative), so the first units split at once
         s_ov = 0;
     }
     __syncthreads();
@@ -698,7 +699,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         }
 
         // ---------------- donate on demand (feed: set by this iteration's queue snapshot)
-        if (feed && L.active && !L.done && L.steps - last_split >= A.split_min) {
+        // (the first generations split at once: the walk starts from one unit per start
+        // vertex and every lane of the GPU needs work)
+        if (feed && L.active && !L.done && (L.steps - last_split >= A.split_min || ugen < kEagerGens)) {
             // backlog of queued, unclaimed units below the low-water mark: donate the shallowest siblings
             int j0 = -1;
             const int m = lane_donate<T, TS, false>(G, tab, L, mp, uscc, j0, nullptr);
