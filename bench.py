@@ -308,7 +308,7 @@ def main():
         dfs_ach = ext / (ms_dfs * 1e-3) / 1e9
         traffic = ncu_traffic()
         roofline = {
-            "bound": "alu", "kernel": "dfs_kernel<uint32_t,TS=1>",
+            "bound": "alu", "kernel": "dfs_kernel<unsigned int,TS=1>",
             "achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak,
             "traffic": traffic.get("dfs_kernel", {}).get("dram_bytes_per_launch"),
             "ms_per_launch": ms_dfs, "units_per_launch": ext,
@@ -316,10 +316,12 @@ def main():
                           "(SURVEY 8(d)); DESIGN.md Rooflines",
             "share_of_step": ms_dfs / ms_dev,
             "second": {
-                "bound": "hbm", "kernel": "expand_kernel<1,1>",
+                "bound": "hbm", "kernel": (f"expand_fast_kernel<{max(1, (int(st['max_scc']) + 3) // 4)},false>"
+                                           if int(st["max_scc"]) <= 63 else "expand_kernel"),
                 "achieved": o_bytes / (ms_expand * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": o_bytes / (ms_expand * 1e-3) / 1e9 / peak,
-                "traffic": traffic.get("expand_kernel", {}).get("dram_bytes_per_launch"),
+                "traffic": traffic.get("expand_fast_kernel" if int(st["max_scc"]) <= 63 else "expand_kernel",
+                                       {}).get("dram_bytes_per_launch"),
                 "algorithmic_bytes_per_launch": o_bytes, "ms_per_launch": ms_expand,
                 "share_of_step": ms_expand / ms_dev,
                 "model": "4 B per output vertex + 8 B per offset (written once)"},

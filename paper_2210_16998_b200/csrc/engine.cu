@@ -524,6 +524,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         A.chunk_next = qc + 48;
         A.chunk_cap = plim;  // (the sink chunk is chunk plim: inside the allocation)
         A.split_min = P.split_min;
+        if (const char *ev = getenv("TPGEN_SPLIT_MIN")) A.split_min = (uint32_t)atoi(ev);  // tuning knob
         A.dbg = nullptr;
         if (getenv("TPGEN_DEBUG")) {
             TPG_TRY(P.dbgbuf.ensure(160 * 8, s));
