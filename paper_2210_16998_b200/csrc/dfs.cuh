@@ -42,9 +42,9 @@ struct MT<uint32_t> {
     static __device__ __forceinline__ uint32_t andnot(uint32_t a, uint32_t b) { return a & ~b; }
     // lowest set bit >= k of (sin & (~M | sbit)), BITS if none
     static __device__ __forceinline__ int next(uint32_t sin, uint32_t M, uint32_t sbit, int k) {
-        uint32_t c = sin & (~M | sbit);
-        c = (k < 32) ? (c & (0xffffffffu << k)) : 0u;
-        return c ? (__ffs((int)c) - 1) : 32;
+        // k <= 32; the 64-bit shift clears everything for k = 32; ctz(0) = 32 = none
+        const uint32_t c = sin & (~M | sbit) & (uint32_t)(0xffffffffull << k);
+        return __clz(__brev(c));
     }
     static __device__ __forceinline__ uint32_t load(const uint64_t *w) { return (uint32_t)__ldg(w); }
     static __device__ __forceinline__ uint32_t from(const uint64_t *w) { return (uint32_t)w[0]; }
@@ -60,9 +60,8 @@ struct MT<uint64_t> {
     static __device__ __forceinline__ bool subset(uint64_t a, uint64_t b) { return (a & ~b) == 0ull; }
     static __device__ __forceinline__ uint64_t andnot(uint64_t a, uint64_t b) { return a & ~b; }
     static __device__ __forceinline__ int next(uint64_t sin, uint64_t M, uint64_t sbit, int k) {
-        uint64_t c = sin & (~M | sbit);
-        c = (k < 64) ? (c & (~0ull << k)) : 0ull;
-        return c ? (__ffsll((long long)c) - 1) : 64;
+        const uint64_t c = sin & (~M | sbit) & ((k < 64) ? (~0ull << k) : 0ull);
+        return __clzll(__brevll(c));  // 64 = none
     }
     static __device__ __forceinline__ uint64_t load(const uint64_t *w) { return __ldg(w); }
     static __device__ __forceinline__ uint64_t from(const uint64_t *w) { return w[0]; }
@@ -136,16 +135,16 @@ __device__ __forceinline__ void sts_u8(uint32_t a, int v) {
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-// n <= 5 consecutive path bytes starting at position p (shared-memory layout of pidx):
-// two 32-bit words of the lane's column, funnel-shifted.
-template <int W>
-__device__ __forceinline__ uint64_t path_bytes(uint32_t mp, int p, int n) {
-    const int q = p >> 2;
-    uint32_t lo, hi = 0u;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(mp + (q << 7)) : "memory");
-    if (q + 1 < 16 * W) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(mp + ((q + 1) << 7)) : "memory");
-    const uint64_t v = (((uint64_t)hi << 32) | lo) >> (8 * (p & 3));
-    return v & ((1ull << (8 * n)) - 1ull);
+// Up to 5 consecutive path bytes starting at position p (shared-memory layout of
+// pidx): two 32-bit words of the lane's column, funnel-shifted.  Bytes past the
+// record's count are left in place (decoders read only the first n); the word
+// after the last level is a spare row of the path array.
+__device__ __forceinline__ uint64_t path_bytes(uint32_t mp, int p) {
+    const uint32_t a = mp + ((p >> 2) << 7);
+    uint32_t lo, hi;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(a) : "memory");
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(a + 128) : "memory");
+    return (((uint64_t)hi << 32) | lo) >> (8 * (p & 3));
 }
 
 template <class T>
@@ -192,13 +191,11 @@ __device__ __forceinline__ void load_slot(const TabView<MT<T>::W, TS> &tab, Lane
 template <class T>
 __device__ __forceinline__ int node_event(const Lane<T> &L, int w) {
     using O = MT<T>;
-    if (L.flags & F_EXIT) return 0;
     const int len = (L.l + 1) << 8;
-    if (L.seg) return O::subset(L.sin, L.M) ? (EV_TAIL | len) : 0;
-    if (!L.emit) return 0;
-    T inner_h = L.M;
-    O::clr(inner_h, w);
-    return (O::subset(L.sin, O::andnot(L.M, L.sbit)) && O::subset(L.ps, inner_h)) ? (EV_PP | len) : 0;
+    const bool tail = O::subset(L.sin, L.M);
+    const bool pp = O::subset(L.sin, O::andnot(L.M, L.sbit)) && O::subset(L.ps, O::andnot(L.M, O::bit(w)));
+    const int ev = L.seg ? (tail ? (EV_TAIL | len) : 0) : ((L.emit && pp) ? (EV_PP | len) : 0);
+    return (L.flags & F_EXIT) ? 0 : ev;
 }
 
 // Arc to an out-of-SCC successor from the current node.
@@ -219,7 +216,7 @@ struct RecWriter {
     uint64_t *cur;   // current chunk
     int fill;        // records used in it (kChunkRecs - 1: full, the next record needs a new chunk)
     long long next;  // chunk reserved for when this one fills (-1: none)
-    int64_t count;   // records of the current unit
+    int count;       // records of the current unit
 };
 
 __device__ __forceinline__ void rec_switch(const DfsArgs &A, RecWriter &R) {
@@ -234,9 +231,13 @@ __device__ __forceinline__ void rec_switch(const DfsArgs &A, RecWriter &R) {
     R.fill = 0;
 }
 
-__device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t rec) {
+__device__ __forceinline__ void rec_edge(const DfsArgs &A, RecWriter &R) {
     if (R.fill == kChunkRecs - 1) rec_switch(A, R);
-    else if (R.fill == kChunkRecs / 2 && R.next < 0) R.next = (long long)atomicAdd(A.chunk_next, 1ull);
+    else if (R.next < 0) R.next = (long long)atomicAdd(A.chunk_next, 1ull);
+}
+__device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t rec) {
+    // (fill == 32: reserve the next chunk; fill == 63: switch to it)
+    if (R.fill == kChunkRecs - 1 || R.fill == kChunkRecs / 2) rec_edge(A, R);
     R.cur[R.fill++] = rec;
     R.count++;
 }
@@ -416,10 +417,11 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     using O = MT<T>;
     constexpr int W = O::W;
     constexpr int WARPS = DfsTraits<T>::warps;
-    __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32];
+    __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32 + 128];  // + a spare row (path_bytes)
     extern __shared__ __align__(16) uint8_t stab[];  // slot table copy (TS)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t mp = (uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32) + lane * 4;
+    uint32_t mp;  // this lane's column of the shared path array (opaque: not recomputed in the loop)
+    asm volatile("mov.b32 %0, %1;" : "=r"(mp) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32) + lane * 4));
     const DevGraph &G = A.G;
     TabView<W, TS> tab;
     if (TS) {
@@ -662,12 +664,12 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 int nb = L.l + 1 - L.base;
                 while (nb > kRecBytes) {  // continuation records
                     rec_put(A, R, (uint64_t)R_PATH | ((uint64_t)L.base << 4) | ((uint64_t)kRecBytes << 13) |
-                                      (path_bytes<MT<T>::W>(mp, L.base, kRecBytes) << 16));
+                                      (path_bytes(mp, L.base) << 16));
                     L.base += kRecBytes;
                     nb -= kRecBytes;
                 }
                 rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)nb << 13) |
-                                  (path_bytes<MT<T>::W>(mp, L.base, nb) << 16));
+                                  (path_bytes(mp, L.base) << 16));
                 L.base = L.l + 1;
                 if (ty == EV_PP) {
                     c_pp += 1;
