@@ -262,12 +262,10 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
             return out_event(L);
         }
     }
-    if (w >= O::BITS) {
-        if (L.l == L.r) {  // subtree of the unit's root exhausted
-            L.done = true;
-            return 0;
-        }
-        // pop
+    // straight-line, predicated: [pop] then [closure | push]
+    const bool none = w >= O::BITS;
+    const bool fin = none && L.l == L.r;  // subtree of the unit's root exhausted
+    if (none && !fin) {  // pop, then the parent's next child (unless the parent merges out-arcs)
         const int wold = L.u;
         const int parent = lds_u8(mp + pidx(L.l - 1));
         L.M = O::andnot(L.M, O::bit(wold));
@@ -276,27 +274,27 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
         load_slot(tab, L, parent);
         L.k = wold + 1;
         L.base = min(L.base, L.l + 1);  // the record decoder's known prefix shortens
-        if (L.ocnt > 0) {  // rare: an exit vertex, whose out-of-SCC arcs merge with its children
-            L.o = count_out_le(G, L.ooff, L.ocnt, wold);
-            return 0;
-        }
-        w = O::next(L.sin, L.M, L.sbit, L.k);
-        if (w >= O::BITS) return 0;
+        if (L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: an exit vertex
+        w = (L.ocnt > 0) ? O::BITS : O::next(L.sin, L.M, L.sbit, L.k);
     }
-    if (L.emit) ext++;
-    if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
-        L.k = w + 1;
-        return L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
+    if (fin) L.done = true;
+    const bool go = !fin && w < O::BITS;
+    const bool clo = go && w == L.s;  // cycle closure: always prime (Alg. 4 l.4-6)
+    const bool push = go && !clo;
+    if (go && L.emit) ext++;
+    int ev = (clo && L.emit) ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
+    if (clo) L.k = w + 1;
+    if (push) {
+        sts_u8(mp + pidx(L.l + 1), w);
+        L.M = L.M | O::bit(w);
+        L.k = 0;
+        L.l += 1;
+        L.u = w;
+        load_slot(tab, L, w);
+        L.o = 0;
+        ev = node_event(L, w);
     }
-    // push
-    sts_u8(mp + pidx(L.l + 1), w);
-    L.M = L.M | O::bit(w);
-    L.k = 0;
-    L.l += 1;
-    L.u = w;
-    load_slot(tab, L, w);
-    L.o = 0;
-    return node_event(L, w);
+    return ev;
 }
 
 template <class T>
