@@ -159,11 +159,36 @@ struct Lane {
 };
 
 // View of the slot table: staged in shared memory (TS) when it fits, else read through L1.
+// The shared copy is addressed through a 32-bit shared-window base kept in a register.
+template <class T, bool TS>
+struct ShTab {  // generic fallback (masks of several words): through the generic pointer
+    static __device__ __forceinline__ T sin(const void *p, uint32_t, int i) {
+        return MT<T>::from(reinterpret_cast<const Slot<MT<T>::W> *>(p)[i].sin);
+    }
+};
+template <>
+struct ShTab<uint32_t, true> {
+    static __device__ __forceinline__ uint32_t sin(const void *, uint32_t sb, int i) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sb + (uint32_t)i * 32u) : "memory");
+        return v;
+    }
+};
+template <>
+struct ShTab<uint64_t, true> {
+    static __device__ __forceinline__ uint64_t sin(const void *, uint32_t sb, int i) {
+        uint64_t v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sb + (uint32_t)i * 32u) : "memory");
+        return v;
+    }
+};
 template <int W, bool TS>
 struct TabView {
     const Slot<W> *p;
+    uint32_t sb;  // TS: shared-window address of the table
     template <class T>
     __device__ __forceinline__ T sin(int i) const {
+        if (TS && W == 1) return ShTab<T, true>::sin(p, sb, i);
         return TS ? MT<T>::from(p[i].sin) : MT<T>::load(p[i].sin);
     }
     template <class T>
@@ -171,6 +196,14 @@ struct TabView {
         return TS ? MT<T>::from(p[i].pin) : MT<T>::load(p[i].pin);
     }
     __device__ __forceinline__ int4 meta(int i) const {
+        if (TS && W == 1) {
+            int4 v;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(sb + (uint32_t)i * 32u + 16u)
+                         : "memory");
+            return v;
+        }
         return TS ? *reinterpret_cast<const int4 *>(&p[i].gid) : ld_meta(p + i);
     }
 };
@@ -428,8 +461,10 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         for (int i = threadIdx.x; i < A.n_slots * (int)(sizeof(Slot<W>) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
         __syncthreads();
         tab.p = reinterpret_cast<const Slot<W> *>(stab);
+        asm volatile("mov.b32 %0, %1;" : "=r"(tab.sb) : "r"((uint32_t)__cvta_generic_to_shared(stab)));
     } else {
         tab.p = reinterpret_cast<const Slot<W> *>(G.slots);
+        tab.sb = 0;
     }
     Unit<W> *units = reinterpret_cast<Unit<W> *>(A.units);
 
