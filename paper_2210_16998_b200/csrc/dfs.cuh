@@ -112,7 +112,7 @@ struct MT<Mask<WW>> {
 enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAIL, R_TRANSIT = EV_TRANSIT, R_ARG = 6 };
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
-constexpr int kStepsPerIter = 8; // DFS steps per pass of the persistent loop
+constexpr int kStepsPerIter = 16;// DFS steps per pass of the persistent loop
 constexpr int kEagerGens = 4;    // donation generations that split without waiting split_min steps
 
 // Event codes inside the DFS: type in bits 0-2, closure flag bit 3, path length in bits 8+.
