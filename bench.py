@@ -1,18 +1,22 @@
 #!/usr/bin/env python
 """Benchmark of the TPGen hot path on B200 (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs): at N=1 the largest single-GPU configuration,
-config 3 -- one dense SCC of 22 vertices, exact out-degree 4 (seed 1):
-E_canon = 2.34e8 path extensions, 6.0e7 prime paths, 1.1e9 output vertices.
-For N > 1 the job is weak-scaled: N disjoint copies of that SCC, rank r owns
-the start vertices of copy r (no data-path collective; counts and times are
-reduced over NCCL at the end).
+Default workload (BASELINE.json configs): config 3 -- one dense SCC of 22
+vertices, exact out-degree 4 (seed 1): E_canon = 2.34e8 path extensions,
+6.0e7 prime paths, 1.1e9 output vertices (4.9 GB).  For N > 1 the job is
+weak-scaled: N disjoint copies of that SCC, rank r owns the start vertices of
+copy r (no data-path collective; counts and times are reduced over NCCL).
 
-A "step" is one full tpgen_plan_prime_paths call: count rounds + completion DP
-+ scan + DFS write pass + stitching, output materialised in HBM (canonical
-offsets + vertices).  `value` = prime paths / s over all ranks (device time,
-CUDA events, max over ranks); `e2e` = the same through tpgen_prime_paths with
-the CSR in host memory and the result copied into pinned host memory.
+A "step" is one full tpgen_plan_prime_paths call: DFS enumeration (segment and
+prime-path phases), linearization of the unit forest, canonical writer,
+cross-SCC stitching, output materialised in HBM (canonical offsets +
+vertices).  `value` = prime paths / s over all ranks (device time, CUDA events,
+max over ranks); `e2e` = the same through tpgen_prime_paths with the CSR in
+host memory and the result copied into pinned host memory.
+
+--workload config5: 16 parallel 56-vertex SCCs (~1.3e10 extensions) in
+COUNT_HASH mode (counts + digest; the ~200 GB output is not materialized),
+strong-scaled by start-vertex shards.
 
 --impl reference runs the CPU oracle (oracle/, single core) on a bounded
 sample of the same workload.
@@ -210,6 +214,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="config3", choices=["config3", "config5"],
+                    help="config3 (default, the headline): dense 22-vertex SCC, full output, weak scaling over "
+                         "disjoint copies; config5: 16 parallel 56-vertex SCCs (~1.3e10 extensions), COUNT_HASH "
+                         "(counts + digest; the ~200 GB output is not materialized), strong scaling by "
+                         "start-vertex shards")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -227,8 +236,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
-    g, ranges = workload(world)
-    rng = ranges[rank]
+    c5 = args.workload == "config5"
+    if c5:  # one graph; rank r takes start-vertex shard r of `world` (strong scaling)
+        g = gen.config5()
+        kw = dict(shard=(rank, world), mode="count", digest=True)
+    else:
+        g, ranges = workload(world)
+        kw = dict(start_range=ranges[rank])
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -240,7 +254,7 @@ def main():
 
     # ---------------- device-resident timing (value)
     for _ in range(args.warmup):
-        ps = plan.prime_paths(start_range=rng)
+        ps = plan.prime_paths(**kw)
         del ps
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -251,7 +265,7 @@ def main():
         for k in range(args.steps):
             flush.fill_(k & 0xff)  # L2 flush between timed steps (outside the events)
             ev[k][0].record(stream)
-            ps = plan.prime_paths(start_range=rng)
+            ps = plan.prime_paths(**kw)
             ev[k][1].record(stream)
             stats.append(ps.stats)
             del ps
@@ -266,7 +280,26 @@ def main():
 
     # ---------------- end-to-end through the public C ABI (host CSR in, pinned host result out)
     e2e = None
-    if not args.no_e2e:
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    mem_used_gb = (total_b - free_b) / 1e9  # device memory held after the timed steps (pools included)
+    if not args.no_e2e and c5:  # counts + digest come back in the stats; the CSR goes up every call
+        plan.close()  # its workspaces return to the device pool, where the e2e call's plan finds them
+        h2d = int(g.offsets.nbytes + g.targets.nbytes)
+        e2e_steps = max(1, min(args.steps, 3))
+        del_ = tp.prime_paths(g, device=dev, **kw)
+        del del_
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ps = tp.prime_paths(g, device=dev, **kw)
+            del ps
+        torch.cuda.synchronize()
+        e2e = {"value": None, "unit": "PP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 0,
+               "ms_per_step": 1e3 * (time.perf_counter() - t0) / e2e_steps, "steps": e2e_steps,
+               "note": "COUNT_HASH: counts and the digest are returned in the stats struct"}
+    elif not args.no_e2e:
+        rng = kw["start_range"]
         host_out = torch.empty(8 * (n_pp + 1) + 4 * n_vert, dtype=torch.uint8, pin_memory=True)
         h2d = int(g.offsets.nbytes + g.targets.nbytes)
         d2h = 8 * (n_pp + 1) + 4 * n_vert
@@ -307,8 +340,10 @@ def main():
         alu_peak = ALU_LANES * sm_max * 1e6 / OPS_PER_EXT / 1e9  # Gext/s
         dfs_ach = ext / (ms_dfs * 1e-3) / 1e9
         traffic = ncu_traffic()
+        if c5:  # count mode writes no output: only the extension part of SURVEY 8(d)'s bytes applies
+            a_bytes = 2.0 * 13.0 * ext
         roofline = {
-            "bound": "alu", "kernel": "dfs_kernel<unsigned int,TS=1>",
+            "bound": "alu", "kernel": ("dfs_kernel<unsigned long,TS=1>" if c5 else "dfs_kernel<unsigned int,TS=1>"),
             "achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak,
             "traffic": traffic.get("dfs_kernel", {}).get("dram_bytes_per_launch"),
             "ms_per_launch": ms_dfs, "units_per_launch": ext,
@@ -332,6 +367,12 @@ def main():
             "peak_kind": peak_kind,
             "traffic_source": traffic.get("source"),
         }
+        if c5:
+            roofline["traffic"] = None  # the committed ncu summary is for config 3
+            roofline["second"] = {"note": "COUNT_HASH: the writer digests each path instead of storing it",
+                                  "kernel": f"expand_fast_kernel<{max(1, (int(st['max_scc']) + 3) // 4)},true>",
+                                  "ms_per_launch": ms_expand, "share_of_step": ms_expand / ms_dev}
+            roofline["path_hbm"]["model"] = "SURVEY 8(d): 26 B/extension (no output in COUNT_HASH mode)"
         out = {
             "metric": "prime_paths_per_sec",
             "value": value,
@@ -341,12 +382,14 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if c5 else "weak",
             "vs_baseline": None,
             "dtype": "int32",
             "data": "synthetic",
-            "config": {"workload": "config3: dense SCC n=22 out-degree 4 seed 1" +
-                       (f" x{world} disjoint copies, one per rank" if world > 1 else ""),
+            "config": {"workload": ("config5: 16 parallel SCCs n=56 out-degree 2 seed 5, COUNT_HASH (counts + "
+                                    "digest, output not materialized)" if c5 else
+                                    "config3: dense SCC n=22 out-degree 4 seed 1" +
+                                    (f" x{world} disjoint copies, one per rank" if world > 1 else "")),
                        "n_vertices": g.n, "prime_paths_per_rank": n_pp, "output_vertices_per_rank": n_vert,
                        "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",
                        "parallelism": f"start-vertex shards x{world}"},
@@ -359,6 +402,7 @@ def main():
                                                            for s in stats])),
                              "expand_kernel": ms_expand,
                              "stitch": float(np.mean([s["ms_stitch"] for s in stats])), "device": ms_dev},
+            "device_mem_used_gb": mem_used_gb,
             "count_rounds": st["n_count_rounds"],
             "n_units": st["n_units"],
             "gpu_launches": launches,

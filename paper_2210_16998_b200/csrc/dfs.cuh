@@ -108,7 +108,7 @@ struct MT<Mask<WW>> {
 //   bits 0-2 type, bit 3 closure flag, bits 4-12 c (truncate the path to c
 //   vertices), bits 13-15 n (number of appended vertices, <= 5),
 //   bits 16-55 the n appended local vertex ids (one byte each).
-// R_ARG carries the out-arc index of the HEAD / TRANSIT record that follows it, in bits 32-63.
+// R_ARG carries the out-arc index of the HEAD / TRANSIT record directly after it, in bits 32-63.
 enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAIL, R_TRANSIT = EV_TRANSIT, R_ARG = 6 };
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
@@ -691,8 +691,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             if (ev) {
                 const int ty = ev_type(ev);
                 const uint64_t len = (uint64_t)ev_len(ev);
-                // HEAD / TRANSIT carry their out-arc in an R_ARG record written just before them
-                if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
                 // the bytes path[base..l] the decoder lacks, <= kRecBytes per record
                 int nb = L.l + 1 - L.base;
                 while (nb > kRecBytes) {  // continuation records
@@ -701,6 +699,8 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     L.base += kRecBytes;
                     nb -= kRecBytes;
                 }
+                // HEAD / TRANSIT carry their out-arc in an R_ARG record written directly before them
+                if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
                 rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)nb << 13) |
                                   (path_bytes(mp, L.base) << 16));
                 L.base = L.l + 1;

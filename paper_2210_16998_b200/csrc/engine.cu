@@ -43,6 +43,23 @@ static double now_ms() {
 }
 
 // ------------------------------------------------------------ buffers
+static void out_cache_clear(int dev);
+
+// Stream-ordered allocation from the device pool; on failure the cached output
+// blocks and the pool's idle memory are released and the allocation retried once.
+static cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t s) {
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaStreamSynchronize(s);
+    out_cache_clear(dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    return cudaMallocAsync(p, bytes, s);
+}
+
 tpgen_status DevBuf::ensure(size_t bytes, cudaStream_t s) {
     if (bytes <= cap) return TPGEN_OK;
     // 25 % headroom: per-call sizes (units, records) vary with the dynamic donation pattern,
@@ -52,7 +69,7 @@ tpgen_status DevBuf::ensure(size_t bytes, cudaStream_t s) {
     if (p) TPG_CK(cudaFreeAsync(p, s));
     p = nullptr;
     cap = 0;
-    TPG_CK(cudaMallocAsync(&p, nc, s));
+    TPG_CK(pool_alloc(&p, nc, s));
     cap = nc;
     return TPGEN_OK;
 }
@@ -234,7 +251,7 @@ static bool out_cache_put(int dev, void *p, size_t bytes) {
 }
 
 static void out_cache_clear(int dev) {
-    if (dev < 0 || dev >= 64) return;
+    if (dev < 0 || dev >= 64) return;  // (forward-declared above)
     OutCache &C = g_outcache[dev];
     std::lock_guard<std::mutex> lk(C.mu);
     for (auto &b : C.blocks) cudaFree(b.first);
@@ -258,12 +275,7 @@ static tpgen_status out_alloc_pair(const tpgen_options &o, OutOwner *ow, size_t 
     size_t got = bytes;
     void *p = out_cache_get(ow->device, bytes, &got);
     if (!p) {
-        cudaError_t e = cudaMallocAsync(&p, bytes, s);
-        if (e != cudaSuccess) {  // release the cached blocks and try once more
-            cudaGetLastError();
-            out_cache_clear(ow->device);
-            TPG_CK(cudaMallocAsync(&p, bytes, s));
-        }
+        TPG_CK(pool_alloc(&p, bytes, s));
     }
     ow->kind = 0;
     ow->stream = (void *)s;
@@ -287,7 +299,7 @@ static tpgen_status out_alloc_device(const tpgen_options &o, OutOwner *ow, size_
         ow->ctx = o.alloc_ctx;
         ow->stream = o.stream;
     } else {
-        TPG_CK(cudaMallocAsync(p, bytes, s));
+        TPG_CK(pool_alloc(p, bytes, s));
         ow->kind = 0;
         ow->stream = (void *)s;
     }
@@ -398,7 +410,7 @@ static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
     if (need <= P.chunk_cap) return TPGEN_OK;
     uint64_t cap = std::max<uint64_t>(need, P.chunk_cap * 2);
     void *np = nullptr;
-    TPG_CK(cudaMallocAsync(&np, (cap + 1) * kChunkRecs * 8, s));  // + the overflow sink chunk
+    TPG_CK(pool_alloc(&np, (cap + 1) * kChunkRecs * 8, s));  // + the overflow sink chunk
     if (P.chunk_used && P.chunks.p)
         TPG_CK(cudaMemcpyAsync(np, P.chunks.p, P.chunk_used * kChunkRecs * 8, cudaMemcpyDeviceToDevice, s));
     if (P.chunks.p) TPG_CK(cudaFreeAsync(P.chunks.p, s));
@@ -412,7 +424,7 @@ static tpgen_status grow_pool(PlanImpl &P, uint64_t need, cudaStream_t s) {
 static tpgen_status grow_keep(DevBuf &b, size_t used, size_t cap, size_t es, cudaStream_t s) {
     if (cap * es <= b.cap) return TPGEN_OK;
     void *np = nullptr;
-    TPG_CK(cudaMallocAsync(&np, cap * es, s));
+    TPG_CK(pool_alloc(&np, cap * es, s));
     if (used && b.p) TPG_CK(cudaMemcpyAsync(np, b.p, used * es, cudaMemcpyDeviceToDevice, s));
     if (b.p) TPG_CK(cudaFreeAsync(b.p, s));
     b.p = np;
@@ -602,29 +614,31 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
 // Canonical writer launch: the lane-parallel kernel when every SCC has at most
 // kFastMaxScc vertices (one mask word), else the sequential replay.  HASH: digest only.
 template <int NPW, bool HASH>
-static void launch_fast(const ExpandArgs &E, int64_t nu, int num_sms, cudaStream_t s) {
+static void launch_fast(const ExpandArgs &E, int64_t nu, int num_sms, bool mixed, cudaStream_t s) {
     constexpr int th = FastCfg<NPW>::threads;
-    expand_fast_kernel<NPW, HASH><<<grid_for(nu * 32, th, num_sms * 2048 / th), th, 0, s>>>(E);
+    const int g = grid_for(nu * 32, th, num_sms * 2048 / th);
+    if (mixed) expand_fast_kernel<NPW, HASH, true><<<g, th, 0, s>>>(E);
+    else expand_fast_kernel<NPW, HASH, false><<<g, th, 0, s>>>(E);
 }
 template <bool HASH>
-static void launch_fast_npw(int npw, const ExpandArgs &E, int64_t nu, int num_sms, cudaStream_t s) {
+static void launch_fast_npw(int npw, const ExpandArgs &E, int64_t nu, int num_sms, bool mixed, cudaStream_t s) {
     switch (npw) {
-        case 1: launch_fast<1, HASH>(E, nu, num_sms, s); break;
-        case 2: launch_fast<2, HASH>(E, nu, num_sms, s); break;
-        case 3: launch_fast<3, HASH>(E, nu, num_sms, s); break;
-        case 4: launch_fast<4, HASH>(E, nu, num_sms, s); break;
-        case 5: launch_fast<5, HASH>(E, nu, num_sms, s); break;
-        case 6: launch_fast<6, HASH>(E, nu, num_sms, s); break;
-        case 7: launch_fast<7, HASH>(E, nu, num_sms, s); break;
-        case 8: launch_fast<8, HASH>(E, nu, num_sms, s); break;
-        case 9: launch_fast<9, HASH>(E, nu, num_sms, s); break;
-        case 10: launch_fast<10, HASH>(E, nu, num_sms, s); break;
-        case 11: launch_fast<11, HASH>(E, nu, num_sms, s); break;
-        case 12: launch_fast<12, HASH>(E, nu, num_sms, s); break;
-        case 13: launch_fast<13, HASH>(E, nu, num_sms, s); break;
-        case 14: launch_fast<14, HASH>(E, nu, num_sms, s); break;
-        case 15: launch_fast<15, HASH>(E, nu, num_sms, s); break;
-        default: launch_fast<16, HASH>(E, nu, num_sms, s); break;
+        case 1: launch_fast<1, HASH>(E, nu, num_sms, mixed, s); break;
+        case 2: launch_fast<2, HASH>(E, nu, num_sms, mixed, s); break;
+        case 3: launch_fast<3, HASH>(E, nu, num_sms, mixed, s); break;
+        case 4: launch_fast<4, HASH>(E, nu, num_sms, mixed, s); break;
+        case 5: launch_fast<5, HASH>(E, nu, num_sms, mixed, s); break;
+        case 6: launch_fast<6, HASH>(E, nu, num_sms, mixed, s); break;
+        case 7: launch_fast<7, HASH>(E, nu, num_sms, mixed, s); break;
+        case 8: launch_fast<8, HASH>(E, nu, num_sms, mixed, s); break;
+        case 9: launch_fast<9, HASH>(E, nu, num_sms, mixed, s); break;
+        case 10: launch_fast<10, HASH>(E, nu, num_sms, mixed, s); break;
+        case 11: launch_fast<11, HASH>(E, nu, num_sms, mixed, s); break;
+        case 12: launch_fast<12, HASH>(E, nu, num_sms, mixed, s); break;
+        case 13: launch_fast<13, HASH>(E, nu, num_sms, mixed, s); break;
+        case 14: launch_fast<14, HASH>(E, nu, num_sms, mixed, s); break;
+        case 15: launch_fast<15, HASH>(E, nu, num_sms, mixed, s); break;
+        default: launch_fast<16, HASH>(E, nu, num_sms, mixed, s); break;
     }
 }
 template <int W, bool HASH>
@@ -635,12 +649,13 @@ static void launch_seq(int np, const ExpandArgs &E, int64_t nu, int num_sms, cud
     else expand_kernel<W, 2 * W + 1, HASH><<<eg, kExpandThreads, 0, s>>>(E);
 }
 template <int W>
-static void launch_expand(const HostPlan &H, const ExpandArgs &E, int64_t nu, int num_sms, bool hash, cudaStream_t s) {
+static void launch_expand(const HostPlan &H, const ExpandArgs &E, int64_t nu, int num_sms, bool hash, bool mixed,
+                          cudaStream_t s) {
     const int np = (H.max_scc + 1 + 31) / 32;  // registers per lane for the longest emitted path
     const int npw = std::max(1, (H.max_scc + 3) / 4);  // 32-bit words of local ids for the longest path
     if (W == 1 && H.max_scc <= kFastMaxScc && !getenv("TPGEN_SLOW_EXPAND")) {
-        if (hash) launch_fast_npw<true>(npw, E, nu, num_sms, s);
-        else launch_fast_npw<false>(npw, E, nu, num_sms, s);
+        if (hash) launch_fast_npw<true>(npw, E, nu, num_sms, mixed, s);
+        else launch_fast_npw<false>(npw, E, nu, num_sms, mixed, s);
     } else {
         if (hash) launch_seq<W, true>(np, E, nu, num_sms, s);
         else launch_seq<W, false>(np, E, nu, num_sms, s);
@@ -895,7 +910,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     E.hash_acc = hacc;
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        launch_expand<W>(H, E, nu, P.num_sms, hash_only, s);
+        launch_expand<W>(H, E, nu, P.num_sms, hash_only, n_items > 0 || n_heads > 0, s);
         launches++;
     }
     cudaEventRecord(tw.b, s);

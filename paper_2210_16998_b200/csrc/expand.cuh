@@ -15,7 +15,8 @@
 //  shared-memory stage at offsets from a warp scan of their lengths, and the
 //  warp streams the stage to HBM with coalesced stores.  Batches that contain
 //  other record kinds (segment items, head blocks; they occur only at SCC exits)
-//  fall back to the sequential replay below.
+//  are emitted lane-parallel too: warp scans of the cursor increments give each
+//  lane the offsets of its own record, which it writes directly.
 //
 //  expand_kernel<W, NP> (any SCC size): sequential replay, the current path
 //  distributed over the lanes' registers (lane q holds positions q, q+32, ...);
@@ -246,7 +247,9 @@ __device__ __forceinline__ uint32_t lop_merge(uint32_t mine, uint32_t other, uin
     return (mine & mask) | (other & ~mask);  // one LOP3
 }
 
-template <int NPW, bool HASH>
+// MIXED = false: the call has no segment items and no head blocks (e.g. a graph
+// that is one SCC), so every batch is prime paths and path continuations only.
+template <int NPW, bool HASH, bool MIXED>
 __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(ExpandArgs A) {
     constexpr int kWarps = FastCfg<NPW>::threads / 32;
     constexpr int kStage = HASH ? 1 : 32 * FastCfg<NPW>::max_out;  // one batch of paths
@@ -288,40 +291,40 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
             const uint64_t myrec = fetch32(A, rd, nb, lane);  // lanes >= nb: 0 = an empty R_PATH
             const int ty = (int)(myrec & 7);
-            if (__all_sync(kFull, ty == R_PP || ty == R_PATH)) {
-                // ---- this lane's bytes: positions cc .. cc+n-1 of the path
-                const int cc = (int)((myrec >> 4) & 0x1ff);
-                const int n = (int)((myrec >> 13) & 7);
-                const int sh = 8 * (cc & 3);
-                const uint64_t nm = (1ull << (8 * n)) - 1ull;
-                const uint64_t pay = ((myrec >> 16) & nm) << sh;
-                const uint64_t pm = nm << sh;
-                const int w0 = cc >> 2;
-                uint32_t D[NPW], M[NPW];
+            // ---- this lane's bytes: positions cc .. cc+n-1 of the path
+            const int cc = (int)((myrec >> 4) & 0x1ff);
+            const int n = (int)((myrec >> 13) & 7);
+            const int sh = 8 * (cc & 3);
+            const uint64_t nm = (1ull << (8 * n)) - 1ull;
+            const uint64_t pay = ((myrec >> 16) & nm) << sh;
+            const uint64_t pm = nm << sh;
+            const int w0 = cc >> 2;
+            uint32_t D[NPW], M[NPW];
+#pragma unroll
+            for (int w = 0; w < NPW; w++) {
+                D[w] = (w == w0) ? (uint32_t)pay : ((w == w0 + 1) ? (uint32_t)(pay >> 32) : 0u);
+                M[w] = (w == w0) ? (uint32_t)pm : ((w == w0 + 1) ? (uint32_t)(pm >> 32) : 0u);
+            }
+            // ---- inclusive scan: later records overwrite earlier bytes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
                 for (int w = 0; w < NPW; w++) {
-                    D[w] = (w == w0) ? (uint32_t)pay : ((w == w0 + 1) ? (uint32_t)(pay >> 32) : 0u);
-                    M[w] = (w == w0) ? (uint32_t)pm : ((w == w0 + 1) ? (uint32_t)(pm >> 32) : 0u);
-                }
-                // ---- inclusive scan: later records overwrite earlier bytes
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-                    for (int w = 0; w < NPW; w++) {
-                        const uint32_t dn = __shfl_up_sync(kFull, D[w], o);
-                        const uint32_t mn = __shfl_up_sync(kFull, M[w], o);
-                        if (lane >= o) {
-                            D[w] = lop_merge(D[w], dn, M[w]);
-                            M[w] |= mn;
-                        }
+                    const uint32_t dn = __shfl_up_sync(kFull, D[w], o);
+                    const uint32_t mn = __shfl_up_sync(kFull, M[w], o);
+                    if (lane >= o) {
+                        D[w] = lop_merge(D[w], dn, M[w]);
+                        M[w] |= mn;
                     }
                 }
+            }
 #pragma unroll
-                for (int w = 0; w < NPW; w++) D[w] = lop_merge(D[w], carry[w], M[w]);
+            for (int w = 0; w < NPW; w++) D[w] = lop_merge(D[w], carry[w], M[w]);
 #pragma unroll
-                for (int w = 0; w < NPW; w++) carry[w] = __shfl_sync(kFull, D[w], 31);
+            for (int w = 0; w < NPW; w++) carry[w] = __shfl_sync(kFull, D[w], 31);
+            const int len = cc + n;
+            if (!MIXED || __all_sync(kFull, ty == R_PP || ty == R_PATH)) {
                 const bool emit = (ty == R_PP);
-                const int len = cc + n;
                 const int tot = emit ? len + (int)((myrec >> 3) & 1) : 0;
                 const unsigned em = __ballot_sync(kFull, emit);
                 if (HASH) {
@@ -375,32 +378,102 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 cu.pp += (uint64_t)__popc(em);
                 cu.vv += (uint64_t)T;
             } else {
-                // ---- segment items / head blocks in this batch: sequential replay
-                constexpr int NP = (4 * NPW + 1 + 31) / 32;
-                int P[NP];
-#pragma unroll
-                for (int r = 0; r < NP; r++) {
-                    const int pos = lane + 32 * r;
-                    const int w = pos >> 2;
-                    uint32_t xw = 0;
-#pragma unroll
-                    for (int k2 = 0; k2 < NPW; k2++)
-                        if (k2 == w) xw = carry[k2];
-                    P[r] = (int)((xw >> (8 * (pos & 3))) & 0xff);
+                // ---- segment items / head blocks in this batch: lane-parallel, every lane
+                // emits its own record at offsets from warp scans of the cursor increments
+                const int myarg = (int)(myrec >> 32);
+                int argv = __shfl_up_sync(kFull, myarg, 1);  // an R_ARG record precedes its HEAD / TRANSIT
+                if (lane == 0) argv = cu.arg;
+                const int lastty = __shfl_sync(kFull, ty, 31);
+                const int lastarg = __shfl_sync(kFull, myarg, 31);
+                if (lastty == R_ARG) cu.arg = lastarg;
+                const bool isPP = ty == R_PP, isH = ty == R_HEAD, isI = ty == R_TAIL || ty == R_TRANSIT;
+                const int tot = len + (isPP ? (int)((myrec >> 3) & 1) : 0);
+                int32_t x = 0;
+                uint64_t dpp = 0, dvv = 0;
+                if (isPP) {
+                    dpp = 1;
+                    dvv = (uint64_t)tot;
+                } else if (isH) {
+                    x = __ldg(G.out_gid + argv);
+                    const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                    dpp = Wx;
+                    dvv = (uint64_t)len * Wx + Vx;
                 }
-                for (int i = 0; i < nb; i++)
-                    replay_one<NP, HASH>(A, __shfl_sync(kFull, myrec, i), P, cu, lane, ga, vb, s0g, acc);
-                // back to bytes: word w = positions 4w..4w+3 (lane (4w+b) & 31 of register (4w+b) >> 5)
+                const uint32_t dhd = isH ? 1u : 0u, dhdv = isH ? (uint32_t)len : 0u;
+                const uint32_t dit = isI ? 1u : 0u, ditv = isI ? (uint32_t)len : 0u;
+                // inclusive warp scans, then exclusive = inclusive - own
+                uint64_t spp = dpp, svv = dvv;
+                uint32_t shd = dhd, shdv = dhdv, sit = dit, sitv = ditv;
 #pragma unroll
-                for (int w = 0; w < NPW; w++) {
-                    uint32_t xw = 0;
-#pragma unroll
-                    for (int b = 0; b < 4; b++) {
-                        const int pos = 4 * w + b;
-                        xw |= ((uint32_t)__shfl_sync(kFull, P[pos >> 5], pos & 31) & 0xffu) << (8 * b);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t a1 = __shfl_up_sync(kFull, spp, o), a2 = __shfl_up_sync(kFull, svv, o);
+                    const uint32_t b1 = __shfl_up_sync(kFull, shd, o), b2 = __shfl_up_sync(kFull, shdv, o);
+                    const uint32_t c1 = __shfl_up_sync(kFull, sit, o), c2 = __shfl_up_sync(kFull, sitv, o);
+                    if (lane >= o) {
+                        spp += a1;
+                        svv += a2;
+                        shd += b1;
+                        shdv += b2;
+                        sit += c1;
+                        sitv += c2;
                     }
-                    carry[w] = xw;
                 }
+                const uint64_t pp = cu.pp + spp - dpp, vv = cu.vv + svv - dvv;
+                const uint64_t hd = cu.hd + shd - dhd, hdv = cu.hdv + shdv - dhdv;
+                const uint64_t it = cu.it + sit - dit, itv = cu.itv + sitv - ditv;
+                int32_t *dst = nullptr;
+                if (isPP && !HASH) {
+                    A.out_off[pp] = (int64_t)vv;
+                    dst = A.out_vert + vv;
+                } else if (isH) {
+                    HeadRec hr;
+                    hr.pp_off = pp;
+                    hr.v_off = vv;
+                    hr.hv_off = hdv;
+                    hr.len = len;
+                    hr.x = x;
+                    A.heads[hd] = hr;
+                    dst = A.head_pool + hdv;
+                } else if (isI) {
+                    ItemRec ir;
+                    ir.pool_off = (int64_t)itv;
+                    ir.len = len;
+                    ir.y = (ty == R_TRANSIT) ? __ldg(G.out_gid + argv) : -1;
+                    ir.ent = s0g;
+                    ir.pad = 0;
+                    A.items[it] = ir;
+                    dst = A.item_pool + itv;
+                }
+                if (HASH && isPP) {
+                    PathHash hs;
+                    hs.init((uint64_t)tot);
+#pragma unroll
+                    for (int p = 0; p < 4 * NPW; p++) {
+                        if (p < len) {
+                            const int loc = (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
+                            hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
+                        }
+                    }
+                    if (len < tot) hs.add(s0g);
+                    acc.a += hs.a;
+                    acc.b += hs.b;
+                }
+                if (dst) {
+#pragma unroll
+                    for (int p = 0; p < 4 * NPW; p++) {
+                        if (p < len) {
+                            const int loc = (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
+                            dst[p] = (ga >= 0) ? ga + loc : __ldg(G.slot_gid + vb + loc);
+                        }
+                    }
+                    if (len < tot) dst[len] = s0g;  // closing vertex of a cycle
+                }
+                cu.pp += __shfl_sync(kFull, spp, 31);
+                cu.vv += __shfl_sync(kFull, svv, 31);
+                cu.hd += __shfl_sync(kFull, shd, 31);
+                cu.hdv += __shfl_sync(kFull, shdv, 31);
+                cu.it += __shfl_sync(kFull, sit, 31);
+                cu.itv += __shfl_sync(kFull, sitv, 31);
             }
         }
     }
