@@ -287,9 +287,12 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
         Cursor cu = unit_cursor(A, u);
         const int64_t nrec = A.rcount[u];
         RecReader rd{A.chunks + (A.rfirst[u] & ~(int64_t)(kChunkRecs - 1)), (int)(A.rfirst[u] & (kChunkRecs - 1))};
+        // records are fetched one batch ahead: the next batch's loads overlap this batch's work
+        uint64_t nextrec = (nrec > 0) ? fetch32(A, rd, (nrec < 32) ? (int)nrec : 32, lane) : 0ull;
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
-            const uint64_t myrec = fetch32(A, rd, nb, lane);  // lanes >= nb: 0 = an empty R_PATH
+            const uint64_t myrec = nextrec;  // lanes >= nb: 0 = an empty R_PATH
+            if (r0 + 32 < nrec) nextrec = fetch32(A, rd, (nrec - r0 - 32 < 32) ? (int)(nrec - r0 - 32) : 32, lane);
             const int ty = (int)(myrec & 7);
             // ---- this lane's bytes: positions cc .. cc+n-1 of the path
             const int cc = (int)((myrec >> 4) & 0x1ff);
