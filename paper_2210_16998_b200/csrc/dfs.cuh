@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
     int64_t child_head = -1;  // latest donated block of the running unit
     int nchild = 0;           // units donated by the running unit
 #ifdef TPGEN_KERNEL_DEBUG
-    unsigned long long d_it = 0, d_act = 0, d_don = 0;
+    unsigned long long d_it = 0, d_act = 0, d_don = 0, d_last = 0, d_prev = 0, d_lt = 0;
     const unsigned long long t0 = A.dbg ? A.dbg[7] : 0;
 #endif
     uint32_t last_split = 0;
@@ -663,12 +663,22 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         {
             const int na = __popc(__ballot_sync(kFull, L.active));
             d_act += na;
-            if (A.dbg && lane == 0 && (d_it & 15) == 0) {  // timeline: 64 buckets of 0.5 ms
+            if (A.dbg && lane == 0) {  // time-weighted timeline: 64 buckets of 0.1 ms
                 unsigned long long now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-                const unsigned long long bkt = min((now - t0) / 500000ull, 63ull);
-                atomicAdd(A.dbg + 8 + 2 * bkt, (unsigned long long)na);
-                atomicAdd(A.dbg + 9 + 2 * bkt, 1ull);
+                if (d_last == 0) {
+                    d_last = now;
+                } else {
+                    d_lt += (unsigned long long)na * (now - d_prev);  // lanes busy since the last pass
+                    if (now - d_last > 2000ull) {                     // flush about every 2 us
+                        const unsigned long long bkt = min((now - t0) / 100000ull, 63ull);
+                        atomicAdd(A.dbg + 8 + 2 * bkt, d_lt);
+                        atomicAdd(A.dbg + 9 + 2 * bkt, 32ull * (now - d_last));
+                        d_lt = 0;
+                        d_last = now;
+                    }
+                }
+                d_prev = now;
             }
         }
 #endif

@@ -592,9 +592,9 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
             unsigned long long d[160];
             TPG_CK(cudaMemcpyAsync(d, A.dbg, 160 * 8, cudaMemcpyDeviceToHost, s));
             TPG_CK(cudaStreamSynchronize(s));
-            fprintf(stderr, "[tpgen dfs timeline] avg active lanes per warp-iteration per 0.5 ms:");
+            fprintf(stderr, "[tpgen dfs timeline] busy lane fraction per 0.1 ms:");
             for (int b = 0; b < 64; b++)
-                if (d[9 + 2 * b]) fprintf(stderr, " %.1f", (double)d[8 + 2 * b] / d[9 + 2 * b]);
+                if (d[9 + 2 * b]) fprintf(stderr, " %.2f", (double)d[8 + 2 * b] / d[9 + 2 * b]);
             fprintf(stderr, "\n");
             fprintf(stderr, "[tpgen dfs] ms=%.3f iters=%llu active_lane_iters=%llu (%.2f/warp-iter) donations=%llu units=%llu\n",
                     ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], (h[1] >> 32) - qbase);
