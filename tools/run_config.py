@@ -12,7 +12,7 @@ from workloads import generators as gen  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--mode", default="materialize", choices=["materialize", "count_hash"])
+ap.add_argument("--mode", default="materialize", choices=["materialize", "count"])
 a = ap.parse_args()
 g = gen.make_config(a.config)
 plan = tp.Plan(g)
