@@ -308,24 +308,34 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 D[w] = (w == w0) ? (uint32_t)pay : ((w == w0 + 1) ? (uint32_t)(pay >> 32) : 0u);
                 M[w] = (w == w0) ? (uint32_t)pm : ((w == w0 + 1) ? (uint32_t)(pm >> 32) : 0u);
             }
+            const int len = cc + n;
+            // Words below the batch's smallest common prefix are the carry's in every lane, and
+            // words from the longest path on are never read: only [wlo, whi) take part
+            // (warp-uniform bounds, so the skipped words cost a uniform branch each).
+            const int wlo = __reduce_min_sync(kFull, (unsigned)(n > 0 ? cc : 4 * NPW)) >> 2;
+            const int whi = (__reduce_max_sync(kFull, (unsigned)len) + 3) >> 2;
             // ---- inclusive scan: later records overwrite earlier bytes
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
                 for (int w = 0; w < NPW; w++) {
-                    const uint32_t dn = __shfl_up_sync(kFull, D[w], o);
-                    const uint32_t mn = __shfl_up_sync(kFull, M[w], o);
-                    if (lane >= o) {
-                        D[w] = lop_merge(D[w], dn, M[w]);
-                        M[w] |= mn;
+                    if (w >= wlo && w < whi) {
+                        const uint32_t dn = __shfl_up_sync(kFull, D[w], o);
+                        const uint32_t mn = __shfl_up_sync(kFull, M[w], o);
+                        if (lane >= o) {
+                            D[w] = lop_merge(D[w], dn, M[w]);
+                            M[w] |= mn;
+                        }
                     }
                 }
             }
 #pragma unroll
-            for (int w = 0; w < NPW; w++) D[w] = lop_merge(D[w], carry[w], M[w]);
-#pragma unroll
-            for (int w = 0; w < NPW; w++) carry[w] = __shfl_sync(kFull, D[w], 31);
-            const int len = cc + n;
+            for (int w = 0; w < NPW; w++) {
+                if (w < whi) {
+                    D[w] = (w >= wlo) ? lop_merge(D[w], carry[w], M[w]) : carry[w];
+                    if (w >= wlo) carry[w] = __shfl_sync(kFull, D[w], 31);
+                }
+            }
             if (!MIXED || __all_sync(kFull, ty == R_PP || ty == R_PATH)) {
                 const bool emit = (ty == R_PP);
                 const int tot = emit ? len + (int)((myrec >> 3) & 1) : 0;
