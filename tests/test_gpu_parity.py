@@ -243,3 +243,41 @@ def test_overflow_retry_paths(monkeypatch, qcap, pool):
         st = _assert_same(g)
         rounds += st["n_count_rounds"]
     assert rounds > 10  # the caps forced retries
+
+
+@pytest.mark.parametrize("n,chords", [(100, [(0, 50), (70, 10)]), (150, [(0, 75), (100, 20), (40, 120)]),
+                                      (230, [(5, 200), (150, 7)])])
+def test_large_scc_masks(n, chords):
+    """SCCs of 65-256 vertices: multi-word visited masks (W = 2, 4) and the
+    sequential writer; materialized and COUNT_HASH digests agree with the oracle."""
+    arcs = [(i, (i + 1) % n) for i in range(n)] + chords
+    g = gen.from_arcs(n, arcs)
+    st = _assert_same(g)
+    cnt = tp.prime_paths(g, mode="count", digest=True).stats
+    assert (cnt["n_paths"], cnt["total_vertices"], cnt["hash_lo"], cnt["hash_hi"]) == \
+        (st["n_paths"], st["total_vertices"], st["hash_lo"], st["hash_hi"])
+
+
+def test_count_mode_digest_matches_oracle():
+    """COUNT_HASH (hash-mode writers, no output) gives the oracle's counts and digest on
+    graphs with segment items and head blocks (mixed batches) and without."""
+    rng = np.random.default_rng(7)
+    graphs = [gen.fig1b(), gen.config2(), gen.config4(K=40), gen.dense_scc(14, 3, 1), gen.k_seq_loops(4, 5)]
+    graphs += [gen.random_digraph(int(rng.integers(3, 10)), 0.3, 900 + i) for i in range(20)]
+    for g in graphs:
+        ro, rv = oracle.prime_paths(g)
+        st = tp.prime_paths(g, mode="count", digest=True).stats
+        assert st["n_paths"] == len(ro) - 1, g.name
+        assert st["total_vertices"] == int(ro[-1]), g.name
+        assert (st["hash_lo"], st["hash_hi"]) == oracle.digest(ro, rv), g.name
+        assert st["n_extensions"] == oracle.ext_count(g), g.name
+
+
+def test_test_paths_config4():
+    g = gen.config4(K=40)
+    ro, rv = oracle.prime_paths(g)
+    to, tv = oracle.test_paths(g, ro, rv, g.entry, g.exit)
+    ts = tp.test_paths(g, g.entry, g.exit)
+    o, v = ts.to_numpy()
+    np.testing.assert_array_equal(o, to)
+    np.testing.assert_array_equal(v, tv)
