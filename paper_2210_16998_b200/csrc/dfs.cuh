@@ -243,18 +243,19 @@ __device__ __forceinline__ int out_event(const Lane<T> &L) {
 
 // A lane writes the records of all its units into one chain of chunks: a unit
 // starts wherever the previous one ended (rfirst = global record index), so
-// starting a unit costs no allocation.  The next chunk is reserved (atomic
-// issued) when the current one is half full and consumed when it fills.
+// starting a unit costs no allocation.  When a chunk fills, the lane switches to
+// the chunk it reserved at its previous switch and reserves the next one (the
+// atomic's result is needed only one chunk later).
 struct RecWriter {
     uint64_t *cur;   // current chunk
     int fill;        // records used in it (kChunkRecs - 1: full, the next record needs a new chunk)
-    long long next;  // chunk reserved for when this one fills (-1: none)
+    long long next;  // chunk reserved for the next switch (-1: none)
     int count;       // records of the current unit
 };
 
 __device__ __forceinline__ void rec_switch(const DfsArgs &A, RecWriter &R) {
     unsigned long long nc = (R.next >= 0) ? (unsigned long long)R.next : atomicAdd(A.chunk_next, 1ull);
-    R.next = -1;
+    R.next = (long long)atomicAdd(A.chunk_next, 1ull);
     if (nc >= A.chunk_cap) {  // pool exhausted: the phase is retried with a bigger pool;
         atomicOr(A.overflow, 2u);  // meanwhile write into the sink chunk past the end
         nc = A.chunk_cap;
@@ -264,13 +265,8 @@ __device__ __forceinline__ void rec_switch(const DfsArgs &A, RecWriter &R) {
     R.fill = 0;
 }
 
-__device__ __forceinline__ void rec_edge(const DfsArgs &A, RecWriter &R) {
-    if (R.fill == kChunkRecs - 1) rec_switch(A, R);
-    else if (R.next < 0) R.next = (long long)atomicAdd(A.chunk_next, 1ull);
-}
 __device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t rec) {
-    // (fill == 32: reserve the next chunk; fill == 63: switch to it)
-    if (R.fill == kChunkRecs - 1 || R.fill == kChunkRecs / 2) rec_edge(A, R);
+    if (R.fill == kChunkRecs - 1) rec_switch(A, R);
     R.cur[R.fill++] = rec;
     R.count++;
 }
