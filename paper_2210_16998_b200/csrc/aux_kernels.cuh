@@ -265,6 +265,7 @@ struct StitchArgs {
     const int32_t *head_pool, *item_pool;
     int64_t *out_off;
     int32_t *out_vert;
+    uint64_t n_pp, n_vert;  // output sizes (debug-build bounds checks)
 };
 
 __device__ __forceinline__ int64_t upper_bound_u64(const uint64_t *a, int64_t lo, int64_t hi, uint64_t key) {
@@ -303,6 +304,7 @@ __global__ void stitch_kernel(StitchArgs A) {
             kk = k2;
         }
         const uint64_t vstart = H.v_off + k * (uint64_t)H.len + vrel;
+        TPG_DCHECK(H.pp_off + k < A.n_pp && vstart + H.len <= A.n_vert, "stitch: path out of range");
         if (lane == 0) A.out_off[H.pp_off + k] = (int64_t)vstart;
         int32_t *dst = A.out_vert + vstart;
         for (int j = lane; j < H.len; j += 32) dst[j] = A.head_pool[H.hv_off + j];

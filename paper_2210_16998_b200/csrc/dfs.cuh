@@ -260,6 +260,7 @@ __device__ __forceinline__ void rec_switch(const DfsArgs &A, RecWriter &R) {
         atomicOr(A.overflow, 2u);  // meanwhile write into the sink chunk past the end
         nc = A.chunk_cap;
     }
+    TPG_DCHECK(nc <= A.chunk_cap, "dfs: chunk out of range");
     R.cur[kChunkRecs - 1] = nc;  // link
     R.cur = A.chunks + nc * kChunkRecs;
     R.fill = 0;
@@ -550,6 +551,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             if (rdy != 0u) {
                 waiting = false;
                 // queue slots are written by other SMs during this launch: read them at L2 (ld.cg)
+                TPG_DCHECK(slot >= 0 && slot < (int64_t)A.qcap, "dfs: claimed slot out of range");
                 const Unit<W> *U = units + slot;
                 const int4 h = __ldcg(reinterpret_cast<const int4 *>(&U->scc));  // scc, e, -, depth|kind
                 {

@@ -908,6 +908,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     E.items = P.items.as<ItemRec>();
     E.item_pool = P.item_pool.as<int32_t>();
     E.hash_acc = hacc;
+    for (int c = 0; c < C_NUM; c++) E.lim[c] = tot[c];
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
         launch_expand<W>(H, E, nu, P.num_sms, hash_only, n_items > 0 || n_heads > 0, s);
@@ -958,6 +959,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         SA.item_pool = P.item_pool.as<int32_t>();
         SA.out_off = (int64_t *)d_off;
         SA.out_vert = (int32_t *)d_vert;
+        SA.n_pp = (uint64_t)n_pp;
+        SA.n_vert = (uint64_t)n_vert;
         if (ncomp > 0) {
             if (hash_only) stitch_hash_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(SA, hacc);
             else stitch_kernel<<<grid_for((int64_t)ncomp * 32, 256, P.num_sms * 8), 256, 0, s>>>(SA);

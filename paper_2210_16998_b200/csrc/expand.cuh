@@ -42,6 +42,7 @@ struct ExpandArgs {
     ItemRec *items;
     int32_t *item_pool;
     unsigned long long *hash_acc;  // HASH kernels: digest of the prime paths instead of writing them
+    uint64_t lim[C_NUM];           // totals of the call (debug-build bounds checks)
 };
 
 constexpr int kExpandThreads = 256;
@@ -135,11 +136,13 @@ __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, in
         return;
     }
     if (ty == R_PP) {
+        TPG_DCHECK(cu.pp < A.lim[C_PP] && cu.vv + tot <= A.lim[C_VERT], "replay: prime path out of range");
         dst = A.out_vert + cu.vv;
         if (lane == 0) A.out_off[cu.pp] = (int64_t)cu.vv;
         cu.pp += 1;
         cu.vv += (uint64_t)tot;
     } else if (ty == R_HEAD) {
+        TPG_DCHECK(cu.arg >= 0 && cu.hd < A.lim[C_HEADS] && cu.hdv + len <= A.lim[C_HEADV], "replay: head out of range");
         const int32_t x = __ldg(G.out_gid + cu.arg);
         dst = A.head_pool + cu.hdv;
         if (lane == 0) {
@@ -157,6 +160,7 @@ __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, in
         cu.hd += 1;
         cu.hdv += (uint64_t)len;
     } else {  // R_TAIL / R_TRANSIT
+        TPG_DCHECK(cu.it < A.lim[C_ITEMS] && cu.itv + len <= A.lim[C_ITEMV], "replay: item out of range");
         dst = A.item_pool + cu.itv;
         if (lane == 0) {
             ItemRec ir;
@@ -372,6 +376,8 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 }
                 const int T = __shfl_sync(kFull, ex, 31);
                 ex -= tot;
+                TPG_DCHECK(cu.pp + __popc(em) <= A.lim[C_PP] && cu.vv + (uint64_t)T <= A.lim[C_VERT],
+                           "expand: batch out of range");
                 if (emit) A.out_off[cu.pp + __popc(em & lt_mask)] = (int64_t)(cu.vv + (uint64_t)ex);
                 // ---- stage the vertices (global ids), then stream them out coalesced
                 if (ga >= 0) {
@@ -434,6 +440,10 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 const uint64_t pp = cu.pp + spp - dpp, vv = cu.vv + svv - dvv;
                 const uint64_t hd = cu.hd + shd - dhd, hdv = cu.hdv + shdv - dhdv;
                 const uint64_t it = cu.it + sit - dit, itv = cu.itv + sitv - ditv;
+                TPG_DCHECK(!isPP || (pp < A.lim[C_PP] && vv + tot <= A.lim[C_VERT]), "expand: mixed pp out of range");
+                TPG_DCHECK(!isH || (argv >= 0 && hd < A.lim[C_HEADS] && hdv + len <= A.lim[C_HEADV]),
+                           "expand: mixed head out of range");
+                TPG_DCHECK(!isI || (it < A.lim[C_ITEMS] && itv + len <= A.lim[C_ITEMV]), "expand: mixed item out of range");
                 int32_t *dst = nullptr;
                 if (isPP && !HASH) {
                     A.out_off[pp] = (int64_t)vv;

@@ -25,6 +25,23 @@
 
 #include "internal.h"
 
+// Bounds checks of debug builds (TPGEN_KERNEL_DEBUG=1 python paper_2210_16998_b200/build.py --force):
+// a failed check prints its site and traps; release builds compile them away.
+#ifdef TPGEN_KERNEL_DEBUG
+#include <cstdio>
+#define TPG_DCHECK(cond, what)                                                          \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            printf("tpgen device check failed: %s (%s:%d)\n", what, __FILE__, __LINE__); \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define TPG_DCHECK(cond, what) \
+    do {                       \
+    } while (0)
+#endif
+
 namespace tpg {
 
 enum UnitKind : uint8_t { K_NODE = 0, K_SELF = 1, K_CLOSURE = 2, K_OUT = 3 };
