@@ -281,3 +281,25 @@ def test_test_paths_config4():
     o, v = ts.to_numpy()
     np.testing.assert_array_equal(o, to)
     np.testing.assert_array_equal(v, tv)
+
+
+def test_long_paths_and_many_sccs():
+    """Paths far longer than one SCC (a 20000-vertex chain: one prime path of 20000
+    vertices, stitched from 20000 one-vertex segments), 2^16 source-sink paths of a
+    ladder DAG, and a chain of 3000 three-cycles (many small SCCs)."""
+    n = 20000
+    _assert_same(gen.from_arcs(n, [(i, i + 1) for i in range(n - 1)]))
+    k = 16  # ladder: i -> (i+1 top, i+1 bottom) for both rails
+    arcs = []
+    for i in range(k):
+        for a in (2 * i, 2 * i + 1):
+            arcs += [(a, 2 * i + 2), (a, 2 * i + 3)]
+    st = _assert_same(gen.from_arcs(2 * k + 2, arcs))
+    assert st["n_paths"] == 2 * 2 ** k  # 2 sources x 2^k rail choices (each ending in one of the 2 sinks)
+    arcs = []
+    for c in range(3000):
+        b = 3 * c
+        arcs += [(b, b + 1), (b + 1, b + 2), (b + 2, b)]
+        if c + 1 < 3000:
+            arcs.append((b + 2, b + 3))
+    _assert_same(gen.from_arcs(9000, arcs))
