@@ -328,6 +328,160 @@ __global__ void stitch_kernel(StitchArgs A) {
     }
 }
 
+// Cross-SCC writer by ranges: warp w writes the completions [g0, g1) of the
+// global cross-PP index space (an even split).  It unranks g0 once (binary
+// searches over the cumulative item weights, level by level) into a stack of
+// (entry, item, prefix length) per level, then steps through the following
+// completions in lexicographic order like an odometer: the deepest level that
+// still has a next item advances and the levels below restart at the first item
+// of their entry; when a head's completions run out, the next head starts from
+// its entry's first items.  Consecutive completions are adjacent in the output
+// and share the prefix up to the changed level, which the warp copies from the
+// path it wrote just before (coalesced, L2-resident); only the changed items
+// come from the segment pool.  (Every item leads to at least one completion: a
+// sink SCC always has a tail, so no zero-weight item needs skipping.)
+struct StitchRangeArgs {
+    StitchArgs S;
+    int64_t *scratch;  // per warp: 3 * dmax int64 (entry, item, prefix length per level)
+    int dmax;
+};
+
+__global__ void stitch_range_kernel(StitchRangeArgs C) {
+    const StitchArgs &A = C.S;
+    const int lane = threadIdx.x & 31;
+    const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t *sx = C.scratch + wg * 3 * (uint64_t)C.dmax;  // entry of each level
+    int64_t *si = sx + C.dmax;                            // item of each level
+    int64_t *sp = si + C.dmax;                            // path length before each level's item
+    const uint64_t q = A.n_comp / nw, r = A.n_comp % nw;
+    const uint64_t g0 = q * wg + (wg < r ? wg : r), g1 = g0 + q + (wg < r ? 1 : 0);
+    if (g0 >= g1) return;
+    int64_t h = upper_bound_u64(A.comp_off, 0, A.n_heads, g0) - 1;
+    HeadRec H = A.heads[h];
+    uint64_t k = g0 - A.comp_off[h];
+    uint64_t wh = ((h + 1 < A.n_heads) ? A.comp_off[h + 1] : A.n_comp) - A.comp_off[h];
+    // ---- unrank completion k of head h (lane 0) into the stack; its vertex offset inside the head block
+    int depth = 0;
+    int64_t total = 0;
+    uint64_t vrel = 0;
+    if (lane == 0) {
+        uint64_t kk = k;
+        int32_t x = H.x;
+        int64_t pl = H.len;
+        while (true) {
+            const int64_t b = A.ibeg[x], e = A.iend[x];
+            const uint64_t bc = A.cum[b], bv = A.vcum[b];
+            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            const uint64_t k2 = kk - (A.cum[i] - bc);
+            const ItemRec it = A.items[i];
+            vrel += A.vcum[i] - bv;
+            TPG_DCHECK(depth < C.dmax, "stitch: stack depth");
+            sx[depth] = x;
+            si[depth] = i;
+            sp[depth] = pl;
+            depth++;
+            pl += it.len;
+            if (it.y < 0) break;
+            vrel += k2 * (uint64_t)it.len;
+            x = it.y;
+            kk = k2;
+        }
+        total = pl;
+    }
+    depth = __shfl_sync(kFull, depth, 0);
+    total = __shfl_sync(kFull, total, 0);
+    vrel = __shfl_sync(kFull, vrel, 0);
+    __syncwarp();
+    uint64_t vstart = H.v_off + k * (uint64_t)H.len + vrel, pstart = 0;
+    int changed = 0;  // first level that differs from the previous completion (0 with a new head: all of it)
+    bool fresh = true;
+    for (uint64_t g = g0; g < g1; g++) {
+        if (g > g0) {
+            // ---- advance: the next completion of this head, or the first one of the next head
+            int64_t ntotal = 0;
+            int nchanged = 0;
+            bool nfresh = false;
+            if (lane == 0) {
+                int j = -1;
+                int64_t i = 0;
+                int32_t x = 0;
+                if (k + 1 < wh) {
+                    j = depth - 1;
+                    i = si[j] + 1;
+                    x = (int32_t)sx[j];
+                    while (i >= A.iend[x]) {  // this level is exhausted: advance the one above
+                        j--;
+                        TPG_DCHECK(j >= 0, "stitch: odometer underflow");
+                        i = si[j] + 1;
+                        x = (int32_t)sx[j];
+                    }
+                } else {  // next head: its entry's first items
+                    nfresh = true;
+                }
+                int d = nfresh ? 0 : j;
+                int64_t pl = nfresh ? 0 : sp[j];
+                if (nfresh) {
+                    const HeadRec Hn = A.heads[h + 1];
+                    x = Hn.x;
+                    i = A.ibeg[x];
+                    pl = Hn.len;
+                }
+                nchanged = d;
+                while (true) {  // the new item at level d, then the first items below it
+                    const ItemRec it = A.items[i];
+                    TPG_DCHECK(d < C.dmax, "stitch: stack depth");
+                    sx[d] = x;
+                    si[d] = i;
+                    sp[d] = pl;
+                    d++;
+                    pl += it.len;
+                    if (it.y < 0) break;
+                    x = it.y;
+                    i = A.ibeg[x];
+                }
+                depth = d;
+                ntotal = pl;
+            }
+            nfresh = __shfl_sync(kFull, nfresh, 0);
+            nchanged = __shfl_sync(kFull, nchanged, 0);
+            depth = __shfl_sync(kFull, depth, 0);
+            ntotal = __shfl_sync(kFull, ntotal, 0);
+            __syncwarp();  // the stack and the previous path are visible to every lane
+            if (nfresh) {
+                h++;
+                H = A.heads[h];
+                k = 0;
+                wh = ((h + 1 < A.n_heads) ? A.comp_off[h + 1] : A.n_comp) - A.comp_off[h];
+                vstart = H.v_off;
+            } else {
+                k++;
+                pstart = vstart;
+                vstart += (uint64_t)total;
+            }
+            total = ntotal;
+            changed = nchanged;
+            fresh = nfresh;
+        }
+        TPG_DCHECK(H.pp_off + k < A.n_pp && vstart + (uint64_t)total <= A.n_vert, "stitch: path out of range");
+        int32_t *dst = A.out_vert + vstart;
+        if (fresh) {  // head vertices, then every level's item
+            for (int j = lane; j < H.len; j += 32) dst[j] = __ldg(A.head_pool + H.hv_off + j);
+        } else {  // the prefix shared with the previous completion (written just before)
+            const int64_t keep = sp[changed];
+            const int32_t *src = A.out_vert + pstart;
+            for (int64_t j = lane; j < keep; j += 32) dst[j] = __ldcg(src + j);
+        }
+        for (int d = changed; d < depth; d++) {
+            const ItemRec it = A.items[si[d]];
+            const int32_t *src = A.item_pool + it.pool_off;
+            for (int j = lane; j < it.len; j += 32) dst[sp[d] + j] = __ldg(src + j);
+        }
+        if (lane == 0) A.out_off[H.pp_off + k] = (int64_t)vstart;
+        __syncwarp();
+    }
+}
+
 // COUNT_HASH mode: the digest of every cross-SCC prime path without writing it;
 // one thread per path (completion), vertices absorbed in path order.
 __global__ void stitch_hash_kernel(StitchArgs A, unsigned long long *acc) {

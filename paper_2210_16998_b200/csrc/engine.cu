@@ -104,7 +104,7 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr};
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
@@ -962,9 +962,28 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         SA.n_pp = (uint64_t)n_pp;
         SA.n_vert = (uint64_t)n_vert;
         if (ncomp > 0) {
-            if (hash_only) stitch_hash_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(SA, hacc);
-            else stitch_kernel<<<grid_for((int64_t)ncomp * 32, 256, P.num_sms * 8), 256, 0, s>>>(SA);
-            launches++;
+            if (hash_only) {
+                stitch_hash_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(SA, hacc);
+                launches++;
+            } else {
+                // range writer: an even split of the completions over the warps, one unranking each
+                const int dmax = std::min(H.n_scc, H.n) + 1;  // levels: one SCC each along a DAG path
+                int64_t warps = std::min<int64_t>((int64_t)ncomp, (int64_t)P.num_sms * 32);
+                const size_t per_warp = (size_t)3 * dmax * 8;
+                warps = std::min<int64_t>(warps, (int64_t)((size_t)(512u << 20) / per_warp));
+                warps = (warps + 7) & ~(int64_t)7;  // whole 256-thread blocks: every launched warp has its stack
+                if ((size_t)warps * per_warp <= ((size_t)1 << 30)) {
+                    TPG_TRY(P.sscratch.ensure((size_t)warps * per_warp, s));
+                    StitchRangeArgs CA;
+                    CA.S = SA;
+                    CA.scratch = P.sscratch.as<int64_t>();
+                    CA.dmax = dmax;
+                    stitch_range_kernel<<<(int)(warps / 8), 256, 0, s>>>(CA);
+                } else {  // very deep component DAGs: one warp per path, no stack
+                    stitch_kernel<<<grid_for((int64_t)ncomp * 32, 256, P.num_sms * 8), 256, 0, s>>>(SA);
+                }
+                launches++;
+            }
         }
     }
     if (!hash_only) {

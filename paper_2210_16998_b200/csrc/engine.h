@@ -46,6 +46,7 @@ struct PlanImpl {
     int maxgen = 0;               // deepest split generation so far in this call
     uint32_t split_min = 32;      // steps between two donations of a unit
     DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
+    DevBuf sscratch;  // cross-SCC range writer: per-warp level stacks
     bool overflow = false;
     ~PlanImpl();
     std::vector<DevBuf *> all_bufs();
