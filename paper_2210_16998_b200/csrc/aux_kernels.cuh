@@ -470,7 +470,16 @@ __global__ void stitch_range_kernel(StitchRangeArgs C) {
         } else {  // the prefix shared with the previous completion (written just before)
             const int64_t keep = sp[changed];
             const int32_t *src = A.out_vert + pstart;
-            for (int64_t j = lane; j < keep; j += 32) dst[j] = __ldcg(src + j);
+            int64_t j = lane;
+            for (; j + 96 < keep; j += 128) {  // four loads in flight per lane
+                const int32_t a0 = __ldcg(src + j), a1 = __ldcg(src + j + 32), a2 = __ldcg(src + j + 64),
+                              a3 = __ldcg(src + j + 96);
+                dst[j] = a0;
+                dst[j + 32] = a1;
+                dst[j + 64] = a2;
+                dst[j + 96] = a3;
+            }
+            for (; j < keep; j += 32) dst[j] = __ldcg(src + j);
         }
         for (int d = changed; d < depth; d++) {
             const ItemRec it = A.items[si[d]];
