@@ -471,7 +471,14 @@ __global__ void stitch_range_kernel(StitchRangeArgs C) {
             const int64_t keep = sp[changed];
             const int32_t *src = A.out_vert + pstart;
             int64_t j = lane;
-            for (; j + 96 < keep; j += 128) {  // four loads in flight per lane
+            for (; j + 224 < keep; j += 256) {  // eight loads in flight per lane
+                int32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = __ldcg(src + j + 32 * u);
+#pragma unroll
+                for (int u = 0; u < 8; u++) dst[j + 32 * u] = v[u];
+            }
+            for (; j + 96 < keep; j += 128) {  // four
                 const int32_t a0 = __ldcg(src + j), a1 = __ldcg(src + j + 32), a2 = __ldcg(src + j + 64),
                               a3 = __ldcg(src + j + 96);
                 dst[j] = a0;
