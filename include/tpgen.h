@@ -172,6 +172,9 @@ tpgen_status tpgen_plan_create(const int64_t *csr_offsets, const int32_t *csr_ta
                                const tpgen_options *opt, tpgen_plan **plan);
 tpgen_status tpgen_plan_prime_paths(tpgen_plan *plan, const tpgen_options *opt, tpgen_paths *out,
                                     tpgen_stats *stats);
+/* Test paths of the plan's graph (same contract as tpgen_test_paths, no re-planning). */
+tpgen_status tpgen_plan_test_paths(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t entry, int32_t exit,
+                                   const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats);
 void tpgen_plan_destroy(tpgen_plan *plan);
 
 #ifdef __cplusplus

@@ -225,29 +225,35 @@ def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *,
     so, st, n = _csr(graph)
     alloc = None
     o = _options(device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(device, stream), alloc)
-    pin = None
     keep = []
-    if prime is not None:
-        pin = _abi.Paths()
-        pin.n_paths = prime.n_paths
-        if prime.on_device:
-            pin.offsets = ctypes.cast(prime.offsets.data_ptr(), ctypes.POINTER(ctypes.c_int64))
-            pin.vertices = ctypes.cast(prime.vertices.data_ptr(), ctypes.POINTER(ctypes.c_int32))
-            pin.on_device = 1
-        else:
-            a = np.ascontiguousarray(prime.offsets, dtype=np.int64)
-            b = np.ascontiguousarray(prime.vertices, dtype=np.int32)
-            if b.size == 0:
-                b = np.zeros(1, dtype=np.int32)
-            keep += [a, b]
-            pin.offsets = _p64(a)
-            pin.vertices = _p32(b)
-            pin.on_device = 0
-        pin.device = device
+    pin = _paths_in(prime, device, keep)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_test_paths(_p64(so), _p32(st), n, ctypes.byref(pin) if pin is not None else None, entry, exit,
                                 ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc)
+
+
+def _paths_in(prime: Optional[PathSet], device: int, keep: list):
+    """A PathSet as the ABI's tpgen_paths input (device views or host arrays kept alive in `keep`)."""
+    if prime is None:
+        return None
+    pin = _abi.Paths()
+    pin.n_paths = prime.n_paths
+    if prime.on_device:
+        pin.offsets = ctypes.cast(prime.offsets.data_ptr(), ctypes.POINTER(ctypes.c_int64))
+        pin.vertices = ctypes.cast(prime.vertices.data_ptr(), ctypes.POINTER(ctypes.c_int32))
+        pin.on_device = 1
+    else:
+        a = np.ascontiguousarray(prime.offsets, dtype=np.int64)
+        b = np.ascontiguousarray(prime.vertices, dtype=np.int32)
+        if b.size == 0:
+            b = np.zeros(1, dtype=np.int32)
+        keep += [a, b]
+        pin.offsets = _p64(a)
+        pin.vertices = _p32(b)
+        pin.on_device = 0
+    pin.device = device
+    return pin
 
 
 def components(graph):
@@ -286,6 +292,19 @@ class Plan:
         paths, stats = _abi.Paths(), _abi.Stats()
         _check(lib.tpgen_plan_prime_paths(self._h, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
         return _wrap(paths, stats, alloc, host_out)
+
+    def test_paths(self, entry: int, exit: int, prime: Optional[PathSet] = None, *, output: str = "device",
+                   stream=None) -> PathSet:
+        """Test paths of the plan's graph (tpgen_plan_test_paths): no re-planning per call."""
+        lib = library()
+        o = _options(self.device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(self.device, stream),
+                     None)
+        keep = []
+        pin = _paths_in(prime, self.device, keep)
+        paths, stats = _abi.Paths(), _abi.Stats()
+        _check(lib.tpgen_plan_test_paths(self._h, ctypes.byref(pin) if pin is not None else None, entry, exit,
+                                         ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
+        return _wrap(paths, stats, None)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

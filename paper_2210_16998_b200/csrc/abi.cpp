@@ -171,6 +171,28 @@ tpgen_status tpgen_plan_prime_paths(tpgen_plan *plan, const tpgen_options *opt, 
     return s;
 }
 
+tpgen_status tpgen_plan_test_paths(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t entry, int32_t exit,
+                                   const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats) {
+    if (!plan || !out) return TPGEN_ERR_INVALID_ARGUMENT;
+    memset(out, 0, sizeof(*out));
+    tpgen_options o = resolve(opt);
+    tpgen_status s = check_options(o);
+    if (s != TPGEN_OK) return s;
+    const int32_t n = plan->impl.hp.n;
+    if (entry < 0 || entry >= n || exit < 0 || exit >= n) {
+        tpg::set_error("entry/exit out of range");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (prime_paths && prime_paths->n_paths > 0 && (!prime_paths->offsets || !prime_paths->vertices)) {
+        tpg::set_error("prime_paths has NULL arrays");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    DeviceScope ds(plan->impl.device);
+    s = tpg::run_test_paths(plan->impl, prime_paths, entry, exit, o, out, stats);
+    if (s != TPGEN_OK) memset(out, 0, sizeof(*out));
+    return s;
+}
+
 void tpgen_plan_destroy(tpgen_plan *plan) { delete plan; }
 
 tpgen_status tpgen_prime_paths(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options *opt,

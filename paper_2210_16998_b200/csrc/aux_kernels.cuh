@@ -606,6 +606,47 @@ __global__ void tp_len_kernel(TpArgs A) {
     }
 }
 
+// Flat prefix / suffix walk tables from the two walk trees: vertex v's prefix is
+// the BFS-tree path entry -> v (written backwards along parents), its suffix the
+// greedy walk v -> exit along next (R15).
+__global__ void tp_flat_kernel(int32_t n, const int32_t *parent, const int32_t *next, const int64_t *pre_off,
+                               const int32_t *pre_len, const int64_t *suf_off, const int32_t *suf_len,
+                               int32_t *pre_flat, int32_t *suf_flat) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int32_t pl = pre_len[v];
+        if (pl > 0) {
+            int32_t *d = pre_flat + pre_off[v];
+            int32_t c = v;
+            for (int32_t j = pl - 1; j >= 0; j--) {
+                d[j] = c;
+                c = __ldg(parent + c);
+            }
+        }
+        const int32_t sl = suf_len[v];
+        if (sl > 0) {
+            int32_t *d = suf_flat + suf_off[v];
+            int32_t c = v;
+            for (int32_t j = 0; j < sl; j++) {
+                d[j] = c;
+                c = __ldg(next + c);
+            }
+        }
+    }
+}
+
+// Warp copy of n int32 with eight loads in flight per lane.
+__device__ __forceinline__ void warp_copy(int32_t *dst, const int32_t *src, int64_t n, int lane) {
+    int64_t j = lane;
+    for (; j + 224 < n; j += 256) {
+        int32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = __ldg(src + j + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; u++) dst[j + 32 * u] = v[u];
+    }
+    for (; j < n; j += 32) dst[j] = __ldg(src + j);
+}
+
 __global__ void tp_write_kernel(TpArgs A) {
     const int lane = threadIdx.x & 31;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -617,13 +658,11 @@ __global__ void tp_write_kernel(TpArgs A) {
         const int64_t t0 = (int64_t)A.tp_len[i];
         if (lane == 0) A.tp_off[i] = t0;
         int32_t *d = A.tp_vert + t0;
-        const int32_t *pre = A.pre_flat + A.pre_off[f];
-        for (int j = lane; j < pl; j += 32) d[j] = pre[j];
+        warp_copy(d, A.pre_flat + A.pre_off[f], pl, lane);
         d += pl;
-        for (int64_t j = lane; j < e - s; j += 32) d[j] = A.pp_vert[s + j];
+        warp_copy(d, A.pp_vert + s, e - s, lane);
         d += e - s;
-        const int32_t *suf = A.suf_flat + A.suf_off[l] + 1;
-        for (int j = lane; j < sl; j += 32) d[j] = suf[j];
+        warp_copy(d, A.suf_flat + A.suf_off[l] + 1, sl, lane);
     }
 }
 

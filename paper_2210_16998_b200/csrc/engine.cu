@@ -1089,27 +1089,43 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
         d_ppo = tmp_o.as<int64_t>();
         d_ppv = tmp_v.as<int32_t>();
     }
+    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;
+    double hprev = now_ms();
+    auto HT = [&](const char *what) {
+        if (!hdbg) return;
+        cudaStreamSynchronize(s);
+        const double t = now_ms();
+        fprintf(stderr, "[tpgen tp host] %-24s %8.3f ms\n", what, t - hprev);
+        hprev = t;
+    };
+    HT("prime paths ready");
     TpTables T;
     build_tp_tables(H, entry, exit, T);
-    // one buffer: pre_off, suf_off (int64 n each), pre_len, suf_len (int32 n each), flats
+    HT("host tables");
+    // one buffer: pre_off, suf_off (int64 n each), pre_len, suf_len, parent, next (int32 n each), flats
     const size_t nn = std::max<int32_t>(H.n, 1);
-    const size_t bytes = nn * 8 * 2 + nn * 4 * 2 + (T.pre_flat.size() + T.suf_flat.size() + 2) * 4 + 64;
+    const size_t bytes = nn * 8 * 2 + nn * 4 * 4 + (size_t)(T.pre_total + T.suf_total + 2) * 4 + 64;
     TPG_TRY(P.tp_tabs.ensure(bytes, s));
     char *b = (char *)P.tp_tabs.p;
     int64_t *d_pre_off = (int64_t *)b;
     int64_t *d_suf_off = d_pre_off + nn;
     int32_t *d_pre_len = (int32_t *)(d_suf_off + nn);
     int32_t *d_suf_len = d_pre_len + nn;
-    int32_t *d_pre_flat = d_suf_len + nn;
-    int32_t *d_suf_flat = d_pre_flat + T.pre_flat.size() + 1;
+    int32_t *d_parent = d_suf_len + nn;
+    int32_t *d_next = d_parent + nn;
+    int32_t *d_pre_flat = d_next + nn;
+    int32_t *d_suf_flat = d_pre_flat + T.pre_total + 1;
     TPG_CK(cudaMemcpyAsync(d_pre_off, T.pre_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     TPG_CK(cudaMemcpyAsync(d_suf_off, T.suf_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
     TPG_CK(cudaMemcpyAsync(d_pre_len, T.pre_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
     TPG_CK(cudaMemcpyAsync(d_suf_len, T.suf_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
-    if (!T.pre_flat.empty())
-        TPG_CK(cudaMemcpyAsync(d_pre_flat, T.pre_flat.data(), T.pre_flat.size() * 4, cudaMemcpyHostToDevice, s));
-    if (!T.suf_flat.empty())
-        TPG_CK(cudaMemcpyAsync(d_suf_flat, T.suf_flat.data(), T.suf_flat.size() * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(d_parent, T.parent.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(d_next, T.next.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    if (H.n > 0) {
+        tp_flat_kernel<<<grid_for(H.n, 128, P.num_sms * 8), 128, 0, s>>>(H.n, d_parent, d_next, d_pre_off, d_pre_len,
+                                                                          d_suf_off, d_suf_len, d_pre_flat, d_suf_flat);
+        st.gpu_launches++;
+    }
 
     DevBuf lenb;
     struct LGuard {
@@ -1147,11 +1163,13 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
             return TPGEN_ERR_UNREACHABLE;
         }
     }
+    HT("lengths + scan");
     OutOwner *ow = new OutOwner();
     ow->device = P.device;
     std::unique_ptr<OutOwner> ow_guard(ow);
     void *d_off = nullptr, *d_vert = nullptr;
     TPG_TRY(out_alloc_pair(o, ow, (size_t)(n + 1) * 8, (size_t)total * 4, &d_off, &d_vert, s));
+    HT("alloc");
     A.tp_off = (int64_t *)d_off;
     A.tp_vert = (int32_t *)d_vert;
     if (n > 0) {
@@ -1161,6 +1179,7 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
     set_last_offset_kernel<<<1, 1, 0, s>>>((int64_t *)d_off, n, (int64_t)total);
     launches++;
     TPG_CK(cudaGetLastError());
+    HT("write");
     ow_guard.release();
     TPG_TRY(finish_output(o, ow, n, (int64_t)total, (int64_t *)d_off, (int32_t *)d_vert, s, out));
     st.gpu_launches = launches;

@@ -90,9 +90,10 @@ bool completion_dp(const HostPlan &plan, const std::vector<uint64_t> &tail_cnt, 
 
 // Test-path tables (R15): lexmin-shortest walks.
 struct TpTables {
-    std::vector<int64_t> pre_off, suf_off;  // per vertex, -1 if unreachable
-    std::vector<int32_t> pre_len, suf_len;
-    std::vector<int32_t> pre_flat, suf_flat;
+    std::vector<int64_t> pre_off, suf_off;  // per vertex: offset of its walk in the flat table, -1 if none
+    std::vector<int32_t> pre_len, suf_len;  // walk lengths in vertices, -1 if none
+    std::vector<int32_t> parent, next;      // BFS-tree parent (prefix walks), greedy next hop (suffix walks)
+    int64_t pre_total = 0, suf_total = 0;   // sizes of the flat tables (built on the device)
 };
 void build_tp_tables(const HostPlan &plan, int32_t entry, int32_t exit, TpTables &tp);
 

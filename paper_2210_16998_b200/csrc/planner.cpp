@@ -307,35 +307,42 @@ bool completion_dp(const HostPlan &P, const std::vector<uint64_t> &tail_cnt, con
 }
 
 void build_tp_tables(const HostPlan &P, int32_t entry, int32_t exit, TpTables &T) {
+    // The host computes the two walk trees, O(n + m); the GPU expands them into the
+    // flat prefix / suffix tables (tp_flat_kernel) -- those are O(n * depth).
     int32_t n = P.n;
     T.pre_off.assign(n, -1);
     T.suf_off.assign(n, -1);
     T.pre_len.assign(n, -1);
     T.suf_len.assign(n, -1);
-    T.pre_flat.clear();
-    T.suf_flat.clear();
+    T.parent.assign(n, -1);
+    T.next.assign(n, -1);
     // BFS from entry, successors ascending, first discoverer becomes the parent:
     // the tree path is the lexicographically smallest minimum-hop walk.
     std::vector<int32_t> parent(n, -2), order;
     order.reserve(n);
     parent[entry] = -1;
+    T.pre_len[entry] = 1;
     order.push_back(entry);
     for (size_t h = 0; h < order.size(); h++) {
         int32_t v = order[h];
         for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) {
             int32_t w = P.st[e];
-            if (parent[w] == -2) { parent[w] = v; order.push_back(w); }
+            if (parent[w] == -2) {
+                parent[w] = v;
+                T.pre_len[w] = T.pre_len[v] + 1;
+                order.push_back(w);
+            }
         }
     }
-    std::vector<int32_t> tmp;
+    int64_t acc = 0;
     for (int32_t v = 0; v < n; v++) {
-        if (parent[v] == -2) continue;
-        tmp.clear();
-        for (int32_t c = v; c != -1; c = parent[c]) tmp.push_back(c);
-        T.pre_off[v] = (int64_t)T.pre_flat.size();
-        T.pre_len[v] = (int32_t)tmp.size();
-        T.pre_flat.insert(T.pre_flat.end(), tmp.rbegin(), tmp.rend());
+        T.parent[v] = parent[v] < 0 ? -1 : parent[v];
+        if (T.pre_len[v] > 0) {
+            T.pre_off[v] = acc;
+            acc += T.pre_len[v];
+        }
     }
+    T.pre_total = acc;
     // reverse BFS distances to exit; suffix = greedy smallest successor one hop closer
     std::vector<int32_t> dist(n, -1);
     order.clear();
@@ -348,21 +355,17 @@ void build_tp_tables(const HostPlan &P, int32_t entry, int32_t exit, TpTables &T
             if (dist[u] < 0) { dist[u] = dist[v] + 1; order.push_back(u); }
         }
     }
+    acc = 0;
     for (int32_t v = 0; v < n; v++) {
         if (dist[v] < 0) continue;
-        T.suf_off[v] = (int64_t)T.suf_flat.size();
-        int32_t cur = v, len = 1;
-        T.suf_flat.push_back(cur);
-        while (cur != exit) {
-            int32_t best = -1;
-            for (int64_t e = P.so[cur]; e < P.so[cur + 1]; e++)  // successors ascending
-                if (dist[P.st[e]] == dist[cur] - 1) { best = P.st[e]; break; }
-            cur = best;
-            T.suf_flat.push_back(cur);
-            len++;
-        }
-        T.suf_len[v] = len;
+        if (v != exit)
+            for (int64_t e = P.so[v]; e < P.so[v + 1]; e++)  // successors ascending
+                if (dist[P.st[e]] == dist[v] - 1) { T.next[v] = P.st[e]; break; }
+        T.suf_len[v] = dist[v] + 1;
+        T.suf_off[v] = acc;
+        acc += T.suf_len[v];
     }
+    T.suf_total = acc;
 }
 
 }  // namespace tpg

@@ -303,3 +303,17 @@ def test_long_paths_and_many_sccs():
         if c + 1 < 3000:
             arcs.append((b + 2, b + 3))
     _assert_same(gen.from_arcs(9000, arcs))
+
+
+def test_plan_test_paths():
+    """tpgen_plan_test_paths (the plan's graph, no re-planning) equals the oracle, with the
+    prime paths given (device) or computed by the call."""
+    for g in (gen.fig1b(), gen.config2(), gen.config4(K=30)):
+        ro, rv = oracle.prime_paths(g)
+        to, tv = oracle.test_paths(g, ro, rv, g.entry, g.exit)
+        plan = tp.Plan(g)
+        for pin in (plan.prime_paths(), None):
+            o, v = plan.test_paths(g.entry, g.exit, pin).to_numpy()
+            np.testing.assert_array_equal(o, to, err_msg=g.name)
+            np.testing.assert_array_equal(v, tv, err_msg=g.name)
+        plan.close()
