@@ -251,12 +251,37 @@ __device__ __forceinline__ uint32_t lop_merge(uint32_t mine, uint32_t other, uin
     return (mine & mask) | (other & ~mask);  // one LOP3
 }
 
+// HASH mode: a lane's path digest.  The bytes go through the lane's slice of the
+// warp's stage so that the per-vertex loop is a rolled loop (unrolled over up to
+// 64 positions with two splitmix64 chains each, the kernel outgrows the
+// instruction cache).
+template <int NPW>
+__device__ __forceinline__ void hash_path(const DevGraph &G, const uint32_t (&D)[NPW], int32_t *stage, int lane, int len,
+                                          int tot, int ga, int vb, int s0g, PathHash &acc) {
+    uint32_t *mine = reinterpret_cast<uint32_t *>(stage) + lane * NPW;
+#pragma unroll
+    for (int w = 0; w < NPW; w++)
+        if (4 * w < len) mine[w] = D[w];
+    const uint8_t *bytes = reinterpret_cast<const uint8_t *>(mine);
+    PathHash hs;
+    hs.init((uint64_t)tot);
+#pragma unroll 1
+    for (int p = 0; p < len; p++) {
+        const int loc = bytes[p];
+        hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
+    }
+    if (len < tot) hs.add(s0g);
+    acc.a += hs.a;
+    acc.b += hs.b;
+}
+
 // MIXED = false: the call has no segment items and no head blocks (e.g. a graph
 // that is one SCC), so every batch is prime paths and path continuations only.
 template <int NPW, bool HASH, bool MIXED>
 __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(ExpandArgs A) {
     constexpr int kWarps = FastCfg<NPW>::threads / 32;
-    constexpr int kStage = HASH ? 1 : 32 * FastCfg<NPW>::max_out;  // one batch of paths
+    // one batch of paths (HASH: each lane's path bytes, NPW words)
+    constexpr int kStage = HASH ? 32 * NPW : 32 * FastCfg<NPW>::max_out;
     __shared__ __align__(16) int32_t stage_all[kWarps][kStage];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int32_t *stage = stage_all[wid];
@@ -346,20 +371,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 const unsigned em = __ballot_sync(kFull, emit);
                 if (HASH) {
                     // ---- digest only: every emitting lane hashes its own path
-                    if (emit) {
-                        PathHash hs;
-                        hs.init((uint64_t)tot);
-#pragma unroll
-                        for (int p = 0; p < 4 * NPW; p++) {
-                            if (p < len) {
-                                const int loc = (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
-                                hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
-                            }
-                        }
-                        if (len < tot) hs.add(s0g);
-                        acc.a += hs.a;
-                        acc.b += hs.b;
-                    }
+                    if (emit) hash_path<NPW>(G, D, stage, lane, len, tot, ga, vb, s0g, acc);
                     int T = tot;
 #pragma unroll
                     for (int o = 16; o; o >>= 1) T += __shfl_xor_sync(kFull, T, o);
@@ -467,20 +479,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                     A.items[it] = ir;
                     dst = A.item_pool + itv;
                 }
-                if (HASH && isPP) {
-                    PathHash hs;
-                    hs.init((uint64_t)tot);
-#pragma unroll
-                    for (int p = 0; p < 4 * NPW; p++) {
-                        if (p < len) {
-                            const int loc = (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
-                            hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
-                        }
-                    }
-                    if (len < tot) hs.add(s0g);
-                    acc.a += hs.a;
-                    acc.b += hs.b;
-                }
+                if (HASH && isPP) hash_path<NPW>(G, D, stage, lane, len, tot, ga, vb, s0g, acc);
                 if (dst) {
 #pragma unroll
                     for (int p = 0; p < 4 * NPW; p++) {
