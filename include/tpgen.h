@@ -172,6 +172,15 @@ tpgen_status tpgen_plan_create(const int64_t *csr_offsets, const int32_t *csr_ta
                                const tpgen_options *opt, tpgen_plan **plan);
 tpgen_status tpgen_plan_prime_paths(tpgen_plan *plan, const tpgen_options *opt, tpgen_paths *out,
                                     tpgen_stats *stats);
+/*
+ * Five-class report of a canonical prime-path list of the plan's graph (
+ * DESIGN.md R19): counts[0..4] = complete (Start ... End, Def. 2), entry
+ * (Start into an SCC, Def. 11), exit (an SCC to End, Def. 10), internal (inside one
+ * SCC, Def. 9), transit (SCC to SCC, the class the paper's taxonomy misses).
+ * prime_paths: host or device arrays; counts: caller-owned int64[5].
+ */
+tpgen_status tpgen_plan_classify(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t start, int32_t end,
+                                 const tpgen_options *opt, int64_t counts[5]);
 /* Test paths of the plan's graph (same contract as tpgen_test_paths, no re-planning). */
 tpgen_status tpgen_plan_test_paths(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t entry, int32_t exit,
                                    const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats);

@@ -174,3 +174,37 @@ def test_paths(g, offsets: np.ndarray, vertices: np.ndarray, entry: int, exit: i
 
 def as_list(offsets: np.ndarray, vertices: np.ndarray):
     return [tuple(vertices[offsets[i]:offsets[i + 1]].tolist()) for i in range(len(offsets) - 1)]
+
+
+PP_CLASSES = ("complete", "entry", "exit", "internal", "transit")
+
+
+def pp_class(first: int, last: int, start: int, end: int, scc: np.ndarray) -> str:
+    """The paper's PP taxonomy (reading R19): complete = Start ... End
+    (Def. 2); entry = from Start into an SCC (Def. 11, P:182-186 read as
+    Start -> SCC, R7); exit = from an SCC to End (Def. 10); internal = inside one SCC
+    (Def. 9); transit = SCC -> SCC, the class Defs. 2-11 miss (R7).  A
+    path cannot leave an SCC and come back, so "inside one SCC" is scc[first] ==
+    scc[last]."""
+    if first == start and last == end:
+        return "complete"
+    if first == start:
+        return "entry"
+    if last == end:
+        return "exit"
+    if scc[first] == scc[last]:
+        return "internal"
+    return "transit"
+
+
+def pp_classes(g, offsets: np.ndarray, vertices: np.ndarray, start: int, end: int):
+    """Class of every prime path (a plain loop) and the counts per class."""
+    scc = scc_labels(g)
+    labels = []
+    for i in range(len(offsets) - 1):
+        a, b = int(offsets[i]), int(offsets[i + 1])
+        labels.append(pp_class(int(vertices[a]), int(vertices[b - 1]), start, end, scc))
+    counts = {c: 0 for c in PP_CLASSES}
+    for c in labels:
+        counts[c] += 1
+    return labels, counts

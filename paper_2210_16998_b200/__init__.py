@@ -268,6 +268,33 @@ def components(graph):
     return comp[:n], flags[:n], int(nscc.value)
 
 
+def metrics(graph) -> Dict[str, int]:
+    """Structure metrics of Table 1: Nodes, Edges, SCCs (nontrivial),
+    SccNodes, SccEdges and the cyclomatic complexity CC = E - V + 2P (P = number
+    of weakly connected components).  Host code over tpgen_components."""
+    so, st, n = _csr(graph)
+    comp, flags, _ = components(graph)
+    m = int(so[-1]) if n else 0
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(so)) if n else np.zeros(0, dtype=np.int64)
+    dst = np.asarray(st[:m], dtype=np.int64)
+    nontriv = (flags & 4) != 0
+    # weakly connected components by label propagation over the arcs (min label, to a fixpoint)
+    lab = np.arange(n, dtype=np.int64)
+    while m:
+        lo = np.minimum(lab[src], lab[dst])
+        new = lab.copy()
+        np.minimum.at(new, src, lo)
+        np.minimum.at(new, dst, lo)
+        new = new[new]
+        if np.array_equal(new, lab):
+            break
+        lab = new
+    parts = int(np.unique(lab).size) if n else 0
+    in_scc = (comp[src] == comp[dst]) & nontriv[src] if m else np.zeros(0, dtype=bool)
+    return {"nodes": n, "edges": m, "sccs": int(np.unique(comp[nontriv]).size) if n else 0,
+            "scc_nodes": int(nontriv.sum()), "scc_edges": int(in_scc.sum()), "cc": m - n + 2 * parts}
+
+
 class Plan:
     """Host plan + device-resident graph tables (``tpgen_plan_create``); ``prime_paths()``
     then runs device-only (what bench.py times as ``value``)."""
@@ -305,6 +332,17 @@ class Plan:
         _check(lib.tpgen_plan_test_paths(self._h, ctypes.byref(pin) if pin is not None else None, entry, exit,
                                          ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
         return _wrap(paths, stats, None)
+
+    def classify(self, prime: PathSet, start: int, end: int, stream=None) -> Dict[str, int]:
+        """Five-class report of a prime-path list (tpgen_plan_classify; R19)."""
+        lib = library()
+        o = _options(self.device, "device", "materialize", (0, 1), False, 0, 0, _stream_handle(self.device, stream),
+                     None)
+        keep = []
+        pin = _paths_in(prime, self.device, keep)
+        counts = (ctypes.c_int64 * 5)()
+        _check(lib.tpgen_plan_classify(self._h, ctypes.byref(pin), start, end, ctypes.byref(o), counts))
+        return dict(zip(("complete", "entry", "exit", "internal", "transit"), (int(c) for c in counts)))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

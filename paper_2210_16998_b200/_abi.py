@@ -69,6 +69,8 @@ SYMBOLS = {
     "tpgen_plan_prime_paths": (c_int, [c_void_p, POINTER(Options), POINTER(Paths), POINTER(Stats)]),
     "tpgen_plan_test_paths": (c_int, [c_void_p, POINTER(Paths), c_int32, c_int32, POINTER(Options), POINTER(Paths),
                                       POINTER(Stats)]),
+    "tpgen_plan_classify": (c_int, [c_void_p, POINTER(Paths), c_int32, c_int32, POINTER(Options),
+                                    POINTER(c_int64)]),
     "tpgen_plan_destroy": (None, [c_void_p]),
 }
 

@@ -193,6 +193,25 @@ tpgen_status tpgen_plan_test_paths(tpgen_plan *plan, const tpgen_paths *prime_pa
     return s;
 }
 
+tpgen_status tpgen_plan_classify(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t start, int32_t end,
+                                 const tpgen_options *opt, int64_t counts[5]) {
+    if (!plan || !prime_paths || !counts) return TPGEN_ERR_INVALID_ARGUMENT;
+    tpgen_options o = resolve(opt);
+    tpgen_status s = check_options(o);
+    if (s != TPGEN_OK) return s;
+    const int32_t n = plan->impl.hp.n;
+    if (start < 0 || start >= n || end < 0 || end >= n) {
+        tpg::set_error("start/end out of range");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (prime_paths->n_paths > 0 && (!prime_paths->offsets || !prime_paths->vertices)) {
+        tpg::set_error("prime_paths has NULL arrays");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    DeviceScope ds(plan->impl.device);
+    return tpg::run_classify(plan->impl, prime_paths, start, end, o, counts);
+}
+
 void tpgen_plan_destroy(tpgen_plan *plan) { delete plan; }
 
 tpgen_status tpgen_prime_paths(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options *opt,

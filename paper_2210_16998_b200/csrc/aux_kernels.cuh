@@ -634,6 +634,26 @@ __global__ void tp_flat_kernel(int32_t n, const int32_t *parent, const int32_t *
     }
 }
 
+// Class of every prime path from its end vertices (complete, entry, exit, internal,
+// transit -- DESIGN.md R19); a path cannot leave an SCC and return, so it lies in
+// one SCC iff its end vertices do.  Counts reduced per warp, one atomic each.
+__global__ void classify_kernel(const int64_t *off, const int32_t *vert, int64_t n, const int32_t *comp,
+                                int32_t start, int32_t end, unsigned long long *counts) {
+    unsigned long long c[5] = {0, 0, 0, 0, 0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = vert[off[i]], l = vert[off[i + 1] - 1];
+        const int k = (f == start) ? ((l == end) ? 0 : 1) : ((l == end) ? 2 : ((comp[f] == comp[l]) ? 3 : 4));
+#pragma unroll
+        for (int q = 0; q < 5; q++) c[q] += (k == q);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+#pragma unroll
+        for (int d = 16; d; d >>= 1) c[q] += __shfl_xor_sync(kFull, c[q], d);
+        if ((threadIdx.x & 31) == 0 && c[q]) atomicAdd(counts + q, c[q]);
+    }
+}
+
 // Warp copy of n int32 with eight loads in flight per lane.
 __device__ __forceinline__ void warp_copy(int32_t *dst, const int32_t *src, int64_t n, int lane) {
     int64_t j = lane;

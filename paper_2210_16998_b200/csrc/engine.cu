@@ -101,7 +101,7 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch};
@@ -137,6 +137,7 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     TPG_TRY(upload(P.d_scc_nout, H.scc_nout, s));
     TPG_TRY(upload(P.d_scc_pair_base, H.scc_pair_base, s));
     TPG_TRY(upload(P.d_slot_eidx, H.slot_eidx, s));
+    TPG_TRY(upload(P.d_comp, H.comp, s));
     TPG_TRY(P.d_Wc.ensure(std::max<size_t>(H.n, 1) * 8, s));
     TPG_TRY(P.d_Wv.ensure(std::max<size_t>(H.n, 1) * 8, s));
     TPG_CK(cudaMemsetAsync(P.d_Wc.p, 0, std::max<size_t>(H.n, 1) * 8, s));
@@ -1187,6 +1188,47 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
     st.total_vertices = (int64_t)total;
     st.ms_total = now_ms() - t0;
     if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
+// Five-class report (R19): every prime path is
+// complete / entry / exit / internal / transit by its end vertices and SCCs.
+tpgen_status run_classify(PlanImpl &P, const tpgen_paths *pp, int32_t start, int32_t end, const tpgen_options &o,
+                          int64_t counts[5]) {
+    cudaStream_t s = (cudaStream_t)o.stream;
+    const int64_t n = pp->n_paths;
+    for (int c = 0; c < 5; c++) counts[c] = 0;
+    if (n <= 0) return TPGEN_OK;
+    const int64_t *d_off = pp->offsets;
+    const int32_t *d_vert = pp->vertices;
+    DevBuf tmp_o, tmp_v;
+    struct BufGuard {
+        DevBuf *a, *b;
+        cudaStream_t s;
+        ~BufGuard() {
+            a->release(s);
+            b->release(s);
+        }
+    } bg{&tmp_o, &tmp_v, s};
+    if (!pp->on_device) {
+        const int64_t nv = pp->offsets[n];
+        TPG_TRY(tmp_o.ensure((size_t)(n + 1) * 8, s));
+        TPG_TRY(tmp_v.ensure((size_t)std::max<int64_t>(nv, 1) * 4, s));
+        TPG_CK(cudaMemcpyAsync(tmp_o.p, pp->offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (nv) TPG_CK(cudaMemcpyAsync(tmp_v.p, pp->vertices, (size_t)nv * 4, cudaMemcpyHostToDevice, s));
+        d_off = tmp_o.as<int64_t>();
+        d_vert = tmp_v.as<int32_t>();
+    }
+    TPG_TRY(P.ctr.ensure(32 * 8, s));
+    unsigned long long *acc = P.ctr.as<unsigned long long>() + 24;
+    TPG_CK(cudaMemsetAsync(acc, 0, 5 * 8, s));
+    classify_kernel<<<grid_for(n, 256, P.num_sms * 8), 256, 0, s>>>(d_off, d_vert, n, P.d_comp.as<int32_t>(), start,
+                                                                     end, acc);
+    TPG_CK(cudaGetLastError());
+    unsigned long long h[5];
+    TPG_CK(cudaMemcpyAsync(h, acc, 5 * 8, cudaMemcpyDeviceToHost, s));
+    TPG_CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < 5; c++) counts[c] = (int64_t)h[c];
     return TPGEN_OK;
 }
 

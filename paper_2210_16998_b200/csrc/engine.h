@@ -32,7 +32,7 @@ struct PlanImpl {
     double ms_plan = 0;
     // device tables
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
-        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase;
+        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase, d_comp;
     // DFS work queue (one slot per unit) and its per-unit results
     DevBuf qunits, qready, qcnt[kCnt], qext, qrfirst, qrcount, qchead, qgen, roots;
     DevBuf qparent, qnchild;  // donor / number of donated units, per unit
@@ -57,6 +57,8 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s);
 tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st);
 tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp, int32_t entry, int32_t exit, const tpgen_options &o,
                             tpgen_paths *out, tpgen_stats *st);
+tpgen_status run_classify(PlanImpl &P, const tpgen_paths *pp, int32_t start, int32_t end, const tpgen_options &o,
+                          int64_t counts[5]);
 void free_paths(tpgen_paths *p);
 const char *last_error();
 

@@ -118,3 +118,15 @@ def test_compute_calls_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(Exception):
         tp.prime_paths(gen.fig1b())
+
+
+def test_metrics_fig1b_and_loops():
+    """Table-1 structure metrics on the host: Fig. 1(b) has CC = 4, one SCC
+    {2,3,4,5,6,8} with 7 internal arcs; K sequential loops of N vertices: K SCCs."""
+    import paper_2210_16998_b200 as tp
+    from workloads import generators as gen
+    m = tp.metrics(gen.fig1b())
+    assert m["nodes"] == 11 and m["edges"] == 13 and m["cc"] == 4
+    assert m["sccs"] == 1 and m["scc_nodes"] == 6 and m["scc_edges"] == 7
+    m = tp.metrics(gen.k_seq_loops(3, 4))
+    assert m["sccs"] == 3 and m["cc"] == m["edges"] - m["nodes"] + 2

@@ -317,3 +317,22 @@ def test_plan_test_paths():
             np.testing.assert_array_equal(o, to, err_msg=g.name)
             np.testing.assert_array_equal(v, tv, err_msg=g.name)
         plan.close()
+
+
+def test_pp_class_report():
+    """tpgen_plan_classify (five-class report, R19) equals the oracle's per-path
+    classification, for device and host prime-path lists."""
+    rng = np.random.default_rng(3)
+    graphs = [gen.fig1b(), gen.k_seq_loops(5, 3), gen.config2(), gen.config4(K=40)]
+    graphs += [gen.random_digraph(int(rng.integers(4, 10)), 0.3, 700 + i) for i in range(10)]
+    for g in graphs:
+        start = g.entry if g.entry >= 0 else 0
+        end = g.exit if g.exit >= 0 else g.n - 1
+        ro, rv = oracle.prime_paths(g)
+        _, want = oracle.pp_classes(g, ro, rv, start, end)
+        plan = tp.Plan(g)
+        ps = plan.prime_paths()
+        assert plan.classify(ps, start, end) == want, g.name
+        host = tp.PathSet(ro, rv, len(ro) - 1, False, {})
+        assert plan.classify(host, start, end) == want, g.name
+        plan.close()

@@ -310,3 +310,26 @@ def test_fig1b_test_paths():
         assert all((a, b) in arcs for a, b in zip(t[:-1], t[1:]))
         assert any(t[i:i + len(p)] == p for i in range(len(t) - len(p) + 1))
     assert len(set(tps)) == 10
+
+
+def test_fig1b_pp_classes_match_paper():
+    """Every one of the 19 PPs gets the class the paper prints for it."""
+    rows = load_golden("fig1b_prime_paths.txt")
+    tag = {tuple(p): t for t, p in rows}
+    g = gen.fig1b()
+    off, vert = oracle.prime_paths(g)
+    labels, counts = oracle.pp_classes(g, off, vert, g.entry, g.exit)
+    for i, lab in enumerate(labels):
+        p = tuple(int(v) for v in vert[off[i]:off[i + 1]])
+        assert tag[p] == lab, (p, tag[p], lab)
+    assert counts == {"complete": 2, "entry": 2, "exit": 4, "internal": 11, "transit": 0}
+
+
+@pytest.mark.parametrize("K,N", [(1, 3), (3, 3), (4, 2), (6, 3)])
+def test_seq_loops_pp_classes(K, N):
+    """K loops in sequence (R7): 1 complete, K*N internal, K exit, K entry and
+    K(K-1)/2 SCC->SCC transit prime paths."""
+    g = gen.k_seq_loops(K, N)
+    off, vert = oracle.prime_paths(g)
+    _, counts = oracle.pp_classes(g, off, vert, g.entry, g.exit)
+    assert counts == {"complete": 1, "entry": K, "exit": K, "internal": K * N, "transit": K * (K - 1) // 2}
