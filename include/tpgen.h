@@ -61,7 +61,7 @@ typedef enum {
 } tpgen_status;
 
 enum { TPGEN_OUT_MATERIALIZE = 0, TPGEN_OUT_COUNT_HASH = 1 };
-enum { TPGEN_TP_PER_PP = 0 };
+enum { TPGEN_TP_PER_PP = 0, TPGEN_TP_GREEDY = 1 };
 
 /* Canonical flat path array (see conventions). */
 typedef struct {
@@ -87,7 +87,9 @@ typedef struct {
                                     start_hi > start_lo (e.g. one rank per independent component) */
     int64_t max_paths;         /* 0 = unlimited */
     int64_t max_extensions;    /* 0 = unlimited */
-    int32_t tp_mode;           /* TPGEN_TP_PER_PP */
+    int32_t tp_mode;           /* TPGEN_TP_PER_PP: one TP per PP, aligned; TPGEN_TP_GREEDY: greedy cover --
+                                  longest uncovered PP first (ties lexicographic), extended by the R15 walks,
+                                  every PP contained in it covered */
     int32_t compute_digest;    /* 1: fill stats->hash_lo/hi (extra pass over the output) */
     tpgen_alloc_fn device_alloc;  /* output allocator; NULL -> cudaMallocAsync */
     tpgen_free_fn device_free;

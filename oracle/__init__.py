@@ -172,6 +172,44 @@ def test_paths(g, offsets: np.ndarray, vertices: np.ndarray, entry: int, exit: i
     return np.asarray(out_off, dtype=np.int64), np.asarray(out_v, dtype=np.int32)
 
 
+def _contains(t, q) -> bool:
+    """q is a contiguous subsequence of t (plain scan)."""
+    m = len(q)
+    for i in range(len(t) - m + 1):
+        if t[i:i + m] == q:
+            return True
+    return False
+
+
+def greedy_test_paths(g, offsets: np.ndarray, vertices: np.ndarray, entry: int, exit: int
+                      ) -> Tuple[np.ndarray, np.ndarray]:
+    """Greedy test-path cover ("starts with the
+    longest PP ... extends every PP to visit initial and final nodes").
+    Prime paths in order of decreasing length, ties in canonical (lexicographic)
+    order; the first one not yet covered becomes TP = prefix ++ PP ++ suffix (the
+    R15 walks); every prime path that is a contiguous subpath of that TP is covered.
+    Plain loops with a naive containment scan -- small graphs only."""
+    pre, suf = tp_tables(g, entry, exit)
+    pps = [vertices[offsets[i]:offsets[i + 1]].tolist() for i in range(len(offsets) - 1)]
+    order = sorted(range(len(pps)), key=lambda i: (-len(pps[i]), i))
+    covered = [False] * len(pps)
+    out_off, out_v = [0], []
+    for i in order:
+        if covered[i]:
+            continue
+        p = pps[i]
+        a, b = pre[p[0]], suf[p[-1]]
+        if a is None or b is None:
+            raise ValueError(f"PP {i} endpoints unreachable from entry / to exit")
+        tp = a[:-1] + p + b[1:]
+        out_v.extend(tp)
+        out_off.append(len(out_v))
+        for j, q in enumerate(pps):
+            if not covered[j] and len(q) <= len(tp) and _contains(tp, q):
+                covered[j] = True
+    return np.asarray(out_off, dtype=np.int64), np.asarray(out_v, dtype=np.int32)
+
+
 def as_list(offsets: np.ndarray, vertices: np.ndarray):
     return [tuple(vertices[offsets[i]:offsets[i + 1]].tolist()) for i in range(len(offsets) - 1)]
 

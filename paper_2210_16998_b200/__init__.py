@@ -219,18 +219,27 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
 
 
 def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *, device: int = 0,
-               output: str = "device", stream=None) -> PathSet:
-    """One entry->exit test path per prime path (R15)."""
+               output: str = "device", stream=None, cover: str = "per_pp") -> PathSet:
+    """Entry->exit test paths (R15): one per prime path,
+    aligned with the prime-path list (cover="per_pp"), or the greedy cover -- longest
+    uncovered prime path first, every prime path contained in a TP covered (cover="greedy")."""
     lib = library()
     so, st, n = _csr(graph)
     alloc = None
     o = _options(device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(device, stream), alloc)
+    o.tp_mode = _tp_mode(cover)
     keep = []
     pin = _paths_in(prime, device, keep)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_test_paths(_p64(so), _p32(st), n, ctypes.byref(pin) if pin is not None else None, entry, exit,
                                 ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc)
+
+
+def _tp_mode(cover: str) -> int:
+    if cover not in ("per_pp", "greedy"):
+        raise ValueError("cover must be 'per_pp' or 'greedy'")
+    return 1 if cover == "greedy" else 0
 
 
 def _paths_in(prime: Optional[PathSet], device: int, keep: list):
@@ -321,11 +330,12 @@ class Plan:
         return _wrap(paths, stats, alloc, host_out)
 
     def test_paths(self, entry: int, exit: int, prime: Optional[PathSet] = None, *, output: str = "device",
-                   stream=None) -> PathSet:
+                   stream=None, cover: str = "per_pp") -> PathSet:
         """Test paths of the plan's graph (tpgen_plan_test_paths): no re-planning per call."""
         lib = library()
         o = _options(self.device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(self.device, stream),
                      None)
+        o.tp_mode = _tp_mode(cover)
         keep = []
         pin = _paths_in(prime, self.device, keep)
         paths, stats = _abi.Paths(), _abi.Stats()

@@ -26,6 +26,10 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("bad output_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
+    if (o.tp_mode != TPGEN_TP_PER_PP && o.tp_mode != TPGEN_TP_GREEDY) {
+        tpg::set_error("bad tp_mode");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
     return TPGEN_OK;
 }
 

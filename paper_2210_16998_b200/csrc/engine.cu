@@ -1103,6 +1103,44 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
     TpTables T;
     build_tp_tables(H, entry, exit, T);
     HT("host tables");
+    if (o.tp_mode == TPGEN_TP_GREEDY) {  // greedy cover: sequential, on the host (tpcover.cpp)
+        std::vector<int64_t> hoff;
+        std::vector<int32_t> hvert;
+        const int64_t *po = pp->offsets;
+        const int32_t *pv = pp->vertices;
+        if (n > 0 && pp->on_device) {
+            hoff.resize((size_t)n + 1);
+            TPG_CK(cudaMemcpyAsync(hoff.data(), pp->offsets, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, s));
+            TPG_CK(cudaStreamSynchronize(s));
+            hvert.resize((size_t)std::max<int64_t>(hoff[(size_t)n], 1));
+            TPG_CK(cudaMemcpyAsync(hvert.data(), pp->vertices, (size_t)hoff[(size_t)n] * 4, cudaMemcpyDeviceToHost, s));
+            TPG_CK(cudaStreamSynchronize(s));
+            po = hoff.data();
+            pv = hvert.data();
+        }
+        std::vector<int64_t> toff;
+        std::vector<int32_t> tvert;
+        if (!greedy_cover(H, T, entry, exit, po, pv, n, toff, tvert)) {
+            set_error("a prime path's first vertex is unreachable from entry or its last cannot reach exit");
+            return TPGEN_ERR_UNREACHABLE;
+        }
+        const int64_t ntp = (int64_t)toff.size() - 1, nv = (int64_t)tvert.size();
+        OutOwner *ow = new OutOwner();
+        ow->device = P.device;
+        std::unique_ptr<OutOwner> ow_guard(ow);
+        void *d_off = nullptr, *d_vert = nullptr;
+        TPG_TRY(out_alloc_pair(o, ow, (size_t)(ntp + 1) * 8, (size_t)nv * 4, &d_off, &d_vert, s));
+        TPG_CK(cudaMemcpyAsync(d_off, toff.data(), (size_t)(ntp + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (nv) TPG_CK(cudaMemcpyAsync(d_vert, tvert.data(), (size_t)nv * 4, cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        ow_guard.release();
+        TPG_TRY(finish_output(o, ow, ntp, nv, (int64_t *)d_off, (int32_t *)d_vert, s, out));
+        st.n_paths = ntp;
+        st.total_vertices = nv;
+        st.ms_total = now_ms() - t0;
+        if (stp) *stp = st;
+        return TPGEN_OK;
+    }
     // one buffer: pre_off, suf_off (int64 n each), pre_len, suf_len, parent, next (int32 n each), flats
     const size_t nn = std::max<int32_t>(H.n, 1);
     const size_t bytes = nn * 8 * 2 + nn * 4 * 4 + (size_t)(T.pre_total + T.suf_total + 2) * 4 + 64;

@@ -96,6 +96,10 @@ struct TpTables {
     int64_t pre_total = 0, suf_total = 0;   // sizes of the flat tables (built on the device)
 };
 void build_tp_tables(const HostPlan &plan, int32_t entry, int32_t exit, TpTables &tp);
+// Greedy test-path cover (tpcover.cpp) of a canonical prime-path list in host memory;
+// false if a prime path's end vertices cannot be reached from entry / reach exit.
+bool greedy_cover(const HostPlan &H, const TpTables &T, int32_t entry, int32_t exit, const int64_t *off,
+                  const int32_t *vert, int64_t n, std::vector<int64_t> &tp_off, std::vector<int32_t> &tp_vert);
 
 void set_error(const std::string &msg);
 

@@ -336,3 +336,19 @@ def test_pp_class_report():
         host = tp.PathSet(ro, rv, len(ro) - 1, False, {})
         assert plan.classify(host, start, end) == want, g.name
         plan.close()
+
+
+def test_greedy_test_path_cover():
+    """TPGEN_TP_GREEDY (host greedy cover with linear-time marking) equals the oracle's
+    plain greedy cover (naive containment scans), element by element."""
+    for g in (gen.fig1b(), gen.config2(), gen.k_seq_loops(4, 3), gen.k_nested_if(5), gen.config4(K=12)):
+        ro, rv = oracle.prime_paths(g)
+        to, tv = oracle.greedy_test_paths(g, ro, rv, g.entry, g.exit)
+        o, v = tp.test_paths(g, g.entry, g.exit, cover="greedy").to_numpy()
+        np.testing.assert_array_equal(o, to, err_msg=g.name)
+        np.testing.assert_array_equal(v, tv, err_msg=g.name)
+        plan = tp.Plan(g)
+        o2, v2 = plan.test_paths(g.entry, g.exit, plan.prime_paths(), cover="greedy").to_numpy()
+        np.testing.assert_array_equal(o2, to, err_msg=g.name)
+        np.testing.assert_array_equal(v2, tv, err_msg=g.name)
+        plan.close()

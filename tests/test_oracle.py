@@ -333,3 +333,46 @@ def test_seq_loops_pp_classes(K, N):
     off, vert = oracle.prime_paths(g)
     _, counts = oracle.pp_classes(g, off, vert, g.entry, g.exit)
     assert counts == {"complete": 1, "entry": K, "exit": K, "internal": K * N, "transit": K * (K - 1) // 2}
+
+
+def _check_greedy_cover(g):
+    off, vert = oracle.prime_paths(g)
+    pps = oracle.as_list(off, vert)
+    to, tv = oracle.greedy_test_paths(g, off, vert, g.entry, g.exit)
+    tps = oracle.as_list(to, tv)
+    succ = {v: set(g.succ(v).tolist()) for v in range(g.n)}
+    for t in tps:  # entry -> exit walks along arcs
+        assert t[0] == g.entry and t[-1] == g.exit
+        assert all(b in succ[a] for a, b in zip(t, t[1:]))
+    for q in pps:  # every prime path is covered
+        assert any(oracle._contains(list(t), list(q)) for t in tps), q
+    # the seeds: the longest uncovered PP at each step, in order; never more TPs than PPs
+    assert len(tps) <= len(pps)
+    return pps, tps
+
+
+def test_greedy_cover_fig1b():
+    """Fig. 1(b): every PP covered by entry->exit walks; the first TP extends the first
+    (lexicographically) of the longest PPs, <Start,1,2,3,5,6,8> (length 7), and
+    also covers the exit PP <3,5,6,8,2,9,End>; fewer TPs than the 19 per-PP ones."""
+    pps, tps = _check_greedy_cover(gen.fig1b())
+    assert tps[0] == (0, 1, 2, 3, 5, 6, 8, 2, 9, 10)
+    assert len(tps) < len(pps)
+
+
+def test_greedy_cover_dag_is_identity():
+    """In a DAG with one source and one sink every PP is a complete Start->End path
+    (P:604): each is its own TP, in length-then-lexicographic order."""
+    for K in (3, 5):
+        g = gen.k_seq_if(K)
+        off, vert = oracle.prime_paths(g)
+        to, tv = oracle.greedy_test_paths(g, off, vert, g.entry, g.exit)
+        pps = oracle.as_list(off, vert)
+        tps = oracle.as_list(to, tv)
+        assert sorted(tps) == sorted(pps)
+        assert [len(t) for t in tps] == sorted((len(p) for p in pps), reverse=True)
+
+
+def test_greedy_cover_invariants():
+    for g in (gen.config2(), gen.k_seq_loops(3, 3), gen.k_nested_if(4)):
+        _check_greedy_cover(g)

@@ -24,7 +24,7 @@ import paper_2210_16998_b200 as tp  # noqa: E402
 from workloads import generators as gen  # noqa: E402
 
 
-def run(name, g, steps, warmup, with_tp=True):
+def run(name, g, steps, warmup, with_tp=True, greedy=True):
     plan = tp.Plan(g)
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
@@ -48,7 +48,6 @@ def run(name, g, steps, warmup, with_tp=True):
     tp_ms = float(np.median([r[1] for r in rec]))
     st, tst = rec[-1][2], rec[-1][3]
     out_b = 4.0 * st["total_vertices"] + 8.0 * (st["n_paths"] + 1)
-    plan.close()
     res = {
         "workload": name, "n_vertices": g.n, "n_sccs": st["n_scc"], "max_scc": st["max_scc"],
         "prime_paths": st["n_paths"], "cross_scc": st["n_cross"], "output_vertices": st["total_vertices"],
@@ -56,11 +55,28 @@ def run(name, g, steps, warmup, with_tp=True):
         "stitch_ms": float(np.median([r[2]["ms_stitch"] for r in rec])),
         "pp_output_gbs": out_b / (pp_ms * 1e-3) / 1e9,
     }
+    if with_tp and greedy:
+        gt = []
+        for _ in range(max(1, steps // 2)):
+            ps = plan.prime_paths()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            gs = plan.test_paths(g.entry, g.exit, ps, cover="greedy")
+            e1.record(stream)
+            torch.cuda.synchronize()
+            gt.append(e0.elapsed_time(e1))
+            res_g = gs.stats
+            del ps, gs
+        res["greedy_ms"] = float(np.median(gt))
+        res["greedy_test_paths"] = res_g["n_paths"]
+        res["greedy_vertices"] = res_g["total_vertices"]
     if tst is not None:
         tp_b = 4.0 * tst["total_vertices"] + 8.0 * (tst["n_paths"] + 1)
         res.update({"tp_ms": tp_ms, "test_path_vertices": tst["total_vertices"],
                     "tp_output_gbs": tp_b / (tp_ms * 1e-3) / 1e9,
                     "note": "median of steps; tp_ms = Plan.test_paths (host walk trees + device tables and writer)"})
+    plan.close()
     return res
 
 
