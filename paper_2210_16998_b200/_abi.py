@@ -82,8 +82,17 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is None:
         if not os.path.exists(path):
-            raise ImportError(f"libtpgen.so not found at {path}; run __graft_entry__.build() "
-                              "(python paper_2210_16998_b200/build.py)")
+            # build the CUDA library in-tree (nvcc, sm_100a) -- never a fallback: if nvcc
+            # fails the import fails
+            import sys
+
+            from . import build as _build
+
+            sys.stderr.write(f"[tpgen] {path} missing: building it with nvcc (sm_100a)\n")
+            try:
+                _build.build()
+            except Exception as e:  # noqa: BLE001
+                raise ImportError(f"libtpgen.so not found at {path} and the nvcc build failed: {e}") from e
         lib = ctypes.CDLL(path)
         for name, (res, args) in SYMBOLS.items():
             fn = getattr(lib, name)
