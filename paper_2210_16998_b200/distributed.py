@@ -1,0 +1,70 @@
+"""Multi-GPU prime paths: one process per GPU over torch.distributed.
+
+Every rank enumerates the prime paths whose first vertex lies in its start-vertex
+shard (``tpgen_options.shard_rank / shard_count``: contiguous ranges balanced by
+the planner's cost estimates).  The per-start trees are independent and a
+shard's output is a contiguous block of the global canonical list, so the only
+exchange is one all_gather of five words per rank (SURVEY §8(e) C1 + C2): the
+block's global prime-path and vertex offsets, the totals, and the
+order-independent digest.  Results stay where they were computed (no C4 gather:
+config 5's output is ~200 GB).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional, Tuple
+
+from . import PathSet, prime_paths
+
+_MASK64 = (1 << 64) - 1
+
+
+@dataclass
+class ShardResult:
+    paths: PathSet          # this rank's contiguous block of the global canonical list
+    pp_base: int            # global index of its first prime path
+    vertex_base: int        # global offset of its first vertex
+    n_paths: int            # totals over all ranks
+    total_vertices: int
+    n_extensions: int
+    digest: Tuple[int, int]  # set digest of the whole list (sum mod 2^64 of the ranks' digests)
+
+
+def _signed(u: int) -> int:
+    u &= _MASK64
+    return u - (1 << 64) if u >= (1 << 63) else u
+
+
+def sharded_prime_paths(graph, group=None, *, device: Optional[int] = None, mode: str = "materialize",
+                        digest: bool = True, compute: Optional[Callable[[int, int], PathSet]] = None
+                        ) -> ShardResult:
+    """This rank's prime paths plus their place in the global list.
+
+    ``compute(rank, world)`` replaces the GPU call (a test seam: the gloo tests run
+    the collective logic on CPU with the oracle's shards)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if compute is None:
+        dev = torch.cuda.current_device() if device is None else device
+        ps = prime_paths(graph, device=dev, shard=(rank, world), mode=mode, digest=digest)
+    else:
+        ps = compute(rank, world)
+    st = ps.stats
+    words = [int(st["n_paths"]), int(st["total_vertices"]), int(st["n_extensions"]),
+             _signed(int(st.get("hash_lo", 0))), _signed(int(st.get("hash_hi", 0)))]
+    on_gpu = dist.get_backend(group) == "nccl"
+    t = torch.tensor(words, dtype=torch.int64, device="cuda" if on_gpu else "cpu")
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    rows = [[int(x) for x in r.cpu().tolist()] for r in out]
+    return ShardResult(
+        paths=ps,
+        pp_base=sum(r[0] for r in rows[:rank]),
+        vertex_base=sum(r[1] for r in rows[:rank]),
+        n_paths=sum(r[0] for r in rows),
+        total_vertices=sum(r[1] for r in rows),
+        n_extensions=sum(r[2] for r in rows),
+        digest=(sum(r[3] for r in rows) & _MASK64, sum(r[4] for r in rows) & _MASK64),
+    )

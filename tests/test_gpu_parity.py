@@ -352,3 +352,32 @@ def test_greedy_test_path_cover():
         np.testing.assert_array_equal(o2, to, err_msg=g.name)
         np.testing.assert_array_equal(v2, tv, err_msg=g.name)
         plan.close()
+
+
+def test_sharded_prime_paths_nccl_single_rank():
+    """The distributed helper on the real path (NCCL, world size 1 on cuda:0): the block
+    is the whole list, totals and digest match the oracle."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_16998_b200.distributed import sharded_prime_paths
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        g = gen.config2()
+        res = sharded_prime_paths(g)
+        ro, rv = oracle.prime_paths(g)
+        o, v = res.paths.to_numpy()
+        np.testing.assert_array_equal(o, ro)
+        np.testing.assert_array_equal(v, rv)
+        assert res.pp_base == 0 and res.vertex_base == 0 and res.n_paths == len(ro) - 1
+        assert res.digest == oracle.digest(ro, rv)
+    finally:
+        dist.destroy_process_group()

@@ -106,3 +106,70 @@ def test_two_rank_gloo_shards_and_reduce():
     assert (lo, hi) == oracle.digest(off, vert)
     # each copy contributes the same block (weak scaling: equal work per rank)
     assert len(res["blocks"][0][1]) == len(res["blocks"][1][1])
+
+
+def _worker_sharded(rank: int, world: int, port: int, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2210_16998_b200 import PathSet
+    from paper_2210_16998_b200.distributed import sharded_prime_paths
+    from workloads import generators as gen
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = gen.config2()
+        cut = [0, 30, g.n]  # stand-in for the planner's cost-balanced shard boundaries
+
+        def compute(r, w):  # the oracle's block for this rank's start-vertex range
+            off, vert = oracle.prime_paths(g, v_lo=cut[r], v_hi=cut[r + 1])
+            lo, hi = oracle.digest(off, vert)
+            st = {"n_paths": len(off) - 1, "total_vertices": int(off[-1]),
+                  "n_extensions": oracle.ext_count(g, v_lo=cut[r], v_hi=cut[r + 1]), "hash_lo": lo, "hash_hi": hi}
+            return PathSet(off, vert, len(off) - 1, False, st)
+
+        res = sharded_prime_paths(g, compute=compute)
+        if rank == 1:
+            q.put(dict(pp_base=res.pp_base, vertex_base=res.vertex_base, n_paths=res.n_paths,
+                       total_vertices=res.total_vertices, n_extensions=res.n_extensions, digest=res.digest,
+                       local=(res.paths.offsets.tolist(), res.paths.vertices.tolist())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_prime_paths_gloo():
+    """paper_2210_16998_b200.distributed: the one all_gather gives each rank the global
+    offsets of its block, the totals and the set digest of the whole list."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    from workloads import generators as gen
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sharded, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = gen.config2()
+    off, vert = oracle.prime_paths(g)
+    lo_off, lo_vert = res["local"]
+    a = res["pp_base"]
+    # rank 1's block sits at its global offsets in the whole canonical list
+    assert np.array_equal(np.asarray(lo_off, dtype=np.int64) + res["vertex_base"], off[a:a + len(lo_off)])
+    assert np.array_equal(np.asarray(lo_vert, dtype=np.int32), vert[res["vertex_base"]:int(off[-1])])
+    assert res["n_paths"] == len(off) - 1 and res["total_vertices"] == int(off[-1])
+    assert res["n_extensions"] == oracle.ext_count(g)
+    assert tuple(res["digest"]) == oracle.digest(off, vert)
