@@ -129,6 +129,11 @@ __device__ __forceinline__ int lds_u8(uint32_t a) {
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
+__device__ __forceinline__ int lds_u32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ void sts_u8(uint32_t a, int v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -327,6 +332,96 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
     return ev;
 }
 
+// ---------------------------------------------------------------- lean step
+// LEAN kernels (engine.cu picks them): prime-path mode only, 32-bit masks, and
+// no vertex of the call has an arc leaving its SCC -- so there are no head,
+// tail or transit events and a node's children are exactly the bits of
+// succ(u) & (~M | {s}) in ascending local (= global) id, the bit of s being the
+// closing arc (Alg. 4 l.4-6).  The lane keeps the untried children
+// of its current node in L.sin and those of every ancestor in a shared-memory
+// stack rem[level] (one 32-bit word per level, [level][lane] so the lanes of a
+// warp never share a bank): a pop is two independent shared loads, a push two
+// shared stores and one slot-table load, with no next-child search.
+__device__ __forceinline__ uint32_t lane_rem(uint32_t rp, int l) { return (uint32_t)lds_u32(rp + ((uint32_t)l << 7)); }
+
+// Own event of a node reached by pushing w (c = its children, Mp = the mask before w):
+// internal prime path iff succ(w) within {v2..vk} (c == 0: no child, no closure)
+// and pred(s) within {v1..v(k-1)} (Def. 1 / Def. 9; R3).
+__device__ __forceinline__ int lean_node_event(uint32_t c, uint32_t ps, uint32_t Mp, int l, bool emit) {
+    return (emit && c == 0u && (ps & ~Mp) == 0u) ? (EV_PP | ((l + 1) << 8)) : 0;
+}
+
+template <bool TS>
+__device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, Lane<uint32_t> &L, uint32_t mp, uint32_t rp,
+                                         uint32_t &ext) {
+    const bool pop = L.sin == 0u;
+    const bool fin = pop && L.l == L.r;  // the unit's subtree is exhausted
+    if (pop && !fin) {                   // back to the parent and its untried children
+        const int u = lds_u8(mp + pidx(L.l));
+        L.l -= 1;
+        L.sin = lane_rem(rp, L.l);
+        L.M &= ~(1u << u);
+        L.base = min(L.base, L.l + 1);  // the record decoder's known prefix shortens
+    }
+    if (fin) L.done = true;
+    int ev = 0;
+    if (!fin && L.sin != 0u) {
+        const int w = __ffs(L.sin) - 1;
+        L.sin &= L.sin - 1u;
+        if (L.emit) ext++;
+        if (w == L.s) {  // cycle closure: always prime (Alg. 4 l.4-6)
+            ev = L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
+        } else {
+            sts_u32(rp + ((uint32_t)L.l << 7), L.sin);
+            sts_u8(mp + pidx(L.l + 1), w);
+            const uint32_t Mp = L.M;
+            L.M |= 1u << w;
+            L.l += 1;
+            L.sin = tab.template sin<uint32_t>(L.vb + w) & (~L.M | L.sbit);
+            ev = lean_node_event(L.sin, L.ps, Mp, L.l, L.emit);
+        }
+    }
+    return ev;
+}
+
+// Donation for LEAN lanes: the untried children of the shallowest level j0 in
+// [r, l] that has any (rem[j0], or L.sin when j0 == l), as units in ascending id.
+template <bool TS, bool WRITE>
+__device__ int lean_donate(const Lane<uint32_t> &L, uint32_t mp, uint32_t rp, int uscc, int &j0, Unit<1> *out) {
+    if (!WRITE) {
+        for (int j = L.r; j <= L.l; j++) {
+            const uint32_t c = (j == L.l) ? L.sin : lane_rem(rp, j);
+            if (c) {
+                j0 = j;
+                return __popc(c);
+            }
+        }
+        return 0;
+    }
+    uint32_t c = (j0 == L.l) ? L.sin : lane_rem(rp, j0);
+    uint32_t M = L.M;  // the mask of path[0..j0]
+    for (int j = j0 + 1; j <= L.l; j++) M &= ~(1u << lds_u8(mp + pidx(j)));
+    int n = 0;
+    while (c) {
+        const int w = __ffs(c) - 1;
+        c &= c - 1u;
+        const int kind = (w == L.s) ? K_CLOSURE : K_NODE;
+        Unit<1> &U = out[n];
+        uint32_t *pw = reinterpret_cast<uint32_t *>(U.path);
+        for (int q = 0; q <= (j0 >> 2); q++) pw[q] = (uint32_t)lds_u32(mp + (q << 7));
+        uint64_t Mu = M;
+        if (kind == K_NODE) {
+            U.path[j0 + 1] = (uint8_t)w;
+            Mu |= 1ull << w;
+        }
+        U.M[0] = Mu;
+        const int depth = (kind == K_NODE) ? j0 + 1 : j0;
+        *reinterpret_cast<int4 *>(&U.scc) = make_int4(uscc, -1, 0, depth | (kind << 8));
+        n++;
+    }
+    return n;
+}
+
 template <class T>
 struct DfsTraits {
     static constexpr int W = MT<T>::W;
@@ -358,11 +453,6 @@ __device__ __forceinline__ void st_relaxed(unsigned int *p, unsigned int v) {
 __device__ __forceinline__ unsigned int ld_relaxed(const unsigned int *p) {
     unsigned int v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ int lds_u32(uint32_t a) {
-    int v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
 
@@ -440,16 +530,21 @@ __device__ int lane_donate(const DevGraph &G, const TabView<MT<T>::W, TS> &tab, 
 // (children of the piece in the unit forest).  The kernel ends when every
 // pushed unit has finished (done == tail; both live in one 64-bit word so a
 // single load gives a consistent snapshot).
-template <class T, bool TS>
+template <class T, bool TS, bool LEAN>
 __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
     using O = MT<T>;
     constexpr int W = O::W;
     constexpr int WARPS = DfsTraits<T>::warps;
-    __shared__ __align__(16) uint8_t spath[WARPS * 64 * W * 32 + 128];  // + a spare row (path_bytes)
+    static_assert(!LEAN || MT<T>::BITS == 32, "LEAN kernels use 32-bit masks");
+    constexpr int PLEV = LEAN ? 32 : 64 * W;  // path levels per lane
+    __shared__ __align__(16) uint8_t spath[WARPS * PLEV * 32 + 128];  // + a spare row (path_bytes)
+    __shared__ __align__(16) uint32_t srem[LEAN ? WARPS * 32 * 32 : 1];  // LEAN: rem[level][lane] per warp
     extern __shared__ __align__(16) uint8_t stab[];  // slot table copy (TS)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t mp;  // this lane's column of the shared path array (opaque: not recomputed in the loop)
-    asm volatile("mov.b32 %0, %1;" : "=r"(mp) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * 64 * W * 32) + lane * 4));
+    asm volatile("mov.b32 %0, %1;" : "=r"(mp) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * PLEV * 32) + lane * 4));
+    uint32_t rp;  // LEAN: this lane's column of the rem stack (level l at rp + 128 l)
+    asm volatile("mov.b32 %0, %1;" : "=r"(rp) : "r"((uint32_t)__cvta_generic_to_shared(srem + (LEAN ? wid * 32 * 32 : 0)) + (LEAN ? lane * 4 : 0)));
     const DevGraph &G = A.G;
     TabView<W, TS> tab;
     if (TS) {
@@ -602,7 +697,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                 A.rfirst[slot] = (int64_t)(R.cur - A.chunks) + R.fill;  // global record index
                 R.count = 0;
                 // the unit's root event (no step is counted for it)
-                if (kind == K_NODE) {
+                bool lean_root = false;
+                if constexpr (LEAN) {  // the root's children; its own event
+                    if (kind == K_NODE) {
+                        L.sin = tab.template sin<T>(L.vb + u) & (~L.M | L.sbit);
+                        if (depth > 0 && L.emit) ext++;
+                        ev = lean_node_event(L.sin, L.ps, L.M & ~O::bit(u), depth, L.emit);
+                        lean_root = true;
+                    }
+                }
+                if (lean_root) {
+                } else if (kind == K_NODE) {
                     load_slot(tab, L, u);
                     if (depth > 0 && L.emit) ext++;
                     ev = node_event(L, u);
@@ -691,7 +796,11 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
 #pragma unroll 1
         for (int t = 0; t < kStepsPerIter; t++) {
             if (L.active && !L.done && !(fresh && ev != 0)) {
-                ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
+                if constexpr (LEAN) {
+                    ev = lean_step<TS>(tab, L, mp, rp, ext);
+                } else {
+                    ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
+                }
                 L.steps++;
             }
 
@@ -708,11 +817,11 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
                     nb -= kRecBytes;
                 }
                 // HEAD / TRANSIT carry their out-arc in an R_ARG record written directly before them
-                if (ty == EV_HEAD || ty == EV_TRANSIT) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
+                if (!LEAN && (ty == EV_HEAD || ty == EV_TRANSIT)) rec_put(A, R, (uint64_t)R_ARG | ((uint64_t)(uint32_t)e << 32));
                 rec_put(A, R, (uint64_t)ty | (uint64_t)(ev & EV_CLO) | ((uint64_t)L.base << 4) | ((uint64_t)nb << 13) |
                                   (path_bytes(mp, L.base) << 16));
                 L.base = L.l + 1;
-                if (ty == EV_PP) {
+                if (LEAN || ty == EV_PP) {
                     c_pp += 1;
                     c_vert += len;
                 } else if (ty == EV_HEAD) {
@@ -747,14 +856,17 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         if (feed && L.active && !L.done && (L.steps - last_split >= A.split_min || ugen < kEagerGens)) {
             // backlog of queued, unclaimed units below the low-water mark: donate the shallowest siblings
             int j0 = -1;
-            const int m = lane_donate<T, TS, false>(G, tab, L, mp, uscc, j0, nullptr);
+            int m;
+            if constexpr (LEAN) m = lean_donate<TS, false>(L, mp, rp, uscc, j0, nullptr);
+            else m = lane_donate<T, TS, false>(G, tab, L, mp, uscc, j0, nullptr);
             if (m > 0) {
                 const unsigned long long base = atomicAdd(A.qtd, (unsigned long long)m << 32) >> 32;
                 const unsigned long long b = base;  // a block is named by its first slot
                 if (base + m > A.qcap) {
                     atomicOr(A.overflow, 4u);
                 } else {
-                    lane_donate<T, TS, true>(G, tab, L, mp, uscc, j0, units + base);
+                    if constexpr (LEAN) lean_donate<TS, true>(L, mp, rp, uscc, j0, units + base);
+                    else lane_donate<T, TS, true>(G, tab, L, mp, uscc, j0, units + base);
                     for (int i = 0; i < m; i++) {
                         A.gen[base + i] = ugen + 1;
                         A.child_head[base + i] = -1;

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <type_traits>
 
 #include "aux_kernels.cuh"
 #include "expand.cuh"
@@ -122,6 +123,9 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
         const int32_t meta[4] = {H.slot_gid[i], H.slot_out_off[i], H.slot_out_cnt[i], H.slot_flags[i]};
         memcpy(r + 16 * W, meta, 16);
     }
+    P.any_exit = false;  // no arc leaves any SCC: the LEAN DFS applies
+    for (int32_t i = 0; i < H.n; i++)
+        if (H.slot_out_cnt[i] > 0 || (H.slot_flags[i] & (F_EXIT | F_ENTRY))) P.any_exit = true;
     TPG_TRY(upload(P.d_slots, packed, s));
     TPG_TRY(upload(P.d_slot_gid, H.slot_gid, s));
     std::vector<int32_t> gbase(std::max(H.n_scc, 1), -1);
@@ -399,6 +403,7 @@ struct Timer {
 };
 
 constexpr size_t kSmemTabMax = 40 * 1024;  // slot tables up to this size are staged in shared memory
+constexpr size_t kSmemTabLean = 20 * 1024;  // LEAN kernels: 3 blocks x (16.5 KB paths + 32 KB rem stacks + table) per SM
 
 __global__ void set_t0_kernel(unsigned long long *p) {
     unsigned long long now;
@@ -549,12 +554,27 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<
         cudaEventRecord(t.a, s);
         A.n_slots = H.n;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
-        if (tab_bytes <= kSmemTabMax) {
-            TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        // LEAN: 32-bit masks, prime-path phase, no arc leaves any SCC (no head / segment
+        // events), the slot table staged in shared memory next to the rem stacks
+        const bool lean = std::is_same<T, uint32_t>::value && !seg && !P.any_exit && tab_bytes <= kSmemTabLean &&
+                          !getenv("TPGEN_NO_LEAN");
+        const int grid = P.num_sms * DfsCfg<W>::min_blocks;
+        bool launched = false;
+        if constexpr (std::is_same<T, uint32_t>::value) {
+            if (lean) {
+                TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kSmemTabLean));
+                dfs_kernel<T, true, true><<<grid, DfsCfg<W>::threads, tab_bytes, s>>>(A);
+                launched = true;
+            }
+        }
+        if (launched) {
+        } else if (tab_bytes <= kSmemTabMax) {
+            TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kSmemTabMax));
-            dfs_kernel<T, true><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, tab_bytes, s>>>(A);
+            dfs_kernel<T, true, false><<<grid, DfsCfg<W>::threads, tab_bytes, s>>>(A);
         } else {
-            dfs_kernel<T, false><<<P.num_sms * DfsCfg<W>::min_blocks, DfsCfg<W>::threads, 0, s>>>(A);
+            dfs_kernel<T, false, false><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
         }
         cudaEventRecord(t.b, s);
         launches++;

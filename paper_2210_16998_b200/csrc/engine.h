@@ -48,6 +48,7 @@ struct PlanImpl {
     DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     DevBuf sscratch;  // cross-SCC range writer: per-warp level stacks
     bool overflow = false;
+    bool any_exit = true;  // some arc leaves its SCC (head / segment events possible; no LEAN DFS)
     ~PlanImpl();
     std::vector<DevBuf *> all_bufs();
 };
