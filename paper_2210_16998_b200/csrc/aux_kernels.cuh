@@ -176,6 +176,23 @@ __global__ void lin_roots_kernel(LinArgs A) {
     }
 }
 
+// Many roots: tmp[c][j] = subtree total of root j; scanned device-wide, then scattered.
+__global__ void lin_roots_gather_kernel(LinArgs A, uint64_t *tmp) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < A.n_roots; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = A.roots[j];
+#pragma unroll
+        for (int c = 0; c < C_NUM; c++) tmp[(int64_t)c * A.n_roots + j] = A.sub[c][r];
+    }
+}
+__global__ void lin_roots_scatter_kernel(LinArgs A, const uint64_t *tmp) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < A.n_roots; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = A.roots[j];
+#pragma unroll
+        for (int c = 0; c < C_NUM; c++) A.node[r].v[c] = tmp[(int64_t)c * A.n_roots + j];
+        A.node[r].jmp = -1;
+    }
+}
+
 // Children placed after their parent's own output, newest block first.
 __global__ void lin_rel_kernel(LinArgs A) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -551,6 +568,10 @@ __global__ void stitch_hash_kernel(StitchArgs A, unsigned long long *acc) {
         atomicAdd(acc, (unsigned long long)sa);
         atomicAdd(acc + 1, (unsigned long long)sb);
     }
+}
+
+__global__ void fill_u32_kernel(uint32_t *p, uint32_t v, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
 __global__ void set_last_offset_kernel(int64_t *off, int64_t n_paths, int64_t total) { off[n_paths] = total; }

@@ -105,7 +105,7 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch};
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
@@ -123,6 +123,9 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
         const int32_t meta[4] = {H.slot_gid[i], H.slot_out_off[i], H.slot_out_cnt[i], H.slot_flags[i]};
         memcpy(r + 16 * W, meta, 16);
     }
+    P.presplit_lo = P.presplit_hi = -1;  // a new graph: the cached pre-split roots are stale
+    P.presplit_n = 0;
+    P.presplit_roots_n = -1;
     P.any_exit = false;  // no arc leaves any SCC: the LEAN DFS applies
     for (int32_t i = 0; i < H.n; i++)
         if (H.slot_out_cnt[i] > 0 || (H.slot_flags[i] & (F_EXIT | F_ENTRY))) P.any_exit = true;
@@ -459,26 +462,116 @@ static tpgen_status grow_queue(PlanImpl &P, uint64_t used, uint64_t cap, cudaStr
     return TPGEN_OK;
 }
 
+template <int W>
+struct RootSpan {  // the roots of one DFS phase (host memory; not owned)
+    const Unit<W> *p = nullptr;
+    size_t n = 0;
+    RootSpan() = default;
+    RootSpan(const std::vector<Unit<W>> &v) : p(v.data()), n(v.size()) {}
+    RootSpan(const Unit<W> *q, size_t k) : p(q), n(k) {}
+    size_t size() const { return n; }
+    const Unit<W> *data() const { return p; }
+};
+
 // Writes `roots` into the queue at slots [qbase, qbase + roots.size()).
 template <int W>
-static tpgen_status put_roots(PlanImpl &P, const std::vector<Unit<W>> &roots, uint64_t qbase, cudaStream_t s) {
+static tpgen_status put_roots(PlanImpl &P, RootSpan<W> roots, uint64_t qbase, cudaStream_t s) {
     const size_t n = roots.size();
     if (!n) return TPGEN_OK;
-    TPG_CK(cudaMemcpyAsync(P.qunits.as<Unit<W>>() + qbase, roots.data(), n * sizeof(Unit<W>), cudaMemcpyHostToDevice,
-                           s));
-    std::vector<uint32_t> ones(n, 1u);
-    TPG_CK(cudaMemcpyAsync(P.qready.as<uint32_t>() + qbase, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
+    if (P.presplit_active && P.presplit_n == (int64_t)n) {  // the plan's cached pre-split roots (device copy)
+        TPG_CK(cudaMemcpyAsync(P.qunits.as<Unit<W>>() + qbase, P.presplit_dev.p, n * sizeof(Unit<W>),
+                               cudaMemcpyDeviceToDevice, s));
+        fill_u32_kernel<<<grid_for((int64_t)n, 256, P.num_sms * 4), 256, 0, s>>>(P.qready.as<uint32_t>() + qbase, 1u,
+                                                                                 (int64_t)n);
+    } else {
+        TPG_CK(cudaMemcpyAsync(P.qunits.as<Unit<W>>() + qbase, roots.data(), n * sizeof(Unit<W>),
+                               cudaMemcpyHostToDevice, s));
+        std::vector<uint32_t> ones(n, 1u);
+        TPG_CK(cudaMemcpyAsync(P.qready.as<uint32_t>() + qbase, ones.data(), n * 4, cudaMemcpyHostToDevice, s));
+    }
     TPG_CK(cudaMemsetAsync(P.qgen.as<int32_t>() + qbase, 0, n * 4, s));
     TPG_CK(cudaMemsetAsync(P.qchead.as<int64_t>() + qbase, 0xff, n * 8, s));  // -1: no donated block
     TPG_CK(cudaMemsetAsync(P.qparent.as<int64_t>() + qbase, 0xff, n * 8, s));  // -1: a root
     return TPGEN_OK;
 }
 
+// Host pre-split of the per-start tries for LEAN calls (no arc leaves any SCC):
+// the top levels of every start vertex's trie are expanded on the host, in DFS
+// preorder, into the units a donation would have produced -- K_NODE units at the
+// cut depth or at leaves, K_CLOSURE units for cycle closures above the cut --
+// so the persistent kernel starts with enough units for every lane instead of
+// one per start vertex (the ramp-up of repeated donations).  Nodes above the cut
+// that have children carry no event (an internal prime path has no child,
+// Def. 1 / R3) but each is one extension (E_canon): counted here.  Cached per
+// plan and start range; the device copy is reused by every call.
+template <int W>
+static void presplit_roots(PlanImpl &P, int32_t lo, int32_t hi, int64_t target, std::vector<Unit<W>> &units,
+                           std::vector<int32_t> &gids, uint64_t &ext) {
+    const HostPlan &H = P.hp;
+    units.clear();
+    gids.clear();
+    ext = 0;
+    for (int32_t v = lo; v < hi; v++) {
+        const int32_t slot = H.v_slot[v], c = H.comp[v];
+        Unit<W> u;
+        memset(&u, 0, sizeof(u));
+        const int loc = slot - H.scc_vbase[c];
+        u.M[0] = 1ull << loc;
+        u.scc = c;
+        u.e = -1;
+        u.kind = K_NODE;
+        u.path[0] = (uint8_t)loc;
+        units.push_back(u);
+        gids.push_back(v);
+    }
+    for (int depth = 0; depth < 30 && (int64_t)units.size() < target; depth++) {
+        size_t grown = 0;  // size of the next level (bounded: a dense SCC can branch 31 ways)
+        for (const Unit<W> &u : units) {
+            const uint64_t ch = H.sin[(size_t)(H.scc_vbase[u.scc] + u.path[u.depth]) * W] & (~u.M[0] | (1ull << u.path[0]));
+            grown += (u.kind == K_NODE && u.depth == depth && ch) ? (size_t)__builtin_popcountll(ch) : 1;
+        }
+        if ((int64_t)grown > 16 * target) break;
+        std::vector<Unit<W>> next;
+        std::vector<int32_t> ngid;
+        next.reserve(grown);
+        bool grew = false;
+        for (size_t i = 0; i < units.size(); i++) {
+            const Unit<W> &u = units[i];
+            const int vb = H.scc_vbase[u.scc], s0 = u.path[0], x = u.path[u.depth];
+            const uint64_t sbit = 1ull << s0;
+            const uint64_t ch = H.sin[(size_t)(vb + x) * W] & (~u.M[0] | sbit);
+            if (u.kind != K_NODE || u.depth != depth || ch == 0) {  // terminal: kept as it is
+                next.push_back(u);
+                ngid.push_back(gids[i]);
+                continue;
+            }
+            grew = true;
+            if (depth > 0) ext++;  // this node's own extension (its unit is replaced by its children)
+            for (uint64_t cc = ch; cc; cc &= cc - 1) {
+                const int w = __builtin_ctzll(cc);
+                Unit<W> k = u;
+                if (w == s0) {
+                    k.kind = K_CLOSURE;
+                } else {
+                    k.depth = (uint8_t)(depth + 1);
+                    k.path[depth + 1] = (uint8_t)w;
+                    k.M[0] |= 1ull << w;
+                }
+                next.push_back(k);
+                ngid.push_back(gids[i]);
+            }
+        }
+        units.swap(next);
+        gids.swap(ngid);
+        if (!grew) break;
+    }
+}
+
 // One phase of the persistent DFS (seg = SCC-entry starts, else prime-path
 // starts) over the roots already placed at [qbase, qbase + nroots).  Retried
 // with a larger record pool or queue if either overflows.  Returns the new tail.
 template <class T>
-static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, const std::vector<Unit<MT<T>::W>> &roots, int seg,
+static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W> roots, int seg,
                               uint64_t qbase, cudaStream_t s, tpgen_stats &st, int64_t &launches, double &ms_dfs,
                               uint64_t &tail_out) {
     constexpr int W = MT<T>::W;
@@ -759,6 +852,32 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
                                                 P.chunk_hwm * 3 / 2), s));
     }
 
+    // LEAN calls: pre-split tries (cached per plan and start range)
+    uint64_t presplit_ext = 0;
+    bool presplit_ext_used = false;
+    RootSpan<W> pp_span(pp_roots);
+    const std::vector<int32_t> *pp_gid_p = &pp_gid;
+    if (std::is_same<T, uint32_t>::value && seg_roots.empty() && !P.any_exit &&
+        (size_t)H.n * sizeof(Slot<W>) <= kSmemTabLean && !getenv("TPGEN_NO_LEAN") && !getenv("TPGEN_NO_PRESPLIT")) {
+        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_dev.p)) {
+            const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
+            std::vector<Unit<W>> units;
+            presplit_roots<W>(P, lo, hi, lanes / 4, units, P.presplit_gid, P.presplit_ext);
+            P.presplit_host.assign(reinterpret_cast<const uint8_t *>(units.data()),
+                                   reinterpret_cast<const uint8_t *>(units.data() + units.size()));
+            P.presplit_n = (int64_t)units.size();
+            P.presplit_roots_n = -1;  // the cached root table belongs to the previous range
+            TPG_TRY(upload(P.presplit_dev, P.presplit_host, s));
+            P.presplit_lo = lo;
+            P.presplit_hi = hi;
+        }
+        pp_span = RootSpan<W>(reinterpret_cast<const Unit<W> *>(P.presplit_host.data()), (size_t)P.presplit_n);
+        pp_gid_p = &P.presplit_gid;
+        presplit_ext = P.presplit_ext;
+        P.presplit_active = true;
+        presplit_ext_used = true;
+    }
+
     double ms_dfs = 0;
     uint64_t tail_seg = 0, tail = 0;
     // ---- segment phase (SCC entries) -> completion DP
@@ -781,7 +900,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     }
     // ---- prime-path phase
     HT("before pp phase");
-    TPG_TRY(dfs_phase<T>(P, G, pp_roots, 0, tail_seg, s, st, launches, ms_dfs, tail));
+    {
+        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail);
+        P.presplit_active = false;
+        if (r != TPGEN_OK) return r;
+    }
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
@@ -793,8 +916,12 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     // ---- canonical order: roots by global id, then preorder of the split forest
     std::vector<int64_t> root_order;
     std::vector<int32_t> root_gid;
-    root_order.reserve(seg_roots.size() + pp_roots.size());
-    {
+    const std::vector<int32_t> &pp_gid_r = *pp_gid_p;
+    const bool roots_cached = presplit_ext_used && P.presplit_roots_n == (int64_t)pp_gid_r.size() &&
+                              P.presplit_roots_tail == (int64_t)tail_seg;
+    if (!roots_cached) {
+        root_order.reserve(seg_roots.size() + pp_gid_r.size());
+        const std::vector<int32_t> &pp_gid = pp_gid_r;
         size_t a = 0, b = 0;
         while (a < seg_gid.size() || b < pp_gid.size()) {
             if (b >= pp_gid.size() || (a < seg_gid.size() && seg_gid[a] < pp_gid[b])) {
@@ -806,16 +933,26 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             }
         }
     }
-    const int64_t n_roots = (int64_t)root_order.size();
+    const int64_t n_roots = roots_cached ? P.presplit_roots_n : (int64_t)root_order.size();
     const size_t nu1 = (size_t)std::max<int64_t>(nu, 1);
     // scratch: sub[C_NUM] | acc[C_NUM] | node ping | node pong
     TPG_TRY(P.offs.ensure(nu1 * (16 * C_NUM + 2 * sizeof(LinNode)) + 256, s));
-    TPG_TRY(P.roots.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
-    if (n_roots) {
-        TPG_CK(cudaMemcpyAsync(P.roots.p, root_order.data(), n_roots * 8, cudaMemcpyHostToDevice, s));
-        TPG_CK(cudaMemcpyAsync(P.roots.as<char>() + n_roots * 8, root_gid.data(), n_roots * 4, cudaMemcpyHostToDevice,
-                               s));
+    // root table (canonical root order + start gids); the pre-split roots' table is uploaded once per plan
+    DevBuf &rbuf = presplit_ext_used ? P.presplit_roots : P.roots;
+    if (!roots_cached) {
+        TPG_TRY(rbuf.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
+        if (n_roots) {
+            TPG_CK(cudaMemcpyAsync(rbuf.p, root_order.data(), n_roots * 8, cudaMemcpyHostToDevice, s));
+            TPG_CK(cudaMemcpyAsync(rbuf.as<char>() + n_roots * 8, root_gid.data(), n_roots * 4,
+                                   cudaMemcpyHostToDevice, s));
+        }
+        if (presplit_ext_used) {
+            P.presplit_roots_n = n_roots;
+            P.presplit_roots_tail = (int64_t)tail_seg;
+        }
     }
+    const int64_t *roots_d = rbuf.as<int64_t>();
+    const int32_t *rgid_d = reinterpret_cast<const int32_t *>(rbuf.as<char>() + n_roots * 8);
     uint64_t *sub[C_NUM];
     unsigned long long *ctr = P.ctr.as<unsigned long long>();
     uint64_t *tot_d = reinterpret_cast<uint64_t *>(ctr + 8);
@@ -837,7 +974,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     LA.blk_count = P.blk_count.as<int32_t>();
     LA.blk_next = P.blk_next.as<int64_t>();
     LA.n = nu;
-    LA.roots = P.roots.as<int64_t>();
+    LA.roots = roots_d;
     LA.n_roots = n_roots;
     LA.totals = tot_d;
     const LinNode *off = node[0];  // final canonical offsets
@@ -847,7 +984,19 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         const int lg = grid_for(nu, 256, P.num_sms * 8);
         TPG_CK(cudaMemsetAsync(LA.acc[0], 0, (size_t)C_NUM * nu1 * 8, s));
         lin_up_flow_kernel<<<lg, 256, 0, s>>>(LA);
-        lin_roots_kernel<<<1, kScanThreads, 0, s>>>(LA);
+        if (n_roots <= 4 * kScanThreads) {
+            lin_roots_kernel<<<1, kScanThreads, 0, s>>>(LA);
+        } else {  // many roots (pre-split tries): gather, device-wide scan, scatter
+            TPG_TRY(P.rscan.ensure((size_t)C_NUM * n_roots * 8, s));
+            uint64_t *ra[C_NUM];
+            for (int c = 0; c < C_NUM; c++) ra[c] = P.rscan.as<uint64_t>() + (size_t)c * n_roots;
+            const int rg = grid_for(n_roots, 256, P.num_sms * 8);
+            lin_roots_gather_kernel<<<rg, 256, 0, s>>>(LA, P.rscan.as<uint64_t>());
+            TPG_TRY(scan_multi(P, ra, C_NUM, n_roots, nullptr, s, launches));
+            lin_roots_scatter_kernel<<<rg, 256, 0, s>>>(LA, P.rscan.as<uint64_t>());
+            TPG_CK(cudaMemcpyAsync(tot_d, P.scan_tot.p, C_NUM * 8, cudaMemcpyDeviceToDevice, s));
+            launches += 2;
+        }
         lin_rel_kernel<<<lg, 256, 0, s>>>(LA);
         launches += 3;
         // rounds: after r rounds a unit has summed its 2^r nearest ancestors' relative offsets
@@ -870,7 +1019,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         st.ms_linearize = lms;
     }
     const int64_t n_pp = (int64_t)tot[C_PP], n_vert = (int64_t)tot[C_VERT];
-    st.n_extensions = (int64_t)tot[C_NUM];
+    st.n_extensions = (int64_t)(tot[C_NUM] + presplit_ext);
     st.n_heads = (int64_t)tot[C_HEADS];
     st.n_segments = (int64_t)tot[C_ITEMS];
     if ((o.max_paths > 0 && n_pp > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
@@ -963,7 +1112,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             TPG_TRY(scan_multi(P, ia, 2, n_items, nullptr, s, launches));
         }
         item_bounds_kernel<<<grid_for(n_roots, 256, 4096), 256, 0, s>>>(
-            P.roots.as<int64_t>(), reinterpret_cast<const int32_t *>(P.roots.as<char>() + n_roots * 8), n_roots,
+            roots_d, rgid_d, n_roots,
             off, sub[C_ITEMS], P.ibeg.as<int64_t>(), P.iend.as<int64_t>());
         launches++;
         StitchArgs SA;

@@ -48,7 +48,17 @@ struct PlanImpl {
     DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     DevBuf sscratch;  // cross-SCC range writer: per-warp level stacks
     bool overflow = false;
-    bool any_exit = true;  // some arc leaves its SCC (head / segment events possible; no LEAN DFS)
+    bool any_exit = true;
+    // LEAN pre-split roots (host copy, device copy, their start gids and the extensions above the cut)
+    std::vector<uint8_t> presplit_host;
+    std::vector<int32_t> presplit_gid;
+    DevBuf presplit_dev;
+    int64_t presplit_n = 0;
+    uint64_t presplit_ext = 0;
+    int32_t presplit_lo = -1, presplit_hi = -1;
+    bool presplit_active = false;
+    DevBuf presplit_roots, rscan;  // pre-split root table (cached); root-scan scratch
+    int64_t presplit_roots_n = -1, presplit_roots_tail = -1;  // the running PP phase's roots are the cached pre-split units  // some arc leaves its SCC (head / segment events possible; no LEAN DFS)
     ~PlanImpl();
     std::vector<DevBuf *> all_bufs();
 };

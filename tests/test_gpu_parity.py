@@ -133,6 +133,37 @@ def test_shards_concatenate_to_whole():
     np.testing.assert_array_equal(np.asarray(cat_o), ro)
 
 
+@pytest.mark.parametrize("env", [{}, {"TPGEN_NO_PRESPLIT": "1"}, {"TPGEN_NO_LEAN": "1"}],
+                         ids=["lean+presplit", "lean", "generic"])
+def test_dfs_kernel_variants(env, monkeypatch):
+    """Graphs where no arc leaves an SCC take the LEAN DFS (rem-mask stacks) with host
+    pre-split roots; the same graphs through the generic kernel must agree."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for n, d, seed in [(12, 3, 1), (16, 3, 2), (20, 3, 3), (31, 2, 4), (2, 1, 1)]:
+        _assert_same(gen.dense_scc(n, d, seed))
+    _assert_same(gen.disjoint_union([gen.dense_scc(10, 3, s) for s in range(6)], name="sccs6"))
+    _assert_same(gen.disjoint_union([gen.dense_scc(8, 2, 1), gen.random_digraph(1, 0.0, 1)], name="scc+isolated"))
+
+
+def test_lean_plan_shards_reuse_presplit_cache():
+    """One Plan, several start ranges: the pre-split roots are cached per range."""
+    g = gen.disjoint_union([gen.dense_scc(14, 3, s) for s in range(3)], name="lean_shards")
+    ro, rv = oracle.prime_paths(g)
+    plan = tp.Plan(g)
+    for _ in range(2):
+        verts, n_ext = [], 0
+        for r in range(3):
+            ps = plan.prime_paths(shard=(r, 3), digest=True)
+            verts.append(ps.to_numpy()[1])
+            n_ext += ps.stats["n_extensions"]
+        np.testing.assert_array_equal(np.concatenate(verts), rv)
+        assert n_ext == oracle.ext_count(g)
+        o, v = plan.prime_paths().to_numpy()
+        np.testing.assert_array_equal(o, ro)
+        np.testing.assert_array_equal(v, rv)
+
+
 def test_host_output_and_plan_reuse():
     g = gen.config2()
     ro, rv = oracle.prime_paths(g)
