@@ -113,7 +113,7 @@ enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAI
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
 constexpr int kStepsPerIter = 16;// DFS steps per pass of the persistent loop
-constexpr int kEagerGens = 4;    // donation generations that split without waiting split_min steps
+constexpr int kEagerGens = 4;    // donation generations that split without waiting split_min steps (default)
 
 // Event codes inside the DFS: type in bits 0-2, closure flag bit 3, path length in bits 8+.
 constexpr int EV_CLO = 8;
@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         // hot: every claim, push and completion is an atomic on them); it publishes its
         // snapshot in shared memory, where the other warps read it.
         bool feed = false;
+        uint32_t split_need = A.split_min;  // steps a unit runs before it may donate
         {
             bool have = false;
             unsigned long long td = 0, hd = 0;
@@ -638,7 +639,10 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
             if (have) {
                 qdone = ((td >> 32) == (td & 0xffffffffull)) || ((ov & 6u) != 0u);
                 // donate when the backlog of queued, unclaimed units is below the low-water mark
-                feed = (long long)(td >> 32) - (long long)hd < (long long)A.low_water;
+                const long long backlog = (long long)(td >> 32) - (long long)hd;
+                feed = backlog < (long long)A.low_water;
+                // many lanes waiting for work (the end game): split after few steps
+                if (backlog < -(long long)A.starve_lanes) split_need = A.split_min_starve;
             }
         }
         // ---------------- waiting lanes: start the unit once written, or stop when all work is done
@@ -853,7 +857,7 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_block
         // ---------------- donate on demand (feed: set by this iteration's queue snapshot)
         // (the first generations split at once: the walk starts from one unit per start
         // vertex and every lane of the GPU needs work)
-        if (feed && L.active && !L.done && (L.steps - last_split >= A.split_min || ugen < kEagerGens)) {
+        if (feed && L.active && !L.done && (L.steps - last_split >= split_need || ugen < A.eager_gens)) {
             // backlog of queued, unclaimed units below the low-water mark: donate the shallowest siblings
             int j0 = -1;
             int m;

@@ -634,8 +634,11 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.chunks = P.chunks.as<uint64_t>();
         A.chunk_next = qc + 48;
         A.chunk_cap = plim;  // (the sink chunk is chunk plim: inside the allocation)
-        A.split_min = P.split_min;
-        if (const char *ev = getenv("TPGEN_SPLIT_MIN")) A.split_min = (uint32_t)atoi(ev);  // tuning knob
+        // pre-split roots already give every lane work: no eager generations, longer units
+        A.split_min = P.presplit_active ? P.split_min_presplit : P.split_min;
+        A.eager_gens = P.presplit_active ? 1 : kEagerGens;
+        if (const char *ev = getenv("TPGEN_SPLIT_MIN")) A.split_min = (uint32_t)atoi(ev);  // tuning knobs
+        if (const char *ev = getenv("TPGEN_EAGER_GENS")) A.eager_gens = atoi(ev);
         A.dbg = nullptr;
         if (getenv("TPGEN_DEBUG")) {
             TPG_TRY(P.dbgbuf.ensure(160 * 8, s));
@@ -644,6 +647,12 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
             set_t0_kernel<<<1, 1, 0, s>>>(A.dbg + 7);
         }
         A.low_water = (uint32_t)std::max<int64_t>(64, lanes / 8);
+        if (const char *ev = getenv("TPGEN_LOW_WATER")) A.low_water = (uint32_t)atoi(ev);  // tuning knob
+        // end game (more than half the lanes waiting): donate after fewer steps
+        A.split_min_starve = P.presplit_active ? 96u : P.split_min;
+        A.starve_lanes = (int32_t)(lanes / 2);
+        if (const char *ev = getenv("TPGEN_SPLIT_STARVE")) A.split_min_starve = (uint32_t)atoi(ev);
+        if (const char *ev = getenv("TPGEN_STARVE_LANES")) A.starve_lanes = atoi(ev);
         cudaEventRecord(t.a, s);
         A.n_slots = H.n;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);

@@ -45,6 +45,7 @@ struct PlanImpl {
     uint64_t q_hwm = 0;           // most queue slots any call of this plan used
     int maxgen = 0;               // deepest split generation so far in this call
     uint32_t split_min = 32;      // steps between two donations of a unit
+    uint32_t split_min_presplit = 1024;  // ... when the phase starts from pre-split roots (measured sweep, config 3)
     DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     DevBuf sscratch;  // cross-SCC range writer: per-warp level stacks
     bool overflow = false;

@@ -186,6 +186,9 @@ struct DfsArgs {
     unsigned long long chunk_cap;
     uint32_t split_min;       // steps a unit runs before it may be split
     uint32_t low_water;       // split when fewer queued units than this are waiting to be claimed
+    int32_t eager_gens;       // donation generations that split at once (the ramp-up from one root per start)
+    uint32_t split_min_starve;  // ... split_min while more than starve_lanes lanes wait for work
+    int32_t starve_lanes;
     unsigned long long *dbg;  // TPGEN_KERNEL_DEBUG builds: iterations, idle iterations, lane-steps, donations
     int n_slots;              // slot table size (copied to shared memory by the TS kernels)
 };
