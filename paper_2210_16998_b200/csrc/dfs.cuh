@@ -342,6 +342,9 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
 // stack rem[level] (one 32-bit word per level, [level][lane] so the lanes of a
 // warp never share a bank): a pop is two independent shared loads, a push two
 // shared stores and one slot-table load, with no next-child search.
+#ifndef LEAN_POPS
+#define LEAN_POPS 2  // levels a LEAN step may pop (measured: 1 -> 2 saves 5 % of the DFS)
+#endif
 __device__ __forceinline__ uint32_t lane_rem(uint32_t rp, int l) { return (uint32_t)lds_u32(rp + ((uint32_t)l << 7)); }
 
 // Own event of a node reached by pushing w (c = its children, Mp = the mask before w):
@@ -362,6 +365,16 @@ __device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, Lane<uint32_
         L.sin = lane_rem(rp, L.l);
         L.M &= ~(1u << u);
         L.base = min(L.base, L.l + 1);  // the record decoder's known prefix shortens
+#pragma unroll
+        for (int x = 1; x < LEAN_POPS; x++) {  // exhausted ancestors: more levels in the same step
+            if (L.sin == 0u && L.l > L.r) {
+                const int u2 = lds_u8(mp + pidx(L.l));
+                L.l -= 1;
+                L.sin = lane_rem(rp, L.l);
+                L.M &= ~(1u << u2);
+                L.base = min(L.base, L.l + 1);
+            }
+        }
     }
     if (fin) L.done = true;
     int ev = 0;
