@@ -74,19 +74,34 @@ __device__ __forceinline__ Cursor unit_cursor(const ExpandArgs &A, int64_t u) {
 struct RecReader {
     const uint64_t *ch;  // current chunk
     int slot;            // next record slot in it
+    int64_t left;        // records of the unit not yet fetched
+    uint64_t link;       // the current chunk's link word, loaded when the reader entered the chunk (if the
+                         // unit continues past it), so crossing into the next chunk is one load, not two
 };
 
+__device__ __forceinline__ RecReader rec_reader(const ExpandArgs &A, int64_t rfirst, int64_t nrec) {
+    RecReader rd;
+    rd.ch = A.chunks + (rfirst & ~(int64_t)(kChunkRecs - 1));
+    rd.slot = (int)(rfirst & (kChunkRecs - 1));
+    rd.left = nrec;
+    rd.link = (rd.slot + nrec > kChunkRecs - 1) ? rd.ch[kChunkRecs - 1] : 0ull;
+    return rd;
+}
+
 __device__ __forceinline__ uint64_t fetch32(const ExpandArgs &A, RecReader &rd, int nb, int lane) {
-    // link word of a full chunk (read, but only followed when the unit has records beyond it)
-    const uint64_t *nxt = (rd.slot + nb >= kChunkRecs - 1) ? A.chunks + rd.ch[kChunkRecs - 1] * kChunkRecs : rd.ch;
+    const bool cross = rd.slot + nb >= kChunkRecs - 1;
+    // the next chunk (its address is only followed when the unit has records beyond this one)
+    const uint64_t *nxt = cross ? A.chunks + rd.link * kChunkRecs : rd.ch;
     uint64_t myrec = 0;
     if (lane < nb) {
         const int sj = rd.slot + lane;
         myrec = (sj < kChunkRecs - 1) ? rd.ch[sj] : nxt[sj - (kChunkRecs - 1)];
     }
-    if (rd.slot + nb >= kChunkRecs - 1) {
+    rd.left -= nb;
+    if (cross) {
         rd.slot = rd.slot + nb - (kChunkRecs - 1);
         rd.ch = nxt;
+        if (rd.slot + rd.left > kChunkRecs - 1) rd.link = nxt[kChunkRecs - 1];  // prefetch the next link
     } else {
         rd.slot += nb;
     }
@@ -227,7 +242,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
         const int sgid = __ldg(G.slot_gid + vb + __shfl_sync(kFull, P[0], 0));
         Cursor cu = unit_cursor(A, u);
         const int64_t nrec = A.rcount[u];
-        RecReader rd{A.chunks + (A.rfirst[u] & ~(int64_t)(kChunkRecs - 1)), (int)(A.rfirst[u] & (kChunkRecs - 1))};
+        RecReader rd = rec_reader(A, A.rfirst[u], nrec);
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
             const uint64_t myrec = fetch32(A, rd, nb, lane);
@@ -292,9 +307,23 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
     const unsigned lt_mask = (1u << lane) - 1u;
     PathHash acc{0, 0};
 
+    // the next unit's header, record range and count are loaded one unit ahead
+    int4 h_next = make_int4(0, 0, 0, 0);
+    int64_t rf_next = 0, rc_next = 0;
+    if (gw < A.n_units) {
+        h_next = *reinterpret_cast<const int4 *>(&units[gw].scc);
+        rf_next = A.rfirst[gw];
+        rc_next = A.rcount[gw];
+    }
     for (int64_t u = gw; u < A.n_units; u += nw) {
         const Unit<1> *U = units + u;
-        const int4 h = *reinterpret_cast<const int4 *>(&U->scc);
+        const int4 h = h_next;
+        const int64_t rfirst = rf_next, nrec = rc_next;
+        if (u + nw < A.n_units) {
+            h_next = *reinterpret_cast<const int4 *>(&units[u + nw].scc);
+            rf_next = A.rfirst[u + nw];
+            rc_next = A.rcount[u + nw];
+        }
         // carry = the current path as bytes (positions 0..depth valid; the others are
         // always written by a record before an emitted path reads them)
         uint32_t carry[NPW];
@@ -314,8 +343,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
         const int s0 = (int)(carry[0] & 0xff);
         const int s0g = (ga >= 0) ? ga + s0 : __ldg(G.slot_gid + vb + s0);  // global id of the start vertex
         Cursor cu = unit_cursor(A, u);
-        const int64_t nrec = A.rcount[u];
-        RecReader rd{A.chunks + (A.rfirst[u] & ~(int64_t)(kChunkRecs - 1)), (int)(A.rfirst[u] & (kChunkRecs - 1))};
+        RecReader rd = rec_reader(A, rfirst, nrec);
         // records are fetched one batch ahead: the next batch's loads overlap this batch's work
         uint64_t nextrec = (nrec > 0) ? fetch32(A, rd, (nrec < 32) ? (int)nrec : 32, lane) : 0ull;
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
