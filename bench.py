@@ -343,7 +343,7 @@ def main():
         if c5:  # count mode writes no output: only the extension part of SURVEY 8(d)'s bytes applies
             a_bytes = 2.0 * 13.0 * ext
         roofline = {
-            "bound": "alu", "kernel": ("dfs_kernel<unsigned long,TS=1>" if c5 else "dfs_kernel<unsigned int,TS=1>"),
+            "bound": "alu", "kernel": ("dfs_kernel<unsigned long,TS=1,LEAN=0>" if c5 else "dfs_kernel<unsigned int,TS=1,LEAN=1>"),
             "achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak,
             "traffic": traffic.get("dfs_kernel", {}).get("dram_bytes_per_launch"),
             "ms_per_launch": ms_dfs, "units_per_launch": ext,

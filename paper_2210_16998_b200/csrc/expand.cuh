@@ -79,29 +79,32 @@ struct RecReader {
                          // unit continues past it), so crossing into the next chunk is one load, not two
 };
 
+// PREF = false (HASH kernels, short of registers): the link word is read when the chunk is crossed.
+template <bool PREF = true>
 __device__ __forceinline__ RecReader rec_reader(const ExpandArgs &A, int64_t rfirst, int64_t nrec) {
     RecReader rd;
     rd.ch = A.chunks + (rfirst & ~(int64_t)(kChunkRecs - 1));
     rd.slot = (int)(rfirst & (kChunkRecs - 1));
     rd.left = nrec;
-    rd.link = (rd.slot + nrec > kChunkRecs - 1) ? rd.ch[kChunkRecs - 1] : 0ull;
+    rd.link = (PREF && rd.slot + nrec > kChunkRecs - 1) ? rd.ch[kChunkRecs - 1] : 0ull;
     return rd;
 }
 
+template <bool PREF = true>
 __device__ __forceinline__ uint64_t fetch32(const ExpandArgs &A, RecReader &rd, int nb, int lane) {
     const bool cross = rd.slot + nb >= kChunkRecs - 1;
     // the next chunk (its address is only followed when the unit has records beyond this one)
-    const uint64_t *nxt = cross ? A.chunks + rd.link * kChunkRecs : rd.ch;
+    const uint64_t *nxt = cross ? A.chunks + (PREF ? rd.link : rd.ch[kChunkRecs - 1]) * kChunkRecs : rd.ch;
     uint64_t myrec = 0;
     if (lane < nb) {
         const int sj = rd.slot + lane;
         myrec = (sj < kChunkRecs - 1) ? rd.ch[sj] : nxt[sj - (kChunkRecs - 1)];
     }
-    rd.left -= nb;
+    if (PREF) rd.left -= nb;
     if (cross) {
         rd.slot = rd.slot + nb - (kChunkRecs - 1);
         rd.ch = nxt;
-        if (rd.slot + rd.left > kChunkRecs - 1) rd.link = nxt[kChunkRecs - 1];  // prefetch the next link
+        if (PREF && rd.slot + rd.left > kChunkRecs - 1) rd.link = nxt[kChunkRecs - 1];  // prefetch the next link
     } else {
         rd.slot += nb;
     }
@@ -310,16 +313,25 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
     // the next unit's header, record range and count are loaded one unit ahead
     int4 h_next = make_int4(0, 0, 0, 0);
     int64_t rf_next = 0, rc_next = 0;
-    if (gw < A.n_units) {
+    if (!HASH && gw < A.n_units) {
         h_next = *reinterpret_cast<const int4 *>(&units[gw].scc);
         rf_next = A.rfirst[gw];
         rc_next = A.rcount[gw];
     }
     for (int64_t u = gw; u < A.n_units; u += nw) {
         const Unit<1> *U = units + u;
-        const int4 h = h_next;
-        const int64_t rfirst = rf_next, nrec = rc_next;
-        if (u + nw < A.n_units) {
+        int4 h;
+        int64_t rfirst, nrec;
+        if (HASH) {  // (HASH kernels: registers are scarce; the digest chain bounds them, not latency)
+            h = *reinterpret_cast<const int4 *>(&U->scc);
+            rfirst = A.rfirst[u];
+            nrec = A.rcount[u];
+        } else {
+            h = h_next;
+            rfirst = rf_next;
+            nrec = rc_next;
+        }
+        if (!HASH && u + nw < A.n_units) {
             h_next = *reinterpret_cast<const int4 *>(&units[u + nw].scc);
             rf_next = A.rfirst[u + nw];
             rc_next = A.rcount[u + nw];
@@ -343,13 +355,13 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
         const int s0 = (int)(carry[0] & 0xff);
         const int s0g = (ga >= 0) ? ga + s0 : __ldg(G.slot_gid + vb + s0);  // global id of the start vertex
         Cursor cu = unit_cursor(A, u);
-        RecReader rd = rec_reader(A, rfirst, nrec);
+        RecReader rd = rec_reader<!HASH>(A, rfirst, nrec);
         // records are fetched one batch ahead: the next batch's loads overlap this batch's work
-        uint64_t nextrec = (nrec > 0) ? fetch32(A, rd, (nrec < 32) ? (int)nrec : 32, lane) : 0ull;
+        uint64_t nextrec = (nrec > 0) ? fetch32<!HASH>(A, rd, (nrec < 32) ? (int)nrec : 32, lane) : 0ull;
         for (int64_t r0 = 0; r0 < nrec; r0 += 32) {
             const int nb = (nrec - r0 < 32) ? (int)(nrec - r0) : 32;
             const uint64_t myrec = nextrec;  // lanes >= nb: 0 = an empty R_PATH
-            if (r0 + 32 < nrec) nextrec = fetch32(A, rd, (nrec - r0 - 32 < 32) ? (int)(nrec - r0 - 32) : 32, lane);
+            if (r0 + 32 < nrec) nextrec = fetch32<!HASH>(A, rd, (nrec - r0 - 32 < 32) ? (int)(nrec - r0 - 32) : 32, lane);
             const int ty = (int)(myrec & 7);
             // ---- this lane's bytes: positions cc .. cc+n-1 of the path
             const int cc = (int)((myrec >> 4) & 0x1ff);
