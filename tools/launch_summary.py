@@ -25,7 +25,7 @@ def main():
     calls, cur = [], None
     for r in rows[1:]:
         name = r[ki]
-        if "tpg::" not in name:  # torch's own launches (the bench's L2 flush) are not part of the path
+        if "at::" in name:  # torch's own launches (the bench's L2 flush) are not part of the path
             continue
         scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[ui], 1e-6)
         ms = float(r[vi].replace(",", "")) * scale
