@@ -39,8 +39,9 @@
  *     of the number of simple paths with >= 2 vertices inside C starting at s,
  *     cycle closures included (the number of ExtendPath calls of Alg. 4,
  *     P:459-472, restricted to one SCC).  Counted by its own DFS.
- *   - Digest: per path, z = mix(seed ^ len); z = mix(z ^ v) for each vertex;
- *     set digest = sum over paths mod 2^64, two seeds.
+ *   - Digest: per path, S = sum over positions i of mix(i << 32 | v_i) and
+ *     z = mix(S ^ (seed + len)); set digest = sum over paths mod 2^64
+ *     (reading R20), two seeds.
  *   - Test paths: prefix[v] = lexicographically-first shortest
  *     walk entry -> v (BFS from entry, successors ascending, first discoverer is
  *     the parent); suffix[v] = v then repeatedly the smallest successor w with
@@ -336,10 +337,11 @@ static uint64_t mix64(uint64_t z) {
     return z;
 }
 
+/* DESIGN.md reading R20: S = sum_i mix(i << 32 | v_i), path digest = mix(S ^ (seed + len)). */
 static uint64_t path_hash(uint64_t seed, const int32_t *v, int64_t len) {
-    uint64_t z = mix64(seed ^ (uint64_t)len);
-    for (int64_t i = 0; i < len; i++) z = mix64(z ^ (uint64_t)(uint32_t)v[i]);
-    return z;
+    uint64_t S = 0;
+    for (int64_t i = 0; i < len; i++) S += mix64(((uint64_t)i << 32) | (uint64_t)(uint32_t)v[i]);
+    return mix64(S ^ (seed + (uint64_t)len));
 }
 
 void oracle_digest(int64_t n_paths, const int64_t *off, const int32_t *vert, uint64_t *out2) {

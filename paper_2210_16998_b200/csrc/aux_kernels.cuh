@@ -556,6 +556,7 @@ __global__ void stitch_hash_kernel(StitchArgs A, unsigned long long *acc) {
             x = it.y;
             kk = k2;
         }
+        hs.fin();
         sa += hs.a;
         sb += hs.b;
     }
@@ -585,6 +586,7 @@ __global__ void digest_kernel(const int64_t *off, const int32_t *vert, int64_t n
         PathHash h;
         h.init((uint64_t)(e - s));
         for (int64_t j = s; j < e; j++) h.add(__ldg(vert + j));
+        h.fin();
         a += h.a;
         b += h.b;
     }

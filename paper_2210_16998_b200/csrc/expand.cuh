@@ -145,6 +145,7 @@ __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, in
             const int loc = (pos < len) ? __shfl_sync(kFull, xq, pos & 31) : s0;
             hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
         }
+        hs.fin();
         if (lane == 0) {
             acc.a += hs.a;
             acc.b += hs.b;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
 
-    PathHash acc{0, 0};
+    PathHash acc{0, 0, 0, 0, 0};
     for (int64_t u = gw; u < A.n_units; u += nw) {
         const Unit<W> *U = units + u;
         const int4 h = *reinterpret_cast<const int4 *>(&U->scc);
@@ -283,12 +284,13 @@ __device__ __forceinline__ void hash_path(const DevGraph &G, const uint32_t (&D)
     const uint8_t *bytes = reinterpret_cast<const uint8_t *>(mine);
     PathHash hs;
     hs.init((uint64_t)tot);
-#pragma unroll 1
+#pragma unroll 2
     for (int p = 0; p < len; p++) {
         const int loc = bytes[p];
         hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
     }
     if (len < tot) hs.add(s0g);
+    hs.fin();
     acc.a += hs.a;
     acc.b += hs.b;
 }
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
-    PathHash acc{0, 0};
+    PathHash acc{0, 0, 0, 0, 0};
 
     // the next unit's header, record range and count are loaded one unit ahead
     int4 h_next = make_int4(0, 0, 0, 0);

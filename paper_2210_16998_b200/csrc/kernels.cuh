@@ -252,8 +252,10 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     return v;
 }
 
-// Digest: per path z = mix(seed ^ len), then z = mix(z ^ v)
-// for each vertex, under two seeds; the set digest is the sum over paths mod 2^64.
+// Digest (reading R20): a path v_0..v_{k-1} has the position-keyed
+// sum S = sum_i mix(i << 32 | v_i) and the two digests a = mix(S ^ (SEED_A + k)),
+// b = mix(S ^ (SEED_B + k)); the set digest is the sum over paths mod 2^64 (order
+// independent, so shards add up).  The terms of S are independent: no per-vertex chain.
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finalizer
     z ^= z >> 30;
     z *= 0xbf58476d1ce4e5b9ull;
@@ -263,14 +265,21 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finalizer
     return z;
 }
 struct PathHash {
-    uint64_t a, b;
+    uint64_t a, b;  // the path's digests after fin() (accumulators: sums of them)
+    uint64_t s;     // position-keyed vertex sum
+    uint32_t p, n;  // next position, path length
     __device__ __forceinline__ void init(uint64_t len) {
-        a = mix64(0x9E3779B97F4A7C15ull ^ len);
-        b = mix64(0xD1B54A32D192ED03ull ^ len);
+        s = 0;
+        p = 0;
+        n = (uint32_t)len;
     }
     __device__ __forceinline__ void add(int32_t v) {
-        a = mix64(a ^ (uint64_t)(uint32_t)v);
-        b = mix64(b ^ (uint64_t)(uint32_t)v);
+        s += mix64(((uint64_t)p << 32) | (uint64_t)(uint32_t)v);
+        p++;
+    }
+    __device__ __forceinline__ void fin() {
+        a = mix64(s ^ (0x9E3779B97F4A7C15ull + (uint64_t)n));
+        b = mix64(s ^ (0xD1B54A32D192ED03ull + (uint64_t)n));
     }
 };
 

@@ -376,3 +376,40 @@ def test_greedy_cover_dag_is_identity():
 def test_greedy_cover_invariants():
     for g in (gen.config2(), gen.k_seq_loops(3, 3), gen.k_nested_if(4)):
         _check_greedy_cover(g)
+
+
+# ---------------------------------------------------------------- digest (R20)
+def _flat(paths):
+    off = np.zeros(len(paths) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(p) for p in paths])
+    vert = np.asarray([v for p in paths for v in p], dtype=np.int32)
+    return off, vert
+
+
+def _dig(paths):
+    return oracle.digest(*_flat(paths))
+
+
+def test_digest_order_independent_and_additive():
+    """The set digest is a sum over paths: any order, and shards add up (mod 2^64)."""
+    rng = np.random.default_rng(3)
+    paths = [list(rng.integers(0, 50, size=int(rng.integers(1, 12)))) for _ in range(200)]
+    whole = _dig(paths)
+    perm = [paths[i] for i in rng.permutation(len(paths))]
+    assert _dig(perm) == whole
+    a, b = _dig(paths[:77]), _dig(paths[77:])
+    assert ((a[0] + b[0]) % 2**64, (a[1] + b[1]) % 2**64) == whole
+    assert _dig([]) == (0, 0)
+
+
+def test_digest_sensitive_to_vertices_order_and_binding():
+    """A changed vertex, a reorder inside a path, a rotation, and two paths that swap
+    their suffixes (same multiset of (position, vertex) pairs) all change the digest."""
+    p, q = [3, 1, 4, 1, 5], [9, 2, 6, 5, 3]
+    base = _dig([p, q])
+    assert _dig([[3, 1, 4, 1, 6], q]) != base
+    assert _dig([[1, 3, 4, 1, 5], q]) != base
+    assert _dig([[1, 4, 1, 5, 3], q]) != base
+    assert _dig([[3, 1, 6, 5, 3], [9, 2, 4, 1, 5]]) != base  # suffixes swapped at position 2
+    assert _dig([p + [7], q]) != base and _dig([p[:-1], q]) != base
+    assert _dig([p]) != _dig([p, p])  # multiplicity counts
