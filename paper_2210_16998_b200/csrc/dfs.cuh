@@ -113,6 +113,10 @@ enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAI
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
 constexpr int kStepsPerIter = 16;// DFS steps per pass of the persistent loop
+#ifndef TPGEN_LEAN_BLOCKS
+#define TPGEN_LEAN_BLOCKS 3
+#endif
+constexpr int kLeanBlocks = TPGEN_LEAN_BLOCKS;  // resident LEAN blocks per SM (4 at 64 registers: faster DFS, more units, slower step)
 constexpr int kEagerGens = 4;    // donation generations that split without waiting split_min steps (default)
 
 // Event codes inside the DFS: type in bits 0-2, closure flag bit 3, path length in bits 8+.
@@ -544,7 +548,7 @@ __device__ int lane_donate(const DevGraph &G, const TabView<MT<T>::W, TS> &tab, 
 // pushed unit has finished (done == tail; both live in one 64-bit word so a
 // single load gives a consistent snapshot).
 template <class T, bool TS, bool LEAN>
-__global__ void __launch_bounds__(DfsTraits<T>::threads, DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
+__global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
     using O = MT<T>;
     constexpr int W = O::W;
     constexpr int WARPS = DfsTraits<T>::warps;

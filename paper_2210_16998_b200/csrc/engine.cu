@@ -581,7 +581,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
     const uint64_t nroots = roots.size();
     tail_out = qbase + nroots;
     if (nroots == 0) return TPGEN_OK;
-    const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
+    const int64_t lanes = (int64_t)P.num_sms * std::max(DfsCfg<W>::min_blocks, kLeanBlocks) * DfsCfg<W>::threads;
     TPG_TRY(grow_queue<W>(P, qbase, std::max<uint64_t>(std::max<uint64_t>(qbase + nroots + 8 * (uint64_t)lanes, 1u << 21),
                                                        P.q_hwm * 3 / 2), s));
     if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
@@ -660,7 +660,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         // events), the slot table staged in shared memory next to the rem stacks
         const bool lean = std::is_same<T, uint32_t>::value && !seg && !P.any_exit && tab_bytes <= kSmemTabLean &&
                           !getenv("TPGEN_NO_LEAN");
-        const int grid = P.num_sms * DfsCfg<W>::min_blocks;
+        const int grid = P.num_sms * (lean ? kLeanBlocks : DfsCfg<W>::min_blocks);
         bool launched = false;
         if constexpr (std::is_same<T, uint32_t>::value) {
             if (lean) {
