@@ -113,6 +113,9 @@ enum RecType : int { R_PATH = 0, R_PP = EV_PP, R_HEAD = EV_HEAD, R_TAIL = EV_TAI
 constexpr int kChunkRecs = 64;  // records per chunk; the last word links to the next chunk
 constexpr int kRecBytes = 5;    // appended vertices carried by one record
 constexpr int kStepsPerIter = 16;// DFS steps per pass of the persistent loop
+#ifndef GEN_POP2
+#define GEN_POP2 1  // generic step: pop a second exhausted level in the same step
+#endif
 #ifndef TPGEN_LEAN_BLOCKS
 #define TPGEN_LEAN_BLOCKS 3
 #endif
@@ -315,6 +318,18 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
         L.base = min(L.base, L.l + 1);  // the record decoder's known prefix shortens
         if (L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold);  // rare: an exit vertex
         w = (L.ocnt > 0) ? O::BITS : O::next(L.sin, L.M, L.sbit, L.k);
+        if (GEN_POP2 && w >= O::BITS && L.ocnt == 0 && L.l > L.r) {  // the parent is exhausted too: one more level
+            const int wold2 = L.u;
+            const int parent2 = lds_u8(mp + pidx(L.l - 1));
+            L.M = O::andnot(L.M, O::bit(wold2));
+            L.l -= 1;
+            L.u = parent2;
+            load_slot(tab, L, parent2);
+            L.k = wold2 + 1;
+            L.base = min(L.base, L.l + 1);
+            if (L.ocnt > 0) L.o = count_out_le(G, L.ooff, L.ocnt, wold2);
+            w = (L.ocnt > 0) ? O::BITS : O::next(L.sin, L.M, L.sbit, L.k);
+        }
     }
     if (fin) L.done = true;
     const bool go = !fin && w < O::BITS;
