@@ -163,6 +163,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+CONFIG3_WORKLOAD = "config3: dense SCC n=22 out-degree 4 seed 1"  # the workload both arms name
+
+
 def run_reference(args):
     """The CPU oracle as it stands, single core, bounded sample per step."""
     import oracle
@@ -188,7 +191,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": g.name, "n_vertices": g.n, "sample": sample},
+        "config": {"workload": CONFIG3_WORKLOAD, "n_vertices": g.n, "parallelism": "start-vertex shards x1",
+                   "sample": sample},
         "cpu_baseline": {"value": value, "unit": "PP/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "PP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -388,7 +392,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": ("config5: 16 parallel SCCs n=56 out-degree 2 seed 5, COUNT_HASH (counts + "
                                     "digest, output not materialized)" if c5 else
-                                    "config3: dense SCC n=22 out-degree 4 seed 1" +
+                                    CONFIG3_WORKLOAD +
                                     (f" x{world} disjoint copies, one per rank" if world > 1 else "")),
                        "n_vertices": g.n, "prime_paths_per_rank": n_pp, "output_vertices_per_rank": n_vert,
                        "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",
