@@ -164,6 +164,20 @@ def test_lean_plan_shards_reuse_presplit_cache():
         np.testing.assert_array_equal(v, rv)
 
 
+def test_one_shot_plan_cache_detects_graph_change():
+    """One-shot calls reuse the previous plan only when the CSR is byte-identical."""
+    g1 = gen.dense_scc(12, 3, 1)
+    t2 = np.asarray(g1.targets).copy()
+    row = np.asarray(g1.offsets)
+    v = 0
+    succ = set(t2[row[v]:row[v + 1]].tolist())
+    t2[row[v]] = next(w for w in range(1, g1.n) if w not in succ)  # same offsets, one arc moved
+    t2[row[v]:row[v + 1]] = np.sort(t2[row[v]:row[v + 1]])
+    g2 = gen.Graph(g1.n, np.asarray(g1.offsets), t2.astype(np.int32), g1.entry, g1.exit, "moved_arc", {})
+    for g in (g1, g1, g2, g2, g1):
+        _assert_same(g)
+
+
 def test_host_output_and_plan_reuse():
     g = gen.config2()
     ro, rv = oracle.prime_paths(g)
