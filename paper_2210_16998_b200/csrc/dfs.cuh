@@ -637,7 +637,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
     __syncthreads();
     while (true) {
         int ev = 0, e = -1;
-        bool fresh = false;
         iter++;
         // ---------------- consume last iteration's queue snapshot / claim
         // The queue words are polled by warp 0 of each block only (the lines they live on are
@@ -725,7 +724,6 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
                 nchild = 0;
                 last_split = 0;
                 L.base = depth + 1;
-                fresh = true;
                 ext = 0;
                 c_pp = c_vert = 0;
                 c_it = c_itv = c_hd = c_hdv = 0;
@@ -830,16 +828,10 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
         // ---------------- kStepsPerIter DFS steps for every running lane; the queue housekeeping
         // above runs once per kStepsPerIter steps (lanes that just started emit their root event first)
 #pragma unroll 1
-        for (int t = 0; t < kStepsPerIter; t++) {
-            if (L.active && !L.done && !(fresh && ev != 0)) {
-                if constexpr (LEAN) {
-                    ev = lean_step<TS>(tab, L, mp, rp, ext);
-                } else {
-                    ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
-                }
-                L.steps++;
-            }
-
+        // (the event of a step is written at the top of the next pass of this loop; a unit
+        // that just started carries its root event into the first pass; pass kStepsPerIter
+        // only writes the last step's event)
+        for (int t = 0; t <= kStepsPerIter; t++) {
             // ---------------- event: counters + one record (lane-local)
             if (ev) {
                 const int ty = ev_type(ev);
@@ -883,8 +875,15 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
                 }
             }
             ev = 0;
-            fresh = false;
+            if (t < kStepsPerIter && L.active && !L.done) {
+                if constexpr (LEAN) {
+                    ev = lean_step<TS>(tab, L, mp, rp, ext);
+                } else {
+                    ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
+                }
+            }
         }
+        if (L.active) L.steps += kStepsPerIter;  // (approximate: only the donation policy reads it)
 
         // ---------------- donate on demand (feed: set by this iteration's queue snapshot)
         // (the first generations split at once: the walk starts from one unit per start
