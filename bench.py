@@ -223,7 +223,14 @@ def main():
                          "disjoint copies; config5: 16 parallel 56-vertex SCCs (~1.3e10 extensions), COUNT_HASH "
                          "(counts + digest; the ~200 GB output is not materialized), strong scaling by "
                          "start-vertex shards")
+    ap.add_argument("--engine", default="dfs", choices=["dfs", "frontier"],
+                    help="dfs (default): depth-first engine, full output; frontier: the level-synchronous "
+                         "frontier engine on config 3 in COUNT_HASH mode (counts + digest; DESIGN.md 6.6)")
+    ap.add_argument("--count", action="store_true",
+                    help="config 3 in COUNT_HASH mode (counts + digest, no output) with the chosen engine")
     args = ap.parse_args()
+    if args.engine == "frontier" and args.workload != "config3":
+        ap.error("--engine frontier runs config 3 (config 5 has arcs leaving its SCCs)")
     if args.impl == "reference":
         run_reference(args)
         return
@@ -241,12 +248,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
     c5 = args.workload == "config5"
+    fr = args.engine == "frontier"
+    cnt3 = (fr or args.count) and not c5  # config 3, counts + digest only
     if c5:  # one graph; rank r takes start-vertex shard r of `world` (strong scaling)
         g = gen.config5()
         kw = dict(shard=(rank, world), mode="count", digest=True)
     else:
         g, ranges = workload(world)
         kw = dict(start_range=ranges[rank])
+        if cnt3:
+            kw.update(mode="count", digest=True, engine=args.engine)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -286,7 +297,7 @@ def main():
     e2e = None
     free_b, total_b = torch.cuda.mem_get_info(dev)
     mem_used_gb = (total_b - free_b) / 1e9  # device memory held after the timed steps (pools included)
-    if not args.no_e2e and c5:  # counts + digest come back in the stats; the CSR goes up every call
+    if not args.no_e2e and (c5 or cnt3):  # counts + digest come back in the stats; the CSR goes up every call
         plan.close()  # its workspaces return to the device pool, where the e2e call's plan finds them
         h2d = int(g.offsets.nbytes + g.targets.nbytes)
         e2e_steps = max(1, min(args.steps, 3))
@@ -339,12 +350,12 @@ def main():
         except Exception:
             sm_max = 1965.0
         ms_dfs = float(np.mean([s["ms_dfs_write"] for s in stats]))
-        ms_expand = float(np.mean([s["ms_write"] for s in stats]))
+        ms_expand = max(float(np.mean([s["ms_write"] for s in stats])), 1e-9)  # 0 for the frontier engine
         ms_dev = float(np.mean([s["ms_device"] for s in stats]))
         alu_peak = ALU_LANES * sm_max * 1e6 / OPS_PER_EXT / 1e9  # Gext/s
         dfs_ach = ext / (ms_dfs * 1e-3) / 1e9
         traffic = ncu_traffic()
-        if c5:  # count mode writes no output: only the extension part of SURVEY 8(d)'s bytes applies
+        if c5 or cnt3:  # count mode writes no output: only the extension part of SURVEY 8(d)'s bytes applies
             a_bytes = 2.0 * 13.0 * ext
         roofline = {
             "bound": "alu", "kernel": ("dfs_kernel<unsigned long,TS=1,LEAN=0>" if c5 else "dfs_kernel<unsigned int,TS=1,LEAN=1>"),
@@ -371,12 +382,29 @@ def main():
             "peak_kind": peak_kind,
             "traffic_source": traffic.get("source"),
         }
-        if c5:
+        if c5 or cnt3:
             roofline["traffic"] = None  # the committed ncu summary is for config 3
             roofline["second"] = {"note": "COUNT_HASH: the writer digests each path instead of storing it",
                                   "kernel": f"expand_fast_kernel<{max(1, (int(st['max_scc']) + 3) // 4)},true>",
                                   "ms_per_launch": ms_expand, "share_of_step": ms_expand / ms_dev}
             roofline["path_hbm"]["model"] = "SURVEY 8(d): 26 B/extension (no output in COUNT_HASH mode)"
+        if fr:  # every frontier record is written once and read once: 16 B each way
+            f_bytes = 32.0 * st["n_units"]
+            f_ach = f_bytes / (ms_dfs * 1e-3) / 1e9
+            roofline = {
+                "bound": "hbm", "kernel": "frontier_level_kernel<TS=1> (all levels + root kernel)",
+                "achieved": f_ach, "peak": peak, "unit": "GB/s", "frac": f_ach / peak,
+                "traffic": traffic.get("frontier_level_kernel", {}).get("dram_bytes_per_launch"),
+                "algorithmic_bytes_per_step": f_bytes, "records_per_step": st["n_units"],
+                "ms_per_step": ms_dfs, "share_of_step": ms_dfs / ms_dev,
+                "model": "16-byte path record {mask, last, first, slot base | digest sum} written once and read "
+                         "once per record (DESIGN.md 6.6); traffic is per level launch (the levels differ)",
+                "alu_view": {"achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak},
+                "path_hbm": {"achieved": a_bytes / (ms_dev * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                             "frac": a_bytes / (ms_dev * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,
+                             "model": "SURVEY 8(d): 26 B/extension (no output in COUNT_HASH mode)"},
+                "peak_kind": peak_kind,
+            }
         out = {
             "metric": "prime_paths_per_sec",
             "value": value,
@@ -392,7 +420,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": ("config5: 16 parallel SCCs n=56 out-degree 2 seed 5, COUNT_HASH (counts + "
                                     "digest, output not materialized)" if c5 else
-                                    CONFIG3_WORKLOAD +
+                                    CONFIG3_WORKLOAD + (f", COUNT_HASH, {args.engine} engine" if cnt3 else "") +
                                     (f" x{world} disjoint copies, one per rank" if world > 1 else "")),
                        "n_vertices": g.n, "prime_paths_per_rank": n_pp, "output_vertices_per_rank": n_vert,
                        "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",

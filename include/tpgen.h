@@ -62,6 +62,8 @@ typedef enum {
 
 enum { TPGEN_OUT_MATERIALIZE = 0, TPGEN_OUT_COUNT_HASH = 1 };
 enum { TPGEN_TP_PER_PP = 0, TPGEN_TP_GREEDY = 1 };
+/* Enumeration engine (tpgen_options.engine). */
+enum { TPGEN_ENGINE_DFS = 0, TPGEN_ENGINE_FRONTIER = 1 };
 
 /* Canonical flat path array (see conventions). */
 typedef struct {
@@ -99,6 +101,17 @@ typedef struct {
                                   host_out_bytes >= 8*(n_paths+1) + 4*n_vertices, else pinned memory is
                                   allocated by the library.  The caller keeps ownership. */
     size_t host_out_bytes;
+    int32_t engine;            /* TPGEN_ENGINE_DFS (default): depth-first walk, on-chip path stacks, every
+                                  output mode.  TPGEN_ENGINE_FRONTIER: level-synchronous frontier extension
+                                  (Alg. 4 ExtendPath applied to every simple path of length l at once,
+                                  P:459-472; the north-star's level-by-level kernel): 16-byte path records
+                                  {visited mask, last, first, position-keyed digest sum} streamed through HBM,
+                                  ping-pong buffers, warp-scan compaction.  Requires output_mode =
+                                  TPGEN_OUT_COUNT_HASH (counts, E_canon and the digest; the order-free
+                                  frontier never materializes the canonical list) and a graph whose SCCs
+                                  have <= 32 vertices with no arc leaving any SCC (else
+                                  TPGEN_ERR_INVALID_ARGUMENT); a frontier larger than half the free device
+                                  memory -> TPGEN_ERR_OUT_OF_MEMORY. */
 } tpgen_options;
 
 typedef struct {

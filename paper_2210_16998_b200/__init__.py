@@ -133,7 +133,7 @@ class _TorchAllocator:
 
 def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest: bool, max_paths: int,
              max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None,
-             start_range: Optional[Tuple[int, int]] = None) -> _abi.Options:
+             start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs") -> _abi.Options:
     lib = library()
     o = _abi.Options()
     lib.tpgen_options_init(ctypes.byref(o))
@@ -147,6 +147,7 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
     o.max_paths = max_paths
     o.max_extensions = max_extensions
     o.compute_digest = 1 if digest else 0
+    o.engine = _engine(engine)
     if alloc is not None:
         o.device_alloc = alloc.alloc_fn
         o.device_free = alloc.free_fn
@@ -154,6 +155,12 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
         o.host_out = host_out.data_ptr()
         o.host_out_bytes = host_out.numel() * host_out.element_size()
     return o
+
+
+def _engine(engine: str) -> int:
+    if engine not in ("dfs", "frontier"):
+        raise ValueError(f"engine must be 'dfs' or 'frontier', not {engine!r}")
+    return _abi.ENGINE_FRONTIER if engine == "frontier" else _abi.ENGINE_DFS
 
 
 def _stream_handle(device: int, stream):
@@ -204,15 +211,18 @@ def _wrap(paths: _abi.Paths, stats: _abi.Stats, alloc: Optional[_TorchAllocator]
 def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "materialize",
                 shard: Tuple[int, int] = (0, 1), digest: bool = False, max_paths: int = 0,
                 max_extensions: int = 0, stream=None, host_out=None,
-                start_range: Optional[Tuple[int, int]] = None) -> PathSet:
+                start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs") -> PathSet:
     """All prime paths of ``graph`` (Def. 1), canonical order.
 
-    ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host)."""
+    ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host).
+    ``engine``: "dfs" (default) or "frontier" (level-synchronous, ``mode="count"`` only;
+    include/tpgen.h TPGEN_ENGINE_FRONTIER)."""
     lib = library()
+    _engine(engine)
     so, st, n = _csr(graph)
     alloc = None  # outputs come from the library's device memory pool (no Python callback while timing)
     o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
-                 alloc, host_out, start_range)
+                 alloc, host_out, start_range, engine)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_prime_paths(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc, host_out)
@@ -320,11 +330,11 @@ class Plan:
 
     def prime_paths(self, *, output: str = "device", mode: str = "materialize", shard: Tuple[int, int] = (0, 1),
                     digest: bool = False, max_paths: int = 0, stream=None, host_out=None,
-                    start_range: Optional[Tuple[int, int]] = None) -> PathSet:
+                    start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs") -> PathSet:
         lib = library()
         alloc = None
         o = _options(self.device, output, mode, shard, digest, max_paths, 0, _stream_handle(self.device, stream),
-                     alloc, host_out, start_range)
+                     alloc, host_out, start_range, engine)
         paths, stats = _abi.Paths(), _abi.Stats()
         _check(lib.tpgen_plan_prime_paths(self._h, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
         return _wrap(paths, stats, alloc, host_out)

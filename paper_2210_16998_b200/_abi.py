@@ -18,6 +18,8 @@ STATUS_NAMES = {
 }
 OUT_MATERIALIZE = 0
 OUT_COUNT_HASH = 1
+ENGINE_DFS = 0
+ENGINE_FRONTIER = 1
 
 ALLOC_FN = CFUNCTYPE(c_void_p, c_size_t, c_void_p, c_void_p)
 FREE_FN = CFUNCTYPE(None, c_void_p, c_void_p, c_void_p)
@@ -34,7 +36,8 @@ class Options(Structure):
                 ("start_lo", c_int32), ("start_hi", c_int32),
                 ("max_paths", c_int64), ("max_extensions", c_int64), ("tp_mode", c_int32),
                 ("compute_digest", c_int32), ("device_alloc", ALLOC_FN), ("device_free", FREE_FN),
-                ("alloc_ctx", c_void_p), ("host_out", c_void_p), ("host_out_bytes", c_size_t)]
+                ("alloc_ctx", c_void_p), ("host_out", c_void_p), ("host_out_bytes", c_size_t),
+                ("engine", c_int32)]
 
 
 class Stats(Structure):

@@ -32,6 +32,14 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("bad output_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
+    if (o.engine != TPGEN_ENGINE_DFS && o.engine != TPGEN_ENGINE_FRONTIER) {
+        tpg::set_error("bad engine");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (o.engine == TPGEN_ENGINE_FRONTIER && o.output_mode != TPGEN_OUT_COUNT_HASH) {
+        tpg::set_error("the frontier engine computes counts and the digest only (output_mode COUNT_HASH)");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
     if (o.tp_mode != TPGEN_TP_PER_PP && o.tp_mode != TPGEN_TP_GREEDY) {
         tpg::set_error("bad tp_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;

@@ -20,6 +20,7 @@
 
 #include "aux_kernels.cuh"
 #include "expand.cuh"
+#include "frontier.cuh"
 #include "engine.h"
 
 namespace tpg {
@@ -105,7 +106,8 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
                                &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
-                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan};
+                               &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan,
+                               &f_tab, &f_roots, &f_buf0, &f_buf1, &f_ctr};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
@@ -126,6 +128,8 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     P.presplit_lo = P.presplit_hi = -1;  // a new graph: the cached pre-split roots are stale
     P.presplit_n = 0;
     P.presplit_roots_n = -1;
+    P.f_tab_ok = false;  // frontier engine: slot table and record high-water mark belong to the old graph
+    P.f_cap_hwm = 0;
     P.any_exit = false;  // no arc leaves any SCC: the LEAN DFS applies
     for (int32_t i = 0; i < H.n; i++)
         if (H.slot_out_cnt[i] > 0 || (H.slot_flags[i] & (F_EXIT | F_ENTRY))) P.any_exit = true;
@@ -1212,7 +1216,146 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     return TPGEN_OK;
 }
 
+// ------------------------------------------------------------ frontier engine
+// TPGEN_ENGINE_FRONTIER (frontier.cuh): level-synchronous
+// extension of all paths of one length at a time; counts, E_canon and digest.
+static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    const HostPlan &H = P.hp;
+    if (H.max_scc > 32 || P.any_exit || H.n >= (1 << 22)) {
+        set_error("the frontier engine needs SCCs of <= 32 vertices and no arc leaving any SCC (use the DFS engine)");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    cudaStream_t s = (cudaStream_t)o.stream;
+    int32_t lo = 0, hi = H.n;
+    shard_range(H, o.shard_rank, o.shard_count, lo, hi);
+    if (o.start_hi > o.start_lo) {
+        lo = std::max(0, o.start_lo);
+        hi = std::min(H.n, o.start_hi);
+    }
+    st.shard_lo = lo;
+    st.shard_hi = hi;
+    st.n_scc = H.n_scc;
+    st.n_scc_nontrivial = H.n_nontrivial;
+    st.max_scc = H.max_scc;
+    st.ms_plan = P.ms_plan;
+    const int W = H.W;
+    // slot table (uploaded once per plan)
+    const int32_t n_tab = std::max(H.n, 1);
+    if (!P.f_tab_ok) {
+        std::vector<FSlot> tab(n_tab, FSlot{0, 0, 0, 0});
+        for (int32_t i = 0; i < H.n; i++)
+            tab[i] = FSlot{(uint32_t)H.sin[(size_t)i * W], (uint32_t)H.pin[(size_t)i * W], H.slot_gid[i], 0};
+        TPG_TRY(upload(P.f_tab, tab, s));
+        P.f_tab_ok = true;
+    }
+    std::vector<int32_t> roots;  // slots, then slot bases
+    roots.reserve(2 * (size_t)std::max(hi - lo, 0));
+    for (int32_t v = lo; v < hi; v++) roots.push_back(H.v_slot[v]);
+    for (int32_t v = lo; v < hi; v++) roots.push_back(H.scc_vbase[H.comp[v]]);
+    const int32_t n_roots = std::max(hi - lo, 0);
+    if (n_roots) TPG_TRY(upload(P.f_roots, roots, s));
+    const int Lmax = std::max(H.max_scc, 1);  // records exist for paths of 1..max_scc vertices
+    const size_t nctr = 8 + (size_t)Lmax + 2;
+    TPG_TRY(P.f_ctr.ensure(nctr * 8, s));
+    unsigned long long *ctr = P.f_ctr.as<unsigned long long>();
+    double est = 0;
+    for (int32_t v = lo; v < hi; v++) est += H.cost[v];
+    uint64_t cap = std::max<uint64_t>({1ull << 22, (uint64_t)(est / 4), P.f_cap_hwm + P.f_cap_hwm / 4});
+    if (const char *ev = getenv("TPGEN_FRONTIER_CAP")) cap = std::max<uint64_t>(64, atoll(ev));  // test hook: retries
+    size_t free_b = 0, total_b = 0;
+    TPG_CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t cap_max = (uint64_t)((double)(free_b + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / 16);
+    const size_t smem = (size_t)n_tab * sizeof(FSm);
+    const bool ts = smem <= 32 * 1024;
+    int per_sm = 0;  // persistent grid: every block resident
+    if (ts) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<true>, kFThreads, smem));
+    else TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<false>, kFThreads, 0));
+    const int grid = P.num_sms * std::max(per_sm, 1);
+    Timer tall;
+    std::vector<unsigned long long> h(nctr);
+    int64_t launches = 0;
+    float ms = 0;
+    for (int attempt = 0;; attempt++) {
+        cap = std::min(cap, cap_max);
+        TPG_TRY(P.f_buf0.ensure(cap * 16, s));
+        TPG_TRY(P.f_buf1.ensure(cap * 16, s));
+        ulonglong2 *buf[2] = {P.f_buf0.as<ulonglong2>(), P.f_buf1.as<ulonglong2>()};
+        TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
+        cudaEventRecord(tall.a, s);
+        FrontierArgs A;
+        A.tab = P.f_tab.as<FSlot>();
+        A.n_tab = n_tab;
+        A.cap = cap;
+        A.acc = ctr;
+        A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
+        if (n_roots) {
+            A.in = nullptr;
+            A.out = buf[0];
+            A.cnt_in = nullptr;
+            A.cnt_out = ctr + 8;
+            A.l = -1;
+            frontier_root_kernel<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
+                                                                        P.f_roots.as<int32_t>() + n_roots, n_roots);
+            launches++;
+            for (int l = 0; l < Lmax; l++) {
+                A.in = buf[l & 1];
+                A.out = buf[(l + 1) & 1];
+                A.cnt_in = ctr + 8 + l;
+                A.cnt_out = ctr + 8 + l + 1;
+                A.l = l;
+                if (ts) frontier_level_kernel<true><<<grid, kFThreads, smem, s>>>(A);
+                else frontier_level_kernel<false><<<grid, kFThreads, 0, s>>>(A);
+                launches++;
+            }
+        }
+        cudaEventRecord(tall.b, s);
+        TPG_CK(cudaGetLastError());
+        TPG_CK(cudaMemcpyAsync(h.data(), ctr, nctr * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        cudaEventElapsedTime(&ms, tall.a, tall.b);
+        uint64_t peak = 0;
+        for (int l = 0; l <= Lmax; l++) peak = std::max<uint64_t>(peak, h[8 + l]);
+        if (!(h[5] & 1u)) {
+            P.f_cap_hwm = std::max<uint64_t>(P.f_cap_hwm, peak);
+            break;
+        }
+        if (cap >= cap_max) {
+            set_error("frontier level exceeds the device memory budget (use the DFS engine)");
+            return TPGEN_ERR_OUT_OF_MEMORY;
+        }
+        cap = std::max<uint64_t>(2 * cap, peak + peak / 4);  // a truncated level under-counts the next ones
+        st.n_count_rounds = attempt + 1;
+    }
+    uint64_t recs = 0;
+    for (int l = 0; l <= Lmax; l++) recs += h[8 + l];
+    st.n_paths = (int64_t)h[0];
+    st.total_vertices = (int64_t)h[1];
+    st.n_extensions = (int64_t)h[2];
+    st.hash_lo = h[3];
+    st.hash_hi = h[4];
+    st.n_units = (int64_t)recs;  // frontier records written (all levels)
+    if ((o.max_paths > 0 && st.n_paths > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
+        set_error("result exceeds max_paths / max_extensions");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    st.ms_device = ms;
+    st.ms_count = ms;
+    st.ms_dfs_count = ms;
+    st.ms_dfs_write = ms;
+    st.gpu_launches = launches;
+    st.ms_total = now_ms() - t0;
+    if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
 tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st) {
+    if (o.engine == TPGEN_ENGINE_FRONTIER) {
+        memset(out, 0, sizeof(*out));
+        return run_frontier(P, o, st);
+    }
     if (P.hp.max_scc <= 32) return run_pp<uint32_t>(P, o, out, st);
     switch (P.hp.W) {
         case 1: return run_pp<uint64_t>(P, o, out, st);

@@ -48,6 +48,9 @@ struct PlanImpl {
     uint32_t split_min_presplit = 1024;  // ... when the phase starts from pre-split roots (measured sweep, config 3)
     DevBuf dbgbuf, qctr, scan_b, scan_tot, ctr, heads, head_pool, items, item_pool, icum, ivcum, ibeg, iend, hcomp, offs, tp_tabs;
     DevBuf sscratch;  // cross-SCC range writer: per-warp level stacks
+    DevBuf f_tab, f_roots, f_buf0, f_buf1, f_ctr;  // frontier engine: slot table, roots, ping-pong levels, counters
+    bool f_tab_ok = false;
+    uint64_t f_cap_hwm = 0;                        // frontier engine: most records any level of this plan held
     bool overflow = false;
     bool any_exit = true;
     // LEAN pre-split roots (host copy, device copy, their start gids and the extensions above the cut)

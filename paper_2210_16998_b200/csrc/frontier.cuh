@@ -1,0 +1,264 @@
+// frontier.cuh -- level-synchronous frontier extension (TPGEN_ENGINE_FRONTIER;
+// DESIGN.md §6.6).
+//
+// Alg. 4 "ExtendPath" applied to every simple path of l+1 vertices
+// at once: level l's frontier is a flat array of 16-byte path records in HBM,
+// each launch reads it once and writes level l+1's frontier once (the paper's
+// level-by-level shape, without its per-vertex path lists).  A record
+// carries what the extension and the maximality test need -- the visited mask M
+// (<= 32 SCC-local vertices), the last vertex u, the first vertex s and the SCC's
+// slot base -- plus S, the position-keyed digest sum of the path so far (R20), so
+// that a prime path's digest is finished at the moment it is recognised and no
+// path is ever re-read.  Events, as in the LEAN DFS step (R3, Def. 1):
+//   child w == s            -> cycle closure, a prime path of l+2 vertices;
+//   child w not in M        -> new path p' = p + w with untried-child mask
+//                              c' = succ(w) & (~M' | {s}); p' is an internal prime
+//                              path iff c' == 0 and pred(s) within M (= M' \ {w});
+//                              p' joins level l+1 only if c' != 0 (a record with
+//                              no child would be read for nothing).
+// Compaction: one warp-wide exclusive scan of the per-lane child counts and one
+// atomicAdd per warp on the level's record counter (the frontier's order is
+// irrelevant: counts, E_canon and the order-free digest are all sums).
+#pragma once
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace tpg {
+
+struct FSlot {        // per SCC slot (local ids ascend with global ids)
+    uint32_t sin;     // in-SCC successor bits (local)
+    uint32_t pin;     // in-SCC predecessor bits (local)
+    int32_t gid;      // global vertex id
+    int32_t pad;
+};
+
+// record key: bits 0-31 visited mask, 32-36 last (local), 37-41 first (local), 42-63 slot base
+__device__ __forceinline__ uint64_t fkey(uint32_t M, uint32_t u, uint32_t s, uint32_t vb) {
+    return (uint64_t)M | ((uint64_t)u << 32) | ((uint64_t)s << 37) | ((uint64_t)vb << 42);
+}
+
+struct FrontierArgs {
+    const FSlot *tab;
+    int32_t n_tab;
+    const ulonglong2 *in;        // level l records {key, S}
+    ulonglong2 *out;             // level l+1 records
+    const unsigned long long *cnt_in;
+    unsigned long long *cnt_out;
+    unsigned long long cap;      // records per buffer
+    unsigned long long *acc;     // [0] prime paths, [1] vertices, [2] extensions, [3] digest a, [4] digest b
+    unsigned int *overflow;
+    int32_t l;                   // input paths have l + 1 vertices
+};
+
+struct FAcc {
+    unsigned long long pp = 0, vert = 0, ext = 0, ha = 0, hb = 0;
+    __device__ __forceinline__ void emit(uint64_t S, uint32_t len) {
+        pp++;
+        vert += len;
+        ha += mix64(S ^ (0x9E3779B97F4A7C15ull + (uint64_t)len));
+        hb += mix64(S ^ (0xD1B54A32D192ED03ull + (uint64_t)len));
+    }
+    __device__ __forceinline__ void flush(unsigned long long *acc) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pp += __shfl_down_sync(0xffffffffu, pp, o);
+            vert += __shfl_down_sync(0xffffffffu, vert, o);
+            ext += __shfl_down_sync(0xffffffffu, ext, o);
+            ha += __shfl_down_sync(0xffffffffu, ha, o);
+            hb += __shfl_down_sync(0xffffffffu, hb, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (pp) atomicAdd(acc + 0, pp);
+            if (vert) atomicAdd(acc + 1, vert);
+            if (ext) atomicAdd(acc + 2, ext);
+            atomicAdd(acc + 3, ha);
+            atomicAdd(acc + 4, hb);
+        }
+    }
+};
+
+template <bool TS>
+__device__ __forceinline__ FSlot fslot(const FSlot *st, const FSlot *g, uint32_t i) {
+    if constexpr (TS) {
+        return st[i];
+    } else {
+        const int4 v = __ldg(reinterpret_cast<const int4 *>(g) + i);
+        return FSlot{(uint32_t)v.x, (uint32_t)v.y, v.z, v.w};
+    }
+}
+
+// Roots: one record per start vertex of a nontrivial SCC; an isolated vertex
+// (no arc at all in a graph where no arc leaves any SCC) is itself a prime path.
+__global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, const int32_t *root_vb, int32_t n) {
+    FAcc f;
+    unsigned int write = 0;
+    ulonglong2 rec = make_ulonglong2(0, 0);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const int32_t slot = root_slot[i], vb = root_vb[i];
+        const FSlot t = A.tab[slot];
+        const uint32_t s = (uint32_t)(slot - vb);
+        const uint64_t S = mix64((uint64_t)(uint32_t)t.gid);  // position 0
+        if (t.sin == 0u) {
+            f.emit(S, 1);
+        } else {
+            rec = make_ulonglong2(fkey(1u << s, s, s, (uint32_t)vb), S);
+            write = 1;
+        }
+    }
+    const unsigned int lane = threadIdx.x & 31;
+    const unsigned int bal = __ballot_sync(0xffffffffu, write);
+    unsigned long long base = 0;
+    if (lane == 0 && bal) base = atomicAdd(A.cnt_out, (unsigned long long)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (write) {
+        const unsigned long long j = base + __popc(bal & ((1u << lane) - 1u));
+        if (j < A.cap) A.out[j] = rec;
+        else atomicOr(A.overflow, 1u);
+    }
+    f.flush(A.acc);
+}
+
+// One level: every record of level l, every untried child.  Persistent grid;
+// a block takes tiles of kFTile records (kFRec per thread, coalesced per k) and
+// reserves the tile's surviving children with ONE atomicAdd (block scan): the
+// record counter is a single address, and one atomic per warp serialised there
+// (1.5 atomics/ns measured: a warp-per-atomic level kernel ran at 1.1 TB/s).
+// TS: slot table in shared memory as {sin, pin, mix(l+1, gid)} -- the digest
+// term of a vertex at this level's position is computed once per block.
+constexpr int kFThreads = 256;
+constexpr int kFRec = 4;
+constexpr int kFTile = kFThreads * kFRec;
+
+struct FSm {  // shared-memory slot entry
+    uint32_t sin, pin;
+    uint64_t mix;  // mix64((l+1) << 32 | gid)
+};
+
+template <bool TS>
+__global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs A) {
+    extern __shared__ int4 fsm[];
+    FSm *st = reinterpret_cast<FSm *>(fsm);
+    __shared__ uint32_t wsum[2][kFThreads / 32];
+    __shared__ unsigned long long bbase[2];
+    __shared__ unsigned long long red[5][kFThreads / 32];
+    const uint64_t pos = (uint64_t)(A.l + 1) << 32;  // position of the new vertex
+    if constexpr (TS) {
+        for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
+            const FSlot t = A.tab[i];
+            st[i] = FSm{t.sin, t.pin, mix64(pos | (uint32_t)t.gid)};
+        }
+        __syncthreads();
+    }
+    auto sinof = [&](uint32_t i) -> uint32_t {
+        if constexpr (TS) return st[i].sin;
+        else return (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i));
+    };
+    auto pinof = [&](uint32_t i) -> uint32_t {
+        if constexpr (TS) return st[i].pin;
+        else return (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i) + 1);
+    };
+    auto mixof = [&](uint32_t i) -> uint64_t {
+        if constexpr (TS) return st[i].mix;
+        else return mix64(pos | (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i) + 2));
+    };
+    const unsigned long long n_in = min(*A.cnt_in, A.cap);  // an overflowed level holds cap records
+    const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path
+    FAcc f;
+    int par = 0;
+    for (unsigned long long t0 = (unsigned long long)blockIdx.x * kFTile; t0 < n_in;
+         t0 += (unsigned long long)gridDim.x * kFTile, par ^= 1) {
+        uint32_t M[kFRec], sv[kFRec], vb[kFRec], keep[kFRec];
+        uint64_t S[kFRec];
+        ulonglong2 r[kFRec];
+#pragma unroll
+        for (int k = 0; k < kFRec; k++) {  // all loads first: kFRec records in flight per thread
+            const unsigned long long i = t0 + k * kFThreads + threadIdx.x;
+            r[k] = i < n_in ? __ldcs(A.in + i) : make_ulonglong2(0, 0);
+        }
+        uint32_t nk = 0;
+#pragma unroll
+        for (int k = 0; k < kFRec; k++) {
+            const unsigned long long i = t0 + k * kFThreads + threadIdx.x;
+            M[k] = (uint32_t)r[k].x;
+            const uint32_t u = (uint32_t)(r[k].x >> 32) & 31u;
+            const uint32_t s = (uint32_t)(r[k].x >> 37) & 31u;
+            sv[k] = s;
+            vb[k] = (uint32_t)(r[k].x >> 42);
+            S[k] = r[k].y;
+            keep[k] = 0;
+            if (i < n_in) {
+                const uint32_t sbit = 1u << s;
+                const uint32_t c = sinof(vb[k] + u) & (~M[k] | sbit);
+                const bool head_closed = (pinof(vb[k] + s) & ~M[k]) == 0u;  // pred(s) within M = M' \ {w}
+                f.ext += __popc(c);
+                uint32_t cc = c;
+                while (cc) {
+                    const uint32_t w = __ffs(cc) - 1;
+                    cc &= cc - 1u;
+                    const uint32_t cw = (w == s) ? 0u : (sinof(vb[k] + w) & (~(M[k] | (1u << w)) | sbit));
+                    if (cw) keep[k] |= 1u << w;
+                    else if (w == s || head_closed) f.emit(S[k] + mixof(vb[k] + w), len);  // closure / internal PP
+                }
+                nk += __popc(keep[k]);
+            }
+        }
+        // block compaction: warp scans, one atomicAdd per tile
+        uint32_t inc = nk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (unsigned)o) inc += t;
+        }
+        if (lane == 31) wsum[par][warp] = inc;
+        __syncthreads();
+        uint32_t woff = 0, btot = 0;
+#pragma unroll
+        for (int x = 0; x < kFThreads / 32; x++) {
+            const uint32_t v = wsum[par][x];
+            woff += (x < (int)warp) ? v : 0u;
+            btot += v;
+        }
+        if (threadIdx.x == 0) bbase[par] = btot ? atomicAdd(A.cnt_out, (unsigned long long)btot) : 0ull;
+        __syncthreads();
+        const unsigned long long bb = bbase[par];
+        if (btot) {
+            if (bb + btot > A.cap) {
+                if (threadIdx.x == 0) atomicOr(A.overflow, 1u);
+            } else {
+                unsigned long long j = bb + woff + (inc - nk);
+#pragma unroll
+                for (int k = 0; k < kFRec; k++) {
+                    uint32_t kp = keep[k];
+                    while (kp) {
+                        const uint32_t w = __ffs(kp) - 1;
+                        kp &= kp - 1u;
+                        __stcs(A.out + j, make_ulonglong2(fkey(M[k] | (1u << w), w, sv[k], vb[k]),
+                                                          S[k] + mixof(vb[k] + w)));
+                        j++;
+                    }
+                }
+            }
+        }
+    }
+    // block reduction of the accumulators, one set of atomics per block
+    unsigned long long v[5] = {f.pp, f.vert, f.ext, f.ha, f.hb};
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
+        if (lane == 0) red[q][warp] = v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        unsigned long long a = 0;
+#pragma unroll
+        for (int x = 0; x < kFThreads / 32; x++) a += red[threadIdx.x][x];
+        if (a || threadIdx.x >= 3) atomicAdd(A.acc + threadIdx.x, a);
+    }
+}
+
+}  // namespace tpg

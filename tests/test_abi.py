@@ -49,8 +49,8 @@ def test_abi_struct_sizes_match_header():
 #include <stdio.h>
 #include <stddef.h>
 #include "tpgen.h"
-int main(void){printf("%zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
- offsetof(tpgen_stats, ms_plan), offsetof(tpgen_options, host_out));return 0;}
+int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
+ offsetof(tpgen_stats, ms_plan), offsetof(tpgen_options, host_out), offsetof(tpgen_options, engine));return 0;}
 '''
     tmpd = os.path.join(ROOT, "build")
     os.makedirs(tmpd, exist_ok=True)
@@ -60,7 +60,7 @@ int main(void){printf("%zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpg
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
     vals = [int(x) for x in subprocess.check_output([exe]).split()]
     assert vals == [ctypes.sizeof(_abi.Options), ctypes.sizeof(_abi.Stats), ctypes.sizeof(_abi.Paths),
-                    _abi.Stats.ms_plan.offset, _abi.Options.host_out.offset]
+                    _abi.Stats.ms_plan.offset, _abi.Options.host_out.offset, _abi.Options.engine.offset]
 
 
 def _corpus(count, seed0):
@@ -118,6 +118,27 @@ def test_compute_calls_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(Exception):
         tp.prime_paths(gen.fig1b())
+
+
+def test_frontier_engine_option_checks():
+    """TPGEN_ENGINE_FRONTIER computes counts + digest only; the option checks run before
+    any device work (include/tpgen.h tpgen_options.engine)."""
+    lib = tp.library()
+    g = gen.fig1b()
+    so, st = g.offsets, g.targets
+    for engine, mode in ((_abi.ENGINE_FRONTIER, _abi.OUT_MATERIALIZE), (7, _abi.OUT_COUNT_HASH)):
+        o = _abi.Options()
+        lib.tpgen_options_init(ctypes.byref(o))
+        assert o.engine == _abi.ENGINE_DFS
+        o.engine, o.output_mode = engine, mode
+        paths, stats = _abi.Paths(), _abi.Stats()
+        r = lib.tpgen_prime_paths(so.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  st.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), g.n, ctypes.byref(o),
+                                  ctypes.byref(paths), ctypes.byref(stats))
+        assert r == 1  # TPGEN_ERR_INVALID_ARGUMENT
+        assert paths.n_paths == 0
+    with pytest.raises(ValueError):
+        tp.prime_paths(g, mode="count", engine="bfs")
 
 
 def test_metrics_fig1b_and_loops():

@@ -1,0 +1,97 @@
+"""GPU parity of the level-synchronous frontier engine (TPGEN_ENGINE_FRONTIER, DESIGN.md
+§6.6): counts, E_canon and the order-free digest vs the CPU oracle (expected values from
+oracle/ only), and vs the DFS engine at config 3's full size."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import generators as gen
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2210_16998_b200")
+
+
+def _oracle_stats(g, v_lo=0, v_hi=None):
+    ro, rv = oracle.prime_paths(g, v_lo=v_lo, v_hi=v_hi)
+    return {"n_paths": len(ro) - 1, "total_vertices": int(ro[-1]),
+            "n_extensions": oracle.ext_count(g, v_lo=v_lo, v_hi=v_hi), "digest": oracle.digest(ro, rv)}
+
+
+def _frontier(g, **kw):
+    st = tp.prime_paths(g, mode="count", digest=True, engine="frontier", **kw).stats
+    return {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
+            "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])}
+
+
+def _lean_corpus():
+    yield gen.from_arcs(1, [(0, 0)])                       # self-loop: [0, 0]
+    yield gen.from_arcs(2, [(0, 1), (1, 0)])               # 2-cycle
+    yield gen.from_arcs(3, [])                             # isolated vertices only
+    for n, d, seed in ((5, 2, 1), (8, 3, 2), (12, 3, 3), (14, 4, 4), (16, 3, 5)):
+        yield gen.dense_scc(n, d, seed)
+    ring = [(i, (i + 1) % 32) for i in range(32)] + [(i, (i + 5) % 32) for i in range(0, 32, 4)]
+    yield gen.from_arcs(32, ring)                          # a 32-vertex SCC: every mask bit in use
+    parts = [gen.dense_scc(6 + i % 5, 2 + i % 2, 50 + i) for i in range(12)]
+    parts += [gen.from_arcs(1, [(0, 0)]), gen.from_arcs(2, []), gen.from_arcs(2, [(0, 1), (1, 0)])]
+    yield gen.disjoint_union(parts, name="lean-union")
+
+
+def test_frontier_matches_oracle():
+    for g in _lean_corpus():
+        assert _frontier(g) == _oracle_stats(g), g.name
+
+
+def test_frontier_start_ranges_add_up():
+    g = gen.disjoint_union([gen.dense_scc(10, 3, 7), gen.from_arcs(3, [(0, 0), (1, 2), (2, 1)]),
+                            gen.dense_scc(9, 3, 8)], name="ranges")
+    whole = _frontier(g)
+    assert whole == _oracle_stats(g)
+    cuts = [0, 4, 10, 11, 15, g.n]
+    tot = [0, 0, 0, 0, 0]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        part = _frontier(g, start_range=(a, b))
+        assert part == _oracle_stats(g, a, b), (a, b)
+        tot = [tot[0] + part["n_paths"], tot[1] + part["total_vertices"], tot[2] + part["n_extensions"],
+               (tot[3] + part["digest"][0]) % 2**64, (tot[4] + part["digest"][1]) % 2**64]
+    assert tot == [whole["n_paths"], whole["total_vertices"], whole["n_extensions"], *whole["digest"]]
+
+
+def test_frontier_overflow_retry(monkeypatch):
+    """A record buffer far too small: every call retries with a larger one until it fits."""
+    monkeypatch.setenv("TPGEN_FRONTIER_CAP", "64")
+    g = gen.dense_scc(13, 3, 11)
+    plan = tp.Plan(g)
+    st = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
+    assert st["n_count_rounds"] >= 1
+    assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
+            "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == _oracle_stats(g)
+    plan.close()
+
+
+def test_frontier_rejects_non_lean_graphs():
+    for g in (gen.fig1b(), gen.config5(K=2, n=40)):
+        with pytest.raises(tp.TpgenError) as e:
+            _frontier(g)
+        assert e.value.status_name.endswith("INVALID_ARGUMENT")
+    with pytest.raises(tp.TpgenError):
+        tp.prime_paths(gen.dense_scc(8, 2, 1), engine="frontier")  # materialize: counts only
+
+
+def test_frontier_config3_full_size():
+    """config 3 in the bench's launch configuration: equal to the DFS engine's count mode
+    (itself bit-exact against the oracle), E_canon equal to the oracle's counter, and two
+    start vertices' counts and digests equal to the oracle's."""
+    g = gen.config3()
+    plan = tp.Plan(g)
+    f = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
+    d = plan.prime_paths(mode="count", digest=True).stats
+    for k in ("n_paths", "total_vertices", "n_extensions", "hash_lo", "hash_hi"):
+        assert f[k] == d[k], k
+    assert f["n_extensions"] == oracle.ext_count(g)
+    for s in (3, 17):
+        st = plan.prime_paths(mode="count", digest=True, engine="frontier", start_range=(s, s + 1)).stats
+        assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
+                "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == \
+            _oracle_stats(g, s, s + 1)
+    plan.close()
