@@ -394,11 +394,12 @@ def main():
             roofline = {
                 "bound": "hbm", "kernel": "frontier_level_kernel<TS=1> (all levels + root kernel)",
                 "achieved": f_ach, "peak": peak, "unit": "GB/s", "frac": f_ach / peak,
-                "traffic": traffic.get("frontier_level_kernel", {}).get("dram_bytes_per_launch"),
+                "traffic": traffic.get("frontier_level_kernel", {}).get("dram_bytes_per_step"),
                 "algorithmic_bytes_per_step": f_bytes, "records_per_step": st["n_units"],
                 "ms_per_step": ms_dfs, "share_of_step": ms_dfs / ms_dev,
                 "model": "16-byte path record {mask, last, first, slot base | digest sum} written once and read "
-                         "once per record (DESIGN.md 6.6); traffic is per level launch (the levels differ)",
+                         "once per record (DESIGN.md 6.6); traffic = DRAM bytes of all level launches of one call "
+                         "(ncu launch list, profiles/traffic.json)",
                 "alu_view": {"achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak},
                 "path_hbm": {"achieved": a_bytes / (ms_dev * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                              "frac": a_bytes / (ms_dev * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,

@@ -16,9 +16,10 @@
 //                              path iff c' == 0 and pred(s) within M (= M' \ {w});
 //                              p' joins level l+1 only if c' != 0 (a record with
 //                              no child would be read for nothing).
-// Compaction: one warp-wide exclusive scan of the per-lane child counts and one
-// atomicAdd per warp on the level's record counter (the frontier's order is
-// irrelevant: counts, E_canon and the order-free digest are all sums).
+// Compaction: block scan of the per-thread child counts, one atomicAdd per tile
+// on the level's record counter (the frontier's order is irrelevant: counts,
+// E_canon and the order-free digest are all sums).  Prime paths found in the
+// (divergent) child loop are queued per warp and hashed 32 at a time.
 #pragma once
 
 #include <cstdint>
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     __shared__ uint32_t wsum[2][kFThreads / 32];
     __shared__ unsigned long long bbase[2];
     __shared__ unsigned long long red[5][kFThreads / 32];
+    __shared__ uint64_t pqs[kFThreads / 32][64];  // per warp: digest sums S of prime paths awaiting their hash
     const uint64_t pos = (uint64_t)(A.l + 1) << 32;  // position of the new vertex
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
@@ -166,7 +168,10 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     };
     const unsigned long long n_in = min(*A.cnt_in, A.cap);  // an overflowed level holds cap records
     const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path (every prime path found at this level)
+    uint64_t *pq = pqs[warp];
+    uint32_t qn = 0;  // queued prime paths (warp-uniform, < 32 between drains)
     FAcc f;
     int par = 0;
     for (unsigned long long t0 = (unsigned long long)blockIdx.x * kFTile; t0 < n_in;
@@ -190,21 +195,40 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
             vb[k] = (uint32_t)(r[k].x >> 42);
             S[k] = r[k].y;
             keep[k] = 0;
+            uint32_t cc = 0;
+            bool head_closed = false;
             if (i < n_in) {
-                const uint32_t sbit = 1u << s;
-                const uint32_t c = sinof(vb[k] + u) & (~M[k] | sbit);
-                const bool head_closed = (pinof(vb[k] + s) & ~M[k]) == 0u;  // pred(s) within M = M' \ {w}
-                f.ext += __popc(c);
-                uint32_t cc = c;
-                while (cc) {
+                cc = sinof(vb[k] + u) & (~M[k] | (1u << s));
+                head_closed = (pinof(vb[k] + s) & ~M[k]) == 0u;  // pred(s) within M = M' \ {w}
+                f.ext += __popc(cc);
+            }
+            // warp-uniform child loop; prime paths are queued and hashed 32 at a time
+            const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(cc));
+            for (int it = 0; it < maxc; it++) {
+                bool em = false;
+                uint64_t Sx = 0;
+                if (cc) {
                     const uint32_t w = __ffs(cc) - 1;
                     cc &= cc - 1u;
-                    const uint32_t cw = (w == s) ? 0u : (sinof(vb[k] + w) & (~(M[k] | (1u << w)) | sbit));
-                    if (cw) keep[k] |= 1u << w;
-                    else if (w == s || head_closed) f.emit(S[k] + mixof(vb[k] + w), len);  // closure / internal PP
+                    const uint32_t cw = (w == s) ? 0u : (sinof(vb[k] + w) & (~(M[k] | (1u << w)) | (1u << s)));
+                    if (cw) {
+                        keep[k] |= 1u << w;
+                    } else if (w == s || head_closed) {  // cycle closure, or an internal prime path
+                        em = true;
+                        Sx = S[k] + mixof(vb[k] + w);
+                    }
                 }
-                nk += __popc(keep[k]);
+                const uint32_t bal = __ballot_sync(0xffffffffu, em);
+                if (em) pq[qn + __popc(bal & lt)] = Sx;
+                qn += __popc(bal);
+                if (qn >= 32) {
+                    __syncwarp();
+                    qn -= 32;
+                    f.emit(pq[qn + lane], len);
+                    __syncwarp();
+                }
             }
+            nk += __popc(keep[k]);
         }
         // block compaction: warp scans, one atomicAdd per tile
         uint32_t inc = nk;
@@ -244,6 +268,8 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
             }
         }
     }
+    __syncwarp();
+    if (lane < qn) f.emit(pq[lane], len);  // the queue's remainder
     // block reduction of the accumulators, one set of atomics per block
     unsigned long long v[5] = {f.pp, f.vert, f.ext, f.ha, f.hb};
 #pragma unroll
