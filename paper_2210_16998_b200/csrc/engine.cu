@@ -1278,7 +1278,14 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     std::vector<unsigned long long> h(nctr);
     int64_t launches = 0;
     float ms = 0;
-    for (int attempt = 0;; attempt++) {
+    uint64_t recs = 0;
+    bool chunked = false;
+    uint64_t capc = 0;  // chunked mode: records per level buffer
+    if (const char *ev = getenv("TPGEN_FRONTIER_CHUNK")) {  // test hook: force the DFS-chunked frontier
+        chunked = true;
+        capc = std::max<uint64_t>(64, atoll(ev));
+    }
+    for (int attempt = 0; !chunked; attempt++) {
         cap = std::min(cap, cap_max);
         TPG_TRY(P.f_buf0.ensure(cap * 16, s));
         TPG_TRY(P.f_buf1.ensure(cap * 16, s));
@@ -1289,6 +1296,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         A.tab = P.f_tab.as<FSlot>();
         A.n_tab = n_tab;
         A.cap = cap;
+        A.lim = ~0ull;
         A.acc = ctr;
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
         if (n_roots) {
@@ -1320,17 +1328,90 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         for (int l = 0; l <= Lmax; l++) peak = std::max<uint64_t>(peak, h[8 + l]);
         if (!(h[5] & 1u)) {
             P.f_cap_hwm = std::max<uint64_t>(P.f_cap_hwm, peak);
+            for (int l = 0; l <= Lmax; l++) recs += h[8 + l];
             break;
         }
-        if (cap >= cap_max) {
-            set_error("frontier level exceeds the device memory budget (use the DFS engine)");
-            return TPGEN_ERR_OUT_OF_MEMORY;
+        st.n_count_rounds = attempt + 1;
+        if (cap >= cap_max) {  // no level fits: the DFS-chunked frontier in the same memory
+            chunked = true;
+            capc = cap_max * 2 / (uint64_t)(Lmax + 1);
+            break;
         }
         cap = std::max<uint64_t>(2 * cap, peak + peak / 4);  // a truncated level under-counts the next ones
-        st.n_count_rounds = attempt + 1;
     }
-    uint64_t recs = 0;
-    for (int l = 0; l <= Lmax; l++) recs += h[8 + l];
+    if (chunked) {
+        // DFS over chunks of levels (the north star's "DFS-chunked when the frontier would
+        // overflow HBM"): one buffer of capc records per level; a chunk of level l holds at
+        // most capc / D records (D = the largest out-degree), so its children always fit in
+        // level l+1's buffer, which is consumed completely before level l's next chunk.
+        uint32_t D = 1;
+        for (int32_t i = 0; i < H.n; i++) D = std::max<uint32_t>(D, (uint32_t)__builtin_popcount((uint32_t)H.sin[(size_t)i * W]));
+        if (capc < (uint64_t)std::max<int64_t>(n_roots, D)) {
+            set_error("frontier chunk buffers too small for the roots (use the DFS engine)");
+            return TPGEN_ERR_OUT_OF_MEMORY;
+        }
+        TPG_TRY(P.f_buf0.ensure((size_t)(Lmax + 1) * capc * 16, s));
+        ulonglong2 *base = P.f_buf0.as<ulonglong2>();
+        TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
+        cudaEventRecord(tall.a, s);
+        FrontierArgs A;
+        A.tab = P.f_tab.as<FSlot>();
+        A.n_tab = n_tab;
+        A.cap = capc;
+        A.acc = ctr;
+        A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
+        std::vector<uint64_t> nl(Lmax + 1, 0), cur(Lmax + 1, 0);
+        if (n_roots) {
+            A.lim = ~0ull;
+            A.in = nullptr;
+            A.out = base;
+            A.cnt_in = nullptr;
+            A.cnt_out = ctr + 8;
+            A.l = -1;
+            frontier_root_kernel<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
+                                                                        P.f_roots.as<int32_t>() + n_roots, n_roots);
+            launches++;
+            TPG_CK(cudaMemcpyAsync(&nl[0], ctr + 8, 8, cudaMemcpyDeviceToHost, s));
+            TPG_CK(cudaStreamSynchronize(s));
+            recs += nl[0];
+        }
+        const uint64_t chunk = std::max<uint64_t>(1, capc / D);
+        int l = 0;
+        while (l >= 0) {
+            if (cur[l] >= nl[l]) {
+                l--;
+                continue;
+            }
+            const uint64_t k = std::min<uint64_t>(nl[l] - cur[l], chunk);
+            TPG_CK(cudaMemsetAsync(ctr + 8 + l + 1, 0, 8, s));
+            A.in = base + (size_t)l * capc + cur[l];
+            A.out = base + (size_t)(l + 1) * capc;
+            A.cnt_in = ctr + 8 + l;  // = nl[l] until level l is consumed
+            A.cnt_out = ctr + 8 + l + 1;
+            A.lim = k;
+            A.l = l;
+            if (ts) frontier_level_kernel<true><<<grid, kFThreads, smem, s>>>(A);
+            else frontier_level_kernel<false><<<grid, kFThreads, 0, s>>>(A);
+            launches++;
+            cur[l] += k;
+            if (l + 1 < Lmax) {  // level l+1 records can have children: descend
+                TPG_CK(cudaMemcpyAsync(&nl[l + 1], ctr + 8 + l + 1, 8, cudaMemcpyDeviceToHost, s));
+                TPG_CK(cudaStreamSynchronize(s));
+                recs += nl[l + 1];
+                cur[l + 1] = 0;
+                l++;
+            }
+        }
+        cudaEventRecord(tall.b, s);
+        TPG_CK(cudaGetLastError());
+        TPG_CK(cudaMemcpyAsync(h.data(), ctr, nctr * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        cudaEventElapsedTime(&ms, tall.a, tall.b);
+        if (h[5] & 1u) {
+            set_error("frontier chunk overflow (internal)");
+            return TPGEN_ERR_INTERNAL;
+        }
+    }
     st.n_paths = (int64_t)h[0];
     st.total_vertices = (int64_t)h[1];
     st.n_extensions = (int64_t)h[2];

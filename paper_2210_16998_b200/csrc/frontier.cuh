@@ -48,6 +48,7 @@ struct FrontierArgs {
     const unsigned long long *cnt_in;
     unsigned long long *cnt_out;
     unsigned long long cap;      // records per buffer
+    unsigned long long lim;      // records of the input to process (chunked mode), ~0 = all
     unsigned long long *acc;     // [0] prime paths, [1] vertices, [2] extensions, [3] digest a, [4] digest b
     unsigned int *overflow;
     int32_t l;                   // input paths have l + 1 vertices
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
         if constexpr (TS) return st[i].mix;
         else return mix64(pos | (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i) + 2));
     };
-    const unsigned long long n_in = min(*A.cnt_in, A.cap);  // an overflowed level holds cap records
+    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);  // an overflowed level holds cap records
     const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path (every prime path found at this level)

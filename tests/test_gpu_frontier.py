@@ -69,6 +69,21 @@ def test_frontier_overflow_retry(monkeypatch):
     plan.close()
 
 
+def test_frontier_dfs_chunked(monkeypatch):
+    """The DFS-chunked frontier (level buffers of a few hundred records, chunks of
+    capacity / out-degree records, each level drained before its parent's next chunk)
+    gives the oracle's counts, E_canon and digest."""
+    monkeypatch.setenv("TPGEN_FRONTIER_CHUNK", "256")
+    for g in (gen.dense_scc(13, 3, 11), gen.dense_scc(16, 3, 5),
+              gen.disjoint_union([gen.dense_scc(9, 3, 60), gen.from_arcs(2, [(0, 1), (1, 0)]),
+                                  gen.from_arcs(1, [])], name="chunk-union")):
+        st = tp.prime_paths(g, mode="count", digest=True, engine="frontier").stats
+        assert st["gpu_launches"] > st["max_scc"] + 1  # more than one chunk per level
+        assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
+                "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == \
+            _oracle_stats(g), g.name
+
+
 def test_frontier_rejects_non_lean_graphs():
     for g in (gen.fig1b(), gen.config5(K=2, n=40)):
         with pytest.raises(tp.TpgenError) as e:
@@ -88,6 +103,16 @@ def test_frontier_config3_full_size():
     d = plan.prime_paths(mode="count", digest=True).stats
     for k in ("n_paths", "total_vertices", "n_extensions", "hash_lo", "hash_hi"):
         assert f[k] == d[k], k
+    # the DFS-chunked frontier at full size (4 M records per level buffer, peak level ~3.4e7)
+    import os
+    os.environ["TPGEN_FRONTIER_CHUNK"] = str(1 << 22)
+    try:
+        c = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
+    finally:
+        del os.environ["TPGEN_FRONTIER_CHUNK"]
+    assert c["gpu_launches"] > 100
+    for k in ("n_paths", "total_vertices", "n_extensions", "hash_lo", "hash_hi"):
+        assert c[k] == f[k], k
     assert f["n_extensions"] == oracle.ext_count(g)
     for s in (3, 17):
         st = plan.prime_paths(mode="count", digest=True, engine="frontier", start_range=(s, s + 1)).stats
