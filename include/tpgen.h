@@ -109,9 +109,10 @@ typedef struct {
                                   ping-pong buffers, warp-scan compaction.  Requires output_mode =
                                   TPGEN_OUT_COUNT_HASH (counts, E_canon and the digest; the order-free
                                   frontier never materializes the canonical list) and a graph whose SCCs
-                                  have <= 32 vertices with no arc leaving any SCC (else
-                                  TPGEN_ERR_INVALID_ARGUMENT); a frontier larger than half the free device
-                                  memory -> TPGEN_ERR_OUT_OF_MEMORY. */
+                                  have <= 64 vertices with no arc leaving any SCC (else
+                                  TPGEN_ERR_INVALID_ARGUMENT).  A level that does not fit in the device
+                                  memory budget switches the call to the DFS-chunked frontier (DESIGN.md
+                                  §6.6); TPGEN_ERR_OUT_OF_MEMORY only when even one chunk cannot fit. */
 } tpgen_options;
 
 typedef struct {

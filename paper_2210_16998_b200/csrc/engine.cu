@@ -1219,13 +1219,15 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
 // ------------------------------------------------------------ frontier engine
 // TPGEN_ENGINE_FRONTIER (frontier.cuh): level-synchronous
 // extension of all paths of one length at a time; counts, E_canon and digest.
+template <class T>
 static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    constexpr size_t kRecB = sizeof(T) == 4 ? 16 : 24;  // bytes per frontier record (key + S)
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
     const HostPlan &H = P.hp;
-    if (H.max_scc > 32 || P.any_exit || H.n >= (1 << 22)) {
-        set_error("the frontier engine needs SCCs of <= 32 vertices and no arc leaving any SCC (use the DFS engine)");
+    if (H.max_scc > 64 || H.W != 1 || P.any_exit || H.n >= (1 << 22)) {
+        set_error("the frontier engine needs SCCs of <= 64 vertices and no arc leaving any SCC (use the DFS engine)");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
     cudaStream_t s = (cudaStream_t)o.stream;
@@ -1245,9 +1247,9 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     // slot table (uploaded once per plan)
     const int32_t n_tab = std::max(H.n, 1);
     if (!P.f_tab_ok) {
-        std::vector<FSlot> tab(n_tab, FSlot{0, 0, 0, 0});
+        std::vector<FSlot<T>> tab(n_tab, FSlot<T>{0, 0, 0, 0});
         for (int32_t i = 0; i < H.n; i++)
-            tab[i] = FSlot{(uint32_t)H.sin[(size_t)i * W], (uint32_t)H.pin[(size_t)i * W], H.slot_gid[i], 0};
+            tab[i] = FSlot<T>{(T)H.sin[(size_t)i * W], (T)H.pin[(size_t)i * W], H.slot_gid[i], 0};
         TPG_TRY(upload(P.f_tab, tab, s));
         P.f_tab_ok = true;
     }
@@ -1267,12 +1269,12 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     if (const char *ev = getenv("TPGEN_FRONTIER_CAP")) cap = std::max<uint64_t>(64, atoll(ev));  // test hook: retries
     size_t free_b = 0, total_b = 0;
     TPG_CK(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t cap_max = (uint64_t)((double)(free_b + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / 16);
-    const size_t smem = (size_t)n_tab * sizeof(FSm);
+    const uint64_t cap_max = (uint64_t)((double)(free_b + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / kRecB);
+    const size_t smem = (size_t)n_tab * sizeof(FSm<T>);
     const bool ts = smem <= 32 * 1024;
     int per_sm = 0;  // persistent grid: every block resident
-    if (ts) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<true>, kFThreads, smem));
-    else TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<false>, kFThreads, 0));
+    if (ts) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, true>, kFThreads, smem));
+    else TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, false>, kFThreads, 0));
     const int grid = P.num_sms * std::max(per_sm, 1);
     Timer tall;
     std::vector<unsigned long long> h(nctr);
@@ -1287,13 +1289,14 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     }
     for (int attempt = 0; !chunked; attempt++) {
         cap = std::min(cap, cap_max);
-        TPG_TRY(P.f_buf0.ensure(cap * 16, s));
-        TPG_TRY(P.f_buf1.ensure(cap * 16, s));
+        TPG_TRY(P.f_buf0.ensure(cap * kRecB, s));
+        TPG_TRY(P.f_buf1.ensure(cap * kRecB, s));
         ulonglong2 *buf[2] = {P.f_buf0.as<ulonglong2>(), P.f_buf1.as<ulonglong2>()};
+        uint64_t *bufS[2] = {reinterpret_cast<uint64_t *>(buf[0] + cap), reinterpret_cast<uint64_t *>(buf[1] + cap)};
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
         cudaEventRecord(tall.a, s);
         FrontierArgs A;
-        A.tab = P.f_tab.as<FSlot>();
+        A.tab = P.f_tab.p;
         A.n_tab = n_tab;
         A.cap = cap;
         A.lim = ~0ull;
@@ -1301,21 +1304,25 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
         if (n_roots) {
             A.in = nullptr;
+            A.in_S = nullptr;
             A.out = buf[0];
+            A.out_S = bufS[0];
             A.cnt_in = nullptr;
             A.cnt_out = ctr + 8;
             A.l = -1;
-            frontier_root_kernel<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
+            frontier_root_kernel<T><<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
             for (int l = 0; l < Lmax; l++) {
                 A.in = buf[l & 1];
+                A.in_S = bufS[l & 1];
                 A.out = buf[(l + 1) & 1];
+                A.out_S = bufS[(l + 1) & 1];
                 A.cnt_in = ctr + 8 + l;
                 A.cnt_out = ctr + 8 + l + 1;
                 A.l = l;
-                if (ts) frontier_level_kernel<true><<<grid, kFThreads, smem, s>>>(A);
-                else frontier_level_kernel<false><<<grid, kFThreads, 0, s>>>(A);
+                if (ts) frontier_level_kernel<T, true><<<grid, kFThreads, smem, s>>>(A);
+                else frontier_level_kernel<T, false><<<grid, kFThreads, 0, s>>>(A);
                 launches++;
             }
         }
@@ -1345,17 +1352,18 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         // most capc / D records (D = the largest out-degree), so its children always fit in
         // level l+1's buffer, which is consumed completely before level l's next chunk.
         uint32_t D = 1;
-        for (int32_t i = 0; i < H.n; i++) D = std::max<uint32_t>(D, (uint32_t)__builtin_popcount((uint32_t)H.sin[(size_t)i * W]));
+        for (int32_t i = 0; i < H.n; i++) D = std::max<uint32_t>(D, (uint32_t)__builtin_popcountll(H.sin[(size_t)i * W]));
         if (capc < (uint64_t)std::max<int64_t>(n_roots, D)) {
             set_error("frontier chunk buffers too small for the roots (use the DFS engine)");
             return TPGEN_ERR_OUT_OF_MEMORY;
         }
-        TPG_TRY(P.f_buf0.ensure((size_t)(Lmax + 1) * capc * 16, s));
+        TPG_TRY(P.f_buf0.ensure((size_t)(Lmax + 1) * capc * kRecB, s));
         ulonglong2 *base = P.f_buf0.as<ulonglong2>();
+        uint64_t *baseS = reinterpret_cast<uint64_t *>(base + (size_t)(Lmax + 1) * capc);
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
         cudaEventRecord(tall.a, s);
         FrontierArgs A;
-        A.tab = P.f_tab.as<FSlot>();
+        A.tab = P.f_tab.p;
         A.n_tab = n_tab;
         A.cap = capc;
         A.acc = ctr;
@@ -1364,11 +1372,13 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         if (n_roots) {
             A.lim = ~0ull;
             A.in = nullptr;
+            A.in_S = nullptr;
             A.out = base;
+            A.out_S = baseS;
             A.cnt_in = nullptr;
             A.cnt_out = ctr + 8;
             A.l = -1;
-            frontier_root_kernel<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
+            frontier_root_kernel<T><<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
             TPG_CK(cudaMemcpyAsync(&nl[0], ctr + 8, 8, cudaMemcpyDeviceToHost, s));
@@ -1385,13 +1395,15 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             const uint64_t k = std::min<uint64_t>(nl[l] - cur[l], chunk);
             TPG_CK(cudaMemsetAsync(ctr + 8 + l + 1, 0, 8, s));
             A.in = base + (size_t)l * capc + cur[l];
+            A.in_S = baseS + (size_t)l * capc + cur[l];
             A.out = base + (size_t)(l + 1) * capc;
+            A.out_S = baseS + (size_t)(l + 1) * capc;
             A.cnt_in = ctr + 8 + l;  // = nl[l] until level l is consumed
             A.cnt_out = ctr + 8 + l + 1;
             A.lim = k;
             A.l = l;
-            if (ts) frontier_level_kernel<true><<<grid, kFThreads, smem, s>>>(A);
-            else frontier_level_kernel<false><<<grid, kFThreads, 0, s>>>(A);
+            if (ts) frontier_level_kernel<T, true><<<grid, kFThreads, smem, s>>>(A);
+            else frontier_level_kernel<T, false><<<grid, kFThreads, 0, s>>>(A);
             launches++;
             cur[l] += k;
             if (l + 1 < Lmax) {  // level l+1 records can have children: descend
@@ -1435,7 +1447,8 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
 tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st) {
     if (o.engine == TPGEN_ENGINE_FRONTIER) {
         memset(out, 0, sizeof(*out));
-        return run_frontier(P, o, st);
+        if (P.hp.max_scc <= 32) return run_frontier<uint32_t>(P, o, st);
+        return run_frontier<uint64_t>(P, o, st);
     }
     if (P.hp.max_scc <= 32) return run_pp<uint32_t>(P, o, out, st);
     switch (P.hp.W) {

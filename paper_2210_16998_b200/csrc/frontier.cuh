@@ -28,23 +28,29 @@
 
 namespace tpg {
 
+template <class T>
 struct FSlot {        // per SCC slot (local ids ascend with global ids)
-    uint32_t sin;     // in-SCC successor bits (local)
-    uint32_t pin;     // in-SCC predecessor bits (local)
+    T sin;            // in-SCC successor bits (local)
+    T pin;            // in-SCC predecessor bits (local)
     int32_t gid;      // global vertex id
     int32_t pad;
 };
 
-// record key: bits 0-31 visited mask, 32-36 last (local), 37-41 first (local), 42-63 slot base
+// Records.  32-bit masks (SCCs of <= 32 vertices): one 16-byte record
+//   {key = mask | last << 32 | first << 37 | slot base << 42, S}.
+// 64-bit masks (<= 64 vertices): a 16-byte record {mask, last | first << 6 |
+// slot base << 12} plus S in a parallel array (24 bytes per record).
 __device__ __forceinline__ uint64_t fkey(uint32_t M, uint32_t u, uint32_t s, uint32_t vb) {
     return (uint64_t)M | ((uint64_t)u << 32) | ((uint64_t)s << 37) | ((uint64_t)vb << 42);
 }
 
 struct FrontierArgs {
-    const FSlot *tab;
+    const void *tab;             // FSlot<T>[n_tab]
     int32_t n_tab;
     const ulonglong2 *in;        // level l records {key, S}
     ulonglong2 *out;             // level l+1 records
+    const uint64_t *in_S;        // 64-bit masks: S of the level l records
+    uint64_t *out_S;             //               S of the level l+1 records
     const unsigned long long *cnt_in;
     unsigned long long *cnt_out;
     unsigned long long cap;      // records per buffer
@@ -81,34 +87,66 @@ struct FAcc {
     }
 };
 
-template <bool TS>
-__device__ __forceinline__ FSlot fslot(const FSlot *st, const FSlot *g, uint32_t i) {
-    if constexpr (TS) {
-        return st[i];
-    } else {
-        const int4 v = __ldg(reinterpret_cast<const int4 *>(g) + i);
-        return FSlot{(uint32_t)v.x, (uint32_t)v.y, v.z, v.w};
+template <class T>
+struct FT;
+template <>
+struct FT<uint32_t> {
+    __device__ static int ffs(uint32_t x) { return __ffs(x); }
+    __device__ static int popc(uint32_t x) { return __popc(x); }
+    __device__ static ulonglong2 ld(const FrontierArgs &A, unsigned long long i, uint64_t &S) {
+        const ulonglong2 r = __ldcs(A.in + i);
+        S = r.y;
+        return r;
     }
-}
+    __device__ static void dec(const ulonglong2 &r, uint32_t &M, uint32_t &u, uint32_t &s, uint32_t &vb) {
+        M = (uint32_t)r.x;
+        u = (uint32_t)(r.x >> 32) & 31u;
+        s = (uint32_t)(r.x >> 37) & 31u;
+        vb = (uint32_t)(r.x >> 42);
+    }
+    __device__ static void st(const FrontierArgs &A, unsigned long long j, uint32_t M, uint32_t w, uint32_t s,
+                              uint32_t vb, uint64_t S) {
+        __stcs(A.out + j, make_ulonglong2(fkey(M, w, s, vb), S));
+    }
+};
+template <>
+struct FT<uint64_t> {
+    __device__ static int ffs(uint64_t x) { return __ffsll((long long)x); }
+    __device__ static int popc(uint64_t x) { return __popcll(x); }
+    __device__ static ulonglong2 ld(const FrontierArgs &A, unsigned long long i, uint64_t &S) {
+        S = __ldcs(reinterpret_cast<const unsigned long long *>(A.in_S) + i);
+        return __ldcs(A.in + i);
+    }
+    __device__ static void dec(const ulonglong2 &r, uint64_t &M, uint32_t &u, uint32_t &s, uint32_t &vb) {
+        M = r.x;
+        u = (uint32_t)r.y & 63u;
+        s = (uint32_t)(r.y >> 6) & 63u;
+        vb = (uint32_t)(r.y >> 12);
+    }
+    __device__ static void st(const FrontierArgs &A, unsigned long long j, uint64_t M, uint32_t w, uint32_t s,
+                              uint32_t vb, uint64_t S) {
+        __stcs(A.out + j, make_ulonglong2(M, (uint64_t)w | ((uint64_t)s << 6) | ((uint64_t)vb << 12)));
+        __stcs(reinterpret_cast<unsigned long long *>(A.out_S) + j, (unsigned long long)S);
+    }
+};
 
 // Roots: one record per start vertex of a nontrivial SCC; an isolated vertex
 // (no arc at all in a graph where no arc leaves any SCC) is itself a prime path.
+template <class T>
 __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, const int32_t *root_vb, int32_t n) {
     FAcc f;
     unsigned int write = 0;
-    ulonglong2 rec = make_ulonglong2(0, 0);
+    uint32_t s = 0, vb = 0;
+    uint64_t S = 0;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        const int32_t slot = root_slot[i], vb = root_vb[i];
-        const FSlot t = A.tab[slot];
-        const uint32_t s = (uint32_t)(slot - vb);
-        const uint64_t S = mix64((uint64_t)(uint32_t)t.gid);  // position 0
-        if (t.sin == 0u) {
-            f.emit(S, 1);
-        } else {
-            rec = make_ulonglong2(fkey(1u << s, s, s, (uint32_t)vb), S);
-            write = 1;
-        }
+        const int32_t slot = root_slot[i];
+        vb = (uint32_t)root_vb[i];
+        const FSlot<T> t = static_cast<const FSlot<T> *>(A.tab)[slot];
+        s = (uint32_t)slot - vb;
+        S = mix64((uint64_t)(uint32_t)t.gid);  // position 0
+        if (t.sin == 0) f.emit(S, 1);
+        else write = 1;
     }
     const unsigned int lane = threadIdx.x & 31;
     const unsigned int bal = __ballot_sync(0xffffffffu, write);
@@ -117,7 +155,7 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
     base = __shfl_sync(0xffffffffu, base, 0);
     if (write) {
         const unsigned long long j = base + __popc(bal & ((1u << lane) - 1u));
-        if (j < A.cap) A.out[j] = rec;
+        if (j < A.cap) FT<T>::st(A, j, (T)1 << s, s, s, vb, S);
         else atomicOr(A.overflow, 1u);
     }
     f.flush(A.acc);
@@ -134,15 +172,17 @@ constexpr int kFThreads = 256;
 constexpr int kFRec = 4;
 constexpr int kFTile = kFThreads * kFRec;
 
+template <class T>
 struct FSm {  // shared-memory slot entry
-    uint32_t sin, pin;
+    T sin, pin;
     uint64_t mix;  // mix64((l+1) << 32 | gid)
 };
 
-template <bool TS>
+template <class T, bool TS>
 __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs A) {
     extern __shared__ int4 fsm[];
-    FSm *st = reinterpret_cast<FSm *>(fsm);
+    FSm<T> *st = reinterpret_cast<FSm<T> *>(fsm);
+    const FSlot<T> *tab = static_cast<const FSlot<T> *>(A.tab);
     __shared__ uint32_t wsum[2][kFThreads / 32];
     __shared__ unsigned long long bbase[2];
     __shared__ unsigned long long red[5][kFThreads / 32];
@@ -150,22 +190,22 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     const uint64_t pos = (uint64_t)(A.l + 1) << 32;  // position of the new vertex
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
-            const FSlot t = A.tab[i];
-            st[i] = FSm{t.sin, t.pin, mix64(pos | (uint32_t)t.gid)};
+            const FSlot<T> t = tab[i];
+            st[i] = FSm<T>{t.sin, t.pin, mix64(pos | (uint32_t)t.gid)};
         }
         __syncthreads();
     }
-    auto sinof = [&](uint32_t i) -> uint32_t {
+    auto sinof = [&](uint32_t i) -> T {
         if constexpr (TS) return st[i].sin;
-        else return (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i));
+        else return __ldg(&tab[i].sin);
     };
-    auto pinof = [&](uint32_t i) -> uint32_t {
+    auto pinof = [&](uint32_t i) -> T {
         if constexpr (TS) return st[i].pin;
-        else return (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i) + 1);
+        else return __ldg(&tab[i].pin);
     };
     auto mixof = [&](uint32_t i) -> uint64_t {
         if constexpr (TS) return st[i].mix;
-        else return mix64(pos | (uint32_t)__ldg(reinterpret_cast<const int *>(A.tab + i) + 2));
+        else return mix64(pos | (uint32_t)__ldg(&tab[i].gid));
     };
     const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);  // an overflowed level holds cap records
     const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -177,43 +217,42 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     int par = 0;
     for (unsigned long long t0 = (unsigned long long)blockIdx.x * kFTile; t0 < n_in;
          t0 += (unsigned long long)gridDim.x * kFTile, par ^= 1) {
-        uint32_t M[kFRec], sv[kFRec], vb[kFRec], keep[kFRec];
+        T M[kFRec], keep[kFRec];
+        uint32_t sv[kFRec], vb[kFRec];
         uint64_t S[kFRec];
         ulonglong2 r[kFRec];
 #pragma unroll
         for (int k = 0; k < kFRec; k++) {  // all loads first: kFRec records in flight per thread
             const unsigned long long i = t0 + k * kFThreads + threadIdx.x;
-            r[k] = i < n_in ? __ldcs(A.in + i) : make_ulonglong2(0, 0);
+            S[k] = 0;
+            r[k] = i < n_in ? FT<T>::ld(A, i, S[k]) : make_ulonglong2(0, 0);
         }
         uint32_t nk = 0;
 #pragma unroll
         for (int k = 0; k < kFRec; k++) {
             const unsigned long long i = t0 + k * kFThreads + threadIdx.x;
-            M[k] = (uint32_t)r[k].x;
-            const uint32_t u = (uint32_t)(r[k].x >> 32) & 31u;
-            const uint32_t s = (uint32_t)(r[k].x >> 37) & 31u;
+            uint32_t u, s;
+            FT<T>::dec(r[k], M[k], u, s, vb[k]);
             sv[k] = s;
-            vb[k] = (uint32_t)(r[k].x >> 42);
-            S[k] = r[k].y;
             keep[k] = 0;
-            uint32_t cc = 0;
+            T cc = 0;
             bool head_closed = false;
             if (i < n_in) {
-                cc = sinof(vb[k] + u) & (~M[k] | (1u << s));
-                head_closed = (pinof(vb[k] + s) & ~M[k]) == 0u;  // pred(s) within M = M' \ {w}
-                f.ext += __popc(cc);
+                cc = sinof(vb[k] + u) & (~M[k] | ((T)1 << s));
+                head_closed = (pinof(vb[k] + s) & ~M[k]) == 0;  // pred(s) within M = M' \ {w}
+                f.ext += FT<T>::popc(cc);
             }
             // warp-uniform child loop; prime paths are queued and hashed 32 at a time
-            const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(cc));
+            const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)FT<T>::popc(cc));
             for (int it = 0; it < maxc; it++) {
                 bool em = false;
                 uint64_t Sx = 0;
                 if (cc) {
-                    const uint32_t w = __ffs(cc) - 1;
-                    cc &= cc - 1u;
-                    const uint32_t cw = (w == s) ? 0u : (sinof(vb[k] + w) & (~(M[k] | (1u << w)) | (1u << s)));
+                    const uint32_t w = FT<T>::ffs(cc) - 1;
+                    cc &= cc - 1;
+                    const T cw = (w == s) ? (T)0 : (sinof(vb[k] + w) & (~(M[k] | ((T)1 << w)) | ((T)1 << s)));
                     if (cw) {
-                        keep[k] |= 1u << w;
+                        keep[k] |= (T)1 << w;
                     } else if (w == s || head_closed) {  // cycle closure, or an internal prime path
                         em = true;
                         Sx = S[k] + mixof(vb[k] + w);
@@ -229,7 +268,7 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
                     __syncwarp();
                 }
             }
-            nk += __popc(keep[k]);
+            nk += FT<T>::popc(keep[k]);
         }
         // block compaction: warp scans, one atomicAdd per tile
         uint32_t inc = nk;
@@ -257,12 +296,11 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
                 unsigned long long j = bb + woff + (inc - nk);
 #pragma unroll
                 for (int k = 0; k < kFRec; k++) {
-                    uint32_t kp = keep[k];
+                    T kp = keep[k];
                     while (kp) {
-                        const uint32_t w = __ffs(kp) - 1;
-                        kp &= kp - 1u;
-                        __stcs(A.out + j, make_ulonglong2(fkey(M[k] | (1u << w), w, sv[k], vb[k]),
-                                                          S[k] + mixof(vb[k] + w)));
+                        const uint32_t w = FT<T>::ffs(kp) - 1;
+                        kp &= kp - 1;
+                        FT<T>::st(A, j, M[k] | ((T)1 << w), w, sv[k], vb[k], S[k] + mixof(vb[k] + w));
                         j++;
                     }
                 }

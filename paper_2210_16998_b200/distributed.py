@@ -36,10 +36,12 @@ def _signed(u: int) -> int:
 
 
 def sharded_prime_paths(graph, group=None, *, device: Optional[int] = None, mode: str = "materialize",
-                        digest: bool = True, compute: Optional[Callable[[int, int], PathSet]] = None
-                        ) -> ShardResult:
+                        digest: bool = True, compute: Optional[Callable[[int, int], PathSet]] = None,
+                        engine: str = "dfs") -> ShardResult:
     """This rank's prime paths plus their place in the global list.
 
+    ``engine="frontier"`` (with ``mode="count"``) runs the level-synchronous engine on
+    this rank's start vertices; the exchange is the same.
     ``compute(rank, world)`` replaces the GPU call (a test seam: the gloo tests run
     the collective logic on CPU with the oracle's shards)."""
     import torch
@@ -48,7 +50,7 @@ def sharded_prime_paths(graph, group=None, *, device: Optional[int] = None, mode
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     if compute is None:
         dev = torch.cuda.current_device() if device is None else device
-        ps = prime_paths(graph, device=dev, shard=(rank, world), mode=mode, digest=digest)
+        ps = prime_paths(graph, device=dev, shard=(rank, world), mode=mode, digest=digest, engine=engine)
     else:
         ps = compute(rank, world)
     st = ps.stats

@@ -42,6 +42,29 @@ def test_frontier_matches_oracle():
         assert _frontier(g) == _oracle_stats(g), g.name
 
 
+def _wide_corpus():
+    """SCCs of 33..64 vertices: the 64-bit-mask records (24 bytes: mask, meta | S)."""
+    yield gen.dense_scc(36, 2, 3)
+    yield gen.dense_scc(40, 2, 4)
+    yield gen.from_arcs(64, [(i, (i + 1) % 64) for i in range(64)] + [(i, (i + 7) % 64) for i in range(0, 64, 8)])
+    yield gen.disjoint_union([gen.dense_scc(34, 2, 9), gen.dense_scc(7, 3, 10), gen.from_arcs(1, [(0, 0)]),
+                              gen.from_arcs(2, [])], name="wide-union")
+
+
+def test_frontier_wide_masks_match_oracle():
+    for g in _wide_corpus():
+        assert _frontier(g) == _oracle_stats(g), g.name
+
+
+def test_frontier_wide_masks_chunked(monkeypatch):
+    monkeypatch.setenv("TPGEN_FRONTIER_CHUNK", "512")
+    g = gen.dense_scc(36, 2, 3)
+    st = tp.prime_paths(g, mode="count", digest=True, engine="frontier").stats
+    assert st["gpu_launches"] > st["max_scc"] + 1
+    assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
+            "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == _oracle_stats(g)
+
+
 def test_frontier_start_ranges_add_up():
     g = gen.disjoint_union([gen.dense_scc(10, 3, 7), gen.from_arcs(3, [(0, 0), (1, 2), (2, 1)]),
                             gen.dense_scc(9, 3, 8)], name="ranges")
@@ -85,7 +108,7 @@ def test_frontier_dfs_chunked(monkeypatch):
 
 
 def test_frontier_rejects_non_lean_graphs():
-    for g in (gen.fig1b(), gen.config5(K=2, n=40)):
+    for g in (gen.fig1b(), gen.config5(K=2, n=40), gen.from_arcs(70, [(i, (i + 1) % 70) for i in range(70)])):
         with pytest.raises(tp.TpgenError) as e:
             _frontier(g)
         assert e.value.status_name.endswith("INVALID_ARGUMENT")

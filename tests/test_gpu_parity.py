@@ -424,5 +424,10 @@ def test_sharded_prime_paths_nccl_single_rank():
         np.testing.assert_array_equal(v, rv)
         assert res.pp_base == 0 and res.vertex_base == 0 and res.n_paths == len(ro) - 1
         assert res.digest == oracle.digest(ro, rv)
+        g = gen.dense_scc(14, 3, 9)  # the frontier engine's count mode through the same exchange
+        res = sharded_prime_paths(g, mode="count", engine="frontier")
+        ro, rv = oracle.prime_paths(g)
+        assert res.n_paths == len(ro) - 1 and res.total_vertices == int(ro[-1])
+        assert res.n_extensions == oracle.ext_count(g) and res.digest == oracle.digest(ro, rv)
     finally:
         dist.destroy_process_group()
