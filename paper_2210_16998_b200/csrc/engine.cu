@@ -128,7 +128,8 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     P.presplit_lo = P.presplit_hi = -1;  // a new graph: the cached pre-split roots are stale
     P.presplit_n = 0;
     P.presplit_roots_n = -1;
-    P.f_tab_ok = false;  // frontier engine: slot table and record high-water mark belong to the old graph
+    P.f_tab_ok = false;  // frontier engine: slot table, roots and record high-water mark belong to the old graph
+    P.f_roots_lo = P.f_roots_hi = -1;
     P.f_cap_hwm = 0;
     P.any_exit = false;  // no arc leaves any SCC: the LEAN DFS applies
     for (int32_t i = 0; i < H.n; i++)
@@ -1253,12 +1254,16 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         TPG_TRY(upload(P.f_tab, tab, s));
         P.f_tab_ok = true;
     }
-    std::vector<int32_t> roots;  // slots, then slot bases
-    roots.reserve(2 * (size_t)std::max(hi - lo, 0));
-    for (int32_t v = lo; v < hi; v++) roots.push_back(H.v_slot[v]);
-    for (int32_t v = lo; v < hi; v++) roots.push_back(H.scc_vbase[H.comp[v]]);
     const int32_t n_roots = std::max(hi - lo, 0);
-    if (n_roots) TPG_TRY(upload(P.f_roots, roots, s));
+    if (n_roots && !(P.f_roots_lo == lo && P.f_roots_hi == hi)) {  // root table cached per start range
+        std::vector<int32_t> roots;  // slots, then slot bases
+        roots.reserve(2 * (size_t)n_roots);
+        for (int32_t v = lo; v < hi; v++) roots.push_back(H.v_slot[v]);
+        for (int32_t v = lo; v < hi; v++) roots.push_back(H.scc_vbase[H.comp[v]]);
+        TPG_TRY(upload(P.f_roots, roots, s));
+        P.f_roots_lo = lo;
+        P.f_roots_hi = hi;
+    }
     const int Lmax = std::max(H.max_scc, 1);  // records exist for paths of 1..max_scc vertices
     const size_t nctr = 8 + (size_t)Lmax + 2;
     TPG_TRY(P.f_ctr.ensure(nctr * 8, s));
@@ -1267,14 +1272,22 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     for (int32_t v = lo; v < hi; v++) est += H.cost[v];
     uint64_t cap = std::max<uint64_t>({1ull << 22, (uint64_t)(est / 4), P.f_cap_hwm + P.f_cap_hwm / 4});
     if (const char *ev = getenv("TPGEN_FRONTIER_CAP")) cap = std::max<uint64_t>(64, atoll(ev));  // test hook: retries
-    size_t free_b = 0, total_b = 0;
-    TPG_CK(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t cap_max = (uint64_t)((double)(free_b + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / kRecB);
+    uint64_t cap_max = ~0ull;  // memory budget: queried only when a buffer has to grow
+    auto budget = [&]() -> tpgen_status {
+        size_t free_b = 0, total_b = 0;
+        TPG_CK(cudaMemGetInfo(&free_b, &total_b));
+        cap_max = (uint64_t)((double)(free_b + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / kRecB);
+        return TPGEN_OK;
+    };
+    if (cap * kRecB > std::min(P.f_buf0.cap, P.f_buf1.cap)) TPG_TRY(budget());
     const size_t smem = (size_t)n_tab * sizeof(FSm<T>);
     const bool ts = smem <= 32 * 1024;
-    int per_sm = 0;  // persistent grid: every block resident
-    if (ts) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, true>, kFThreads, smem));
-    else TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, false>, kFThreads, 0));
+    static int occ[2] = {0, 0};  // resident blocks per SM of the two variants (per build; queried once)
+    int &per_sm = occ[ts ? 1 : 0];
+    if (per_sm == 0) {
+        if (ts) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, true>, kFThreads, 32 * 1024));
+        else TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, false>, kFThreads, 0));
+    }
     const int grid = P.num_sms * std::max(per_sm, 1);
     Timer tall;
     std::vector<unsigned long long> h(nctr);
@@ -1339,6 +1352,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             break;
         }
         st.n_count_rounds = attempt + 1;
+        if (cap_max == ~0ull) TPG_TRY(budget());
         if (cap >= cap_max) {  // no level fits: the DFS-chunked frontier in the same memory
             chunked = true;
             capc = cap_max * 2 / (uint64_t)(Lmax + 1);
@@ -1347,6 +1361,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         cap = std::max<uint64_t>(2 * cap, peak + peak / 4);  // a truncated level under-counts the next ones
     }
     if (chunked) {
+        if (cap_max == ~0ull) TPG_TRY(budget());
         // DFS over chunks of levels (the north star's "DFS-chunked when the frontier would
         // overflow HBM"): one buffer of capc records per level; a chunk of level l holds at
         // most capc / D records (D = the largest out-degree), so its children always fit in

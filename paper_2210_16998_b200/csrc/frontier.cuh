@@ -188,6 +188,8 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     __shared__ unsigned long long red[5][kFThreads / 32];
     __shared__ uint64_t pqs[kFThreads / 32][64];  // per warp: digest sums S of prime paths awaiting their hash
     const uint64_t pos = (uint64_t)(A.l + 1) << 32;  // position of the new vertex
+    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);  // an overflowed level holds cap records
+    if ((unsigned long long)blockIdx.x * kFTile >= n_in) return;  // small levels: idle blocks leave at once
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
             const FSlot<T> t = tab[i];
@@ -207,7 +209,6 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
         if constexpr (TS) return st[i].mix;
         else return mix64(pos | (uint32_t)__ldg(&tab[i].gid));
     };
-    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);  // an overflowed level holds cap records
     const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path (every prime path found at this level)
