@@ -166,26 +166,62 @@ class ClockSampler:
 CONFIG3_WORKLOAD = "config3: dense SCC n=22 out-degree 4 seed 1"  # the workload both arms name
 
 
-def run_reference(args):
-    """The CPU oracle as it stands, single core, bounded sample per step."""
+def _oracle_block(s: int):
+    """Worker: the oracle's prime paths of config 3's start vertex s (count, seconds)."""
     import oracle
 
+    g, _ = workload(1)
+    t = time.perf_counter()
+    off, _ = oracle.prime_paths(g, v_lo=s, v_hi=s + 1)
+    return len(off) - 1, time.perf_counter() - t
+
+
+def _oracle_warm(_):
+    import oracle  # noqa: F401  (loads liboracle.so in the worker)
+
+    workload(1)
+    return 0
+
+
+class OraclePool:
+    """The oracle as it stands, run on the host's cores: one process per start vertex
+    of config 3 (independent per-start enumerations; no change to the oracle)."""
+
+    def __init__(self):
+        import multiprocessing as mp
+
+        self.cores = max(1, min(os.cpu_count() or 1, 22))
+        self.pool = mp.get_context("spawn").Pool(self.cores)
+        self.pool.map(_oracle_warm, range(self.cores))
+
+    def step(self):
+        t = time.perf_counter()
+        res = self.pool.map(_oracle_block, range(22), chunksize=1)
+        return sum(r[0] for r in res), time.perf_counter() - t
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def run_reference(args):
+    """The CPU oracle as it stands on the host's cores; each step = all of config 3."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     g, _ = workload(1)
-    starts = list(range(0, 4))  # bounded sample: start vertices 0..3 of config 3 (~2.5 s per step)
+    op = OraclePool()
     times, npp = [], 0
     for i in range(args.warmup + args.steps):
-        t = time.perf_counter()
-        off, _ = oracle.prime_paths(g, v_lo=starts[0], v_hi=starts[-1] + 1)
-        dt = time.perf_counter() - t
+        n, dt = op.step()
         if i >= args.warmup:
             times.append(dt)
-            npp = len(off) - 1
+            npp = n
+    op.close()
     total = sum(times)
     value = npp * len(times) / total
-    sample = f"config3 start vertices {starts[0]}..{starts[-1]} ({npp} prime paths per step), oracle/oracle.c DFS"
+    sample = (f"all of config3 ({npp} prime paths per step): its 22 start vertices as independent oracle calls "
+              f"(oracle/oracle.c DFS) on {op.cores} processes")
     print(json.dumps({
         "impl": "reference", "metric": "prime_paths_per_sec", "value": value, "unit": "PP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -193,7 +229,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": CONFIG3_WORKLOAD, "n_vertices": g.n, "parallelism": "start-vertex shards x1",
                    "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "PP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "PP/s", "cores": op.cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "PP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -206,8 +242,17 @@ def cpu_baseline_leg():
     off, _ = oracle.prime_paths(g, v_lo=0, v_hi=4)
     dt = time.perf_counter() - t
     npp = len(off) - 1
-    return {"value": npp / dt, "unit": "PP/s", "cores": 1, "kind": "oracle",
-            "sample": f"config3 start vertices 0..3: {npp} prime paths in {dt:.2f} s (single core, oracle/oracle.c)"}
+    out = {"value": npp / dt, "unit": "PP/s", "cores": 1, "kind": "oracle",
+           "sample": f"config3 start vertices 0..3: {npp} prime paths in {dt:.2f} s (single core, oracle/oracle.c)"}
+    try:  # the same oracle on the host's cores: all of config 3, one process per start vertex
+        op = OraclePool()
+        n, wall = op.step()
+        op.close()
+        out["all_cores"] = {"value": n / wall, "unit": "PP/s", "cores": op.cores, "kind": "oracle",
+                            "sample": f"all of config3: {n} prime paths in {wall:.2f} s on {op.cores} processes"}
+    except Exception as e:  # noqa: BLE001 -- the single-core figure stands on its own
+        out["all_cores"] = {"unavailable": str(e)[:200]}
+    return out
 
 
 def main():
