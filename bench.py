@@ -271,6 +271,8 @@ def main():
     ap.add_argument("--engine", default="dfs", choices=["dfs", "frontier"],
                     help="dfs (default): depth-first engine, full output; frontier: the level-synchronous "
                          "frontier engine on config 3 in COUNT_HASH mode (counts + digest; DESIGN.md 6.6)")
+    ap.add_argument("--no-digest", action="store_true",
+                    help="with --count / --engine frontier: counts and E_canon only (no digest)")
     ap.add_argument("--count", action="store_true",
                     help="config 3 in COUNT_HASH mode (counts + digest, no output) with the chosen engine")
     args = ap.parse_args()
@@ -302,7 +304,7 @@ def main():
         g, ranges = workload(world)
         kw = dict(start_range=ranges[rank])
         if cnt3:
-            kw.update(mode="count", digest=True, engine=args.engine)
+            kw.update(mode="count", digest=not args.no_digest, engine=args.engine)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -433,8 +435,8 @@ def main():
                                   "kernel": f"expand_fast_kernel<{max(1, (int(st['max_scc']) + 3) // 4)},true>",
                                   "ms_per_launch": ms_expand, "share_of_step": ms_expand / ms_dev}
             roofline["path_hbm"]["model"] = "SURVEY 8(d): 26 B/extension (no output in COUNT_HASH mode)"
-        if fr:  # every frontier record is written once and read once: 16 B each way
-            f_bytes = 32.0 * st["n_units"]
+        if fr:  # every frontier record is written once and read once: 16 B each way (8 B without digest)
+            f_bytes = (16.0 if args.no_digest else 32.0) * st["n_units"]
             f_ach = f_bytes / (ms_dfs * 1e-3) / 1e9
             roofline = {
                 "bound": "hbm", "kernel": "frontier_level_kernel<TS=1> (all levels + root kernel)",
@@ -466,7 +468,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": ("config5: 16 parallel SCCs n=56 out-degree 2 seed 5, COUNT_HASH (counts + "
                                     "digest, output not materialized)" if c5 else
-                                    CONFIG3_WORKLOAD + (f", COUNT_HASH, {args.engine} engine" if cnt3 else "") +
+                                    CONFIG3_WORKLOAD + (f", COUNT_HASH{' without digest' if args.no_digest else ''}, "
+                                                       f"{args.engine} engine" if cnt3 else "") +
                                     (f" x{world} disjoint copies, one per rank" if world > 1 else "")),
                        "n_vertices": g.n, "prime_paths_per_rank": n_pp, "output_vertices_per_rank": n_vert,
                        "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",

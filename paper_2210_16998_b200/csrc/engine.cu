@@ -1222,7 +1222,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
 // extension of all paths of one length at a time; counts, E_canon and digest.
 template <class T>
 static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
-    constexpr size_t kRecB = sizeof(T) == 4 ? 16 : 24;  // bytes per frontier record (key + S)
+    const bool hash = o.compute_digest != 0;  // without the digest: no S, no mixing
+    const size_t kRecB = (sizeof(T) == 4 ? 8 : 16) + (hash ? 8 : 0);  // bytes per frontier record (key [+ S])
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
@@ -1282,12 +1283,15 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     if (cap * kRecB > std::min(P.f_buf0.cap, P.f_buf1.cap)) TPG_TRY(budget());
     const size_t smem = (size_t)n_tab * sizeof(FSm<T>);
     const bool ts = smem <= 32 * 1024;
-    static int occ[2] = {0, 0};  // resident blocks per SM of the two variants (per build; queried once)
-    int &per_sm = occ[ts ? 1 : 0];
-    if (per_sm == 0) {
-        if (ts) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, true>, kFThreads, 32 * 1024));
-        else TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frontier_level_kernel<T, false>, kFThreads, 0));
-    }
+    void (*const level_k)(FrontierArgs) =
+        ts ? (hash ? frontier_level_kernel<T, true, true> : frontier_level_kernel<T, true, false>)
+           : (hash ? frontier_level_kernel<T, false, true> : frontier_level_kernel<T, false, false>);
+    void (*const root_k)(FrontierArgs, const int32_t *, const int32_t *, int32_t) =
+        hash ? frontier_root_kernel<T, true> : frontier_root_kernel<T, false>;
+    const size_t lsmem = ts ? smem : 0;
+    static int occ[2][2] = {{0, 0}, {0, 0}};  // resident blocks per SM per variant (per build; queried once)
+    int &per_sm = occ[ts ? 1 : 0][hash ? 1 : 0];
+    if (per_sm == 0) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_k, kFThreads, ts ? 32 * 1024 : 0));
     const int grid = P.num_sms * std::max(per_sm, 1);
     Timer tall;
     std::vector<unsigned long long> h(nctr);
@@ -1323,7 +1327,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             A.cnt_in = nullptr;
             A.cnt_out = ctr + 8;
             A.l = -1;
-            frontier_root_kernel<T><<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
+            root_k<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
             for (int l = 0; l < Lmax; l++) {
@@ -1334,8 +1338,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
                 A.cnt_in = ctr + 8 + l;
                 A.cnt_out = ctr + 8 + l + 1;
                 A.l = l;
-                if (ts) frontier_level_kernel<T, true><<<grid, kFThreads, smem, s>>>(A);
-                else frontier_level_kernel<T, false><<<grid, kFThreads, 0, s>>>(A);
+                level_k<<<grid, kFThreads, lsmem, s>>>(A);
                 launches++;
             }
         }
@@ -1372,7 +1375,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             set_error("frontier chunk buffers too small for the roots (use the DFS engine)");
             return TPGEN_ERR_OUT_OF_MEMORY;
         }
-        TPG_TRY(P.f_buf0.ensure((size_t)(Lmax + 1) * capc * kRecB, s));
+        TPG_TRY(P.f_buf0.ensure((size_t)(Lmax + 1) * capc * std::max<size_t>(kRecB, 16), s));  // 16-B level stride
         ulonglong2 *base = P.f_buf0.as<ulonglong2>();
         uint64_t *baseS = reinterpret_cast<uint64_t *>(base + (size_t)(Lmax + 1) * capc);
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
@@ -1393,7 +1396,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             A.cnt_in = nullptr;
             A.cnt_out = ctr + 8;
             A.l = -1;
-            frontier_root_kernel<T><<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
+            root_k<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
             TPG_CK(cudaMemcpyAsync(&nl[0], ctr + 8, 8, cudaMemcpyDeviceToHost, s));
@@ -1409,7 +1412,8 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             }
             const uint64_t k = std::min<uint64_t>(nl[l] - cur[l], chunk);
             TPG_CK(cudaMemsetAsync(ctr + 8 + l + 1, 0, 8, s));
-            A.in = base + (size_t)l * capc + cur[l];
+            const size_t key_b = (sizeof(T) == 4 && !hash) ? 8 : 16;  // bytes per record in the key array
+            A.in = reinterpret_cast<ulonglong2 *>(reinterpret_cast<char *>(base + (size_t)l * capc) + cur[l] * key_b);
             A.in_S = baseS + (size_t)l * capc + cur[l];
             A.out = base + (size_t)(l + 1) * capc;
             A.out_S = baseS + (size_t)(l + 1) * capc;
@@ -1417,8 +1421,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             A.cnt_out = ctr + 8 + l + 1;
             A.lim = k;
             A.l = l;
-            if (ts) frontier_level_kernel<T, true><<<grid, kFThreads, smem, s>>>(A);
-            else frontier_level_kernel<T, false><<<grid, kFThreads, 0, s>>>(A);
+            level_k<<<grid, kFThreads, lsmem, s>>>(A);
             launches++;
             cur[l] += k;
             if (l + 1 < Lmax) {  // level l+1 records can have children: descend

@@ -93,7 +93,12 @@ template <>
 struct FT<uint32_t> {
     __device__ static int ffs(uint32_t x) { return __ffs(x); }
     __device__ static int popc(uint32_t x) { return __popc(x); }
+    template <bool HASH>
     __device__ static ulonglong2 ld(const FrontierArgs &A, unsigned long long i, uint64_t &S) {
+        if constexpr (!HASH) {  // counts only: 8-byte records (the key)
+            S = 0;
+            return make_ulonglong2(__ldcs(reinterpret_cast<const unsigned long long *>(A.in) + i), 0);
+        }
         const ulonglong2 r = __ldcs(A.in + i);
         S = r.y;
         return r;
@@ -104,17 +109,20 @@ struct FT<uint32_t> {
         s = (uint32_t)(r.x >> 37) & 31u;
         vb = (uint32_t)(r.x >> 42);
     }
+    template <bool HASH>
     __device__ static void st(const FrontierArgs &A, unsigned long long j, uint32_t M, uint32_t w, uint32_t s,
                               uint32_t vb, uint64_t S) {
-        __stcs(A.out + j, make_ulonglong2(fkey(M, w, s, vb), S));
+        if constexpr (HASH) __stcs(A.out + j, make_ulonglong2(fkey(M, w, s, vb), S));
+        else __stcs(reinterpret_cast<unsigned long long *>(A.out) + j, (unsigned long long)fkey(M, w, s, vb));
     }
 };
 template <>
 struct FT<uint64_t> {
     __device__ static int ffs(uint64_t x) { return __ffsll((long long)x); }
     __device__ static int popc(uint64_t x) { return __popcll(x); }
+    template <bool HASH>
     __device__ static ulonglong2 ld(const FrontierArgs &A, unsigned long long i, uint64_t &S) {
-        S = __ldcs(reinterpret_cast<const unsigned long long *>(A.in_S) + i);
+        S = HASH ? __ldcs(reinterpret_cast<const unsigned long long *>(A.in_S) + i) : 0ull;
         return __ldcs(A.in + i);
     }
     __device__ static void dec(const ulonglong2 &r, uint64_t &M, uint32_t &u, uint32_t &s, uint32_t &vb) {
@@ -123,16 +131,17 @@ struct FT<uint64_t> {
         s = (uint32_t)(r.y >> 6) & 63u;
         vb = (uint32_t)(r.y >> 12);
     }
+    template <bool HASH>
     __device__ static void st(const FrontierArgs &A, unsigned long long j, uint64_t M, uint32_t w, uint32_t s,
                               uint32_t vb, uint64_t S) {
         __stcs(A.out + j, make_ulonglong2(M, (uint64_t)w | ((uint64_t)s << 6) | ((uint64_t)vb << 12)));
-        __stcs(reinterpret_cast<unsigned long long *>(A.out_S) + j, (unsigned long long)S);
+        if constexpr (HASH) __stcs(reinterpret_cast<unsigned long long *>(A.out_S) + j, (unsigned long long)S);
     }
 };
 
 // Roots: one record per start vertex of a nontrivial SCC; an isolated vertex
 // (no arc at all in a graph where no arc leaves any SCC) is itself a prime path.
-template <class T>
+template <class T, bool HASH>
 __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, const int32_t *root_vb, int32_t n) {
     FAcc f;
     unsigned int write = 0;
@@ -144,9 +153,13 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
         vb = (uint32_t)root_vb[i];
         const FSlot<T> t = static_cast<const FSlot<T> *>(A.tab)[slot];
         s = (uint32_t)slot - vb;
-        S = mix64((uint64_t)(uint32_t)t.gid);  // position 0
-        if (t.sin == 0) f.emit(S, 1);
-        else write = 1;
+        S = HASH ? mix64((uint64_t)(uint32_t)t.gid) : 0ull;  // position 0
+        if (t.sin == 0) {
+            if constexpr (HASH) f.emit(S, 1);
+            else f.pp++, f.vert++;
+        } else {
+            write = 1;
+        }
     }
     const unsigned int lane = threadIdx.x & 31;
     const unsigned int bal = __ballot_sync(0xffffffffu, write);
@@ -155,7 +168,7 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
     base = __shfl_sync(0xffffffffu, base, 0);
     if (write) {
         const unsigned long long j = base + __popc(bal & ((1u << lane) - 1u));
-        if (j < A.cap) FT<T>::st(A, j, (T)1 << s, s, s, vb, S);
+        if (j < A.cap) FT<T>::template st<HASH>(A, j, (T)1 << s, s, s, vb, S);
         else atomicOr(A.overflow, 1u);
     }
     f.flush(A.acc);
@@ -178,7 +191,7 @@ struct FSm {  // shared-memory slot entry
     uint64_t mix;  // mix64((l+1) << 32 | gid)
 };
 
-template <class T, bool TS>
+template <class T, bool TS, bool HASH>
 __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs A) {
     extern __shared__ int4 fsm[];
     FSm<T> *st = reinterpret_cast<FSm<T> *>(fsm);
@@ -226,7 +239,7 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
         for (int k = 0; k < kFRec; k++) {  // all loads first: kFRec records in flight per thread
             const unsigned long long i = t0 + k * kFThreads + threadIdx.x;
             S[k] = 0;
-            r[k] = i < n_in ? FT<T>::ld(A, i, S[k]) : make_ulonglong2(0, 0);
+            r[k] = i < n_in ? FT<T>::template ld<HASH>(A, i, S[k]) : make_ulonglong2(0, 0);
         }
         uint32_t nk = 0;
 #pragma unroll
@@ -256,8 +269,12 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
                         keep[k] |= (T)1 << w;
                     } else if (w == s || head_closed) {  // cycle closure, or an internal prime path
                         em = true;
-                        Sx = S[k] + mixof(vb[k] + w);
+                        if constexpr (HASH) Sx = S[k] + mixof(vb[k] + w);
                     }
+                }
+                if constexpr (!HASH) {  // counts only
+                    if (em) f.pp++, f.vert += len;
+                    continue;
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, em);
                 if (em) pq[qn + __popc(bal & lt)] = Sx;
@@ -301,7 +318,9 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
                     while (kp) {
                         const uint32_t w = FT<T>::ffs(kp) - 1;
                         kp &= kp - 1;
-                        FT<T>::st(A, j, M[k] | ((T)1 << w), w, sv[k], vb[k], S[k] + mixof(vb[k] + w));
+                        uint64_t Sw = 0;
+                        if constexpr (HASH) Sw = S[k] + mixof(vb[k] + w);
+                        FT<T>::template st<HASH>(A, j, M[k] | ((T)1 << w), w, sv[k], vb[k], Sw);
                         j++;
                     }
                 }

@@ -65,6 +65,22 @@ def test_frontier_wide_masks_chunked(monkeypatch):
             "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == _oracle_stats(g)
 
 
+def test_frontier_counts_only(monkeypatch):
+    """digest=False: records without the digest sum (8 bytes for 32-bit masks, 16 for
+    64-bit) and no hashing; counts and E_canon equal to the oracle's, in one pass and
+    DFS-chunked."""
+    graphs = list(_lean_corpus()) + list(_wide_corpus())
+    for chunk in (None, "300"):
+        if chunk:
+            monkeypatch.setenv("TPGEN_FRONTIER_CHUNK", chunk)
+        for g in graphs:
+            st = tp.prime_paths(g, mode="count", digest=False, engine="frontier").stats
+            ref = _oracle_stats(g)
+            assert (st["n_paths"], st["total_vertices"], st["n_extensions"]) == \
+                (ref["n_paths"], ref["total_vertices"], ref["n_extensions"]), (g.name, chunk)
+            assert (st["hash_lo"], st["hash_hi"]) == (0, 0)
+
+
 def test_frontier_start_ranges_add_up():
     g = gen.disjoint_union([gen.dense_scc(10, 3, 7), gen.from_arcs(3, [(0, 0), (1, 2), (2, 1)]),
                             gen.dense_scc(9, 3, 8)], name="ranges")
@@ -136,6 +152,9 @@ def test_frontier_config3_full_size():
     assert c["gpu_launches"] > 100
     for k in ("n_paths", "total_vertices", "n_extensions", "hash_lo", "hash_hi"):
         assert c[k] == f[k], k
+    n = plan.prime_paths(mode="count", digest=False, engine="frontier").stats  # counts only
+    for k in ("n_paths", "total_vertices", "n_extensions"):
+        assert n[k] == f[k], k
     assert f["n_extensions"] == oracle.ext_count(g)
     for s in (3, 17):
         st = plan.prime_paths(mode="count", digest=True, engine="frontier", start_range=(s, s + 1)).stats
