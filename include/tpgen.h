@@ -107,8 +107,10 @@ typedef struct {
                                   P:459-472; the north-star's level-by-level kernel): 16-byte path records
                                   {visited mask, last, first, position-keyed digest sum} streamed through HBM,
                                   ping-pong buffers, warp-scan compaction.  Requires output_mode =
-                                  TPGEN_OUT_COUNT_HASH (counts, E_canon and the digest; the order-free
-                                  frontier never materializes the canonical list) and a graph whose SCCs
+                                  TPGEN_OUT_COUNT_HASH (counts, E_canon and -- with compute_digest = 1 --
+                                  the digest; compute_digest = 0 drops the digest sum from the records:
+                                  8-byte records, no mixing; the order-free frontier never materializes
+                                  the canonical list) and a graph whose SCCs
                                   have <= 64 vertices with no arc leaving any SCC (else
                                   TPGEN_ERR_INVALID_ARGUMENT).  A level that does not fit in the device
                                   memory budget switches the call to the DFS-chunked frontier (DESIGN.md
