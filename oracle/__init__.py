@@ -64,6 +64,13 @@ def _load():
         lib.oracle_tp_tables.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32),
                                          ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int32),
                                          P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)]
+        lib.oracle_pp_stats.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32), ctypes.c_int32,
+                                        ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_uint64)]
+        lib.oracle_pp_stats.restype = ctypes.c_int
+        lib.oracle_tp_stats.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_int32), ctypes.c_int32,
+                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64),
+                                        P(ctypes.c_uint64)]
+        lib.oracle_tp_stats.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -134,6 +141,65 @@ def digest(offsets: np.ndarray, vertices: np.ndarray) -> Tuple[int, int]:
     out = (ctypes.c_uint64 * 2)()
     lib.oracle_digest(off.shape[0] - 1, _p64(off), _p32(vert), out)
     return int(out[0]), int(out[1])
+
+
+def pp_stats(g, v_lo: int = 0, v_hi: Optional[int] = None, tp: Optional[Tuple[int, int]] = None) -> np.ndarray:
+    """Per start vertex v in [v_lo, v_hi): (n_paths, n_vertices, hash_lo, hash_hi) of the prime
+    paths whose first vertex is v -- or, with ``tp=(entry, exit)``, of their test paths (R15) --
+    hashed while they are enumerated (oracle_pp_stats / oracle_tp_stats; nothing stored).
+    Returns a uint64 array [v_hi - v_lo, 4]."""
+    lib = _load()
+    so, st = _csr(g)
+    v_hi = g.n if v_hi is None else v_hi
+    k = max(v_hi - v_lo, 0)
+    cnt = np.zeros(2 * max(k, 1), dtype=np.int64)
+    hs = np.zeros(2 * max(k, 1), dtype=np.uint64)
+    ph = hs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    if tp is None:
+        rc = lib.oracle_pp_stats(g.n, _p64(so), _p32(st), v_lo, v_hi, _p64(cnt), ph)
+    else:
+        rc = lib.oracle_tp_stats(g.n, _p64(so), _p32(st), v_lo, v_hi, int(tp[0]), int(tp[1]), _p64(cnt), ph)
+    if rc == -2:
+        raise ValueError("a prime path's endpoints are unreachable from entry / to exit")
+    if rc != 0:
+        raise MemoryError("oracle_pp_stats failed")
+    out = np.zeros((k, 4), dtype=np.uint64)
+    out[:, 0] = cnt[0:2 * k:2]
+    out[:, 1] = cnt[1:2 * k:2]
+    out[:, 2] = hs[0:2 * k:2]
+    out[:, 3] = hs[1:2 * k:2]
+    return out
+
+
+def _stats_worker(a):
+    n, so, st, lo, hi, tp = a
+
+    class _G:
+        pass
+
+    g = _G()
+    g.n, g.offsets, g.targets = n, so, st
+    return lo, pp_stats(g, lo, hi, tp)
+
+
+def pp_stats_parallel(g, v_lo: int = 0, v_hi: Optional[int] = None, tp: Optional[Tuple[int, int]] = None,
+                      procs: Optional[int] = None, chunk: int = 4) -> np.ndarray:
+    """``pp_stats`` over [v_lo, v_hi) split into blocks of ``chunk`` start vertices, run on
+    ``procs`` host processes (the per-start enumerations are independent)."""
+    import multiprocessing as mp
+
+    v_hi = g.n if v_hi is None else v_hi
+    procs = procs or max(1, os.cpu_count() or 1)
+    so, st = _csr(g)
+    jobs = [(g.n, so, st, lo, min(lo + chunk, v_hi), tp) for lo in range(v_lo, v_hi, chunk)]
+    out = np.zeros((max(v_hi - v_lo, 0), 4), dtype=np.uint64)
+    if not jobs:
+        return out
+    build()
+    with mp.get_context("spawn").Pool(min(procs, len(jobs))) as pool:
+        for lo, part in pool.imap_unordered(_stats_worker, jobs):
+            out[lo - v_lo: lo - v_lo + part.shape[0]] = part
+    return out
 
 
 def tp_tables(g, entry: int, exit: int):

@@ -158,13 +158,81 @@ static void g_free(ograph *g) {
     free(g->nontriv);
 }
 
+/* -------------------------------------------------------------- digest */
+static uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return z;
+}
+
+#define SEED_A 0x9E3779B97F4A7C15ULL
+#define SEED_B 0xD1B54A32D192ED03ULL
+
+/* DESIGN.md reading R20: S = sum_i mix(v_i) * (2i + 1), path digest = mix(S ^ (seed + len)). */
+static uint64_t path_hash(uint64_t seed, const int32_t *v, int64_t len) {
+    uint64_t S = 0;
+    for (int64_t i = 0; i < len; i++) S += mix64((uint64_t)(uint32_t)v[i]) * (2 * (uint64_t)i + 1);
+    return mix64(S ^ (seed + (uint64_t)len));
+}
+
 /* ------------------------------------------------------- prime paths */
+/* Test-path context of oracle_tp_stats: the prefix / suffix walks (R15). */
 typedef struct {
-    ovec64 off;   /* path start offsets (n_paths + 1 once finished) */
-    ovec32 vert;  /* concatenated vertices */
+    const int32_t *pre_len, *pre_tab, *suf_len, *suf_tab;
+    int32_t n;
+    int32_t *buf;  /* room for one test path (3n vertices) */
+    int unreachable;
+} otp;
+
+typedef struct {
+    ovec64 off;      /* path start offsets (n_paths + 1 once finished) */
+    ovec32 vert;     /* concatenated vertices */
+    int stats_only;  /* 1: hash every emitted path instead of storing it */
+    int64_t n_paths, n_vert;
+    uint64_t ha, hb;
+    otp *tp;         /* non-NULL: hash the prime path's test path instead of the path */
 } opaths;
 
+static void hash_into(opaths *out, const int32_t *p, int64_t len) {
+    out->n_paths++;
+    out->n_vert += len;
+    out->ha += path_hash(SEED_A, p, len);
+    out->hb += path_hash(SEED_B, p, len);
+}
+
+/* Stats mode: the emitted prime path (closing vertex appended), or its test path
+ * prefix[first] minus its last vertex ++ PP ++ suffix[last] minus its first vertex. */
+static void emit_stats(opaths *out, const int32_t *path, int32_t k, int32_t closing) {
+    otp *t = out->tp;
+    int32_t last = closing >= 0 ? closing : path[k - 1];
+    if (!t) {
+        int32_t buf[k + 1];
+        for (int32_t i = 0; i < k; i++) buf[i] = path[i];
+        if (closing >= 0) buf[k] = closing;
+        hash_into(out, buf, closing >= 0 ? k + 1 : k);
+        return;
+    }
+    int32_t first = path[0];
+    if (t->pre_len[first] < 0 || t->suf_len[last] < 0) {
+        t->unreachable = 1;
+        return;
+    }
+    int64_t m = 0;
+    for (int32_t i = 0; i + 1 < t->pre_len[first]; i++) t->buf[m++] = t->pre_tab[(size_t)first * t->n + i];
+    for (int32_t i = 0; i < k; i++) t->buf[m++] = path[i];
+    if (closing >= 0) t->buf[m++] = closing;
+    for (int32_t i = 1; i < t->suf_len[last]; i++) t->buf[m++] = t->suf_tab[(size_t)last * t->n + i];
+    hash_into(out, t->buf, m);
+}
+
 static int emit(opaths *out, const int32_t *path, int32_t k, int32_t closing) {
+    if (out->stats_only) {
+        emit_stats(out, path, k, closing);
+        return 0;
+    }
     if (v64_push(&out->off, out->vert.len)) return -1;
     for (int32_t i = 0; i < k; i++)
         if (v32_push(&out->vert, path[i])) return -1;
@@ -273,6 +341,75 @@ int oracle_prime_paths(int32_t n, const int64_t *so, const int32_t *st, int32_t 
 
 void oracle_free(void *p) { free(p); }
 
+int oracle_tp_tables(int32_t n, const int64_t *so, const int32_t *st, int32_t entry, int32_t exit_v,
+                     int32_t *pre_len, int32_t *pre_tab, int32_t *suf_len, int32_t *suf_tab);
+
+/*
+ * oracle_pp_stats: for every start vertex v in [v_lo, v_hi), the prime paths
+ * whose first vertex is v, hashed as they are enumerated (same DFS and test as
+ * oracle_prime_paths, nothing stored): cnt[2*(v-v_lo)] = number of paths,
+ * cnt[2*(v-v_lo)+1] = their vertices, hash[2*(v-v_lo)], hash[..+1] = digest.
+ * With entry >= 0 the TEST PATH of every prime path (R15, entry -> exit) is
+ * hashed instead (returns -2 if some prime path's TP does not exist).
+ */
+static int pp_stats_impl(int32_t n, const int64_t *so, const int32_t *st, int32_t v_lo, int32_t v_hi,
+                         int32_t entry, int32_t exit_v, int64_t *cnt, uint64_t *hash) {
+    ograph g;
+    if (g_init(&g, n, so, st)) return -1;
+    int32_t *path = (int32_t *)malloc(((size_t)n + 1) * sizeof(int32_t));
+    int64_t *nxt = (int64_t *)malloc(((size_t)n + 1) * sizeof(int64_t));
+    uint8_t *on = (uint8_t *)calloc((size_t)n + 1, 1);
+    otp tp;
+    memset(&tp, 0, sizeof(tp));
+    int32_t *tabs = NULL;
+    int rc = (!path || !nxt || !on) ? -1 : 0;
+    if (rc == 0 && entry >= 0) {
+        tabs = (int32_t *)malloc(((size_t)2 * n * n + 5 * (size_t)n + 3) * sizeof(int32_t));
+        if (!tabs) rc = -1;
+        else {
+            int32_t *pl = tabs, *sl = tabs + n, *pt = tabs + 2 * (size_t)n, *stb = pt + (size_t)n * n;
+            tp.buf = stb + (size_t)n * n;
+            oracle_tp_tables(n, so, st, entry, exit_v, pl, pt, sl, stb);
+            tp.pre_len = pl;
+            tp.suf_len = sl;
+            tp.pre_tab = pt;
+            tp.suf_tab = stb;
+            tp.n = n;
+        }
+    }
+    if (v_lo < 0) v_lo = 0;
+    if (v_hi > n) v_hi = n;
+    for (int32_t v = v_lo; v < v_hi && rc == 0; v++) {
+        opaths out;
+        memset(&out, 0, sizeof(out));
+        out.stats_only = 1;
+        out.tp = entry >= 0 ? &tp : NULL;
+        rc = pp_from(&g, v, 1, &out, path, nxt, on);
+        cnt[2 * (size_t)(v - v_lo)] = out.n_paths;
+        cnt[2 * (size_t)(v - v_lo) + 1] = out.n_vert;
+        hash[2 * (size_t)(v - v_lo)] = out.ha;
+        hash[2 * (size_t)(v - v_lo) + 1] = out.hb;
+    }
+    if (rc == 0 && tp.unreachable) rc = -2;
+    free(tabs);
+    free(path);
+    free(nxt);
+    free(on);
+    g_free(&g);
+    return rc;
+}
+
+int oracle_pp_stats(int32_t n, const int64_t *so, const int32_t *st, int32_t v_lo, int32_t v_hi, int64_t *cnt,
+                    uint64_t *hash) {
+    return pp_stats_impl(n, so, st, v_lo, v_hi, -1, -1, cnt, hash);
+}
+
+int oracle_tp_stats(int32_t n, const int64_t *so, const int32_t *st, int32_t v_lo, int32_t v_hi, int32_t entry,
+                    int32_t exit_v, int64_t *cnt, uint64_t *hash) {
+    if (entry < 0 || entry >= n || exit_v < 0 || exit_v >= n) return -3;
+    return pp_stats_impl(n, so, st, v_lo, v_hi, entry, exit_v, cnt, hash);
+}
+
 /* ------------------------------------------------------------ E_canon */
 static int64_t count_in_scc(const ograph *g, int32_t s, int32_t *path, int64_t *nxt, uint8_t *on) {
     int64_t cnt = 0;
@@ -328,27 +465,11 @@ int oracle_scc_labels(int32_t n, const int64_t *so, const int32_t *st, int32_t *
 }
 
 /* -------------------------------------------------------------- digest */
-static uint64_t mix64(uint64_t z) {
-    z ^= z >> 30;
-    z *= 0xbf58476d1ce4e5b9ULL;
-    z ^= z >> 27;
-    z *= 0x94d049bb133111ebULL;
-    z ^= z >> 31;
-    return z;
-}
-
-/* DESIGN.md reading R20: S = sum_i mix(i << 32 | v_i), path digest = mix(S ^ (seed + len)). */
-static uint64_t path_hash(uint64_t seed, const int32_t *v, int64_t len) {
-    uint64_t S = 0;
-    for (int64_t i = 0; i < len; i++) S += mix64(((uint64_t)i << 32) | (uint64_t)(uint32_t)v[i]);
-    return mix64(S ^ (seed + (uint64_t)len));
-}
-
 void oracle_digest(int64_t n_paths, const int64_t *off, const int32_t *vert, uint64_t *out2) {
     uint64_t a = 0, b = 0;
     for (int64_t i = 0; i < n_paths; i++) {
-        a += path_hash(0x9E3779B97F4A7C15ULL, vert + off[i], off[i + 1] - off[i]);
-        b += path_hash(0xD1B54A32D192ED03ULL, vert + off[i], off[i + 1] - off[i]);
+        a += path_hash(SEED_A, vert + off[i], off[i + 1] - off[i]);
+        b += path_hash(SEED_B, vert + off[i], off[i + 1] - off[i]);
     }
     out2[0] = a;
     out2[1] = b;

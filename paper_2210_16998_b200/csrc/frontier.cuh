@@ -153,7 +153,7 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
         vb = (uint32_t)root_vb[i];
         const FSlot<T> t = static_cast<const FSlot<T> *>(A.tab)[slot];
         s = (uint32_t)slot - vb;
-        S = HASH ? mix64((uint64_t)(uint32_t)t.gid) : 0ull;  // position 0
+        S = HASH ? mix64((uint64_t)(uint32_t)t.gid) : 0ull;  // position 0 (weight 1)
         if (t.sin == 0) {
             if constexpr (HASH) f.emit(S, 1);
             else f.pp++, f.vert++;
@@ -179,7 +179,7 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
 // reserves the tile's surviving children with ONE atomicAdd (block scan): the
 // record counter is a single address, and one atomic per warp serialised there
 // (1.5 atomics/ns measured: a warp-per-atomic level kernel ran at 1.1 TB/s).
-// TS: slot table in shared memory as {sin, pin, mix(l+1, gid)} -- the digest
+// TS: slot table in shared memory as {sin, pin, mix(gid) * (2(l+1)+1)} -- the digest
 // term of a vertex at this level's position is computed once per block.
 constexpr int kFThreads = 256;
 constexpr int kFRec = 4;
@@ -188,7 +188,7 @@ constexpr int kFTile = kFThreads * kFRec;
 template <class T>
 struct FSm {  // shared-memory slot entry
     T sin, pin;
-    uint64_t mix;  // mix64((l+1) << 32 | gid)
+    uint64_t mix;  // digest term of the vertex at position l+1: mix64(gid) * (2(l+1) + 1)
 };
 
 template <class T, bool TS, bool HASH>
@@ -200,13 +200,13 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     __shared__ unsigned long long bbase[2];
     __shared__ unsigned long long red[5][kFThreads / 32];
     __shared__ uint64_t pqs[kFThreads / 32][64];  // per warp: digest sums S of prime paths awaiting their hash
-    const uint64_t pos = (uint64_t)(A.l + 1) << 32;  // position of the new vertex
+    const uint64_t pw = pos_weight((uint32_t)(A.l + 1));  // digest weight of the new vertex's position
     const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);  // an overflowed level holds cap records
     if ((unsigned long long)blockIdx.x * kFTile >= n_in) return;  // small levels: idle blocks leave at once
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
             const FSlot<T> t = tab[i];
-            st[i] = FSm<T>{t.sin, t.pin, mix64(pos | (uint32_t)t.gid)};
+            st[i] = FSm<T>{t.sin, t.pin, mix64((uint64_t)(uint32_t)t.gid) * pw};
         }
         __syncthreads();
     }
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     };
     auto mixof = [&](uint32_t i) -> uint64_t {
         if constexpr (TS) return st[i].mix;
-        else return mix64(pos | (uint32_t)__ldg(&tab[i].gid));
+        else return mix64((uint64_t)(uint32_t)__ldg(&tab[i].gid)) * pw;
     };
     const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;

@@ -413,3 +413,61 @@ def test_digest_sensitive_to_vertices_order_and_binding():
     assert _dig([[3, 1, 6, 5, 3], [9, 2, 4, 1, 5]]) != base  # suffixes swapped at position 2
     assert _dig([p + [7], q]) != base and _dig([p[:-1], q]) != base
     assert _dig([p]) != _dig([p, p])  # multiplicity counts
+
+
+# ------------------------------------------------- per-start statistics (streamed)
+def _stats_graphs():
+    gs = [gen.fig1b(), gen.config2(), gen.k_seq_loops(3, 3), gen.k_nested_if(4), gen.config4(K=12),
+          gen.dense_scc(9, 3, 2)]
+    gs += [g for g in _corpus(60, seed0=9100)]
+    return gs
+
+
+def test_pp_stats_equal_materialized_blocks():
+    """oracle_pp_stats (prime paths hashed while enumerated, nothing stored) equals, per
+    start vertex, the count, vertex total and digest of the materialized block
+    (oracle_prime_paths, pinned above) -- the streaming comparison of SURVEY 8(d)."""
+    for g in _stats_graphs():
+        st = oracle.pp_stats(g)
+        for v in range(g.n):
+            o, vv = oracle.prime_paths(g, v_lo=v, v_hi=v + 1)
+            assert (int(st[v, 0]), int(st[v, 1])) == (len(o) - 1, int(o[-1])), (g.name, v)
+            assert (int(st[v, 2]), int(st[v, 3])) == oracle.digest(o, vv), (g.name, v)
+        o, vv = oracle.prime_paths(g)
+        lo, hi = oracle.digest(o, vv)
+        assert (int(st[:, 2].sum(dtype=np.uint64)), int(st[:, 3].sum(dtype=np.uint64))) == (lo, hi)
+
+
+def test_tp_stats_equal_materialized_test_paths():
+    """oracle_tp_stats hashes every prime path's test path (R15) as it is formed: per start
+    vertex equal to the materialized test paths (oracle.test_paths, pinned by the brute-force
+    lexmin walks and the S:536 example above) of that start's prime paths."""
+    for g in (gen.fig1b(), gen.config2(), gen.k_seq_loops(3, 3), gen.config4(K=8)):
+        st = oracle.pp_stats(g, tp=(g.entry, g.exit))
+        for v in range(g.n):
+            o, vv = oracle.prime_paths(g, v_lo=v, v_hi=v + 1)
+            to, tv = oracle.test_paths(g, o, vv, g.entry, g.exit)
+            assert (int(st[v, 0]), int(st[v, 1])) == (len(to) - 1, int(to[-1])), (g.name, v)
+            assert (int(st[v, 2]), int(st[v, 3])) == oracle.digest(to, tv), (g.name, v)
+    g = gen.from_arcs(4, [(0, 1), (1, 0), (2, 3)])  # vertices 2, 3 unreachable from entry 0
+    with pytest.raises(ValueError):
+        oracle.pp_stats(g, tp=(0, 1))
+
+
+def test_pp_stats_parallel_equals_serial():
+    g = gen.config2()
+    assert np.array_equal(oracle.pp_stats_parallel(g, procs=3, chunk=7), oracle.pp_stats(g))
+    assert np.array_equal(oracle.pp_stats_parallel(g, 5, 40, tp=(g.entry, g.exit), procs=2, chunk=3),
+                          oracle.pp_stats(g, 5, 40, tp=(g.entry, g.exit)))
+
+
+def test_digest_single_vertex_and_cycle_closed_forms():
+    """Closed forms of R20 (S = sum_i mix(v_i)(2i+1)): a path <v> and its repetition
+    <v, v> differ only by the weight of the second position, so for every v the two
+    digests differ; a K-cycle's K rotations are K distinct paths with K distinct digests."""
+    ones = [_dig([[v]]) for v in range(50)]
+    assert len(set(ones)) == 50
+    assert all(_dig([[v]]) != _dig([[v, v]]) for v in range(50))
+    K = 7
+    rot = [[(i + j) % K for j in range(K)] + [i] for i in range(K)]
+    assert len({_dig([r]) for r in rot}) == K
