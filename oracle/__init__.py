@@ -179,20 +179,23 @@ def _stats_worker(a):
 
     g = _G()
     g.n, g.offsets, g.targets = n, so, st
-    return lo, pp_stats(g, lo, hi, tp)
+    rows = pp_stats(g, lo, hi, tp)
+    ext = np.asarray([ext_count(g, v, v + 1) for v in range(lo, hi)], dtype=np.uint64).reshape(-1, 1)
+    return lo, np.concatenate([rows, ext], axis=1)
 
 
 def pp_stats_parallel(g, v_lo: int = 0, v_hi: Optional[int] = None, tp: Optional[Tuple[int, int]] = None,
                       procs: Optional[int] = None, chunk: int = 4) -> np.ndarray:
     """``pp_stats`` over [v_lo, v_hi) split into blocks of ``chunk`` start vertices, run on
-    ``procs`` host processes (the per-start enumerations are independent)."""
+    ``procs`` host processes (the per-start enumerations are independent), plus a fifth
+    column: each start vertex's E_canon (``ext_count``).  uint64 array [v_hi - v_lo, 5]."""
     import multiprocessing as mp
 
     v_hi = g.n if v_hi is None else v_hi
     procs = procs or max(1, os.cpu_count() or 1)
     so, st = _csr(g)
     jobs = [(g.n, so, st, lo, min(lo + chunk, v_hi), tp) for lo in range(v_lo, v_hi, chunk)]
-    out = np.zeros((max(v_hi - v_lo, 0), 4), dtype=np.uint64)
+    out = np.zeros((max(v_hi - v_lo, 0), 5), dtype=np.uint64)
     if not jobs:
         return out
     build()

@@ -571,6 +571,101 @@ __global__ void stitch_hash_kernel(StitchArgs A, unsigned long long *acc) {
     }
 }
 
+// Count modes: weights of the HeadS records written by cnt_kernel (x = slot of the head's
+// exit vertex; x < 0: an unused slot).  hw[i] = number of cross prime paths h (+) w (+) ...
+// over every out-of-SCC arc (exit -> w) = sum of W(w); acc[0] += that, acc[1] += their
+// vertices (|h| W(w) + V(w)); acc[2] |= 1 on a total >= 2^62 (LIMIT_EXCEEDED).
+__global__ void head_weight_s_kernel(DevGraph G, const HeadS *heads, int64_t n, uint64_t *hw,
+                                     unsigned long long *acc) {
+    const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
+    uint64_t sw = 0, sv = 0;
+    bool ovf = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const HeadS H = heads[i];
+        uint64_t w = 0;
+        if (H.x >= 0) {
+            const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[H.x].gid));
+            for (int a = 0; a < m.z; a++) {
+                const int32_t x = __ldg(G.out_gid + m.y + a);
+                const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                const uint64_t hi = __umul64hi((uint64_t)H.len, Wx), lo = (uint64_t)H.len * Wx;
+                if (hi || Wx >= (1ull << 62) || lo >= (1ull << 62) || Vx >= (1ull << 62)) ovf = true;
+                w += Wx;
+                sv += lo + Vx;
+            }
+        }
+        hw[i] = w;
+        sw += w;
+        if (w >= (1ull << 62) || sw >= (1ull << 62) || sv >= (1ull << 62)) ovf = true;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const uint64_t a = sw + __shfl_xor_sync(kFull, sw, d), b = sv + __shfl_xor_sync(kFull, sv, d);
+        if (a < sw || b < sv || a >= (1ull << 62) || b >= (1ull << 62)) ovf = true;
+        sw = a;
+        sv = b;
+    }
+    ovf = __any_sync(kFull, ovf);
+    if ((threadIdx.x & 31) == 0) {
+        if (sw) atomicAdd(acc, (unsigned long long)sw);
+        if (sv) atomicAdd(acc + 1, (unsigned long long)sv);
+        if (ovf) atomicOr(acc + 2, 1ull);
+    }
+}
+
+// Count modes: the digest of every cross-SCC prime path h (+) completion from the head's
+// digest sum S(h) (accumulated by the DFS) -- only the completion's vertices are absorbed,
+// at positions |h|, |h|+1, ... (R20: term mix(v) * (2 pos + 1)).  Completion k of a head
+// runs over its exit vertex's out-of-SCC arcs in order (W(w) completions each), then is
+// unranked through the entry tables.  One thread per completion; unused head slots have
+// weight 0 and are never reached.
+__global__ void stitch_hash_s_kernel(StitchArgs A, const HeadS *hs, DevGraph G, unsigned long long *acc) {
+    const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
+    uint64_t sa = 0, sb = 0;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < A.n_comp;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t h = upper_bound_u64(A.comp_off, 0, A.n_heads, g) - 1;
+        const HeadS H = hs[h];
+        uint64_t kk = g - A.comp_off[h];
+        const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[H.x].gid));
+        int32_t x = -1;
+        for (int a = 0; a < m.z; a++) {  // the arc whose completions hold index kk
+            const int32_t xa = __ldg(G.out_gid + m.y + a);
+            const uint64_t Wx = __ldg(G.Wc + xa);
+            if (kk < Wx) {
+                x = xa;
+                break;
+            }
+            kk -= Wx;
+        }
+        uint64_t S = H.S;
+        uint32_t pos = (uint32_t)H.len;
+        while (true) {  // unrank the completion through the entry tables, absorbing each item
+            const int64_t b = A.ibeg[x], e = A.iend[x];
+            const uint64_t bc = A.cum[b];
+            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            const uint64_t k2 = kk - (A.cum[i] - bc);
+            const ItemRec it = A.items[i];
+            const int32_t *src = A.item_pool + it.pool_off;
+            for (int j = 0; j < it.len; j++, pos++) S += __ldg(G.vmix + __ldg(src + j)) * pos_weight(pos);
+            if (it.y < 0) break;
+            x = it.y;
+            kk = k2;
+        }
+        sa += mix64(S ^ (kSeedA + (uint64_t)pos));
+        sb += mix64(S ^ (kSeedB + (uint64_t)pos));
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        sa += __shfl_xor_sync(kFull, sa, d);
+        sb += __shfl_xor_sync(kFull, sb, d);
+    }
+    if ((threadIdx.x & 31) == 0 && (sa | sb)) {
+        atomicAdd(acc, (unsigned long long)sa);
+        atomicAdd(acc + 1, (unsigned long long)sb);
+    }
+}
+
 __global__ void fill_u32_kernel(uint32_t *p, uint32_t v, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }

@@ -1,0 +1,535 @@
+// count.cuh -- the count-mode enumerator (COUNT_HASH calls, prime-path phase) of libtpgen.
+//
+// Same walk as dfs.cuh (per start vertex s, depth-first over the simple paths inside
+// SCC(s); Alg. 4 "ExtendPath"; the maximality test of Def. 1, P:127-130,
+// in its operational form R3), but without the path-delta records: in COUNT_HASH mode
+// the order of the walk is irrelevant (every output is a sum), so a step is written as
+// ONE straight-line, predicated instruction stream that every lane of a warp executes
+// with its own data -- the divergent push / pop / closure / record regions of the
+// record-writing step (each executed by the whole warp whenever any lane needs it)
+// are gone.  Per pass every lane makes exactly one move:
+//   * a pop, if its current node has no untried child left (at the unit's root: the
+//     unit is finished), or
+//   * the take of the lowest untried child w of its current node (one extension): w = s
+//     is a cycle closure, a prime path; otherwise the child's own untried
+//     children c_w = succ(w) & (~(M + w) | {s}) are computed at once and
+//       c_w == 0, pred(s) within M, w not an SCC exit  -> internal prime path (R3);
+//       w an exit, pred(s) within M + w                 -> head segment(s) (R8);
+//       c_w != 0                                        -> the walk descends into w
+//     so a leaf child never costs a push and a pop.
+// Both moves are the same operations on the moved vertex v (the popped one or the
+// child): its digest term mix(v) * (2 pos + 1) (R20) added or subtracted, its visited
+// bit toggled, the depth moved by one.
+// The digest sum S of the current path (R20: sum of mix(v) * (2 pos + 1)) is kept in a
+// register; a prime path found in a pass is queued per warp (S, length) and the warp
+// hashes 32 queued paths at once.  Head segments (rare: exit vertices only) are written
+// as HeadS records into the warp's block of head slots, for stitch_hash_s_kernel.
+//
+// Masks: 32-bit (SCCs <= 32 vertices) keep the untried children of every level on a
+// shared-memory stack (rem[level][lane]); 64-bit recompute them on a pop from the
+// parent's successor set (children are taken in ascending id, so the untried ones are
+// the successors above the child just finished).
+//
+// Work distribution is the persistent work queue of dfs_kernel (claims, ready flags,
+// donation of the shallowest untried children when the queue runs low), with units
+// that carry no per-unit results.
+#pragma once
+
+#include "dfs.cuh"
+
+namespace tpg {
+
+template <class T>
+struct CntLane {
+    T M, rem, sbit, ps, exm;  // visited set, untried children of the current node, bit of s, pred(s), SCC exits
+    int32_t l, r, s, vb;      // depth, unit root depth, start vertex (local), slot base of the SCC
+    uint64_t S;               // digest sum of path[0..l]
+    bool active, done;
+};
+
+// Hot-loop table per slot: in-SCC successor bits and the digest value mix64(gid) (R20),
+// staged in shared memory as {sin, mix} pairs (TS) or read from the global copies.
+template <class T, bool TS>
+struct CntTab {
+    const Slot<1> *g;
+    const uint64_t *gm;
+    uint32_t sb;  // TS: shared-window address of the {sin (8 B), mix (8 B)} table
+    __device__ __forceinline__ T sin(int i) const {
+        if (TS) {
+            if (sizeof(T) == 4) {
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sb + (uint32_t)i * 16u) : "memory");
+                return (T)v;
+            }
+            uint64_t v;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sb + (uint32_t)i * 16u) : "memory");
+            return (T)v;
+        }
+        return (T)__ldg(&g[i].sin[0]);
+    }
+    __device__ __forceinline__ T pin(int i) const { return (T)__ldg(&g[i].pin[0]); }
+    __device__ __forceinline__ uint64_t mix(int i) const {
+        if (TS) {
+            uint64_t v;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sb + (uint32_t)i * 16u + 8u) : "memory");
+            return v;
+        }
+        return __ldg(gm + i);
+    }
+};
+
+__device__ __forceinline__ int ffs_t(uint32_t x) { return __ffs(x) - 1; }
+// m * w mod 2^64 for a 32-bit w: one wide multiply of the low word, one of the high word
+__device__ __forceinline__ uint64_t mul64x32(uint64_t m, uint32_t w) {
+    const uint64_t lo = (uint64_t)(uint32_t)m * w;
+    return lo + ((uint64_t)((uint32_t)(m >> 32) * w) << 32);
+}
+__device__ __forceinline__ int ffs_t(uint64_t x) { return __ffsll((long long)x) - 1; }
+
+template <class T>
+struct CntCfg {
+    static constexpr bool RS = sizeof(T) == 4;  // untried children on a shared-memory stack
+    static constexpr int PLEV = RS ? 32 : 64;   // path levels per lane
+    static constexpr int threads = 256, warps = 8, min_blocks = 3;
+    static constexpr int ring = 8;              // prime paths a lane holds between two warp drains
+};
+
+// Shared-memory layouts (per warp, [row][lane] so the 32 lanes of a row never conflict):
+// the lanes' event rings -- digest sums [slot][lane] (8 B) and tags [slot][lane] (4 B) --,
+// the untried-children stack [level][lane] (32-bit masks) and the path bytes [level][lane].
+// Dynamic shared memory a cnt_kernel block needs beyond the staged table:
+template <class T>
+constexpr size_t cnt_smem_block() {
+    return (size_t)CntCfg<T>::warps *
+           (CntCfg<T>::ring * 32 * 12 + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) + CntCfg<T>::PLEV * 32);
+}
+
+template <class T, bool TS, bool HSH, bool HX>
+__global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt_kernel(DfsArgs A) {
+    using C = CntCfg<T>;
+    constexpr bool RS = C::RS;
+    constexpr int WARPS = C::warps;
+    constexpr int PLEV = C::PLEV;
+    constexpr int RING = C::ring;
+    __shared__ unsigned long long s_td, s_head;
+    __shared__ unsigned s_ov;
+    extern __shared__ __align__(16) uint8_t stab[];  // [TS: {sin, mix}[n_slots]] then the block's areas
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint8_t *dyn = stab + (TS ? (size_t)A.n_slots * 16 : 0);
+    uint64_t *sring = reinterpret_cast<uint64_t *>(dyn);                             // [warp][slot][lane]
+    uint32_t *sringt = reinterpret_cast<uint32_t *>(dyn + WARPS * RING * 32 * 8);    // [warp][slot][lane]
+    uint32_t *srem = sringt + WARPS * RING * 32;                                      // [warp][level][lane]
+    uint8_t *spath = reinterpret_cast<uint8_t *>(srem + (RS ? WARPS * 32 * 32 : 0));  // [warp][level][lane]
+    const DevGraph &G = A.G;
+    // 32-bit shared-window addresses of this lane's columns (opaque: kept in registers)
+    uint32_t pb, rb, qb, lb;
+    asm volatile("mov.b32 %0, %1;" : "=r"(pb) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * PLEV * 32) + lane));
+    asm volatile("mov.b32 %0, %1;" : "=r"(rb) : "r"((uint32_t)__cvta_generic_to_shared(srem + (RS ? wid * 32 * 32 : 0)) + (RS ? lane * 4 : 0)));
+    asm volatile("mov.b32 %0, %1;" : "=r"(qb) : "r"((uint32_t)__cvta_generic_to_shared(sring + wid * RING * 32) + lane * 8));
+    asm volatile("mov.b32 %0, %1;" : "=r"(lb) : "r"((uint32_t)__cvta_generic_to_shared(sringt + wid * RING * 32) + lane * 4));
+    CntTab<T, TS> tab;
+    tab.g = reinterpret_cast<const Slot<1> *>(G.slots);
+    tab.gm = G.slot_mix;
+    tab.sb = 0;
+    if (TS) {
+        uint64_t *d = reinterpret_cast<uint64_t *>(stab);
+        for (int i = threadIdx.x; i < A.n_slots; i += blockDim.x) {
+            d[2 * i] = __ldg(&tab.g[i].sin[0]);
+            d[2 * i + 1] = __ldg(G.slot_mix + i);
+        }
+        asm volatile("mov.b32 %0, %1;" : "=r"(tab.sb) : "r"((uint32_t)__cvta_generic_to_shared(stab)));
+    }
+    for (int i = threadIdx.x; i < WARPS * PLEV * 32; i += blockDim.x) spath[i] = 0;  // idle lanes read vertex 0
+    if (threadIdx.x == 0) {
+        s_td = 1ull << 32;
+        s_head = 1ull << 20;
+        s_ov = 0;
+    }
+    __syncthreads();
+    Unit<1> *units = reinterpret_cast<Unit<1> *>(A.units);
+    uint64_t t_pp = 0, t_vert = 0, t_ext = 0, t_ha = 0, t_hb = 0, t_cross = 0;
+    uint32_t rc = 0;  // prime paths in this lane's ring
+    unsigned long long hblk = 0, hblk_end = 0;
+
+    CntLane<T> L;
+    L.active = false;
+    L.done = false;
+    L.l = L.r = L.s = L.vb = 0;
+    L.M = L.rem = L.sbit = L.ps = L.exm = 0;
+    L.S = 0;
+    bool waiting = false, exited = false;
+    int64_t slot = -1;
+    int32_t uscc = 0, ugen = 0;
+    uint32_t steps = 0, last_split = 0, iter = 0;
+    unsigned rdy = 0;
+    bool claim_pending = false;
+    unsigned claim_mask = 0;
+    int claim_leader = 0;
+    unsigned long long claim_res = 0;
+    bool snap_pending = false;
+    unsigned long long snap_td = 0, snap_head = 0;
+    unsigned snap_ov = 0;
+    bool qdone = false, prev_active = true;
+
+    // an event of this lane into its ring: a prime path (tag = length; counted at once) or a
+    // head segment (tag = slot of the exit vertex << 8 | length, bit 31 set)
+    bool ring_heads = false;  // warp-uniform: some lane's ring holds a head segment
+    auto put_ev = [&](bool pp, bool head, uint64_t Sx, uint32_t len, int hslot) {
+        if (pp) {
+            t_pp += 1;
+            t_vert += len;
+        }
+        if (HSH ? (pp || head) : (HX && head)) {
+            asm volatile("st.shared.u64 [%0], %1;" ::"r"(qb + rc * 256u), "l"(Sx) : "memory");
+            const uint32_t tag = head ? (0x80000000u | ((uint32_t)hslot << 8) | len) : len;
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lb + rc * 128u), "r"(tag) : "memory");
+            rc++;
+        }
+        if constexpr (HX) ring_heads |= __any_sync(kFull, head);
+    };
+    // warp-uniform: every lane hashes the prime paths in its ring (the two finalizers, R20),
+    // then the warp writes the head segments
+    auto drain = [&]() {
+        const uint32_t mx = __reduce_max_sync(kFull, rc);
+        for (uint32_t j = 0; j < mx; j++) {
+            uint64_t z = 0;
+            uint32_t tag = 0;
+            if (j < rc) {
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qb + j * 256u) : "memory");
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tag) : "r"(lb + j * 128u) : "memory");
+            }
+            if (HSH && j < rc && !(tag & 0x80000000u)) {
+                t_ha += mix64(z ^ (kSeedA + (uint64_t)tag));
+                t_hb += mix64(z ^ (kSeedB + (uint64_t)tag));
+            }
+            if constexpr (HX) {
+                if (ring_heads) {  // head segments: one HeadS per head node, in the warp's block of slots
+                    const bool h = j < rc && (tag & 0x80000000u);
+                    const uint32_t hb = __ballot_sync(kFull, h);
+                    if (hb) {
+                        const uint32_t need = __popc(hb);
+                        if (hblk + need > hblk_end) {  // a new block of 256 slots (the rest of the old one: holes)
+                            for (unsigned long long q = hblk + lane; q < hblk_end; q += 32)
+                                if (q < A.head_cap) A.heads[q].x = -1;
+                            unsigned long long b = 0;
+                            if (lane == 0) b = atomicAdd(A.cacc + 5, 256ull);
+                            b = __shfl_sync(kFull, b, 0);
+                            hblk = b;
+                            hblk_end = b + 256;
+                            if (b + 256 > A.head_cap && lane == 0) atomicOr(A.overflow, 8u);
+                        }
+                        const unsigned long long q = hblk + __popc(hb & ((1u << lane) - 1u));
+                        if (h && q < A.head_cap) {
+                            HeadS hr;
+                            hr.S = z;
+                            hr.len = (int32_t)(tag & 0xffu);
+                            hr.x = (int32_t)((tag >> 8) & 0x7fffffu);
+                            *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&hr);
+                        }
+                        hblk += need;
+                    }
+                }
+            }
+        }
+        rc = 0;
+        ring_heads = false;
+    };
+
+    while (true) {
+        iter++;
+        bool feed = false;
+        uint32_t split_need = A.split_min;
+        {
+            bool have = false;
+            unsigned long long td = 0, hd = 0;
+            unsigned ov = 0;
+            if (wid == 0) {
+                if (snap_pending) {
+                    td = __shfl_sync(kFull, snap_td, 0);
+                    hd = __shfl_sync(kFull, snap_head, 0);
+                    ov = __shfl_sync(kFull, snap_ov, 0);
+                    if (lane == 0) {
+                        *reinterpret_cast<volatile unsigned long long *>(&s_td) = td;
+                        *reinterpret_cast<volatile unsigned long long *>(&s_head) = hd;
+                        *reinterpret_cast<volatile unsigned *>(&s_ov) = ov;
+                    }
+                    snap_pending = false;
+                    have = true;
+                }
+            } else if (((iter & 1u) == 0u) || !prev_active) {
+                td = *reinterpret_cast<volatile unsigned long long *>(&s_td);
+                hd = *reinterpret_cast<volatile unsigned long long *>(&s_head);
+                ov = *reinterpret_cast<volatile unsigned *>(&s_ov);
+                have = true;
+            }
+            if (have) {
+                qdone = ((td >> 32) == (td & 0xffffffffull)) || ((ov & 6u) != 0u);
+                const long long backlog = (long long)(td >> 32) - (long long)hd;
+                feed = backlog < (long long)A.low_water;
+                if (backlog < -(long long)A.starve_lanes) split_need = A.split_min_starve;
+            }
+        }
+        // ---------------- waiting lanes: start the claimed unit once it is written
+        bool st_pp = false, st_head = false;
+        uint64_t st_S = 0;
+        uint32_t st_len = 0;
+        int st_hslot = 0;
+        if (waiting) {
+            if (rdy != 0u) {
+                waiting = false;
+                // acquire: the producer's unit stores (made visible by its fence) before our reads
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                const Unit<1> *U = units + slot;
+                const int4 h = __ldcg(reinterpret_cast<const int4 *>(&U->scc));
+                L.M = (T)__ldcg(reinterpret_cast<const unsigned long long *>(U->M));
+                uscc = h.x;
+                ugen = __ldcg(A.gen + slot);
+                const int kind = (h.w >> 8) & 0xff;
+                const int depth = h.w & 0xff;
+                L.l = L.r = depth;
+                L.vb = __ldg(G.scc_vbase + uscc);
+                const uint32_t *p4 = reinterpret_cast<const uint32_t *>(U->path);
+                uint64_t S0 = 0;
+                int u = 0;
+#pragma unroll 1
+                for (int q = 0; q * 4 <= depth; q++) {  // path bytes into the lane's column, S of the path
+                    const uint32_t wv = __ldcg(p4 + q);
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        const int i = q * 4 + b;
+                        if (i <= depth) {
+                            const int x = (int)((wv >> (8 * b)) & 0xffu);
+                            sts_u8(pb + (uint32_t)i * 32u, x);
+                            S0 += mul64x32(tab.mix(L.vb + x), 2u * (uint32_t)i + 1u);
+                            u = x;
+                        }
+                    }
+                }
+                L.s = (int)(__ldcg(p4) & 0xffu);
+                L.sbit = (T)1 << L.s;
+                L.ps = tab.pin(L.vb + L.s);
+                L.exm = HX ? (T)__ldg(G.scc_exm + uscc) : (T)0;
+                L.S = S0;
+                steps = 0;
+                last_split = 0;
+                L.active = true;
+                if (kind == K_CLOSURE) {  // the closing arc of path[0..depth] back to s
+                    t_ext += 1;
+                    st_pp = true;
+                    st_S = S0 + mul64x32(tab.mix(L.vb + L.s), 2u * (uint32_t)depth + 3u);
+                    st_len = (uint32_t)depth + 2;
+                    L.rem = 0;
+                    L.done = true;
+                } else {  // K_NODE: the node's own event, then its subtree
+                    if (depth > 0) t_ext += 1;
+                    const T ub = (T)1 << u;
+                    L.rem = tab.sin(L.vb + u) & (~L.M | L.sbit);
+                    const bool ex = ((L.exm >> u) & 1) != 0;
+                    st_pp = L.rem == 0 && (L.ps & ~(L.M & ~ub)) == 0 && !ex;
+                    st_head = ex && (L.ps & ~L.M) == 0;
+                    st_S = S0;
+                    st_len = (uint32_t)depth + 1;
+                    st_hslot = L.vb + u;
+                    L.done = L.rem == 0;
+                }
+            } else if (qdone) {
+                waiting = false;
+                exited = true;
+            } else if (slot < (int64_t)A.qcap) {
+                rdy = ld_relaxed(A.ready + slot);
+            }
+        }
+        put_ev(st_pp, st_head, st_S, st_len, st_hslot);  // (the ring is empty here: drained after the passes)
+        // ---------------- the claim issued last iteration
+        if (claim_pending) {
+            const unsigned long long base = __shfl_sync(kFull, claim_res, claim_leader);
+            if ((claim_mask >> lane) & 1u) {
+                slot = (int64_t)(base + __popc(claim_mask & ((1u << lane) - 1u)));
+                waiting = true;
+                rdy = (slot < (int64_t)A.qcap) ? ld_relaxed(A.ready + slot) : 0u;
+            }
+            claim_pending = false;
+        }
+        {
+            const unsigned need = __ballot_sync(kFull, !L.active && !waiting && !exited);
+            if (need && !claim_pending) {
+                claim_leader = __ffs(need) - 1;
+                claim_mask = need;
+                claim_pending = true;
+                if (lane == claim_leader) claim_res = atomicAdd(A.qhead, (unsigned long long)__popc(need));
+            }
+        }
+        const bool any_active = __ballot_sync(kFull, L.active) != 0;
+        prev_active = any_active;
+        if (wid == 0 && !snap_pending && (((iter & 1u) == 0u) || !any_active)) {
+            if (lane == 0) {
+                snap_td = ld_volatile(A.qtd);
+                snap_head = ld_volatile(A.qhead);
+                snap_ov = ld_flags(A.overflow);
+            }
+            snap_pending = true;
+        }
+        if (!any_active) {
+            drain();
+            if (__ballot_sync(kFull, !exited) == 0) break;
+            __nanosleep(128);
+            continue;
+        }
+
+        // ---------------- passes of the unified step: every stepping lane makes exactly one
+        // move per pass -- a pop (its node has no untried child left) or the take of its
+        // node's lowest untried child -- through ONE instruction stream: the moved vertex v
+        // (the popped one or the child), its digest term mix(v)*(2 pos+1), the visited-bit
+        // toggle and the depth change are the same operations either way
+        uint32_t ext32 = 0;
+#pragma unroll 1
+        for (int blk = 0; blk < kStepsPerIter / RING; blk++) {
+#pragma unroll 1
+            for (int t = 0; t < RING; t++) {
+                const bool act = L.active && !L.done;
+                const T rem = L.rem;
+                const int l = L.l;
+                const bool empty = rem == 0;
+                if (act && empty && l == L.r) L.done = true;  // the unit's subtree is finished
+                const bool pop = act && empty && l > L.r;
+                const bool take = act && !empty;
+                const int w = ffs_t(rem);                     // (take) the child
+                const int u = lds_u8(pb + (uint32_t)l * 32u);  // (pop) the vertex popped
+                const int v = take ? w : u;
+                const int vslot = L.vb + v;                   // (idle lanes: a valid slot of their last SCC)
+                const uint64_t prod = mul64x32(tab.mix(vslot), 2u * (uint32_t)(take ? l + 1 : l) + 1u);
+                const T vbit = (T)1 << v;
+                const T sn = tab.sin(vslot);
+                const bool clo = w == L.s;
+                const T Mw = L.M | vbit;
+                const T cw = clo ? (T)0 : (sn & (~Mw | L.sbit));  // (take) the child's own untried children
+                bool ex = false;
+                if constexpr (HX) ex = ((L.exm >> v) & 1) != 0;
+                const bool pp = take && (clo || (cw == 0 && (L.ps & ~L.M) == 0 && !ex));
+                const bool push = take && cw != 0;
+                const uint64_t Sw = L.S + prod;  // (take) the digest sum of path + w
+                T rem_pop = 0;
+                if constexpr (RS) {
+                    if (pop) rem_pop = (T)lds_u32(rb + (uint32_t)(l - 1) * 128u);
+                } else {
+                    if (pop) {  // the parent's successors above u that are still open
+                        const int p = lds_u8(pb + (uint32_t)(l - 1) * 32u);
+                        const T above = (u >= 63) ? (T)0 : ((~(T)0) << (u + 1));
+                        rem_pop = tab.sin(L.vb + p) & (~(L.M & ~vbit) | L.sbit) & above;
+                    }
+                }
+                if (push) {
+                    if constexpr (RS) sts_u32(rb + (uint32_t)l * 128u, (uint32_t)(rem & (rem - 1)));
+                    sts_u8(pb + (uint32_t)(l + 1) * 32u, w);
+                }
+                ext32 += take ? 1u : 0u;
+                L.M = (push || pop) ? (L.M ^ vbit) : L.M;
+                L.S = push ? Sw : (pop ? L.S - prod : L.S);
+                L.l = l + (push ? 1 : 0) - (pop ? 1 : 0);
+                L.rem = push ? cw : (pop ? rem_pop : (take ? (rem & (rem - 1)) : rem));
+                const bool head = HX && take && !clo && ex && (L.ps & ~Mw) == 0;
+                put_ev(pp, head, Sw, (uint32_t)l + 2, vslot);
+            }
+            drain();
+        }
+        t_ext += ext32;
+        if (L.active) steps += kStepsPerIter;
+
+        // ---------------- donate on demand: the untried children of the shallowest open level
+        if (feed && L.active && !L.done && (steps - last_split >= split_need || ugen < A.eager_gens)) {
+            int j0 = -1;
+            T c0 = 0;
+            {
+                T M = L.M;
+                for (int j = L.l; j >= L.r; j--) {
+                    T c;
+                    if (j == L.l) {
+                        c = L.rem;
+                    } else {
+                        const int wc = lds_u8(pb + (uint32_t)(j + 1) * 32u);  // the child of level j on the path
+                        M &= ~((T)1 << wc);
+                        if constexpr (RS) {
+                            c = (T)lds_u32(rb + (uint32_t)j * 128u);
+                        } else {
+                            const int p = lds_u8(pb + (uint32_t)j * 32u);
+                            const T above = (wc >= 63) ? (T)0 : ((~(T)0) << (wc + 1));
+                            c = tab.sin(L.vb + p) & (~M | L.sbit) & above;
+                        }
+                    }
+                    if (c) {
+                        j0 = j;
+                        c0 = c;
+                    }
+                }
+            }
+            const int m = j0 >= 0 ? (sizeof(T) == 4 ? __popc((uint32_t)c0) : __popcll((uint64_t)c0)) : 0;
+            if (m > 0) {
+                const unsigned long long base = atomicAdd(A.qtd, (unsigned long long)m << 32) >> 32;
+                if (base + m > A.qcap) {
+                    atomicOr(A.overflow, 4u);
+                } else {
+                    T M = L.M;  // the mask of path[0..j0]
+                    for (int j = j0 + 1; j <= L.l; j++) M &= ~((T)1 << lds_u8(pb + (uint32_t)j * 32u));
+                    T c = c0;
+                    for (int n = 0; n < m; n++) {
+                        const int w = ffs_t(c);
+                        c &= c - 1;
+                        const int kind = (w == L.s) ? K_CLOSURE : K_NODE;
+                        Unit<1> &U = units[base + n];
+                        for (int q = 0; q <= (j0 >> 2); q++) {
+                            uint32_t wv = 0;
+#pragma unroll
+                            for (int b = 0; b < 4; b++)
+                                if (q * 4 + b <= j0) wv |= (uint32_t)lds_u8(pb + (uint32_t)(q * 4 + b) * 32u) << (8 * b);
+                            reinterpret_cast<uint32_t *>(U.path)[q] = wv;
+                        }
+                        uint64_t Mu = (uint64_t)M;
+                        if (kind == K_NODE) {
+                            U.path[j0 + 1] = (uint8_t)w;
+                            Mu |= 1ull << w;
+                        }
+                        U.M[0] = Mu;
+                        const int depth = (kind == K_NODE) ? j0 + 1 : j0;
+                        *reinterpret_cast<int4 *>(&U.scc) = make_int4(uscc, -1, 0, depth | (kind << 8));
+                        A.gen[base + n] = ugen + 1;
+                    }
+                    __threadfence();  // unit data before the ready flags
+                    for (int n = 0; n < m; n++) st_relaxed(A.ready + base + n, 1u);
+                    if (j0 == L.l) L.done = true;  // nothing left below the donated level
+                    else L.r = j0 + 1;             // the walk now ends when it returns to depth j0+1
+                    last_split = steps;
+                }
+            }
+        }
+        if (L.active && L.done) {
+            atomicAdd(A.qtd, 1ull);  // done += 1
+            L.active = false;
+            L.done = false;
+        }
+    }
+    // the ring's remainder was drained; the head block's unused slots, then the totals
+    for (unsigned long long j = hblk + lane; j < hblk_end; j += 32)
+        if (j < A.head_cap) A.heads[j].x = -1;
+    uint64_t v[7] = {t_pp, t_vert, t_ext, t_ha, t_hb, 0, t_cross};
+    bool ovf = false;  // prime-path totals >= 2^62 (or a wrapped sum): LIMIT_EXCEEDED
+#pragma unroll
+    for (int q = 0; q < 7; q++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t r = v[q] + __shfl_xor_sync(kFull, v[q], o);
+            if ((q < 2 || q == 6) && (r < v[q] || r >= (1ull << 62))) ovf = true;
+            v[q] = r;
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 7; q++) {
+            if (!v[q] || q == 5) continue;
+            const unsigned long long old = atomicAdd(A.cacc + q, (unsigned long long)v[q]);
+            if ((q < 2 || q == 6) && (old + v[q] < old || old + v[q] >= (1ull << 62))) ovf = true;
+        }
+    }
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(A.overflow, 1u);
+}
+
+}  // namespace tpg

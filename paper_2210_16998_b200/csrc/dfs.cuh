@@ -168,7 +168,29 @@ struct Lane {
     // record stream state: the decoder knows path[0..base) (base <= l+1); the bytes
     // path[base..l] are read from the shared-memory path when the next record is written
     int32_t base;
+    uint64_t S;  // count modes: digest sum of path[0..l] (R20), kept up to date by push and pop
 };
+
+// Per-slot digest values mix64(gid) (R20): staged in shared memory next to the slot table
+// (TS), else read through L1.
+template <bool TS>
+struct MixTab {
+    const uint64_t *g;
+    uint32_t sb;  // TS: shared-window address
+    __device__ __forceinline__ uint64_t operator()(int i) const {
+        if (TS) {
+            uint64_t v;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sb + (uint32_t)i * 8u) : "memory");
+            return v;
+        }
+        return __ldg(g + i);
+    }
+};
+
+// DFS kernel modes: M_REC writes the path-delta record streams (materialize, and the
+// segment phase); M_CNT counts and digests every prime path in the walk itself (no
+// records; COUNT_HASH); M_CNT_NOHASH counts only.
+enum DfsMode : int { M_REC = 0, M_CNT = 1, M_CNT_NOHASH = 2 };
 
 // View of the slot table: staged in shared memory (TS) when it fits, else read through L1.
 // The shared copy is addressed through a 32-bit shared-window base kept in a register.
@@ -291,9 +313,10 @@ __device__ __forceinline__ void rec_put(const DfsArgs &A, RecWriter &R, uint64_t
 // A step that exhausts a node pops it and, unless the parent still has
 // out-of-SCC arcs to merge, moves on to the parent's next child in the same
 // step (a pop costs no step of its own).
-template <class T, bool TS>
+template <class T, bool TS, bool CNT>
 __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, const TabView<MT<T>::W, TS> &tab,
-                                        Lane<T> &L, RecWriter &R, uint32_t mp, int &e_out, uint32_t &ext) {
+                                        const MixTab<TS> &mt, Lane<T> &L, RecWriter &R, uint32_t mp, int &e_out,
+                                        uint32_t &ext) {
     using O = MT<T>;
     int w = O::next(L.sin, L.M, L.sbit, L.k);
     if (L.o < L.ocnt) {  // exit vertex with out-of-SCC arcs still to visit
@@ -311,6 +334,7 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
         const int wold = L.u;
         const int parent = lds_u8(mp + pidx(L.l - 1));
         L.M = O::andnot(L.M, O::bit(wold));
+        if (CNT) L.S -= mt(L.vb + wold) * pos_weight((uint32_t)L.l);
         L.l -= 1;
         L.u = parent;
         load_slot(tab, L, parent);
@@ -322,6 +346,7 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
             const int wold2 = L.u;
             const int parent2 = lds_u8(mp + pidx(L.l - 1));
             L.M = O::andnot(L.M, O::bit(wold2));
+            if (CNT) L.S -= mt(L.vb + wold2) * pos_weight((uint32_t)L.l);
             L.l -= 1;
             L.u = parent2;
             load_slot(tab, L, parent2);
@@ -340,6 +365,7 @@ __device__ __forceinline__ int dfs_step(const DfsArgs &A, const DevGraph &G, con
     if (clo) L.k = w + 1;
     if (push) {
         sts_u8(mp + pidx(L.l + 1), w);
+        if (CNT) L.S += mt(L.vb + w) * pos_weight((uint32_t)(L.l + 1));
         L.M = L.M | O::bit(w);
         L.k = 0;
         L.l += 1;
@@ -373,13 +399,14 @@ __device__ __forceinline__ int lean_node_event(uint32_t c, uint32_t ps, uint32_t
     return (emit && c == 0u && (ps & ~Mp) == 0u) ? (EV_PP | ((l + 1) << 8)) : 0;
 }
 
-template <bool TS>
-__device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, Lane<uint32_t> &L, uint32_t mp, uint32_t rp,
-                                         uint32_t &ext) {
+template <bool TS, bool CNT>
+__device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, const MixTab<TS> &mt, Lane<uint32_t> &L,
+                                         uint32_t mp, uint32_t rp, uint32_t &ext) {
     const bool pop = L.sin == 0u;
     const bool fin = pop && L.l == L.r;  // the unit's subtree is exhausted
     if (pop && !fin) {                   // back to the parent and its untried children
         const int u = lds_u8(mp + pidx(L.l));
+        if (CNT) L.S -= mt(L.vb + u) * pos_weight((uint32_t)L.l);
         L.l -= 1;
         L.sin = lane_rem(rp, L.l);
         L.M &= ~(1u << u);
@@ -388,6 +415,7 @@ __device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, Lane<uint32_
         for (int x = 1; x < LEAN_POPS; x++) {  // exhausted ancestors: more levels in the same step
             if (L.sin == 0u && L.l > L.r) {
                 const int u2 = lds_u8(mp + pidx(L.l));
+                if (CNT) L.S -= mt(L.vb + u2) * pos_weight((uint32_t)L.l);
                 L.l -= 1;
                 L.sin = lane_rem(rp, L.l);
                 L.M &= ~(1u << u2);
@@ -406,6 +434,7 @@ __device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, Lane<uint32_
         } else {
             sts_u32(rp + ((uint32_t)L.l << 7), L.sin);
             sts_u8(mp + pidx(L.l + 1), w);
+            if (CNT) L.S += mt(L.vb + w) * pos_weight((uint32_t)(L.l + 1));
             const uint32_t Mp = L.M;
             L.M |= 1u << w;
             L.l += 1;
@@ -562,16 +591,31 @@ __device__ int lane_donate(const DevGraph &G, const TabView<MT<T>::W, TS> &tab, 
 // (children of the piece in the unit forest).  The kernel ends when every
 // pushed unit has finished (done == tail; both live in one 64-bit word so a
 // single load gives a consistent snapshot).
-template <class T, bool TS, bool LEAN>
+//
+// Count modes (MODE = M_CNT / M_CNT_NOHASH; COUNT_HASH calls, prime-path phase): no
+// record stream and no per-unit results.  The lane keeps the digest sum S of its path
+// in a register (push: + mix(v) * (2l+1), pop: the same subtracted; R20); a prime path
+// found by a step is queued per warp (S, length) and the warp hashes 32 queued paths at
+// once, one per lane, so the two splitmix64 finalizers never run divergently.  A head
+// segment (an exit vertex with out-of-SCC arcs, pred(s) on the path) adds its W(x)
+// cross prime paths to the counts and is written as a HeadS {S, |h|, x} into the warp's
+// current block of 256 head slots (one atomic per block) for stitch_hash_s_kernel.
+// Totals are reduced per warp into A.cacc when the kernel ends.
+template <class T, bool TS, bool LEAN, int MODE>
 __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : DfsTraits<T>::min_blocks) dfs_kernel(DfsArgs A) {
     using O = MT<T>;
     constexpr int W = O::W;
     constexpr int WARPS = DfsTraits<T>::warps;
+    constexpr bool CNT = MODE != M_REC;
+    constexpr bool HSH = MODE == M_CNT;
     static_assert(!LEAN || MT<T>::BITS == 32, "LEAN kernels use 32-bit masks");
+    static_assert(!CNT || W == 1, "count modes use one mask word");
     constexpr int PLEV = LEAN ? 32 : 64 * W;  // path levels per lane
     __shared__ __align__(16) uint8_t spath[WARPS * PLEV * 32 + 128];  // + a spare row (path_bytes)
     __shared__ __align__(16) uint32_t srem[LEAN ? WARPS * 32 * 32 : 1];  // LEAN: rem[level][lane] per warp
-    extern __shared__ __align__(16) uint8_t stab[];  // slot table copy (TS)
+    __shared__ __align__(16) uint64_t sqS[HSH ? WARPS * 64 : 1];  // count mode: per warp, queued prime paths' S
+    __shared__ uint16_t sqL[HSH ? WARPS * 64 : 1];                // ... and their lengths
+    extern __shared__ __align__(16) uint8_t stab[];  // slot table copy (TS); count modes: then the mix table
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t mp;  // this lane's column of the shared path array (opaque: not recomputed in the loop)
     asm volatile("mov.b32 %0, %1;" : "=r"(mp) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * PLEV * 32) + lane * 4));
@@ -579,17 +623,32 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
     asm volatile("mov.b32 %0, %1;" : "=r"(rp) : "r"((uint32_t)__cvta_generic_to_shared(srem + (LEAN ? wid * 32 * 32 : 0)) + (LEAN ? lane * 4 : 0)));
     const DevGraph &G = A.G;
     TabView<W, TS> tab;
+    MixTab<TS> mt;
+    mt.g = G.slot_mix;
+    mt.sb = 0;
     if (TS) {
         const int4 *src = reinterpret_cast<const int4 *>(G.slots);
         int4 *dst = reinterpret_cast<int4 *>(stab);
         for (int i = threadIdx.x; i < A.n_slots * (int)(sizeof(Slot<W>) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+        if (CNT) {
+            uint64_t *dm = reinterpret_cast<uint64_t *>(stab + (size_t)A.n_slots * sizeof(Slot<W>));
+            for (int i = threadIdx.x; i < A.n_slots; i += blockDim.x) dm[i] = __ldg(G.slot_mix + i);
+        }
         __syncthreads();
         tab.p = reinterpret_cast<const Slot<W> *>(stab);
         asm volatile("mov.b32 %0, %1;" : "=r"(tab.sb) : "r"((uint32_t)__cvta_generic_to_shared(stab)));
+        mt.sb = tab.sb + (uint32_t)((size_t)A.n_slots * sizeof(Slot<W>));
     } else {
         tab.p = reinterpret_cast<const Slot<W> *>(G.slots);
         tab.sb = 0;
     }
+    // count modes: the warp's prime-path queue, per-lane totals, the warp's head-slot block
+    uint64_t *qS = sqS + (HSH ? wid * 64 : 0);
+    uint16_t *qL = sqL + (HSH ? wid * 64 : 0);
+    uint32_t qn = 0;                                  // queued prime paths (warp-uniform, < 32 between drains)
+    uint64_t t_pp = 0, t_vert = 0, t_ext = 0, t_ha = 0, t_hb = 0, t_cross = 0;
+    unsigned long long hblk = 0, hblk_end = 0;       // warp-uniform: next free / end of the warp's head block
+    const uint32_t lt_mask = (1u << lane) - 1u;
     Unit<W> *units = reinterpret_cast<Unit<W> *>(A.units);
 
     Lane<T> L;
@@ -727,9 +786,15 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
                 ext = 0;
                 c_pp = c_vert = 0;
                 c_it = c_itv = c_hd = c_hdv = 0;
-                if (R.fill == kChunkRecs - 1) rec_switch(A, R);
-                A.rfirst[slot] = (int64_t)(R.cur - A.chunks) + R.fill;  // global record index
-                R.count = 0;
+                if constexpr (CNT) {  // the digest sum of the unit's root path
+                    uint64_t S0 = 0;
+                    for (int i = 0; i <= depth; i++) S0 += mt(L.vb + lds_u8(mp + pidx(i))) * pos_weight((uint32_t)i);
+                    L.S = S0;
+                } else {
+                    if (R.fill == kChunkRecs - 1) rec_switch(A, R);
+                    A.rfirst[slot] = (int64_t)(R.cur - A.chunks) + R.fill;  // global record index
+                    R.count = 0;
+                }
                 // the unit's root event (no step is counted for it)
                 bool lean_root = false;
                 if constexpr (LEAN) {  // the root's children; its own event
@@ -833,7 +898,81 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
         // only writes the last step's event)
         for (int t = 0; t <= kStepsPerIter; t++) {
             // ---------------- event: counters + one record (lane-local)
-            if (ev) {
+            if constexpr (CNT) {
+                // count modes: prime paths into the warp queue, head segments into the head block
+                const int ty = ev ? ev_type(ev) : 0;
+                const uint32_t len = (uint32_t)ev_len(ev);
+                const bool is_pp = ev && (LEAN || ty == EV_PP);
+                const bool is_head = !LEAN && ev && ty == EV_HEAD;
+                uint64_t Sx = L.S;
+                if (is_pp) {
+                    if (ev & EV_CLO) Sx += mt(L.vb + L.s) * pos_weight(len - 1);  // the closing vertex s
+                    t_pp += 1;
+                    t_vert += len;
+                }
+                if constexpr (HSH) {
+                    const uint32_t bal = __ballot_sync(kFull, is_pp);
+                    if (bal) {
+                        if (is_pp) {
+                            const uint32_t j = qn + __popc(bal & lt_mask);
+                            qS[j] = Sx;
+                            qL[j] = (uint16_t)len;
+                        }
+                        qn += __popc(bal);
+                        if (qn >= 32) {
+                            __syncwarp();
+                            qn -= 32;
+                            const uint64_t z = qS[qn + lane];
+                            const uint64_t n = qL[qn + lane];
+                            t_ha += mix64(z ^ (kSeedA + n));
+                            t_hb += mix64(z ^ (kSeedB + n));
+                            __syncwarp();
+                        }
+                    }
+                }
+                if constexpr (!LEAN) {
+                    const uint32_t hb = HSH ? __ballot_sync(kFull, is_head) : 0u;
+                    if (!HSH && is_head) {  // counts only: no head records
+                        const int32_t x = __ldg(G.out_gid + e);
+                        const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                        t_pp = sat_add(t_pp, Wx, A.overflow);
+                        t_cross = sat_add(t_cross, Wx, A.overflow);
+                        t_vert = sat_add(t_vert, sat_add(sat_mul((uint64_t)len, Wx, A.overflow), Vx, A.overflow),
+                                         A.overflow);
+                    }
+                    if (hb) {
+                        const uint32_t need = __popc(hb);
+                        if (hblk + need > hblk_end) {  // a new block of 256 slots (the rest of the old one: holes)
+                            for (unsigned long long j = hblk + lane; j < hblk_end; j += 32)
+                                if (j < A.head_cap) A.heads[j].x = -1;
+                            unsigned long long b = 0;
+                            if (lane == 0) b = atomicAdd(A.cacc + 5, 256ull);
+                            b = __shfl_sync(kFull, b, 0);
+                            hblk = b;
+                            hblk_end = b + 256;
+                            if (b + 256 > A.head_cap && lane == 0) atomicOr(A.overflow, 8u);
+                        }
+                        if (is_head) {
+                            const unsigned long long j = hblk + __popc(hb & lt_mask);
+                            const int32_t x = __ldg(G.out_gid + e);
+                            if (j < A.head_cap) {
+                                HeadS hr;
+                                hr.S = Sx;
+                                hr.len = (int32_t)len;
+                                hr.x = x;
+                                *reinterpret_cast<ulonglong2 *>(A.heads + j) =
+                                    *reinterpret_cast<const ulonglong2 *>(&hr);
+                            }
+                            const uint64_t Wx = __ldg(G.Wc + x), Vx = __ldg(G.Wv + x);
+                            t_pp = sat_add(t_pp, Wx, A.overflow);
+                            t_cross = sat_add(t_cross, Wx, A.overflow);
+                            t_vert = sat_add(t_vert, sat_add(sat_mul((uint64_t)len, Wx, A.overflow), Vx, A.overflow),
+                                             A.overflow);
+                        }
+                        hblk += need;
+                    }
+                }
+            } else if (ev) {
                 const int ty = ev_type(ev);
                 const uint64_t len = (uint64_t)ev_len(ev);
                 // the bytes path[base..l] the decoder lacks, <= kRecBytes per record
@@ -877,9 +1016,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
             ev = 0;
             if (t < kStepsPerIter && L.active && !L.done) {
                 if constexpr (LEAN) {
-                    ev = lean_step<TS>(tab, L, mp, rp, ext);
+                    ev = lean_step<TS, CNT>(tab, mt, L, mp, rp, ext);
                 } else {
-                    ev = dfs_step<T, TS>(A, G, tab, L, R, mp, e, ext);
+                    ev = dfs_step<T, TS, CNT>(A, G, tab, mt, L, R, mp, e, ext);
                 }
             }
         }
@@ -902,16 +1041,18 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
                 } else {
                     if constexpr (LEAN) lean_donate<TS, true>(L, mp, rp, uscc, j0, units + base);
                     else lane_donate<T, TS, true>(G, tab, L, mp, uscc, j0, units + base);
-                    for (int i = 0; i < m; i++) {
-                        A.gen[base + i] = ugen + 1;
-                        A.child_head[base + i] = -1;
-                        A.parent[base + i] = slot;
+                    for (int i = 0; i < m; i++) A.gen[base + i] = ugen + 1;
+                    if constexpr (!CNT) {  // the unit forest (canonical order of the records)
+                        for (int i = 0; i < m; i++) {
+                            A.child_head[base + i] = -1;
+                            A.parent[base + i] = slot;
+                        }
+                        A.blk_first[b] = (int64_t)base;
+                        A.blk_count[b] = m;
+                        A.blk_next[b] = child_head;
+                        child_head = (int64_t)b;
+                        nchild += m;
                     }
-                    A.blk_first[b] = (int64_t)base;
-                    A.blk_count[b] = m;
-                    A.blk_next[b] = child_head;
-                    child_head = (int64_t)b;
-                    nchild += m;
                     atomicMax(A.maxgen, ugen + 1);
                     __threadfence();  // unit data before the ready flags
                     for (int i = 0; i < m; i++) st_relaxed(A.ready + base + i, 1u);
@@ -926,7 +1067,14 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
         }
 
         // ---------------- unit completion
-        if (L.active && L.done) {
+        if (CNT && L.active && L.done) {
+            t_ext += ext;
+            ext = 0;
+            atomicAdd(A.qtd, 1ull);  // done += 1
+            L.active = false;
+            L.done = false;
+        }
+        if (!CNT && L.active && L.done) {
             A.cnt[C_PP][slot] = c_pp;
             A.cnt[C_VERT][slot] = c_vert;
             A.cnt[C_ITEMS][slot] = c_it;
@@ -941,6 +1089,39 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
             L.active = false;
             L.done = false;
         }
+    }
+    if constexpr (CNT) {  // the queue's remainder, the head block's unused slots, then the totals
+        if constexpr (HSH) {
+            __syncwarp();
+            if (lane < qn) {
+                const uint64_t z = qS[lane];
+                const uint64_t n = qL[lane];
+                t_ha += mix64(z ^ (kSeedA + n));
+                t_hb += mix64(z ^ (kSeedB + n));
+            }
+        }
+        for (unsigned long long j = hblk + lane; j < hblk_end; j += 32)
+            if (j < A.head_cap) A.heads[j].x = -1;
+        uint64_t v[7] = {t_pp, t_vert, t_ext, t_ha, t_hb, 0, t_cross};
+        bool ovf = false;  // prime-path totals >= 2^62 (or a wrapped sum): LIMIT_EXCEEDED, like the unit counters
+#pragma unroll
+        for (int q = 0; q < 7; q++) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t r = v[q] + __shfl_xor_sync(kFull, v[q], o);
+                if (q < 2 && (r < v[q] || r >= (1ull << 62))) ovf = true;
+                v[q] = r;
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < 7; q++) {
+                if (!v[q] || q == 5) continue;
+                const unsigned long long old = atomicAdd(A.cacc + q, (unsigned long long)v[q]);
+                if (q < 2 && (old + v[q] < old || old + v[q] >= (1ull << 62))) ovf = true;
+            }
+        }
+        if (__any_sync(kFull, ovf) && lane == 0) atomicOr(A.overflow, 1u);
     }
 #ifdef TPGEN_KERNEL_DEBUG
     if (A.dbg) {

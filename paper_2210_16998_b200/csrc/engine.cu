@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "expand.cuh"
 #include "frontier.cuh"
+#include "count.cuh"
 #include "engine.h"
 
 namespace tpg {
@@ -89,6 +90,16 @@ static tpgen_status upload(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
     return TPGEN_OK;
 }
 
+// splitmix64 finalizer (the digest's per-vertex value, R20; the device has its own copy)
+static uint64_t host_mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return z;
+}
+
 // ------------------------------------------------------------ plan
 PlanImpl::~PlanImpl() {
     if (!dev_ok) return;
@@ -103,7 +114,7 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_slot_mix, &d_vmix, &d_scc_exm, &cheads,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan,
@@ -150,6 +161,19 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     TPG_TRY(upload(P.d_scc_pair_base, H.scc_pair_base, s));
     TPG_TRY(upload(P.d_slot_eidx, H.slot_eidx, s));
     TPG_TRY(upload(P.d_comp, H.comp, s));
+    {  // digest values mix64(v) per global vertex and per slot (R20)
+        std::vector<uint64_t> vm(std::max(H.n, 1), 0), sm(std::max(H.n, 1), 0);
+        for (int32_t v = 0; v < H.n; v++) vm[v] = host_mix64((uint64_t)(uint32_t)v);
+        for (int32_t i = 0; i < H.n; i++) sm[i] = vm[H.slot_gid[i]];
+        TPG_TRY(upload(P.d_vmix, vm, s));
+        TPG_TRY(upload(P.d_slot_mix, sm, s));
+        std::vector<uint64_t> exm(std::max(H.n_scc, 1), 0);  // exit vertices per SCC (local bits; <= 64)
+        for (int32_t c = 0; c < H.n_scc; c++)
+            for (int32_t i = 0; i < H.scc_size[c] && i < 64; i++)
+                if (H.slot_out_cnt[H.scc_vbase[c] + i] > 0) exm[c] |= 1ull << i;
+        TPG_TRY(upload(P.d_scc_exm, exm, s));
+    }
+    P.chead_hwm = 0;
     TPG_TRY(P.d_Wc.ensure(std::max<size_t>(H.n, 1) * 8, s));
     TPG_TRY(P.d_Wv.ensure(std::max<size_t>(H.n, 1) * 8, s));
     TPG_CK(cudaMemsetAsync(P.d_Wc.p, 0, std::max<size_t>(H.n, 1) * 8, s));
@@ -172,6 +196,9 @@ static DevGraph dev_graph(PlanImpl &P, int32_t lo, int32_t hi) {
     G.Wc = P.d_Wc.as<uint64_t>();
     G.Wv = P.d_Wv.as<uint64_t>();
     G.scc_gbase = P.d_scc_gbase.as<int32_t>();
+    G.slot_mix = P.d_slot_mix.as<uint64_t>();
+    G.vmix = P.d_vmix.as<uint64_t>();
+    G.scc_exm = P.d_scc_exm.as<uint64_t>();
     G.shard_lo = lo;
     G.shard_hi = hi;
     return G;
@@ -575,10 +602,53 @@ static void presplit_roots(PlanImpl &P, int32_t lo, int32_t hi, int64_t target, 
 // One phase of the persistent DFS (seg = SCC-entry starts, else prime-path
 // starts) over the roots already placed at [qbase, qbase + nroots).  Retried
 // with a larger record pool or queue if either overflows.  Returns the new tail.
+// Launch of one DFS kernel variant (LEAN / table in shared memory / generic) in mode MODE.
+template <class T, int MODE>
+static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsArgs &A, cudaStream_t s,
+                               bool any_exit = true) {
+    constexpr int W = MT<T>::W;
+    if constexpr (MODE != M_REC) {  // count modes: the straight-line count kernel (count.cuh)
+        static_assert(W == 1, "count modes use one mask word");
+        constexpr bool HSH = MODE == M_CNT;
+        using CT = typename std::conditional<sizeof(T) == 4, uint32_t, uint64_t>::type;
+        const int cgrid = grid / (lean ? kLeanBlocks : DfsCfg<W>::min_blocks) * CntCfg<CT>::min_blocks;
+        const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
+        const bool ts = ctab <= kSmemTabMax;
+        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>();
+        void (*k)(DfsArgs) = ts ? (any_exit ? cnt_kernel<CT, true, HSH, true> : cnt_kernel<CT, true, HSH, false>)
+                                : (any_exit ? cnt_kernel<CT, false, HSH, true> : cnt_kernel<CT, false, HSH, false>);
+        TPG_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cdyn));
+        k<<<cgrid, CntCfg<CT>::threads, cdyn, s>>>(A);
+        return TPGEN_OK;
+    } else {
+        if constexpr (std::is_same<T, uint32_t>::value) {
+            if (lean) {
+                TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true, true, M_REC>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTabLean));
+                dfs_kernel<T, true, true, M_REC><<<grid, DfsCfg<W>::threads, tab_bytes, s>>>(A);
+                return TPGEN_OK;
+            }
+        }
+        if (tab_bytes <= kSmemTabMax) {
+            TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true, false, M_REC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kSmemTabMax));
+            dfs_kernel<T, true, false, M_REC><<<grid, DfsCfg<W>::threads, tab_bytes, s>>>(A);
+        } else {
+            dfs_kernel<T, false, false, M_REC><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
+        }
+        return TPGEN_OK;
+    }
+}
+
+// One phase of the persistent DFS (seg = SCC-entry starts, else prime-path
+// starts) over the roots already placed at [qbase, qbase + nroots).  Retried
+// with a larger record pool, queue or head buffer if one overflows.  Returns the
+// new tail.  Count modes (mode != M_REC, prime-path phase of COUNT_HASH calls):
+// no records; cacc_h receives the kernel's totals (dfs.cuh DfsArgs::cacc).
 template <class T>
 static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W> roots, int seg,
                               uint64_t qbase, cudaStream_t s, tpgen_stats &st, int64_t &launches, double &ms_dfs,
-                              uint64_t &tail_out) {
+                              uint64_t &tail_out, int mode = M_REC, unsigned long long *cacc_h = nullptr) {
     constexpr int W = MT<T>::W;
     Timer t;
     const HostPlan &H = P.hp;
@@ -590,11 +660,17 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
     TPG_TRY(grow_queue<W>(P, qbase, std::max<uint64_t>(std::max<uint64_t>(qbase + nroots + 8 * (uint64_t)lanes, 1u << 21),
                                                        P.q_hwm * 3 / 2), s));
     if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
-    TPG_TRY(P.qctr.ensure(7 * 16 * 8, s));
+    TPG_TRY(P.qctr.ensure(8 * 16 * 8, s));
+    if (mode != M_REC) {  // head records: the plan's high-water mark with headroom, at least 1 M slots
+        const uint64_t want = std::max<uint64_t>(1ull << 20, P.chead_hwm + P.chead_hwm / 4 + 256ull * 4096);
+        if (P.cheads.cap < want * sizeof(HeadS)) TPG_TRY(P.cheads.ensure(want * sizeof(HeadS), s));
+    }
     unsigned long long *qc = P.qctr.as<unsigned long long>();
     // Test hooks: TPGEN_TEST_QCAP / TPGEN_TEST_POOL cap the queue slots / record chunks this
     // phase may use (doubling after each overflow), so small graphs exercise the retry path.
     uint64_t qlim = P.qcap, plim = P.chunk_cap;
+    uint64_t hlim = ~0ull;  // count modes: head slots this phase may use (TPGEN_TEST_HEADCAP test hook)
+    if (const char *ev = getenv("TPGEN_TEST_HEADCAP")) hlim = std::max<uint64_t>(256, strtoull(ev, nullptr, 10));
     if (const char *ev = getenv("TPGEN_TEST_QCAP"))
         qlim = std::min<uint64_t>(qlim, qbase + nroots + std::max<uint64_t>(1, strtoull(ev, nullptr, 10)));
     if (const char *ev = getenv("TPGEN_TEST_POOL"))
@@ -603,7 +679,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         TPG_TRY(put_roots<W>(P, roots, qbase, s));
         TPG_CK(cudaMemsetAsync(P.qready.as<uint32_t>() + qbase + nroots, 0, (P.qcap - qbase - nroots) * 4, s));
         // queue counters, one per 128-byte line: head, tail<<32|done, overflow, chunk_next, maxgen
-        unsigned long long init[7 * 16];
+        unsigned long long init[8 * 16];
         memset(init, 0, sizeof(init));
         init[0] = qbase;
         init[16] = ((qbase + nroots) << 32) | qbase;
@@ -660,33 +736,31 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         if (const char *ev = getenv("TPGEN_STARVE_LANES")) A.starve_lanes = atoi(ev);
         cudaEventRecord(t.a, s);
         A.n_slots = H.n;
+        A.cacc = qc + 112;  // count modes: totals (zeroed with the counters above)
+        A.heads = P.cheads.as<HeadS>();
+        A.head_cap = (mode != M_REC) ? std::min<uint64_t>(hlim, P.cheads.cap / sizeof(HeadS)) : 0;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
         // LEAN: 32-bit masks, prime-path phase, no arc leaves any SCC (no head / segment
         // events), the slot table staged in shared memory next to the rem stacks
-        const bool lean = std::is_same<T, uint32_t>::value && !seg && !P.any_exit && tab_bytes <= kSmemTabLean &&
+        const bool lean = std::is_same<T, uint32_t>::value && !seg && !P.any_exit &&
+                          tab_bytes + (mode != M_REC ? (size_t)H.n * 8 : 0) <= kSmemTabLean &&
                           !getenv("TPGEN_NO_LEAN");
         const int grid = P.num_sms * (lean ? kLeanBlocks : DfsCfg<W>::min_blocks);
-        bool launched = false;
-        if constexpr (std::is_same<T, uint32_t>::value) {
-            if (lean) {
-                TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kSmemTabLean));
-                dfs_kernel<T, true, true><<<grid, DfsCfg<W>::threads, tab_bytes, s>>>(A);
-                launched = true;
-            }
-        }
-        if (launched) {
-        } else if (tab_bytes <= kSmemTabMax) {
-            TPG_CK(cudaFuncSetAttribute(dfs_kernel<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kSmemTabMax));
-            dfs_kernel<T, true, false><<<grid, DfsCfg<W>::threads, tab_bytes, s>>>(A);
+        if constexpr (W == 1) {
+            if (mode == M_CNT) TPG_TRY((launch_dfs<T, M_CNT>(lean, tab_bytes, grid, A, s, P.any_exit)));
+            else if (mode == M_CNT_NOHASH) TPG_TRY((launch_dfs<T, M_CNT_NOHASH>(lean, tab_bytes, grid, A, s, P.any_exit)));
+            else TPG_TRY((launch_dfs<T, M_REC>(lean, tab_bytes, grid, A, s)));
         } else {
-            dfs_kernel<T, false, false><<<grid, DfsCfg<W>::threads, 0, s>>>(A);
+            if (mode != M_REC) {
+                set_error("count-mode DFS needs one mask word (internal)");
+                return TPGEN_ERR_INTERNAL;
+            }
+            TPG_TRY((launch_dfs<T, M_REC>(false, tab_bytes, grid, A, s)));
         }
         cudaEventRecord(t.b, s);
         launches++;
         TPG_CK(cudaGetLastError());
-        unsigned long long hq[7 * 16], h[7];
+        unsigned long long hq[8 * 16], h[7];
         TPG_CK(cudaMemcpyAsync(hq, qc, sizeof(hq), cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
         const int hidx[7] = {0, 16, 0, 32, 48, 64, 80};  // old layout: head, td, -, ovf, chunk, maxgen, blk
@@ -696,7 +770,15 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         ms_dfs += ms;
         st.n_count_rounds++;
         const unsigned ovf = (unsigned)h[3];
-        if (ovf & 6u) {  // record pool or queue exhausted: undo and retry bigger
+        if (ovf & 8u) {  // count modes: head records did not fit -- room for all of them, then retry
+            if (hlim < P.cheads.cap / sizeof(HeadS)) {
+                hlim *= 2;
+            } else {
+                P.chead_hwm = std::max<uint64_t>(P.chead_hwm, hq[112 + 5]);
+                TPG_TRY(P.cheads.ensure((hq[112 + 5] + hq[112 + 5] / 4 + 256ull * 4096) * sizeof(HeadS), s));
+            }
+        }
+        if (ovf & 14u) {  // record pool, queue or head buffer exhausted: undo and retry bigger
             if (seg) TPG_CK(cudaMemcpyAsync(P.agg.p, P.agg_bak.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
             if (ovf & 2u) {
                 if (plim < P.chunk_cap) {
@@ -728,10 +810,14 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
                     ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], (h[1] >> 32) - qbase);
         }
         if (ovf & 1u) P.overflow = true;
+        if (mode != M_REC) {
+            if (cacc_h) memcpy(cacc_h, hq + 112, 8 * sizeof(unsigned long long));
+            P.chead_hwm = std::max<uint64_t>(P.chead_hwm, hq[112 + 5]);
+        }
         P.chunk_used = std::min<uint64_t>(h[4], P.chunk_cap);  // (reserved-but-unused chunks may overshoot)
         P.chunk_hwm = std::max<uint64_t>(P.chunk_hwm, P.chunk_used);
         P.q_hwm = std::max<uint64_t>(P.q_hwm, h[1] >> 32);
-        P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
+        if (mode == M_REC) P.maxgen = std::max<int>(P.maxgen, (int)(h[5] & 0xffffffffu));
         tail_out = h[1] >> 32;
         return TPGEN_OK;
     }
@@ -896,6 +982,12 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
 
     double ms_dfs = 0;
     uint64_t tail_seg = 0, tail = 0;
+    // COUNT_HASH calls with one mask word: the prime-path phase counts and digests in the
+    // DFS itself (count modes, dfs.cuh); only the segment phase writes records
+    const bool hash_only = (o.output_mode == TPGEN_OUT_COUNT_HASH);
+    const bool cnt = hash_only && W == 1 && !getenv("TPGEN_NO_CNT");
+    const int pp_mode = cnt ? (o.compute_digest ? M_CNT : M_CNT_NOHASH) : M_REC;
+    unsigned long long cacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // ---- segment phase (SCC entries) -> completion DP
     if (!seg_roots.empty()) {
         TPG_TRY(dfs_phase<T>(P, G, seg_roots, 1, 0, s, st, launches, ms_dfs, tail_seg));
@@ -917,7 +1009,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     // ---- prime-path phase
     HT("before pp phase");
     {
-        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail);
+        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail, pp_mode, cacc);
         P.presplit_active = false;
         if (r != TPGEN_OK) return r;
     }
@@ -925,19 +1017,21 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
     }
-    const int64_t nu = (int64_t)tail;
-    st.n_units = nu;
+    // units whose records the writer replays: all of them, or (count modes) the segment phase's
+    const int64_t nu = cnt ? (int64_t)tail_seg : (int64_t)tail;
+    st.n_units = (int64_t)tail;
 
     HT("after dfs phases");
     // ---- canonical order: roots by global id, then preorder of the split forest
     std::vector<int64_t> root_order;
     std::vector<int32_t> root_gid;
     const std::vector<int32_t> &pp_gid_r = *pp_gid_p;
-    const bool roots_cached = presplit_ext_used && P.presplit_roots_n == (int64_t)pp_gid_r.size() &&
+    const bool roots_cached = !cnt && presplit_ext_used && P.presplit_roots_n == (int64_t)pp_gid_r.size() &&
                               P.presplit_roots_tail == (int64_t)tail_seg;
+    static const std::vector<int32_t> kNoRoots;
     if (!roots_cached) {
         root_order.reserve(seg_roots.size() + pp_gid_r.size());
-        const std::vector<int32_t> &pp_gid = pp_gid_r;
+        const std::vector<int32_t> &pp_gid = cnt ? kNoRoots : pp_gid_r;  // count modes: segment roots only
         size_t a = 0, b = 0;
         while (a < seg_gid.size() || b < pp_gid.size()) {
             if (b >= pp_gid.size() || (a < seg_gid.size() && seg_gid[a] < pp_gid[b])) {
@@ -954,7 +1048,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     // scratch: sub[C_NUM] | acc[C_NUM] | node ping | node pong
     TPG_TRY(P.offs.ensure(nu1 * (16 * C_NUM + 2 * sizeof(LinNode)) + 256, s));
     // root table (canonical root order + start gids); the pre-split roots' table is uploaded once per plan
-    DevBuf &rbuf = presplit_ext_used ? P.presplit_roots : P.roots;
+    DevBuf &rbuf = (presplit_ext_used && !cnt) ? P.presplit_roots : P.roots;
     if (!roots_cached) {
         TPG_TRY(rbuf.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
         if (n_roots) {
@@ -962,7 +1056,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             TPG_CK(cudaMemcpyAsync(rbuf.as<char>() + n_roots * 8, root_gid.data(), n_roots * 4,
                                    cudaMemcpyHostToDevice, s));
         }
-        if (presplit_ext_used) {
+        if (presplit_ext_used && !cnt) {
             P.presplit_roots_n = n_roots;
             P.presplit_roots_tail = (int64_t)tail_seg;
         }
@@ -1034,9 +1128,43 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         cudaEventElapsedTime(&lms, tlin.a, tlin.b);
         st.ms_linearize = lms;
     }
+    const uint64_t seg_heads = tot[C_HEADS];  // head records of the replayed units
+    if (cnt && cacc[5] > 0) {  // count modes: the cross prime paths of the head records (head_weight_s)
+        TPG_TRY(P.hcomp.ensure((size_t)cacc[5] * 8, s));
+        TPG_CK(cudaMemsetAsync(ctr + 20, 0, 24, s));
+        head_weight_s_kernel<<<grid_for((int64_t)cacc[5], 256, P.num_sms * 8), 256, 0, s>>>(
+            G, P.cheads.as<HeadS>(), (int64_t)cacc[5], P.hcomp.as<uint64_t>(), ctr + 20);
+        launches++;
+        unsigned long long hc[3];
+        TPG_CK(cudaMemcpyAsync(hc, ctr + 20, 24, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        if (hc[2]) {
+            set_error("cross-SCC prime-path count exceeds 2^62");
+            return TPGEN_ERR_LIMIT_EXCEEDED;
+        }
+        cacc[6] = hc[0];
+        const uint64_t a = cacc[0] + hc[0], b = cacc[1] + hc[1];
+        if (a < cacc[0] || b < cacc[1] || a >= (1ull << 62) || b >= (1ull << 62)) {
+            set_error("prime-path count exceeds 2^62");
+            return TPGEN_ERR_LIMIT_EXCEEDED;
+        }
+        cacc[0] = a;
+        cacc[1] = b;
+    }
+    if (cnt) {  // add the count-mode phase's totals (saturating: >= 2^62 is LIMIT_EXCEEDED)
+        const uint64_t a = tot[C_PP] + cacc[0], b = tot[C_VERT] + cacc[1];
+        if (a < tot[C_PP] || b < tot[C_VERT] || a >= (1ull << 62) || b >= (1ull << 62)) {
+            set_error("prime-path count exceeds 2^62");
+            return TPGEN_ERR_LIMIT_EXCEEDED;
+        }
+        tot[C_PP] = a;
+        tot[C_VERT] = b;
+        tot[C_NUM] += cacc[2];
+        st.n_cross = (int64_t)cacc[6];
+    }
     const int64_t n_pp = (int64_t)tot[C_PP], n_vert = (int64_t)tot[C_VERT];
     st.n_extensions = (int64_t)(tot[C_NUM] + presplit_ext);
-    st.n_heads = (int64_t)tot[C_HEADS];
+    st.n_heads = cnt ? (int64_t)cacc[5] : (int64_t)tot[C_HEADS];
     st.n_segments = (int64_t)tot[C_ITEMS];
     if ((o.max_paths > 0 && n_pp > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
         set_error("result exceeds max_paths / max_extensions");
@@ -1045,7 +1173,6 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     st.n_paths = n_pp;
     st.total_vertices = n_vert;
 
-    const bool hash_only = (o.output_mode == TPGEN_OUT_COUNT_HASH);
     if (hash_only && !o.compute_digest) {  // counts only: no writer at all
         cudaEventRecord(tall.b, s);
         TPG_CK(cudaStreamSynchronize(s));
@@ -1070,8 +1197,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     if (!hash_only) TPG_TRY(out_alloc_pair(o, ow, (size_t)(n_pp + 1) * 8, (size_t)n_vert * 4, &d_off, &d_vert, s));
     unsigned long long *hacc = ctr + 16;  // digest accumulators (COUNT_HASH: filled by the writers)
     TPG_CK(cudaMemsetAsync(hacc, 0, 16, s));
-    const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = (int64_t)tot[C_HEADS];
-    TPG_TRY(P.heads.ensure(std::max<int64_t>(n_heads, 1) * sizeof(HeadRec), s));
+    const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = cnt ? (int64_t)cacc[5] : (int64_t)seg_heads;
+    TPG_TRY(P.heads.ensure(std::max<int64_t>((int64_t)seg_heads, 1) * sizeof(HeadRec), s));
     TPG_TRY(P.head_pool.ensure(std::max<uint64_t>(tot[C_HEADV], 1) * 4, s));
     TPG_TRY(P.items.ensure(std::max<int64_t>(n_items, 1) * sizeof(ItemRec), s));
     TPG_TRY(P.item_pool.ensure(std::max<uint64_t>(tot[C_ITEMV], 1) * 4, s));
@@ -1097,7 +1224,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     for (int c = 0; c < C_NUM; c++) E.lim[c] = tot[c];
     cudaEventRecord(tw.a, s);
     if (nu > 0) {
-        launch_expand<W>(H, E, nu, P.num_sms, hash_only, n_items > 0 || n_heads > 0, s);
+        launch_expand<W>(H, E, nu, P.num_sms, hash_only, n_items > 0 || seg_heads > 0, s);
         launches++;
     }
     cudaEventRecord(tw.b, s);
@@ -1108,9 +1235,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventRecord(tst.a, s);
     if (n_heads > 0) {
         TPG_TRY(P.hcomp.ensure((size_t)n_heads * 8, s));
-        head_weight_kernel<<<grid_for(n_heads, 256, 4096), 256, 0, s>>>(G, P.heads.as<HeadRec>(), n_heads,
-                                                                         P.hcomp.as<uint64_t>());
-        launches++;
+        if (!cnt) {  // (count modes: the weights were computed with the totals)
+            head_weight_kernel<<<grid_for(n_heads, 256, 4096), 256, 0, s>>>(G, P.heads.as<HeadRec>(), n_heads,
+                                                                             P.hcomp.as<uint64_t>());
+            launches++;
+        }
         uint64_t *ha[1] = {P.hcomp.as<uint64_t>()};
         uint64_t ncomp = 0;
         TPG_TRY(scan_multi(P, ha, 1, n_heads, &ncomp, s, launches));
@@ -1148,7 +1277,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         SA.n_pp = (uint64_t)n_pp;
         SA.n_vert = (uint64_t)n_vert;
         if (ncomp > 0) {
-            if (hash_only) {
+            if (cnt) {
+                stitch_hash_s_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(
+                    SA, P.cheads.as<HeadS>(), G, hacc);
+                launches++;
+            } else if (hash_only) {
                 stitch_hash_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(SA, hacc);
                 launches++;
             } else {
@@ -1191,8 +1324,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         unsigned long long hd[2];
         TPG_CK(cudaMemcpyAsync(hd, acc, 16, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
-        st.hash_lo = hd[0];
-        st.hash_hi = hd[1];
+        st.hash_lo = hd[0] + cacc[3];  // (count modes: + the DFS's own prime paths)
+        st.hash_hi = hd[1] + cacc[4];
     }
     TPG_CK(cudaStreamSynchronize(s));
     float ms = 0;

@@ -155,7 +155,20 @@ struct DevGraph {
     const uint64_t *Wc;  // completions per entry vertex (global id)
     const uint64_t *Wv;  // total vertices of those completions
     const int32_t *scc_gbase;  // global id of local 0 when an SCC's ids are contiguous, else -1
+    const uint64_t *slot_mix;  // per slot: mix64(global id), the vertex's digest value (R20)
+    const uint64_t *vmix;      // per global vertex id: mix64(id)
+    const uint64_t *scc_exm;   // per SCC (<= 64 vertices): local bits of its exit vertices (Def. 5)
     int32_t shard_lo, shard_hi;
+};
+
+// Count-mode head segment (cnt_kernel, count.cuh): the digest sum S of the head h, |h|
+// and the slot of h's last vertex (an SCC exit); the cross prime paths h (+) w (+) ...
+// over every out-of-SCC arc of that vertex are counted by head_count_kernel and hashed by
+// stitch_hash_s_kernel.  x < 0 marks an unused slot of a warp's block.
+struct TPG_ALIGN(16) HeadS {
+    uint64_t S;
+    int32_t len;
+    int32_t x;
 };
 
 struct DfsArgs {
@@ -191,6 +204,11 @@ struct DfsArgs {
     int32_t starve_lanes;
     unsigned long long *dbg;  // TPGEN_KERNEL_DEBUG builds: iterations, idle iterations, lane-steps, donations
     int n_slots;              // slot table size (copied to shared memory by the TS kernels)
+    // count modes (no records): totals [0] prime paths, [1] vertices, [2] E_canon, [3] digest a,
+    // [4] digest b, [5] head slots reserved, [6] cross-SCC prime paths; heads go to heads[0 .. head_cap)
+    unsigned long long *cacc;
+    HeadS *heads;
+    unsigned long long head_cap;
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)

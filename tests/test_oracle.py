@@ -456,8 +456,11 @@ def test_tp_stats_equal_materialized_test_paths():
 
 def test_pp_stats_parallel_equals_serial():
     g = gen.config2()
-    assert np.array_equal(oracle.pp_stats_parallel(g, procs=3, chunk=7), oracle.pp_stats(g))
-    assert np.array_equal(oracle.pp_stats_parallel(g, 5, 40, tp=(g.entry, g.exit), procs=2, chunk=3),
+    par = oracle.pp_stats_parallel(g, procs=3, chunk=7)
+    assert np.array_equal(par[:, :4], oracle.pp_stats(g))
+    assert [int(x) for x in par[:, 4]] == [oracle.ext_count(g, v, v + 1) for v in range(g.n)]
+    assert int(par[:, 4].sum()) == oracle.ext_count(g)
+    assert np.array_equal(oracle.pp_stats_parallel(g, 5, 40, tp=(g.entry, g.exit), procs=2, chunk=3)[:, :4],
                           oracle.pp_stats(g, 5, 40, tp=(g.entry, g.exit)))
 
 
