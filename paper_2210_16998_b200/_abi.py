@@ -81,9 +81,12 @@ _lib = None
 
 
 def load(path: str = LIB_PATH):
-    """Load libtpgen.so; raises if the CUDA library has not been built (no fallback)."""
+    """Load libtpgen.so; raises if the CUDA library has not been built (no fallback).
+    TPGEN_LIB_VARIANT=<name> loads the experiment build libtpgen_<name>.so instead."""
     global _lib
     if _lib is None:
+        if os.environ.get("TPGEN_LIB_VARIANT"):
+            path = os.path.join(HERE, f"libtpgen_{os.environ['TPGEN_LIB_VARIANT']}.so")
         if not os.path.exists(path):
             # build the CUDA library in-tree (nvcc, sm_100a) -- never a fallback: if nvcc
             # fails the import fails

@@ -31,11 +31,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Builds libtpgen.so (or, for A/B experiments, libtpgen_<variant>.so with extra -D defines;
+    loaded when TPGEN_LIB_VARIANT=<variant>)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libtpgen_{variant}.so")
+    if not force and not variant and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     dbg = ["-DTPGEN_KERNEL_DEBUG"] if os.environ.get("TPGEN_KERNEL_DEBUG") else []
+    dbg += [f"-D{d}" for d in defines]
     cmd = [NVCC] + FLAGS + dbg + (["-Xptxas", "-v"] if verbose else []) + \
         [os.path.join(CSRC, f) for f in SOURCES] + ["-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -44,10 +48,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc build of libtpgen.so failed")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var, defines=defs))

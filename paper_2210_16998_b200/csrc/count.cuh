@@ -39,6 +39,13 @@
 
 namespace tpg {
 
+#ifndef CNT_QUEUE
+#define CNT_QUEUE 1  // 1: prime paths into a per-warp queue (ballot), hashed 32 at a time; 0: per-lane rings
+#endif
+#ifndef CNT_PASSES
+#define CNT_PASSES 32  // passes of the step between two rounds of queue housekeeping
+#endif
+
 template <class T>
 struct CntLane {
     T M, rem, sbit, ps, exm;  // visited set, untried children of the current node, bit of s, pred(s), SCC exits
@@ -100,8 +107,8 @@ struct CntCfg {
 // Dynamic shared memory a cnt_kernel block needs beyond the staged table:
 template <class T>
 constexpr size_t cnt_smem_block() {
-    return (size_t)CntCfg<T>::warps *
-           (CntCfg<T>::ring * 32 * 12 + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) + CntCfg<T>::PLEV * 32);
+    return (size_t)CntCfg<T>::warps * (CntCfg<T>::ring * 32 * 12 + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) +
+                                       CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 10 : 0));
 }
 
 template <class T, bool TS, bool HSH, bool HX>
@@ -120,6 +127,8 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     uint32_t *sringt = reinterpret_cast<uint32_t *>(dyn + WARPS * RING * 32 * 8);    // [warp][slot][lane]
     uint32_t *srem = sringt + WARPS * RING * 32;                                      // [warp][level][lane]
     uint8_t *spath = reinterpret_cast<uint8_t *>(srem + (RS ? WARPS * 32 * 32 : 0));  // [warp][level][lane]
+    uint64_t *sq = reinterpret_cast<uint64_t *>(spath + WARPS * PLEV * 32);            // CNT_QUEUE: [warp][64]
+    uint16_t *sql = reinterpret_cast<uint16_t *>(sq + (CNT_QUEUE ? WARPS * 64 : 0));  //            [warp][64]
     const DevGraph &G = A.G;
     // 32-bit shared-window addresses of this lane's columns (opaque: kept in registers)
     uint32_t pb, rb, qb, lb;
@@ -174,12 +183,38 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     // an event of this lane into its ring: a prime path (tag = length; counted at once) or a
     // head segment (tag = slot of the exit vertex << 8 | length, bit 31 set)
     bool ring_heads = false;  // warp-uniform: some lane's ring holds a head segment
+    uint32_t qn = 0;          // CNT_QUEUE: queued prime paths of the warp (warp-uniform, < 32 between hashes)
+    uint32_t qSa, qLa;  // CNT_QUEUE: shared-window addresses of the warp's queue (opaque: kept in registers)
+    asm volatile("mov.b32 %0, %1;" : "=r"(qSa) : "r"((uint32_t)__cvta_generic_to_shared(sq + (CNT_QUEUE ? wid * 64 : 0))));
+    asm volatile("mov.b32 %0, %1;" : "=r"(qLa) : "r"((uint32_t)__cvta_generic_to_shared(sql + (CNT_QUEUE ? wid * 64 : 0))));
+    const uint32_t ltm = (1u << lane) - 1u;
     auto put_ev = [&](bool pp, bool head, uint64_t Sx, uint32_t len, int hslot) {
         if (pp) {
             t_pp += 1;
             t_vert += len;
         }
-        if (HSH ? (pp || head) : (HX && head)) {
+        if constexpr (HSH && CNT_QUEUE) {
+            const uint32_t bal = __ballot_sync(kFull, pp);
+            if (pp) {
+                const uint32_t j = qn + __popc(bal & ltm);
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(qSa + j * 8u), "l"(Sx) : "memory");
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(qLa + j * 2u), "h"((uint16_t)len) : "memory");
+            }
+            qn += __popc(bal);
+            if (qn >= 32) {
+                __syncwarp();
+                qn -= 32;
+                uint64_t z;
+                uint16_t n16;
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qSa + (qn + lane) * 8u) : "memory");
+                asm volatile("ld.shared.u16 %0, [%1];" : "=h"(n16) : "r"(qLa + (qn + lane) * 2u) : "memory");
+                const uint64_t n = n16;
+                t_ha += mix64(z ^ (kSeedA + n));
+                t_hb += mix64(z ^ (kSeedB + n));
+                __syncwarp();
+            }
+        }
+        if ((HSH && !CNT_QUEUE) ? (pp || head) : (HX && head)) {
             asm volatile("st.shared.u64 [%0], %1;" ::"r"(qb + rc * 256u), "l"(Sx) : "memory");
             const uint32_t tag = head ? (0x80000000u | ((uint32_t)hslot << 8) | len) : len;
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(lb + rc * 128u), "r"(tag) : "memory");
@@ -198,7 +233,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qb + j * 256u) : "memory");
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tag) : "r"(lb + j * 128u) : "memory");
             }
-            if (HSH && j < rc && !(tag & 0x80000000u)) {
+            if (HSH && !CNT_QUEUE && j < rc && !(tag & 0x80000000u)) {
                 t_ha += mix64(z ^ (kSeedA + (uint64_t)tag));
                 t_hb += mix64(z ^ (kSeedB + (uint64_t)tag));
             }
@@ -383,7 +418,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
         // toggle and the depth change are the same operations either way
         uint32_t ext32 = 0;
 #pragma unroll 1
-        for (int blk = 0; blk < kStepsPerIter / RING; blk++) {
+        for (int blk = 0; blk < CNT_PASSES / RING; blk++) {
 #pragma unroll 1
             for (int t = 0; t < RING; t++) {
                 const bool act = L.active && !L.done;
@@ -433,7 +468,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
             drain();
         }
         t_ext += ext32;
-        if (L.active) steps += kStepsPerIter;
+        if (L.active) steps += CNT_PASSES;
 
         // ---------------- donate on demand: the untried children of the shallowest open level
         if (feed && L.active && !L.done && (steps - last_split >= split_need || ugen < A.eager_gens)) {
@@ -507,7 +542,18 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
             L.done = false;
         }
     }
-    // the ring's remainder was drained; the head block's unused slots, then the totals
+    if constexpr (HSH && CNT_QUEUE) {  // the queue's remainder
+        __syncwarp();
+        if (lane < qn) {
+            uint64_t z;
+            uint16_t n16;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qSa + lane * 8u) : "memory");
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(n16) : "r"(qLa + lane * 2u) : "memory");
+            t_ha += mix64(z ^ (kSeedA + (uint64_t)n16));
+            t_hb += mix64(z ^ (kSeedB + (uint64_t)n16));
+        }
+    }
+    // the rings were drained; the head block's unused slots, then the totals
     for (unsigned long long j = hblk + lane; j < hblk_end; j += 32)
         if (j < A.head_cap) A.heads[j].x = -1;
     uint64_t v[7] = {t_pp, t_vert, t_ext, t_ha, t_hb, 0, t_cross};
