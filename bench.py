@@ -1,29 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the TPGen hot path on B200 (contract: one JSON line on rank 0).
 
-Default workload (BASELINE.json configs): config 3 -- one dense SCC of 22
-vertices, exact out-degree 4 (seed 1): E_canon = 2.34e8 path extensions,
-6.0e7 prime paths, 1.1e9 output vertices (4.9 GB).  For N > 1 the job is
-weak-scaled: N disjoint copies of that SCC, rank r owns the start vertices of
-copy r (no data-path collective; counts and times are reduced over NCCL).
+Headline workload (BASELINE.json: "prime paths/sec + path extensions/sec (HBM GB/s
+vs peak) at 1/2/4/8 B200"; configs[4] "high-Npath CFG ... sharded by start vertex at
+1/2/4/8 B200"): config 5 -- Start -> d1..d16 -> J -> End with 16 random strongly
+connected out-degree-2 SCCs of 56 vertices (seed 5): E_canon = 1.33e10 path
+extensions, 1.51e9 prime paths.  Its output (~5.7e10 vertices, ~230 GB) exceeds one
+GPU, so every step runs COUNT_HASH (counts, E_canon and the R20 digest of every prime
+path, nothing written).  N ranks strong-scale it by start-vertex shards: rank r runs
+shard (r, N) of the planner's cost-balanced split; `value` = prime
+paths of the whole graph per second of the slowest rank (CUDA events, max over ranks).
 
-A "step" is one full tpgen_plan_prime_paths call: DFS enumeration (segment and
-prime-path phases), linearization of the unit forest, canonical writer,
-cross-SCC stitching, output materialised in HBM (canonical offsets +
-vertices).  `value` = prime paths / s over all ranks (device time, CUDA events,
-max over ranks); `e2e` = the same through tpgen_prime_paths with the CSR in
-host memory and the result copied into pinned host memory.
+A "step" is one tpgen_plan_prime_paths call: segment phase (SCC entry trees, records
+and items), completion DP, the count-mode enumeration of every prime-path start
+(cnt_kernel), head weights and the cross-SCC stitch hash.  `e2e` is the same call
+through tpgen_prime_paths with the CSR in host memory, planned and uploaded anew
+every step (no_plan_cache), the stats struct read back.
 
---workload config5: 16 parallel 56-vertex SCCs (~1.3e10 extensions) in
-COUNT_HASH mode (counts + digest; the ~200 GB output is not materialized),
-strong-scaled by start-vertex shards.
+`secondary` (rank 0): config 3 (one dense 22-vertex SCC, out-degree 4, seed 1) with
+its full output materialized in HBM (6.0e7 prime paths, 4.9 GB), the round-1 headline.
 
---impl reference runs the CPU oracle (oracle/, single core) on a bounded
-sample of the same workload.
+--impl reference: the CPU oracle (oracle/, as it stands) on the host's cores, each
+step a fixed bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -39,71 +42,48 @@ import numpy as np  # noqa: E402
 from workloads import generators as gen  # noqa: E402
 
 HBM_FALLBACK = 6650.0
+ISSUE_PER_SM = 4  # warp schedulers per SM, one warp instruction per cycle each
 
 
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured", float(d.get("sm_max_mhz", 1965.0))
     except Exception:
-        return HBM_FALLBACK, "fallback"
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)", 1965.0
 
 
-def workload(n_ranks: int, base=None):
-    """Weak scaling: rank r enumerates the r-th of n_ranks disjoint
-    copies of the config-3 graph, i.e. the start-vertex range [r*n, (r+1)*n) of
-    their union; its output is that contiguous block of the union's canonical list."""
-    base = gen.config3() if base is None else base
-    if n_ranks == 1:
-        return base, [(0, base.n)]
-    g = gen.disjoint_union([base] * n_ranks, name=f"{n_ranks}x_{base.name}")
-    return g, [(r * base.n, (r + 1) * base.n) for r in range(n_ranks)]
-
-
-def rank_reduce(dist, world: int, n_pp: float, ext: float, ms_total: float, e2e_ms: float, device):
-    """Whole-job totals: PP and extension counts summed over ranks, times maxed
-    (the slowest rank defines the job time)."""
-    import torch
-
-    vals = torch.tensor([n_pp, ext, ms_total, e2e_ms], dtype=torch.float64, device=device)
-    if world > 1:
-        sums = vals[:2].clone()
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        mx = vals[2:].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        vals = torch.cat([sums, mx])
-    return vals.tolist()
-
-
-# SURVEY.md §8(d): algorithmic bytes per unit of the hot path --
+# algorithmic bytes per unit of the hot path --
 # 2 x (8W + 1 + 4) B per extension (frontier record written + read, W = 1)
-# + (4 len + 8) B per prime path (int32 vertices + int64 offset).
-def algorithmic_bytes(ext: int, n_pp: int, n_vert: int) -> float:
-    """A = 2*(8W+1+4)*E_canon + sum_PP (4 len + 8)  (W = 1 here)."""
-    return 2.0 * 13.0 * ext + 4.0 * n_vert + 8.0 * n_pp
+# + (4 len + 8) B per prime path when the output is materialized.
+BYTES_PER_EXT = 2.0 * (8 + 1 + 4)
 
 
 def output_bytes(n_pp: int, n_vert: int) -> float:
-    """What expand_kernel must write: int32 vertices + int64 offsets."""
+    """What the canonical writer must write: int32 vertices + int64 offsets."""
     return 4.0 * n_vert + 8.0 * (n_pp + 1)
 
 
-# ALU ceiling of the DFS enumerator (DESIGN.md "Rooflines"): 148 SMs x 128 INT32
-# lanes x SM clock / 30 lane-ops per extension (SURVEY.md 8(d): "K1 does ~10-30
-# int ops per extension"; the upper figure, so the ceiling is not overstated).
-ALU_LANES = 148 * 128
-OPS_PER_EXT = 30.0
-
-
 def ncu_traffic():
-    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) from the
-    committed ncu --set full summary of this round (profiles/), or {}."""
+    """Per-launch DRAM bytes and instruction counts (ncu --set full summaries of this round,
+    profiles/traffic.json), or {}."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f)
     except Exception:
         return {}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -163,41 +143,72 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-CONFIG3_WORKLOAD = "config3: dense SCC n=22 out-degree 4 seed 1"  # the workload both arms name
+CONFIG5_WORKLOAD = ("config5: Start->d1..d16->J->End, 16 random strongly connected out-degree-2 SCCs of 56 "
+                    "vertices, seed 5")
+CONFIG3_WORKLOAD = "config3: dense SCC n=22 out-degree 4 seed 1"
 
 
-def _oracle_block(s: int):
-    """Worker: the oracle's prime paths of config 3's start vertex s (count, seconds)."""
+def bench_config(world: int) -> dict:
+    """The workload both arms name (identical dict in the GPU arm and the reference arm)."""
+    g = gen.config5()
+    return {"workload": CONFIG5_WORKLOAD, "n_vertices": g.n, "n_arcs": int(g.offsets[-1]),
+            "mode": "COUNT_HASH: prime-path count, vertices, E_canon and the R20 digest (the ~230 GB output is "
+                    "not materialized)",
+            "l2": "flushed between timed steps (256 MB write, untimed)",
+            "parallelism": f"start-vertex shards x{world} (strong scaling)"}
+
+
+def config5_sample():
+    """The bounded oracle sample of config 5: one start vertex per 56-vertex SCC -- its first
+    vertex that is not an SCC entry -- i.e. 16 independent per-start enumerations.  SCC labels
+    come from the oracle (the reference arm never loads the CUDA library)."""
     import oracle
 
-    g, _ = workload(1)
+    g = gen.config5()
+    so, st = np.asarray(g.offsets), np.asarray(g.targets)
+    src = np.repeat(np.arange(g.n), np.diff(so))
+    lab = oracle.scc_labels(g)
+    sizes = np.bincount(lab, minlength=g.n)
+    entry = np.zeros(g.n, dtype=bool)
+    entry[st[lab[src] != lab[st]]] = True  # a predecessor outside its SCC (Def. 4)
+    starts, seen = [], set()
+    for v in range(g.n):
+        if sizes[lab[v]] > 1 and not entry[v] and lab[v] not in seen:
+            seen.add(int(lab[v]))
+            starts.append(v)
+    return g, starts
+
+
+def _sample_worker(v: int):
+    import oracle
+
+    g = gen.config5()
     t = time.perf_counter()
-    off, _ = oracle.prime_paths(g, v_lo=s, v_hi=s + 1)
-    return len(off) - 1, time.perf_counter() - t
+    row = oracle.pp_stats(g, v, v + 1)[0]
+    return int(row[0]), int(row[1]), time.perf_counter() - t
 
 
-def _oracle_warm(_):
-    import oracle  # noqa: F401  (loads liboracle.so in the worker)
+def _warm(_):
+    import oracle  # noqa: F401
 
-    workload(1)
+    gen.config5()
     return 0
 
 
 class OraclePool:
-    """The oracle as it stands, run on the host's cores: one process per start vertex
-    of config 3 (independent per-start enumerations; no change to the oracle)."""
+    """The oracle as it stands on the host's cores: one process per sampled start vertex."""
 
-    def __init__(self):
+    def __init__(self, n: int):
         import multiprocessing as mp
 
-        self.cores = max(1, min(os.cpu_count() or 1, 22))
+        self.cores = max(1, min(os.cpu_count() or 1, n))
         self.pool = mp.get_context("spawn").Pool(self.cores)
-        self.pool.map(_oracle_warm, range(self.cores))
+        self.pool.map(_warm, range(self.cores))
 
-    def step(self):
+    def run(self, starts):
         t = time.perf_counter()
-        res = self.pool.map(_oracle_block, range(22), chunksize=1)
-        return sum(r[0] for r in res), time.perf_counter() - t
+        res = self.pool.map(_sample_worker, starts, chunksize=1)
+        return sum(r[0] for r in res), sum(r[1] for r in res), time.perf_counter() - t
 
     def close(self):
         self.pool.close()
@@ -205,53 +216,165 @@ class OraclePool:
 
 
 def run_reference(args):
-    """The CPU oracle as it stands on the host's cores; each step = all of config 3."""
+    """The CPU oracle on the host's cores; each step = the bounded config-5 sample."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    g, _ = workload(1)
-    op = OraclePool()
+    g, starts = config5_sample()
+    op = OraclePool(len(starts))
     times, npp = [], 0
     for i in range(args.warmup + args.steps):
-        n, dt = op.step()
+        n, _, dt = op.run(starts)
         if i >= args.warmup:
             times.append(dt)
             npp = n
     op.close()
     total = sum(times)
     value = npp * len(times) / total
-    sample = (f"all of config3 ({npp} prime paths per step): its 22 start vertices as independent oracle calls "
-              f"(oracle/oracle.c DFS) on {op.cores} processes")
+    sample = (f"config5 start vertices {starts} (one interior vertex per SCC; {npp} prime paths per step, counted "
+              f"and hashed by oracle_pp_stats) on {op.cores} processes")
     print(json.dumps({
         "impl": "reference", "metric": "prime_paths_per_sec", "value": value, "unit": "PP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": CONFIG3_WORKLOAD, "n_vertices": g.n, "parallelism": "start-vertex shards x1",
-                   "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "PP/s", "cores": op.cores, "kind": "oracle", "sample": sample},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": bench_config(world),
+        "cpu_baseline": {"value": value, "unit": "PP/s", "cores": op.cores, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "PP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
 def cpu_baseline_leg():
+    """The oracle (oracle_pp_stats, as it stands) on a bounded sample of config 5: 4 sampled start
+    vertices on one core, then the 16-vertex sample on the host's cores."""
     import oracle
 
-    g, _ = workload(1)
+    g, starts = config5_sample()
     t = time.perf_counter()
-    off, _ = oracle.prime_paths(g, v_lo=0, v_hi=4)
+    n1 = 0
+    for v in starts[:4]:
+        n1 += int(oracle.pp_stats(g, v, v + 1)[0][0])
     dt = time.perf_counter() - t
-    npp = len(off) - 1
-    out = {"value": npp / dt, "unit": "PP/s", "cores": 1, "kind": "oracle",
-           "sample": f"config3 start vertices 0..3: {npp} prime paths in {dt:.2f} s (single core, oracle/oracle.c)"}
-    try:  # the same oracle on the host's cores: all of config 3, one process per start vertex
-        op = OraclePool()
-        n, wall = op.step()
+    out = {"value": n1 / dt, "unit": "PP/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+           "sample": f"config5 start vertices {starts[:4]}: {n1} prime paths counted and hashed in {dt:.2f} s "
+                     f"(one core, oracle/oracle.c oracle_pp_stats)"}
+    try:
+        op = OraclePool(len(starts))
+        n, _, wall = op.run(starts)
         op.close()
         out["all_cores"] = {"value": n / wall, "unit": "PP/s", "cores": op.cores, "kind": "oracle",
-                            "sample": f"all of config3: {n} prime paths in {wall:.2f} s on {op.cores} processes"}
+                            "sample": f"config5 start vertices {starts}: {n} prime paths in {wall:.2f} s on "
+                                      f"{op.cores} processes"}
     except Exception as e:  # noqa: BLE001 -- the single-core figure stands on its own
         out["all_cores"] = {"unavailable": str(e)[:200]}
+    return out
+
+
+def timed_steps(plan, kw, steps, warmup, stream, flush):
+    """W untimed calls, then K calls bracketed by CUDA events on the call's stream, L2 flushed
+    (untimed) before each.  Returns (per-step ms, per-step stats)."""
+    import torch
+
+    for _ in range(warmup):
+        ps = plan.prime_paths(**kw)
+        del ps
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    stats = []
+    for k in range(steps):
+        flush.fill_(k & 0xff)
+        ev[k][0].record(stream)
+        ps = plan.prime_paths(**kw)
+        ev[k][1].record(stream)
+        stats.append(ps.stats)
+        del ps
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev], stats
+
+
+def mean(stats, key):
+    return float(np.mean([s[key] for s in stats]))
+
+
+def dominant_roofline(stats, kernel: str, traffic_key: str, peak: float, peak_kind: str, sm_max: float):
+    """SURVEY 8(d) roofline of the dominant launch: 26 B per extension it made (frontier record
+    written + read, W = 1) / its CUDA-event duration, against the measured HBM copy peak; the
+    issue-slot view next to it (warp instructions per extension from the committed ncu capture)."""
+    traffic = ncu_traffic().get(traffic_key, {})
+    ms = mean(stats, "ms_dominant")
+    ext = mean(stats, "ext_dominant")
+    achieved = BYTES_PER_EXT * ext / (ms * 1e-3) / 1e9
+    r = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+         "frac": achieved / peak, "traffic": traffic.get("dram_bytes_per_launch"),
+         "algorithmic_bytes_per_launch": BYTES_PER_EXT * ext, "extensions_per_launch": ext,
+         "ms_per_launch": ms, "share_of_step": ms / mean(stats, "ms_device"),
+         "model": "SURVEY 8(d): 2 x (8W+1+4) = 26 B per extension (W = 1); achieved = that x the launch's "
+                  "extensions / its CUDA-event time", "peak_kind": peak_kind,
+         "traffic_source": traffic.get("source")}
+    ipe = traffic.get("warp_inst_per_ext")
+    if ipe:
+        ceil = 148 * ISSUE_PER_SM * sm_max * 1e6 / ipe / 1e9
+        ach = ext / (ms * 1e-3) / 1e9
+        r["alu_view"] = {"bound": "issue", "achieved": ach, "unit": "Gext/s", "peak": ceil, "frac": ach / ceil,
+                         "warp_inst_per_ext": ipe,
+                         "model": f"148 SM x {ISSUE_PER_SM} schedulers x {sm_max:.0f} MHz warp-instruction issue / "
+                                  f"the launch's warp instructions per extension (ncu smsp__inst_executed.sum)"}
+    return r
+
+
+def secondary_config3(dev, steps, warmup, flush, peak, peak_kind, sm_max, no_e2e):
+    """Config 3 with its whole output materialized (rank 0; the round-1 headline)."""
+    import torch
+
+    import paper_2210_16998_b200 as tp
+
+    g = gen.config3()
+    plan = tp.Plan(g, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ms_steps, stats = timed_steps(plan, {}, steps, warmup, stream, flush)
+    plan.close()
+    st = stats[-1]
+    n_pp, n_vert = st["n_paths"], st["total_vertices"]
+    ms = float(np.mean(ms_steps))
+    o_bytes = output_bytes(n_pp, n_vert)
+    ms_w = mean(stats, "ms_write")
+    rl = dominant_roofline(stats, "dfs_kernel<uint32,TS=1,LEAN=1> (records)", "dfs_kernel_c3", peak, peak_kind,
+                           sm_max)
+    rl["second"] = {"bound": "hbm", "kernel": "expand_fast_kernel<6,false>",
+                    "achieved": o_bytes / (ms_w * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": o_bytes / (ms_w * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_launch": o_bytes,
+                    "ms_per_launch": ms_w, "traffic": ncu_traffic().get("expand_fast_kernel", {}).get(
+                        "dram_bytes_per_launch"), "model": "4 B per output vertex + 8 B per offset (written once)"}
+    a_bytes = BYTES_PER_EXT * st["n_extensions"] + output_bytes(n_pp, n_vert)
+    out = {"workload": CONFIG3_WORKLOAD + ", full output materialized in HBM (canonical offsets + vertices)",
+           "metric": "prime_paths_per_sec", "value": n_pp / (ms * 1e-3), "unit": "PP/s", "ms_per_step": ms,
+           "steps": steps, "prime_paths": n_pp, "output_vertices": n_vert, "extensions": st["n_extensions"],
+           "extensions_per_sec": st["n_extensions"] / (ms * 1e-3), "roofline": rl,
+           "path_hbm": {"achieved": a_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": a_bytes / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,
+                        "model": "SURVEY 8(d): 26 B/extension + (4 len + 8) B/prime path, whole step"},
+           "breakdown_ms": {"dfs_kernel": mean(stats, "ms_dfs_write"), "linearize": mean(stats, "ms_linearize"),
+                            "expand_kernel": ms_w, "device": mean(stats, "ms_device")},
+           "presplit": "host pre-split trie tops cached per plan (planned once, outside the timed steps); e2e "
+                       "re-plans every call",
+           "gpu_launches": int(sum(s["gpu_launches"] for s in stats))}
+    if not no_e2e:
+        host_out = torch.empty(8 * (n_pp + 1) + 4 * n_vert, dtype=torch.uint8, pin_memory=True)
+        ps = tp.prime_paths(g, device=dev, output="host", host_out=host_out, plan_cache=False)
+        del ps
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        k = 3
+        for _ in range(k):
+            ps = tp.prime_paths(g, device=dev, output="host", host_out=host_out, plan_cache=False)
+            del ps
+        torch.cuda.synchronize()
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / k
+        out["e2e"] = {"value": n_pp / (e2e_ms * 1e-3), "unit": "PP/s", "ms_per_step": e2e_ms, "steps": k,
+                      "h2d_bytes_per_step": int(g.offsets.nbytes + g.targets.nbytes),
+                      "d2h_bytes_per_step": int(8 * (n_pp + 1) + 4 * n_vert),
+                      "note": "planned and uploaded anew every call; output copied into pinned host memory"}
     return out
 
 
@@ -263,18 +386,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="config3", choices=["config3", "config5"],
-                    help="config3 (default, the headline): dense 22-vertex SCC, full output, weak scaling over "
-                         "disjoint copies; config5: 16 parallel 56-vertex SCCs (~1.3e10 extensions), COUNT_HASH "
-                         "(counts + digest; the ~200 GB output is not materialized), strong scaling by "
-                         "start-vertex shards")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-3 materialized record")
+    ap.add_argument("--workload", default="config5", choices=["config5", "config3"],
+                    help="config5 (default, the headline; see the module docstring); config3: the dense 22-vertex "
+                         "SCC as the main line (weak scaling over disjoint copies), materialized or --count")
     ap.add_argument("--engine", default="dfs", choices=["dfs", "frontier"],
-                    help="dfs (default): depth-first engine, full output; frontier: the level-synchronous "
-                         "frontier engine on config 3 in COUNT_HASH mode (counts + digest; DESIGN.md 6.6)")
-    ap.add_argument("--no-digest", action="store_true",
-                    help="with --count / --engine frontier: counts and E_canon only (no digest)")
-    ap.add_argument("--count", action="store_true",
-                    help="config 3 in COUNT_HASH mode (counts + digest, no output) with the chosen engine")
+                    help="dfs (default); frontier: the level-synchronous frontier engine (config 3, COUNT_HASH)")
+    ap.add_argument("--no-digest", action="store_true", help="COUNT_HASH without the digest (counts only)")
+    ap.add_argument("--count", action="store_true", help="config 3 in COUNT_HASH mode")
     args = ap.parse_args()
     if args.engine == "frontier" and args.workload != "config3":
         ap.error("--engine frontier runs config 3 (config 5 has arcs leaving its SCCs)")
@@ -286,6 +405,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2210_16998_b200 as tp
+    from paper_2210_16998_b200 import _abi
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -294,165 +414,99 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
+    peak, peak_kind, sm_max = measured_peaks()
     c5 = args.workload == "config5"
-    fr = args.engine == "frontier"
-    cnt3 = (fr or args.count) and not c5  # config 3, counts + digest only
-    if c5:  # one graph; rank r takes start-vertex shard r of `world` (strong scaling)
+    if c5:
         g = gen.config5()
-        kw = dict(shard=(rank, world), mode="count", digest=True)
+        kw = dict(shard=(rank, world), mode="count", digest=not args.no_digest)
+        config = bench_config(world)
     else:
-        g, ranges = workload(world)
-        kw = dict(start_range=ranges[rank])
-        if cnt3:
+        base = gen.config3()
+        g = base if world == 1 else gen.disjoint_union([base] * world, name=f"{world}x_{base.name}")
+        kw = dict(start_range=(rank * base.n, (rank + 1) * base.n))
+        if args.count or args.engine == "frontier":
             kw.update(mode="count", digest=not args.no_digest, engine=args.engine)
+        config = {"workload": CONFIG3_WORKLOAD + (f" x{world} disjoint copies, one per rank" if world > 1 else ""),
+                  "n_vertices": g.n, "mode": ("COUNT_HASH" if kw.get("mode") == "count" else "materialize") +
+                  f", {args.engine} engine", "l2": "flushed between timed steps (256 MB write, untimed)",
+                  "parallelism": f"start-vertex ranges x{world} (weak scaling)"}
     stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     plan = tp.Plan(g, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
 
-    # ---------------- device-resident timing (value)
-    for _ in range(args.warmup):
-        ps = plan.prime_paths(**kw)
-        del ps
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stats = []
-    barrier()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
-        for k in range(args.steps):
-            flush.fill_(k & 0xff)  # L2 flush between timed steps (outside the events)
-            ev[k][0].record(stream)
-            ps = plan.prime_paths(**kw)
-            ev[k][1].record(stream)
-            stats.append(ps.stats)
-            del ps
-        torch.cuda.synchronize()
-    barrier()
-    ms_steps = [a.elapsed_time(b) for a, b in ev]
+        ms_steps, stats = timed_steps(plan, kw, args.steps, args.warmup, stream, flush)
+    if world > 1:
+        dist.barrier()
+    plan.close()
     ms_total = float(sum(ms_steps))
     st = stats[-1]
     n_pp, n_vert, ext = st["n_paths"], st["total_vertices"], st["n_extensions"]
-    ms_write = float(np.mean([s["ms_dfs_write"] for s in stats]))
-    launches = int(sum(s["gpu_launches"] for s in stats))
-
-    # ---------------- end-to-end through the public C ABI (host CSR in, pinned host result out)
-    e2e = None
     free_b, total_b = torch.cuda.mem_get_info(dev)
-    mem_used_gb = (total_b - free_b) / 1e9  # device memory held after the timed steps (pools included)
-    if not args.no_e2e and (c5 or cnt3):  # counts + digest come back in the stats; the CSR goes up every call
-        plan.close()  # its workspaces return to the device pool, where the e2e call's plan finds them
-        h2d = int(g.offsets.nbytes + g.targets.nbytes)
-        e2e_steps = max(1, min(args.steps, 3))
-        del_ = tp.prime_paths(g, device=dev, **kw)
-        del del_
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            ps = tp.prime_paths(g, device=dev, **kw)
-            del ps
-        torch.cuda.synchronize()
-        e2e = {"value": None, "unit": "PP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 0,
-               "ms_per_step": 1e3 * (time.perf_counter() - t0) / e2e_steps, "steps": e2e_steps,
-               "note": "COUNT_HASH: counts and the digest are returned in the stats struct"}
-    elif not args.no_e2e:
-        rng = kw["start_range"]
-        host_out = torch.empty(8 * (n_pp + 1) + 4 * n_vert, dtype=torch.uint8, pin_memory=True)
-        h2d = int(g.offsets.nbytes + g.targets.nbytes)
-        d2h = 8 * (n_pp + 1) + 4 * n_vert
-        e2e_steps = max(1, min(args.steps, 3))
-        ps = tp.prime_paths(g, device=dev, output="host", host_out=host_out, start_range=rng)
-        del ps
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            ps = tp.prime_paths(g, device=dev, output="host", host_out=host_out, start_range=rng)
-            del ps
-        torch.cuda.synchronize()
-        e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
-        e2e = {"value": None, "unit": "PP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e2e_ms, "steps": e2e_steps}
 
-    # ---------------- reduce over ranks
-    tot_pp, tot_ext, ms_max, e2e_ms_max = rank_reduce(dist, world, float(n_pp) * args.steps, float(ext) * args.steps,
-                                                      ms_total, e2e["ms_per_step"] if e2e else 0.0, dev)
+    # ---------------- end to end through the public C ABI: host CSR in, planned and uploaded anew
+    e2e = None
+    if not args.no_e2e:
+        e2e_kw = dict(kw)
+        host_out = None
+        if kw.get("mode") != "count":
+            host_out = torch.empty(8 * (n_pp + 1) + 4 * n_vert, dtype=torch.uint8, pin_memory=True)
+            e2e_kw.update(output="host", host_out=host_out)
+        ps = tp.prime_paths(g, device=dev, plan_cache=False, **e2e_kw)
+        del ps
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            ps = tp.prime_paths(g, device=dev, plan_cache=False, **e2e_kw)
+            del ps
+        torch.cuda.synchronize()
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / k
+        d2h = ctypes.sizeof(_abi.Stats) if host_out is None else int(8 * (n_pp + 1) + 4 * n_vert)
+        e2e = {"value": None, "unit": "PP/s", "h2d_bytes_per_step": int(g.offsets.nbytes + g.targets.nbytes),
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": k,
+               "note": "tpgen_prime_paths with the CSR in host memory, planned and uploaded anew every call "
+                       "(no_plan_cache = 1); " + ("counts and digest returned in the stats struct" if host_out is None
+                                                  else "output copied into pinned host memory")}
+
+    # ---------------- reduce over ranks: counts summed, times maxed (the slowest rank defines the job)
+    vals = torch.tensor([float(n_pp) * args.steps, float(ext) * args.steps, ms_total,
+                         e2e["ms_per_step"] if e2e else 0.0, float(n_pp)], dtype=torch.float64, device=dev)
+    if world > 1:
+        sums = vals[[0, 1, 4]].clone()
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        mx = vals[2:4].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        vals = torch.stack([sums[0], sums[1], mx[0], mx[1], sums[2]])
+    tot_pp, tot_ext, ms_max, e2e_max, pp_per_step = vals.tolist()
 
     if rank == 0:
-        peak, peak_kind = measured_peaks()
-        a_bytes = algorithmic_bytes(ext, n_pp, n_vert)
-        o_bytes = output_bytes(n_pp, n_vert)
         value = tot_pp / (ms_max * 1e-3)
         if e2e is not None:
-            e2e["value"] = (tot_pp / args.steps) / (e2e_ms_max * 1e-3)
-            e2e["ms_per_step"] = e2e_ms_max
-        try:
-            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-                sm_max = float(json.load(f).get("sm_max_mhz", 1965.0))
-        except Exception:
-            sm_max = 1965.0
-        ms_dfs = float(np.mean([s["ms_dfs_write"] for s in stats]))
-        ms_expand = max(float(np.mean([s["ms_write"] for s in stats])), 1e-9)  # 0 for the frontier engine
-        ms_dev = float(np.mean([s["ms_device"] for s in stats]))
-        alu_peak = ALU_LANES * sm_max * 1e6 / OPS_PER_EXT / 1e9  # Gext/s
-        dfs_ach = ext / (ms_dfs * 1e-3) / 1e9
-        traffic = ncu_traffic()
-        if c5 or cnt3:  # count mode writes no output: only the extension part of SURVEY 8(d)'s bytes applies
-            a_bytes = 2.0 * 13.0 * ext
-        roofline = {
-            "bound": "alu", "kernel": ("dfs_kernel<unsigned long,TS=1,LEAN=0>" if c5 else "dfs_kernel<unsigned int,TS=1,LEAN=1>"),
-            "achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak,
-            "traffic": traffic.get("dfs_kernel", {}).get("dram_bytes_per_launch"),
-            "ms_per_launch": ms_dfs, "units_per_launch": ext,
-            "peak_model": f"148 SM x 128 INT32 lanes x {sm_max:.0f} MHz / {OPS_PER_EXT:.0f} lane-ops per extension "
-                          "(SURVEY 8(d)); DESIGN.md Rooflines",
-            "share_of_step": ms_dfs / ms_dev,
-            "second": {
-                "bound": "hbm", "kernel": (f"expand_fast_kernel<{max(1, (int(st['max_scc']) + 3) // 4)},false>"
-                                           if int(st["max_scc"]) <= 63 else "expand_kernel"),
-                "achieved": o_bytes / (ms_expand * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": o_bytes / (ms_expand * 1e-3) / 1e9 / peak,
-                "traffic": traffic.get("expand_fast_kernel" if int(st["max_scc"]) <= 63 else "expand_kernel",
-                                       {}).get("dram_bytes_per_launch"),
-                "algorithmic_bytes_per_launch": o_bytes, "ms_per_launch": ms_expand,
-                "share_of_step": ms_expand / ms_dev,
-                "model": "4 B per output vertex + 8 B per offset (written once)"},
-            "path_hbm": {
-                "achieved": a_bytes / (ms_dev * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": a_bytes / (ms_dev * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,
-                "model": "SURVEY 8(d): 26 B/extension + (4 len + 8) B/prime path, over the whole step"},
-            "peak_kind": peak_kind,
-            "traffic_source": traffic.get("source"),
-        }
-        if c5 or cnt3:
-            roofline["traffic"] = None  # the committed ncu summary is for config 3
-            roofline["second"] = {"note": "COUNT_HASH: the writer digests each path instead of storing it",
-                                  "kernel": f"expand_fast_kernel<{max(1, (int(st['max_scc']) + 3) // 4)},true>",
-                                  "ms_per_launch": ms_expand, "share_of_step": ms_expand / ms_dev}
-            roofline["path_hbm"]["model"] = "SURVEY 8(d): 26 B/extension (no output in COUNT_HASH mode)"
-        if fr:  # every frontier record is written once and read once: 16 B each way (8 B without digest)
-            f_bytes = (16.0 if args.no_digest else 32.0) * st["n_units"]
-            f_ach = f_bytes / (ms_dfs * 1e-3) / 1e9
-            roofline = {
-                "bound": "hbm", "kernel": "frontier_level_kernel<TS=1> (all levels + root kernel)",
-                "achieved": f_ach, "peak": peak, "unit": "GB/s", "frac": f_ach / peak,
-                "traffic": traffic.get("frontier_level_kernel", {}).get("dram_bytes_per_step"),
-                "algorithmic_bytes_per_step": f_bytes, "records_per_step": st["n_units"],
-                "ms_per_step": ms_dfs, "share_of_step": ms_dfs / ms_dev,
-                "model": "16-byte path record {mask, last, first, slot base | digest sum} written once and read "
-                         "once per record (DESIGN.md 6.6); traffic = DRAM bytes of all level launches of one call "
-                         "(ncu launch list, profiles/traffic.json)",
-                "alu_view": {"achieved": dfs_ach, "peak": alu_peak, "unit": "Gext/s", "frac": dfs_ach / alu_peak},
-                "path_hbm": {"achieved": a_bytes / (ms_dev * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                             "frac": a_bytes / (ms_dev * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,
-                             "model": "SURVEY 8(d): 26 B/extension (no output in COUNT_HASH mode)"},
-                "peak_kind": peak_kind,
-            }
+            e2e["value"] = pp_per_step / (e2e_max * 1e-3)
+            e2e["ms_per_step"] = e2e_max
+        ms_dev = mean(stats, "ms_device")
+        if c5:
+            roofline = dominant_roofline(stats, "cnt_kernel<uint64,TS=1,HSH=1,HX=1> (count-mode DFS, prime-path "
+                                                "phase)", "cnt_kernel_c5", peak, peak_kind, sm_max)
+        elif kw.get("engine") == "frontier":
+            roofline = dominant_roofline(stats, "frontier_level_kernel (all levels of the call)", "frontier", peak,
+                                         peak_kind, sm_max)
+        elif kw.get("mode") == "count":
+            roofline = dominant_roofline(stats, "cnt_kernel<uint32,TS=1,HSH=1,HX=0>", "cnt_kernel_c3", peak,
+                                         peak_kind, sm_max)
+        else:
+            roofline = dominant_roofline(stats, "dfs_kernel<uint32,TS=1,LEAN=1> (records)", "dfs_kernel_c3", peak,
+                                         peak_kind, sm_max)
+        a_bytes = BYTES_PER_EXT * ext + (0.0 if kw.get("mode") == "count" else output_bytes(n_pp, n_vert))
+        roofline["path_hbm"] = {"achieved": a_bytes / (ms_dev * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                                "frac": a_bytes / (ms_dev * 1e-3) / 1e9 / peak, "algorithmic_bytes": a_bytes,
+                                "model": "SURVEY 8(d) bytes of the whole step (rank 0's shard)"}
         out = {
             "metric": "prime_paths_per_sec",
             "value": value,
@@ -466,34 +520,29 @@ def main():
             "vs_baseline": None,
             "dtype": "int32",
             "data": "synthetic",
-            "config": {"workload": ("config5: 16 parallel SCCs n=56 out-degree 2 seed 5, COUNT_HASH (counts + "
-                                    "digest, output not materialized)" if c5 else
-                                    CONFIG3_WORKLOAD + (f", COUNT_HASH{' without digest' if args.no_digest else ''}, "
-                                                       f"{args.engine} engine" if cnt3 else "") +
-                                    (f" x{world} disjoint copies, one per rank" if world > 1 else "")),
-                       "n_vertices": g.n, "prime_paths_per_rank": n_pp, "output_vertices_per_rank": n_vert,
-                       "extensions_per_rank": ext, "l2": "flushed between timed steps (256 MB write, untimed)",
-                       "parallelism": f"start-vertex shards x{world}"},
+            "config": config,
             "extensions_per_sec": tot_ext / (ms_max * 1e-3),
+            "counts": {"prime_paths": int(pp_per_step), "prime_paths_rank0": n_pp, "output_vertices_rank0": n_vert,
+                       "extensions_rank0": ext, "cross_scc_rank0": st["n_cross"],
+                       "digest_rank0": [st["hash_lo"], st["hash_hi"]], "shard_rank0": [st["shard_lo"], st["shard_hi"]]},
             "roofline": roofline,
             "ms_steps": {"min": float(np.min(ms_steps)), "median": float(np.median(ms_steps)),
                          "max": float(np.max(ms_steps))},
-            "breakdown_ms": {"dfs_kernel": ms_dfs, "linearize": float(np.mean([s["ms_linearize"] for s in stats])),
-                             "other_count": float(np.mean([s["ms_count"] - s["ms_dfs_count"] - s["ms_linearize"]
-                                                           for s in stats])),
-                             "expand_kernel": ms_expand,
-                             "stitch": float(np.mean([s["ms_stitch"] for s in stats])), "device": ms_dev},
-            "device_mem_used_gb": mem_used_gb,
+            "breakdown_ms": {"dominant": mean(stats, "ms_dominant"), "dfs_phases": mean(stats, "ms_dfs_write"),
+                             "linearize": mean(stats, "ms_linearize"), "writer": mean(stats, "ms_write"),
+                             "stitch": mean(stats, "ms_stitch"), "device": ms_dev},
+            "device_mem_used_gb": (total_b - free_b) / 1e9,
             "count_rounds": st["n_count_rounds"],
-            "n_units": st["n_units"],
-            "gpu_launches": launches,
+            "gpu_launches": int(sum(s["gpu_launches"] for s in stats)),
             "e2e": e2e,
             "clocks": clk.summary(),
         }
+        if c5 and not args.no_secondary:
+            out["secondary"] = secondary_config3(dev, min(args.steps, 10), max(args.warmup, 3), flush, peak,
+                                                 peak_kind, sm_max, args.no_e2e)
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_leg()
         print(json.dumps(out))
-    plan.close()
     if world > 1:
         dist.destroy_process_group()
 

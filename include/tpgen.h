@@ -115,6 +115,10 @@ typedef struct {
                                   TPGEN_ERR_INVALID_ARGUMENT).  A level that does not fit in the device
                                   memory budget switches the call to the DFS-chunked frontier (DESIGN.md
                                   §6.6); TPGEN_ERR_OUT_OF_MEMORY only when even one chunk cannot fit. */
+    int32_t no_plan_cache;     /* one-shot calls (tpgen_prime_paths / tpgen_test_paths) keep the last graph's plan
+                                  and device tables per device and reuse them when the next call passes a
+                                  byte-identical CSR; 1 = always plan and upload anew (what an end-to-end timing of a
+                                  fresh graph measures).  Ignored by the tpgen_plan_* calls. */
 } tpgen_options;
 
 typedef struct {
@@ -138,6 +142,8 @@ typedef struct {
     double ms_dfs_write;     /* device time of the dominant kernel (dfs_kernel, both phases) */
     double ms_dfs_count;     /* same as ms_dfs_write (kept for ABI stability) */
     double ms_linearize;     /* device: linearization of the unit forest (canonical offsets) */
+    double ms_dominant;      /* device time of the prime-path phase's enumeration kernel (the dominant launch) */
+    int64_t ext_dominant;    /* extensions (E_canon terms) that launch made */
 } tpgen_stats;
 
 void tpgen_options_init(tpgen_options *opt);

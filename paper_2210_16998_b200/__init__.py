@@ -133,7 +133,8 @@ class _TorchAllocator:
 
 def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest: bool, max_paths: int,
              max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None,
-             start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs") -> _abi.Options:
+             start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
+             plan_cache: bool = True) -> _abi.Options:
     lib = library()
     o = _abi.Options()
     lib.tpgen_options_init(ctypes.byref(o))
@@ -148,6 +149,7 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
     o.max_extensions = max_extensions
     o.compute_digest = 1 if digest else 0
     o.engine = _engine(engine)
+    o.no_plan_cache = 0 if plan_cache else 1
     if alloc is not None:
         o.device_alloc = alloc.alloc_fn
         o.device_free = alloc.free_fn
@@ -211,18 +213,20 @@ def _wrap(paths: _abi.Paths, stats: _abi.Stats, alloc: Optional[_TorchAllocator]
 def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "materialize",
                 shard: Tuple[int, int] = (0, 1), digest: bool = False, max_paths: int = 0,
                 max_extensions: int = 0, stream=None, host_out=None,
-                start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs") -> PathSet:
+                start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
+                plan_cache: bool = True) -> PathSet:
     """All prime paths of ``graph`` (Def. 1), canonical order.
 
     ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host).
     ``engine``: "dfs" (default) or "frontier" (level-synchronous, ``mode="count"`` only;
-    include/tpgen.h TPGEN_ENGINE_FRONTIER)."""
+    include/tpgen.h TPGEN_ENGINE_FRONTIER).  ``plan_cache=False``: plan and upload the graph
+    anew even if the previous call passed the same CSR (tpgen_options.no_plan_cache)."""
     lib = library()
     _engine(engine)
     so, st, n = _csr(graph)
     alloc = None  # outputs come from the library's device memory pool (no Python callback while timing)
     o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
-                 alloc, host_out, start_range, engine)
+                 alloc, host_out, start_range, engine, plan_cache)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_prime_paths(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc, host_out)

@@ -37,7 +37,7 @@ class Options(Structure):
                 ("max_paths", c_int64), ("max_extensions", c_int64), ("tp_mode", c_int32),
                 ("compute_digest", c_int32), ("device_alloc", ALLOC_FN), ("device_free", FREE_FN),
                 ("alloc_ctx", c_void_p), ("host_out", c_void_p), ("host_out_bytes", c_size_t),
-                ("engine", c_int32)]
+                ("engine", c_int32), ("no_plan_cache", c_int32)]
 
 
 class Stats(Structure):
@@ -48,7 +48,8 @@ class Stats(Structure):
                 ("gpu_launches", c_int64), ("shard_lo", c_int32), ("shard_hi", c_int32),
                 ("ms_plan", c_double), ("ms_count", c_double), ("ms_write", c_double), ("ms_stitch", c_double),
                 ("ms_device", c_double), ("ms_total", c_double), ("ms_dfs_write", c_double),
-                ("ms_dfs_count", c_double), ("ms_linearize", c_double)]
+                ("ms_dfs_count", c_double), ("ms_linearize", c_double), ("ms_dominant", c_double),
+                ("ext_dominant", c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -104,7 +104,7 @@ tpgen_status cached_plan(const int64_t *so, const int32_t *st, int32_t n, const 
     if (cudaSetDevice(dev) != cudaSuccess) return TPGEN_ERR_CUDA;
     const double t0 = now_ms();
     const int64_t m = (n > 0) ? so[n] - so[0] : 0;
-    if (p->last_valid && n >= 0 && (int64_t)p->last_off.size() == (int64_t)n + 1 && (int64_t)p->last_tgt.size() == m &&
+    if (!o.no_plan_cache && p->last_valid && n >= 0 && (int64_t)p->last_off.size() == (int64_t)n + 1 && (int64_t)p->last_tgt.size() == m &&
         (n == 0 || memcmp(p->last_off.data(), so, sizeof(int64_t) * ((size_t)n + 1)) == 0) &&
         (m == 0 || memcmp(p->last_tgt.data(), st + so[0], sizeof(int32_t) * (size_t)m) == 0)) {
         p->impl.ms_plan = now_ms() - t0;  // the same graph as the previous call: the plan stands

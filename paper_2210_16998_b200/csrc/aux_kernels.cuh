@@ -613,48 +613,169 @@ __global__ void head_weight_s_kernel(DevGraph G, const HeadS *heads, int64_t n, 
     }
 }
 
-// Count modes: the digest of every cross-SCC prime path h (+) completion from the head's
-// digest sum S(h) (accumulated by the DFS) -- only the completion's vertices are absorbed,
-// at positions |h|, |h|+1, ... (R20: term mix(v) * (2 pos + 1)).  Completion k of a head
-// runs over its exit vertex's out-of-SCC arcs in order (W(w) completions each), then is
-// unranked through the entry tables.  One thread per completion; unused head slots have
-// weight 0 and are never reached.
-__global__ void stitch_hash_s_kernel(StitchArgs A, const HeadS *hs, DevGraph G, unsigned long long *acc) {
+// ------------------------------------------------ count modes: items and stitching
+// Items of the count-mode segment phase (ItemS, written in no order by cnt_kernel<SEG>):
+// counted per entry vertex, scattered into per-entry groups (order inside a group is
+// irrelevant: every completion is hashed once), weighted and scanned like the record path's.
+// (warp-aggregated: the lanes of a warp holding items of the same entry -- usually all of
+// them: a warp's items come from one walk -- add their count with one atomic)
+__global__ void item_count_s_kernel(const ItemS *items, int64_t n, unsigned long long *cnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_up = (n + 31) & ~(int64_t)31;  // whole warps iterate together
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
+        const int32_t e = i < n ? items[i].ent : -1;
+        const unsigned grp = __match_any_sync(kFull, e);
+        if (e >= 0 && lane == __ffs(grp) - 1) atomicAdd(cnt + e, (unsigned long long)__popc(grp));
+    }
+}
+__global__ void item_scatter_s_kernel(const ItemS *items, int64_t n, unsigned long long *cursor, ItemS *out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_up = (n + 31) & ~(int64_t)31;
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
+        ItemS it;
+        it.ent = -1;
+        if (i < n) it = items[i];
+        const unsigned grp = __match_any_sync(kFull, it.ent);
+        const int leader = __ffs(grp) - 1;
+        unsigned long long base = 0;
+        if (it.ent >= 0 && lane == leader) base = atomicAdd(cursor + it.ent, (unsigned long long)__popc(grp));
+        base = __shfl_sync(kFull, base, leader);
+        if (it.ent >= 0) out[base + __popc(grp & ((1u << lane) - 1u))] = it;
+    }
+}
+// per entry (global id): first and end item of its group, from the exclusive scan of the counts
+__global__ void item_bounds_s_kernel(const uint64_t *start, const uint64_t *cnt, int32_t n, int64_t *ibeg,
+                                     int64_t *iend) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        ibeg[v] = (int64_t)start[v];
+        iend[v] = (int64_t)(start[v] + cnt[v]);
+    }
+}
+// Completion-DP aggregates from the raw items (before the DP): per entry (slot) the number
+// and total length of its tail segments, per (entry, out-arc) pair those of its transit
+// segments (Def. 6, R9).  Warp-aggregated: one atomic per distinct key of a warp.
+__global__ void item_agg_s_kernel(DevGraph G, const ItemS *items, int64_t n, unsigned long long *tail_cnt,
+                                  unsigned long long *tail_len, unsigned long long *pair_cnt,
+                                  unsigned long long *pair_len) {
     const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
-    uint64_t sa = 0, sb = 0;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < A.n_comp;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t h = upper_bound_u64(A.comp_off, 0, A.n_heads, g) - 1;
-        const HeadS H = hs[h];
-        uint64_t kk = g - A.comp_off[h];
-        const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[H.x].gid));
-        int32_t x = -1;
-        for (int a = 0; a < m.z; a++) {  // the arc whose completions hold index kk
-            const int32_t xa = __ldg(G.out_gid + m.y + a);
-            const uint64_t Wx = __ldg(G.Wc + xa);
-            if (kk < Wx) {
-                x = xa;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_up = (n + 31) & ~(int64_t)31;
+    const int lane = threadIdx.x & 31;
+    auto add = [&](long long key, uint32_t len, unsigned long long *c, unsigned long long *l) {
+        const unsigned grp = __match_any_sync(kFull, key);
+        const unsigned sl = __reduce_add_sync(grp, key >= 0 ? len : 0u);
+        if (key >= 0 && lane == __ffs(grp) - 1) {
+            atomicAdd(c + key, (unsigned long long)__popc(grp));
+            atomicAdd(l + key, (unsigned long long)sl);
+        }
+    };
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
+        ItemS it;
+        it.ent = -1;
+        if (i < n) it = items[i];
+        const bool ok = it.ent >= 0;
+        const int32_t es = ok ? __ldg(G.v_slot + it.ent) : 0;
+        add((ok && it.x < 0) ? (long long)es : -1ll, (uint32_t)it.len, tail_cnt, tail_len);
+        int off = 0, cnt = 0;
+        long long pbase = 0;
+        if (ok && it.x >= 0) {
+            const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[it.x].gid));
+            off = m.y;
+            cnt = m.z;
+            const int32_t c = __ldg(G.comp + it.ent);
+            pbase = __ldg(G.scc_pair_base + c) + (long long)__ldg(G.slot_eidx + es) * __ldg(G.scc_nout + c) -
+                    __ldg(G.scc_out_base + c);
+        }
+        const int mx = (int)__reduce_max_sync(kFull, (unsigned)cnt);
+        for (int a = 0; a < mx; a++) add(a < cnt ? pbase + off + a : -1ll, (uint32_t)it.len, pair_cnt, pair_len);
+    }
+}
+
+// completions of an item and their vertices: a tail 1 / len; a transit sum over the exit's arcs
+__global__ void item_weight_s_kernel(DevGraph G, const ItemS *items, int64_t n, uint64_t *cw, uint64_t *vw) {
+    const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const ItemS it = items[i];
+        if (it.x < 0) {
+            cw[i] = 1;
+            vw[i] = (uint64_t)it.len;
+        } else {
+            const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[it.x].gid));
+            uint64_t W = 0, V = 0;
+            for (int a = 0; a < m.z; a++) {
+                const int32_t y = __ldg(G.out_gid + m.y + a);
+                const uint64_t Wy = __ldg(G.Wc + y);
+                W += Wy;
+                V += (uint64_t)it.len * Wy + __ldg(G.Wv + y);
+            }
+            cw[i] = W;
+            vw[i] = V;
+        }
+    }
+}
+
+struct StitchSArgs {
+    const HeadS *heads;
+    int64_t n_heads;
+    const uint64_t *comp_off;  // exclusive scan of the heads' completion counts
+    uint64_t n_comp;
+    const ItemS *items;        // grouped by entry vertex
+    const uint64_t *cum;       // global exclusive scan of the items' completion counts
+    const int64_t *ibeg, *iend;  // per entry vertex (global id)
+};
+
+// Count modes: the digest of the cross-SCC prime path h (+) completion k of head H, from the
+// head's digest sum S(h) and the items' (A, B): an item at offset o adds A + 2 o B (R20).
+// Completion k runs over the exit vertex's out-of-SCC arcs in order (W(w) completions each),
+// then is unranked through the entry groups (a binary search per level inside one group).
+__device__ __forceinline__ void hash_completion(const StitchSArgs &A, const DevGraph &G, const HeadS &H, uint64_t kk,
+                                                uint64_t &sa, uint64_t &sb) {
+    const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
+    const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[H.x].gid));
+    int32_t x = -1;
+    for (int a = 0; a < m.z; a++) {  // the arc whose completions hold index kk
+        const int32_t xa = __ldg(G.out_gid + m.y + a);
+        const uint64_t Wx = __ldg(G.Wc + xa);
+        if (kk < Wx) {
+            x = xa;
+            break;
+        }
+        kk -= Wx;
+    }
+    uint64_t S = H.S;
+    uint32_t pos = (uint32_t)H.len;
+    while (true) {
+        const int64_t b = A.ibeg[x], e = A.iend[x];
+        int64_t i = b;
+        uint64_t k2 = kk;
+        if (e - b > 1) {
+            const uint64_t bc = A.cum[b];
+            i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            k2 = kk - (A.cum[i] - bc);
+        }
+        const ItemS it = A.items[i];
+        S += it.A + ((uint64_t)(uint32_t)it.B * (2u * pos) + ((uint64_t)((uint32_t)(it.B >> 32) * (2u * pos)) << 32));
+        pos += (uint32_t)it.len;
+        if (it.x < 0) break;  // a tail segment ends the path
+        const int4 mi = __ldg(reinterpret_cast<const int4 *>(&slots[it.x].gid));
+        for (int a = 0; a < mi.z; a++) {  // the out-arc of the transit whose completions hold k2
+            const int32_t ya = __ldg(G.out_gid + mi.y + a);
+            const uint64_t Wy = __ldg(G.Wc + ya);
+            if (k2 < Wy) {
+                x = ya;
                 break;
             }
-            kk -= Wx;
+            k2 -= Wy;
         }
-        uint64_t S = H.S;
-        uint32_t pos = (uint32_t)H.len;
-        while (true) {  // unrank the completion through the entry tables, absorbing each item
-            const int64_t b = A.ibeg[x], e = A.iend[x];
-            const uint64_t bc = A.cum[b];
-            const int64_t i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
-            const uint64_t k2 = kk - (A.cum[i] - bc);
-            const ItemRec it = A.items[i];
-            const int32_t *src = A.item_pool + it.pool_off;
-            for (int j = 0; j < it.len; j++, pos++) S += __ldg(G.vmix + __ldg(src + j)) * pos_weight(pos);
-            if (it.y < 0) break;
-            x = it.y;
-            kk = k2;
-        }
-        sa += mix64(S ^ (kSeedA + (uint64_t)pos));
-        sb += mix64(S ^ (kSeedB + (uint64_t)pos));
+        kk = k2;
     }
+    sa += mix64(S ^ (kSeedA + (uint64_t)pos));
+    sb += mix64(S ^ (kSeedB + (uint64_t)pos));
+}
+
+__device__ __forceinline__ void hash_flush(uint64_t sa, uint64_t sb, unsigned long long *acc) {
 #pragma unroll
     for (int d = 16; d; d >>= 1) {
         sa += __shfl_xor_sync(kFull, sa, d);
@@ -664,6 +785,43 @@ __global__ void stitch_hash_s_kernel(StitchArgs A, const HeadS *hs, DevGraph G, 
         atomicAdd(acc, (unsigned long long)sa);
         atomicAdd(acc + 1, (unsigned long long)sb);
     }
+}
+
+constexpr uint64_t kSmallHead = 32;  // heads with at most this many completions: one thread each
+
+// Small heads: one thread per head slot hashes all of its W <= kSmallHead completions (no search
+// over the heads); big[h] = 1 marks the others for stitch_big_kernel.
+__global__ void stitch_small_kernel(StitchSArgs A, DevGraph G, uint64_t *big, unsigned long long *acc) {
+    uint64_t sa = 0, sb = 0;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < A.n_heads; h += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = ((h + 1 < A.n_heads) ? A.comp_off[h + 1] : A.n_comp) - A.comp_off[h];
+        big[h] = w > kSmallHead ? 1 : 0;
+        if (w == 0 || w > kSmallHead) continue;
+        const HeadS H = A.heads[h];
+        for (uint64_t k = 0; k < w; k++) hash_completion(A, G, H, k, sa, sb);
+    }
+    hash_flush(sa, sb, acc);
+}
+// big heads, compacted: idx[j] = head slot, w[j] = its completion count
+__global__ void stitch_big_list_kernel(StitchSArgs A, const uint64_t *pos, int64_t *idx, uint64_t *w) {
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < A.n_heads; h += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t wh = ((h + 1 < A.n_heads) ? A.comp_off[h + 1] : A.n_comp) - A.comp_off[h];
+        if (wh > kSmallHead) {
+            idx[pos[h]] = h;
+            w[pos[h]] = wh;
+        }
+    }
+}
+// big heads: one thread per completion (a binary search over the few big heads' offsets)
+__global__ void stitch_big_kernel(StitchSArgs A, DevGraph G, const int64_t *idx, const uint64_t *off, int64_t n_big,
+                                  uint64_t n_big_comp, unsigned long long *acc) {
+    uint64_t sa = 0, sb = 0;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_big_comp;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t j = upper_bound_u64(off, 0, n_big, g) - 1;
+        hash_completion(A, G, A.heads[idx[j]], g - off[j], sa, sb);
+    }
+    hash_flush(sa, sb, acc);
 }
 
 __global__ void fill_u32_kernel(uint32_t *p, uint32_t v, int64_t n) {

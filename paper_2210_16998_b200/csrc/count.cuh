@@ -51,8 +51,14 @@ struct CntLane {
     T M, rem, sbit, ps, exm;  // visited set, untried children of the current node, bit of s, pred(s), SCC exits
     int32_t l, r, s, vb;      // depth, unit root depth, start vertex (local), slot base of the SCC
     uint64_t S;               // digest sum of path[0..l]
-    bool active, done;
+    uint64_t B;               // segment phase: sum of mix(v) over path[0..l] (an item's offset slope)
+    bool active, done, emit;  // emit (segment phase): s lies in the call's start range
 };
+
+// Event kinds of a lane's ring (tag bits 29-31; bits 8-28 the slot of the path's last
+// vertex, bits 0-7 the path length): a prime path, a head segment (prime-path phase), a
+// tail segment or the transit segments over an exit vertex's out-of-SCC arcs (segment phase).
+enum CntEv : uint32_t { EK_PP = 0, EK_HEAD = 1, EK_TAIL = 2, EK_TRANSIT = 3 };
 
 // Hot-loop table per slot: in-SCC successor bits and the digest value mix64(gid) (R20),
 // staged in shared memory as {sin, mix} pairs (TS) or read from the global copies.
@@ -98,44 +104,53 @@ struct CntCfg {
     static constexpr bool RS = sizeof(T) == 4;  // untried children on a shared-memory stack
     static constexpr int PLEV = RS ? 32 : 64;   // path levels per lane
     static constexpr int threads = 256, warps = 8, min_blocks = 3;
-    static constexpr int ring = 8;              // prime paths a lane holds between two warp drains
+    static constexpr int ring = 8;              // passes between two warp drains of the lanes' rings
+    static constexpr int ring_slots = ring + 1; // events a lane holds between drains: one per pass + its unit
+                                                // root's (put when the unit starts, before the passes)
 };
 
 // Shared-memory layouts (per warp, [row][lane] so the 32 lanes of a row never conflict):
-// the lanes' event rings -- digest sums [slot][lane] (8 B) and tags [slot][lane] (4 B) --,
-// the untried-children stack [level][lane] (32-bit masks) and the path bytes [level][lane].
+// the lanes' event rings -- digest sums [slot][lane] (8 B), tags [slot][lane] (4 B), and in
+// the segment phase the B sums [slot][lane] (8 B) --, the untried-children stack
+// [level][lane] (32-bit masks) and the path bytes [level][lane].
 // Dynamic shared memory a cnt_kernel block needs beyond the staged table:
 template <class T>
-constexpr size_t cnt_smem_block() {
-    return (size_t)CntCfg<T>::warps * (CntCfg<T>::ring * 32 * 12 + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) +
+constexpr size_t cnt_smem_block(bool seg) {
+    return (size_t)CntCfg<T>::warps * (CntCfg<T>::ring_slots * 32 * (seg ? 20 : 12) + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) +
                                        CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 10 : 0));
 }
 
-template <class T, bool TS, bool HSH, bool HX>
+// SEG: the segment phase -- the trees of the SCC entry vertices: their cycles are prime
+// paths (when the entry lies in the call's start range), their tail and transit segments
+// (R8/R9) become ItemS records and the completion-DP aggregates.
+template <class T, bool TS, bool HSH, bool HX, bool SEG>
 __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt_kernel(DfsArgs A) {
     using C = CntCfg<T>;
     constexpr bool RS = C::RS;
     constexpr int WARPS = C::warps;
     constexpr int PLEV = C::PLEV;
     constexpr int RING = C::ring;
+    constexpr int RSLOTS = C::ring_slots;
     __shared__ unsigned long long s_td, s_head;
     __shared__ unsigned s_ov;
     extern __shared__ __align__(16) uint8_t stab[];  // [TS: {sin, mix}[n_slots]] then the block's areas
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint8_t *dyn = stab + (TS ? (size_t)A.n_slots * 16 : 0);
     uint64_t *sring = reinterpret_cast<uint64_t *>(dyn);                             // [warp][slot][lane]
-    uint32_t *sringt = reinterpret_cast<uint32_t *>(dyn + WARPS * RING * 32 * 8);    // [warp][slot][lane]
-    uint32_t *srem = sringt + WARPS * RING * 32;                                      // [warp][level][lane]
+    uint32_t *sringt = reinterpret_cast<uint32_t *>(dyn + WARPS * RSLOTS * 32 * 8);    // [warp][slot][lane]
+    uint32_t *srem = sringt + WARPS * RSLOTS * 32;                                      // [warp][level][lane]
     uint8_t *spath = reinterpret_cast<uint8_t *>(srem + (RS ? WARPS * 32 * 32 : 0));  // [warp][level][lane]
     uint64_t *sq = reinterpret_cast<uint64_t *>(spath + WARPS * PLEV * 32);            // CNT_QUEUE: [warp][64]
     uint16_t *sql = reinterpret_cast<uint16_t *>(sq + (CNT_QUEUE ? WARPS * 64 : 0));  //            [warp][64]
+    uint64_t *sringb = reinterpret_cast<uint64_t *>(sql + (CNT_QUEUE ? WARPS * 64 : 0));  // SEG: [warp][slot][lane]
     const DevGraph &G = A.G;
     // 32-bit shared-window addresses of this lane's columns (opaque: kept in registers)
-    uint32_t pb, rb, qb, lb;
+    uint32_t pb, rb, qb, lb, bb = 0;
+    if (SEG) asm volatile("mov.b32 %0, %1;" : "=r"(bb) : "r"((uint32_t)__cvta_generic_to_shared(sringb + wid * RSLOTS * 32) + lane * 8));
     asm volatile("mov.b32 %0, %1;" : "=r"(pb) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * PLEV * 32) + lane));
     asm volatile("mov.b32 %0, %1;" : "=r"(rb) : "r"((uint32_t)__cvta_generic_to_shared(srem + (RS ? wid * 32 * 32 : 0)) + (RS ? lane * 4 : 0)));
-    asm volatile("mov.b32 %0, %1;" : "=r"(qb) : "r"((uint32_t)__cvta_generic_to_shared(sring + wid * RING * 32) + lane * 8));
-    asm volatile("mov.b32 %0, %1;" : "=r"(lb) : "r"((uint32_t)__cvta_generic_to_shared(sringt + wid * RING * 32) + lane * 4));
+    asm volatile("mov.b32 %0, %1;" : "=r"(qb) : "r"((uint32_t)__cvta_generic_to_shared(sring + wid * RSLOTS * 32) + lane * 8));
+    asm volatile("mov.b32 %0, %1;" : "=r"(lb) : "r"((uint32_t)__cvta_generic_to_shared(sringt + wid * RSLOTS * 32) + lane * 4));
     CntTab<T, TS> tab;
     tab.g = reinterpret_cast<const Slot<1> *>(G.slots);
     tab.gm = G.slot_mix;
@@ -158,14 +173,16 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     Unit<1> *units = reinterpret_cast<Unit<1> *>(A.units);
     uint64_t t_pp = 0, t_vert = 0, t_ext = 0, t_ha = 0, t_hb = 0, t_cross = 0;
     uint32_t rc = 0;  // prime paths in this lane's ring
-    unsigned long long hblk = 0, hblk_end = 0;
+    unsigned long long hblk = 0, hblk_end = 0;  // warp-uniform: the warp's block of head slots
+    unsigned long long iblk = 0, iblk_end = 0;  // ... of item slots (segment phase)
 
     CntLane<T> L;
     L.active = false;
     L.done = false;
     L.l = L.r = L.s = L.vb = 0;
     L.M = L.rem = L.sbit = L.ps = L.exm = 0;
-    L.S = 0;
+    L.S = L.B = 0;
+    L.emit = true;
     bool waiting = false, exited = false;
     int64_t slot = -1;
     int32_t uscc = 0, ugen = 0;
@@ -180,15 +197,15 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     unsigned snap_ov = 0;
     bool qdone = false, prev_active = true;
 
-    // an event of this lane into its ring: a prime path (tag = length; counted at once) or a
-    // head segment (tag = slot of the exit vertex << 8 | length, bit 31 set)
-    bool ring_heads = false;  // warp-uniform: some lane's ring holds a head segment
-    uint32_t qn = 0;          // CNT_QUEUE: queued prime paths of the warp (warp-uniform, < 32 between hashes)
+    // an event of this lane into its ring (see CntEv): prime paths are counted at once and, with
+    // CNT_QUEUE, go to the warp's queue instead; everything else waits for the drain
+    bool ring_ev = false;  // warp-uniform: some lane's ring holds an event other than a prime path
     uint32_t qSa, qLa;  // CNT_QUEUE: shared-window addresses of the warp's queue (opaque: kept in registers)
     asm volatile("mov.b32 %0, %1;" : "=r"(qSa) : "r"((uint32_t)__cvta_generic_to_shared(sq + (CNT_QUEUE ? wid * 64 : 0))));
     asm volatile("mov.b32 %0, %1;" : "=r"(qLa) : "r"((uint32_t)__cvta_generic_to_shared(sql + (CNT_QUEUE ? wid * 64 : 0))));
+    uint32_t qn = 0;  // CNT_QUEUE: queued prime paths of the warp (warp-uniform, < 32 between hashes)
     const uint32_t ltm = (1u << lane) - 1u;
-    auto put_ev = [&](bool pp, bool head, uint64_t Sx, uint32_t len, int hslot) {
+    auto put_ev = [&](bool pp, bool other, uint32_t kind, uint64_t Sx, uint64_t Bx, uint32_t len, int slot_) {
         if (pp) {
             t_pp += 1;
             t_vert += len;
@@ -214,16 +231,18 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 __syncwarp();
             }
         }
-        if ((HSH && !CNT_QUEUE) ? (pp || head) : (HX && head)) {
+        const bool to_ring = ((HSH && !CNT_QUEUE) && pp) || ((HX || SEG) && other);
+        if (to_ring) {
             asm volatile("st.shared.u64 [%0], %1;" ::"r"(qb + rc * 256u), "l"(Sx) : "memory");
-            const uint32_t tag = head ? (0x80000000u | ((uint32_t)hslot << 8) | len) : len;
+            if constexpr (SEG) asm volatile("st.shared.u64 [%0], %1;" ::"r"(bb + rc * 256u), "l"(Bx) : "memory");
+            const uint32_t tag = (pp ? (EK_PP << 29) : (kind << 29)) | ((uint32_t)slot_ << 8) | len;
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(lb + rc * 128u), "r"(tag) : "memory");
             rc++;
         }
-        if constexpr (HX) ring_heads |= __any_sync(kFull, head);
+        if constexpr (HX || SEG) ring_ev |= __any_sync(kFull, other);
     };
     // warp-uniform: every lane hashes the prime paths in its ring (the two finalizers, R20),
-    // then the warp writes the head segments
+    // then the warp writes the head segments (prime-path phase) or the items (segment phase)
     auto drain = [&]() {
         const uint32_t mx = __reduce_max_sync(kFull, rc);
         for (uint32_t j = 0; j < mx; j++) {
@@ -233,13 +252,15 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qb + j * 256u) : "memory");
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tag) : "r"(lb + j * 128u) : "memory");
             }
-            if (HSH && !CNT_QUEUE && j < rc && !(tag & 0x80000000u)) {
-                t_ha += mix64(z ^ (kSeedA + (uint64_t)tag));
-                t_hb += mix64(z ^ (kSeedB + (uint64_t)tag));
+            const uint32_t kind = tag >> 29, len = tag & 0xffu;
+            const int tslot = (int)((tag >> 8) & 0x1fffffu);
+            if (HSH && !CNT_QUEUE && j < rc && kind == EK_PP) {
+                t_ha += mix64(z ^ (kSeedA + (uint64_t)len));
+                t_hb += mix64(z ^ (kSeedB + (uint64_t)len));
             }
-            if constexpr (HX) {
-                if (ring_heads) {  // head segments: one HeadS per head node, in the warp's block of slots
-                    const bool h = j < rc && (tag & 0x80000000u);
+            if constexpr (HX && !SEG) {
+                if (ring_ev) {  // head segments: one HeadS per head node, in the warp's block of slots
+                    const bool h = j < rc && kind == EK_HEAD;
                     const uint32_t hb = __ballot_sync(kFull, h);
                     if (hb) {
                         const uint32_t need = __popc(hb);
@@ -257,17 +278,48 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                         if (h && q < A.head_cap) {
                             HeadS hr;
                             hr.S = z;
-                            hr.len = (int32_t)(tag & 0xffu);
-                            hr.x = (int32_t)((tag >> 8) & 0x7fffffu);
+                            hr.len = (int32_t)len;
+                            hr.x = tslot;
                             *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&hr);
                         }
                         hblk += need;
                     }
                 }
             }
+            if constexpr (SEG) {
+                if (ring_ev) {  // items: a tail segment, or a transit segment over an exit vertex's arcs
+                    const bool it = j < rc && (kind == EK_TAIL || kind == EK_TRANSIT);
+                    const uint32_t ib = __ballot_sync(kFull, it);
+                    if (ib) {
+                        const uint32_t need = __popc(ib);
+                        if (iblk + need > iblk_end) {  // a new block of 256 slots (the rest of the old one: holes)
+                            for (unsigned long long q = iblk + lane; q < iblk_end; q += 32)
+                                if (q < A.item_cap) A.items[q].ent = -1;
+                            unsigned long long b = 0;
+                            if (lane == 0) b = atomicAdd(A.cacc + 7, 256ull);
+                            b = __shfl_sync(kFull, b, 0);
+                            iblk = b;
+                            iblk_end = b + 256;
+                            if (b + 256 > A.item_cap && lane == 0) atomicOr(A.overflow, 8u);
+                        }
+                        const unsigned long long q = iblk + __popc(ib & ((1u << lane) - 1u));
+                        if (it && q < A.item_cap) {
+                            uint64_t Bx;
+                            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(Bx) : "r"(bb + j * 256u) : "memory");
+                            const int32_t ent = __ldg(&reinterpret_cast<const Slot<1> *>(G.slots)[L.vb + L.s].gid);
+                            ulonglong2 *d = reinterpret_cast<ulonglong2 *>(A.items + q);
+                            d[0] = make_ulonglong2(z, Bx);
+                            d[1] = make_ulonglong2(
+                                (unsigned long long)len | ((unsigned long long)(uint32_t)(kind == EK_TAIL ? -1 : tslot) << 32),
+                                (unsigned long long)(uint32_t)ent);
+                        }
+                        iblk += need;
+                    }
+                }
+            }
         }
         rc = 0;
-        ring_heads = false;
+        ring_ev = false;
     };
 
     while (true) {
@@ -305,10 +357,11 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
             }
         }
         // ---------------- waiting lanes: start the claimed unit once it is written
-        bool st_pp = false, st_head = false;
-        uint64_t st_S = 0;
+        bool st_pp = false, st_other = false;  // the unit root's event (a prime path, or see CntEv)
+        uint32_t st_kind = 0;
+        uint64_t st_S = 0, st_B = 0;
         uint32_t st_len = 0;
-        int st_hslot = 0;
+        int st_slot = 0;
         if (waiting) {
             if (rdy != 0u) {
                 waiting = false;
@@ -324,7 +377,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 L.l = L.r = depth;
                 L.vb = __ldg(G.scc_vbase + uscc);
                 const uint32_t *p4 = reinterpret_cast<const uint32_t *>(U->path);
-                uint64_t S0 = 0;
+                uint64_t S0 = 0, B0 = 0;
                 int u = 0;
 #pragma unroll 1
                 for (int q = 0; q * 4 <= depth; q++) {  // path bytes into the lane's column, S of the path
@@ -335,7 +388,9 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                         if (i <= depth) {
                             const int x = (int)((wv >> (8 * b)) & 0xffu);
                             sts_u8(pb + (uint32_t)i * 32u, x);
-                            S0 += mul64x32(tab.mix(L.vb + x), 2u * (uint32_t)i + 1u);
+                            const uint64_t mx = tab.mix(L.vb + x);
+                            S0 += mul64x32(mx, 2u * (uint32_t)i + 1u);
+                            B0 += mx;
                             u = x;
                         }
                     }
@@ -343,28 +398,41 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 L.s = (int)(__ldcg(p4) & 0xffu);
                 L.sbit = (T)1 << L.s;
                 L.ps = tab.pin(L.vb + L.s);
-                L.exm = HX ? (T)__ldg(G.scc_exm + uscc) : (T)0;
+                L.exm = (HX || SEG) ? (T)__ldg(G.scc_exm + uscc) : (T)0;
                 L.S = S0;
+                L.B = B0;
+                if constexpr (SEG) {
+                    const int32_t sg = __ldg(&reinterpret_cast<const Slot<1> *>(G.slots)[L.vb + L.s].gid);
+                    L.emit = sg >= G.shard_lo && sg < G.shard_hi;
+                }
                 steps = 0;
                 last_split = 0;
                 L.active = true;
                 if (kind == K_CLOSURE) {  // the closing arc of path[0..depth] back to s
-                    t_ext += 1;
-                    st_pp = true;
+                    t_ext += L.emit ? 1 : 0;
+                    st_pp = L.emit;
                     st_S = S0 + mul64x32(tab.mix(L.vb + L.s), 2u * (uint32_t)depth + 3u);
                     st_len = (uint32_t)depth + 2;
                     L.rem = 0;
                     L.done = true;
                 } else {  // K_NODE: the node's own event, then its subtree
-                    if (depth > 0) t_ext += 1;
+                    if (depth > 0 && L.emit) t_ext += 1;
                     const T ub = (T)1 << u;
-                    L.rem = tab.sin(L.vb + u) & (~L.M | L.sbit);
+                    const T su = tab.sin(L.vb + u);
+                    L.rem = su & (~L.M | L.sbit);
                     const bool ex = ((L.exm >> u) & 1) != 0;
-                    st_pp = L.rem == 0 && (L.ps & ~(L.M & ~ub)) == 0 && !ex;
-                    st_head = ex && (L.ps & ~L.M) == 0;
+                    if constexpr (SEG) {  // tail segment (succ(u) on the path) or transit segments (R8, R9)
+                        st_other = ex || (su & ~L.M) == 0;
+                        st_kind = ex ? EK_TRANSIT : EK_TAIL;
+                    } else {
+                        st_pp = L.rem == 0 && (L.ps & ~(L.M & ~ub)) == 0 && !ex;
+                        st_other = ex && (L.ps & ~L.M) == 0;
+                        st_kind = EK_HEAD;
+                    }
                     st_S = S0;
+                    st_B = B0;
                     st_len = (uint32_t)depth + 1;
-                    st_hslot = L.vb + u;
+                    st_slot = L.vb + u;
                     L.done = L.rem == 0;
                 }
             } else if (qdone) {
@@ -374,7 +442,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 rdy = ld_relaxed(A.ready + slot);
             }
         }
-        put_ev(st_pp, st_head, st_S, st_len, st_hslot);  // (the ring is empty here: drained after the passes)
+        put_ev(st_pp, st_other, st_kind, st_S, st_B, st_len, st_slot);  // (the ring is empty: drained after the passes)
         // ---------------- the claim issued last iteration
         if (claim_pending) {
             const unsigned long long base = __shfl_sync(kFull, claim_res, claim_leader);
@@ -432,15 +500,26 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 const int u = lds_u8(pb + (uint32_t)l * 32u);  // (pop) the vertex popped
                 const int v = take ? w : u;
                 const int vslot = L.vb + v;                   // (idle lanes: a valid slot of their last SCC)
-                const uint64_t prod = mul64x32(tab.mix(vslot), 2u * (uint32_t)(take ? l + 1 : l) + 1u);
+                const uint64_t mv = tab.mix(vslot);
+                const uint64_t prod = mul64x32(mv, 2u * (uint32_t)(take ? l + 1 : l) + 1u);
                 const T vbit = (T)1 << v;
                 const T sn = tab.sin(vslot);
                 const bool clo = w == L.s;
                 const T Mw = L.M | vbit;
                 const T cw = clo ? (T)0 : (sn & (~Mw | L.sbit));  // (take) the child's own untried children
                 bool ex = false;
-                if constexpr (HX) ex = ((L.exm >> v) & 1) != 0;
-                const bool pp = take && (clo || (cw == 0 && (L.ps & ~L.M) == 0 && !ex));
+                if constexpr (HX || SEG) ex = ((L.exm >> v) & 1) != 0;
+                bool pp, other;
+                uint32_t kind;
+                if constexpr (SEG) {  // cycles are prime paths; tail / transit segments become items
+                    pp = take && clo && L.emit;
+                    other = take && !clo && (ex || (sn & ~Mw) == 0);
+                    kind = ex ? EK_TRANSIT : EK_TAIL;
+                } else {
+                    pp = take && (clo || (cw == 0 && (L.ps & ~L.M) == 0 && !ex));
+                    other = HX && take && !clo && ex && (L.ps & ~Mw) == 0;  // a head segment
+                    kind = EK_HEAD;
+                }
                 const bool push = take && cw != 0;
                 const uint64_t Sw = L.S + prod;  // (take) the digest sum of path + w
                 T rem_pop = 0;
@@ -457,13 +536,14 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                     if constexpr (RS) sts_u32(rb + (uint32_t)l * 128u, (uint32_t)(rem & (rem - 1)));
                     sts_u8(pb + (uint32_t)(l + 1) * 32u, w);
                 }
-                ext32 += take ? 1u : 0u;
+                ext32 += (take && (!SEG || L.emit)) ? 1u : 0u;
                 L.M = (push || pop) ? (L.M ^ vbit) : L.M;
                 L.S = push ? Sw : (pop ? L.S - prod : L.S);
+                const uint64_t Bw = L.B + mv;
+                if constexpr (SEG) L.B = push ? Bw : (pop ? L.B - mv : L.B);
                 L.l = l + (push ? 1 : 0) - (pop ? 1 : 0);
                 L.rem = push ? cw : (pop ? rem_pop : (take ? (rem & (rem - 1)) : rem));
-                const bool head = HX && take && !clo && ex && (L.ps & ~Mw) == 0;
-                put_ev(pp, head, Sw, (uint32_t)l + 2, vslot);
+                put_ev(pp, other, kind, Sw, Bw, (uint32_t)l + 2, vslot);
             }
             drain();
         }
@@ -556,6 +636,8 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     // the rings were drained; the head block's unused slots, then the totals
     for (unsigned long long j = hblk + lane; j < hblk_end; j += 32)
         if (j < A.head_cap) A.heads[j].x = -1;
+    for (unsigned long long j = iblk + lane; j < iblk_end; j += 32)
+        if (j < A.item_cap) A.items[j].ent = -1;
     uint64_t v[7] = {t_pp, t_vert, t_ext, t_ha, t_hb, 0, t_cross};
     bool ovf = false;  // prime-path totals >= 2^62 (or a wrapped sum): LIMIT_EXCEEDED
 #pragma unroll

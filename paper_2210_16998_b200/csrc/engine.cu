@@ -114,7 +114,7 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_slot_mix, &d_vmix, &d_scc_exm, &cheads,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_v_slot, &d_slot_mix, &d_vmix, &d_scc_exm, &cheads, &citems, &citems2, &icnt,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan,
@@ -161,6 +161,7 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
     TPG_TRY(upload(P.d_scc_pair_base, H.scc_pair_base, s));
     TPG_TRY(upload(P.d_slot_eidx, H.slot_eidx, s));
     TPG_TRY(upload(P.d_comp, H.comp, s));
+    TPG_TRY(upload(P.d_v_slot, H.v_slot, s));
     {  // digest values mix64(v) per global vertex and per slot (R20)
         std::vector<uint64_t> vm(std::max(H.n, 1), 0), sm(std::max(H.n, 1), 0);
         for (int32_t v = 0; v < H.n; v++) vm[v] = host_mix64((uint64_t)(uint32_t)v);
@@ -199,6 +200,8 @@ static DevGraph dev_graph(PlanImpl &P, int32_t lo, int32_t hi) {
     G.slot_mix = P.d_slot_mix.as<uint64_t>();
     G.vmix = P.d_vmix.as<uint64_t>();
     G.scc_exm = P.d_scc_exm.as<uint64_t>();
+    G.v_slot = P.d_v_slot.as<int32_t>();
+    G.comp = P.d_comp.as<int32_t>();
     G.shard_lo = lo;
     G.shard_hi = hi;
     return G;
@@ -605,7 +608,7 @@ static void presplit_roots(PlanImpl &P, int32_t lo, int32_t hi, int64_t target, 
 // Launch of one DFS kernel variant (LEAN / table in shared memory / generic) in mode MODE.
 template <class T, int MODE>
 static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsArgs &A, cudaStream_t s,
-                               bool any_exit = true) {
+                               bool any_exit = true, bool seg = false) {
     constexpr int W = MT<T>::W;
     if constexpr (MODE != M_REC) {  // count modes: the straight-line count kernel (count.cuh)
         static_assert(W == 1, "count modes use one mask word");
@@ -614,9 +617,11 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         const int cgrid = grid / (lean ? kLeanBlocks : DfsCfg<W>::min_blocks) * CntCfg<CT>::min_blocks;
         const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
         const bool ts = ctab <= kSmemTabMax;
-        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>();
-        void (*k)(DfsArgs) = ts ? (any_exit ? cnt_kernel<CT, true, HSH, true> : cnt_kernel<CT, true, HSH, false>)
-                                : (any_exit ? cnt_kernel<CT, false, HSH, true> : cnt_kernel<CT, false, HSH, false>);
+        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg);
+        void (*k)(DfsArgs) =
+            seg ? (ts ? cnt_kernel<CT, true, HSH, true, true> : cnt_kernel<CT, false, HSH, true, true>)
+                : (ts ? (any_exit ? cnt_kernel<CT, true, HSH, true, false> : cnt_kernel<CT, true, HSH, false, false>)
+                      : (any_exit ? cnt_kernel<CT, false, HSH, true, false> : cnt_kernel<CT, false, HSH, false, false>));
         TPG_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cdyn));
         k<<<cgrid, CntCfg<CT>::threads, cdyn, s>>>(A);
         return TPGEN_OK;
@@ -648,7 +653,8 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
 template <class T>
 static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W> roots, int seg,
                               uint64_t qbase, cudaStream_t s, tpgen_stats &st, int64_t &launches, double &ms_dfs,
-                              uint64_t &tail_out, int mode = M_REC, unsigned long long *cacc_h = nullptr) {
+                              uint64_t &tail_out, int mode = M_REC, unsigned long long *cacc_h = nullptr,
+                              double *ms_last = nullptr) {
     constexpr int W = MT<T>::W;
     Timer t;
     const HostPlan &H = P.hp;
@@ -661,9 +667,13 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
                                                        P.q_hwm * 3 / 2), s));
     if (seg) TPG_CK(cudaMemcpyAsync(P.agg_bak.p, P.agg.p, agg_n * 8, cudaMemcpyDeviceToDevice, s));
     TPG_TRY(P.qctr.ensure(8 * 16 * 8, s));
-    if (mode != M_REC) {  // head records: the plan's high-water mark with headroom, at least 1 M slots
+    if (mode != M_REC && !seg) {  // head records: the plan's high-water mark with headroom, at least 1 M slots
         const uint64_t want = std::max<uint64_t>(1ull << 20, P.chead_hwm + P.chead_hwm / 4 + 256ull * 4096);
         if (P.cheads.cap < want * sizeof(HeadS)) TPG_TRY(P.cheads.ensure(want * sizeof(HeadS), s));
+    }
+    if (mode != M_REC && seg) {  // segment items: likewise
+        const uint64_t want = std::max<uint64_t>(1ull << 20, P.citem_hwm + P.citem_hwm / 4 + 256ull * 4096);
+        if (P.citems.cap < want * sizeof(ItemS)) TPG_TRY(P.citems.ensure(want * sizeof(ItemS), s));
     }
     unsigned long long *qc = P.qctr.as<unsigned long long>();
     // Test hooks: TPGEN_TEST_QCAP / TPGEN_TEST_POOL cap the queue slots / record chunks this
@@ -738,7 +748,9 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.n_slots = H.n;
         A.cacc = qc + 112;  // count modes: totals (zeroed with the counters above)
         A.heads = P.cheads.as<HeadS>();
-        A.head_cap = (mode != M_REC) ? std::min<uint64_t>(hlim, P.cheads.cap / sizeof(HeadS)) : 0;
+        A.head_cap = (mode != M_REC && !seg) ? std::min<uint64_t>(hlim, P.cheads.cap / sizeof(HeadS)) : 0;
+        A.items = P.citems.as<ItemS>();
+        A.item_cap = (mode != M_REC && seg) ? std::min<uint64_t>(hlim, P.citems.cap / sizeof(ItemS)) : 0;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
         // LEAN: 32-bit masks, prime-path phase, no arc leaves any SCC (no head / segment
         // events), the slot table staged in shared memory next to the rem stacks
@@ -747,8 +759,9 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
                           !getenv("TPGEN_NO_LEAN");
         const int grid = P.num_sms * (lean ? kLeanBlocks : DfsCfg<W>::min_blocks);
         if constexpr (W == 1) {
-            if (mode == M_CNT) TPG_TRY((launch_dfs<T, M_CNT>(lean, tab_bytes, grid, A, s, P.any_exit)));
-            else if (mode == M_CNT_NOHASH) TPG_TRY((launch_dfs<T, M_CNT_NOHASH>(lean, tab_bytes, grid, A, s, P.any_exit)));
+            if (mode == M_CNT) TPG_TRY((launch_dfs<T, M_CNT>(lean, tab_bytes, grid, A, s, P.any_exit, seg != 0)));
+            else if (mode == M_CNT_NOHASH)
+                TPG_TRY((launch_dfs<T, M_CNT_NOHASH>(lean, tab_bytes, grid, A, s, P.any_exit, seg != 0)));
             else TPG_TRY((launch_dfs<T, M_REC>(lean, tab_bytes, grid, A, s)));
         } else {
             if (mode != M_REC) {
@@ -768,14 +781,18 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         float ms = 0;
         cudaEventElapsedTime(&ms, t.a, t.b);
         ms_dfs += ms;
+        if (ms_last) *ms_last = ms;
         st.n_count_rounds++;
         const unsigned ovf = (unsigned)h[3];
-        if (ovf & 8u) {  // count modes: head records did not fit -- room for all of them, then retry
-            if (hlim < P.cheads.cap / sizeof(HeadS)) {
+        if (ovf & 8u) {  // count modes: head records / items did not fit -- room for all of them, then retry
+            DevBuf &buf = seg ? P.citems : P.cheads;
+            const size_t es = seg ? sizeof(ItemS) : sizeof(HeadS);
+            const uint64_t used = hq[112 + (seg ? 7 : 5)];
+            if (hlim < buf.cap / es) {
                 hlim *= 2;
             } else {
-                P.chead_hwm = std::max<uint64_t>(P.chead_hwm, hq[112 + 5]);
-                TPG_TRY(P.cheads.ensure((hq[112 + 5] + hq[112 + 5] / 4 + 256ull * 4096) * sizeof(HeadS), s));
+                (seg ? P.citem_hwm : P.chead_hwm) = std::max<uint64_t>(seg ? P.citem_hwm : P.chead_hwm, used);
+                TPG_TRY(buf.ensure((used + used / 4 + 256ull * 4096) * es, s));
             }
         }
         if (ovf & 14u) {  // record pool, queue or head buffer exhausted: undo and retry bigger
@@ -813,6 +830,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         if (mode != M_REC) {
             if (cacc_h) memcpy(cacc_h, hq + 112, 8 * sizeof(unsigned long long));
             P.chead_hwm = std::max<uint64_t>(P.chead_hwm, hq[112 + 5]);
+            P.citem_hwm = std::max<uint64_t>(P.citem_hwm, hq[112 + 7]);
         }
         P.chunk_used = std::min<uint64_t>(h[4], P.chunk_cap);  // (reserved-but-unused chunks may overshoot)
         P.chunk_hwm = std::max<uint64_t>(P.chunk_hwm, P.chunk_used);
@@ -982,12 +1000,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
 
     double ms_dfs = 0;
     uint64_t tail_seg = 0, tail = 0;
-    // COUNT_HASH calls with one mask word: the prime-path phase counts and digests in the
-    // DFS itself (count modes, dfs.cuh); only the segment phase writes records
+    // (COUNT_HASH calls whose SCCs fit one mask word take run_count; here the record path)
     const bool hash_only = (o.output_mode == TPGEN_OUT_COUNT_HASH);
-    const bool cnt = hash_only && W == 1 && !getenv("TPGEN_NO_CNT");
-    const int pp_mode = cnt ? (o.compute_digest ? M_CNT : M_CNT_NOHASH) : M_REC;
-    unsigned long long cacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // ---- segment phase (SCC entries) -> completion DP
     if (!seg_roots.empty()) {
         TPG_TRY(dfs_phase<T>(P, G, seg_roots, 1, 0, s, st, launches, ms_dfs, tail_seg));
@@ -1009,7 +1023,10 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     // ---- prime-path phase
     HT("before pp phase");
     {
-        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail, pp_mode, cacc);
+        double ms_pp = 0;
+        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail, M_REC,
+                                            nullptr, &ms_pp);
+        st.ms_dominant = ms_pp;
         P.presplit_active = false;
         if (r != TPGEN_OK) return r;
     }
@@ -1017,8 +1034,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
     }
-    // units whose records the writer replays: all of them, or (count modes) the segment phase's
-    const int64_t nu = cnt ? (int64_t)tail_seg : (int64_t)tail;
+    const int64_t nu = (int64_t)tail;
     st.n_units = (int64_t)tail;
 
     HT("after dfs phases");
@@ -1026,12 +1042,11 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     std::vector<int64_t> root_order;
     std::vector<int32_t> root_gid;
     const std::vector<int32_t> &pp_gid_r = *pp_gid_p;
-    const bool roots_cached = !cnt && presplit_ext_used && P.presplit_roots_n == (int64_t)pp_gid_r.size() &&
+    const bool roots_cached = presplit_ext_used && P.presplit_roots_n == (int64_t)pp_gid_r.size() &&
                               P.presplit_roots_tail == (int64_t)tail_seg;
-    static const std::vector<int32_t> kNoRoots;
     if (!roots_cached) {
         root_order.reserve(seg_roots.size() + pp_gid_r.size());
-        const std::vector<int32_t> &pp_gid = cnt ? kNoRoots : pp_gid_r;  // count modes: segment roots only
+        const std::vector<int32_t> &pp_gid = pp_gid_r;
         size_t a = 0, b = 0;
         while (a < seg_gid.size() || b < pp_gid.size()) {
             if (b >= pp_gid.size() || (a < seg_gid.size() && seg_gid[a] < pp_gid[b])) {
@@ -1048,7 +1063,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     // scratch: sub[C_NUM] | acc[C_NUM] | node ping | node pong
     TPG_TRY(P.offs.ensure(nu1 * (16 * C_NUM + 2 * sizeof(LinNode)) + 256, s));
     // root table (canonical root order + start gids); the pre-split roots' table is uploaded once per plan
-    DevBuf &rbuf = (presplit_ext_used && !cnt) ? P.presplit_roots : P.roots;
+    DevBuf &rbuf = presplit_ext_used ? P.presplit_roots : P.roots;
     if (!roots_cached) {
         TPG_TRY(rbuf.ensure(std::max<size_t>(root_order.size(), 1) * 12, s));
         if (n_roots) {
@@ -1056,7 +1071,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             TPG_CK(cudaMemcpyAsync(rbuf.as<char>() + n_roots * 8, root_gid.data(), n_roots * 4,
                                    cudaMemcpyHostToDevice, s));
         }
-        if (presplit_ext_used && !cnt) {
+        if (presplit_ext_used) {
             P.presplit_roots_n = n_roots;
             P.presplit_roots_tail = (int64_t)tail_seg;
         }
@@ -1117,54 +1132,25 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             launches++;
         }
         off = node[rounds & 1];
-        TPG_CK(cudaMemsetAsync(ctr + 14, 0, 8, s));
-        sum_kernel<<<lg, 256, 0, s>>>(P.qext.as<uint64_t>(), nu, ctr + 14);
-        launches++;
+        TPG_CK(cudaMemsetAsync(ctr + 14, 0, 16, s));
+        sum_kernel<<<lg, 256, 0, s>>>(P.qext.as<uint64_t>(), (int64_t)tail_seg, ctr + 15);  // segment phase
+        sum_kernel<<<lg, 256, 0, s>>>(P.qext.as<uint64_t>() + tail_seg, nu - (int64_t)tail_seg, ctr + 14);
+        launches += 2;
         cudaEventRecord(tlin.b, s);
         TPG_CK(cudaMemcpyAsync(tot, tot_d, C_NUM * 8, cudaMemcpyDeviceToHost, s));
-        TPG_CK(cudaMemcpyAsync(tot + C_NUM, ctr + 14, 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long ext2[2];
+        TPG_CK(cudaMemcpyAsync(ext2, ctr + 14, 16, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
+        tot[C_NUM] = ext2[0] + ext2[1];
+        st.ext_dominant = (int64_t)ext2[0];
         float lms = 0;
         cudaEventElapsedTime(&lms, tlin.a, tlin.b);
         st.ms_linearize = lms;
     }
     const uint64_t seg_heads = tot[C_HEADS];  // head records of the replayed units
-    if (cnt && cacc[5] > 0) {  // count modes: the cross prime paths of the head records (head_weight_s)
-        TPG_TRY(P.hcomp.ensure((size_t)cacc[5] * 8, s));
-        TPG_CK(cudaMemsetAsync(ctr + 20, 0, 24, s));
-        head_weight_s_kernel<<<grid_for((int64_t)cacc[5], 256, P.num_sms * 8), 256, 0, s>>>(
-            G, P.cheads.as<HeadS>(), (int64_t)cacc[5], P.hcomp.as<uint64_t>(), ctr + 20);
-        launches++;
-        unsigned long long hc[3];
-        TPG_CK(cudaMemcpyAsync(hc, ctr + 20, 24, cudaMemcpyDeviceToHost, s));
-        TPG_CK(cudaStreamSynchronize(s));
-        if (hc[2]) {
-            set_error("cross-SCC prime-path count exceeds 2^62");
-            return TPGEN_ERR_LIMIT_EXCEEDED;
-        }
-        cacc[6] = hc[0];
-        const uint64_t a = cacc[0] + hc[0], b = cacc[1] + hc[1];
-        if (a < cacc[0] || b < cacc[1] || a >= (1ull << 62) || b >= (1ull << 62)) {
-            set_error("prime-path count exceeds 2^62");
-            return TPGEN_ERR_LIMIT_EXCEEDED;
-        }
-        cacc[0] = a;
-        cacc[1] = b;
-    }
-    if (cnt) {  // add the count-mode phase's totals (saturating: >= 2^62 is LIMIT_EXCEEDED)
-        const uint64_t a = tot[C_PP] + cacc[0], b = tot[C_VERT] + cacc[1];
-        if (a < tot[C_PP] || b < tot[C_VERT] || a >= (1ull << 62) || b >= (1ull << 62)) {
-            set_error("prime-path count exceeds 2^62");
-            return TPGEN_ERR_LIMIT_EXCEEDED;
-        }
-        tot[C_PP] = a;
-        tot[C_VERT] = b;
-        tot[C_NUM] += cacc[2];
-        st.n_cross = (int64_t)cacc[6];
-    }
     const int64_t n_pp = (int64_t)tot[C_PP], n_vert = (int64_t)tot[C_VERT];
     st.n_extensions = (int64_t)(tot[C_NUM] + presplit_ext);
-    st.n_heads = cnt ? (int64_t)cacc[5] : (int64_t)tot[C_HEADS];
+    st.n_heads = (int64_t)tot[C_HEADS];
     st.n_segments = (int64_t)tot[C_ITEMS];
     if ((o.max_paths > 0 && n_pp > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
         set_error("result exceeds max_paths / max_extensions");
@@ -1197,7 +1183,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     if (!hash_only) TPG_TRY(out_alloc_pair(o, ow, (size_t)(n_pp + 1) * 8, (size_t)n_vert * 4, &d_off, &d_vert, s));
     unsigned long long *hacc = ctr + 16;  // digest accumulators (COUNT_HASH: filled by the writers)
     TPG_CK(cudaMemsetAsync(hacc, 0, 16, s));
-    const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = cnt ? (int64_t)cacc[5] : (int64_t)seg_heads;
+    const int64_t n_items = (int64_t)tot[C_ITEMS], n_heads = (int64_t)seg_heads;
     TPG_TRY(P.heads.ensure(std::max<int64_t>((int64_t)seg_heads, 1) * sizeof(HeadRec), s));
     TPG_TRY(P.head_pool.ensure(std::max<uint64_t>(tot[C_HEADV], 1) * 4, s));
     TPG_TRY(P.items.ensure(std::max<int64_t>(n_items, 1) * sizeof(ItemRec), s));
@@ -1235,11 +1221,9 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     cudaEventRecord(tst.a, s);
     if (n_heads > 0) {
         TPG_TRY(P.hcomp.ensure((size_t)n_heads * 8, s));
-        if (!cnt) {  // (count modes: the weights were computed with the totals)
-            head_weight_kernel<<<grid_for(n_heads, 256, 4096), 256, 0, s>>>(G, P.heads.as<HeadRec>(), n_heads,
-                                                                             P.hcomp.as<uint64_t>());
-            launches++;
-        }
+        head_weight_kernel<<<grid_for(n_heads, 256, 4096), 256, 0, s>>>(G, P.heads.as<HeadRec>(), n_heads,
+                                                                         P.hcomp.as<uint64_t>());
+        launches++;
         uint64_t *ha[1] = {P.hcomp.as<uint64_t>()};
         uint64_t ncomp = 0;
         TPG_TRY(scan_multi(P, ha, 1, n_heads, &ncomp, s, launches));
@@ -1277,11 +1261,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         SA.n_pp = (uint64_t)n_pp;
         SA.n_vert = (uint64_t)n_vert;
         if (ncomp > 0) {
-            if (cnt) {
-                stitch_hash_s_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(
-                    SA, P.cheads.as<HeadS>(), G, hacc);
-                launches++;
-            } else if (hash_only) {
+            if (hash_only) {
                 stitch_hash_kernel<<<grid_for((int64_t)ncomp, 256, P.num_sms * 8), 256, 0, s>>>(SA, hacc);
                 launches++;
             } else {
@@ -1324,8 +1304,8 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         unsigned long long hd[2];
         TPG_CK(cudaMemcpyAsync(hd, acc, 16, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
-        st.hash_lo = hd[0] + cacc[3];  // (count modes: + the DFS's own prime paths)
-        st.hash_hi = hd[1] + cacc[4];
+        st.hash_lo = hd[0];
+        st.hash_hi = hd[1];
     }
     TPG_CK(cudaStreamSynchronize(s));
     float ms = 0;
@@ -1345,6 +1325,275 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         ow_guard.release();
         TPG_TRY(finish_output(o, ow, n_pp, n_vert, (int64_t *)d_off, (int32_t *)d_vert, s, out));
     }
+    st.ms_total = now_ms() - t0;
+    if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
+// ------------------------------------------------------------ count modes
+// COUNT_HASH calls on graphs whose SCCs have <= 64 vertices: no record
+// streams at all.  (1) The segment phase runs cnt_kernel<SEG> over the SCC entry vertices:
+// their cycles are counted and hashed, their tail / transit segments become ItemS records
+// plus the completion-DP aggregates.  (2) Host completion DP (u64, overflow checked).
+// (3) The prime-path phase runs cnt_kernel over every other start vertex: counts, E_canon,
+// digests, HeadS records.  (4) head_weight_s: the cross prime paths' counts and vertices.
+// (5) With the digest: items grouped by entry, weighted and scanned; stitch_hash_s hashes
+// every cross prime path from S(h) and the items' (A, B).
+template <class T>
+static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    int64_t launches = 0;
+    const HostPlan &H = P.hp;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    int32_t lo = 0, hi = H.n;
+    shard_range(H, o.shard_rank, o.shard_count, lo, hi);
+    if (o.start_hi > o.start_lo) {
+        lo = std::max(0, o.start_lo);
+        hi = std::min(H.n, o.start_hi);
+    }
+    st.shard_lo = lo;
+    st.shard_hi = hi;
+    st.n_scc = H.n_scc;
+    st.n_scc_nontrivial = H.n_nontrivial;
+    st.max_scc = H.max_scc;
+    st.ms_plan = P.ms_plan;
+    P.overflow = false;
+    P.maxgen = 0;
+    const int mode = o.compute_digest ? M_CNT : M_CNT_NOHASH;
+    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;  // host stage marks, synchronised
+    auto HT = [&](const char *what) {
+        if (!hdbg) return;
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[tpgen count] %-28s %s\n", what, cudaGetErrorString(cudaGetLastError()));
+    };
+    Timer tall, tst;
+    cudaEventRecord(tall.a, s);
+    const DevGraph G = dev_graph(P, lo, hi);
+    // roots: one K_NODE unit per start vertex (segment phase: every SCC entry; prime-path phase: the
+    // range's other vertices)
+    std::vector<Unit<1>> seg_roots, pp_roots;
+    for (int32_t v = 0; v < H.n; v++) {
+        const int32_t slot = H.v_slot[v];
+        const bool entry = (H.slot_flags[slot] & F_ENTRY) != 0;
+        if (!entry && !(v >= lo && v < hi)) continue;
+        Unit<1> u;
+        memset(&u, 0, sizeof(u));
+        const int32_t c = H.comp[v];
+        const int loc = slot - H.scc_vbase[c];
+        u.M[0] = 1ull << loc;
+        u.scc = c;
+        u.e = -1;
+        u.kind = K_NODE;
+        u.path[0] = (uint8_t)loc;
+        (entry ? seg_roots : pp_roots).push_back(u);
+    }
+    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
+    TPG_TRY(P.ctr.ensure(32 * 8, s));
+    TPG_TRY(P.agg.ensure(agg_n * 8, s));
+    TPG_TRY(P.agg_bak.ensure(agg_n * 8, s));
+    TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();
+    // graphs with no arc leaving any SCC: the host pre-split trie tops (cached per plan and range)
+    RootSpan<1> pp_span(pp_roots);
+    uint64_t presplit_ext = 0;
+    if (std::is_same<T, uint32_t>::value && seg_roots.empty() && !P.any_exit && !getenv("TPGEN_NO_PRESPLIT")) {
+        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_dev.p)) {
+            const int64_t lanes = (int64_t)P.num_sms * CntCfg<uint32_t>::min_blocks * CntCfg<uint32_t>::threads;
+            std::vector<Unit<1>> units;
+            int64_t target = lanes;
+            if (const char *ev = getenv("TPGEN_PRESPLIT_TARGET")) target = atoll(ev);
+            presplit_roots<1>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext);
+            P.presplit_host.assign(reinterpret_cast<const uint8_t *>(units.data()),
+                                   reinterpret_cast<const uint8_t *>(units.data() + units.size()));
+            P.presplit_n = (int64_t)units.size();
+            P.presplit_roots_n = -1;
+            TPG_TRY(upload(P.presplit_dev, P.presplit_host, s));
+            P.presplit_lo = lo;
+            P.presplit_hi = hi;
+        }
+        pp_span = RootSpan<1>(reinterpret_cast<const Unit<1> *>(P.presplit_host.data()), (size_t)P.presplit_n);
+        presplit_ext = P.presplit_ext;
+        P.presplit_active = true;
+    }
+    double ms_dfs = 0;
+    uint64_t tail_seg = 0, tail = 0;
+    unsigned long long cseg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cpp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // (1) segment phase
+    if (!seg_roots.empty())
+        TPG_TRY(dfs_phase<T>(P, G, RootSpan<1>(seg_roots), 1, 0, s, st, launches, ms_dfs, tail_seg, mode, cseg));
+    HT("segment phase");
+    // (3) prime-path phase
+    {
+        double ms_pp = 0;
+        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail, mode, cpp, &ms_pp);
+        P.presplit_active = false;
+        if (r != TPGEN_OK) return r;
+        st.ms_dominant = ms_pp;
+        st.ext_dominant = (int64_t)cpp[2];
+    }
+    if (P.overflow) {
+        set_error("prime-path count exceeds 2^62");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    st.n_units = (int64_t)tail;
+    HT("prime-path phase");
+    // (2) completion DP from the items' aggregates
+    if (!seg_roots.empty()) {
+        const int64_t n_slots = (int64_t)cseg[7];
+        unsigned long long *agg = P.agg.as<unsigned long long>();
+        if (n_slots > 0) {
+            item_agg_s_kernel<<<grid_for(n_slots, 256, P.num_sms * 8), 256, 0, s>>>(
+                G, P.citems.as<ItemS>(), n_slots, agg, agg + H.n, agg + 2 * (int64_t)H.n,
+                agg + 2 * (int64_t)H.n + H.n_pairs);
+            launches++;
+        }
+        std::vector<uint64_t> aggh(agg_n);
+        TPG_CK(cudaMemcpyAsync(aggh.data(), P.agg.p, agg_n * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        std::vector<uint64_t> tail_cnt(aggh.begin(), aggh.begin() + H.n);
+        std::vector<uint64_t> tail_len(aggh.begin() + H.n, aggh.begin() + 2 * H.n);
+        std::vector<uint64_t> pair_cnt(aggh.begin() + 2 * H.n, aggh.begin() + 2 * H.n + H.n_pairs);
+        std::vector<uint64_t> pair_len(aggh.begin() + 2 * H.n + H.n_pairs, aggh.begin() + 2 * H.n + 2 * H.n_pairs);
+        std::vector<uint64_t> Wd, Vd;
+        if (!completion_dp(H, tail_cnt, tail_len, pair_cnt, pair_len, Wd, Vd)) {
+            set_error("cross-SCC prime-path count exceeds 2^62");
+            return TPGEN_ERR_LIMIT_EXCEEDED;
+        }
+        TPG_CK(cudaMemcpyAsync(P.d_Wc.p, Wd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+        TPG_CK(cudaMemcpyAsync(P.d_Wv.p, Vd.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+    }
+    // (4) cross prime paths of the head records
+    const int64_t n_heads = (int64_t)cpp[5];
+    uint64_t cross = 0, cross_v = 0;
+    if (n_heads > 0) {
+        TPG_TRY(P.hcomp.ensure((size_t)n_heads * 8, s));
+        TPG_CK(cudaMemsetAsync(ctr + 20, 0, 24, s));
+        head_weight_s_kernel<<<grid_for(n_heads, 256, P.num_sms * 8), 256, 0, s>>>(
+            G, P.cheads.as<HeadS>(), n_heads, P.hcomp.as<uint64_t>(), ctr + 20);
+        launches++;
+        unsigned long long hc[3];
+        TPG_CK(cudaMemcpyAsync(hc, ctr + 20, 24, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        if (hc[2]) {
+            set_error("cross-SCC prime-path count exceeds 2^62");
+            return TPGEN_ERR_LIMIT_EXCEEDED;
+        }
+        cross = hc[0];
+        cross_v = hc[1];
+    }
+    uint64_t n_pp = 0, n_vert = 0;
+    {
+        const uint64_t parts[3][2] = {{cseg[0], cseg[1]}, {cpp[0], cpp[1]}, {cross, cross_v}};
+        for (const auto &pr : parts) {
+            const uint64_t a = n_pp + pr[0], b = n_vert + pr[1];
+            if (a < n_pp || b < n_vert || a >= (1ull << 62) || b >= (1ull << 62)) {
+                set_error("prime-path count exceeds 2^62");
+                return TPGEN_ERR_LIMIT_EXCEEDED;
+            }
+            n_pp = a;
+            n_vert = b;
+        }
+    }
+    st.n_paths = (int64_t)n_pp;
+    st.total_vertices = (int64_t)n_vert;
+    st.n_cross = (int64_t)cross;
+    st.n_extensions = (int64_t)(cseg[2] + cpp[2] + presplit_ext);
+    st.n_heads = n_heads;
+    st.n_segments = (int64_t)cseg[7];
+    if ((o.max_paths > 0 && st.n_paths > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
+        set_error("result exceeds max_paths / max_extensions");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    // (5) digests of the cross prime paths
+    cudaEventRecord(tst.a, s);
+    uint64_t hd[2] = {cseg[3] + cpp[3], cseg[4] + cpp[4]};
+    if (o.compute_digest && n_heads > 0 && cross > 0) {
+        const int64_t n_slots = (int64_t)cseg[7];  // item slots written by the segment phase (holes: ent < 0)
+        const int32_t nv = std::max(H.n, 1);
+        TPG_TRY(P.icnt.ensure((size_t)nv * 8 * 3, s));
+        uint64_t *icnt = P.icnt.as<uint64_t>(), *istart = icnt + nv, *icur = icnt + 2 * (size_t)nv;
+        TPG_CK(cudaMemsetAsync(icnt, 0, (size_t)nv * 8, s));
+        item_count_s_kernel<<<grid_for(n_slots, 256, P.num_sms * 8), 256, 0, s>>>(P.citems.as<ItemS>(), n_slots,
+                                                                                 reinterpret_cast<unsigned long long *>(icnt));
+        TPG_CK(cudaMemcpyAsync(istart, icnt, (size_t)nv * 8, cudaMemcpyDeviceToDevice, s));
+        uint64_t n_items = 0;
+        uint64_t *sa[1] = {istart};
+        TPG_TRY(scan_multi(P, sa, 1, nv, &n_items, s, launches));
+        TPG_CK(cudaMemcpyAsync(icur, istart, (size_t)nv * 8, cudaMemcpyDeviceToDevice, s));
+        TPG_TRY(P.citems2.ensure(std::max<uint64_t>(n_items, 1) * sizeof(ItemS), s));
+        item_scatter_s_kernel<<<grid_for(n_slots, 256, P.num_sms * 8), 256, 0, s>>>(
+            P.citems.as<ItemS>(), n_slots, reinterpret_cast<unsigned long long *>(icur), P.citems2.as<ItemS>());
+        TPG_TRY(P.ibeg.ensure((size_t)nv * 8, s));
+        TPG_TRY(P.iend.ensure((size_t)nv * 8, s));
+        item_bounds_s_kernel<<<grid_for(nv, 256, 1024), 256, 0, s>>>(istart, icnt, nv, P.ibeg.as<int64_t>(),
+                                                                    P.iend.as<int64_t>());
+        TPG_TRY(P.icum.ensure((size_t)std::max<uint64_t>(n_items, 1) * 8, s));
+        TPG_TRY(P.ivcum.ensure((size_t)std::max<uint64_t>(n_items, 1) * 8, s));
+        item_weight_s_kernel<<<grid_for((int64_t)n_items, 256, P.num_sms * 8), 256, 0, s>>>(
+            G, P.citems2.as<ItemS>(), (int64_t)n_items, P.icum.as<uint64_t>(), P.ivcum.as<uint64_t>());
+        launches += 4;
+        uint64_t tot2[2];
+        uint64_t *ia[2] = {P.icum.as<uint64_t>(), P.ivcum.as<uint64_t>()};
+        TPG_TRY(scan_multi(P, ia, 2, (int64_t)n_items, tot2, s, launches));
+        uint64_t *ha[1] = {P.hcomp.as<uint64_t>()};
+        uint64_t ncomp = 0;
+        TPG_TRY(scan_multi(P, ha, 1, n_heads, &ncomp, s, launches));
+        HT("items grouped");
+        StitchSArgs SA;
+        SA.heads = P.cheads.as<HeadS>();
+        SA.n_heads = n_heads;
+        SA.comp_off = P.hcomp.as<uint64_t>();
+        SA.n_comp = ncomp;
+        SA.items = P.citems2.as<ItemS>();
+        SA.cum = P.icum.as<uint64_t>();
+        SA.ibeg = P.ibeg.as<int64_t>();
+        SA.iend = P.iend.as<int64_t>();
+        unsigned long long *hacc = ctr + 16;
+        TPG_CK(cudaMemsetAsync(hacc, 0, 16, s));
+        // small heads (<= kSmallHead completions): a thread per head; big ones: a thread per completion
+        TPG_TRY(P.sscratch.ensure((size_t)n_heads * 8 * 3 + 64, s));
+        uint64_t *big = P.sscratch.as<uint64_t>();
+        int64_t *bidx = reinterpret_cast<int64_t *>(big + n_heads);
+        uint64_t *bw = big + 2 * n_heads;
+        stitch_small_kernel<<<grid_for(n_heads, 256, P.num_sms * 8), 256, 0, s>>>(SA, G, big, hacc);
+        uint64_t n_big = 0;
+        uint64_t *ba[1] = {big};
+        TPG_TRY(scan_multi(P, ba, 1, n_heads, &n_big, s, launches));
+        launches++;
+        if (n_big > 0) {
+            stitch_big_list_kernel<<<grid_for(n_heads, 256, P.num_sms * 8), 256, 0, s>>>(SA, big, bidx, bw);
+            uint64_t n_big_comp = 0;
+            uint64_t *bwa[1] = {bw};
+            TPG_TRY(scan_multi(P, bwa, 1, (int64_t)n_big, &n_big_comp, s, launches));
+            stitch_big_kernel<<<grid_for((int64_t)n_big_comp, 256, P.num_sms * 8), 256, 0, s>>>(
+                SA, G, bidx, bw, (int64_t)n_big, n_big_comp, hacc);
+            launches += 2;
+        }
+        unsigned long long hh[2];
+        TPG_CK(cudaMemcpyAsync(hh, hacc, 16, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        hd[0] += hh[0];
+        hd[1] += hh[1];
+    }
+    cudaEventRecord(tst.b, s);
+    cudaEventRecord(tall.b, s);
+    TPG_CK(cudaGetLastError());
+    TPG_CK(cudaStreamSynchronize(s));
+    if (o.compute_digest) {
+        st.hash_lo = hd[0];
+        st.hash_hi = hd[1];
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tall.a, tall.b);
+    st.ms_device = ms;
+    cudaEventElapsedTime(&ms, tst.a, tst.b);
+    st.ms_stitch = ms;
+    st.ms_count = st.ms_device - st.ms_stitch;
+    st.ms_dfs_count = ms_dfs;
+    st.ms_dfs_write = ms_dfs;
+    st.gpu_launches = launches;
     st.ms_total = now_ms() - t0;
     if (stp) *stp = st;
     return TPGEN_OK;
@@ -1589,6 +1838,8 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     st.ms_count = ms;
     st.ms_dfs_count = ms;
     st.ms_dfs_write = ms;
+    st.ms_dominant = ms;  // (all level launches of the call)
+    st.ext_dominant = st.n_extensions;
     st.gpu_launches = launches;
     st.ms_total = now_ms() - t0;
     if (stp) *stp = st;
@@ -1600,6 +1851,11 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
         memset(out, 0, sizeof(*out));
         if (P.hp.max_scc <= 32) return run_frontier<uint32_t>(P, o, st);
         return run_frontier<uint64_t>(P, o, st);
+    }
+    if (o.output_mode == TPGEN_OUT_COUNT_HASH && P.hp.max_scc <= 64 && P.hp.n < (1 << 21) && !getenv("TPGEN_NO_CNT")) {
+        memset(out, 0, sizeof(*out));  // count modes
+        if (P.hp.max_scc <= 32) return run_count<uint32_t>(P, o, st);
+        return run_count<uint64_t>(P, o, st);
     }
     if (P.hp.max_scc <= 32) return run_pp<uint32_t>(P, o, out, st);
     switch (P.hp.W) {

@@ -32,9 +32,12 @@ struct PlanImpl {
     double ms_plan = 0;
     // device tables
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
-        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase, d_comp, d_slot_mix, d_vmix, d_scc_exm;
+        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase, d_comp, d_slot_mix, d_vmix, d_scc_exm, d_v_slot;
     DevBuf cheads;           // count modes: HeadS records of the prime-path phase
+    DevBuf citems, citems2;  // count modes: ItemS records of the segment phase (as written; grouped by entry)
+    DevBuf icnt;             // count modes: items per entry vertex, their scan, the scatter cursors
     uint64_t chead_hwm = 0;  // most head slots any count-mode call of this plan reserved
+    uint64_t citem_hwm = 0;  // most item slots any count-mode call of this plan reserved
     // DFS work queue (one slot per unit) and its per-unit results
     DevBuf qunits, qready, qcnt[kCnt], qext, qrfirst, qrcount, qchead, qgen, roots;
     DevBuf qparent, qnchild;  // donor / number of donated units, per unit

@@ -158,6 +158,8 @@ struct DevGraph {
     const uint64_t *slot_mix;  // per slot: mix64(global id), the vertex's digest value (R20)
     const uint64_t *vmix;      // per global vertex id: mix64(id)
     const uint64_t *scc_exm;   // per SCC (<= 64 vertices): local bits of its exit vertices (Def. 5)
+    const int32_t *v_slot;     // per global vertex id: its slot
+    const int32_t *comp;       // per global vertex id: its SCC
     int32_t shard_lo, shard_hi;
 };
 
@@ -169,6 +171,20 @@ struct TPG_ALIGN(16) HeadS {
     uint64_t S;
     int32_t len;
     int32_t x;
+};
+
+// Count-mode segment item (cnt_kernel's segment phase) of the entry vertex ent (global id):
+// a tail segment (x < 0), or a transit segment ending at the exit vertex of slot x, followed
+// by any of that vertex's out-of-SCC arcs (in arc order, W(y) completions each).  With the
+// R20 terms mix(v) * (2 pos + 1) the item's contribution to a path's digest sum at offset o
+// is A + 2 o B (A = its own sum from position 0, B = the sum of its mix(v)), so no vertex
+// list is kept.  ent < 0 marks an unused slot of a warp's block.
+struct TPG_ALIGN(16) ItemS {
+    uint64_t A, B;
+    int32_t len;
+    int32_t x;
+    int32_t ent;
+    int32_t pad;
 };
 
 struct DfsArgs {
@@ -209,6 +225,8 @@ struct DfsArgs {
     unsigned long long *cacc;
     HeadS *heads;
     unsigned long long head_cap;
+    ItemS *items;                 // count modes, segment phase: items go to items[0 .. item_cap)
+    unsigned long long item_cap;  //   (cacc[7] = item slots reserved)
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)

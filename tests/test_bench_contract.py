@@ -17,10 +17,23 @@ def test_reference_arm_json_line():
               "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["metric"] == "prime_paths_per_sec" and d["unit"] == "PP/s"
-    assert d["config"]["workload"].startswith("config3")
+    assert d["config"]["workload"].startswith("config5")
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
-    assert "all of config3" in d["cpu_baseline"]["sample"]  # each step is the whole workload
+    assert "config5 start vertices" in d["cpu_baseline"]["sample"]  # a fixed bounded sample per step
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert d["config"] == bench.bench_config(1)  # the GPU arm names the same config dict
+
+
+def test_config5_sample_is_one_interior_start_per_scc():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    g, starts = bench.config5_sample()
+    assert len(starts) == 16
+    assert all(b - a == 56 for a, b in zip(starts, starts[1:]))  # one per 56-vertex SCC
 
 
 def test_frontier_engine_needs_config3():

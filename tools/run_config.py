@@ -19,7 +19,7 @@ g = gen.make_config(a.config)
 plan = tp.Plan(g)
 for _ in range(a.reps):
     ps = plan.prime_paths(mode=a.mode, digest=a.digest)
-    print({k: ps.stats[k] for k in ("n_paths", "n_extensions", "ms_device", "ms_dfs_write", "ms_dfs_count",
-                                     "n_count_rounds", "n_units")})
+    print({k: ps.stats[k] for k in ("n_paths", "n_extensions", "ms_device", "ms_dfs_write", "ms_dominant",
+                                     "ext_dominant", "n_count_rounds", "n_units")})
     del ps
 torch.cuda.synchronize()
