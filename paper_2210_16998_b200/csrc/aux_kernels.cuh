@@ -617,32 +617,86 @@ __global__ void head_weight_s_kernel(DevGraph G, const HeadS *heads, int64_t n, 
 // Items of the count-mode segment phase (ItemS, written in no order by cnt_kernel<SEG>):
 // counted per entry vertex, scattered into per-entry groups (order inside a group is
 // irrelevant: every completion is hashed once), weighted and scanned like the record path's.
-// (warp-aggregated: the lanes of a warp holding items of the same entry -- usually all of
-// them: a warp's items come from one walk -- add their count with one atomic)
+// Grouping of the raw items by entry.  Each block takes chunks of kGroupChunk items and counts
+// them per entry in a small shared-memory table (the items of a chunk come from few walks, so
+// from few entries), then adds the table to the global counters: one atomic per entry per
+// chunk instead of one per item.  The scatter recounts the chunk, reserves each entry's range
+// with one atomic, and places every item at its entry's next position (shared atomics).
+// Entries that do not fit the table go straight to the global atomics.
+
+constexpr int kGroupChunk = 8192;  // items per block-chunk of the item passes (aggregates, grouping)
+constexpr int kGroupTab = 64;      // distinct keys a chunk counts in shared memory
+
+__device__ __forceinline__ int group_slot(int *keys, int32_t e) {
+    int h = (int)((uint32_t)e * 2654435761u >> 26) & (kGroupTab - 1);
+    for (int p = 0; p < kGroupTab; p++, h = (h + 1) & (kGroupTab - 1)) {
+        const int k = keys[h];
+        if (k == e) return h;
+        if (k == -1) {
+            const int old = atomicCAS(&keys[h], -1, e);
+            if (old == -1 || old == e) return h;
+        }
+    }
+    return -1;
+}
+
 __global__ void item_count_s_kernel(const ItemS *items, int64_t n, unsigned long long *cnt) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t n_up = (n + 31) & ~(int64_t)31;  // whole warps iterate together
-    const int lane = threadIdx.x & 31;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
-        const int32_t e = i < n ? items[i].ent : -1;
-        const unsigned grp = __match_any_sync(kFull, e);
-        if (e >= 0 && lane == __ffs(grp) - 1) atomicAdd(cnt + e, (unsigned long long)__popc(grp));
+    __shared__ int keys[kGroupTab];
+    __shared__ unsigned int cnts[kGroupTab];
+    for (int64_t c0 = (int64_t)blockIdx.x * kGroupChunk; c0 < n; c0 += (int64_t)gridDim.x * kGroupChunk) {
+        if (threadIdx.x < kGroupTab) {
+            keys[threadIdx.x] = -1;
+            cnts[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        const int64_t c1 = min(n, c0 + kGroupChunk);
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const int32_t e = items[i].ent;
+            if (e < 0) continue;
+            const int h = group_slot(keys, e);
+            if (h >= 0) atomicAdd(&cnts[h], 1u);
+            else atomicAdd(cnt + e, 1ull);
+        }
+        __syncthreads();
+        if (threadIdx.x < kGroupTab && keys[threadIdx.x] >= 0 && cnts[threadIdx.x])
+            atomicAdd(cnt + keys[threadIdx.x], (unsigned long long)cnts[threadIdx.x]);
+        __syncthreads();
     }
 }
 __global__ void item_scatter_s_kernel(const ItemS *items, int64_t n, unsigned long long *cursor, ItemS *out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t n_up = (n + 31) & ~(int64_t)31;
-    const int lane = threadIdx.x & 31;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
-        ItemS it;
-        it.ent = -1;
-        if (i < n) it = items[i];
-        const unsigned grp = __match_any_sync(kFull, it.ent);
-        const int leader = __ffs(grp) - 1;
-        unsigned long long base = 0;
-        if (it.ent >= 0 && lane == leader) base = atomicAdd(cursor + it.ent, (unsigned long long)__popc(grp));
-        base = __shfl_sync(kFull, base, leader);
-        if (it.ent >= 0) out[base + __popc(grp & ((1u << lane) - 1u))] = it;
+    __shared__ int keys[kGroupTab];
+    __shared__ unsigned int cnts[kGroupTab];
+    __shared__ unsigned long long base[kGroupTab];
+    for (int64_t c0 = (int64_t)blockIdx.x * kGroupChunk; c0 < n; c0 += (int64_t)gridDim.x * kGroupChunk) {
+        if (threadIdx.x < kGroupTab) {
+            keys[threadIdx.x] = -1;
+            cnts[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        const int64_t c1 = min(n, c0 + kGroupChunk);
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const int32_t e = items[i].ent;
+            if (e < 0) continue;
+            const int h = group_slot(keys, e);
+            if (h >= 0) atomicAdd(&cnts[h], 1u);
+            else out[atomicAdd(cursor + e, 1ull)] = items[i];  // not in the table: placed right away
+        }
+        __syncthreads();
+        if (threadIdx.x < kGroupTab) {
+            if (keys[threadIdx.x] >= 0 && cnts[threadIdx.x])
+                base[threadIdx.x] = atomicAdd(cursor + keys[threadIdx.x], (unsigned long long)cnts[threadIdx.x]);
+            cnts[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const ItemS it = items[i];
+            if (it.ent < 0) continue;
+            int h = (int)((uint32_t)it.ent * 2654435761u >> 26) & (kGroupTab - 1);
+            int p = 0;
+            for (; p < kGroupTab && keys[h] != it.ent; p++) h = (h + 1) & (kGroupTab - 1);
+            if (p < kGroupTab) out[base[h] + atomicAdd(&cnts[h], 1u)] = it;
+        }
+        __syncthreads();
     }
 }
 // per entry (global id): first and end item of its group, from the exclusive scan of the counts
@@ -655,41 +709,71 @@ __global__ void item_bounds_s_kernel(const uint64_t *start, const uint64_t *cnt,
 }
 // Completion-DP aggregates from the raw items (before the DP): per entry (slot) the number
 // and total length of its tail segments, per (entry, out-arc) pair those of its transit
-// segments (Def. 6, R9).  Warp-aggregated: one atomic per distinct key of a warp.
-__global__ void item_agg_s_kernel(DevGraph G, const ItemS *items, int64_t n, unsigned long long *tail_cnt,
-                                  unsigned long long *tail_len, unsigned long long *pair_cnt,
-                                  unsigned long long *pair_len) {
+// segments (Def. 6, R9).  Keys: slot for tails, n_slots + pair index for transits; counted per
+// chunk in a shared-memory table (see item_count_s_kernel), one atomic per key and chunk.
+__global__ void item_agg_s_kernel(DevGraph G, const ItemS *items, int64_t n, int32_t n_slots,
+                                  unsigned long long *tail_cnt, unsigned long long *tail_len,
+                                  unsigned long long *pair_cnt, unsigned long long *pair_len) {
+    __shared__ unsigned long long keys[kGroupTab];
+    __shared__ unsigned int cnts[kGroupTab];
+    __shared__ unsigned long long lens[kGroupTab];
     const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t n_up = (n + 31) & ~(int64_t)31;
-    const int lane = threadIdx.x & 31;
-    auto add = [&](long long key, uint32_t len, unsigned long long *c, unsigned long long *l) {
-        const unsigned grp = __match_any_sync(kFull, key);
-        const unsigned sl = __reduce_add_sync(grp, key >= 0 ? len : 0u);
-        if (key >= 0 && lane == __ffs(grp) - 1) {
-            atomicAdd(c + key, (unsigned long long)__popc(grp));
-            atomicAdd(l + key, (unsigned long long)sl);
+    const unsigned long long kNone = ~0ull;
+    auto add = [&](unsigned long long key, uint32_t len) {
+        int h = (int)((uint32_t)(key * 0x9E3779B97F4A7C15ull >> 40)) & (kGroupTab - 1);
+        for (int p = 0; p < kGroupTab; p++, h = (h + 1) & (kGroupTab - 1)) {
+            unsigned long long k = keys[h];
+            if (k == kNone) k = atomicCAS(&keys[h], kNone, key);
+            if (k == kNone || k == key) {
+                atomicAdd(&cnts[h], 1u);
+                atomicAdd(&lens[h], (unsigned long long)len);
+                return;
+            }
+        }
+        if (key < (unsigned long long)n_slots) {  // the table is full: straight to the global counters
+            atomicAdd(tail_cnt + key, 1ull);
+            atomicAdd(tail_len + key, (unsigned long long)len);
+        } else {
+            atomicAdd(pair_cnt + (key - n_slots), 1ull);
+            atomicAdd(pair_len + (key - n_slots), (unsigned long long)len);
         }
     };
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
-        ItemS it;
-        it.ent = -1;
-        if (i < n) it = items[i];
-        const bool ok = it.ent >= 0;
-        const int32_t es = ok ? __ldg(G.v_slot + it.ent) : 0;
-        add((ok && it.x < 0) ? (long long)es : -1ll, (uint32_t)it.len, tail_cnt, tail_len);
-        int off = 0, cnt = 0;
-        long long pbase = 0;
-        if (ok && it.x >= 0) {
-            const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[it.x].gid));
-            off = m.y;
-            cnt = m.z;
-            const int32_t c = __ldg(G.comp + it.ent);
-            pbase = __ldg(G.scc_pair_base + c) + (long long)__ldg(G.slot_eidx + es) * __ldg(G.scc_nout + c) -
-                    __ldg(G.scc_out_base + c);
+    for (int64_t c0 = (int64_t)blockIdx.x * kGroupChunk; c0 < n; c0 += (int64_t)gridDim.x * kGroupChunk) {
+        if (threadIdx.x < kGroupTab) {
+            keys[threadIdx.x] = kNone;
+            cnts[threadIdx.x] = 0;
+            lens[threadIdx.x] = 0;
         }
-        const int mx = (int)__reduce_max_sync(kFull, (unsigned)cnt);
-        for (int a = 0; a < mx; a++) add(a < cnt ? pbase + off + a : -1ll, (uint32_t)it.len, pair_cnt, pair_len);
+        __syncthreads();
+        const int64_t c1 = min(n, c0 + kGroupChunk);
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const ItemS it = items[i];
+            if (it.ent < 0) continue;
+            const int32_t es = __ldg(G.v_slot + it.ent);
+            if (it.x < 0) {
+                add((unsigned long long)es, (uint32_t)it.len);
+            } else {
+                const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[it.x].gid));
+                const int32_t c = __ldg(G.comp + it.ent);
+                const long long pbase = __ldg(G.scc_pair_base + c) +
+                                        (long long)__ldg(G.slot_eidx + es) * __ldg(G.scc_nout + c) -
+                                        __ldg(G.scc_out_base + c);
+                for (int a = 0; a < m.z; a++)
+                    add((unsigned long long)(n_slots + pbase + m.y + a), (uint32_t)it.len);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < kGroupTab && keys[threadIdx.x] != kNone) {
+            const unsigned long long key = keys[threadIdx.x];
+            if (key < (unsigned long long)n_slots) {
+                atomicAdd(tail_cnt + key, (unsigned long long)cnts[threadIdx.x]);
+                atomicAdd(tail_len + key, lens[threadIdx.x]);
+            } else {
+                atomicAdd(pair_cnt + (key - n_slots), (unsigned long long)cnts[threadIdx.x]);
+                atomicAdd(pair_len + (key - n_slots), lens[threadIdx.x]);
+            }
+        }
+        __syncthreads();
     }
 }
 

@@ -1445,7 +1445,7 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
         unsigned long long *agg = P.agg.as<unsigned long long>();
         if (n_slots > 0) {
             item_agg_s_kernel<<<grid_for(n_slots, 256, P.num_sms * 8), 256, 0, s>>>(
-                G, P.citems.as<ItemS>(), n_slots, agg, agg + H.n, agg + 2 * (int64_t)H.n,
+                G, P.citems.as<ItemS>(), n_slots, H.n, agg, agg + H.n, agg + 2 * (int64_t)H.n,
                 agg + 2 * (int64_t)H.n + H.n_pairs);
             launches++;
         }
