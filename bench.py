@@ -271,6 +271,19 @@ def cpu_baseline_leg():
     return out
 
 
+def rank_reduce(dist, world: int, sums, maxes, device):
+    """The job's totals: per-rank counts summed, per-rank times maxed (the slowest rank defines
+    the job time).  One all_reduce each (NCCL on the GPU, gloo in the CPU tests)."""
+    import torch
+
+    s = torch.tensor([float(x) for x in sums], dtype=torch.float64, device=device)
+    m = torch.tensor([float(x) for x in maxes], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+    return s.tolist(), m.tolist()
+
+
 def timed_steps(plan, kw, steps, warmup, stream, flush):
     """W untimed calls, then K calls bracketed by CUDA events on the call's stream, L2 flushed
     (untimed) before each.  Returns (per-step ms, per-step stats)."""
@@ -475,15 +488,9 @@ def main():
                                                   else "output copied into pinned host memory")}
 
     # ---------------- reduce over ranks: counts summed, times maxed (the slowest rank defines the job)
-    vals = torch.tensor([float(n_pp) * args.steps, float(ext) * args.steps, ms_total,
-                         e2e["ms_per_step"] if e2e else 0.0, float(n_pp)], dtype=torch.float64, device=dev)
-    if world > 1:
-        sums = vals[[0, 1, 4]].clone()
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        mx = vals[2:4].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        vals = torch.stack([sums[0], sums[1], mx[0], mx[1], sums[2]])
-    tot_pp, tot_ext, ms_max, e2e_max, pp_per_step = vals.tolist()
+    (tot_pp, tot_ext, pp_per_step), (ms_max, e2e_max) = rank_reduce(
+        dist, world, [float(n_pp) * args.steps, float(ext) * args.steps, float(n_pp)],
+        [ms_total, e2e["ms_per_step"] if e2e else 0.0], dev)
 
     if rank == 0:
         value = tot_pp / (ms_max * 1e-3)

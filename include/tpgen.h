@@ -184,6 +184,32 @@ tpgen_status tpgen_test_paths(const int64_t *csr_offsets, const int32_t *csr_tar
 tpgen_status tpgen_components(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
                               int32_t *comp, int32_t *flags, int32_t *n_scc);
 
+/*
+ * Start-vertex shard of a graph (host only): [*lo, *hi) of shard `rank` of `count`, the planner's
+ * contiguous ranges balanced by its per-start cost estimates (what tpgen_options.shard_rank /
+ * shard_count select).  Same validation and errors as tpgen_components.
+ */
+tpgen_status tpgen_shard_range(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                               int32_t rank, int32_t count, int32_t *lo, int32_t *hi);
+
+/* Structure metrics of a CFG (Table 1; host only). */
+typedef struct {
+    int64_t nodes, edges;      /* V, E */
+    int64_t sccs;              /* nontrivial SCCs (more than one vertex, or a self-loop) */
+    int64_t scc_nodes;         /* vertices in nontrivial SCCs */
+    int64_t scc_edges;         /* arcs with both ends in the same nontrivial SCC */
+    int64_t weak_components;   /* P: weakly connected components */
+    int64_t cc;                /* cyclomatic complexity E - V + 2P */
+    uint64_t npath;            /* Npath: start -> end paths that use every arc at most once (
+                                  Npath(end) = 1, Npath(v) = sum over arcs (v,w) of Npath(w) in G minus the arc) */
+    int32_t npath_status;      /* 0: exact; 1: >= 2^62 (npath saturated at 2^62); 2: not computed -- the graph
+                                  has cycles and the arc-simple walk search exceeded its budget (10^8 steps) */
+    int32_t pad;
+} tpgen_metrics;
+
+tpgen_status tpgen_metrics_compute(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                                   int32_t start, int32_t end, tpgen_metrics *out);
+
 /* Stream-ordered release; safe on a zeroed struct. */
 void tpgen_paths_free(tpgen_paths *p);
 

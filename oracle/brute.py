@@ -67,3 +67,19 @@ def lexmin_shortest_walk(succ, a: int, b: int):
                 nxt.append(w + (x,))
         frontier = nxt
     return None
+
+
+def npath(n: int, succ: Sequence[Sequence[int]], start: int, end: int) -> int:
+    """Npath written out: Npath(end, G) = 1 and
+    Npath(v, G) = sum over arcs (v, w) of Npath(w, G - (v, w)) -- the number of start -> end
+    walks that use every arc at most once, by plain recursion on the arc set.  Tiny graphs only."""
+    def rec(v: int, removed: frozenset) -> int:
+        if v == end:
+            return 1
+        total = 0
+        for w in succ[v]:
+            if (v, w) not in removed:
+                total += rec(w, removed | {(v, w)})
+        return total
+
+    return rec(start, frozenset())

@@ -16,7 +16,8 @@ import numpy as np
 
 from . import _abi
 
-__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "library", "version"]
+__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "metrics", "shard_range",
+           "library", "version"]
 
 
 class TpgenError(RuntimeError):
@@ -291,31 +292,37 @@ def components(graph):
     return comp[:n], flags[:n], int(nscc.value)
 
 
-def metrics(graph) -> Dict[str, int]:
-    """Structure metrics of Table 1: Nodes, Edges, SCCs (nontrivial),
-    SccNodes, SccEdges and the cyclomatic complexity CC = E - V + 2P (P = number
-    of weakly connected components).  Host code over tpgen_components."""
+def shard_range(graph, rank: int, count: int) -> Tuple[int, int]:
+    """Start-vertex range [lo, hi) of shard ``rank`` of ``count`` (``tpgen_shard_range``, host):
+    the planner's contiguous, cost-balanced split that ``shard=(rank, count)`` selects."""
+    lib = library()
     so, st, n = _csr(graph)
-    comp, flags, _ = components(graph)
-    m = int(so[-1]) if n else 0
-    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(so)) if n else np.zeros(0, dtype=np.int64)
-    dst = np.asarray(st[:m], dtype=np.int64)
-    nontriv = (flags & 4) != 0
-    # weakly connected components by label propagation over the arcs (min label, to a fixpoint)
-    lab = np.arange(n, dtype=np.int64)
-    while m:
-        lo = np.minimum(lab[src], lab[dst])
-        new = lab.copy()
-        np.minimum.at(new, src, lo)
-        np.minimum.at(new, dst, lo)
-        new = new[new]
-        if np.array_equal(new, lab):
-            break
-        lab = new
-    parts = int(np.unique(lab).size) if n else 0
-    in_scc = (comp[src] == comp[dst]) & nontriv[src] if m else np.zeros(0, dtype=bool)
-    return {"nodes": n, "edges": m, "sccs": int(np.unique(comp[nontriv]).size) if n else 0,
-            "scc_nodes": int(nontriv.sum()), "scc_edges": int(in_scc.sum()), "cc": m - n + 2 * parts}
+    lo, hi = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.tpgen_shard_range(_p64(so), _p32(st), n, rank, count, ctypes.byref(lo), ctypes.byref(hi)))
+    return int(lo.value), int(hi.value)
+
+
+NPATH_STATUS = {0: "exact", 1: "saturated at 2^62", 2: "not computed (cyclic, search budget exceeded)"}
+
+
+def metrics(graph, start: Optional[int] = None, end: Optional[int] = None) -> Dict[str, Any]:
+    """Structure metrics of Table 1 from ``tpgen_metrics_compute`` (host
+    C++): Nodes, Edges, SCCs (nontrivial), SccNodes, SccEdges, weakly connected components P,
+    CC = E - V + 2P and Npath = start -> end walks using every arc at most once
+    (P:592-601).  ``start`` / ``end`` default to the graph's entry / exit."""
+    lib = library()
+    so, st, n = _csr(graph)
+    start = getattr(graph, "entry", 0) if start is None else start
+    end = getattr(graph, "exit", n - 1) if end is None else end
+    if n and (start is None or start < 0):
+        start = 0
+    if n and (end is None or end < 0):
+        end = n - 1
+    m = _abi.Metrics()
+    _check(lib.tpgen_metrics_compute(_p64(so), _p32(st), n, int(start or 0), int(end or 0), ctypes.byref(m)))
+    return {"nodes": m.nodes, "edges": m.edges, "sccs": m.sccs, "scc_nodes": m.scc_nodes,
+            "scc_edges": m.scc_edges, "weak_components": m.weak_components, "cc": m.cc, "npath": int(m.npath),
+            "npath_status": NPATH_STATUS[m.npath_status]}
 
 
 class Plan:

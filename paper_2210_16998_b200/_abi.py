@@ -40,6 +40,12 @@ class Options(Structure):
                 ("engine", c_int32), ("no_plan_cache", c_int32)]
 
 
+class Metrics(Structure):
+    _fields_ = [("nodes", c_int64), ("edges", c_int64), ("sccs", c_int64), ("scc_nodes", c_int64),
+                ("scc_edges", c_int64), ("weak_components", c_int64), ("cc", c_int64), ("npath", c_uint64),
+                ("npath_status", c_int32), ("pad", c_int32)]
+
+
 class Stats(Structure):
     _fields_ = [("n_paths", c_int64), ("total_vertices", c_int64), ("n_extensions", c_int64),
                 ("n_cross", c_int64), ("n_units", c_int64), ("n_heads", c_int64), ("n_segments", c_int64),
@@ -68,6 +74,10 @@ SYMBOLS = {
     "tpgen_paths_free": (None, [POINTER(Paths)]),
     "tpgen_components": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, POINTER(c_int32), POINTER(c_int32),
                                  POINTER(c_int32)]),
+    "tpgen_shard_range": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32, POINTER(c_int32),
+                                  POINTER(c_int32)]),
+    "tpgen_metrics_compute": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32,
+                                      POINTER(Metrics)]),
     "tpgen_plan_create": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, POINTER(Options),
                                   POINTER(c_void_p)]),
     "tpgen_plan_prime_paths": (c_int, [c_void_p, POINTER(Options), POINTER(Paths), POINTER(Stats)]),

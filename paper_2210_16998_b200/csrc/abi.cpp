@@ -299,6 +299,41 @@ tpgen_status tpgen_test_paths(const int64_t *so, const int32_t *st, int32_t n, c
 
 void tpgen_paths_free(tpgen_paths *p) { tpg::free_paths(p); }
 
+tpgen_status tpgen_shard_range(const int64_t *so, const int32_t *st, int32_t n, int32_t rank, int32_t count,
+                               int32_t *lo, int32_t *hi) {
+    if (n < 0 || !lo || !hi || count < 1 || rank < 0 || rank >= count) {
+        tpg::set_error("bad shard spec, NULL output pointer or n < 0");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    tpg::HostPlan P;
+    std::string msg;
+    tpgen_status s = tpg::build_plan(so, st, n, P, msg, true);  // (the full plan: its cost estimates)
+    if (s != TPGEN_OK) {
+        tpg::set_error(msg);
+        return s;
+    }
+    tpg::shard_range(P, rank, count, *lo, *hi);
+    return TPGEN_OK;
+}
+
+tpgen_status tpgen_metrics_compute(const int64_t *so, const int32_t *st, int32_t n, int32_t start, int32_t end,
+                                   tpgen_metrics *m) {
+    if (n < 0 || !m || (n > 0 && (start < 0 || start >= n || end < 0 || end >= n))) {
+        tpg::set_error("NULL output, n < 0, or start / end out of range");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    memset(m, 0, sizeof(*m));
+    tpg::HostPlan P;
+    std::string msg;
+    tpgen_status s = tpg::build_plan(so, st, n, P, msg, false);
+    if (s != TPGEN_OK) {
+        tpg::set_error(msg);
+        return s;
+    }
+    tpg::structure_metrics(P, start, end, *m);
+    return TPGEN_OK;
+}
+
 tpgen_status tpgen_components(const int64_t *so, const int32_t *st, int32_t n, int32_t *comp, int32_t *flags,
                               int32_t *n_scc) {
     if (n < 0 || (n > 0 && (!comp || !flags)) || !n_scc) {

@@ -101,6 +101,9 @@ void build_tp_tables(const HostPlan &plan, int32_t entry, int32_t exit, TpTables
 bool greedy_cover(const HostPlan &H, const TpTables &T, int32_t entry, int32_t exit, const int64_t *off,
                   const int32_t *vert, int64_t n, std::vector<int64_t> &tp_off, std::vector<int32_t> &tp_vert);
 
+// Table-1 structure metrics (planner.cpp): counts, CC = E - V + 2P, Npath.
+void structure_metrics(const HostPlan &plan, int32_t start, int32_t end, tpgen_metrics &m);
+
 void set_error(const std::string &msg);
 
 }  // namespace tpg

@@ -369,3 +369,118 @@ void build_tp_tables(const HostPlan &P, int32_t entry, int32_t exit, TpTables &T
 }
 
 }  // namespace tpg
+
+namespace tpg {
+
+// Table 1: V, E, the nontrivial SCCs and the arcs inside them, weakly connected
+// components P (union-find), CC = E - V + 2P, and Npath: the number of
+// start -> end walks that use every arc at most once, Npath(end) = 1.  On an acyclic graph that is
+// the number of start -> end paths (a DP in reverse topological order, saturating at 2^62); with
+// cycles, a depth-first search over arc-simple walks (an arc-used bitmap), within a step budget.
+void structure_metrics(const HostPlan &P, int32_t start, int32_t end, tpgen_metrics &m) {
+    const int32_t n = P.n;
+    m.nodes = n;
+    m.edges = P.m;
+    std::vector<int32_t> size(std::max(P.n_scc, 1), 0);
+    std::vector<char> loop(std::max(P.n_scc, 1), 0);
+    for (int32_t v = 0; v < n; v++) {
+        size[P.comp[v]]++;
+        for (int64_t e = P.so[v]; e < P.so[v + 1]; e++)
+            if (P.st[e] == v) loop[P.comp[v]] = 1;
+    }
+    bool cyclic = false;
+    for (int32_t c = 0; c < P.n_scc; c++)
+        if (size[c] > 1 || loop[c]) {
+            m.sccs++;
+            m.scc_nodes += size[c];
+            cyclic = true;
+        }
+    for (int32_t v = 0; v < n; v++)
+        for (int64_t e = P.so[v]; e < P.so[v + 1]; e++)
+            if (P.comp[P.st[e]] == P.comp[v] && (size[P.comp[v]] > 1 || loop[P.comp[v]])) m.scc_edges++;
+    std::vector<int32_t> par(n);
+    for (int32_t v = 0; v < n; v++) par[v] = v;
+    auto find = [&](int32_t x) {
+        while (par[x] != x) x = par[x] = par[par[x]];
+        return x;
+    };
+    for (int32_t v = 0; v < n; v++)
+        for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) {
+            const int32_t a = find(v), b = find(P.st[e]);
+            if (a != b) par[a] = b;
+        }
+    for (int32_t v = 0; v < n; v++) m.weak_components += (find(v) == v);
+    m.cc = m.edges - m.nodes + 2 * m.weak_components;
+    if (n == 0) return;
+    if (start == end) {  // Npath(end) = 1
+        m.npath = 1;
+        return;
+    }
+    const uint64_t cap = 1ull << 62;
+    if (!cyclic) {  // SCC ids are reverse topological: successors have smaller ids
+        std::vector<int32_t> order(n);
+        for (int32_t v = 0; v < n; v++) order[v] = v;
+        std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return P.comp[a] < P.comp[b]; });
+        std::vector<uint64_t> np(n, 0);
+        for (int32_t v : order) {
+            if (v == end) {
+                np[v] = 1;
+                continue;
+            }
+            uint64_t t = 0;
+            for (int64_t e = P.so[v]; e < P.so[v + 1]; e++) {
+                t += np[P.st[e]];
+                if (t >= cap) {
+                    t = cap;
+                    m.npath_status = 1;
+                }
+            }
+            np[v] = t;
+        }
+        m.npath = np[start];
+        return;
+    }
+    // arc-simple walks from start (iterative DFS over (vertex, next arc) frames)
+    std::vector<char> used((size_t)std::max<int64_t>(P.m, 1), 0);
+    std::vector<std::pair<int32_t, int64_t>> stack;
+    std::vector<int64_t> via;  // arc taken into each frame
+    uint64_t count = 0, steps = 0;
+    const uint64_t budget = 100000000ull;
+    stack.push_back({start, P.so[start]});
+    via.push_back(-1);
+    while (!stack.empty()) {
+        if (++steps > budget) {
+            m.npath = 0;
+            m.npath_status = 2;
+            return;
+        }
+        auto &fr = stack.back();
+        const int32_t v = fr.first;
+        if (v == end && stack.size() > 1) {  // Npath(end) = 1: a walk stops at end
+            used[via.back()] = 0;
+            stack.pop_back();
+            via.pop_back();
+            continue;
+        }
+        if (fr.second >= P.so[v + 1]) {
+            if (via.back() >= 0) used[via.back()] = 0;
+            stack.pop_back();
+            via.pop_back();
+            continue;
+        }
+        const int64_t e = fr.second++;
+        if (used[e]) continue;
+        used[e] = 1;
+        const int32_t w = P.st[e];
+        if (w == end && ++count >= cap) {
+            m.npath = cap;
+            m.npath_status = 1;
+            return;
+        }
+        stack.push_back({w, P.so[w]});
+        via.push_back(e);
+    }
+    m.npath = count;
+}
+
+}  // namespace tpg

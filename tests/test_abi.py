@@ -151,3 +151,35 @@ def test_metrics_fig1b_and_loops():
     assert m["sccs"] == 1 and m["scc_nodes"] == 6 and m["scc_edges"] == 7
     m = tp.metrics(gen.k_seq_loops(3, 4))
     assert m["sccs"] == 3 and m["cc"] == m["edges"] - m["nodes"] + 2
+
+
+def test_metrics_npath_vs_oracle():
+    """tpgen_metrics_compute's Npath (acyclic DP / arc-simple walk search) equals the tier-0
+    recursion on the arc set (oracle/brute.py, pinned to P:592)."""
+    import paper_2210_16998_b200 as tp
+    from workloads import generators as gen
+    assert tp.metrics(gen.fig1b())["npath"] == 4
+    graphs = [gen.fig1b(), gen.k_seq_if(4), gen.k_nested_if(3), gen.k_seq_loops(2, 3), gen.config2()]
+    graphs += [gen.random_dag_cfg(9, s) for s in range(3)]
+    for g in graphs:
+        m = tp.metrics(g)
+        if m["npath_status"] != "exact":
+            continue
+        assert m["npath"] == brute.npath(g.n, brute.graph_succ(g), g.entry, g.exit), g.name
+    for i, g in enumerate(_corpus(80, 77)):
+        if g.n < 2 or g.n > 7:
+            continue
+        m = tp.metrics(g, start=0, end=g.n - 1)
+        assert m["npath_status"] == "exact"
+        assert m["npath"] == brute.npath(g.n, brute.graph_succ(g), 0, g.n - 1), g.name
+        assert m["cc"] == m["edges"] - m["nodes"] + 2 * m["weak_components"]
+
+
+def test_shard_range_partitions_the_starts():
+    import paper_2210_16998_b200 as tp
+    from workloads import generators as gen
+    g = gen.config5()
+    for world in (1, 2, 3, 8):
+        cuts = [tp.shard_range(g, r, world) for r in range(world)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == g.n
+        assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))

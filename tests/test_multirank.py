@@ -1,9 +1,9 @@
 """World-size-2 `gloo` test of the multi-rank path, CPU only.
 
-bench.py's N>1 run gives rank r the start-vertex range of the r-th disjoint
-copy of the workload graph and reduces counts (sum) and times (max) over the
-ranks.  Here each rank computes its block with the ORACLE (no GPU on this box)
-and the test checks, across two real processes talking over gloo:
+bench.py's N>1 run gives rank r start-vertex shard (r, N) of the planner's
+cost-balanced split (tpgen_shard_range) and reduces counts (sum) and times (max)
+over the ranks.  Here each rank computes its block with the ORACLE (no GPU on
+this box) and the test checks, across two real processes talking over gloo:
   * the rank blocks concatenate to the canonical list of the whole union graph
     (shards are contiguous blocks of the global order);
   * bench.rank_reduce sums the counts and maxes the times;
@@ -27,6 +27,16 @@ def _free_port() -> int:
     return p
 
 
+def _cut(g, world):
+    """Start-vertex shard boundaries: the library's planner split (tpgen_shard_range, a host call)."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import paper_2210_16998_b200 as tp
+
+    return [tp.shard_range(g, r, world)[0] for r in range(world)] + [g.n]
+
+
 def _worker(rank: int, world: int, port: int, q):
     import sys
 
@@ -42,14 +52,13 @@ def _worker(rank: int, world: int, port: int, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        base = gen.dense_scc(9, 3, 2)
-        g, ranges = bench.workload(world, base=base)
-        lo, hi = ranges[rank]
+        g = gen.parallel_sccs(3, 7, 4)  # config 5's shape, small: Start -> d_i -> SCC_i -> J -> End
+        lo, hi = _cut(g, world)[rank], _cut(g, world)[rank + 1]
         off, vert = oracle.prime_paths(g, v_lo=lo, v_hi=hi)
         n_pp = len(off) - 1
         ext = oracle.ext_count(g, v_lo=lo, v_hi=hi)
-        tot_pp, tot_ext, ms_max, e2e_max = bench.rank_reduce(dist, world, float(n_pp), float(ext),
-                                                             1.0 + rank, 10.0 * (rank + 1), "cpu")
+        (tot_pp, tot_ext), (ms_max, e2e_max) = bench.rank_reduce(dist, world, [float(n_pp), float(ext)],
+                                                                 [1.0 + rank, 10.0 * (rank + 1)], "cpu")
         # gather the blocks to rank 0 (object collective over gloo)
         blocks = [None] * world
         dist.all_gather_object(blocks, (off.tolist(), vert.tolist()))
@@ -85,8 +94,7 @@ def test_two_rank_gloo_shards_and_reduce():
         p.join(timeout=60)
         assert p.exitcode == 0
 
-    base = gen.dense_scc(9, 3, 2)
-    g, _ = bench.workload(world, base=base)
+    g = gen.parallel_sccs(3, 7, 4)
     off, vert = oracle.prime_paths(g)
     # concatenation of the rank blocks == the whole canonical list
     cat_off, cat_vert = [0], []
@@ -104,8 +112,8 @@ def test_two_rank_gloo_shards_and_reduce():
     lo = sum(int(p[0]) | (int(p[1]) << 32) for p in res["parts"]) % (1 << 64)
     hi = sum(int(p[2]) | (int(p[3]) << 32) for p in res["parts"]) % (1 << 64)
     assert (lo, hi) == oracle.digest(off, vert)
-    # each copy contributes the same block (weak scaling: equal work per rank)
-    assert len(res["blocks"][0][1]) == len(res["blocks"][1][1])
+    # strong scaling: both ranks got work
+    assert len(res["blocks"][0][1]) > 0 and len(res["blocks"][1][1]) > 0
 
 
 def _worker_sharded(rank: int, world: int, port: int, q):

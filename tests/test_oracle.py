@@ -474,3 +474,18 @@ def test_digest_single_vertex_and_cycle_closed_forms():
     K = 7
     rot = [[(i + j) % K for j in range(K)] + [i] for i in range(K)]
     assert len({_dig([r]) for r in rot}) == K
+
+
+# ---------------------------------------------------------------- Npath (NEXT #3)
+def test_npath_closed_forms():
+    """Npath of the paper's examples: 4 for Fig. 1(b) (the loop body runs at
+    most once: <S,1,2,9,E>, <S,..,3,4,8,2,9,E>, <S,..,3,5,6,8,2,9,E>, <S,..,3,5,7,E>);
+    K sequential if-then-else: 2^K; a DAG: the number of start -> end paths."""
+    g = gen.fig1b()
+    assert brute.npath(g.n, brute.graph_succ(g), g.entry, g.exit) == 4
+    for K in (1, 3, 5):
+        g = gen.k_seq_if(K)
+        assert brute.npath(g.n, brute.graph_succ(g), g.entry, g.exit) == 2 ** K
+    for seed in range(4):
+        g = gen.random_dag_cfg(8 + seed, seed)
+        assert brute.npath(g.n, brute.graph_succ(g), g.entry, g.exit) == _count_st_paths(g)
