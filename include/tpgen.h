@@ -85,8 +85,9 @@ typedef struct {
     int32_t output_mode;       /* TPGEN_OUT_MATERIALIZE (default) | TPGEN_OUT_COUNT_HASH (counts + digest only) */
     int32_t shard_rank;        /* start-vertex shard (0-based); with shard_count = 1 the whole graph */
     int32_t shard_count;       /* >= 1 */
-    int32_t start_lo, start_hi;  /* explicit start-vertex range [lo, hi) overriding the shard split when
-                                    start_hi > start_lo (e.g. one rank per independent component) */
+    int32_t start_lo, start_hi;  /* explicit start-vertex range [lo, hi) instead of the shard split when
+                                    start_hi > start_lo (e.g. one rank per independent component); combined
+                                    with shard_count > 1: TPGEN_ERR_INVALID_ARGUMENT */
     int64_t max_paths;         /* 0 = unlimited */
     int64_t max_extensions;    /* 0 = unlimited */
     int32_t tp_mode;           /* TPGEN_TP_PER_PP: one TP per PP, aligned; TPGEN_TP_GREEDY: greedy cover --

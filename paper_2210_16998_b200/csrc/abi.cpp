@@ -28,6 +28,10 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("bad shard spec");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
+    if (o.shard_count > 1 && o.start_hi > o.start_lo) {
+        tpg::set_error("a start range and a shard spec cannot be combined");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
     if (o.output_mode != TPGEN_OUT_MATERIALIZE && o.output_mode != TPGEN_OUT_COUNT_HASH) {
         tpg::set_error("bad output_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;

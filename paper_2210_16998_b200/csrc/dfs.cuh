@@ -507,10 +507,9 @@ __device__ __forceinline__ unsigned int ld_flags(const unsigned int *p) {
 __device__ __forceinline__ void st_relaxed(unsigned int *p, unsigned int v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// The consumer polls the flag with a relaxed load and only then issues its
-// (L2, .cg) loads of the unit payload: the payload was made visible at L2 by
-// the producer's release before the flag, and the payload loads are control
-// dependent on the flag value -- no acquire, so no L1 invalidation per claim.
+// The consumer polls the flag with a relaxed load; once it sees the flag set it
+// issues a fence.acq_rel (the acquire half of the hand-off: one per claimed unit)
+// and then its L2 (.cg) loads of the unit payload.
 __device__ __forceinline__ unsigned int ld_relaxed(const unsigned int *p) {
     unsigned int v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -739,6 +738,9 @@ __global__ void __launch_bounds__(DfsTraits<T>::threads, LEAN ? kLeanBlocks : Df
         if (waiting) {
             if (rdy != 0u) {
                 waiting = false;
+                // acquire: the producer's unit stores (released by its fence before the flag) are
+                // visible to the loads below (Theorem-2-style race freedom of the hand-off)
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 // queue slots are written by other SMs during this launch: read them at L2 (ld.cg)
                 TPG_DCHECK(slot >= 0 && slot < (int64_t)A.qcap, "dfs: claimed slot out of range");
                 const Unit<W> *U = units + slot;

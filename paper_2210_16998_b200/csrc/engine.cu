@@ -76,6 +76,17 @@ tpgen_status DevBuf::ensure(size_t bytes, cudaStream_t s) {
     cap = nc;
     return TPGEN_OK;
 }
+tpgen_status DevBuf::ensure_exact(size_t bytes, cudaStream_t s) {
+    if (bytes <= cap) return TPGEN_OK;
+    const size_t nc = (bytes + 255) & ~(size_t)255;
+    if (p) TPG_CK(cudaFreeAsync(p, s));
+    p = nullptr;
+    cap = 0;
+    TPG_CK(pool_alloc(&p, nc, s));
+    cap = nc;
+    return TPGEN_OK;
+}
+
 void DevBuf::release(cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
     p = nullptr;
@@ -1656,10 +1667,19 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     uint64_t cap = std::max<uint64_t>({1ull << 22, (uint64_t)(est / 4), P.f_cap_hwm + P.f_cap_hwm / 4});
     if (const char *ev = getenv("TPGEN_FRONTIER_CAP")) cap = std::max<uint64_t>(64, atoll(ev));  // test hook: retries
     uint64_t cap_max = ~0ull;  // memory budget: queried only when a buffer has to grow
-    auto budget = [&]() -> tpgen_status {
+    // free device memory the frontier may use: cudaMemGetInfo, or the TPGEN_FRONTIER_BUDGET test hook
+    // (bytes), plus what the frontier buffers already hold
+    auto free_mem = [&](size_t &f) -> tpgen_status {
         size_t free_b = 0, total_b = 0;
         TPG_CK(cudaMemGetInfo(&free_b, &total_b));
-        cap_max = (uint64_t)((double)(free_b + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / kRecB);
+        if (const char *ev = getenv("TPGEN_FRONTIER_BUDGET")) free_b = (size_t)strtoull(ev, nullptr, 10);
+        f = free_b + P.f_buf0.cap + P.f_buf1.cap;
+        return TPGEN_OK;
+    };
+    auto budget = [&]() -> tpgen_status {  // two ping-pong buffers of exactly cap records: 90 % of it
+        size_t f = 0;
+        TPG_TRY(free_mem(f));
+        cap_max = (uint64_t)((double)f * 0.45 / kRecB);
         return TPGEN_OK;
     };
     if (cap * kRecB > std::min(P.f_buf0.cap, P.f_buf1.cap)) TPG_TRY(budget());
@@ -1676,6 +1696,17 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     if (per_sm == 0) TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_k, kFThreads, ts ? 32 * 1024 : 0));
     const int grid = P.num_sms * std::max(per_sm, 1);
     Timer tall;
+    const bool kdbg = getenv("TPGEN_DEBUG") != nullptr;  // a synchronised error check after every launch
+    auto KC = [&](const char *what, int l) -> tpgen_status {
+        if (!kdbg) return TPGEN_OK;
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            fprintf(stderr, "[tpgen frontier] %s level %d: %s\n", what, l, cudaGetErrorString(e));
+            set_error(std::string("frontier ") + what + ": " + cudaGetErrorString(e));
+            return TPGEN_ERR_CUDA;
+        }
+        return TPGEN_OK;
+    };
     std::vector<unsigned long long> h(nctr);
     int64_t launches = 0;
     float ms = 0;
@@ -1688,8 +1719,13 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     }
     for (int attempt = 0; !chunked; attempt++) {
         cap = std::min(cap, cap_max);
-        TPG_TRY(P.f_buf0.ensure(cap * kRecB, s));
-        TPG_TRY(P.f_buf1.ensure(cap * kRecB, s));
+        if (cap_max != ~0ull) {  // under a memory budget: exact sizes (the budget counts every byte)
+            TPG_TRY(P.f_buf0.ensure_exact(cap * kRecB, s));
+            TPG_TRY(P.f_buf1.ensure_exact(cap * kRecB, s));
+        } else {
+            TPG_TRY(P.f_buf0.ensure(cap * kRecB, s));
+            TPG_TRY(P.f_buf1.ensure(cap * kRecB, s));
+        }
         ulonglong2 *buf[2] = {P.f_buf0.as<ulonglong2>(), P.f_buf1.as<ulonglong2>()};
         uint64_t *bufS[2] = {reinterpret_cast<uint64_t *>(buf[0] + cap), reinterpret_cast<uint64_t *>(buf[1] + cap)};
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
@@ -1712,6 +1748,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             root_k<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
+            TPG_TRY(KC("root", -1));
             for (int l = 0; l < Lmax; l++) {
                 A.in = buf[l & 1];
                 A.in_S = bufS[l & 1];
@@ -1722,6 +1759,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
                 A.l = l;
                 level_k<<<grid, kFThreads, lsmem, s>>>(A);
                 launches++;
+                TPG_TRY(KC("level", l));
             }
         }
         cudaEventRecord(tall.b, s);
@@ -1740,13 +1778,18 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         if (cap_max == ~0ull) TPG_TRY(budget());
         if (cap >= cap_max) {  // no level fits: the DFS-chunked frontier in the same memory
             chunked = true;
-            capc = cap_max * 2 / (uint64_t)(Lmax + 1);
             break;
         }
         cap = std::max<uint64_t>(2 * cap, peak + peak / 4);  // a truncated level under-counts the next ones
     }
     if (chunked) {
-        if (cap_max == ~0ull) TPG_TRY(budget());
+        const size_t stride_b = std::max<size_t>(kRecB, 16);  // (16-B level stride of the key array)
+        if (capc == 0) {  // automatic switch: release the second buffer, then one buffer per level
+            P.f_buf1.release(s);
+            size_t f = 0;
+            TPG_TRY(free_mem(f));
+            capc = (uint64_t)((double)f * 0.9 / ((double)(Lmax + 1) * stride_b));
+        }
         // DFS over chunks of levels (the north star's "DFS-chunked when the frontier would
         // overflow HBM"): one buffer of capc records per level; a chunk of level l holds at
         // most capc / D records (D = the largest out-degree), so its children always fit in
@@ -1757,7 +1800,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             set_error("frontier chunk buffers too small for the roots (use the DFS engine)");
             return TPGEN_ERR_OUT_OF_MEMORY;
         }
-        TPG_TRY(P.f_buf0.ensure((size_t)(Lmax + 1) * capc * std::max<size_t>(kRecB, 16), s));  // 16-B level stride
+        TPG_TRY(P.f_buf0.ensure_exact((size_t)(Lmax + 1) * capc * stride_b, s));
         ulonglong2 *base = P.f_buf0.as<ulonglong2>();
         uint64_t *baseS = reinterpret_cast<uint64_t *>(base + (size_t)(Lmax + 1) * capc);
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
@@ -1781,6 +1824,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             root_k<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(),
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
+            TPG_TRY(KC("root", -1));
             TPG_CK(cudaMemcpyAsync(&nl[0], ctr + 8, 8, cudaMemcpyDeviceToHost, s));
             TPG_CK(cudaStreamSynchronize(s));
             recs += nl[0];
@@ -1805,6 +1849,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
             A.l = l;
             level_k<<<grid, kFThreads, lsmem, s>>>(A);
             launches++;
+            TPG_TRY(KC("chunk level", l));
             cur[l] += k;
             if (l + 1 < Lmax) {  // level l+1 records can have children: descend
                 TPG_CK(cudaMemcpyAsync(&nl[l + 1], ctr + 8 + l + 1, 8, cudaMemcpyDeviceToHost, s));

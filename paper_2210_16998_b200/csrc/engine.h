@@ -14,6 +14,7 @@ struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
     tpgen_status ensure(size_t bytes, cudaStream_t s);
+    tpgen_status ensure_exact(size_t bytes, cudaStream_t s);  // no growth headroom (memory-budgeted buffers)
     void release(cudaStream_t s);
     template <class T>
     T *as() const {

@@ -95,6 +95,7 @@ struct FT<uint32_t> {
     __device__ static int popc(uint32_t x) { return __popc(x); }
     template <bool HASH>
     __device__ static ulonglong2 ld(const FrontierArgs &A, unsigned long long i, uint64_t &S) {
+        TPG_DCHECK(i < A.cap, "frontier: record read beyond the level buffer");
         if constexpr (!HASH) {  // counts only: 8-byte records (the key)
             S = 0;
             return make_ulonglong2(__ldcs(reinterpret_cast<const unsigned long long *>(A.in) + i), 0);
@@ -112,6 +113,7 @@ struct FT<uint32_t> {
     template <bool HASH>
     __device__ static void st(const FrontierArgs &A, unsigned long long j, uint32_t M, uint32_t w, uint32_t s,
                               uint32_t vb, uint64_t S) {
+        TPG_DCHECK(j < A.cap, "frontier: record write beyond the level buffer");
         if constexpr (HASH) __stcs(A.out + j, make_ulonglong2(fkey(M, w, s, vb), S));
         else __stcs(reinterpret_cast<unsigned long long *>(A.out) + j, (unsigned long long)fkey(M, w, s, vb));
     }
@@ -201,7 +203,10 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     __shared__ unsigned long long red[5][kFThreads / 32];
     __shared__ uint64_t pqs[kFThreads / 32][64];  // per warp: digest sums S of prime paths awaiting their hash
     const uint64_t pw = pos_weight((uint32_t)(A.l + 1));  // digest weight of the new vertex's position
-    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);  // an overflowed level holds cap records
+    // once a level has overflowed the attempt is discarded (the call retries bigger or goes
+    // chunked): the buffer holds unwritten gaps, so no later level reads it
+    if (*reinterpret_cast<volatile const unsigned int *>(A.overflow) & 1u) return;
+    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);
     if ((unsigned long long)blockIdx.x * kFTile >= n_in) return;  // small levels: idle blocks leave at once
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {

@@ -162,3 +162,19 @@ def test_frontier_config3_full_size():
                 "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == \
             _oracle_stats(g, s, s + 1)
     plan.close()
+
+
+def test_frontier_memory_budget_switches_to_chunks(monkeypatch):
+    """A device-memory budget too small for one level (TPGEN_FRONTIER_BUDGET, bytes) makes the
+    call switch to the DFS-chunked frontier by itself (the budget counts the exact
+    buffer sizes); the results stay equal to the oracle's."""
+    g = gen.dense_scc(14, 4, 4)
+    ref = _oracle_stats(g)
+    monkeypatch.setenv("TPGEN_FRONTIER_BUDGET", str(1 << 20))
+    plan = tp.Plan(g)
+    st = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
+    plan.close()
+    got = {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"], "n_extensions": st["n_extensions"],
+           "digest": (st["hash_lo"], st["hash_hi"])}
+    assert got == ref
+    assert st["gpu_launches"] > 40  # many chunk launches, not one per level

@@ -141,7 +141,9 @@ def _worker_sharded(rank: int, world: int, port: int, q):
                   "n_extensions": oracle.ext_count(g, v_lo=cut[r], v_hi=cut[r + 1]), "hash_lo": lo, "hash_hi": hi}
             return PathSet(off, vert, len(off) - 1, False, st)
 
-        res = sharded_prime_paths(g, compute=compute)
+        res = sharded_prime_paths(g, compute=compute, gather=True)
+        if rank == 0:
+            q.put(dict(whole=(res.whole[0].tolist(), res.whole[1].tolist())))
         if rank == 1:
             q.put(dict(pp_base=res.pp_base, vertex_base=res.vertex_base, n_paths=res.n_paths,
                        total_vertices=res.total_vertices, n_extensions=res.n_extensions, digest=res.digest,
@@ -167,7 +169,9 @@ def test_sharded_prime_paths_gloo():
     procs = [ctx.Process(target=_worker_sharded, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = q.get(timeout=240)
+    got = [q.get(timeout=240), q.get(timeout=240)]
+    res = next(x for x in got if "local" in x)
+    whole = next(x for x in got if "whole" in x)["whole"]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -181,3 +185,6 @@ def test_sharded_prime_paths_gloo():
     assert res["n_paths"] == len(off) - 1 and res["total_vertices"] == int(off[-1])
     assert res["n_extensions"] == oracle.ext_count(g)
     assert tuple(res["digest"]) == oracle.digest(off, vert)
+    # C4: rank 0 holds the whole canonical list, element by element
+    assert np.array_equal(np.asarray(whole[0], dtype=np.int64), off)
+    assert np.array_equal(np.asarray(whole[1], dtype=np.int32), vert)
