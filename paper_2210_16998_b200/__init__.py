@@ -234,14 +234,16 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
 
 
 def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *, device: int = 0,
-               output: str = "device", stream=None, cover: str = "per_pp") -> PathSet:
+               output: str = "device", stream=None, cover: str = "per_pp", mode: str = "materialize") -> PathSet:
     """Entry->exit test paths (R15): one per prime path,
     aligned with the prime-path list (cover="per_pp"), or the greedy cover -- longest
-    uncovered prime path first, every prime path contained in a TP covered (cover="greedy")."""
+    uncovered prime path first, every prime path contained in a TP covered (cover="greedy").
+    ``mode="count"``: COUNT_HASH -- the test paths' count, vertices and R20 digest in the
+    stats, nothing written (fused into the count-mode enumeration when ``prime`` is None)."""
     lib = library()
     so, st, n = _csr(graph)
     alloc = None
-    o = _options(device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(device, stream), alloc)
+    o = _options(device, output, mode, (0, 1), mode == "count", 0, 0, _stream_handle(device, stream), alloc)
     o.tp_mode = _tp_mode(cover)
     keep = []
     pin = _paths_in(prime, device, keep)
@@ -351,11 +353,11 @@ class Plan:
         return _wrap(paths, stats, alloc, host_out)
 
     def test_paths(self, entry: int, exit: int, prime: Optional[PathSet] = None, *, output: str = "device",
-                   stream=None, cover: str = "per_pp") -> PathSet:
+                   stream=None, cover: str = "per_pp", mode: str = "materialize") -> PathSet:
         """Test paths of the plan's graph (tpgen_plan_test_paths): no re-planning per call."""
         lib = library()
-        o = _options(self.device, output, "materialize", (0, 1), False, 0, 0, _stream_handle(self.device, stream),
-                     None)
+        o = _options(self.device, output, mode, (0, 1), mode == "count", 0, 0,
+                     _stream_handle(self.device, stream), None)
         o.tp_mode = _tp_mode(cover)
         keep = []
         pin = _paths_in(prime, self.device, keep)

@@ -801,6 +801,8 @@ __global__ void item_weight_s_kernel(DevGraph G, const ItemS *items, int64_t n, 
 }
 
 struct StitchSArgs {
+    const TpTerm *tp;          // non-null: the test paths of the cross prime paths (terms per slot)
+    unsigned int *unreachable;
     const HeadS *heads;
     int64_t n_heads;
     const uint64_t *comp_off;  // exclusive scan of the heads' completion counts
@@ -815,7 +817,7 @@ struct StitchSArgs {
 // Completion k runs over the exit vertex's out-of-SCC arcs in order (W(w) completions each),
 // then is unranked through the entry groups (a binary search per level inside one group).
 __device__ __forceinline__ void hash_completion(const StitchSArgs &A, const DevGraph &G, const HeadS &H, uint64_t kk,
-                                                uint64_t &sa, uint64_t &sb) {
+                                                uint64_t &sa, uint64_t &sb, uint64_t &sv) {
     const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
     const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[H.x].gid));
     int32_t x = -1;
@@ -842,7 +844,10 @@ __device__ __forceinline__ void hash_completion(const StitchSArgs &A, const DevG
         const ItemS it = A.items[i];
         S += it.A + ((uint64_t)(uint32_t)it.B * (2u * pos) + ((uint64_t)((uint32_t)(it.B >> 32) * (2u * pos)) << 32));
         pos += (uint32_t)it.len;
-        if (it.x < 0) break;  // a tail segment ends the path
+        if (it.x < 0) {  // a tail segment ends the path (test paths: then the suffix walk of its last vertex)
+            if (A.tp != nullptr && !tp_tail(A.tp, it.last, S, pos)) atomicOr(A.unreachable, 1u);
+            break;
+        }
         const int4 mi = __ldg(reinterpret_cast<const int4 *>(&slots[it.x].gid));
         for (int a = 0; a < mi.z; a++) {  // the out-arc of the transit whose completions hold k2
             const int32_t ya = __ldg(G.out_gid + mi.y + a);
@@ -857,17 +862,22 @@ __device__ __forceinline__ void hash_completion(const StitchSArgs &A, const DevG
     }
     sa += mix64(S ^ (kSeedA + (uint64_t)pos));
     sb += mix64(S ^ (kSeedB + (uint64_t)pos));
+    sv += pos;
 }
 
-__device__ __forceinline__ void hash_flush(uint64_t sa, uint64_t sb, unsigned long long *acc) {
+// acc[0], acc[1]: digest; acc[2]: vertices of the hashed paths (test paths: the only place their
+// suffix walks are known)
+__device__ __forceinline__ void hash_flush(uint64_t sa, uint64_t sb, uint64_t sv, unsigned long long *acc) {
 #pragma unroll
     for (int d = 16; d; d >>= 1) {
         sa += __shfl_xor_sync(kFull, sa, d);
         sb += __shfl_xor_sync(kFull, sb, d);
+        sv += __shfl_xor_sync(kFull, sv, d);
     }
-    if ((threadIdx.x & 31) == 0 && (sa | sb)) {
+    if ((threadIdx.x & 31) == 0 && (sa | sb | sv)) {
         atomicAdd(acc, (unsigned long long)sa);
         atomicAdd(acc + 1, (unsigned long long)sb);
+        atomicAdd(acc + 2, (unsigned long long)sv);
     }
 }
 
@@ -876,15 +886,15 @@ constexpr uint64_t kSmallHead = 32;  // heads with at most this many completions
 // Small heads: one thread per head slot hashes all of its W <= kSmallHead completions (no search
 // over the heads); big[h] = 1 marks the others for stitch_big_kernel.
 __global__ void stitch_small_kernel(StitchSArgs A, DevGraph G, uint64_t *big, unsigned long long *acc) {
-    uint64_t sa = 0, sb = 0;
+    uint64_t sa = 0, sb = 0, sv = 0;
     for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < A.n_heads; h += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t w = ((h + 1 < A.n_heads) ? A.comp_off[h + 1] : A.n_comp) - A.comp_off[h];
         big[h] = w > kSmallHead ? 1 : 0;
         if (w == 0 || w > kSmallHead) continue;
         const HeadS H = A.heads[h];
-        for (uint64_t k = 0; k < w; k++) hash_completion(A, G, H, k, sa, sb);
+        for (uint64_t k = 0; k < w; k++) hash_completion(A, G, H, k, sa, sb, sv);
     }
-    hash_flush(sa, sb, acc);
+    hash_flush(sa, sb, sv, acc);
 }
 // big heads, compacted: idx[j] = head slot, w[j] = its completion count
 __global__ void stitch_big_list_kernel(StitchSArgs A, const uint64_t *pos, int64_t *idx, uint64_t *w) {
@@ -899,13 +909,13 @@ __global__ void stitch_big_list_kernel(StitchSArgs A, const uint64_t *pos, int64
 // big heads: one thread per completion (a binary search over the few big heads' offsets)
 __global__ void stitch_big_kernel(StitchSArgs A, DevGraph G, const int64_t *idx, const uint64_t *off, int64_t n_big,
                                   uint64_t n_big_comp, unsigned long long *acc) {
-    uint64_t sa = 0, sb = 0;
+    uint64_t sa = 0, sb = 0, sv = 0;
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_big_comp;
          g += (uint64_t)gridDim.x * blockDim.x) {
         const int64_t j = upper_bound_u64(off, 0, n_big, g) - 1;
-        hash_completion(A, G, A.heads[idx[j]], g - off[j], sa, sb);
+        hash_completion(A, G, A.heads[idx[j]], g - off[j], sa, sb, sv);
     }
-    hash_flush(sa, sb, acc);
+    hash_flush(sa, sb, sv, acc);
 }
 
 __global__ void fill_u32_kernel(uint32_t *p, uint32_t v, int64_t n) {
@@ -991,6 +1001,64 @@ __global__ void tp_flat_kernel(int32_t n, const int32_t *parent, const int32_t *
                 c = __ldg(next + c);
             }
         }
+    }
+}
+
+// Test-path digest terms per slot (TpTerm, kernels.cuh) from the flat walk tables: the prefix
+// walk of v minus its last vertex from position 0, the suffix walk minus its first vertex.
+__global__ void tp_terms_kernel(int32_t n, const int32_t *slot_gid, const uint64_t *vmix, const int64_t *pre_off,
+                                const int32_t *pre_len, const int64_t *suf_off, const int32_t *suf_len,
+                                const int32_t *pre_flat, const int32_t *suf_flat, TpTerm *out) {
+    for (int32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < n; sl += gridDim.x * blockDim.x) {
+        const int32_t v = slot_gid[sl];
+        TpTerm t;
+        t.pre_len = pre_len[v];
+        t.suf_len = suf_len[v];
+        t.S_pre = t.A_suf = t.B_suf = 0;
+        for (int32_t j = 0; j + 1 < t.pre_len; j++)
+            t.S_pre += __ldg(vmix + pre_flat[pre_off[v] + j]) * (2 * (uint64_t)j + 1);
+        for (int32_t j = 1; j < t.suf_len; j++) {
+            const uint64_t m = __ldg(vmix + suf_flat[suf_off[v] + j]);
+            t.A_suf += m * (2 * (uint64_t)(j - 1) + 1);
+            t.B_suf += m;
+        }
+        out[sl] = t;
+    }
+}
+
+// COUNT_HASH test paths of a given canonical prime-path list: per path its digest sum S and
+// mix sum B from its vertices, then the test path's terms (one thread per path).
+__global__ void tp_hash_list_kernel(const int64_t *off, const int32_t *vert, int64_t n, const int32_t *v_slot,
+                                    const uint64_t *vmix, const TpTerm *tp, unsigned long long *acc,
+                                    unsigned int *unreachable) {
+    uint64_t sa = 0, sb = 0, nv = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = off[i], e = off[i + 1];
+        uint64_t S = 0, B = 0;
+        for (int64_t j = a; j < e; j++) {
+            const uint64_t m = __ldg(vmix + vert[j]);
+            S += m * (2 * (uint64_t)(j - a) + 1);
+            B += m;
+        }
+        uint32_t len = (uint32_t)(e - a);
+        if (!tp_head(tp, __ldg(v_slot + vert[a]), S, B, len) || !tp_tail(tp, __ldg(v_slot + vert[e - 1]), S, len)) {
+            atomicOr(unreachable, 1u);
+            continue;
+        }
+        sa += mix64(S ^ (kSeedA + (uint64_t)len));
+        sb += mix64(S ^ (kSeedB + (uint64_t)len));
+        nv += len;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        sa += __shfl_xor_sync(kFull, sa, d);
+        sb += __shfl_xor_sync(kFull, sb, d);
+        nv += __shfl_xor_sync(kFull, nv, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc, (unsigned long long)sa);
+        atomicAdd(acc + 1, (unsigned long long)sb);
+        atomicAdd(acc + 2, (unsigned long long)nv);
     }
 }
 

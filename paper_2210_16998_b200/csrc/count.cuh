@@ -117,14 +117,19 @@ struct CntCfg {
 template <class T>
 constexpr size_t cnt_smem_block(bool seg) {
     return (size_t)CntCfg<T>::warps * (CntCfg<T>::ring_slots * 32 * (seg ? 20 : 12) + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) +
-                                       CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 10 : 0));
+                                       CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 12 : 0));
 }
 
-// SEG: the segment phase -- the trees of the SCC entry vertices: their cycles are prime
-// paths (when the entry lies in the call's start range), their tail and transit segments
-// (R8/R9) become ItemS records and the completion-DP aggregates.
-template <class T, bool TS, bool HSH, bool HX, bool SEG>
+// PH: the phase -- P_PP, the prime-path phase; P_TP, the same hashing every prime path's test
+// path instead (the lanes then also keep the sum B of mix(v) over their path); P_SEG, the
+// segment phase -- the trees of the SCC entry vertices: their cycles are prime paths (when the
+// entry lies in the call's start range; their test paths when A.tp is set), their tail and
+// transit segments (R8/R9) become ItemS records for the completion DP and the stitch.
+enum CntPhase : int { P_PP = 0, P_TP = 1, P_SEG = 2 };
+template <class T, bool TS, bool HSH, bool HX, int PH>
 __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt_kernel(DfsArgs A) {
+    constexpr bool SEG = PH == P_SEG;
+    constexpr bool TRACK_B = PH != P_PP;
     using C = CntCfg<T>;
     constexpr bool RS = C::RS;
     constexpr int WARPS = C::warps;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     uint32_t *srem = sringt + WARPS * RSLOTS * 32;                                      // [warp][level][lane]
     uint8_t *spath = reinterpret_cast<uint8_t *>(srem + (RS ? WARPS * 32 * 32 : 0));  // [warp][level][lane]
     uint64_t *sq = reinterpret_cast<uint64_t *>(spath + WARPS * PLEV * 32);            // CNT_QUEUE: [warp][64]
-    uint16_t *sql = reinterpret_cast<uint16_t *>(sq + (CNT_QUEUE ? WARPS * 64 : 0));  //            [warp][64]
+    uint32_t *sql = reinterpret_cast<uint32_t *>(sq + (CNT_QUEUE ? WARPS * 64 : 0));  //            [warp][64]
     uint64_t *sringb = reinterpret_cast<uint64_t *>(sql + (CNT_QUEUE ? WARPS * 64 : 0));  // SEG: [warp][slot][lane]
     const DevGraph &G = A.G;
     // 32-bit shared-window addresses of this lane's columns (opaque: kept in registers)
@@ -206,6 +211,16 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     uint32_t qn = 0;  // CNT_QUEUE: queued prime paths of the warp (warp-uniform, < 32 between hashes)
     const uint32_t ltm = (1u << lane) - 1u;
     auto put_ev = [&](bool pp, bool other, uint32_t kind, uint64_t Sx, uint64_t Bx, uint32_t len, int slot_) {
+        if ((PH == P_TP || (SEG && A.tp != nullptr)) && (pp || (other && kind == EK_HEAD))) {
+            // test paths instead (R15): the prefix walk of s before the path, the suffix walk of its
+            // last vertex after it (a head's suffix comes at the end of each completion; its tag keeps
+            // |h|, the drain adds the prefix's vertices)
+            uint32_t lt = len;
+            bool ok = tp_head(A.tp, L.vb + L.s, Sx, Bx, lt);
+            if (pp) ok = ok && tp_tail(A.tp, slot_, Sx, lt);
+            if (!ok) atomicOr(A.overflow, 16u);
+            if (pp) len = lt;
+        }
         if (pp) {
             t_pp += 1;
             t_vert += len;
@@ -215,17 +230,17 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
             if (pp) {
                 const uint32_t j = qn + __popc(bal & ltm);
                 asm volatile("st.shared.u64 [%0], %1;" ::"r"(qSa + j * 8u), "l"(Sx) : "memory");
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(qLa + j * 2u), "h"((uint16_t)len) : "memory");
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(qLa + j * 4u), "r"(len) : "memory");
             }
             qn += __popc(bal);
             if (qn >= 32) {
                 __syncwarp();
                 qn -= 32;
                 uint64_t z;
-                uint16_t n16;
+                uint32_t n32;
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qSa + (qn + lane) * 8u) : "memory");
-                asm volatile("ld.shared.u16 %0, [%1];" : "=h"(n16) : "r"(qLa + (qn + lane) * 2u) : "memory");
-                const uint64_t n = n16;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(n32) : "r"(qLa + (qn + lane) * 4u) : "memory");
+                const uint64_t n = n32;
                 t_ha += mix64(z ^ (kSeedA + n));
                 t_hb += mix64(z ^ (kSeedB + n));
                 __syncwarp();
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                         if (h && q < A.head_cap) {
                             HeadS hr;
                             hr.S = z;
-                            hr.len = (int32_t)len;
+                            hr.len = (int32_t)len + (PH == P_TP ? A.tp[L.vb + L.s].pre_len - 1 : 0);
                             hr.x = tslot;
                             *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&hr);
                         }
@@ -306,12 +321,14 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                         if (it && q < A.item_cap) {
                             uint64_t Bx;
                             asm volatile("ld.shared.u64 %0, [%1];" : "=l"(Bx) : "r"(bb + j * 256u) : "memory");
-                            const int32_t ent = __ldg(&reinterpret_cast<const Slot<1> *>(G.slots)[L.vb + L.s].gid);
+                            const Slot<1> *gsl = reinterpret_cast<const Slot<1> *>(G.slots);
+                            const int32_t ent = __ldg(&gsl[L.vb + L.s].gid);
+                            const int32_t lastv = tslot;  // (a slot: the test-path terms are per slot)
                             ulonglong2 *d = reinterpret_cast<ulonglong2 *>(A.items + q);
                             d[0] = make_ulonglong2(z, Bx);
                             d[1] = make_ulonglong2(
                                 (unsigned long long)len | ((unsigned long long)(uint32_t)(kind == EK_TAIL ? -1 : tslot) << 32),
-                                (unsigned long long)(uint32_t)ent);
+                                (unsigned long long)(uint32_t)ent | ((unsigned long long)(uint32_t)lastv << 32));
                         }
                         iblk += need;
                     }
@@ -411,8 +428,11 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 if (kind == K_CLOSURE) {  // the closing arc of path[0..depth] back to s
                     t_ext += L.emit ? 1 : 0;
                     st_pp = L.emit;
-                    st_S = S0 + mul64x32(tab.mix(L.vb + L.s), 2u * (uint32_t)depth + 3u);
+                    const uint64_t ms_ = tab.mix(L.vb + L.s);
+                    st_S = S0 + mul64x32(ms_, 2u * (uint32_t)depth + 3u);
+                    st_B = B0 + ms_;
                     st_len = (uint32_t)depth + 2;
+                    st_slot = L.vb + L.s;
                     L.rem = 0;
                     L.done = true;
                 } else {  // K_NODE: the node's own event, then its subtree
@@ -539,8 +559,8 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 ext32 += (take && (!SEG || L.emit)) ? 1u : 0u;
                 L.M = (push || pop) ? (L.M ^ vbit) : L.M;
                 L.S = push ? Sw : (pop ? L.S - prod : L.S);
-                const uint64_t Bw = L.B + mv;
-                if constexpr (SEG) L.B = push ? Bw : (pop ? L.B - mv : L.B);
+                const uint64_t Bw = L.B + mv;  // (the sum of mix: test-path digests and segment items)
+                if constexpr (TRACK_B) L.B = push ? Bw : (pop ? L.B - mv : L.B);
                 L.l = l + (push ? 1 : 0) - (pop ? 1 : 0);
                 L.rem = push ? cw : (pop ? rem_pop : (take ? (rem & (rem - 1)) : rem));
                 put_ev(pp, other, kind, Sw, Bw, (uint32_t)l + 2, vslot);
@@ -626,11 +646,11 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
         __syncwarp();
         if (lane < qn) {
             uint64_t z;
-            uint16_t n16;
+            uint32_t n32;
             asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qSa + lane * 8u) : "memory");
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(n16) : "r"(qLa + lane * 2u) : "memory");
-            t_ha += mix64(z ^ (kSeedA + (uint64_t)n16));
-            t_hb += mix64(z ^ (kSeedB + (uint64_t)n16));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(n32) : "r"(qLa + lane * 4u) : "memory");
+            t_ha += mix64(z ^ (kSeedA + (uint64_t)n32));
+            t_hb += mix64(z ^ (kSeedB + (uint64_t)n32));
         }
     }
     // the rings were drained; the head block's unused slots, then the totals

@@ -125,7 +125,7 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_v_slot, &d_slot_mix, &d_vmix, &d_scc_exm, &cheads, &citems, &citems2, &icnt,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_v_slot, &d_slot_mix, &d_vmix, &d_scc_exm, &cheads, &tp_terms, &citems, &citems2, &icnt,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan,
@@ -629,10 +629,16 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
         const bool ts = ctab <= kSmemTabMax;
         const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg);
-        void (*k)(DfsArgs) =
-            seg ? (ts ? cnt_kernel<CT, true, HSH, true, true> : cnt_kernel<CT, false, HSH, true, true>)
-                : (ts ? (any_exit ? cnt_kernel<CT, true, HSH, true, false> : cnt_kernel<CT, true, HSH, false, false>)
-                      : (any_exit ? cnt_kernel<CT, false, HSH, true, false> : cnt_kernel<CT, false, HSH, false, false>));
+        void (*k)(DfsArgs);
+        if (seg) {
+            k = ts ? cnt_kernel<CT, true, HSH, true, P_SEG> : cnt_kernel<CT, false, HSH, true, P_SEG>;
+        } else if (A.tp != nullptr) {
+            k = ts ? (any_exit ? cnt_kernel<CT, true, true, true, P_TP> : cnt_kernel<CT, true, true, false, P_TP>)
+                   : (any_exit ? cnt_kernel<CT, false, true, true, P_TP> : cnt_kernel<CT, false, true, false, P_TP>);
+        } else {
+            k = ts ? (any_exit ? cnt_kernel<CT, true, HSH, true, P_PP> : cnt_kernel<CT, true, HSH, false, P_PP>)
+                   : (any_exit ? cnt_kernel<CT, false, HSH, true, P_PP> : cnt_kernel<CT, false, HSH, false, P_PP>);
+        }
         TPG_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cdyn));
         k<<<cgrid, CntCfg<CT>::threads, cdyn, s>>>(A);
         return TPGEN_OK;
@@ -761,6 +767,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.heads = P.cheads.as<HeadS>();
         A.head_cap = (mode != M_REC && !seg) ? std::min<uint64_t>(hlim, P.cheads.cap / sizeof(HeadS)) : 0;
         A.items = P.citems.as<ItemS>();
+        A.tp = (mode != M_REC) ? P.cur_tp : nullptr;
         A.item_cap = (mode != M_REC && seg) ? std::min<uint64_t>(hlim, P.citems.cap / sizeof(ItemS)) : 0;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
         // LEAN: 32-bit masks, prime-path phase, no arc leaves any SCC (no head / segment
@@ -838,6 +845,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
                     ms, d[0], d[1], d[0] ? (double)d[1] / d[0] : 0.0, d[2], (h[1] >> 32) - qbase);
         }
         if (ovf & 1u) P.overflow = true;
+        if (ovf & 16u) P.tp_unreachable = true;
         if (mode != M_REC) {
             if (cacc_h) memcpy(cacc_h, hq + 112, 8 * sizeof(unsigned long long));
             P.chead_hwm = std::max<uint64_t>(P.chead_hwm, hq[112 + 5]);
@@ -1371,6 +1379,7 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
     st.max_scc = H.max_scc;
     st.ms_plan = P.ms_plan;
     P.overflow = false;
+    P.tp_unreachable = false;
     P.maxgen = 0;
     const int mode = o.compute_digest ? M_CNT : M_CNT_NOHASH;
     const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;  // host stage marks, synchronised
@@ -1447,6 +1456,10 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
     if (P.overflow) {
         set_error("prime-path count exceeds 2^62");
         return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    if (P.tp_unreachable) {
+        set_error("a prime path's first vertex is unreachable from entry or its last cannot reach exit");
+        return TPGEN_ERR_UNREACHABLE;
     }
     st.n_units = (int64_t)tail;
     HT("prime-path phase");
@@ -1553,6 +1566,9 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
         TPG_TRY(scan_multi(P, ha, 1, n_heads, &ncomp, s, launches));
         HT("items grouped");
         StitchSArgs SA;
+        SA.tp = P.cur_tp;
+        SA.unreachable = reinterpret_cast<unsigned int *>(ctr + 23);
+        TPG_CK(cudaMemsetAsync(ctr + 23, 0, 8, s));
         SA.heads = P.cheads.as<HeadS>();
         SA.n_heads = n_heads;
         SA.comp_off = P.hcomp.as<uint64_t>();
@@ -1561,8 +1577,8 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
         SA.cum = P.icum.as<uint64_t>();
         SA.ibeg = P.ibeg.as<int64_t>();
         SA.iend = P.iend.as<int64_t>();
-        unsigned long long *hacc = ctr + 16;
-        TPG_CK(cudaMemsetAsync(hacc, 0, 16, s));
+        unsigned long long *hacc = ctr + 24;  // digest a, b; vertices
+        TPG_CK(cudaMemsetAsync(hacc, 0, 24, s));
         // small heads (<= kSmallHead completions): a thread per head; big ones: a thread per completion
         TPG_TRY(P.sscratch.ensure((size_t)n_heads * 8 * 3 + 64, s));
         uint64_t *big = P.sscratch.as<uint64_t>();
@@ -1582,11 +1598,19 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
                 SA, G, bidx, bw, (int64_t)n_big, n_big_comp, hacc);
             launches += 2;
         }
-        unsigned long long hh[2];
-        TPG_CK(cudaMemcpyAsync(hh, hacc, 16, cudaMemcpyDeviceToHost, s));
+        unsigned long long hh[3], unr = 0;
+        TPG_CK(cudaMemcpyAsync(hh, hacc, 24, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaMemcpyAsync(&unr, ctr + 23, 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
+        if (unr) {
+            set_error("a prime path's last vertex cannot reach exit");
+            return TPGEN_ERR_UNREACHABLE;
+        }
         hd[0] += hh[0];
         hd[1] += hh[1];
+        if (P.cur_tp) {  // test paths: the cross ones' vertices include their suffix walks (known only here)
+            st.total_vertices = (int64_t)(n_vert - cross_v + hh[2]);
+        }
     }
     cudaEventRecord(tst.b, s);
     cudaEventRecord(tall.b, s);
@@ -1913,10 +1937,153 @@ tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *o
 }
 
 // ------------------------------------------------------------ test paths
+// Device copies of the test-path walk tables (R15): the host builds the two walk trees
+// (build_tp_tables), tp_flat_kernel expands them into flat per-vertex walks.
+struct TpDev {
+    int64_t *pre_off, *suf_off;
+    int32_t *pre_len, *suf_len, *parent, *next, *pre_flat, *suf_flat;
+};
+static tpgen_status tp_device_tables(PlanImpl &P, const TpTables &T, cudaStream_t s, int64_t &launches, TpDev &D) {
+    const HostPlan &H = P.hp;
+    const size_t nn = std::max<int32_t>(H.n, 1);
+    const size_t bytes = nn * 8 * 2 + nn * 4 * 4 + (size_t)(T.pre_total + T.suf_total + 2) * 4 + 64;
+    TPG_TRY(P.tp_tabs.ensure(bytes, s));
+    char *b = (char *)P.tp_tabs.p;
+    D.pre_off = (int64_t *)b;
+    D.suf_off = D.pre_off + nn;
+    D.pre_len = (int32_t *)(D.suf_off + nn);
+    D.suf_len = D.pre_len + nn;
+    D.parent = D.suf_len + nn;
+    D.next = D.parent + nn;
+    D.pre_flat = D.next + nn;
+    D.suf_flat = D.pre_flat + T.pre_total + 1;
+    TPG_CK(cudaMemcpyAsync(D.pre_off, T.pre_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(D.suf_off, T.suf_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(D.pre_len, T.pre_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(D.suf_len, T.suf_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(D.parent, T.parent.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaMemcpyAsync(D.next, T.next.data(), H.n * 4, cudaMemcpyHostToDevice, s));
+    if (H.n > 0) {
+        tp_flat_kernel<<<grid_for(H.n, 128, P.num_sms * 8), 128, 0, s>>>(H.n, D.parent, D.next, D.pre_off, D.pre_len,
+                                                                          D.suf_off, D.suf_len, D.pre_flat, D.suf_flat);
+        launches++;
+    }
+    return TPGEN_OK;
+}
+
+// COUNT_HASH test paths (tpgen_test_paths with output_mode COUNT_HASH): the count, vertices and
+// R20 digest of every prime path's test path, nothing written.  Without a prime-path list on a
+// graph the count modes take (SCCs <= 64 vertices), the count-mode enumeration hashes each test
+// path the moment its prime path is found (the TpTerm tables); otherwise tp_hash_list_kernel
+// hashes the test paths of the given (or computed) list.
+static tpgen_status run_test_paths_count(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry, int32_t exit,
+                                         const tpgen_options &o, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    const HostPlan &H = P.hp;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    int64_t launches = 0;
+    TpTables T;
+    build_tp_tables(H, entry, exit, T);
+    TpDev D;
+    TPG_TRY(tp_device_tables(P, T, s, launches, D));
+    TPG_TRY(P.tp_terms.ensure((size_t)std::max<int32_t>(H.n, 1) * sizeof(TpTerm), s));
+    if (H.n > 0) {
+        tp_terms_kernel<<<grid_for(H.n, 128, P.num_sms * 8), 128, 0, s>>>(
+            H.n, P.d_slot_gid.as<int32_t>(), P.d_vmix.as<uint64_t>(), D.pre_off, D.pre_len, D.suf_off, D.suf_len,
+            D.pre_flat, D.suf_flat, P.tp_terms.as<TpTerm>());
+        launches++;
+    }
+    tpgen_options oc = o;
+    oc.output_mode = TPGEN_OUT_COUNT_HASH;
+    oc.compute_digest = 1;
+    if (!pp_in && H.max_scc <= 64 && H.n < (1 << 21) && !getenv("TPGEN_NO_CNT")) {
+        P.cur_tp = P.tp_terms.as<TpTerm>();
+        tpgen_status r = (H.max_scc <= 32) ? run_count<uint32_t>(P, oc, stp) : run_count<uint64_t>(P, oc, stp);
+        P.cur_tp = nullptr;
+        if (r == TPGEN_OK && stp) {
+            stp->gpu_launches += launches;
+            stp->ms_total = now_ms() - t0;
+        }
+        return r;
+    }
+    // the prime paths as a list (given, or computed), then one thread per path
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    tpgen_paths own;
+    memset(&own, 0, sizeof(own));
+    const tpgen_paths *pp = pp_in;
+    if (!pp) {
+        tpgen_options o2 = o;
+        o2.output_mode = TPGEN_OUT_MATERIALIZE;
+        o2.output_on_device = 1;
+        o2.device_alloc = nullptr;
+        o2.device_free = nullptr;
+        o2.host_out = nullptr;
+        TPG_TRY(run_prime_paths(P, o2, &own, &st));
+        pp = &own;
+    }
+    struct Guard {
+        tpgen_paths *p;
+        ~Guard() { free_paths(p); }
+    } g{&own};
+    const int64_t n = pp->n_paths;
+    const int64_t *d_ppo = pp->offsets;
+    const int32_t *d_ppv = pp->vertices;
+    DevBuf tmp_o, tmp_v;
+    struct BufGuard {
+        DevBuf *a, *b;
+        cudaStream_t s;
+        ~BufGuard() {
+            a->release(s);
+            b->release(s);
+        }
+    } bg{&tmp_o, &tmp_v, s};
+    if (n > 0 && !pp->on_device) {
+        const int64_t nv = pp->offsets[n];
+        TPG_TRY(tmp_o.ensure((size_t)(n + 1) * 8, s));
+        TPG_TRY(tmp_v.ensure((size_t)std::max<int64_t>(nv, 1) * 4, s));
+        TPG_CK(cudaMemcpyAsync(tmp_o.p, pp->offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (nv) TPG_CK(cudaMemcpyAsync(tmp_v.p, pp->vertices, (size_t)nv * 4, cudaMemcpyHostToDevice, s));
+        d_ppo = tmp_o.as<int64_t>();
+        d_ppv = tmp_v.as<int32_t>();
+    }
+    TPG_TRY(P.ctr.ensure(32 * 8, s));
+    unsigned long long *acc = P.ctr.as<unsigned long long>() + 24;
+    TPG_CK(cudaMemsetAsync(acc, 0, 32, s));
+    if (n > 0) {
+        tp_hash_list_kernel<<<grid_for(n, 256, P.num_sms * 8), 256, 0, s>>>(
+            d_ppo, d_ppv, n, P.d_v_slot.as<int32_t>(), P.d_vmix.as<uint64_t>(), P.tp_terms.as<TpTerm>(), acc,
+            reinterpret_cast<unsigned int *>(acc + 3));
+        launches++;
+    }
+    unsigned long long h[4];
+    TPG_CK(cudaMemcpyAsync(h, acc, 32, cudaMemcpyDeviceToHost, s));
+    TPG_CK(cudaStreamSynchronize(s));
+    if (h[3]) {
+        set_error("a prime path's first vertex is unreachable from entry or its last cannot reach exit");
+        return TPGEN_ERR_UNREACHABLE;
+    }
+    st.n_paths = n;
+    st.total_vertices = (int64_t)h[2];
+    st.hash_lo = h[0];
+    st.hash_hi = h[1];
+    st.gpu_launches += launches;
+    st.ms_total = now_ms() - t0;
+    if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
 tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry, int32_t exit,
                             const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
     const double t0 = now_ms();
     memset(out, 0, sizeof(*out));
+    if (o.output_mode == TPGEN_OUT_COUNT_HASH) {
+        if (o.tp_mode != TPGEN_TP_PER_PP) {
+            set_error("COUNT_HASH test paths are the per-prime-path ones (tp_mode TPGEN_TP_PER_PP)");
+            return TPGEN_ERR_INVALID_ARGUMENT;
+        }
+        return run_test_paths_count(P, pp_in, entry, exit, o, stp);
+    }
     const HostPlan &H = P.hp;
     cudaStream_t s = (cudaStream_t)o.stream;
     tpgen_stats st;
@@ -2010,30 +2177,14 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
         if (stp) *stp = st;
         return TPGEN_OK;
     }
-    // one buffer: pre_off, suf_off (int64 n each), pre_len, suf_len, parent, next (int32 n each), flats
-    const size_t nn = std::max<int32_t>(H.n, 1);
-    const size_t bytes = nn * 8 * 2 + nn * 4 * 4 + (size_t)(T.pre_total + T.suf_total + 2) * 4 + 64;
-    TPG_TRY(P.tp_tabs.ensure(bytes, s));
-    char *b = (char *)P.tp_tabs.p;
-    int64_t *d_pre_off = (int64_t *)b;
-    int64_t *d_suf_off = d_pre_off + nn;
-    int32_t *d_pre_len = (int32_t *)(d_suf_off + nn);
-    int32_t *d_suf_len = d_pre_len + nn;
-    int32_t *d_parent = d_suf_len + nn;
-    int32_t *d_next = d_parent + nn;
-    int32_t *d_pre_flat = d_next + nn;
-    int32_t *d_suf_flat = d_pre_flat + T.pre_total + 1;
-    TPG_CK(cudaMemcpyAsync(d_pre_off, T.pre_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
-    TPG_CK(cudaMemcpyAsync(d_suf_off, T.suf_off.data(), H.n * 8, cudaMemcpyHostToDevice, s));
-    TPG_CK(cudaMemcpyAsync(d_pre_len, T.pre_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
-    TPG_CK(cudaMemcpyAsync(d_suf_len, T.suf_len.data(), H.n * 4, cudaMemcpyHostToDevice, s));
-    TPG_CK(cudaMemcpyAsync(d_parent, T.parent.data(), H.n * 4, cudaMemcpyHostToDevice, s));
-    TPG_CK(cudaMemcpyAsync(d_next, T.next.data(), H.n * 4, cudaMemcpyHostToDevice, s));
-    if (H.n > 0) {
-        tp_flat_kernel<<<grid_for(H.n, 128, P.num_sms * 8), 128, 0, s>>>(H.n, d_parent, d_next, d_pre_off, d_pre_len,
-                                                                          d_suf_off, d_suf_len, d_pre_flat, d_suf_flat);
-        st.gpu_launches++;
+    TpDev D;
+    {
+        int64_t l0 = 0;
+        TPG_TRY(tp_device_tables(P, T, s, l0, D));
+        st.gpu_launches += l0;
     }
+    int64_t *d_pre_off = D.pre_off, *d_suf_off = D.suf_off;
+    int32_t *d_pre_len = D.pre_len, *d_suf_len = D.suf_len, *d_pre_flat = D.pre_flat, *d_suf_flat = D.suf_flat;
 
     DevBuf lenb;
     struct LGuard {

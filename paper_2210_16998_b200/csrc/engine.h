@@ -8,6 +8,10 @@
 #include "internal.h"
 
 namespace tpg {
+struct TpTerm;
+}
+
+namespace tpg {
 
 // Grow-only, stream-ordered device buffer.
 struct DevBuf {
@@ -37,6 +41,9 @@ struct PlanImpl {
     DevBuf cheads;           // count modes: HeadS records of the prime-path phase
     DevBuf citems, citems2;  // count modes: ItemS records of the segment phase (as written; grouped by entry)
     DevBuf icnt;             // count modes: items per entry vertex, their scan, the scatter cursors
+    DevBuf tp_terms;         // count modes, test paths: TpTerm per slot
+    const TpTerm *cur_tp = nullptr;  // the running count-mode call hashes test paths with these terms
+    bool tp_unreachable = false;     // ... and found a path whose end vertices have no walk
     uint64_t chead_hwm = 0;  // most head slots any count-mode call of this plan reserved
     uint64_t citem_hwm = 0;  // most item slots any count-mode call of this plan reserved
     // DFS work queue (one slot per unit) and its per-unit results

@@ -173,6 +173,39 @@ struct TPG_ALIGN(16) HeadS {
     int32_t x;
 };
 
+// Test-path digest terms of a vertex v (COUNT_HASH test paths, R15 + R20): prefix[v] minus
+// its last vertex contributes S_pre (positions 0..), suffix[v] minus its first vertex
+// contributes A_suf + 2 o B_suf when it starts at position o.  pre_len / suf_len are the
+// walks' vertex counts (-1: no walk).  With them the TP of a path p (digest sum S, sum of
+// mix B, L vertices, first f, last w) has
+//   S_tp = S_pre[f] + S + 2 (pre_len[f] - 1) B + A_suf[w] + 2 (pre_len[f] - 1 + L) B_suf[w],
+//   |TP| = pre_len[f] - 1 + L + suf_len[w] - 1.
+struct TPG_ALIGN(16) TpTerm {
+    uint64_t S_pre, A_suf, B_suf;
+    int32_t pre_len, suf_len;
+};
+
+__device__ __forceinline__ uint64_t mul64x32_(uint64_t m, uint32_t w) {
+    return (uint64_t)(uint32_t)m * w + ((uint64_t)((uint32_t)(m >> 32) * w) << 32);
+}
+// prefix part of a test path: S' = S_pre[f] + S + 2 o B, positions consumed o + L; false if no walk
+__device__ __forceinline__ bool tp_head(const TpTerm *tp, int f, uint64_t &S, uint64_t B, uint32_t &len) {
+    const TpTerm t = tp[f];
+    if (t.pre_len < 0) return false;
+    const uint32_t o = (uint32_t)t.pre_len - 1u;
+    S = t.S_pre + S + mul64x32_(B, 2u * o);
+    len += o;
+    return true;
+}
+// suffix part: S += A_suf[w] + 2 L B_suf[w], L = positions so far; false if no walk
+__device__ __forceinline__ bool tp_tail(const TpTerm *tp, int w, uint64_t &S, uint32_t &len) {
+    const TpTerm t = tp[w];
+    if (t.suf_len < 0) return false;
+    S += t.A_suf + mul64x32_(t.B_suf, 2u * len);
+    len += (uint32_t)t.suf_len - 1u;
+    return true;
+}
+
 // Count-mode segment item (cnt_kernel's segment phase) of the entry vertex ent (global id):
 // a tail segment (x < 0), or a transit segment ending at the exit vertex of slot x, followed
 // by any of that vertex's out-of-SCC arcs (in arc order, W(y) completions each).  With the
@@ -184,7 +217,7 @@ struct TPG_ALIGN(16) ItemS {
     int32_t len;
     int32_t x;
     int32_t ent;
-    int32_t pad;
+    int32_t last;  // slot of its last vertex (the path's last vertex when it is a tail)
 };
 
 struct DfsArgs {
@@ -227,6 +260,7 @@ struct DfsArgs {
     unsigned long long head_cap;
     ItemS *items;                 // count modes, segment phase: items go to items[0 .. item_cap)
     unsigned long long item_cap;  //   (cacc[7] = item slots reserved)
+    const TpTerm *tp;             // count modes: non-null = hash the prime paths' TEST PATHS (per slot)
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)

@@ -135,3 +135,61 @@ def test_config5_every_start_vertex_vs_oracle():
         assert _gpu_tot(st) == tuple(int(x) for x in ref[v, :4]), v
         assert st["n_extensions"] == int(ref[v, 4]), v
     plan.close()
+
+
+# ------------------------------------------------------------ test paths, COUNT_HASH
+def _tp_graphs():
+    yield gen.fig1b()
+    yield gen.config2()
+    yield gen.k_seq_loops(4, 3)
+    yield gen.config4(K=30)
+    yield gen.parallel_sccs(3, 24, 9)
+    yield gen.parallel_sccs(2, 40, 3)
+
+
+def test_tp_count_mode_matches_oracle():
+    """tpgen_test_paths in COUNT_HASH mode (each prime path's R15 test path hashed when the
+    path is found, never written) equals the oracle's streamed TP statistics; the list path
+    (test paths of a given prime-path list) gives the same numbers."""
+    for g in _tp_graphs():
+        ref = _tot(oracle.pp_stats(g, tp=(g.entry, g.exit)))
+        st = tp.test_paths(g, g.entry, g.exit, mode="count").stats
+        assert _gpu_tot(st) == ref, g.name
+        pps = tp.prime_paths(g)
+        st2 = tp.test_paths(g, g.entry, g.exit, pps, mode="count").stats
+        assert _gpu_tot(st2) == ref, g.name
+
+
+def test_tp_count_mode_unreachable():
+    g = gen.from_arcs(4, [(0, 1), (1, 0), (2, 3)])
+    with pytest.raises(tp.TpgenError) as ei:
+        tp.test_paths(g, 0, 1, mode="count")
+    assert ei.value.status_name == "TPGEN_ERR_UNREACHABLE"
+
+
+@pytest.mark.timeout(1200)
+def test_config4_full_test_paths_element_by_element():
+    """Config 4 at full size (K = 150 loops): every test path, element by element, against
+    oracle.test_paths (R15) of the oracle's prime paths; and the COUNT_HASH digest."""
+    g = gen.config4()
+    ro, rv = oracle.prime_paths(g)
+    to, tv = oracle.test_paths(g, ro, rv, g.entry, g.exit)
+    ts = tp.test_paths(g, g.entry, g.exit)
+    o, v = ts.to_numpy()
+    np.testing.assert_array_equal(o, to)
+    np.testing.assert_array_equal(v, tv)
+    st = tp.test_paths(g, g.entry, g.exit, mode="count").stats
+    assert (st["n_paths"], st["total_vertices"]) == (len(to) - 1, int(to[-1]))
+    assert (st["hash_lo"], st["hash_hi"]) == oracle.digest(to, tv)
+
+
+@pytest.mark.timeout(1800)
+def test_config3_and_config5_test_path_digests():
+    """Configs 3 and 5 at full size: the COUNT_HASH test-path count, vertices and digest equal
+    the oracle's streamed TP statistics over every start vertex (host cores)."""
+    for g, entry, exit_ in ((gen.config3(), 0, 21), (gen.config5(), None, None)):
+        entry = g.entry if entry is None else entry
+        exit_ = g.exit if exit_ is None else exit_
+        ref = oracle.pp_stats_parallel(g, tp=(entry, exit_), chunk=2)
+        st = tp.test_paths(g, entry, exit_, mode="count").stats
+        assert _gpu_tot(st) == _tot(ref), g.name
