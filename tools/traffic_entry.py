@@ -2,7 +2,7 @@
 `ncu --set full` report (here, no GPU), to profiles/traffic.json -- what bench.py reports as the
 roofline's `traffic` and its issue-slot view.
 
-usage: python tools/traffic_entry.py <rep> <key> <extensions of the launch> <source .md>"""
+usage: python tools/traffic_entry.py <rep> <key> <extensions of the launch> <source .md> [launch index]"""
 import csv
 import io
 import json
@@ -14,7 +14,7 @@ rep, key, ext, src = sys.argv[1], sys.argv[2], float(sys.argv[3]), sys.argv[4]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
-vals = rows[2]  # the first profiled launch
+vals = rows[2 + (int(sys.argv[5]) if len(sys.argv) > 5 else 0)]  # the profiled launch
 d = dict(zip(hdr, vals))
 u = dict(zip(hdr, units))
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
