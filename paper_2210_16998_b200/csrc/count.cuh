@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
             const uint32_t bal = __ballot_sync(kFull, pp);
             if (pp) {
                 const uint32_t j = qn + __popc(bal & ltm);
+                TPG_DCHECK(j < 64, "cnt: warp queue overflow");
                 asm volatile("st.shared.u64 [%0], %1;" ::"r"(qSa + j * 8u), "l"(Sx) : "memory");
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(qLa + j * 4u), "r"(len) : "memory");
             }
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
         }
         const bool to_ring = ((HSH && !CNT_QUEUE) && pp) || ((HX || SEG) && other);
         if (to_ring) {
+            TPG_DCHECK(rc < (uint32_t)RSLOTS, "cnt: event ring overflow");
             asm volatile("st.shared.u64 [%0], %1;" ::"r"(qb + rc * 256u), "l"(Sx) : "memory");
             if constexpr (SEG) asm volatile("st.shared.u64 [%0], %1;" ::"r"(bb + rc * 256u), "l"(Bx) : "memory");
             const uint32_t tag = (pp ? (EK_PP << 29) : (kind << 29)) | ((uint32_t)slot_ << 8) | len;
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 const bool empty = rem == 0;
                 if (act && empty && l == L.r) L.done = true;  // the unit's subtree is finished
                 const bool pop = act && empty && l > L.r;
+                TPG_DCHECK(!act || (l >= L.r && l < PLEV), "cnt: depth out of range");
                 const bool take = act && !empty;
                 const int w = ffs_t(rem);                     // (take) the child
                 const int u = lds_u8(pb + (uint32_t)l * 32u);  // (pop) the vertex popped
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                     }
                 }
                 if (push) {
+                    TPG_DCHECK(l + 1 < PLEV, "cnt: path deeper than the lane's column");
                     if constexpr (RS) sts_u32(rb + (uint32_t)l * 128u, (uint32_t)(rem & (rem - 1)));
                     sts_u8(pb + (uint32_t)(l + 1) * 32u, w);
                 }
