@@ -1358,113 +1358,26 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
 // digests, HeadS records.  (4) head_weight_s: the cross prime paths' counts and vertices.
 // (5) With the digest: items grouped by entry, weighted and scanned; stitch_hash_s hashes
 // every cross prime path from S(h) and the items' (A, B).
-template <class T>
-static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
-    const double t0 = now_ms();
-    tpgen_stats st;
-    memset(&st, 0, sizeof(st));
-    int64_t launches = 0;
+// The count-mode steps after the enumeration (shared by the DFS count kernel and the frontier
+// engine): the completion DP from the items' aggregates, the heads' cross prime paths, the totals,
+// and with the digest the item grouping and the stitch hash of every cross prime path.
+// cseg / cpp: the segment / prime-path phase's totals ([0] paths, [1] vertices, [2] E_canon,
+// [3..4] digest, [5] head slots, [7] item slots).
+static tpgen_status count_post(PlanImpl &P, const tpgen_options &o, const DevGraph &G, cudaStream_t s, bool has_seg,
+                               const unsigned long long *cseg, const unsigned long long *cpp, uint64_t presplit_ext,
+                               tpgen_stats &st, int64_t &launches, Timer &tall, Timer &tst, double ms_dfs, double t0,
+                               tpgen_stats *stp) {
     const HostPlan &H = P.hp;
-    cudaStream_t s = (cudaStream_t)o.stream;
-    int32_t lo = 0, hi = H.n;
-    shard_range(H, o.shard_rank, o.shard_count, lo, hi);
-    if (o.start_hi > o.start_lo) {
-        lo = std::max(0, o.start_lo);
-        hi = std::min(H.n, o.start_hi);
-    }
-    st.shard_lo = lo;
-    st.shard_hi = hi;
-    st.n_scc = H.n_scc;
-    st.n_scc_nontrivial = H.n_nontrivial;
-    st.max_scc = H.max_scc;
-    st.ms_plan = P.ms_plan;
-    P.overflow = false;
-    P.tp_unreachable = false;
-    P.maxgen = 0;
-    const int mode = o.compute_digest ? M_CNT : M_CNT_NOHASH;
-    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;  // host stage marks, synchronised
+    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();
+    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;
     auto HT = [&](const char *what) {
         if (!hdbg) return;
         cudaStreamSynchronize(s);
         fprintf(stderr, "[tpgen count] %-28s %s\n", what, cudaGetErrorString(cudaGetLastError()));
     };
-    Timer tall, tst;
-    cudaEventRecord(tall.a, s);
-    const DevGraph G = dev_graph(P, lo, hi);
-    // roots: one K_NODE unit per start vertex (segment phase: every SCC entry; prime-path phase: the
-    // range's other vertices)
-    std::vector<Unit<1>> seg_roots, pp_roots;
-    for (int32_t v = 0; v < H.n; v++) {
-        const int32_t slot = H.v_slot[v];
-        const bool entry = (H.slot_flags[slot] & F_ENTRY) != 0;
-        if (!entry && !(v >= lo && v < hi)) continue;
-        Unit<1> u;
-        memset(&u, 0, sizeof(u));
-        const int32_t c = H.comp[v];
-        const int loc = slot - H.scc_vbase[c];
-        u.M[0] = 1ull << loc;
-        u.scc = c;
-        u.e = -1;
-        u.kind = K_NODE;
-        u.path[0] = (uint8_t)loc;
-        (entry ? seg_roots : pp_roots).push_back(u);
-    }
-    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
-    TPG_TRY(P.ctr.ensure(32 * 8, s));
-    TPG_TRY(P.agg.ensure(agg_n * 8, s));
-    TPG_TRY(P.agg_bak.ensure(agg_n * 8, s));
-    TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
-    unsigned long long *ctr = P.ctr.as<unsigned long long>();
-    // graphs with no arc leaving any SCC: the host pre-split trie tops (cached per plan and range)
-    RootSpan<1> pp_span(pp_roots);
-    uint64_t presplit_ext = 0;
-    if (std::is_same<T, uint32_t>::value && seg_roots.empty() && !P.any_exit && !getenv("TPGEN_NO_PRESPLIT")) {
-        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_dev.p)) {
-            const int64_t lanes = (int64_t)P.num_sms * CntCfg<uint32_t>::min_blocks * CntCfg<uint32_t>::threads;
-            std::vector<Unit<1>> units;
-            int64_t target = lanes;
-            if (const char *ev = getenv("TPGEN_PRESPLIT_TARGET")) target = atoll(ev);
-            presplit_roots<1>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext);
-            P.presplit_host.assign(reinterpret_cast<const uint8_t *>(units.data()),
-                                   reinterpret_cast<const uint8_t *>(units.data() + units.size()));
-            P.presplit_n = (int64_t)units.size();
-            P.presplit_roots_n = -1;
-            TPG_TRY(upload(P.presplit_dev, P.presplit_host, s));
-            P.presplit_lo = lo;
-            P.presplit_hi = hi;
-        }
-        pp_span = RootSpan<1>(reinterpret_cast<const Unit<1> *>(P.presplit_host.data()), (size_t)P.presplit_n);
-        presplit_ext = P.presplit_ext;
-        P.presplit_active = true;
-    }
-    double ms_dfs = 0;
-    uint64_t tail_seg = 0, tail = 0;
-    unsigned long long cseg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cpp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // (1) segment phase
-    if (!seg_roots.empty())
-        TPG_TRY(dfs_phase<T>(P, G, RootSpan<1>(seg_roots), 1, 0, s, st, launches, ms_dfs, tail_seg, mode, cseg));
-    HT("segment phase");
-    // (3) prime-path phase
-    {
-        double ms_pp = 0;
-        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail, mode, cpp, &ms_pp);
-        P.presplit_active = false;
-        if (r != TPGEN_OK) return r;
-        st.ms_dominant = ms_pp;
-        st.ext_dominant = (int64_t)cpp[2];
-    }
-    if (P.overflow) {
-        set_error("prime-path count exceeds 2^62");
-        return TPGEN_ERR_LIMIT_EXCEEDED;
-    }
-    if (P.tp_unreachable) {
-        set_error("a prime path's first vertex is unreachable from entry or its last cannot reach exit");
-        return TPGEN_ERR_UNREACHABLE;
-    }
-    st.n_units = (int64_t)tail;
-    HT("prime-path phase");
     // (2) completion DP from the items' aggregates
-    if (!seg_roots.empty()) {
+    if (has_seg) {
         const int64_t n_slots = (int64_t)cseg[7];
         unsigned long long *agg = P.agg.as<unsigned long long>();
         if (n_slots > 0) {
@@ -1634,6 +1547,115 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
     return TPGEN_OK;
 }
 
+template <class T>
+static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    int64_t launches = 0;
+    const HostPlan &H = P.hp;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    int32_t lo = 0, hi = H.n;
+    shard_range(H, o.shard_rank, o.shard_count, lo, hi);
+    if (o.start_hi > o.start_lo) {
+        lo = std::max(0, o.start_lo);
+        hi = std::min(H.n, o.start_hi);
+    }
+    st.shard_lo = lo;
+    st.shard_hi = hi;
+    st.n_scc = H.n_scc;
+    st.n_scc_nontrivial = H.n_nontrivial;
+    st.max_scc = H.max_scc;
+    st.ms_plan = P.ms_plan;
+    P.overflow = false;
+    P.tp_unreachable = false;
+    P.maxgen = 0;
+    const int mode = o.compute_digest ? M_CNT : M_CNT_NOHASH;
+    const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;  // host stage marks, synchronised
+    auto HT = [&](const char *what) {
+        if (!hdbg) return;
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[tpgen count] %-28s %s\n", what, cudaGetErrorString(cudaGetLastError()));
+    };
+    Timer tall, tst;
+    cudaEventRecord(tall.a, s);
+    const DevGraph G = dev_graph(P, lo, hi);
+    // roots: one K_NODE unit per start vertex (segment phase: every SCC entry; prime-path phase: the
+    // range's other vertices)
+    std::vector<Unit<1>> seg_roots, pp_roots;
+    for (int32_t v = 0; v < H.n; v++) {
+        const int32_t slot = H.v_slot[v];
+        const bool entry = (H.slot_flags[slot] & F_ENTRY) != 0;
+        if (!entry && !(v >= lo && v < hi)) continue;
+        Unit<1> u;
+        memset(&u, 0, sizeof(u));
+        const int32_t c = H.comp[v];
+        const int loc = slot - H.scc_vbase[c];
+        u.M[0] = 1ull << loc;
+        u.scc = c;
+        u.e = -1;
+        u.kind = K_NODE;
+        u.path[0] = (uint8_t)loc;
+        (entry ? seg_roots : pp_roots).push_back(u);
+    }
+    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
+    TPG_TRY(P.ctr.ensure(32 * 8, s));
+    TPG_TRY(P.agg.ensure(agg_n * 8, s));
+    TPG_TRY(P.agg_bak.ensure(agg_n * 8, s));
+    TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
+    unsigned long long *ctr = P.ctr.as<unsigned long long>();
+    // graphs with no arc leaving any SCC: the host pre-split trie tops (cached per plan and range)
+    RootSpan<1> pp_span(pp_roots);
+    uint64_t presplit_ext = 0;
+    if (std::is_same<T, uint32_t>::value && seg_roots.empty() && !P.any_exit && !getenv("TPGEN_NO_PRESPLIT")) {
+        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_dev.p)) {
+            const int64_t lanes = (int64_t)P.num_sms * CntCfg<uint32_t>::min_blocks * CntCfg<uint32_t>::threads;
+            std::vector<Unit<1>> units;
+            int64_t target = lanes;
+            if (const char *ev = getenv("TPGEN_PRESPLIT_TARGET")) target = atoll(ev);
+            presplit_roots<1>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext);
+            P.presplit_host.assign(reinterpret_cast<const uint8_t *>(units.data()),
+                                   reinterpret_cast<const uint8_t *>(units.data() + units.size()));
+            P.presplit_n = (int64_t)units.size();
+            P.presplit_roots_n = -1;
+            TPG_TRY(upload(P.presplit_dev, P.presplit_host, s));
+            P.presplit_lo = lo;
+            P.presplit_hi = hi;
+        }
+        pp_span = RootSpan<1>(reinterpret_cast<const Unit<1> *>(P.presplit_host.data()), (size_t)P.presplit_n);
+        presplit_ext = P.presplit_ext;
+        P.presplit_active = true;
+    }
+    double ms_dfs = 0;
+    uint64_t tail_seg = 0, tail = 0;
+    unsigned long long cseg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cpp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // (1) segment phase
+    if (!seg_roots.empty())
+        TPG_TRY(dfs_phase<T>(P, G, RootSpan<1>(seg_roots), 1, 0, s, st, launches, ms_dfs, tail_seg, mode, cseg));
+    HT("segment phase");
+    // (3) prime-path phase
+    {
+        double ms_pp = 0;
+        const tpgen_status r = dfs_phase<T>(P, G, pp_span, 0, tail_seg, s, st, launches, ms_dfs, tail, mode, cpp, &ms_pp);
+        P.presplit_active = false;
+        if (r != TPGEN_OK) return r;
+        st.ms_dominant = ms_pp;
+        st.ext_dominant = (int64_t)cpp[2];
+    }
+    if (P.overflow) {
+        set_error("prime-path count exceeds 2^62");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    if (P.tp_unreachable) {
+        set_error("a prime path's first vertex is unreachable from entry or its last cannot reach exit");
+        return TPGEN_ERR_UNREACHABLE;
+    }
+    st.n_units = (int64_t)tail;
+    HT("prime-path phase");
+    return count_post(P, o, G, s, !seg_roots.empty(), cseg, cpp, presplit_ext, st, launches, tall, tst, ms_dfs, t0,
+                      stp);
+}
+
 // ------------------------------------------------------------ frontier engine
 // TPGEN_ENGINE_FRONTIER (frontier.cuh): level-synchronous
 // extension of all paths of one length at a time; counts, E_canon and digest.
@@ -1645,8 +1667,8 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
     const HostPlan &H = P.hp;
-    if (H.max_scc > 64 || H.W != 1 || P.any_exit || H.n >= (1 << 22)) {
-        set_error("the frontier engine needs SCCs of <= 64 vertices and no arc leaving any SCC (use the DFS engine)");
+    if (H.max_scc > 64 || H.W != 1 || H.n >= (1 << 21)) {
+        set_error("the frontier engine needs SCCs of <= 64 vertices (use the DFS engine)");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
     cudaStream_t s = (cudaStream_t)o.stream;
@@ -1668,7 +1690,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     if (!P.f_tab_ok) {
         std::vector<FSlot<T>> tab(n_tab, FSlot<T>{0, 0, 0, 0});
         for (int32_t i = 0; i < H.n; i++)
-            tab[i] = FSlot<T>{(T)H.sin[(size_t)i * W], (T)H.pin[(size_t)i * W], H.slot_gid[i], 0};
+            tab[i] = FSlot<T>{(T)H.sin[(size_t)i * W], (T)H.pin[(size_t)i * W], H.slot_gid[i], H.slot_flags[i]};
         TPG_TRY(upload(P.f_tab, tab, s));
         P.f_tab_ok = true;
     }
@@ -1915,9 +1937,207 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     return TPGEN_OK;
 }
 
+// One frontier pass over a root set for graphs whose arcs leave SCCs: all
+// levels, ping-pong buffers, retried bigger when a level or the head / item buffer overflows.
+// HX: heads (prime-path phase); SEG: the segment phase (items; records carry B).  out[0..4]: the
+// pass's prime paths, vertices, E_canon, digest a, b; *ev_slots: head or item slots reserved.
+template <class T, bool SEG>
+static tpgen_status frontier_pass(PlanImpl &P, const tpgen_options &o, cudaStream_t s, int32_t lo, int32_t hi,
+                                  const std::vector<int32_t> &roots, bool hash, unsigned long long *out,
+                                  unsigned long long *ev_slots, double &ms, int64_t &launches, uint64_t &recs) {
+    const HostPlan &H = P.hp;
+    const int32_t n_roots = (int32_t)(roots.size() / 2);
+    memset(out, 0, 5 * sizeof(unsigned long long));
+    *ev_slots = 0;
+    if (n_roots == 0) return TPGEN_OK;
+    const size_t key_b = 16, s_b = sizeof(T) == 8 ? 8 : 0, b_b = SEG ? 8 : 0;
+    const size_t kRecB = key_b + s_b + b_b;
+    const int Lmax = std::max(H.max_scc, 1);
+    const size_t nctr = 8 + (size_t)Lmax + 2;
+    TPG_TRY(P.f_ctr.ensure((nctr + 8) * 8, s));
+    unsigned long long *ctr = P.f_ctr.as<unsigned long long>();
+    TPG_TRY(upload(P.f_roots, roots, s));
+    P.f_roots_lo = P.f_roots_hi = -1;  // (the no-exit engine's cached root table is gone)
+    double est = 0;
+    for (size_t i = 0; i < (size_t)n_roots; i++) est += H.cost[H.slot_gid[roots[i]]];
+    uint64_t cap = std::max<uint64_t>({1ull << 20, (uint64_t)(est / 4), P.f_cap_hwm + P.f_cap_hwm / 4});
+    if (const char *ev = getenv("TPGEN_FRONTIER_CAP")) cap = std::max<uint64_t>(64, atoll(ev));
+    DevBuf &evb = SEG ? P.citems : P.cheads;
+    const size_t ev_es = SEG ? sizeof(ItemS) : sizeof(HeadS);
+    uint64_t &ev_hwm = SEG ? P.citem_hwm : P.chead_hwm;
+    {
+        const uint64_t want = std::max<uint64_t>(1ull << 20, ev_hwm + ev_hwm / 4 + 256ull * 4096);
+        if (evb.cap < want * ev_es) TPG_TRY(evb.ensure(want * ev_es, s));
+    }
+    const size_t smem = (size_t)std::max(H.n, 1) * sizeof(FSm<T>);
+    const bool ts = smem <= 32 * 1024;
+    void (*const level_k)(FrontierArgs) =
+        ts ? (hash ? frontier_level_kernel<T, true, true, true, SEG> : frontier_level_kernel<T, true, false, true, SEG>)
+           : (hash ? frontier_level_kernel<T, false, true, true, SEG> : frontier_level_kernel<T, false, false, true, SEG>);
+    void (*const root_k)(FrontierArgs, const int32_t *, const int32_t *, int32_t) =
+        hash ? frontier_root_kernel<T, true, true, SEG> : frontier_root_kernel<T, false, true, SEG>;
+    int per_sm = 0;
+    TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_k, kFThreads, ts ? (int)smem : 0));
+    const int grid = P.num_sms * std::max(per_sm, 1);
+    std::vector<unsigned long long> h(nctr + 8);
+    Timer t;
+    for (int attempt = 0; attempt < 24; attempt++) {
+        size_t f = 0, tot = 0;
+        TPG_CK(cudaMemGetInfo(&f, &tot));
+        const uint64_t cap_max = (uint64_t)((double)(f + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / kRecB);
+        if (cap > cap_max) {
+            set_error("frontier level larger than the device memory budget (the DFS-chunked frontier handles "
+                      "graphs without arcs leaving SCCs; use the DFS engine)");
+            return TPGEN_ERR_OUT_OF_MEMORY;
+        }
+        TPG_TRY(P.f_buf0.ensure(cap * kRecB, s));
+        TPG_TRY(P.f_buf1.ensure(cap * kRecB, s));
+        ulonglong2 *buf[2] = {P.f_buf0.as<ulonglong2>(), P.f_buf1.as<ulonglong2>()};
+        uint64_t *bufS[2] = {reinterpret_cast<uint64_t *>(buf[0] + cap), reinterpret_cast<uint64_t *>(buf[1] + cap)};
+        uint64_t *bufB[2] = {reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(buf[0]) + cap * (key_b + s_b)),
+                             reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(buf[1]) + cap * (key_b + s_b))};
+        TPG_CK(cudaMemsetAsync(ctr, 0, (nctr + 8) * 8, s));
+        FrontierArgs A;
+        memset(&A, 0, sizeof(A));
+        A.tab = P.f_tab.p;
+        A.n_tab = std::max(H.n, 1);
+        A.cap = cap;
+        A.lim = ~0ull;
+        A.acc = ctr;
+        A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
+        A.heads = P.cheads.as<HeadS>();
+        A.head_cap = SEG ? 0 : P.cheads.cap / sizeof(HeadS);
+        A.items = P.citems.as<ItemS>();
+        A.item_cap = SEG ? P.citems.cap / sizeof(ItemS) : 0;
+        A.hcnt = ctr + nctr;
+        A.slot_mix = P.d_slot_mix.as<uint64_t>();
+        A.shard_lo = lo;
+        A.shard_hi = hi;
+        cudaEventRecord(t.a, s);
+        A.out = buf[0];
+        A.out_S = bufS[0];
+        A.out_B = bufB[0];
+        A.cnt_out = ctr + 8;
+        A.l = -1;
+        root_k<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(), P.f_roots.as<int32_t>() + n_roots,
+                                                     n_roots);
+        launches++;
+        for (int l = 0; l < Lmax; l++) {
+            A.in = buf[l & 1];
+            A.in_S = bufS[l & 1];
+            A.in_B = bufB[l & 1];
+            A.out = buf[(l + 1) & 1];
+            A.out_S = bufS[(l + 1) & 1];
+            A.out_B = bufB[(l + 1) & 1];
+            A.cnt_in = ctr + 8 + l;
+            A.cnt_out = ctr + 8 + l + 1;
+            A.l = l;
+            level_k<<<grid, kFThreads, ts ? smem : 0, s>>>(A);
+            launches++;
+        }
+        cudaEventRecord(t.b, s);
+        TPG_CK(cudaGetLastError());
+        TPG_CK(cudaMemcpyAsync(h.data(), ctr, (nctr + 8) * 8, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        const unsigned ovf = (unsigned)h[5];
+        uint64_t peak = 0;
+        for (int l = 0; l <= Lmax; l++) peak = std::max<uint64_t>(peak, h[8 + l]);
+        const uint64_t used = h[nctr + (SEG ? 1 : 0)];
+        if (ovf & 2u) {  // head / item buffer: room for all of them
+            ev_hwm = std::max<uint64_t>(ev_hwm, used);
+            TPG_TRY(evb.ensure((used + used / 4 + 256ull * 4096) * ev_es, s));
+        }
+        if (ovf & 1u) cap = std::max<uint64_t>(2 * cap, peak + peak / 4);
+        if (ovf & 3u) continue;
+        float m = 0;
+        cudaEventElapsedTime(&m, t.a, t.b);
+        ms += m;
+        P.f_cap_hwm = std::max<uint64_t>(P.f_cap_hwm, peak);
+        ev_hwm = std::max<uint64_t>(ev_hwm, used);
+        for (int l = 0; l <= Lmax; l++) recs += h[8 + l];
+        for (int q = 0; q < 5; q++) out[q] = h[q];
+        *ev_slots = used;
+        return TPGEN_OK;
+    }
+    set_error("frontier pass could not be sized");
+    return TPGEN_ERR_OUT_OF_MEMORY;
+}
+
+// The frontier engine on graphs whose arcs leave SCCs (COUNT_HASH): the segment phase and the
+// prime-path phase as frontier passes (heads, items), then count_post -- the
+// completion DP, the cross prime paths, the stitch hash -- shared with the count-mode DFS.
+template <class T>
+static tpgen_status run_frontier_seg(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    const HostPlan &H = P.hp;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    int32_t lo = 0, hi = H.n;
+    shard_range(H, o.shard_rank, o.shard_count, lo, hi);
+    if (o.start_hi > o.start_lo) {
+        lo = std::max(0, o.start_lo);
+        hi = std::min(H.n, o.start_hi);
+    }
+    st.shard_lo = lo;
+    st.shard_hi = hi;
+    st.n_scc = H.n_scc;
+    st.n_scc_nontrivial = H.n_nontrivial;
+    st.max_scc = H.max_scc;
+    st.ms_plan = P.ms_plan;
+    P.overflow = false;
+    P.tp_unreachable = false;
+    const int W = H.W;
+    if (!P.f_tab_ok) {
+        std::vector<FSlot<T>> tab(std::max(H.n, 1), FSlot<T>{0, 0, 0, 0});
+        for (int32_t i = 0; i < H.n; i++)
+            tab[i] = FSlot<T>{(T)H.sin[(size_t)i * W], (T)H.pin[(size_t)i * W], H.slot_gid[i], H.slot_flags[i]};
+        TPG_TRY(upload(P.f_tab, tab, s));
+        P.f_tab_ok = true;
+    }
+    // roots (slots, then slot bases): segment phase every SCC entry, prime-path phase the range's others
+    std::vector<int32_t> rs, rp, vs, vp;
+    for (int32_t v = 0; v < H.n; v++) {
+        const int32_t slot = H.v_slot[v];
+        const bool entry = (H.slot_flags[slot] & F_ENTRY) != 0;
+        if (entry) {
+            rs.push_back(slot);
+            vs.push_back(H.scc_vbase[H.comp[v]]);
+        } else if (v >= lo && v < hi) {
+            rp.push_back(slot);
+            vp.push_back(H.scc_vbase[H.comp[v]]);
+        }
+    }
+    rs.insert(rs.end(), vs.begin(), vs.end());
+    rp.insert(rp.end(), vp.begin(), vp.end());
+    const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
+    TPG_TRY(P.ctr.ensure(32 * 8, s));
+    TPG_TRY(P.agg.ensure(agg_n * 8, s));
+    TPG_CK(cudaMemsetAsync(P.agg.p, 0, agg_n * 8, s));
+    const DevGraph G = dev_graph(P, lo, hi);
+    Timer tall, tst;
+    cudaEventRecord(tall.a, s);
+    const bool hash = o.compute_digest != 0;
+    int64_t launches = 0;
+    uint64_t recs = 0;
+    double ms_seg = 0, ms_pp = 0;
+    unsigned long long cseg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cpp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    TPG_TRY((frontier_pass<T, true>(P, o, s, lo, hi, rs, hash, cseg, &cseg[7], ms_seg, launches, recs)));
+    TPG_TRY((frontier_pass<T, false>(P, o, s, lo, hi, rp, hash, cpp, &cpp[5], ms_pp, launches, recs)));
+    if (!hash) cseg[3] = cseg[4] = cpp[3] = cpp[4] = 0;
+    st.n_units = (int64_t)recs;
+    st.ms_dominant = ms_pp;
+    st.ext_dominant = (int64_t)cpp[2];
+    return count_post(P, o, G, s, !rs.empty(), cseg, cpp, 0, st, launches, tall, tst, ms_seg + ms_pp, t0, stp);
+}
+
 tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st) {
     if (o.engine == TPGEN_ENGINE_FRONTIER) {
         memset(out, 0, sizeof(*out));
+        if (P.any_exit && P.hp.max_scc <= 64 && P.hp.n < (1 << 21)) {  // arcs leave SCCs: heads and items
+            if (P.hp.max_scc <= 32) return run_frontier_seg<uint32_t>(P, o, st);
+            return run_frontier_seg<uint64_t>(P, o, st);
+        }
         if (P.hp.max_scc <= 32) return run_frontier<uint32_t>(P, o, st);
         return run_frontier<uint64_t>(P, o, st);
     }

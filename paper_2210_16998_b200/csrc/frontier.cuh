@@ -33,7 +33,7 @@ struct FSlot {        // per SCC slot (local ids ascend with global ids)
     T sin;            // in-SCC successor bits (local)
     T pin;            // in-SCC predecessor bits (local)
     int32_t gid;      // global vertex id
-    int32_t pad;
+    int32_t flags;    // F_EXIT (an arc leaves its SCC), F_ENTRY
 };
 
 // Records.  32-bit masks (SCCs of <= 32 vertices): one 16-byte record
@@ -51,6 +51,17 @@ struct FrontierArgs {
     ulonglong2 *out;             // level l+1 records
     const uint64_t *in_S;        // 64-bit masks: S of the level l records
     uint64_t *out_S;             //               S of the level l+1 records
+    const uint64_t *in_B;        // segment phase: sum of mix(v) of the level l paths (item slopes, R20)
+    uint64_t *out_B;
+    // graphs whose arcs leave SCCs (count modes): heads of the prime-path phase and
+    // items of the segment phase, in warp blocks of 256 slots (holes marked), counted in hcnt[0] / hcnt[1]
+    HeadS *heads;
+    unsigned long long head_cap;
+    ItemS *items;
+    unsigned long long item_cap;
+    unsigned long long *hcnt;
+    const uint64_t *slot_mix;    // per slot mix64(gid) (the segment phase's B sums)
+    int32_t shard_lo, shard_hi;  // segment phase: cycles through entries in this range are counted
     const unsigned long long *cnt_in;
     unsigned long long *cnt_out;
     unsigned long long cap;      // records per buffer
@@ -141,27 +152,108 @@ struct FT<uint64_t> {
     }
 };
 
-// Roots: one record per start vertex of a nontrivial SCC; an isolated vertex
-// (no arc at all in a graph where no arc leaves any SCC) is itself a prime path.
-template <class T, bool HASH>
+// Warp-aggregated event slots (heads, items): the warp takes blocks of 256 slots with one
+// atomic and marks the unused rest of a block (mark(q)) before the next or at the end.
+struct EvBlk {
+    unsigned long long next = 0, end = 0;
+    template <class Mark>
+    __device__ __forceinline__ unsigned long long take(uint32_t bal, unsigned long long *ctr, unsigned long long cap,
+                                                       unsigned int *ovf, Mark mark) {
+        const uint32_t need = __popc(bal);
+        const unsigned lane = threadIdx.x & 31;
+        if (next + need > end) {
+            for (unsigned long long q = next + lane; q < end; q += 32)
+                if (q < cap) mark(q);
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(ctr, 256ull);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            next = b;
+            end = b + 256;
+            if (b + 256 > cap && lane == 0) atomicOr(ovf, 2u);
+        }
+        const unsigned long long q = next + __popc(bal & ((1u << lane) - 1u));
+        next += need;
+        return q;
+    }
+    template <class Mark>
+    __device__ __forceinline__ void close(unsigned long long cap, Mark mark) {
+        for (unsigned long long q = next + (threadIdx.x & 31); q < end; q += 32)
+            if (q < cap) mark(q);
+        next = end;
+    }
+};
+
+__device__ __forceinline__ void put_head(const FrontierArgs &A, EvBlk &hb, bool hd, uint64_t S, uint32_t len,
+                                         int32_t slot) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, hd);
+    if (!bal) return;
+    const unsigned long long q = hb.take(bal, A.hcnt, A.head_cap, A.overflow, [&](unsigned long long i) { A.heads[i].x = -1; });
+    if (hd && q < A.head_cap) {
+        HeadS h;
+        h.S = S;
+        h.len = (int32_t)len;
+        h.x = slot;
+        *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&h);
+    }
+}
+__device__ __forceinline__ void put_item(const FrontierArgs &A, EvBlk &ib, bool it, uint64_t S, uint64_t B,
+                                         uint32_t len, int32_t x, int32_t ent, int32_t last) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, it);
+    if (!bal) return;
+    const unsigned long long q = ib.take(bal, A.hcnt + 1, A.item_cap, A.overflow, [&](unsigned long long i) { A.items[i].ent = -1; });
+    if (it && q < A.item_cap) {
+        ulonglong2 *d = reinterpret_cast<ulonglong2 *>(A.items + q);
+        d[0] = make_ulonglong2(S, B);
+        d[1] = make_ulonglong2((unsigned long long)len | ((unsigned long long)(uint32_t)x << 32),
+                               (unsigned long long)(uint32_t)ent | ((unsigned long long)(uint32_t)last << 32));
+    }
+}
+
+// Roots: one record per start vertex (a child record only if the start has an in-SCC successor).
+// The root's own event: without arcs leaving SCCs an isolated vertex is itself a prime path;
+// with them (HX) a non-entry start is a prime path when it has no arc at all, a head <s> when
+// it is an exit whose predecessors lie on <s>; segment phase (SEG, entry starts): a tail <s>
+// (no successor but itself) or a transit <s> (an exit).
+template <class T, bool HASH, bool HX = false, bool SEG = false>
 __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, const int32_t *root_vb, int32_t n) {
     FAcc f;
     unsigned int write = 0;
     uint32_t s = 0, vb = 0;
-    uint64_t S = 0;
+    uint64_t S = 0, B = 0;
+    bool hd = false, it = false, ex = false;
+    int32_t slot = 0, gid = 0;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        const int32_t slot = root_slot[i];
+        slot = root_slot[i];
         vb = (uint32_t)root_vb[i];
         const FSlot<T> t = static_cast<const FSlot<T> *>(A.tab)[slot];
         s = (uint32_t)slot - vb;
-        S = HASH ? mix64((uint64_t)(uint32_t)t.gid) : 0ull;  // position 0 (weight 1)
-        if (t.sin == 0) {
-            if constexpr (HASH) f.emit(S, 1);
-            else f.pp++, f.vert++;
+        gid = t.gid;
+        const T sbit = (T)1 << s;
+        const uint64_t m = mix64((uint64_t)(uint32_t)t.gid);  // position 0 (weight 1)
+        S = (HASH || HX || SEG) ? m : 0ull;
+        B = m;
+        ex = (HX || SEG) && (t.flags & F_EXIT);
+        if constexpr (SEG) {
+            it = ex || (t.sin & ~sbit) == 0;
         } else {
-            write = 1;
+            if (t.sin == 0 && !ex && (!HX || t.pin == 0)) {
+                if constexpr (HASH) f.emit(S, 1);
+                else f.pp++, f.vert++;
+            }
+            hd = HX && ex && (t.pin & ~sbit) == 0;
         }
+        write = t.sin != 0;
+    }
+    if constexpr (HX && !SEG) {
+        EvBlk hb;
+        put_head(A, hb, hd, S, 1, slot);
+        hb.close(A.head_cap, [&](unsigned long long q) { A.heads[q].x = -1; });
+    }
+    if constexpr (SEG) {
+        EvBlk ib;
+        put_item(A, ib, it, S, B, 1, ex ? slot : -1, gid, slot);
+        ib.close(A.item_cap, [&](unsigned long long q) { A.items[q].ent = -1; });
     }
     const unsigned int lane = threadIdx.x & 31;
     const unsigned int bal = __ballot_sync(0xffffffffu, write);
@@ -170,8 +262,12 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
     base = __shfl_sync(0xffffffffu, base, 0);
     if (write) {
         const unsigned long long j = base + __popc(bal & ((1u << lane) - 1u));
-        if (j < A.cap) FT<T>::template st<HASH>(A, j, (T)1 << s, s, s, vb, S);
-        else atomicOr(A.overflow, 1u);
+        if (j < A.cap) {
+            FT<T>::template st<HASH || HX || SEG>(A, j, (T)1 << s, s, s, vb, S);
+            if constexpr (SEG) A.out_B[j] = B;
+        } else {
+            atomicOr(A.overflow, 1u);
+        }
     }
     f.flush(A.acc);
 }
@@ -181,8 +277,12 @@ __global__ void frontier_root_kernel(FrontierArgs A, const int32_t *root_slot, c
 // reserves the tile's surviving children with ONE atomicAdd (block scan): the
 // record counter is a single address, and one atomic per warp serialised there
 // (1.5 atomics/ns measured: a warp-per-atomic level kernel ran at 1.1 TB/s).
-// TS: slot table in shared memory as {sin, pin, mix(gid) * (2(l+1)+1)} -- the digest
-// term of a vertex at this level's position is computed once per block.
+// TS: slot table in shared memory as {sin, pin, mix(gid) * (2(l+1)+1), flags} -- the
+// digest term of a vertex at this level's position is computed once per block.
+// HX (arcs leave SCCs): an exit child is never an internal prime path; an exit child whose
+// start's predecessors lie on the path is a head segment (HeadS).  SEG (the
+// segment phase, entry starts): cycles are prime paths when the start lies in the call's range,
+// tail / transit segments become ItemS records, the records also carry B = sum of mix(v).
 constexpr int kFThreads = 256;
 constexpr int kFRec = 4;
 constexpr int kFTile = kFThreads * kFRec;
@@ -190,11 +290,14 @@ constexpr int kFTile = kFThreads * kFRec;
 template <class T>
 struct FSm {  // shared-memory slot entry
     T sin, pin;
-    uint64_t mix;  // digest term of the vertex at position l+1: mix64(gid) * (2(l+1) + 1)
+    uint64_t mix;    // digest term of the vertex at position l+1: mix64(gid) * (2(l+1) + 1)
+    int32_t flags;   // F_EXIT, bit 2: the start vertex lies in the call's range (segment phase)
+    int32_t pad;
 };
 
-template <class T, bool TS, bool HASH>
+template <class T, bool TS, bool HASH, bool HX = false, bool SEG = false>
 __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs A) {
+    constexpr bool NEED_S = HASH || HX || SEG;  // heads and items carry their digest sums
     extern __shared__ int4 fsm[];
     FSm<T> *st = reinterpret_cast<FSm<T> *>(fsm);
     const FSlot<T> *tab = static_cast<const FSlot<T> *>(A.tab);
@@ -211,7 +314,8 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
             const FSlot<T> t = tab[i];
-            st[i] = FSm<T>{t.sin, t.pin, mix64((uint64_t)(uint32_t)t.gid) * pw};
+            const int32_t inr = (t.gid >= A.shard_lo && t.gid < A.shard_hi) ? 4 : 0;
+            st[i] = FSm<T>{t.sin, t.pin, mix64((uint64_t)(uint32_t)t.gid) * pw, t.flags | inr, 0};
         }
         __syncthreads();
     }
@@ -227,24 +331,32 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
         if constexpr (TS) return st[i].mix;
         else return mix64((uint64_t)(uint32_t)__ldg(&tab[i].gid)) * pw;
     };
+    auto flagsof = [&](uint32_t i) -> int32_t {
+        if constexpr (TS) return st[i].flags;
+        const int32_t g = __ldg(&tab[i].gid);
+        return __ldg(&tab[i].flags) | ((g >= A.shard_lo && g < A.shard_hi) ? 4 : 0);
+    };
     const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path (every prime path found at this level)
     uint64_t *pq = pqs[warp];
     uint32_t qn = 0;  // queued prime paths (warp-uniform, < 32 between drains)
     FAcc f;
+    EvBlk hblk, iblk;
     int par = 0;
     for (unsigned long long t0 = (unsigned long long)blockIdx.x * kFTile; t0 < n_in;
          t0 += (unsigned long long)gridDim.x * kFTile, par ^= 1) {
         T M[kFRec], keep[kFRec];
         uint32_t sv[kFRec], vb[kFRec];
-        uint64_t S[kFRec];
+        uint64_t S[kFRec], Bv[kFRec];
         ulonglong2 r[kFRec];
 #pragma unroll
         for (int k = 0; k < kFRec; k++) {  // all loads first: kFRec records in flight per thread
             const unsigned long long i = t0 + k * kFThreads + threadIdx.x;
             S[k] = 0;
-            r[k] = i < n_in ? FT<T>::template ld<HASH>(A, i, S[k]) : make_ulonglong2(0, 0);
+            Bv[k] = 0;
+            r[k] = i < n_in ? FT<T>::template ld<NEED_S>(A, i, S[k]) : make_ulonglong2(0, 0);
+            if constexpr (SEG) Bv[k] = i < n_in ? __ldcs(reinterpret_cast<const unsigned long long *>(A.in_B) + i) : 0ull;
         }
         uint32_t nk = 0;
 #pragma unroll
@@ -255,41 +367,58 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
             sv[k] = s;
             keep[k] = 0;
             T cc = 0;
-            bool head_closed = false;
+            bool head_closed = false, emit = true;
+            const T sbit = (T)1 << s;
+            T ps = 0;
             if (i < n_in) {
-                cc = sinof(vb[k] + u) & (~M[k] | ((T)1 << s));
-                head_closed = (pinof(vb[k] + s) & ~M[k]) == 0;  // pred(s) within M = M' \ {w}
-                f.ext += FT<T>::popc(cc);
+                cc = sinof(vb[k] + u) & (~M[k] | sbit);
+                ps = pinof(vb[k] + s);
+                head_closed = (ps & ~M[k]) == 0;  // pred(s) within M = M' \ {w}
+                if constexpr (SEG) emit = (flagsof(vb[k] + s) & 4) != 0;
+                if (emit) f.ext += FT<T>::popc(cc);
             }
             // warp-uniform child loop; prime paths are queued and hashed 32 at a time
             const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)FT<T>::popc(cc));
             for (int it = 0; it < maxc; it++) {
-                bool em = false;
-                uint64_t Sx = 0;
+                bool em = false, hd = false, itm = false, ex = false;
+                uint64_t Sx = 0, Bx = 0;
+                int32_t wsl = 0;
                 if (cc) {
                     const uint32_t w = FT<T>::ffs(cc) - 1;
                     cc &= cc - 1;
-                    const T cw = (w == s) ? (T)0 : (sinof(vb[k] + w) & (~(M[k] | ((T)1 << w)) | ((T)1 << s)));
-                    if (cw) {
-                        keep[k] |= (T)1 << w;
-                    } else if (w == s || head_closed) {  // cycle closure, or an internal prime path
-                        em = true;
-                        if constexpr (HASH) Sx = S[k] + mixof(vb[k] + w);
+                    const T wb = (T)1 << w;
+                    const bool clo = w == s;
+                    const T snw = clo ? (T)0 : sinof(vb[k] + w);
+                    const T cw = snw & (~(M[k] | wb) | sbit);
+                    if constexpr (HX || SEG) ex = (flagsof(vb[k] + w) & F_EXIT) != 0;
+                    if (cw) keep[k] |= wb;
+                    if constexpr (SEG) {
+                        em = clo && emit;
+                        itm = !clo && (ex || (snw & ~(M[k] | wb)) == 0);  // transit, or tail (R8, R9)
+                    } else {
+                        em = !cw && (clo || (head_closed && !ex));  // cycle closure, or an internal prime path
+                        hd = HX && !clo && ex && (ps & ~(M[k] | wb)) == 0;
                     }
+                    wsl = (int32_t)(vb[k] + w);
+                    if constexpr (NEED_S) Sx = S[k] + mixof(vb[k] + w);
+                    if constexpr (SEG) Bx = Bv[k] + __ldg(A.slot_mix + vb[k] + w);
                 }
                 if constexpr (!HASH) {  // counts only
                     if (em) f.pp++, f.vert += len;
-                    continue;
+                } else {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, em);
+                    if (em) pq[qn + __popc(bal & lt)] = Sx;
+                    qn += __popc(bal);
+                    if (qn >= 32) {
+                        __syncwarp();
+                        qn -= 32;
+                        f.emit(pq[qn + lane], len);
+                        __syncwarp();
+                    }
                 }
-                const uint32_t bal = __ballot_sync(0xffffffffu, em);
-                if (em) pq[qn + __popc(bal & lt)] = Sx;
-                qn += __popc(bal);
-                if (qn >= 32) {
-                    __syncwarp();
-                    qn -= 32;
-                    f.emit(pq[qn + lane], len);
-                    __syncwarp();
-                }
+                if constexpr (HX && !SEG) put_head(A, hblk, hd, Sx, len, wsl);
+                if constexpr (SEG)
+                    put_item(A, iblk, itm, Sx, Bx, len, ex ? wsl : -1, __ldg(&tab[vb[k] + s].gid), wsl);
             }
             nk += FT<T>::popc(keep[k]);
         }
@@ -324,8 +453,9 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
                         const uint32_t w = FT<T>::ffs(kp) - 1;
                         kp &= kp - 1;
                         uint64_t Sw = 0;
-                        if constexpr (HASH) Sw = S[k] + mixof(vb[k] + w);
-                        FT<T>::template st<HASH>(A, j, M[k] | ((T)1 << w), w, sv[k], vb[k], Sw);
+                        if constexpr (NEED_S) Sw = S[k] + mixof(vb[k] + w);
+                        FT<T>::template st<NEED_S>(A, j, M[k] | ((T)1 << w), w, sv[k], vb[k], Sw);
+                        if constexpr (SEG) A.out_B[j] = Bv[k] + __ldg(A.slot_mix + vb[k] + w);
                         j++;
                     }
                 }
@@ -333,7 +463,9 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
         }
     }
     __syncwarp();
-    if (lane < qn) f.emit(pq[lane], len);  // the queue's remainder
+    if (HASH && lane < qn) f.emit(pq[lane], len);  // the queue's remainder
+    if constexpr (HX && !SEG) hblk.close(A.head_cap, [&](unsigned long long q) { A.heads[q].x = -1; });
+    if constexpr (SEG) iblk.close(A.item_cap, [&](unsigned long long q) { A.items[q].ent = -1; });
     // block reduction of the accumulators, one set of atomics per block
     unsigned long long v[5] = {f.pp, f.vert, f.ext, f.ha, f.hb};
 #pragma unroll

@@ -123,13 +123,58 @@ def test_frontier_dfs_chunked(monkeypatch):
             _oracle_stats(g), g.name
 
 
-def test_frontier_rejects_non_lean_graphs():
-    for g in (gen.fig1b(), gen.config5(K=2, n=40), gen.from_arcs(70, [(i, (i + 1) % 70) for i in range(70)])):
-        with pytest.raises(tp.TpgenError) as e:
-            _frontier(g)
-        assert e.value.status_name.endswith("INVALID_ARGUMENT")
+def test_frontier_rejects_wide_sccs_and_materialize():
+    with pytest.raises(tp.TpgenError) as e:
+        _frontier(gen.from_arcs(70, [(i, (i + 1) % 70) for i in range(70)]))  # a 70-vertex SCC
+    assert e.value.status_name.endswith("INVALID_ARGUMENT")
     with pytest.raises(tp.TpgenError):
         tp.prime_paths(gen.dense_scc(8, 2, 1), engine="frontier")  # materialize: counts only
+
+
+def _seg_corpus():
+    """Graphs whose arcs leave SCCs: heads, tail / transit items, cross prime paths."""
+    yield gen.fig1b()
+    yield gen.config2()  # (a 71-vertex SCC: skipped below)
+    yield gen.k_seq_loops(5, 4)
+    yield gen.config4(K=30)
+    yield gen.parallel_sccs(3, 24, 9)
+    yield gen.parallel_sccs(2, 40, 3)  # 64-bit masks
+    yield gen.config5(K=2, n=30)
+    rng = np.random.default_rng(29)
+    for i in range(50):
+        n = int(rng.integers(2, 12))
+        yield gen.random_digraph(n, float(rng.choice([0.15, 0.25, 0.35])), 900 + i, self_loops=bool(rng.random() < 0.5))
+
+
+def test_frontier_with_segment_events_matches_oracle():
+    """The frontier engine on graphs whose arcs leave SCCs: the segment phase and
+    the prime-path phase as level-synchronous passes writing items and heads, then the count-mode
+    DP and stitch -- counts, vertices, E_canon and digest equal to the oracle's; counts only too."""
+    for g in _seg_corpus():
+        comp = tp.components(g)[0]
+        if comp.size and np.bincount(comp).max() > 64:
+            continue
+        ref = _oracle_stats(g)
+        assert _frontier(g) == ref, g.name
+        st = tp.prime_paths(g, mode="count", digest=False, engine="frontier").stats
+        assert (st["n_paths"], st["total_vertices"], st["n_extensions"]) == \
+            (ref["n_paths"], ref["total_vertices"], ref["n_extensions"]), g.name
+
+
+@pytest.mark.timeout(1200)
+def test_frontier_config5_full_size():
+    """Config 5 in COUNT_HASH through the frontier engine equals the count-mode DFS (itself equal to
+    the oracle for every start vertex, tests/test_gpu_count.py) and the oracle's totals."""
+    g = gen.config5()
+    ref = oracle.pp_stats_parallel(g, chunk=4)
+    a = ref[:, :4].astype(object)
+    tot = (int(a[:, 0].sum()), int(a[:, 1].sum()), int(a[:, 2].sum()) & ((1 << 64) - 1),
+           int(a[:, 3].sum()) & ((1 << 64) - 1))
+    plan = tp.Plan(g)
+    st = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
+    assert (st["n_paths"], st["total_vertices"], st["hash_lo"], st["hash_hi"]) == tot
+    assert st["n_extensions"] == int(ref[:, 4].sum())
+    plan.close()
 
 
 def test_frontier_config3_full_size():
