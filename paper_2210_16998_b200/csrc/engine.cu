@@ -1777,6 +1777,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
         cudaEventRecord(tall.a, s);
         FrontierArgs A;
+        memset(&A, 0, sizeof(A));
         A.tab = P.f_tab.p;
         A.n_tab = n_tab;
         A.cap = cap;
@@ -1852,12 +1853,20 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         TPG_CK(cudaMemsetAsync(ctr, 0, nctr * 8, s));
         cudaEventRecord(tall.a, s);
         FrontierArgs A;
+        memset(&A, 0, sizeof(A));
         A.tab = P.f_tab.p;
         A.n_tab = n_tab;
         A.cap = capc;
         A.acc = ctr;
         A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
-        std::vector<uint64_t> nl(Lmax + 1, 0), cur(Lmax + 1, 0);
+        if (Lmax + 1 > kFMaxLevels) {
+            set_error("frontier: SCC larger than 64 vertices");
+            return TPGEN_ERR_INVALID_ARGUMENT;
+        }
+        TPG_TRY(P.f_sched.ensure(sizeof(FChunk), s));
+        FChunk *fc = P.f_sched.as<FChunk>();
+        TPG_CK(cudaMemsetAsync(fc, 0, sizeof(FChunk), s));
+        cudaGraphExec_t gexec = nullptr;
         if (n_roots) {
             A.lim = ~0ull;
             A.in = nullptr;
@@ -1871,38 +1880,73 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
                                                                         P.f_roots.as<int32_t>() + n_roots, n_roots);
             launches++;
             TPG_TRY(KC("root", -1));
-            TPG_CK(cudaMemcpyAsync(&nl[0], ctr + 8, 8, cudaMemcpyDeviceToHost, s));
-            TPG_CK(cudaStreamSynchronize(s));
-            recs += nl[0];
-        }
-        const uint64_t chunk = std::max<uint64_t>(1, capc / D);
-        int l = 0;
-        while (l >= 0) {
-            if (cur[l] >= nl[l]) {
-                l--;
-                continue;
-            }
-            const uint64_t k = std::min<uint64_t>(nl[l] - cur[l], chunk);
-            TPG_CK(cudaMemsetAsync(ctr + 8 + l + 1, 0, 8, s));
-            const size_t key_b = (sizeof(T) == 4 && !hash) ? 8 : 16;  // bytes per record in the key array
-            A.in = reinterpret_cast<ulonglong2 *>(reinterpret_cast<char *>(base + (size_t)l * capc) + cur[l] * key_b);
-            A.in_S = baseS + (size_t)l * capc + cur[l];
-            A.out = base + (size_t)(l + 1) * capc;
-            A.out_S = baseS + (size_t)(l + 1) * capc;
-            A.cnt_in = ctr + 8 + l;  // = nl[l] until level l is consumed
-            A.cnt_out = ctr + 8 + l + 1;
-            A.lim = k;
-            A.l = l;
-            level_k<<<grid, kFThreads, lsmem, s>>>(A);
-            launches++;
-            TPG_TRY(KC("chunk level", l));
-            cur[l] += k;
-            if (l + 1 < Lmax) {  // level l+1 records can have children: descend
-                TPG_CK(cudaMemcpyAsync(&nl[l + 1], ctr + 8 + l + 1, 8, cudaMemcpyDeviceToHost, s));
-                TPG_CK(cudaStreamSynchronize(s));
-                recs += nl[l + 1];
-                cur[l + 1] = 0;
-                l++;
+            // the walk over chunks: a graph with one conditional WHILE node whose body is
+            // [frontier_sched_kernel -> frontier_chunk_kernel] (no host round trip per chunk)
+            FSchedArgs sa;
+            sa.c = fc;
+            sa.ctr = ctr;
+            sa.base = base;
+            sa.baseS = baseS;
+            sa.capc = capc;
+            sa.chunk = std::max<uint64_t>(1, capc / D);
+            sa.chunk_div = D;
+            sa.key_b = (sizeof(T) == 4 && !hash) ? 8u : 16u;
+            sa.Lmax = Lmax;
+            void (*const chunk_k)(FrontierArgs, const FChunk *) =
+                ts ? (hash ? frontier_chunk_kernel<T, true, true> : frontier_chunk_kernel<T, true, false>)
+                   : (hash ? frontier_chunk_kernel<T, false, true> : frontier_chunk_kernel<T, false, false>);
+            cudaGraph_t g = nullptr;
+            TPG_CK(cudaGraphCreate(&g, 0));
+            auto build = [&]() -> cudaError_t {
+                cudaGraphConditionalHandle hdl;
+                cudaError_t e = cudaGraphConditionalHandleCreate(&hdl, g, 1, cudaGraphCondAssignDefault);
+                if (e != cudaSuccess) return e;
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = hdl;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t cn;
+                if ((e = cudaGraphAddNode(&cn, g, nullptr, 0, &cp)) != cudaSuccess) return e;
+                cudaGraph_t body = cp.conditional.phGraph_out[0];
+                void *sargs[2] = {&sa, &hdl};
+                cudaKernelNodeParams kp;
+                memset(&kp, 0, sizeof(kp));
+                kp.func = reinterpret_cast<void *>(&frontier_sched_kernel);
+                kp.gridDim = dim3(1);
+                kp.blockDim = dim3(32);
+                kp.kernelParams = sargs;
+                cudaGraphNode_t n_sched, n_lvl;
+                if ((e = cudaGraphAddKernelNode(&n_sched, body, nullptr, 0, &kp)) != cudaSuccess) return e;
+                const FChunk *fcc = fc;
+                void *largs[2] = {&A, &fcc};
+                kp.func = reinterpret_cast<void *>(chunk_k);
+                kp.gridDim = dim3(grid);
+                kp.blockDim = dim3(kFThreads);
+                kp.sharedMemBytes = (unsigned)lsmem;
+                kp.kernelParams = largs;
+                if ((e = cudaGraphAddKernelNode(&n_lvl, body, &n_sched, 1, &kp)) != cudaSuccess) return e;
+                return cudaGraphInstantiate(&gexec, g, 0);
+            };
+            const char *wv = getenv("TPGEN_FRONTIER_WALK");  // A/B hook: "graph" = the conditional-node walk
+            if (wv && strcmp(wv, "graph") == 0) {
+                const cudaError_t be = build();
+                cudaGraphDestroy(g);
+                TPG_CK(be);
+                TPG_CK(cudaGraphLaunch(gexec, s));
+                TPG_TRY(KC("chunk graph", 0));
+            } else {  // one persistent cooperative launch, a grid barrier per chunk
+                cudaGraphDestroy(g);
+                void (*const walk_k)(FrontierArgs, FSchedArgs) =
+                    ts ? (hash ? frontier_walk_kernel<T, true, true> : frontier_walk_kernel<T, true, false>)
+                       : (hash ? frontier_walk_kernel<T, false, true> : frontier_walk_kernel<T, false, false>);
+                int wper = 0;
+                TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, walk_k, kFThreads, lsmem));
+                const int wgrid = P.num_sms * std::max(wper, 1);
+                void *wargs[2] = {&A, &sa};
+                TPG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(walk_k), dim3(wgrid), dim3(kFThreads), wargs,
+                                                   lsmem, s));
+                TPG_TRY(KC("chunk walk", 0));
             }
         }
         cudaEventRecord(tall.b, s);
@@ -1910,6 +1954,15 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
         TPG_CK(cudaMemcpyAsync(h.data(), ctr, nctr * 8, cudaMemcpyDeviceToHost, s));
         TPG_CK(cudaStreamSynchronize(s));
         cudaEventElapsedTime(&ms, tall.a, tall.b);
+        if (n_roots) {
+            if (gexec) cudaGraphExecDestroy(gexec);
+            FChunk hc;
+            TPG_CK(cudaMemcpy(&hc, fc, sizeof(FChunk), cudaMemcpyDeviceToHost));
+            recs += hc.recs;
+            const char *wv = getenv("TPGEN_FRONTIER_WALK");
+            launches += (wv && strcmp(wv, "graph") == 0) ? 2 * (int64_t)(hc.steps + 1) : 1;  // (sched + level per pass)
+            st.n_count_rounds = (int32_t)hc.steps;     // chunks
+        }
         if (h[5] & 1u) {
             set_error("frontier chunk overflow (internal)");
             return TPGEN_ERR_INTERNAL;

@@ -66,6 +66,8 @@ struct FrontierArgs {
     unsigned long long *cnt_out;
     unsigned long long cap;      // records per buffer
     unsigned long long lim;      // records of the input to process (chunked mode), ~0 = all
+    unsigned long long ring;     // chunked walk: the output is a ring of `ring` records, appends start at
+    unsigned long long ring_off; //   ring_off (0 = a flat buffer; cap then bounds the appends)
     unsigned long long *acc;     // [0] prime paths, [1] vertices, [2] extensions, [3] digest a, [4] digest b
     unsigned int *overflow;
     int32_t l;                   // input paths have l + 1 vertices
@@ -124,7 +126,7 @@ struct FT<uint32_t> {
     template <bool HASH>
     __device__ static void st(const FrontierArgs &A, unsigned long long j, uint32_t M, uint32_t w, uint32_t s,
                               uint32_t vb, uint64_t S) {
-        TPG_DCHECK(j < A.cap, "frontier: record write beyond the level buffer");
+        TPG_DCHECK(j < (A.ring ? A.ring : A.cap), "frontier: record write beyond the level buffer");
         if constexpr (HASH) __stcs(A.out + j, make_ulonglong2(fkey(M, w, s, vb), S));
         else __stcs(reinterpret_cast<unsigned long long *>(A.out) + j, (unsigned long long)fkey(M, w, s, vb));
     }
@@ -295,22 +297,18 @@ struct FSm {  // shared-memory slot entry
     int32_t pad;
 };
 
-template <class T, bool TS, bool HASH, bool HX = false, bool SEG = false>
-__global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs A) {
+template <class T, bool TS, bool HASH, bool HX, bool SEG>
+__device__ __forceinline__ void frontier_level_body(const FrontierArgs &A, FAcc &f, unsigned int vblk) {
     constexpr bool NEED_S = HASH || HX || SEG;  // heads and items carry their digest sums
     extern __shared__ int4 fsm[];
     FSm<T> *st = reinterpret_cast<FSm<T> *>(fsm);
     const FSlot<T> *tab = static_cast<const FSlot<T> *>(A.tab);
     __shared__ uint32_t wsum[2][kFThreads / 32];
     __shared__ unsigned long long bbase[2];
-    __shared__ unsigned long long red[5][kFThreads / 32];
     __shared__ uint64_t pqs[kFThreads / 32][64];  // per warp: digest sums S of prime paths awaiting their hash
     const uint64_t pw = pos_weight((uint32_t)(A.l + 1));  // digest weight of the new vertex's position
-    // once a level has overflowed the attempt is discarded (the call retries bigger or goes
-    // chunked): the buffer holds unwritten gaps, so no later level reads it
-    if (*reinterpret_cast<volatile const unsigned int *>(A.overflow) & 1u) return;
-    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);
-    if ((unsigned long long)blockIdx.x * kFTile >= n_in) return;  // small levels: idle blocks leave at once
+    const unsigned long long n_in = min(min(A.cnt_in ? *A.cnt_in : ~0ull, A.cap), A.lim);
+    if ((unsigned long long)vblk * kFTile >= n_in) return;
     if constexpr (TS) {
         for (int i = threadIdx.x; i < A.n_tab; i += blockDim.x) {
             const FSlot<T> t = tab[i];
@@ -341,10 +339,9 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     const uint32_t len = (uint32_t)A.l + 2;  // vertices of a child path (every prime path found at this level)
     uint64_t *pq = pqs[warp];
     uint32_t qn = 0;  // queued prime paths (warp-uniform, < 32 between drains)
-    FAcc f;
     EvBlk hblk, iblk;
     int par = 0;
-    for (unsigned long long t0 = (unsigned long long)blockIdx.x * kFTile; t0 < n_in;
+    for (unsigned long long t0 = (unsigned long long)vblk * kFTile; t0 < n_in;
          t0 += (unsigned long long)gridDim.x * kFTile, par ^= 1) {
         T M[kFRec], keep[kFRec];
         uint32_t sv[kFRec], vb[kFRec];
@@ -454,8 +451,13 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
                         kp &= kp - 1;
                         uint64_t Sw = 0;
                         if constexpr (NEED_S) Sw = S[k] + mixof(vb[k] + w);
-                        FT<T>::template st<NEED_S>(A, j, M[k] | ((T)1 << w), w, sv[k], vb[k], Sw);
-                        if constexpr (SEG) A.out_B[j] = Bv[k] + __ldg(A.slot_mix + vb[k] + w);
+                        unsigned long long jj = j;  // ring buffer (the chunked walk): wrap the append index
+                        if (A.ring) {
+                            jj += A.ring_off;
+                            if (jj >= A.ring) jj -= A.ring;
+                        }
+                        FT<T>::template st<NEED_S>(A, jj, M[k] | ((T)1 << w), w, sv[k], vb[k], Sw);
+                        if constexpr (SEG) A.out_B[jj] = Bv[k] + __ldg(A.slot_mix + vb[k] + w);
                         j++;
                     }
                 }
@@ -466,7 +468,12 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
     if (HASH && lane < qn) f.emit(pq[lane], len);  // the queue's remainder
     if constexpr (HX && !SEG) hblk.close(A.head_cap, [&](unsigned long long q) { A.heads[q].x = -1; });
     if constexpr (SEG) iblk.close(A.item_cap, [&](unsigned long long q) { A.items[q].ent = -1; });
-    // block reduction of the accumulators, one set of atomics per block
+}
+
+// Block reduction of the accumulators, one set of atomics per block.
+__device__ __forceinline__ void frontier_flush(const FrontierArgs &A, const FAcc &f) {
+    __shared__ unsigned long long red[5][kFThreads / 32];
+    const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long v[5] = {f.pp, f.vert, f.ext, f.ha, f.hb};
 #pragma unroll
     for (int q = 0; q < 5; q++) {
@@ -480,6 +487,210 @@ __global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs 
 #pragma unroll
         for (int x = 0; x < kFThreads / 32; x++) a += red[threadIdx.x][x];
         if (a || threadIdx.x >= 3) atomicAdd(A.acc + threadIdx.x, a);
+    }
+}
+
+template <class T, bool TS, bool HASH, bool HX = false, bool SEG = false>
+__global__ void __launch_bounds__(kFThreads) frontier_level_kernel(FrontierArgs A) {
+    // once a level has overflowed the attempt is discarded (the call retries bigger or goes
+    // chunked): the buffer holds unwritten gaps, so no later level reads it
+    if (*reinterpret_cast<volatile const unsigned int *>(A.overflow) & 1u) return;
+    const unsigned long long n_in = min(min(*A.cnt_in, A.cap), A.lim);
+    if ((unsigned long long)blockIdx.x * kFTile >= n_in) return;  // small levels: idle blocks leave at once
+    FAcc f;
+    frontier_level_body<T, TS, HASH, HX, SEG>(A, f, blockIdx.x);
+    frontier_flush(A, f);
+}
+
+// DFS-chunked frontier, scheduled on the device: a CUDA graph whose
+// conditional WHILE node runs [frontier_sched_kernel -> frontier_chunk_kernel] until the walk
+// over chunks of levels ends, so no chunk waits for a host round trip.  FChunk is the walk's
+// state (cur / nl: records consumed / produced per level) plus the next chunk's parameters.
+constexpr int kFMaxLevels = 66;  // levels 0..64 (masks of <= 64 vertices) + 1
+struct FChunk {
+    const ulonglong2 *in;
+    const uint64_t *in_S;
+    ulonglong2 *out;
+    uint64_t *out_S;
+    unsigned long long lim;     // records of level l to process
+    int32_t l;                  // the chunk's level
+    int32_t done;               // the walk has ended (the body's level launch returns at once)
+    int32_t started;
+    int32_t pad;
+    unsigned long long steps;   // chunks scheduled
+    unsigned long long recs;    // records written over all levels
+    unsigned long long cur[kFMaxLevels], nl[kFMaxLevels];
+    unsigned long long oc[3][kFMaxLevels];  // persistent walk: step t's appends to level l: oc[t % 3][l]
+    unsigned long long bar;     // persistent walk: grid-barrier arrivals
+};
+struct FSchedArgs {
+    FChunk *c;
+    unsigned long long *ctr;    // ctr[8 + l]: records written to level l's buffer
+    ulonglong2 *base;           // level l's key array at base + l * capc (16-byte stride)
+    uint64_t *baseS;            // level l's S array at baseS + l * capc (64-bit masks)
+    unsigned long long capc;    // records per level buffer
+    unsigned long long chunk;   // records per chunk (capc / the largest out-degree)
+    unsigned long long chunk_div;  // the largest out-degree D (a chunk of k records has <= k * D children)
+    uint32_t key_b;             // bytes per record in the key array (8: u32 masks, counts only)
+    int32_t Lmax;
+};
+
+// One thread: account for the chunk that just ran, pick the next one (the deepest level with
+// unconsumed records), or end the while loop.
+__global__ void frontier_sched_kernel(FSchedArgs a, cudaGraphConditionalHandle h) {
+    if (threadIdx.x != 0) return;
+    FChunk &c = *a.c;
+    int l;
+    if (!c.started) {
+        c.started = 1;
+        c.nl[0] = a.ctr[8];
+        c.cur[0] = 0;
+        c.recs = c.nl[0];
+        l = 0;
+    } else {
+        l = c.l;
+        c.cur[l] += c.lim;
+        if (l + 1 < a.Lmax) {  // level l+1's records can have children: descend
+            c.nl[l + 1] = a.ctr[8 + l + 1];
+            c.cur[l + 1] = 0;
+            c.recs += c.nl[l + 1];
+            l++;
+        }
+    }
+    while (l >= 0 && c.cur[l] >= c.nl[l]) l--;
+    if (l < 0) {
+        c.done = 1;
+        cudaGraphSetConditional(h, 0);
+        return;
+    }
+    const unsigned long long k = min(c.nl[l] - c.cur[l], a.chunk);
+    a.ctr[8 + l + 1] = 0;
+    c.in = reinterpret_cast<const ulonglong2 *>(reinterpret_cast<const char *>(a.base + (size_t)l * a.capc) +
+                                                c.cur[l] * a.key_b);
+    c.in_S = a.baseS + (size_t)l * a.capc + c.cur[l];
+    c.out = a.base + (size_t)(l + 1) * a.capc;
+    c.out_S = a.baseS + (size_t)(l + 1) * a.capc;
+    c.lim = k;
+    c.l = l;
+    c.steps++;
+}
+
+// The level kernel on the chunk FChunk names (cnt_in = ctr[8 + l] >= lim, so lim bounds it).
+template <class T, bool TS, bool HASH>
+__global__ void __launch_bounds__(kFThreads) frontier_chunk_kernel(FrontierArgs A, const FChunk *c) {
+    const FChunk *cv = c;
+    if (*reinterpret_cast<volatile const int32_t *>(&cv->done)) return;
+    FrontierArgs B = A;
+    B.in = cv->in;
+    B.in_S = cv->in_S;
+    B.out = cv->out;
+    B.out_S = cv->out_S;
+    B.lim = cv->lim;
+    B.l = cv->l;
+    B.cnt_in = A.acc + 8 + B.l;
+    B.cnt_out = A.acc + 8 + B.l + 1;
+    if ((unsigned long long)blockIdx.x * kFTile >= B.lim) return;
+    FAcc f;
+    frontier_level_body<T, TS, HASH, false, false>(B, f, blockIdx.x);
+    frontier_flush(A, f);
+}
+
+// The DFS-chunked frontier as ONE persistent launch (grid = the co-resident blocks), a
+// wavefront over the levels: in each step EVERY level with pending records takes a chunk of
+// them -- as many as its child level's free space / D guarantees room for (D = the largest
+// out-degree) -- so the walk needs about (records / buffer space) steps, not one step per chunk
+// of one level.  Level l's buffer is filled from its start (tail[l]) and consumed in order
+// (head[l]); an empty buffer restarts at 0.  The deepest level with pending records always has
+// an empty (restarted) child buffer, so every step makes progress.  Every block keeps its own
+// copy of head / tail and takes the same decisions from the same counters; a step ends at a
+// grid barrier.  Step t's appends to level l are counted in oc[t % 3][l]; block 0 zeroes
+// oc[(t + 1) % 3] during step t (last read right after the barrier that ended step t - 2).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <class T, bool TS, bool HASH>
+__global__ void __launch_bounds__(kFThreads) frontier_walk_kernel(FrontierArgs A, FSchedArgs sa) {
+    __shared__ unsigned long long head[kFMaxLevels], tail[kFMaxLevels], take[kFMaxLevels];
+    __shared__ unsigned long long s_cnt[kFMaxLevels];
+    FChunk *c = sa.c;
+    const int Lm = sa.Lmax;
+    for (int i = threadIdx.x; i < kFMaxLevels; i += blockDim.x) head[i] = tail[i] = take[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) tail[0] = *reinterpret_cast<volatile unsigned long long *>(sa.ctr + 8);
+    __syncthreads();
+    unsigned long long recs = tail[0], step = 0;
+    FAcc f;  // accumulated over all steps, flushed once
+    for (;;) {
+        // plan the step (thread 0; the same decisions in every block).  head / tail count records
+        // consumed / appended since the start; a level's buffer is a ring of capc records.
+        if (threadIdx.x == 0) {
+            bool any = false;
+            for (int l = 0; l < Lm; l++) {
+                const unsigned long long pend = tail[l] - head[l];
+                any |= pend != 0;
+                unsigned long long k = min(pend, sa.capc - head[l] % sa.capc);  // (a chunk does not wrap)
+                if (l + 1 < Lm) k = min(k, (sa.capc - (tail[l + 1] - head[l + 1])) / sa.chunk_div);
+                take[l] = k;
+            }
+            take[kFMaxLevels - 1] = any;
+        }
+        __syncthreads();
+        if (!take[kFMaxLevels - 1]) break;
+        if (blockIdx.x == 0)
+            for (int i = threadIdx.x; i < kFMaxLevels; i += blockDim.x) c->oc[(step + 1) % 3][i] = 0;
+        unsigned int rot = 0;  // tiles of the step's earlier levels: level l's first tile goes to the next block
+        for (int l = 0; l < Lm; l++) {
+            const unsigned long long k = take[l];
+            if (k == 0) continue;
+            const unsigned int vblk = (blockIdx.x + gridDim.x - rot % gridDim.x) % gridDim.x;
+            rot += (unsigned int)((k + kFTile - 1) / kFTile);
+            if ((unsigned long long)vblk * kFTile >= k) continue;  // no tile of this level for this block
+            FrontierArgs B = A;
+            const unsigned long long h0 = head[l] % sa.capc;
+            B.in = reinterpret_cast<const ulonglong2 *>(reinterpret_cast<const char *>(sa.base + (size_t)l * sa.capc) +
+                                                        h0 * sa.key_b);
+            B.in_S = sa.baseS + (size_t)l * sa.capc + h0;
+            // (level Lm - 1 has no children: level Lm's buffer is never written)
+            B.out = sa.base + (size_t)(l + 1) * sa.capc;
+            B.out_S = sa.baseS + (size_t)(l + 1) * sa.capc;
+            B.ring = sa.capc;
+            B.ring_off = tail[l + 1] % sa.capc;
+            B.cap = sa.capc - (tail[l + 1] - head[l + 1]);  // free records of the ring
+            B.lim = k;
+            B.l = l;
+            B.cnt_in = nullptr;  // (lim bounds the input)
+            B.cnt_out = &c->oc[step % 3][l + 1];
+            frontier_level_body<T, TS, HASH, false, false>(B, f, vblk);
+            __syncthreads();  // (the body's shared memory is reused by the next level)
+        }
+        // grid barrier: every block's children of this step are written and counted
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(&c->bar, 1ull);
+            const unsigned long long target = (unsigned long long)gridDim.x * (step + 1);
+            while (ld_acquire_u64(&c->bar) < target) __nanosleep(32);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i <= Lm; i += blockDim.x)
+            s_cnt[i] = *reinterpret_cast<volatile unsigned long long *>(&c->oc[step % 3][i]);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int l = 0; l < Lm; l++) {
+                head[l] += take[l];
+                if (l + 1 < Lm) tail[l + 1] += s_cnt[l + 1];
+            }
+        for (int l = 1; l < Lm; l++) recs += s_cnt[l];
+        step++;
+        __syncthreads();
+    }
+    frontier_flush(A, f);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c->recs = recs;
+        c->steps = step;
     }
 }
 

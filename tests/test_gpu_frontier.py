@@ -60,7 +60,7 @@ def test_frontier_wide_masks_chunked(monkeypatch):
     monkeypatch.setenv("TPGEN_FRONTIER_CHUNK", "512")
     g = gen.dense_scc(36, 2, 3)
     st = tp.prime_paths(g, mode="count", digest=True, engine="frontier").stats
-    assert st["gpu_launches"] > st["max_scc"] + 1
+    assert st["n_count_rounds"] > st["max_scc"] + 1  # chunks (one persistent launch walks them)
     assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
             "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == _oracle_stats(g)
 
@@ -108,16 +108,19 @@ def test_frontier_overflow_retry(monkeypatch):
     plan.close()
 
 
-def test_frontier_dfs_chunked(monkeypatch):
+@pytest.mark.parametrize("walk", ["persistent", "graph"])
+def test_frontier_dfs_chunked(monkeypatch, walk):
     """The DFS-chunked frontier (level buffers of a few hundred records, chunks of
     capacity / out-degree records, each level drained before its parent's next chunk)
-    gives the oracle's counts, E_canon and digest."""
+    gives the oracle's counts, E_canon and digest -- walked by the persistent kernel (one
+    grid barrier per chunk) and by the CUDA-graph WHILE loop (scheduler + level launch)."""
     monkeypatch.setenv("TPGEN_FRONTIER_CHUNK", "256")
+    monkeypatch.setenv("TPGEN_FRONTIER_WALK", walk)
     for g in (gen.dense_scc(13, 3, 11), gen.dense_scc(16, 3, 5),
               gen.disjoint_union([gen.dense_scc(9, 3, 60), gen.from_arcs(2, [(0, 1), (1, 0)]),
                                   gen.from_arcs(1, [])], name="chunk-union")):
         st = tp.prime_paths(g, mode="count", digest=True, engine="frontier").stats
-        assert st["gpu_launches"] > st["max_scc"] + 1  # more than one chunk per level
+        assert st["n_count_rounds"] > st["max_scc"] + 1  # more than one chunk per level
         assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"],
                 "n_extensions": st["n_extensions"], "digest": (st["hash_lo"], st["hash_hi"])} == \
             _oracle_stats(g), g.name
@@ -194,7 +197,7 @@ def test_frontier_config3_full_size():
         c = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
     finally:
         del os.environ["TPGEN_FRONTIER_CHUNK"]
-    assert c["gpu_launches"] > 100
+    assert c["n_count_rounds"] > 20 and c["gpu_launches"] <= 3  # wavefront steps walked inside one launch
     for k in ("n_paths", "total_vertices", "n_extensions", "hash_lo", "hash_hi"):
         assert c[k] == f[k], k
     n = plan.prime_paths(mode="count", digest=False, engine="frontier").stats  # counts only
@@ -222,4 +225,4 @@ def test_frontier_memory_budget_switches_to_chunks(monkeypatch):
     got = {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"], "n_extensions": st["n_extensions"],
            "digest": (st["hash_lo"], st["hash_hi"])}
     assert got == ref
-    assert st["gpu_launches"] > 40  # many chunk launches, not one per level
+    assert st["n_count_rounds"] > 40  # many chunks, not one per level
