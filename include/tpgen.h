@@ -62,8 +62,8 @@ typedef enum {
 
 enum { TPGEN_OUT_MATERIALIZE = 0, TPGEN_OUT_COUNT_HASH = 1 };
 enum { TPGEN_TP_PER_PP = 0, TPGEN_TP_GREEDY = 1 };
-/* Enumeration engine (tpgen_options.engine; DESIGN.md §6.6). */
-enum { TPGEN_ENGINE_DFS = 0, TPGEN_ENGINE_FRONTIER = 1 };
+/* Enumeration engine (tpgen_options.engine; DESIGN.md §6.6, §6.8). */
+enum { TPGEN_ENGINE_DFS = 0, TPGEN_ENGINE_FRONTIER = 1, TPGEN_ENGINE_ALG3 = 2 };
 
 /* Canonical flat path array (see conventions). */
 typedef struct {
@@ -105,17 +105,27 @@ typedef struct {
     int32_t engine;            /* TPGEN_ENGINE_DFS (default): depth-first walk, on-chip path stacks, every
                                   output mode.  TPGEN_ENGINE_FRONTIER: level-synchronous frontier extension
                                   (Alg. 4 ExtendPath applied to every simple path of length l at once,
-                                  P:459-472; the north-star's level-by-level kernel): 16-byte path records
+                                  P:459-472; the north-star's level-by-level kernel): path records
                                   {visited mask, last, first, position-keyed digest sum} streamed through HBM,
-                                  ping-pong buffers, warp-scan compaction.  Requires output_mode =
-                                  TPGEN_OUT_COUNT_HASH (counts, E_canon and -- with compute_digest = 1 --
-                                  the digest; compute_digest = 0 drops the digest sum from the records:
-                                  8-byte records, no mixing; the order-free frontier never materializes
-                                  the canonical list) and a graph whose SCCs
-                                  have <= 64 vertices with no arc leaving any SCC (else
-                                  TPGEN_ERR_INVALID_ARGUMENT).  A level that does not fit in the device
-                                  memory budget switches the call to the DFS-chunked frontier (DESIGN.md
-                                  §6.6); TPGEN_ERR_OUT_OF_MEMORY only when even one chunk cannot fit. */
+                                  ping-pong buffers, block-scan compaction; on graphs with arcs leaving SCCs
+                                  the levels also write head segments and (for SCC entries) transit / tail
+                                  segments, stitched by the same completion DP as the DFS count mode.
+                                  Requires output_mode = TPGEN_OUT_COUNT_HASH (counts, E_canon and -- with
+                                  compute_digest = 1 -- the digest; compute_digest = 0 drops the digest sum
+                                  from the records of graphs without arcs leaving SCCs) and SCCs of <= 64
+                                  vertices (else TPGEN_ERR_INVALID_ARGUMENT).  Without arcs leaving SCCs, a
+                                  level that does not fit in the device memory budget switches the call to
+                                  the DFS-chunked frontier; TPGEN_ERR_OUT_OF_MEMORY when
+                                  even one chunk cannot fit, or (graphs with arcs leaving SCCs) a level does
+                                  not fit.  TPGEN_ENGINE_ALG3: the paper's vertex-centric self-stabilizing
+                                  algorithm (Alg. 1-4) as a comparison engine -- one cooperative
+                                  launch, one CTA per vertex owning the list of the simple paths ending at
+                                  it, every simple path of the graph held in HBM at once; COUNT_HASH
+                                  only, no shards or start ranges, graphs of <= 128 vertices (and <= the
+                                  SM count), else TPGEN_ERR_INVALID_ARGUMENT; TPGEN_ERR_OUT_OF_MEMORY when
+                                  the lists do not fit.  Its n_extensions is the number of ExtendPath calls
+                                  (every simple path of >= 2 vertices), equal to E_canon on strongly
+                                  connected graphs. */
     int32_t no_plan_cache;     /* one-shot calls (tpgen_prime_paths / tpgen_test_paths) keep the last graph's plan
                                   and device tables per device and reuse them when the next call passes a
                                   byte-identical CSR; 1 = always plan and upload anew (what an end-to-end timing of a
@@ -236,6 +246,25 @@ tpgen_status tpgen_plan_classify(tpgen_plan *plan, const tpgen_paths *prime_path
 tpgen_status tpgen_plan_test_paths(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t entry, int32_t exit,
                                    const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats);
 void tpgen_plan_destroy(tpgen_plan *plan);
+
+/* Out-degree-2 normalization (Fig. 5: "we can convert a vertex v with an out-degree
+ * greater than 2 ... to a vertex with out-degree 2 by adding some new intermediate vertices between
+ * v and its successor vertices"; the figure itself is not in the text -- DESIGN.md R24 reads it as a
+ * chain).  A vertex v with successors w1 < ... < wd, d > 2, keeps the arcs v -> w1 and v -> x1;
+ * the new vertex x_i (i = 1..d-2) has the arcs x_i -> w_{i+1} and x_i -> x_{i+1}, and x_{d-2}
+ * has x_{d-2} -> w_{d-1}, x_{d-2} -> w_d.  New vertices are numbered n, n+1, ... in order of v,
+ * then i.  Every other vertex and arc is kept.  Host-only (the graph is KB-sized).
+ *   csr_offsets / csr_targets / n_vertices: the input CSR (host, borrowed; validated like
+ *     tpgen_prime_paths: TPGEN_ERR_INVALID_GRAPH on decreasing offsets, out-of-range targets or
+ *     duplicate arcs in a row; NULL pointers with n_vertices > 0 -> TPGEN_ERR_INVALID_ARGUMENT).
+ *   *out_n, *out_m: set to the normalized vertex and arc counts (always, when non-NULL).
+ *   out_offsets (out_n + 1 entries), out_targets (out_m), origin (out_n: the input vertex whose
+ *     successor list each vertex splits; itself for the input's vertices): caller-owned host
+ *     arrays, filled when non-NULL (call once with NULLs to size them).  Successor lists of the
+ *     result are ascending. */
+tpgen_status tpgen_normalize_outdeg2(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                                     int32_t *out_n, int64_t *out_m, int64_t *out_offsets, int32_t *out_targets,
+                                     int32_t *origin);
 
 #ifdef __cplusplus
 }

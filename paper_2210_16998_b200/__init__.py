@@ -160,10 +160,13 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
     return o
 
 
+_ENGINES = {"dfs": _abi.ENGINE_DFS, "frontier": _abi.ENGINE_FRONTIER, "alg3": _abi.ENGINE_ALG3}
+
+
 def _engine(engine: str) -> int:
-    if engine not in ("dfs", "frontier"):
-        raise ValueError(f"engine must be 'dfs' or 'frontier', not {engine!r}")
-    return _abi.ENGINE_FRONTIER if engine == "frontier" else _abi.ENGINE_DFS
+    if engine not in _ENGINES:
+        raise ValueError(f"engine must be one of {sorted(_ENGINES)}, not {engine!r}")
+    return _ENGINES[engine]
 
 
 def _stream_handle(device: int, stream):
@@ -219,8 +222,10 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
     """All prime paths of ``graph`` (Def. 1), canonical order.
 
     ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host).
-    ``engine``: "dfs" (default) or "frontier" (level-synchronous, ``mode="count"`` only;
-    include/tpgen.h TPGEN_ENGINE_FRONTIER).  ``plan_cache=False``: plan and upload the graph
+    ``engine``: "dfs" (default), "frontier" (level-synchronous, ``mode="count"`` only;
+    include/tpgen.h TPGEN_ENGINE_FRONTIER) or "alg3" (the paper's vertex-centric
+    self-stabilizing Alg. 3 as a comparison engine, ``mode="count"``, <= 128 vertices;
+    TPGEN_ENGINE_ALG3).  ``plan_cache=False``: plan and upload the graph
     anew even if the previous call passed the same CSR (tpgen_options.no_plan_cache)."""
     lib = library()
     _engine(engine)
@@ -302,6 +307,35 @@ def shard_range(graph, rank: int, count: int) -> Tuple[int, int]:
     lo, hi = ctypes.c_int32(), ctypes.c_int32()
     _check(lib.tpgen_shard_range(_p64(so), _p32(st), n, rank, count, ctypes.byref(lo), ctypes.byref(hi)))
     return int(lo.value), int(hi.value)
+
+
+@dataclass
+class CSRGraph:
+    """A CSR graph returned by the library (host arrays)."""
+    n: int
+    offsets: np.ndarray
+    targets: np.ndarray
+    origin: np.ndarray  # normalize_outdeg2: the input vertex each vertex stands for
+    name: str = ""
+
+
+def normalize_outdeg2(graph) -> CSRGraph:
+    """Out-degree-2 normalization (``tpgen_normalize_outdeg2``, host C++; PAPER.md P:272-290,
+    Fig. 5): every vertex with d > 2 successors w1 < ... < wd keeps v -> w1 and gets a chain of
+    d - 2 new vertices x_i -> w_{i+1}, x_{i+1} (the last one -> w_{d-1}, w_d)."""
+    lib = library()
+    so, st, n = _csr(graph)
+    N, M = ctypes.c_int32(), ctypes.c_int64()
+    z = ctypes.POINTER(ctypes.c_int64)()
+    _check(lib.tpgen_normalize_outdeg2(_p64(so), _p32(st), n, ctypes.byref(N), ctypes.byref(M), z,
+                                       ctypes.POINTER(ctypes.c_int32)(), ctypes.POINTER(ctypes.c_int32)()))
+    off = np.zeros(N.value + 1, dtype=np.int64)
+    tgt = np.zeros(max(M.value, 1), dtype=np.int32)
+    org = np.zeros(max(N.value, 1), dtype=np.int32)
+    _check(lib.tpgen_normalize_outdeg2(_p64(so), _p32(st), n, ctypes.byref(N), ctypes.byref(M), _p64(off),
+                                       _p32(tgt), _p32(org)))
+    return CSRGraph(int(N.value), off, tgt[:M.value], org[:N.value],
+                    name=getattr(graph, "name", "graph") + "-outdeg2")
 
 
 NPATH_STATUS = {0: "exact", 1: "saturated at 2^62", 2: "not computed (cyclic, search budget exceeded)"}

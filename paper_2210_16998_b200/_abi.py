@@ -20,6 +20,7 @@ OUT_MATERIALIZE = 0
 OUT_COUNT_HASH = 1
 ENGINE_DFS = 0
 ENGINE_FRONTIER = 1
+ENGINE_ALG3 = 2
 
 ALLOC_FN = CFUNCTYPE(c_void_p, c_size_t, c_void_p, c_void_p)
 FREE_FN = CFUNCTYPE(None, c_void_p, c_void_p, c_void_p)
@@ -78,6 +79,8 @@ SYMBOLS = {
                                   POINTER(c_int32)]),
     "tpgen_metrics_compute": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32,
                                       POINTER(Metrics)]),
+    "tpgen_normalize_outdeg2": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, POINTER(c_int32),
+                                        POINTER(c_int64), POINTER(c_int64), POINTER(c_int32), POINTER(c_int32)]),
     "tpgen_plan_create": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, POINTER(Options),
                                   POINTER(c_void_p)]),
     "tpgen_plan_prime_paths": (c_int, [c_void_p, POINTER(Options), POINTER(Paths), POINTER(Stats)]),

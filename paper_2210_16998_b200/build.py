@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtpgen.so")
-SOURCES = ["engine.cu", "planner.cpp", "abi.cpp", "tpcover.cpp"]
+SOURCES = ["engine.cu", "planner.cpp", "abi.cpp", "tpcover.cpp", "normalize.cpp"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

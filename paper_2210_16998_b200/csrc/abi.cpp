@@ -36,12 +36,16 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("bad output_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
-    if (o.engine != TPGEN_ENGINE_DFS && o.engine != TPGEN_ENGINE_FRONTIER) {
+    if (o.engine != TPGEN_ENGINE_DFS && o.engine != TPGEN_ENGINE_FRONTIER && o.engine != TPGEN_ENGINE_ALG3) {
         tpg::set_error("bad engine");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
-    if (o.engine == TPGEN_ENGINE_FRONTIER && o.output_mode != TPGEN_OUT_COUNT_HASH) {
-        tpg::set_error("the frontier engine computes counts and the digest only (output_mode COUNT_HASH)");
+    if (o.engine != TPGEN_ENGINE_DFS && o.output_mode != TPGEN_OUT_COUNT_HASH) {
+        tpg::set_error("the frontier and Alg. 3 engines compute counts and the digest only (output_mode COUNT_HASH)");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (o.engine == TPGEN_ENGINE_ALG3 && (o.shard_count > 1 || o.start_hi > o.start_lo)) {
+        tpg::set_error("the Alg. 3 engine has no start-vertex shards (every vertex list is global)");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
     if (o.tp_mode != TPGEN_TP_PER_PP && o.tp_mode != TPGEN_TP_GREEDY) {

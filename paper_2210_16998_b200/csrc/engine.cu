@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "expand.cuh"
 #include "frontier.cuh"
+#include "alg3.cuh"
 #include "count.cuh"
 #include "engine.h"
 
@@ -129,7 +130,7 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan,
-                               &f_tab, &f_roots, &f_buf0, &f_buf1, &f_ctr};
+                               &f_tab, &f_roots, &f_buf0, &f_buf1, &f_ctr, &f_sched, &a3_lists, &a3_aux};
     for (int c = 0; c < kCnt; c++) v.push_back(&qcnt[c]);
     return v;
 }
@@ -2184,7 +2185,175 @@ static tpgen_status run_frontier_seg(PlanImpl &P, const tpgen_options &o, tpgen_
     return count_post(P, o, G, s, !rs.empty(), cseg, cpp, 0, st, launches, tall, tst, ms_seg + ms_pp, t0, stp);
 }
 
+// TPGEN_ENGINE_ALG3 (alg3.cuh): the paper's vertex-centric self-stabilizing
+// algorithm (Alg. 1-4) as a comparison engine: one cooperative launch, one CTA per vertex.
+template <int W>
+static tpgen_status run_alg3(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    const double t0 = now_ms();
+    tpgen_stats st;
+    memset(&st, 0, sizeof(st));
+    const HostPlan &H = P.hp;
+    const int32_t n = H.n;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    st.n_scc = H.n_scc;
+    st.n_scc_nontrivial = H.n_nontrivial;
+    st.max_scc = H.max_scc;
+    st.ms_plan = P.ms_plan;
+    st.shard_lo = 0;
+    st.shard_hi = n;
+    if (n == 0) {
+        if (stp) *stp = st;
+        return TPGEN_OK;
+    }
+    // host tables: successor / predecessor CSR (global ids), arc map, predecessor sets, B(v)
+    std::vector<int64_t> aux64;
+    const size_t n1 = (size_t)n + 1, m = (size_t)H.m;
+    std::vector<int32_t> pidx(m);
+    for (int32_t v = 0; v < n; v++)
+        for (int64_t k = H.po[v]; k < H.po[v + 1]; k++) {
+            const int32_t u = H.pt[k];
+            int64_t e = H.so[u];
+            while (e < H.so[u + 1] && H.st[e] != v) e++;
+            pidx[k] = (int32_t)e;
+        }
+    std::vector<uint64_t> pinm((size_t)n * W, 0), back((size_t)n * W, 0);
+    for (int32_t v = 0; v < n; v++)
+        for (int64_t k = H.po[v]; k < H.po[v + 1]; k++) pinm[(size_t)v * W + (H.pt[k] >> 6)] |= 1ull << (H.pt[k] & 63);
+    for (int32_t v = 0; v < n; v++) {  // B(v): backward BFS
+        uint64_t *b = &back[(size_t)v * W];
+        std::vector<int32_t> q{v};
+        b[v >> 6] |= 1ull << (v & 63);
+        for (size_t i = 0; i < q.size(); i++)
+            for (int64_t k = H.po[q[i]]; k < H.po[q[i] + 1]; k++) {
+                const int32_t x = H.pt[k];
+                if (!((b[x >> 6] >> (x & 63)) & 1ull)) {
+                    b[x >> 6] |= 1ull << (x & 63);
+                    q.push_back(x);
+                }
+            }
+    }
+    // one device block: po, so (int64) | pt, sv, pidx (int32) | pinm, back (u64) | count, consumed, cursor, part
+    const size_t off_so = n1 * 8, off_pt = off_so + n1 * 8, off_sv = off_pt + std::max<size_t>(m, 1) * 4,
+                 off_pidx = off_sv + std::max<size_t>(m, 1) * 4;
+    const size_t off_pinm = (off_pidx + std::max<size_t>(m, 1) * 4 + 7) / 8 * 8, off_back = off_pinm + (size_t)n * W * 8,
+                 off_cnt = off_back + (size_t)n * W * 8, off_cons = off_cnt + (size_t)n * 8,
+                 off_cur = off_cons + (size_t)n * 8, off_part = off_cur + std::max<size_t>(m, 1) * 8,
+                 aux_b = off_part + (size_t)n * 64;
+    std::vector<uint8_t> hb(aux_b, 0);
+    memcpy(hb.data(), H.po.data(), n1 * 8);
+    memcpy(hb.data() + off_so, H.so.data(), n1 * 8);
+    if (m) {
+        memcpy(hb.data() + off_pt, H.pt.data(), m * 4);
+        memcpy(hb.data() + off_sv, H.st.data(), m * 4);
+        memcpy(hb.data() + off_pidx, pidx.data(), m * 4);
+    }
+    memcpy(hb.data() + off_pinm, pinm.data(), (size_t)n * W * 8);
+    memcpy(hb.data() + off_back, back.data(), (size_t)n * W * 8);
+    TPG_TRY(P.a3_aux.ensure(aux_b, s));
+    uint8_t *ad = P.a3_aux.as<uint8_t>();
+    TPG_CK(cudaMemcpyAsync(ad, hb.data(), aux_b, cudaMemcpyHostToDevice, s));
+    TPG_CK(cudaStreamSynchronize(s));  // (hb is pageable and goes out of scope)
+    // list capacity: from the plan's extension estimate (every simple path of an SCC-only graph),
+    // doubled on overflow within the device-memory budget
+    const size_t rec_b = 8 * W + 8 + 4 + 1;
+    double est = 0;
+    for (int32_t v = 0; v < n; v++) est += H.cost[v];
+    unsigned long long cap = std::max<unsigned long long>(4096, (unsigned long long)(1.25 * est / n));
+    if (const char *ev = getenv("TPGEN_ALG3_CAP")) cap = std::max<unsigned long long>(16, strtoull(ev, nullptr, 10));
+    int dev_sms = P.num_sms;
+    if (n > dev_sms) {
+        set_error("the Alg. 3 engine runs one co-resident CTA per vertex: at most one vertex per SM");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    Timer t;
+    float ms = 0;
+    std::vector<unsigned long long> part((size_t)n * 8);
+    int64_t launches = 0;
+    for (int attempt = 0;; attempt++) {
+        size_t fr = 0, tot = 0;
+        TPG_CK(cudaMemGetInfo(&fr, &tot));
+        if ((double)cap * n * rec_b > 0.85 * (double)(fr + P.a3_lists.cap)) {
+            set_error("Alg. 3 path lists exceed the device memory (every simple path is held at once, P:330)");
+            return TPGEN_ERR_OUT_OF_MEMORY;
+        }
+        const size_t nt = (size_t)n * cap;
+        TPG_TRY(P.a3_lists.ensure_exact(nt * rec_b, s));
+        uint8_t *L = P.a3_lists.as<uint8_t>();
+        A3Args a;
+        a.n = n;
+        a.cap = cap;
+        a.po = reinterpret_cast<const int64_t *>(ad);
+        a.so = reinterpret_cast<const int64_t *>(ad + off_so);
+        a.pt = reinterpret_cast<const int32_t *>(ad + off_pt);
+        a.sv = reinterpret_cast<const int32_t *>(ad + off_sv);
+        a.pidx = reinterpret_cast<const int32_t *>(ad + off_pidx);
+        a.vmix = P.d_vmix.as<uint64_t>();
+        a.pinm = reinterpret_cast<const uint64_t *>(ad + off_pinm);
+        a.back = reinterpret_cast<const uint64_t *>(ad + off_back);
+        a.mask = reinterpret_cast<uint64_t *>(L);
+        a.S = reinterpret_cast<uint64_t *>(L + nt * 8 * W);
+        a.meta = reinterpret_cast<uint32_t *>(L + nt * (8 * W + 8));
+        a.ext = L + nt * (8 * W + 12);
+        a.count = reinterpret_cast<unsigned long long *>(ad + off_cnt);
+        a.consumed = reinterpret_cast<unsigned long long *>(ad + off_cons);
+        a.cursor = reinterpret_cast<unsigned long long *>(ad + off_cur);
+        a.part = reinterpret_cast<unsigned long long *>(ad + off_part);
+        TPG_CK(cudaMemsetAsync(ad + off_cnt, 0, aux_b - off_cnt, s));
+        cudaEventRecord(t.a, s);
+        void *args[1] = {&a};
+        TPG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(&alg3_kernel<W>), dim3(n), dim3(kA3Threads), args, 0,
+                                           s));
+        launches++;
+        cudaEventRecord(t.b, s);
+        TPG_CK(cudaMemcpyAsync(part.data(), ad + off_part, (size_t)n * 64, cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        bool ovf = false;
+        for (int32_t v = 0; v < n; v++) ovf |= part[(size_t)v * 8 + 5] != 0;
+        if (!ovf) break;
+        st.n_count_rounds = attempt + 1;
+        cap *= 2;
+    }
+    unsigned long long pp = 0, vert = 0, ha = 0, hbb = 0, recs = 0;
+    for (int32_t v = 0; v < n; v++) {
+        pp += part[(size_t)v * 8 + 0];
+        vert += part[(size_t)v * 8 + 1];
+        ha += part[(size_t)v * 8 + 2];
+        hbb += part[(size_t)v * 8 + 3];
+        recs += part[(size_t)v * 8 + 4];
+    }
+    st.n_paths = (int64_t)pp;
+    st.total_vertices = (int64_t)vert;
+    st.n_extensions = (int64_t)(recs - (unsigned long long)n);  // every record but the n initial <v> is one ExtendPath
+    if (o.compute_digest) {
+        st.hash_lo = ha;
+        st.hash_hi = hbb;
+    }
+    st.n_units = (int64_t)recs;
+    st.ms_device = ms;
+    st.ms_count = ms;
+    st.ms_dominant = ms;
+    st.ext_dominant = st.n_extensions;
+    st.gpu_launches = launches;
+    st.ms_total = now_ms() - t0;
+    if ((o.max_paths > 0 && st.n_paths > o.max_paths) || (o.max_extensions > 0 && st.n_extensions > o.max_extensions)) {
+        set_error("result exceeds max_paths / max_extensions");
+        return TPGEN_ERR_LIMIT_EXCEEDED;
+    }
+    if (stp) *stp = st;
+    return TPGEN_OK;
+}
+
 tpgen_status run_prime_paths(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *st) {
+    if (o.engine == TPGEN_ENGINE_ALG3) {
+        memset(out, 0, sizeof(*out));
+        if (P.hp.n > 128) {
+            set_error("the Alg. 3 engine needs graphs of <= 128 vertices (one CTA and one mask bit per vertex)");
+            return TPGEN_ERR_INVALID_ARGUMENT;
+        }
+        if (P.hp.n <= 64) return run_alg3<1>(P, o, st);
+        return run_alg3<2>(P, o, st);
+    }
     if (o.engine == TPGEN_ENGINE_FRONTIER) {
         memset(out, 0, sizeof(*out));
         if (P.any_exit && P.hp.max_scc <= 64 && P.hp.n < (1 << 21)) {  // arcs leave SCCs: heads and items

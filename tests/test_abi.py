@@ -21,7 +21,7 @@ from paper_2210_16998_b200 import _abi
 def _declared_functions():
     src = open(os.path.join(ROOT, "include", "tpgen.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = set(re.findall(r"\b(tpgen_[a-z_]+)\s*\(", src))
+    names = set(re.findall(r"\b(tpgen_[a-z0-9_]+)\s*\(", src))
     return {n for n in names if not n.endswith("_fn")}
 
 

@@ -1,0 +1,107 @@
+"""GPU parity of the paper's vertex-centric, self-stabilizing Alg. 3 as a comparison engine
+(TPGEN_ENGINE_ALG3, csrc/alg3.cuh): counts, total vertices and the order-free
+digest of the PPs left in the per-vertex lists vs the oracle (expected values from oracle/ only),
+and E_canon on strongly connected graphs (Alg. 3 extends every simple path once)."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import generators as gen
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2210_16998_b200")
+
+
+def _alg3(g, **kw):
+    st = tp.prime_paths(g, mode="count", digest=True, engine="alg3", **kw).stats
+    return st, {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"], "digest": (st["hash_lo"], st["hash_hi"])}
+
+
+def _oracle(g):
+    ro, rv = oracle.prime_paths(g)
+    return {"n_paths": len(ro) - 1, "total_vertices": int(ro[-1]), "digest": oracle.digest(ro, rv)}
+
+
+def _strongly_connected(g):
+    lab = np.asarray(oracle.scc_labels(g))
+    return g.n > 0 and len(np.unique(lab)) == 1
+
+
+def _corpus():
+    yield gen.fig1b()
+    yield gen.from_arcs(1, [(0, 0)])
+    yield gen.from_arcs(3, [])
+    rng = np.random.default_rng(5)
+    for i in range(30):
+        yield gen.random_digraph(int(rng.integers(1, 12)), float(rng.choice([0.15, 0.3, 0.45])), 700 + i,
+                                 self_loops=bool(i % 3 == 0))
+    for n, d, seed in ((8, 3, 1), (12, 3, 2), (14, 4, 3), (16, 3, 4)):
+        yield gen.dense_scc(n, d, seed)
+    for n in (63, 64, 65, 100, 128):  # one- and two-word masks
+        arcs = [(i, (i + 1) % n) for i in range(n)] + [(0, n // 2), (n // 3, n // 8), (3 * n // 4, n // 5)]
+        yield gen.from_arcs(n, arcs, name=f"ring{n}")
+    yield gen.disjoint_union([gen.dense_scc(6, 2, 9), gen.dense_scc(7, 3, 10), gen.from_arcs(2, [(0, 1)])],
+                             name="alg3-union")
+
+
+def test_alg3_matches_oracle():
+    for g in _corpus():
+        st, got = _alg3(g)
+        assert got == _oracle(g), g.name
+        assert st["gpu_launches"] >= 1
+        if _strongly_connected(g):
+            assert st["n_extensions"] == oracle.ext_count(g), g.name
+
+
+def test_alg3_on_normalized_graphs():
+    """Fig. 5's out-degree-2 inputs (tpgen_normalize_outdeg2), the shape Alg. 3 was written for."""
+    for g in (gen.dense_scc(10, 4, 7), gen.dense_scc(14, 4, 3), gen.from_arcs(5, [(0, 1), (0, 2), (0, 3), (0, 4),
+                                                                                    (4, 0), (3, 3), (2, 0)])):
+        h = tp.normalize_outdeg2(g)
+        assert np.all(np.diff(h.offsets) <= 2)
+        st, got = _alg3(h)
+        assert got == _oracle(h), h.name
+
+
+def test_alg3_capacity_retry(monkeypatch):
+    """Per-vertex lists far too small for the graph (TPGEN_ALG3_CAP): the call overflows, doubles
+    the capacity and reruns until every simple path fits; the result is unchanged."""
+    monkeypatch.setenv("TPGEN_ALG3_CAP", "32")
+    g = gen.dense_scc(12, 3, 2)
+    st, got = _alg3(g)
+    assert st["n_count_rounds"] >= 3
+    assert got == _oracle(g)
+
+
+@pytest.mark.timeout(900)
+def test_alg3_config3_full_size():
+    """Config 3 (22 vertices, one SCC, 1.4e8 simple paths held in the lists at once): the whole
+    list's n_paths, total vertices, digest and E_canon equal to the oracle's."""
+    g = gen.config3()
+    ref = oracle.pp_stats_parallel(g, chunk=1)
+    st, got = _alg3(g)
+    assert got["n_paths"] == int(ref[:, 0].sum())
+    assert got["total_vertices"] == int(ref[:, 1].sum())
+    assert got["digest"] == (int(ref[:, 2].sum()) % (1 << 64), int(ref[:, 3].sum()) % (1 << 64))
+    assert st["n_extensions"] == int(ref[:, 4].sum())
+
+
+@pytest.mark.timeout(900)
+def test_alg3_config3_normalized_vs_dfs():
+    """Config 3 normalized to out-degree 2 (66 vertices, two-word masks): Alg. 3 and the DFS
+    engine's COUNT_HASH mode agree (the DFS engine is pinned to the oracle elsewhere)."""
+    h = tp.normalize_outdeg2(gen.config3())
+    st, got = _alg3(h)
+    d = tp.prime_paths(h, mode="count", digest=True).stats
+    assert got == {"n_paths": d["n_paths"], "total_vertices": d["total_vertices"], "digest": (d["hash_lo"], d["hash_hi"])}
+    assert st["n_extensions"] == d["n_extensions"]
+
+
+def test_alg3_rejections():
+    with pytest.raises(Exception):
+        tp.prime_paths(gen.from_arcs(129, [(i, i + 1) for i in range(128)]), mode="count", engine="alg3")
+    with pytest.raises(Exception):
+        tp.prime_paths(gen.fig1b(), engine="alg3")  # materialize: not an Alg. 3 mode
+    with pytest.raises(Exception):
+        tp.prime_paths(gen.fig1b(), mode="count", engine="alg3", shard=(0, 2))
