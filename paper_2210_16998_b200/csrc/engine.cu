@@ -868,9 +868,16 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
 template <int NPW, bool HASH>
 static void launch_fast(const ExpandArgs &E, int64_t nu, int num_sms, bool mixed, cudaStream_t s) {
     constexpr int th = FastCfg<NPW>::threads;
+    constexpr size_t sm = FastCfg<NPW>::smem_bytes(HASH);  // (double-buffered bulk-store stages: > 48 KB)
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(expand_fast_kernel<NPW, HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(expand_fast_kernel<NPW, HASH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
     const int g = grid_for(nu * 32, th, num_sms * 2048 / th);
-    if (mixed) expand_fast_kernel<NPW, HASH, true><<<g, th, 0, s>>>(E);
-    else expand_fast_kernel<NPW, HASH, false><<<g, th, 0, s>>>(E);
+    if (mixed) expand_fast_kernel<NPW, HASH, true><<<g, th, sm, s>>>(E);
+    else expand_fast_kernel<NPW, HASH, false><<<g, th, sm, s>>>(E);
 }
 template <bool HASH>
 static void launch_fast_npw(int npw, const ExpandArgs &E, int64_t nu, int num_sms, bool mixed, cudaStream_t s) {

@@ -51,6 +51,23 @@ __device__ __forceinline__ void st_global_cs(int32_t *p, int v) {
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// TMA bulk copy shared -> global (cp.async.bulk, SASS UBLKCP): 16-byte aligned ends, a
+// multiple of 16 bytes; tracked in bulk groups of the issuing thread.
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the bulk groups issued before the last `n` have finished reading their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the async proxy (the bulk copy's reads)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // Output cursors of one unit (canonical exclusive offsets, advanced as records are replayed).
 struct Cursor {
     uint64_t pp, vv, it, itv, hd, hdv;
@@ -264,6 +281,11 @@ template <int NPW>
 struct FastCfg {
     static constexpr int threads = (NPW > 8) ? 128 : 256;
     static constexpr int max_out = 4 * NPW + 1;  // output vertices per path (incl. the closing vertex)
+    // ints per warp stage: HASH, each lane's path bytes; else one batch's vertices + the 16-byte phase shift
+    static constexpr int stage_ints(bool hash) { return hash ? 32 * NPW : (32 * max_out + 4 + 3) / 4 * 4; }
+    static constexpr size_t smem_bytes(bool hash) {
+        return (size_t)(threads / 32) * (hash ? 1 : 2) * stage_ints(hash) * sizeof(int32_t);
+    }
 };
 
 __device__ __forceinline__ uint32_t lop_merge(uint32_t mine, uint32_t other, uint32_t mask) {
@@ -301,10 +323,15 @@ template <int NPW, bool HASH, bool MIXED>
 __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(ExpandArgs A) {
     constexpr int kWarps = FastCfg<NPW>::threads / 32;
     // one batch of paths (HASH: each lane's path bytes, NPW words)
-    constexpr int kStage = HASH ? 32 * NPW : 32 * FastCfg<NPW>::max_out;
-    __shared__ __align__(16) int32_t stage_all[kWarps][kStage];
+    // (!HASH: two stages per warp, each shifted by the output offset's alignment -- up to 3 ints --
+    // so that the middle of a batch leaves with one TMA bulk store while the next batch is staged)
+    constexpr int kStage = FastCfg<NPW>::stage_ints(HASH);
+    constexpr int kBufs = HASH ? 1 : 2;
+    extern __shared__ __align__(16) int32_t stage_dyn[];  // [kWarps][kBufs][kStage] (launch_fast sizes it)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t *stage = stage_all[wid];
+    int32_t *const stage_w = stage_dyn + (size_t)wid * kBufs * kStage;
+    int32_t *stage = stage_w;
+    int sbuf = 0;  // the stage the next batch fills
     const DevGraph &G = A.G;
     const Unit<1> *units = reinterpret_cast<const Unit<1> *>(A.units);
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -433,21 +460,35 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 TPG_DCHECK(cu.pp + __popc(em) <= A.lim[C_PP] && cu.vv + (uint64_t)T <= A.lim[C_VERT],
                            "expand: batch out of range");
                 if (emit) A.out_off[cu.pp + __popc(em & lt_mask)] = (int64_t)(cu.vv + (uint64_t)ex);
-                // ---- stage the vertices (global ids), then stream them out coalesced
+                // ---- stage the vertices (global ids) at the output's 16-byte phase, then the
+                // aligned middle leaves in ONE bulk store (TMA), the <= 3 + 3 ragged ends per lane
+                if (T == 0) continue;
+                const int al = (int)(cu.vv & 3);
+                int32_t *stg = stage_w + sbuf * kStage + al;
+                if (lane == 0) bulk_wait_read<1>();  // this stage's previous bulk store has read it
+                __syncwarp();
                 if (ga >= 0) {
 #pragma unroll
                     for (int p = 0; p < 4 * NPW; p++)
-                        if (p < tot) stage[ex + p] = ga + (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
+                        if (p < tot) stg[ex + p] = ga + (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff);
                 } else {
 #pragma unroll
                     for (int p = 0; p < 4 * NPW; p++)
-                        if (p < tot) stage[ex + p] = __ldg(G.slot_gid + vb + (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff));
+                        if (p < tot) stg[ex + p] = __ldg(G.slot_gid + vb + (int)((D[p >> 2] >> (8 * (p & 3))) & 0xff));
                 }
-                if (len < tot) stage[ex + len] = s0g;  // closing vertex of a cycle (after the byte loop)
+                if (len < tot) stg[ex + len] = s0g;  // closing vertex of a cycle (after the byte loop)
+                fence_proxy_async_smem();
                 __syncwarp();
                 int32_t *dst = A.out_vert + cu.vv;
-                for (int i = lane; i < T; i += 32) st_global_cs(dst + i, stage[i]);
-                __syncwarp();
+                const int h = min(T, (4 - al) & 3);           // ints before the first 16-byte boundary
+                const int nb = ((T - h) >> 2) << 2;           // the aligned middle
+                if (lane < h) st_global_cs(dst + lane, stg[lane]);
+                if (lane < T - h - nb) st_global_cs(dst + h + nb + lane, stg[h + nb + lane]);
+                if (lane == 0) {  // one bulk group per batch (empty without a middle): wait_read<1> counts batches
+                    if (nb > 0) bulk_store(dst + h, stg + h, (uint32_t)nb * 4u);
+                    bulk_commit();
+                }
+                sbuf ^= 1;
                 cu.pp += (uint64_t)__popc(em);
                 cu.vv += (uint64_t)T;
             } else {
@@ -542,6 +583,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
         }
     }
     if (HASH) flush_hash(A, acc);
+    if (!HASH && lane == 0) bulk_wait_all();  // (the stages must outlive the bulk stores' reads)
 }
 
 }  // namespace tpg
