@@ -61,7 +61,7 @@ typedef enum {
 } tpgen_status;
 
 enum { TPGEN_OUT_MATERIALIZE = 0, TPGEN_OUT_COUNT_HASH = 1 };
-enum { TPGEN_TP_PER_PP = 0, TPGEN_TP_GREEDY = 1 };
+enum { TPGEN_TP_PER_PP = 0, TPGEN_TP_UNIQUE = 1, TPGEN_TP_GREEDY = 2 };
 /* Enumeration engine (tpgen_options.engine). */
 enum { TPGEN_ENGINE_DFS = 0, TPGEN_ENGINE_FRONTIER = 1, TPGEN_ENGINE_ALG3 = 2 };
 
@@ -90,9 +90,12 @@ typedef struct {
                                     with shard_count > 1: TPGEN_ERR_INVALID_ARGUMENT */
     int64_t max_paths;         /* 0 = unlimited */
     int64_t max_extensions;    /* 0 = unlimited */
-    int32_t tp_mode;           /* TPGEN_TP_PER_PP: one TP per PP, aligned; TPGEN_TP_GREEDY: greedy cover --
-                                  longest uncovered PP first (ties lexicographic), extended by the R15 walks,
-                                  every PP contained in it covered */
+    int32_t tp_mode;           /* TPGEN_TP_PER_PP: one TP per PP, aligned; TPGEN_TP_UNIQUE (K7, SURVEY §8(a)
+                                  a6): the set of distinct per-PP TPs ("the set of TPs covering all PPs",
+                                  P:269) in lexicographic order of the int32 sequences -- materialized output
+                                  only (COUNT_HASH: TPGEN_ERR_INVALID_ARGUMENT); TPGEN_TP_GREEDY: greedy cover
+                                  -- longest uncovered PP first (ties lexicographic), extended by the R15
+                                  walks, every PP contained in it covered */
     int32_t compute_digest;    /* 1: fill stats->hash_lo/hi (extra pass over the output) */
     tpgen_alloc_fn device_alloc;  /* output allocator; NULL -> cudaMallocAsync */
     tpgen_free_fn device_free;

@@ -241,6 +241,20 @@ def test_paths(g, offsets: np.ndarray, vertices: np.ndarray, entry: int, exit: i
     return np.asarray(out_off, dtype=np.int64), np.asarray(out_v, dtype=np.int32)
 
 
+def unique_test_paths(g, offsets: np.ndarray, vertices: np.ndarray, entry: int, exit: int
+                      ) -> Tuple[np.ndarray, np.ndarray]:
+    """K7: the distinct test paths of ``test_paths`` -- "the set of TPs
+    covering all PPs" -- in lexicographic order of the vertex sequences
+    (R14: Python's list order, a proper prefix first)."""
+    to, tv = test_paths(g, offsets, vertices, entry, exit)
+    tps = sorted({tuple(tv[to[i]:to[i + 1]].tolist()) for i in range(len(to) - 1)})
+    out_off = np.zeros(len(tps) + 1, dtype=np.int64)
+    for i, t in enumerate(tps):
+        out_off[i + 1] = out_off[i] + len(t)
+    out_v = np.array([x for t in tps for x in t], dtype=np.int32)
+    return out_off, out_v
+
+
 def _contains(t, q) -> bool:
     """q is a contiguous subsequence of t (plain scan)."""
     m = len(q)

@@ -241,7 +241,8 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
 def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *, device: int = 0,
                output: str = "device", stream=None, cover: str = "per_pp", mode: str = "materialize") -> PathSet:
     """Entry->exit test paths (R15): one per prime path,
-    aligned with the prime-path list (cover="per_pp"), or the greedy cover -- longest
+    aligned with the prime-path list (cover="per_pp"), their distinct set in lexicographic order
+    (cover="unique", K7; materialized only), or the greedy cover -- longest
     uncovered prime path first, every prime path contained in a TP covered (cover="greedy").
     ``mode="count"``: COUNT_HASH -- the test paths' count, vertices and R20 digest in the
     stats, nothing written (fused into the count-mode enumeration when ``prime`` is None)."""
@@ -258,10 +259,13 @@ def test_paths(graph, entry: int, exit: int, prime: Optional[PathSet] = None, *,
     return _wrap(paths, stats, alloc)
 
 
+_TP_MODES = {"per_pp": _abi.TP_PER_PP, "unique": _abi.TP_UNIQUE, "greedy": _abi.TP_GREEDY}
+
+
 def _tp_mode(cover: str) -> int:
-    if cover not in ("per_pp", "greedy"):
-        raise ValueError("cover must be 'per_pp' or 'greedy'")
-    return 1 if cover == "greedy" else 0
+    if cover not in _TP_MODES:
+        raise ValueError("cover must be 'per_pp', 'unique' or 'greedy'")
+    return _TP_MODES[cover]
 
 
 def _paths_in(prime: Optional[PathSet], device: int, keep: list):

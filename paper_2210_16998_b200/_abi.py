@@ -21,6 +21,9 @@ OUT_COUNT_HASH = 1
 ENGINE_DFS = 0
 ENGINE_FRONTIER = 1
 ENGINE_ALG3 = 2
+TP_PER_PP = 0
+TP_UNIQUE = 1
+TP_GREEDY = 2
 
 ALLOC_FN = CFUNCTYPE(c_void_p, c_size_t, c_void_p, c_void_p)
 FREE_FN = CFUNCTYPE(None, c_void_p, c_void_p, c_void_p)

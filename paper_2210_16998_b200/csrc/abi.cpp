@@ -48,7 +48,7 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("the Alg. 3 engine has no start-vertex shards (every vertex list is global)");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
-    if (o.tp_mode != TPGEN_TP_PER_PP && o.tp_mode != TPGEN_TP_GREEDY) {
+    if (o.tp_mode != TPGEN_TP_PER_PP && o.tp_mode != TPGEN_TP_UNIQUE && o.tp_mode != TPGEN_TP_GREEDY) {
         tpg::set_error("bad tp_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }

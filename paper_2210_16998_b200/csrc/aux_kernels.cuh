@@ -1114,4 +1114,64 @@ __global__ void tp_write_kernel(TpArgs A) {
     }
 }
 
+// ---------------------------------------------------------------- K7: sorted-unique test paths
+// Lexicographic order of int32 sequences (R14; a proper prefix sorts first) on indices into a
+// flat path array: the comparator of the device merge sort.
+struct SeqLess {
+    const int64_t *off;
+    const int32_t *v;
+    __device__ __forceinline__ bool operator()(const int64_t &a, const int64_t &b) const {
+        int64_t ia = off[a], ib = off[b];
+        const int64_t ea = off[a + 1], eb = off[b + 1];
+        for (; ia < ea && ib < eb; ia++, ib++) {
+            const int32_t x = v[ia], y = v[ib];
+            if (x != y) return x < y;
+        }
+        return (ea - ia) < (eb - ib);
+    }
+};
+
+__global__ void iota_kernel(int64_t *idx, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) idx[i] = i;
+}
+
+// After the sort: keep[i] = the i-th path differs from the (i-1)-th; len = its length if kept
+// (both scanned into the unique list's index and vertex offsets).
+__global__ void tp_unique_mark_kernel(const int64_t *idx, int64_t n, const int64_t *off, const int32_t *v,
+                                      uint64_t *keep, uint64_t *len, uint8_t *kept) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx[i], sb = off[b], eb = off[b + 1];
+        bool k = true;
+        if (i > 0) {
+            const int64_t a = idx[i - 1], sa = off[a], ea = off[a + 1];
+            if (ea - sa == eb - sb) {
+                k = false;
+                for (int64_t q = 0; q < eb - sb; q++)
+                    if (v[sa + q] != v[sb + q]) {
+                        k = true;
+                        break;
+                    }
+            }
+        }
+        keep[i] = k ? 1 : 0;
+        len[i] = k ? (uint64_t)(eb - sb) : 0;
+        kept[i] = k ? 1 : 0;
+    }
+}
+
+// One warp per kept path: its offset, then its vertices (coalesced copy).
+__global__ void tp_unique_gather_kernel(const int64_t *idx, int64_t n, const int64_t *off, const int32_t *v,
+                                        const uint64_t *pos, const uint64_t *vpos, const uint8_t *kept,
+                                        int64_t *out_off, int32_t *out_v) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = wg; i < n; i += nw) {
+        if (!kept[i]) continue;
+        const int64_t b = idx[i], sb = off[b], L = off[b + 1] - sb;
+        if (lane == 0) out_off[pos[i]] = (int64_t)vpos[i];
+        for (int64_t q = lane; q < L; q += 32) out_v[vpos[i] + q] = v[sb + q];
+    }
+}
+
 }  // namespace tpg

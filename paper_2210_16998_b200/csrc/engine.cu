@@ -18,6 +18,8 @@
 #include <mutex>
 #include <type_traits>
 
+#include <cub/device/device_merge_sort.cuh>
+
 #include "aux_kernels.cuh"
 #include "expand.cuh"
 #include "frontier.cuh"
@@ -2672,6 +2674,74 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
         }
     }
     HT("lengths + scan");
+    if (o.tp_mode == TPGEN_TP_UNIQUE) {  // K7: aligned TPs into scratch, then sort + unique into the output
+        DevBuf a_off, a_vert, ws;
+        struct UGuard {
+            DevBuf *a, *b, *c;
+            cudaStream_t s;
+            ~UGuard() {
+                a->release(s);
+                b->release(s);
+                c->release(s);
+            }
+        } ug{&a_off, &a_vert, &ws, s};
+        TPG_TRY(a_off.ensure((size_t)(n + 1) * 8, s));
+        TPG_TRY(a_vert.ensure((size_t)std::max<uint64_t>(total, 1) * 4, s));
+        A.tp_off = a_off.as<int64_t>();
+        A.tp_vert = a_vert.as<int32_t>();
+        if (n > 0) {
+            tp_write_kernel<<<grid_for(n * 32, 256, P.num_sms * 8), 256, 0, s>>>(A);
+            launches++;
+        }
+        set_last_offset_kernel<<<1, 1, 0, s>>>(A.tp_off, n, (int64_t)total);
+        launches++;
+        // indices sorted by their TP (device merge sort, lexicographic comparator), equal neighbours dropped
+        const size_t nn = (size_t)std::max<int64_t>(n, 1);
+        size_t tmp_b = 0;
+        SeqLess cmp{A.tp_off, A.tp_vert};
+        TPG_CK(cub::DeviceMergeSort::StableSortKeys(nullptr, tmp_b, (int64_t *)nullptr, n, cmp, s));
+        const size_t o_idx = 0, o_keep = nn * 8, o_len = o_keep + nn * 8, o_kept = o_len + nn * 8,
+                     o_tmp = (o_kept + nn + 255) / 256 * 256;
+        TPG_TRY(ws.ensure(o_tmp + tmp_b + 16, s));
+        int64_t *idx = reinterpret_cast<int64_t *>(ws.as<char>() + o_idx);
+        uint64_t *keep = reinterpret_cast<uint64_t *>(ws.as<char>() + o_keep);
+        uint64_t *len = reinterpret_cast<uint64_t *>(ws.as<char>() + o_len);
+        uint8_t *kept = reinterpret_cast<uint8_t *>(ws.as<char>() + o_kept);
+        uint64_t tot2[2] = {0, 0};
+        if (n > 0) {
+            iota_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(idx, n);
+            launches++;
+            TPG_CK(cub::DeviceMergeSort::StableSortKeys(ws.as<char>() + o_tmp, tmp_b, idx, n, cmp, s));
+            launches += 3;  // (CUB's merge sort: block sort + merge passes, counted as one group)
+            tp_unique_mark_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(idx, n, A.tp_off, A.tp_vert, keep, len, kept);
+            launches++;
+            uint64_t *arr[2] = {keep, len};
+            TPG_TRY(scan_multi(P, arr, 2, n, tot2, s, launches));
+        }
+        HT("sort + unique");
+        const int64_t nu = (int64_t)tot2[0], nvu = (int64_t)tot2[1];
+        OutOwner *ow = new OutOwner();
+        ow->device = P.device;
+        std::unique_ptr<OutOwner> ow_guard(ow);
+        void *d_off = nullptr, *d_vert = nullptr;
+        TPG_TRY(out_alloc_pair(o, ow, (size_t)(nu + 1) * 8, (size_t)nvu * 4, &d_off, &d_vert, s));
+        if (n > 0) {
+            tp_unique_gather_kernel<<<grid_for(n * 32, 256, P.num_sms * 8), 256, 0, s>>>(
+                idx, n, A.tp_off, A.tp_vert, keep, len, kept, (int64_t *)d_off, (int32_t *)d_vert);
+            launches++;
+        }
+        set_last_offset_kernel<<<1, 1, 0, s>>>((int64_t *)d_off, nu, nvu);
+        launches++;
+        TPG_CK(cudaGetLastError());
+        ow_guard.release();
+        TPG_TRY(finish_output(o, ow, nu, nvu, (int64_t *)d_off, (int32_t *)d_vert, s, out));
+        st.gpu_launches = launches;
+        st.n_paths = nu;
+        st.total_vertices = nvu;
+        st.ms_total = now_ms() - t0;
+        if (stp) *stp = st;
+        return TPGEN_OK;
+    }
     OutOwner *ow = new OutOwner();
     ow->device = P.device;
     std::unique_ptr<OutOwner> ow_guard(ow);

@@ -378,6 +378,47 @@ def test_greedy_cover_invariants():
         _check_greedy_cover(g)
 
 
+# ---------------------------------------------------------------- K7: sorted-unique test paths
+def _is_subpath(t, q):  # (plain scan written here, independent of the oracle's helpers)
+    return any(list(t[i:i + len(q)]) == list(q) for i in range(len(t) - len(q) + 1))
+
+
+def _check_unique(g):
+    off, vert = oracle.prime_paths(g)
+    uo, uv = oracle.unique_test_paths(g, off, vert, g.entry, g.exit)
+    tps = oracle.as_list(uo, uv)
+    arcs = {(u, int(w)) for u in range(g.n) for w in g.targets[g.offsets[u]:g.offsets[u + 1]]}
+    for t in tps:  # entry -> exit walks along arcs
+        assert t[0] == g.entry and t[-1] == g.exit
+        assert all((t[i], t[i + 1]) in arcs for i in range(len(t) - 1))
+    for a, b in zip(tps, tps[1:]):  # strictly increasing: sorted, no duplicates
+        assert tuple(a) < tuple(b)
+    for p in oracle.as_list(off, vert):  # "the set of TPs covering all PPs"
+        assert any(_is_subpath(t, p) for t in tps), p
+    return oracle.as_list(off, vert), tps
+
+
+def test_unique_test_paths_fig1b():
+    """Fig. 1(b): the 19 per-PP test paths collapse to 10 distinct ones (SURVEY §8(d),
+    config 1: "19 TPs (10 unique)"), each an entry->exit walk, together covering all 19 PPs."""
+    pps, tps = _check_unique(gen.fig1b())
+    assert len(pps) == 19 and len(tps) == 10
+
+
+def test_unique_test_paths_dag_are_the_prime_paths():
+    """One-source one-sink DAG: every PP is a complete Start->End path and is its own
+    test path, so the unique set is the PP list itself (already in lexicographic order)."""
+    for K in (3, 5):
+        g = gen.k_seq_if(K)
+        pps, tps = _check_unique(g)
+        assert tps == pps and len(tps) == 2 ** K
+
+
+def test_unique_test_paths_invariants():
+    for g in (gen.config2(), gen.k_seq_loops(3, 3), gen.k_nested_if(4), gen.config4(K=6)):
+        _check_unique(g)
+
+
 # ---------------------------------------------------------------- digest (R20)
 def _flat(paths):
     off = np.zeros(len(paths) + 1, dtype=np.int64)
