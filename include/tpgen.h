@@ -249,6 +249,11 @@ tpgen_status tpgen_plan_classify(tpgen_plan *plan, const tpgen_paths *prime_path
 tpgen_status tpgen_plan_test_paths(tpgen_plan *plan, const tpgen_paths *prime_paths, int32_t entry, int32_t exit,
                                    const tpgen_options *opt, tpgen_paths *out, tpgen_stats *stats);
 void tpgen_plan_destroy(tpgen_plan *plan);
+/* Releases what one-shot calls keep between calls: the per-device cached plans
+ * with their device workspaces and the library's cached output blocks, then trims the device
+ * memory pool.  Plans created with tpgen_plan_create are not affected.  Safe to call at any
+ * time outside a running call. */
+void tpgen_release_cache(void);
 
 /* Out-degree-2 normalization (Fig. 5: "we can convert a vertex v with an out-degree
  * greater than 2 ... to a vertex with out-degree 2 by adding some new intermediate vertices between

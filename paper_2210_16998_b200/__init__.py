@@ -313,6 +313,12 @@ def shard_range(graph, rank: int, count: int) -> Tuple[int, int]:
     return int(lo.value), int(hi.value)
 
 
+def release_cache() -> None:
+    """Frees what one-shot calls keep between calls (``tpgen_release_cache``): the cached plan and
+    its device workspaces per device, the cached output blocks; trims the device memory pool."""
+    library().tpgen_release_cache()
+
+
 @dataclass
 class CSRGraph:
     """A CSR graph returned by the library (host arrays)."""

@@ -92,6 +92,7 @@ SYMBOLS = {
     "tpgen_plan_classify": (c_int, [c_void_p, POINTER(Paths), c_int32, c_int32, POINTER(Options),
                                     POINTER(c_int64)]),
     "tpgen_plan_destroy": (None, [c_void_p]),
+    "tpgen_release_cache": (None, []),
 }
 
 _lib = None

@@ -254,6 +254,19 @@ tpgen_status tpgen_plan_classify(tpgen_plan *plan, const tpgen_paths *prime_path
 
 void tpgen_plan_destroy(tpgen_plan *plan) { delete plan; }
 
+void tpgen_release_cache(void) {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    for (auto &kv : g_cache) delete kv.second;  // (the plan's destructor releases its device workspaces)
+    g_cache.clear();
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        tpg::release_output_cache(dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    }
+}
+
 tpgen_status tpgen_prime_paths(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options *opt,
                                tpgen_paths *out, tpgen_stats *stats) {
     if (!out) return TPGEN_ERR_INVALID_ARGUMENT;

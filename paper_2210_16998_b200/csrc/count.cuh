@@ -39,6 +39,9 @@
 
 namespace tpg {
 
+#ifndef CNT_MINB_PP
+#define CNT_MINB_PP 3  // resident blocks per SM the prime-path / test-path phases are compiled for
+#endif
 #ifndef CNT_QUEUE
 #define CNT_QUEUE 1  // 1: prime paths into a per-warp queue (ballot), hashed 32 at a time; 0: per-lane rings
 #endif
@@ -114,10 +117,13 @@ struct CntCfg {
 // the segment phase the B sums [slot][lane] (8 B) --, the untried-children stack
 // [level][lane] (32-bit masks) and the path bytes [level][lane].
 // Dynamic shared memory a cnt_kernel block needs beyond the staged table:
+// The event ring is needed by the segment phase (items) and, without CNT_QUEUE, for the prime
+// paths; the prime-path phase writes its (rare) head segments at once instead.
+constexpr bool cnt_uses_ring(bool seg) { return seg || !CNT_QUEUE; }
 template <class T>
 constexpr size_t cnt_smem_block(bool seg) {
-    return (size_t)CntCfg<T>::warps * (CntCfg<T>::ring_slots * 32 * (seg ? 20 : 12) + (CntCfg<T>::RS ? 32 * 32 * 4 : 0) +
-                                       CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 12 : 0));
+    return (size_t)CntCfg<T>::warps * ((cnt_uses_ring(seg) ? CntCfg<T>::ring_slots * 32 * (seg ? 20 : 12) : 0) +
+                                       (CntCfg<T>::RS ? 32 * 32 * 4 : 0) + CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 12 : 0));
 }
 
 // PH: the phase -- P_PP, the prime-path phase; P_TP, the same hashing every prime path's test
@@ -126,8 +132,11 @@ constexpr size_t cnt_smem_block(bool seg) {
 // entry lies in the call's start range; their test paths when A.tp is set), their tail and
 // transit segments (R8/R9) become ItemS records for the completion DP and the stitch.
 enum CntPhase : int { P_PP = 0, P_TP = 1, P_SEG = 2 };
+template <class T>
+constexpr int cnt_min_blocks(bool seg) { return seg ? CntCfg<T>::min_blocks : CNT_MINB_PP; }
+
 template <class T, bool TS, bool HSH, bool HX, int PH>
-__global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt_kernel(DfsArgs A) {
+__global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_SEG)) cnt_kernel(DfsArgs A) {
     constexpr bool SEG = PH == P_SEG;
     constexpr bool TRACK_B = PH != P_PP;
     using C = CntCfg<T>;
@@ -135,7 +144,8 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
     constexpr int WARPS = C::warps;
     constexpr int PLEV = C::PLEV;
     constexpr int RING = C::ring;
-    constexpr int RSLOTS = C::ring_slots;
+    constexpr bool USE_RING = cnt_uses_ring(SEG);
+    constexpr int RSLOTS = USE_RING ? C::ring_slots : 0;
     __shared__ unsigned long long s_td, s_head;
     __shared__ unsigned s_ov;
     extern __shared__ __align__(16) uint8_t stab[];  // [TS: {sin, mix}[n_slots]] then the block's areas
@@ -247,7 +257,32 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
                 __syncwarp();
             }
         }
-        const bool to_ring = ((HSH && !CNT_QUEUE) && pp) || ((HX || SEG) && other);
+        if constexpr (HX && !SEG && !USE_RING) {  // a head segment: written at once (one HeadS per head node)
+            const uint32_t hbm = __ballot_sync(kFull, other);
+            if (hbm) {
+                const uint32_t need = __popc(hbm);
+                if (hblk + need > hblk_end) {  // a new block of 256 slots (the rest of the old one: holes)
+                    for (unsigned long long q = hblk + lane; q < hblk_end; q += 32)
+                        if (q < A.head_cap) A.heads[q].x = -1;
+                    unsigned long long b = 0;
+                    if (lane == 0) b = atomicAdd(A.cacc + 5, 256ull);
+                    b = __shfl_sync(kFull, b, 0);
+                    hblk = b;
+                    hblk_end = b + 256;
+                    if (b + 256 > A.head_cap && lane == 0) atomicOr(A.overflow, 8u);
+                }
+                const unsigned long long q = hblk + __popc(hbm & ltm);
+                if (other && q < A.head_cap) {
+                    HeadS hr;
+                    hr.S = Sx;
+                    hr.len = (int32_t)len + (PH == P_TP ? A.tp[L.vb + L.s].pre_len - 1 : 0);
+                    hr.x = slot_;
+                    *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&hr);
+                }
+                hblk += need;
+            }
+        }
+        const bool to_ring = USE_RING && (((HSH && !CNT_QUEUE) && pp) || ((HX || SEG) && other));
         if (to_ring) {
             TPG_DCHECK(rc < (uint32_t)RSLOTS, "cnt: event ring overflow");
             asm volatile("st.shared.u64 [%0], %1;" ::"r"(qb + rc * 256u), "l"(Sx) : "memory");
@@ -256,11 +291,12 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, CntCfg<T>::min_blocks) cnt
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(lb + rc * 128u), "r"(tag) : "memory");
             rc++;
         }
-        if constexpr (HX || SEG) ring_ev |= __any_sync(kFull, other);
+        if constexpr (USE_RING && (HX || SEG)) ring_ev |= __any_sync(kFull, other);
     };
     // warp-uniform: every lane hashes the prime paths in its ring (the two finalizers, R20),
     // then the warp writes the head segments (prime-path phase) or the items (segment phase)
     auto drain = [&]() {
+        if constexpr (!USE_RING) return;
         const uint32_t mx = __reduce_max_sync(kFull, rc);
         for (uint32_t j = 0; j < mx; j++) {
             uint64_t z = 0;

@@ -315,6 +315,8 @@ static void out_cache_clear(int dev) {
     C.blocks.clear();
 }
 
+void release_output_cache(int dev) { out_cache_clear(dev); }
+
 static tpgen_status out_alloc_device(const tpgen_options &o, OutOwner *ow, size_t bytes, void **p, cudaStream_t s);
 
 // Offsets (int64[n+1]) and vertices (int32[...]) of one output.
@@ -628,7 +630,7 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         static_assert(W == 1, "count modes use one mask word");
         constexpr bool HSH = MODE == M_CNT;
         using CT = typename std::conditional<sizeof(T) == 4, uint32_t, uint64_t>::type;
-        const int cgrid = grid / (lean ? kLeanBlocks : DfsCfg<W>::min_blocks) * CntCfg<CT>::min_blocks;
+        const int cgrid = grid / (lean ? kLeanBlocks : DfsCfg<W>::min_blocks) * cnt_min_blocks<CT>(seg);
         const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
         const bool ts = ctab <= kSmemTabMax;
         const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg);
@@ -2053,8 +2055,13 @@ static tpgen_status frontier_pass(PlanImpl &P, const tpgen_options &o, cudaStrea
                       "graphs without arcs leaving SCCs; use the DFS engine)");
             return TPGEN_ERR_OUT_OF_MEMORY;
         }
-        TPG_TRY(P.f_buf0.ensure(cap * kRecB, s));
-        TPG_TRY(P.f_buf1.ensure(cap * kRecB, s));
+        if (2.5 * (double)(cap * kRecB) > 0.9 * (double)(f + P.f_buf0.cap + P.f_buf1.cap)) {  // near the budget: no headroom
+            TPG_TRY(P.f_buf0.ensure_exact(cap * kRecB, s));
+            TPG_TRY(P.f_buf1.ensure_exact(cap * kRecB, s));
+        } else {
+            TPG_TRY(P.f_buf0.ensure(cap * kRecB, s));
+            TPG_TRY(P.f_buf1.ensure(cap * kRecB, s));
+        }
         ulonglong2 *buf[2] = {P.f_buf0.as<ulonglong2>(), P.f_buf1.as<ulonglong2>()};
         uint64_t *bufS[2] = {reinterpret_cast<uint64_t *>(buf[0] + cap), reinterpret_cast<uint64_t *>(buf[1] + cap)};
         uint64_t *bufB[2] = {reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(buf[0]) + cap * (key_b + s_b)),

@@ -93,4 +93,7 @@ tpgen_status run_classify(PlanImpl &P, const tpgen_paths *pp, int32_t start, int
 void free_paths(tpgen_paths *p);
 const char *last_error();
 
+// Frees the cached output blocks of device `dev` (tpgen_release_cache).
+void release_output_cache(int dev);
+
 }  // namespace tpg

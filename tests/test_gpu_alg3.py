@@ -78,6 +78,7 @@ def test_alg3_capacity_retry(monkeypatch):
 def test_alg3_config3_full_size():
     """Config 3 (22 vertices, one SCC, 1.4e8 simple paths held in the lists at once): the whole
     list's n_paths, total vertices, digest and E_canon equal to the oracle's."""
+    tp.release_cache()
     g = gen.config3()
     ref = oracle.pp_stats_parallel(g, chunk=1)
     st, got = _alg3(g)
@@ -91,6 +92,7 @@ def test_alg3_config3_full_size():
 def test_alg3_config3_normalized_vs_dfs():
     """Config 3 normalized to out-degree 2 (66 vertices, two-word masks): Alg. 3 and the DFS
     engine's COUNT_HASH mode agree (the DFS engine is pinned to the oracle elsewhere)."""
+    tp.release_cache()
     h = tp.normalize_outdeg2(gen.config3())
     st, got = _alg3(h)
     d = tp.prime_paths(h, mode="count", digest=True).stats

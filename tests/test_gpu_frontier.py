@@ -168,6 +168,7 @@ def test_frontier_with_segment_events_matches_oracle():
 def test_frontier_config5_full_size():
     """Config 5 in COUNT_HASH through the frontier engine equals the count-mode DFS (itself equal to
     the oracle for every start vertex, tests/test_gpu_count.py) and the oracle's totals."""
+    tp.release_cache()  # (workspaces the earlier tests' one-shot calls keep: this test needs ~100 GB)
     g = gen.config5()
     ref = oracle.pp_stats_parallel(g, chunk=4)
     a = ref[:, :4].astype(object)
