@@ -39,8 +39,9 @@
 
 namespace tpg {
 
-#ifndef CNT_MINB_PP
-#define CNT_MINB_PP 3  // resident blocks per SM the prime-path / test-path phases are compiled for
+#ifndef CNT_MINB_PP64H
+#define CNT_MINB_PP64H 4  // resident blocks per SM of the 64-bit hashing prime-path / test-path kernels (64
+                          // registers: measured 151.5 -> 142.6 ms on config 5; the other variants lose at 4)
 #endif
 #ifndef CNT_QUEUE
 #define CNT_QUEUE 1  // 1: prime paths into a per-warp queue (ballot), hashed 32 at a time; 0: per-lane rings
@@ -133,10 +134,12 @@ constexpr size_t cnt_smem_block(bool seg) {
 // transit segments (R8/R9) become ItemS records for the completion DP and the stitch.
 enum CntPhase : int { P_PP = 0, P_TP = 1, P_SEG = 2 };
 template <class T>
-constexpr int cnt_min_blocks(bool seg) { return seg ? CntCfg<T>::min_blocks : CNT_MINB_PP; }
+constexpr int cnt_min_blocks(bool seg, bool hsh) {
+    return (sizeof(T) == 8 && hsh && !seg) ? CNT_MINB_PP64H : CntCfg<T>::min_blocks;
+}
 
 template <class T, bool TS, bool HSH, bool HX, int PH>
-__global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_SEG)) cnt_kernel(DfsArgs A) {
+__global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_SEG, HSH)) cnt_kernel(DfsArgs A) {
     constexpr bool SEG = PH == P_SEG;
     constexpr bool TRACK_B = PH != P_PP;
     using C = CntCfg<T>;

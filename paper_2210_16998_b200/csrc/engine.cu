@@ -630,7 +630,8 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         static_assert(W == 1, "count modes use one mask word");
         constexpr bool HSH = MODE == M_CNT;
         using CT = typename std::conditional<sizeof(T) == 4, uint32_t, uint64_t>::type;
-        const int cgrid = grid / (lean ? kLeanBlocks : DfsCfg<W>::min_blocks) * cnt_min_blocks<CT>(seg);
+        const int cgrid = grid / (lean ? kLeanBlocks : DfsCfg<W>::min_blocks) *
+                          cnt_min_blocks<CT>(seg, HSH || A.tp != nullptr);
         const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
         const bool ts = ctab <= kSmemTabMax;
         const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg);
