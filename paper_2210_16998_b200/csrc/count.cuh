@@ -43,6 +43,9 @@ namespace tpg {
 #define CNT_MINB_PP64H 4  // resident blocks per SM of the 64-bit hashing prime-path / test-path kernels (64
                           // registers: measured 151.5 -> 142.6 ms on config 5; the other variants lose at 4)
 #endif
+#ifndef CNT_POP2
+#define CNT_POP2 0  // 1: a pop whose parent has no untried child left pops the parent in the same pass
+#endif
 #ifndef CNT_QUEUE
 #define CNT_QUEUE 1  // 1: prime paths into a per-warp queue (ballot), hashed 32 at a time; 0: per-lane rings
 #endif
@@ -606,6 +609,27 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 if constexpr (TRACK_B) L.B = push ? Bw : (pop ? L.B - mv : L.B);
                 L.l = l + (push ? 1 : 0) - (pop ? 1 : 0);
                 L.rem = push ? cw : (pop ? rem_pop : (take ? (rem & (rem - 1)) : rem));
+#if CNT_POP2
+                if (pop && L.rem == 0 && L.l > L.r) {  // the parent has nothing left either: pop it too
+                    const int l2 = L.l;
+                    const int u2 = lds_u8(pb + (uint32_t)l2 * 32u);
+                    const T vb2 = (T)1 << u2;
+                    const uint64_t mv2 = tab.mix(L.vb + u2);
+                    T rp2;
+                    if constexpr (RS) {
+                        rp2 = (T)lds_u32(rb + (uint32_t)(l2 - 1) * 128u);
+                    } else {
+                        const int p2 = lds_u8(pb + (uint32_t)(l2 - 1) * 32u);
+                        const T above2 = (u2 >= 63) ? (T)0 : ((~(T)0) << (u2 + 1));
+                        rp2 = tab.sin(L.vb + p2) & (~(L.M & ~vb2) | L.sbit) & above2;
+                    }
+                    L.M ^= vb2;
+                    L.S -= mul64x32(mv2, 2u * (uint32_t)l2 + 1u);
+                    if constexpr (TRACK_B) L.B -= mv2;
+                    L.l = l2 - 1;
+                    L.rem = rp2;
+                }
+#endif
                 put_ev(pp, other, kind, Sw, Bw, (uint32_t)l + 2, vslot);
             }
             drain();
