@@ -136,9 +136,12 @@ constexpr size_t cnt_smem_block(bool seg) {
 // entry lies in the call's start range; their test paths when A.tp is set), their tail and
 // transit segments (R8/R9) become ItemS records for the completion DP and the stitch.
 enum CntPhase : int { P_PP = 0, P_TP = 1, P_SEG = 2 };
+#ifndef CNT_MINB_SEG
+#define CNT_MINB_SEG 3
+#endif
 template <class T>
 constexpr int cnt_min_blocks(bool seg, bool hsh) {
-    return (sizeof(T) == 8 && hsh && !seg) ? CNT_MINB_PP64H : CntCfg<T>::min_blocks;
+    return seg ? CNT_MINB_SEG : ((sizeof(T) == 8 && hsh) ? CNT_MINB_PP64H : CntCfg<T>::min_blocks);
 }
 
 template <class T, bool TS, bool HSH, bool HX, int PH>
