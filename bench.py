@@ -391,6 +391,35 @@ def secondary_config3(dev, steps, warmup, flush, peak, peak_kind, sm_max, no_e2e
     return out
 
 
+def engine_comparison(dev, flush):
+    """Config 3 COUNT_HASH (counts, E_canon, digest) through the three engines -- the count-mode
+    DFS, the level-synchronous frontier and the paper's vertex-centric Alg. 3
+    -- device ms per call (median of 3 after one warm-up, L2 flushed between calls) and whether
+    all three agree (rank 0, informational; not the headline)."""
+    import torch
+
+    import paper_2210_16998_b200 as tp
+
+    g = gen.config3()
+    plan = tp.Plan(g, device=dev)
+    out, keys = {}, set()
+    for eng in ("dfs", "frontier", "alg3"):
+        ms = []
+        for i in range(4):
+            flush.fill_(i & 0xff)
+            torch.cuda.synchronize(dev)
+            st = plan.prime_paths(mode="count", digest=True, engine=eng).stats
+            if i:
+                ms.append(st["ms_device"])
+        keys.add((st["n_paths"], st["total_vertices"], st["n_extensions"], st["hash_lo"], st["hash_hi"]))
+        out[eng] = {"ms_per_call": float(np.median(ms)), "pp_per_sec": st["n_paths"] / (np.median(ms) * 1e-3),
+                    "gpu_launches": int(st["gpu_launches"])}
+    plan.close()
+    out["agree"] = len(keys) == 1
+    out["workload"] = CONFIG3_WORKLOAD + ", COUNT_HASH"
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -547,6 +576,7 @@ def main():
         if c5 and not args.no_secondary:
             out["secondary"] = secondary_config3(dev, min(args.steps, 10), max(args.warmup, 3), flush, peak,
                                                  peak_kind, sm_max, args.no_e2e)
+            out["engines_config3"] = engine_comparison(dev, flush)
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_leg()
         print(json.dumps(out))

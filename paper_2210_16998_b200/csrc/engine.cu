@@ -2276,7 +2276,9 @@ static tpgen_status run_alg3(PlanImpl &P, const tpgen_options &o, tpgen_stats *s
     double est = 0;
     for (int32_t v = 0; v < n; v++) est += H.cost[v];
     unsigned long long cap = std::max<unsigned long long>(4096, (unsigned long long)(1.25 * est / n));
+    cap = std::max<unsigned long long>(cap, P.a3_cap_hwm);  // (a capacity that fitted an earlier call of this plan)
     if (const char *ev = getenv("TPGEN_ALG3_CAP")) cap = std::max<unsigned long long>(16, strtoull(ev, nullptr, 10));
+    if (getenv("TPGEN_ALG3_CAP")) P.a3_cap_hwm = 0;  // (the test hook starts small every call)
     int dev_sms = P.num_sms;
     if (n > dev_sms) {
         set_error("the Alg. 3 engine runs one co-resident CTA per vertex: at most one vertex per SM");
@@ -2326,8 +2328,15 @@ static tpgen_status run_alg3(PlanImpl &P, const tpgen_options &o, tpgen_stats *s
         TPG_CK(cudaStreamSynchronize(s));
         cudaEventElapsedTime(&ms, t.a, t.b);
         bool ovf = false;
-        for (int32_t v = 0; v < n; v++) ovf |= part[(size_t)v * 8 + 5] != 0;
-        if (!ovf) break;
+        unsigned long long longest = 0;
+        for (int32_t v = 0; v < n; v++) {
+            ovf |= part[(size_t)v * 8 + 5] != 0;
+            longest = std::max<unsigned long long>(longest, part[(size_t)v * 8 + 4]);
+        }
+        if (!ovf) {
+            P.a3_cap_hwm = std::max<unsigned long long>(P.a3_cap_hwm, longest + longest / 8);
+            break;
+        }
         st.n_count_rounds = attempt + 1;
         cap *= 2;
     }

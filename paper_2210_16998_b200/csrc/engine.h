@@ -64,6 +64,7 @@ struct PlanImpl {
     DevBuf f_tab, f_roots, f_buf0, f_buf1, f_ctr;  // frontier engine: slot table, roots, ping-pong levels, counters
     DevBuf f_sched;                                // DFS-chunked frontier: the device chunk scheduler's state (FChunk)
     DevBuf a3_lists, a3_aux;                       // Alg. 3 comparison engine: per-vertex path lists, CSR / flags
+    unsigned long long a3_cap_hwm = 0;             // Alg. 3: a list capacity that fitted (records per vertex)
     bool f_tab_ok = false;
     int32_t f_roots_lo = -1, f_roots_hi = -1;  // start range of the uploaded frontier roots
     uint64_t f_cap_hwm = 0;                        // frontier engine: most records any level of this plan held
