@@ -277,6 +277,12 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs A) {
 // ---------------------------------------------------------------- fast path
 constexpr int kFastMaxScc = 63;  // a path of local ids fits NPW <= 16 32-bit words (W = 1 masks)
 
+#ifndef EXP_MINB
+#define EXP_MINB 4  // min resident blocks per SM of the fast writer (launch bounds; 64 registers at 256 threads)
+#endif
+#ifndef EXP_BUFS
+#define EXP_BUFS 2  // bulk-store stages per warp
+#endif
 template <int NPW>
 struct FastCfg {
     static constexpr int threads = (NPW > 8) ? 128 : 256;
@@ -284,7 +290,7 @@ struct FastCfg {
     // ints per warp stage: HASH, each lane's path bytes; else one batch's vertices + the 16-byte phase shift
     static constexpr int stage_ints(bool hash) { return hash ? 32 * NPW : (32 * max_out + 4 + 3) / 4 * 4; }
     static constexpr size_t smem_bytes(bool hash) {
-        return (size_t)(threads / 32) * (hash ? 1 : 2) * stage_ints(hash) * sizeof(int32_t);
+        return (size_t)(threads / 32) * (hash ? 1 : EXP_BUFS) * stage_ints(hash) * sizeof(int32_t);
     }
 };
 
@@ -320,13 +326,13 @@ __device__ __forceinline__ void hash_path(const DevGraph &G, const uint32_t (&D)
 // MIXED = false: the call has no segment items and no head blocks (e.g. a graph
 // that is one SCC), so every batch is prime paths and path continuations only.
 template <int NPW, bool HASH, bool MIXED>
-__global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(ExpandArgs A) {
+__global__ void __launch_bounds__(FastCfg<NPW>::threads, EXP_MINB) expand_fast_kernel(ExpandArgs A) {
     constexpr int kWarps = FastCfg<NPW>::threads / 32;
     // one batch of paths (HASH: each lane's path bytes, NPW words)
     // (!HASH: two stages per warp, each shifted by the output offset's alignment -- up to 3 ints --
     // so that the middle of a batch leaves with one TMA bulk store while the next batch is staged)
     constexpr int kStage = FastCfg<NPW>::stage_ints(HASH);
-    constexpr int kBufs = HASH ? 1 : 2;
+    constexpr int kBufs = HASH ? 1 : EXP_BUFS;
     extern __shared__ __align__(16) int32_t stage_dyn[];  // [kWarps][kBufs][kStage] (launch_fast sizes it)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int32_t *const stage_w = stage_dyn + (size_t)wid * kBufs * kStage;
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                 if (T == 0) continue;
                 const int al = (int)(cu.vv & 3);
                 int32_t *stg = stage_w + sbuf * kStage + al;
-                if (lane == 0) bulk_wait_read<1>();  // this stage's previous bulk store has read it
+                if (lane == 0) bulk_wait_read<EXP_BUFS - 1>();  // this stage's previous bulk store has read it
                 __syncwarp();
                 if (ga >= 0) {
 #pragma unroll
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(FastCfg<NPW>::threads) expand_fast_kernel(Expa
                     if (nb > 0) bulk_store(dst + h, stg + h, (uint32_t)nb * 4u);
                     bulk_commit();
                 }
-                sbuf ^= 1;
+                if (kBufs > 1) sbuf ^= 1;
                 cu.pp += (uint64_t)__popc(em);
                 cu.vv += (uint64_t)T;
             } else {
