@@ -150,22 +150,19 @@ __device__ __forceinline__ void replay_one(const ExpandArgs &A, uint64_t rec, in
     const int len = cc + n;
     const int tot = len + (int)((rec >> 3) & 1);
     int32_t *dst;
-    if (HASH && ty == R_PP) {  // digest only: absorb the vertices in order (lane q holds position q + 32 r)
+    if (HASH && ty == R_PP) {  // digest only (R20): lane q adds the terms of positions q + 32 r, one warp sum
         const int s0 = __shfl_sync(kFull, P[0], 0);
-        PathHash hs;
-        hs.init((uint64_t)tot);
-        for (int pos = 0; pos < tot; pos++) {
-            int xq = 0;
+        uint64_t part = 0;
 #pragma unroll
-            for (int r = 0; r < NP; r++)
-                if (r == (pos >> 5)) xq = P[r];
-            const int loc = (pos < len) ? __shfl_sync(kFull, xq, pos & 31) : s0;
-            hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
+        for (int r = 0; r < NP; r++) {
+            const int pos = lane + 32 * r;
+            if (pos < tot) part += __ldg(G.slot_mix + vb + ((pos < len) ? P[r] : s0)) * (2ull * (uint64_t)pos + 1ull);
         }
-        hs.fin();
+#pragma unroll
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
         if (lane == 0) {
-            acc.a += hs.a;
-            acc.b += hs.b;
+            acc.a += mix64(part ^ (kSeedA + (uint64_t)tot));
+            acc.b += mix64(part ^ (kSeedB + (uint64_t)tot));
         }
         cu.pp += 1;
         cu.vv += (uint64_t)tot;
