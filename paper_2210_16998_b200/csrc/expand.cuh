@@ -307,17 +307,12 @@ __device__ __forceinline__ void hash_path(const DevGraph &G, const uint32_t (&D)
     for (int w = 0; w < NPW; w++)
         if (4 * w < len) mine[w] = D[w];
     const uint8_t *bytes = reinterpret_cast<const uint8_t *>(mine);
-    PathHash hs;
-    hs.init((uint64_t)tot);
+    uint64_t S = 0;  // R20: the terms from the per-slot mix table (no splitmix64 per vertex)
 #pragma unroll 2
-    for (int p = 0; p < len; p++) {
-        const int loc = bytes[p];
-        hs.add(ga >= 0 ? ga + loc : __ldg(G.slot_gid + vb + loc));
-    }
-    if (len < tot) hs.add(s0g);
-    hs.fin();
-    acc.a += hs.a;
-    acc.b += hs.b;
+    for (int p = 0; p < len; p++) S += __ldg(G.slot_mix + vb + bytes[p]) * (2ull * (uint64_t)p + 1ull);
+    if (len < tot) S += __ldg(G.slot_mix + vb + bytes[0]) * (2ull * (uint64_t)len + 1ull);  // the cycle's closing s
+    acc.a += mix64(S ^ (kSeedA + (uint64_t)tot));
+    acc.b += mix64(S ^ (kSeedB + (uint64_t)tot));
 }
 
 // MIXED = false: the call has no segment items and no head blocks (e.g. a graph
