@@ -180,7 +180,9 @@ const char *tpgen_status_string(tpgen_status s) {
 
 const char *tpgen_last_error_message(void) { return tpg::last_error(); }
 
-const char *tpgen_version(void) { return "tpgen-b200 0.1 (sm_100a; DFS units + warp-cooperative writer; frontier engine)"; }
+const char *tpgen_version(void) {
+    return "tpgen-b200 0.2 (sm_100a; DFS + count-mode DFS, frontier and Alg. 3 engines; TMA-store writer)";
+}
 
 tpgen_status tpgen_plan_create(const int64_t *so, const int32_t *st, int32_t n, const tpgen_options *opt,
                                tpgen_plan **plan) {

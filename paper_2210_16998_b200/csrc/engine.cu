@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include <cub/device/device_merge_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "aux_kernels.cuh"
 #include "expand.cuh"
@@ -28,6 +29,15 @@
 #include "engine.h"
 
 namespace tpg {
+
+// NVTX range over a host-side stage (SURVEY §5 tracing): the kernels a stage launches appear
+// under its name in ncu (--nvtx) / nsys timelines; a no-op unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 #define TPG_CK(x)                                                                                      \
     do {                                                                                               \
@@ -138,6 +148,7 @@ std::vector<DevBuf *> PlanImpl::all_bufs() {
 }
 
 tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
+    NvtxRange nvtx_range("tpgen: plan upload");
     const HostPlan &H = P.hp;
     // pack Slot<W> records (sin[W], pin[W], gid, out_off, out_cnt, flags)
     const int W = H.W;
@@ -678,6 +689,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
                               uint64_t qbase, cudaStream_t s, tpgen_stats &st, int64_t &launches, double &ms_dfs,
                               uint64_t &tail_out, int mode = M_REC, unsigned long long *cacc_h = nullptr,
                               double *ms_last = nullptr) {
+    NvtxRange nvtx_range(seg ? "tpgen: DFS segment phase" : "tpgen: DFS prime-path phase");
     constexpr int W = MT<T>::W;
     Timer t;
     const HostPlan &H = P.hp;
@@ -928,6 +940,7 @@ static void launch_expand(const HostPlan &H, const ExpandArgs &E, int64_t nu, in
 
 template <class T>
 static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: prime paths (record walk + canonical writer)");
     constexpr int W = MT<T>::W;
     const double t0 = now_ms();
     tpgen_stats st;
@@ -1380,6 +1393,7 @@ static tpgen_status count_post(PlanImpl &P, const tpgen_options &o, const DevGra
                                const unsigned long long *cseg, const unsigned long long *cpp, uint64_t presplit_ext,
                                tpgen_stats &st, int64_t &launches, Timer &tall, Timer &tst, double ms_dfs, double t0,
                                tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: count post (items, completion DP, stitch)");
     const HostPlan &H = P.hp;
     const size_t agg_n = 2 * (size_t)H.n + 2 * (size_t)H.n_pairs + 1;
     unsigned long long *ctr = P.ctr.as<unsigned long long>();
@@ -1562,6 +1576,7 @@ static tpgen_status count_post(PlanImpl &P, const tpgen_options &o, const DevGra
 
 template <class T>
 static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: prime paths (count mode)");
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
@@ -1674,6 +1689,7 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
 // extension of all paths of one length at a time; counts, E_canon and digest.
 template <class T>
 static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: frontier engine");
     const bool hash = o.compute_digest != 0;  // without the digest: no S, no mixing
     const size_t kRecB = (sizeof(T) == 4 ? 8 : 16) + (hash ? 8 : 0);  // bytes per frontier record (key [+ S])
     const double t0 = now_ms();
@@ -2011,6 +2027,7 @@ template <class T, bool SEG>
 static tpgen_status frontier_pass(PlanImpl &P, const tpgen_options &o, cudaStream_t s, int32_t lo, int32_t hi,
                                   const std::vector<int32_t> &roots, bool hash, unsigned long long *out,
                                   unsigned long long *ev_slots, double &ms, int64_t &launches, uint64_t &recs) {
+    NvtxRange nvtx_range(SEG ? "tpgen: frontier segment pass" : "tpgen: frontier prime-path pass");
     const HostPlan &H = P.hp;
     const int32_t n_roots = (int32_t)(roots.size() / 2);
     memset(out, 0, 5 * sizeof(unsigned long long));
@@ -2139,6 +2156,7 @@ static tpgen_status frontier_pass(PlanImpl &P, const tpgen_options &o, cudaStrea
 // completion DP, the cross prime paths, the stitch hash -- shared with the count-mode DFS.
 template <class T>
 static tpgen_status run_frontier_seg(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: frontier engine (segment events)");
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
@@ -2206,6 +2224,7 @@ static tpgen_status run_frontier_seg(PlanImpl &P, const tpgen_options &o, tpgen_
 // algorithm (Alg. 1-4) as a comparison engine: one cooperative launch, one CTA per vertex.
 template <int W>
 static tpgen_status run_alg3(PlanImpl &P, const tpgen_options &o, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: Alg. 3 engine");
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
@@ -2446,6 +2465,7 @@ static tpgen_status tp_device_tables(PlanImpl &P, const TpTables &T, cudaStream_
 // hashes the test paths of the given (or computed) list.
 static tpgen_status run_test_paths_count(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry, int32_t exit,
                                          const tpgen_options &o, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: test paths (count mode)");
     const double t0 = now_ms();
     const HostPlan &H = P.hp;
     cudaStream_t s = (cudaStream_t)o.stream;
@@ -2543,6 +2563,7 @@ static tpgen_status run_test_paths_count(PlanImpl &P, const tpgen_paths *pp_in, 
 
 tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry, int32_t exit,
                             const tpgen_options &o, tpgen_paths *out, tpgen_stats *stp) {
+    NvtxRange nvtx_range("tpgen: test paths");
     const double t0 = now_ms();
     memset(out, 0, sizeof(*out));
     if (o.output_mode == TPGEN_OUT_COUNT_HASH) {
