@@ -121,9 +121,12 @@ struct CntCfg {
 // the segment phase the B sums [slot][lane] (8 B) --, the untried-children stack
 // [level][lane] (32-bit masks) and the path bytes [level][lane].
 // Dynamic shared memory a cnt_kernel block needs beyond the staged table:
-// The event ring is needed by the segment phase (items) and, without CNT_QUEUE, for the prime
-// paths; the prime-path phase writes its (rare) head segments at once instead.
-constexpr bool cnt_uses_ring(bool seg) { return seg || !CNT_QUEUE; }
+// The event ring is needed only without CNT_QUEUE (for the prime paths): head segments (prime-path
+// phase) and items (segment phase) are written at once, in warp blocks of slots.
+#ifndef CNT_SEG_RING
+#define CNT_SEG_RING 0  // 1: the segment phase's items go through the ring (round-2 first version)
+#endif
+constexpr bool cnt_uses_ring(bool seg) { return (seg && CNT_SEG_RING) || !CNT_QUEUE; }
 template <class T>
 constexpr size_t cnt_smem_block(bool seg) {
     return (size_t)CntCfg<T>::warps * ((cnt_uses_ring(seg) ? CntCfg<T>::ring_slots * 32 * (seg ? 20 : 12) : 0) +
@@ -289,6 +292,33 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&hr);
                 }
                 hblk += need;
+            }
+        }
+        if constexpr (SEG && !USE_RING) {  // a tail / transit segment: an ItemS written at once
+            const uint32_t ibm = __ballot_sync(kFull, other);
+            if (ibm) {
+                const uint32_t need = __popc(ibm);
+                if (iblk + need > iblk_end) {  // a new block of 256 slots (the rest of the old one: holes)
+                    for (unsigned long long q = iblk + lane; q < iblk_end; q += 32)
+                        if (q < A.item_cap) A.items[q].ent = -1;
+                    unsigned long long b = 0;
+                    if (lane == 0) b = atomicAdd(A.cacc + 7, 256ull);
+                    b = __shfl_sync(kFull, b, 0);
+                    iblk = b;
+                    iblk_end = b + 256;
+                    if (b + 256 > A.item_cap && lane == 0) atomicOr(A.overflow, 8u);
+                }
+                const unsigned long long q = iblk + __popc(ibm & ltm);
+                if (other && q < A.item_cap) {
+                    const Slot<1> *gsl = reinterpret_cast<const Slot<1> *>(G.slots);
+                    const int32_t ent = __ldg(&gsl[L.vb + L.s].gid);
+                    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(A.items + q);
+                    d[0] = make_ulonglong2(Sx, Bx);
+                    d[1] = make_ulonglong2(
+                        (unsigned long long)len | ((unsigned long long)(uint32_t)(kind == EK_TAIL ? -1 : slot_) << 32),
+                        (unsigned long long)(uint32_t)ent | ((unsigned long long)(uint32_t)slot_ << 32));
+                }
+                iblk += need;
             }
         }
         const bool to_ring = USE_RING && (((HSH && !CNT_QUEUE) && pp) || ((HX || SEG) && other));
