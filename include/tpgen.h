@@ -116,11 +116,10 @@ typedef struct {
                                   Requires output_mode = TPGEN_OUT_COUNT_HASH (counts, E_canon and -- with
                                   compute_digest = 1 -- the digest; compute_digest = 0 drops the digest sum
                                   from the records of graphs without arcs leaving SCCs) and SCCs of <= 64
-                                  vertices (else TPGEN_ERR_INVALID_ARGUMENT).  Without arcs leaving SCCs, a
-                                  level that does not fit in the device memory budget switches the call to
-                                  the DFS-chunked frontier; TPGEN_ERR_OUT_OF_MEMORY when
-                                  even one chunk cannot fit, or (graphs with arcs leaving SCCs) a level does
-                                  not fit.  TPGEN_ENGINE_ALG3: the paper's vertex-centric self-stabilizing
+                                  vertices (else TPGEN_ERR_INVALID_ARGUMENT).  A level that does not fit
+                                  in the device memory budget switches the call (or pass) to the
+                                  DFS-chunked frontier; TPGEN_ERR_OUT_OF_MEMORY when
+                                  even the per-level rings cannot hold the roots.  TPGEN_ENGINE_ALG3: the paper's vertex-centric self-stabilizing
                                   algorithm (Alg. 1-4) as a comparison engine -- one cooperative
                                   launch, one CTA per vertex owning the list of the simple paths ending at
                                   it, every simple path of the graph held in HBM at once; COUNT_HASH

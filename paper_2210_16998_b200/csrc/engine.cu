@@ -2064,14 +2064,16 @@ static tpgen_status frontier_pass(PlanImpl &P, const tpgen_options &o, cudaStrea
     const int grid = P.num_sms * std::max(per_sm, 1);
     std::vector<unsigned long long> h(nctr + 8);
     Timer t;
-    for (int attempt = 0; attempt < 24; attempt++) {
+    const char *chunk_hook = getenv("TPGEN_FRONTIER_CHUNK");  // test hook: force the DFS-chunked walk
+    bool chunked = chunk_hook != nullptr;
+    for (int attempt = 0; attempt < 24 && !chunked; attempt++) {
         size_t f = 0, tot = 0;
         TPG_CK(cudaMemGetInfo(&f, &tot));
+        if (const char *ev = getenv("TPGEN_FRONTIER_BUDGET")) f = (size_t)strtoull(ev, nullptr, 10);
         const uint64_t cap_max = (uint64_t)((double)(f + P.f_buf0.cap + P.f_buf1.cap) * 0.45 / kRecB);
-        if (cap > cap_max) {
-            set_error("frontier level larger than the device memory budget (the DFS-chunked frontier handles "
-                      "graphs without arcs leaving SCCs; use the DFS engine)");
-            return TPGEN_ERR_OUT_OF_MEMORY;
+        if (cap > cap_max) {  // no level fits twice: the DFS-chunked walk in the same memory
+            chunked = true;
+            break;
         }
         if (2.5 * (double)(cap * kRecB) > 0.9 * (double)(f + P.f_buf0.cap + P.f_buf1.cap)) {  // near the budget: no headroom
             TPG_TRY(P.f_buf0.ensure_exact(cap * kRecB, s));
@@ -2143,6 +2145,112 @@ static tpgen_status frontier_pass(PlanImpl &P, const tpgen_options &o, cudaStrea
         P.f_cap_hwm = std::max<uint64_t>(P.f_cap_hwm, peak);
         ev_hwm = std::max<uint64_t>(ev_hwm, used);
         for (int l = 0; l <= Lmax; l++) recs += h[8 + l];
+        for (int q = 0; q < 5; q++) out[q] = h[q];
+        *ev_slots = used;
+        return TPGEN_OK;
+    }
+    if (!chunked) {
+        set_error("frontier pass could not be sized");
+        return TPGEN_ERR_OUT_OF_MEMORY;
+    }
+    // ---- the DFS-chunked walk: one ring of capc records per level, one persistent
+    // cooperative launch; heads / items as in the one-pass form
+    P.f_buf1.release(s);
+    uint64_t capc = 0;
+    {
+        size_t f = 0, tot = 0;
+        TPG_CK(cudaStreamSynchronize(s));
+        TPG_CK(cudaMemGetInfo(&f, &tot));
+        if (const char *ev = getenv("TPGEN_FRONTIER_BUDGET")) f = (size_t)strtoull(ev, nullptr, 10);
+        f += P.f_buf0.cap;
+        capc = chunk_hook ? (uint64_t)std::max<long long>(64, atoll(chunk_hook))
+                          : (uint64_t)((double)f * 0.8 / ((double)(Lmax + 1) * kRecB));
+    }
+    uint32_t D = 1;
+    for (int32_t i = 0; i < H.n; i++) D = std::max<uint32_t>(D, (uint32_t)__builtin_popcountll(H.sin[i]));
+    if (capc < (uint64_t)std::max<int64_t>(n_roots, D) || Lmax + 1 > kFMaxLevels) {
+        set_error("frontier chunk buffers too small for the roots (use the DFS engine)");
+        return TPGEN_ERR_OUT_OF_MEMORY;
+    }
+    const size_t nlv = (size_t)(Lmax + 1) * capc;
+    TPG_TRY(P.f_buf0.ensure_exact(nlv * kRecB, s));
+    ulonglong2 *base = P.f_buf0.as<ulonglong2>();
+    uint64_t *baseS = reinterpret_cast<uint64_t *>(base + nlv);
+    uint64_t *baseB = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(base) + nlv * (key_b + s_b));
+    TPG_TRY(P.f_sched.ensure(sizeof(FChunk), s));
+    FChunk *fc = P.f_sched.as<FChunk>();
+    void (*const walk_k)(FrontierArgs, FSchedArgs) =
+        ts ? (hash ? frontier_walk_kernel<T, true, true, true, SEG> : frontier_walk_kernel<T, true, false, true, SEG>)
+           : (hash ? frontier_walk_kernel<T, false, true, true, SEG> : frontier_walk_kernel<T, false, false, true, SEG>);
+    int wper = 0;
+    TPG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, walk_k, kFThreads, ts ? (int)smem : 0));
+    const int wgrid = P.num_sms * std::max(wper, 1);
+    for (int attempt = 0; attempt < 24; attempt++) {
+        TPG_CK(cudaMemsetAsync(ctr, 0, (nctr + 8) * 8, s));
+        TPG_CK(cudaMemsetAsync(fc, 0, sizeof(FChunk), s));
+        FrontierArgs A;
+        memset(&A, 0, sizeof(A));
+        A.tab = P.f_tab.p;
+        A.n_tab = std::max(H.n, 1);
+        A.cap = capc;
+        A.lim = ~0ull;
+        A.acc = ctr;
+        A.overflow = reinterpret_cast<unsigned int *>(ctr + 5);
+        A.heads = P.cheads.as<HeadS>();
+        A.head_cap = SEG ? 0 : P.cheads.cap / sizeof(HeadS);
+        A.items = P.citems.as<ItemS>();
+        A.item_cap = SEG ? P.citems.cap / sizeof(ItemS) : 0;
+        A.hcnt = ctr + nctr;
+        A.slot_mix = P.d_slot_mix.as<uint64_t>();
+        A.shard_lo = lo;
+        A.shard_hi = hi;
+        cudaEventRecord(t.a, s);
+        A.out = base;
+        A.out_S = baseS;
+        A.out_B = baseB;
+        A.cnt_out = ctr + 8;
+        A.l = -1;
+        root_k<<<(n_roots + 255) / 256, 256, 0, s>>>(A, P.f_roots.as<int32_t>(), P.f_roots.as<int32_t>() + n_roots,
+                                                     n_roots);
+        launches++;
+        FSchedArgs sa;
+        memset(&sa, 0, sizeof(sa));
+        sa.c = fc;
+        sa.ctr = ctr;
+        sa.base = base;
+        sa.baseS = baseS;
+        sa.baseB = baseB;
+        sa.capc = capc;
+        sa.chunk = std::max<uint64_t>(1, capc / D);
+        sa.chunk_div = D;
+        sa.key_b = (uint32_t)key_b;
+        sa.Lmax = Lmax;
+        void *wargs[2] = {&A, &sa};
+        TPG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(walk_k), dim3(wgrid), dim3(kFThreads), wargs,
+                                           ts ? smem : 0, s));
+        launches++;
+        cudaEventRecord(t.b, s);
+        TPG_CK(cudaGetLastError());
+        TPG_CK(cudaMemcpyAsync(h.data(), ctr, (nctr + 8) * 8, cudaMemcpyDeviceToHost, s));
+        FChunk hc;
+        TPG_CK(cudaMemcpyAsync(&hc, fc, sizeof(FChunk), cudaMemcpyDeviceToHost, s));
+        TPG_CK(cudaStreamSynchronize(s));
+        const unsigned ovf = (unsigned)h[5];
+        const uint64_t used = h[nctr + (SEG ? 1 : 0)];
+        if (ovf & 1u) {
+            set_error("frontier chunk overflow (internal)");
+            return TPGEN_ERR_INTERNAL;
+        }
+        if (ovf & 2u) {  // head / item buffer: room for all of them, rerun
+            ev_hwm = std::max<uint64_t>(ev_hwm, used);
+            TPG_TRY(evb.ensure((used + used / 4 + 256ull * 4096) * ev_es, s));
+            continue;
+        }
+        float m = 0;
+        cudaEventElapsedTime(&m, t.a, t.b);
+        ms += m;
+        ev_hwm = std::max<uint64_t>(ev_hwm, used);
+        recs += hc.recs;
         for (int q = 0; q < 5; q++) out[q] = h[q];
         *ev_slots = used;
         return TPGEN_OK;

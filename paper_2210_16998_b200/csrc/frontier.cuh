@@ -528,6 +528,7 @@ struct FSchedArgs {
     unsigned long long *ctr;    // ctr[8 + l]: records written to level l's buffer
     ulonglong2 *base;           // level l's key array at base + l * capc (16-byte stride)
     uint64_t *baseS;            // level l's S array at baseS + l * capc (64-bit masks)
+    uint64_t *baseB;            // segment pass: level l's B array at baseB + l * capc
     unsigned long long capc;    // records per level buffer
     unsigned long long chunk;   // records per chunk (capc / the largest out-degree)
     unsigned long long chunk_div;  // the largest out-degree D (a chunk of k records has <= k * D children)
@@ -611,7 +612,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
-template <class T, bool TS, bool HASH>
+template <class T, bool TS, bool HASH, bool HX = false, bool SEG = false>
 __global__ void __launch_bounds__(kFThreads) frontier_walk_kernel(FrontierArgs A, FSchedArgs sa) {
     __shared__ unsigned long long head[kFMaxLevels], tail[kFMaxLevels], take[kFMaxLevels];
     __shared__ unsigned long long s_cnt[kFMaxLevels];
@@ -656,6 +657,10 @@ __global__ void __launch_bounds__(kFThreads) frontier_walk_kernel(FrontierArgs A
             // (level Lm - 1 has no children: level Lm's buffer is never written)
             B.out = sa.base + (size_t)(l + 1) * sa.capc;
             B.out_S = sa.baseS + (size_t)(l + 1) * sa.capc;
+            if constexpr (SEG) {
+                B.in_B = sa.baseB + (size_t)l * sa.capc + h0;
+                B.out_B = sa.baseB + (size_t)(l + 1) * sa.capc;
+            }
             B.ring = sa.capc;
             B.ring_off = tail[l + 1] % sa.capc;
             B.cap = sa.capc - (tail[l + 1] - head[l + 1]);  // free records of the ring
@@ -663,7 +668,7 @@ __global__ void __launch_bounds__(kFThreads) frontier_walk_kernel(FrontierArgs A
             B.l = l;
             B.cnt_in = nullptr;  // (lim bounds the input)
             B.cnt_out = &c->oc[step % 3][l + 1];
-            frontier_level_body<T, TS, HASH, false, false>(B, f, vblk);
+            frontier_level_body<T, TS, HASH, HX, SEG>(B, f, vblk);
             __syncthreads();  // (the body's shared memory is reused by the next level)
         }
         // grid barrier: every block's children of this step are written and counted

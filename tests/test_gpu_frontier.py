@@ -164,6 +164,25 @@ def test_frontier_with_segment_events_matches_oracle():
             (ref["n_paths"], ref["total_vertices"], ref["n_extensions"]), g.name
 
 
+def test_frontier_segment_events_dfs_chunked(monkeypatch):
+    """The DFS-chunked walk (one persistent launch, per-level rings) on graphs whose arcs leave
+    SCCs: forced with rings of max(256, n) records (TPGEN_FRONTIER_CHUNK), and reached by itself under a
+    device-memory budget too small for one level (TPGEN_FRONTIER_BUDGET); equal to the oracle."""
+    graphs = [g for g in _seg_corpus() if not (tp.components(g)[0].size and
+                                               np.bincount(tp.components(g)[0]).max() > 64)]
+    for g in graphs:
+        monkeypatch.setenv("TPGEN_FRONTIER_CHUNK", str(max(256, g.n)))  # (a ring holds every root)
+        assert _frontier(g) == _oracle_stats(g), g.name
+    monkeypatch.delenv("TPGEN_FRONTIER_CHUNK")
+    g = gen.config4(K=40)
+    monkeypatch.setenv("TPGEN_FRONTIER_BUDGET", str(2 << 20))  # 2 MB: rings of ~2000 records per level
+    plan = tp.Plan(g)
+    st = plan.prime_paths(mode="count", digest=True, engine="frontier").stats
+    plan.close()
+    assert {"n_paths": st["n_paths"], "total_vertices": st["total_vertices"], "n_extensions": st["n_extensions"],
+            "digest": (st["hash_lo"], st["hash_hi"])} == _oracle_stats(g)
+
+
 @pytest.mark.timeout(1200)
 def test_frontier_config5_full_size():
     """Config 5 in COUNT_HASH through the frontier engine equals the count-mode DFS (itself equal to
