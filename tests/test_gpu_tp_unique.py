@@ -12,9 +12,11 @@ pytestmark = pytest.mark.gpu
 tp = pytest.importorskip("paper_2210_16998_b200")
 
 
-def _check(g, **kw):
-    ro, rv = oracle.prime_paths(g)
-    uo, uv = oracle.unique_test_paths(g, ro, rv, g.entry, g.exit)
+def _check(g, ref=None, **kw):
+    if ref is None:
+        ro, rv = oracle.prime_paths(g)
+        ref = oracle.unique_test_paths(g, ro, rv, g.entry, g.exit)
+    uo, uv = ref
     ts = tp.test_paths(g, g.entry, g.exit, cover="unique", **kw)
     o, v = ts.to_numpy()
     np.testing.assert_array_equal(o, uo, err_msg=g.name)
@@ -35,10 +37,12 @@ def test_unique_corpus():
 
 def test_unique_config4_full_and_given_prime_list_and_host_output():
     g = gen.config4()  # K = 150
-    _check(g)
+    ro, rv = oracle.prime_paths(g)
+    ref = oracle.unique_test_paths(g, ro, rv, g.entry, g.exit)
+    _check(g, ref)
     pp = tp.prime_paths(g)
-    _check(g, prime=pp)
-    _check(g, output="host")
+    _check(g, ref, prime=pp)
+    _check(g, ref, output="host")
 
 
 def test_unique_rejects_count_mode():
