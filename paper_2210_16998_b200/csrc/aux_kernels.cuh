@@ -816,8 +816,13 @@ struct StitchSArgs {
 // head's digest sum S(h) and the items' (A, B): an item at offset o adds A + 2 o B (R20).
 // Completion k runs over the exit vertex's out-of-SCC arcs in order (W(w) completions each),
 // then is unranked through the entry groups (a binary search per level inside one group).
+// hint_x / hint_i (stitch_big: the first-level group and item of the warp's lane 0, whose
+// completions are the lane's neighbours): when this completion's first level is the same group,
+// the item search starts at hint_i in a window of 64 items (the full search otherwise).
 __device__ __forceinline__ void hash_completion(const StitchSArgs &A, const DevGraph &G, const HeadS &H, uint64_t kk,
-                                                uint64_t &sa, uint64_t &sb, uint64_t &sv) {
+                                                uint64_t &sa, uint64_t &sb, uint64_t &sv, int32_t hint_x = -1,
+                                                int64_t hint_i = -1, int64_t *first_i = nullptr,
+                                                int32_t *first_x = nullptr) {
     const Slot<1> *slots = reinterpret_cast<const Slot<1> *>(G.slots);
     const int4 m = __ldg(reinterpret_cast<const int4 *>(&slots[H.x].gid));
     int32_t x = -1;
@@ -832,14 +837,26 @@ __device__ __forceinline__ void hash_completion(const StitchSArgs &A, const DevG
     }
     uint64_t S = H.S;
     uint32_t pos = (uint32_t)H.len;
+    bool first = true;
     while (true) {
         const int64_t b = A.ibeg[x], e = A.iend[x];
         int64_t i = b;
         uint64_t k2 = kk;
         if (e - b > 1) {
             const uint64_t bc = A.cum[b];
-            i = upper_bound_u64(A.cum, b, e, bc + kk) - 1;
+            int64_t lo = b, hi = e;
+            if (first && x == hint_x && hint_i >= b && hint_i < e && A.cum[hint_i] <= bc + kk) {
+                lo = hint_i;
+                const int64_t w = min(e, hint_i + 64);
+                if (w == e || A.cum[w] > bc + kk) hi = w;
+            }
+            i = upper_bound_u64(A.cum, lo, hi, bc + kk) - 1;
             k2 = kk - (A.cum[i] - bc);
+        }
+        if (first) {
+            if (first_i) *first_i = i;
+            if (first_x) *first_x = x;
+            first = false;
         }
         const ItemS it = A.items[i];
         S += it.A + ((uint64_t)(uint32_t)it.B * (2u * pos) + ((uint64_t)((uint32_t)(it.B >> 32) * (2u * pos)) << 32));
@@ -882,6 +899,7 @@ __device__ __forceinline__ void hash_flush(uint64_t sa, uint64_t sb, uint64_t sv
 }
 
 constexpr uint64_t kSmallHead = 32;  // heads with at most this many completions: one thread each
+constexpr int kBigWarpRun = 8;       // stitch_big: steps of 32 consecutive completions per warp chunk
 
 // Small heads: one thread per head slot hashes all of its W <= kSmallHead completions (no search
 // over the heads); big[h] = 1 marks the others for stitch_big_kernel.
@@ -910,10 +928,26 @@ __global__ void stitch_big_list_kernel(StitchSArgs A, const uint64_t *pos, int64
 __global__ void stitch_big_kernel(StitchSArgs A, DevGraph G, const int64_t *idx, const uint64_t *off, int64_t n_big,
                                   uint64_t n_big_comp, unsigned long long *acc) {
     uint64_t sa = 0, sb = 0, sv = 0;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_big_comp;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t j = upper_bound_u64(off, 0, n_big, g) - 1;
-        hash_completion(A, G, A.heads[idx[j]], g - off[j], sa, sb, sv);
+    const int lane = threadIdx.x & 31;
+    // a warp takes kBigWarpRun * 32 consecutive completions, lane l the ones at l + 32 t: a lane's
+    // first-level item moves forward by about 32 per step, so its search after the first starts at
+    // its previous item (a window of 64) instead of spanning the whole entry group
+    const uint64_t chunk = (uint64_t)kBigWarpRun * 32;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t c0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * chunk; c0 < n_big_comp;
+         c0 += warps * chunk) {
+        int64_t pi = -1;
+        int32_t px = -1;
+        for (int t = 0; t < kBigWarpRun; t++) {
+            const uint64_t g = c0 + (uint64_t)t * 32 + lane;
+            if (g >= n_big_comp) break;
+            const int64_t j = upper_bound_u64(off, 0, n_big, g) - 1;
+            int64_t fi = -1;
+            int32_t fx = -1;
+            hash_completion(A, G, A.heads[idx[j]], g - off[j], sa, sb, sv, px, pi, &fi, &fx);
+            pi = fi;
+            px = fx;
+        }
     }
     hash_flush(sa, sb, sv, acc);
 }
