@@ -59,6 +59,7 @@ struct CntLane {
     int32_t l, r, s, vb;      // depth, unit root depth, start vertex (local), slot base of the SCC
     uint64_t S;               // digest sum of path[0..l]
     uint64_t B;               // segment phase: sum of mix(v) over path[0..l] (an item's offset slope)
+    uint32_t cur;             // D2: the current node's untried children as bytes (byte 0 taken next; 0xff: none)
     bool active, done, emit;  // emit (segment phase): s lies in the call's start range
 };
 
@@ -99,12 +100,34 @@ struct CntTab {
 };
 
 __device__ __forceinline__ int ffs_t(uint32_t x) { return __ffs(x) - 1; }
+__device__ __forceinline__ int ffs_t(uint64_t x) { return __ffsll((long long)x) - 1; }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+// D2: a set of at most 2 children as bytes (0xff: none) -> a mask
+template <class T>
+__device__ __forceinline__ T d2_mask(uint32_t c) {
+    const uint32_t b0 = c & 0xffu, b1 = (c >> 8) & 0xffu;
+    return (b0 != 0xffu ? (T)1 << b0 : (T)0) | (b1 != 0xffu ? (T)1 << b1 : (T)0);
+}
+// ... and back (ascending)
+template <class T>
+__device__ __forceinline__ uint32_t d2_bytes(T m) {
+    const uint32_t b0 = m ? (uint32_t)ffs_t(m) : 0xffu;
+    const T m1 = m & (m - 1);
+    const uint32_t b1 = m1 ? (uint32_t)ffs_t(m1) : 0xffu;
+    return b0 | (b1 << 8);
+}
 // m * w mod 2^64 for a 32-bit w: one wide multiply of the low word, one of the high word
 __device__ __forceinline__ uint64_t mul64x32(uint64_t m, uint32_t w) {
     const uint64_t lo = (uint64_t)(uint32_t)m * w;
     return lo + ((uint64_t)((uint32_t)(m >> 32) * w) << 32);
 }
-__device__ __forceinline__ int ffs_t(uint64_t x) { return __ffsll((long long)x) - 1; }
 
 template <class T>
 struct CntCfg {
@@ -128,9 +151,10 @@ struct CntCfg {
 #endif
 constexpr bool cnt_uses_ring(bool seg) { return (seg && CNT_SEG_RING) || !CNT_QUEUE; }
 template <class T>
-constexpr size_t cnt_smem_block(bool seg) {
+constexpr size_t cnt_smem_block(bool seg, bool d2 = false) {
     return (size_t)CntCfg<T>::warps * ((cnt_uses_ring(seg) ? CntCfg<T>::ring_slots * 32 * (seg ? 20 : 12) : 0) +
-                                       (CntCfg<T>::RS ? 32 * 32 * 4 : 0) + CntCfg<T>::PLEV * 32 + (CNT_QUEUE ? 64 * 12 : 0));
+                                       (CntCfg<T>::RS ? 32 * 32 * 4 : 0) + CntCfg<T>::PLEV * 32 * (d2 ? 2 : 1) +
+                                       (CNT_QUEUE ? 64 * 12 : 0));
 }
 
 // PH: the phase -- P_PP, the prime-path phase; P_TP, the same hashing every prime path's test
@@ -147,8 +171,16 @@ constexpr int cnt_min_blocks(bool seg, bool hsh) {
     return seg ? CNT_MINB_SEG : ((sizeof(T) == 8 && hsh) ? CNT_MINB_PP64H : CntCfg<T>::min_blocks);
 }
 
-template <class T, bool TS, bool HSH, bool HX, int PH>
+// D2 (prime-path phase, table in shared memory, G.slot_d2 set: every in-SCC out-degree <= 2, the
+// normal form of the paper's Fig. 5, and config 5's SCCs): a node has at most two
+// untried children, kept as two bytes instead of a mask (the take is a byte extract, not a 64-bit
+// find-first-set and clear), and a push stores the parent's remaining child next to the child's
+// path byte (one u16 per level), so a pop reads the popped vertex and the parent's untried child
+// with ONE shared load instead of recomputing them from the parent's successor set.
+template <class T, bool TS, bool HSH, bool HX, int PH, bool D2 = false>
 __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_SEG, HSH)) cnt_kernel(DfsArgs A) {
+    static_assert(!D2 || (TS && PH == P_PP), "D2: prime-path phase with the table in shared memory");
+    constexpr uint32_t PST = D2 ? 64u : 32u;  // bytes per path level of a warp's column block
     constexpr bool SEG = PH == P_SEG;
     constexpr bool TRACK_B = PH != P_PP;
     using C = CntCfg<T>;
@@ -167,14 +199,14 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     uint32_t *sringt = reinterpret_cast<uint32_t *>(dyn + WARPS * RSLOTS * 32 * 8);    // [warp][slot][lane]
     uint32_t *srem = sringt + WARPS * RSLOTS * 32;                                      // [warp][level][lane]
     uint8_t *spath = reinterpret_cast<uint8_t *>(srem + (RS ? WARPS * 32 * 32 : 0));  // [warp][level][lane]
-    uint64_t *sq = reinterpret_cast<uint64_t *>(spath + WARPS * PLEV * 32);            // CNT_QUEUE: [warp][64]
+    uint64_t *sq = reinterpret_cast<uint64_t *>(spath + WARPS * PLEV * PST);           // CNT_QUEUE: [warp][64]
     uint32_t *sql = reinterpret_cast<uint32_t *>(sq + (CNT_QUEUE ? WARPS * 64 : 0));  //            [warp][64]
     uint64_t *sringb = reinterpret_cast<uint64_t *>(sql + (CNT_QUEUE ? WARPS * 64 : 0));  // SEG: [warp][slot][lane]
     const DevGraph &G = A.G;
     // 32-bit shared-window addresses of this lane's columns (opaque: kept in registers)
     uint32_t pb, rb, qb, lb, bb = 0;
     if (SEG) asm volatile("mov.b32 %0, %1;" : "=r"(bb) : "r"((uint32_t)__cvta_generic_to_shared(sringb + wid * RSLOTS * 32) + lane * 8));
-    asm volatile("mov.b32 %0, %1;" : "=r"(pb) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * PLEV * 32) + lane));
+    asm volatile("mov.b32 %0, %1;" : "=r"(pb) : "r"((uint32_t)__cvta_generic_to_shared(spath + wid * PLEV * PST) + lane * (PST / 32u)));
     asm volatile("mov.b32 %0, %1;" : "=r"(rb) : "r"((uint32_t)__cvta_generic_to_shared(srem + (RS ? wid * 32 * 32 : 0)) + (RS ? lane * 4 : 0)));
     asm volatile("mov.b32 %0, %1;" : "=r"(qb) : "r"((uint32_t)__cvta_generic_to_shared(sring + wid * RSLOTS * 32) + lane * 8));
     asm volatile("mov.b32 %0, %1;" : "=r"(lb) : "r"((uint32_t)__cvta_generic_to_shared(sringt + wid * RSLOTS * 32) + lane * 4));
@@ -185,12 +217,12 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     if (TS) {
         uint64_t *d = reinterpret_cast<uint64_t *>(stab);
         for (int i = threadIdx.x; i < A.n_slots; i += blockDim.x) {
-            d[2 * i] = __ldg(&tab.g[i].sin[0]);
+            d[2 * i] = D2 ? __ldg(G.slot_d2 + 2 * i) : __ldg(&tab.g[i].sin[0]);
             d[2 * i + 1] = __ldg(G.slot_mix + i);
         }
         asm volatile("mov.b32 %0, %1;" : "=r"(tab.sb) : "r"((uint32_t)__cvta_generic_to_shared(stab)));
     }
-    for (int i = threadIdx.x; i < WARPS * PLEV * 32; i += blockDim.x) spath[i] = 0;  // idle lanes read vertex 0
+    for (int i = threadIdx.x; i < WARPS * PLEV * (int)PST; i += blockDim.x) spath[i] = 0;  // idle lanes read vertex 0
     if (threadIdx.x == 0) {
         s_td = 1ull << 32;
         s_head = 1ull << 20;
@@ -209,6 +241,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     L.l = L.r = L.s = L.vb = 0;
     L.M = L.rem = L.sbit = L.ps = L.exm = 0;
     L.S = L.B = 0;
+    L.cur = 0xffffu;
     L.emit = true;
     bool waiting = false, exited = false;
     int64_t slot = -1;
@@ -481,7 +514,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                         const int i = q * 4 + b;
                         if (i <= depth) {
                             const int x = (int)((wv >> (8 * b)) & 0xffu);
-                            sts_u8(pb + (uint32_t)i * 32u, x);
+                            sts_u8(pb + (uint32_t)i * PST, x);
                             const uint64_t mx = tab.mix(L.vb + x);
                             S0 += mul64x32(mx, 2u * (uint32_t)i + 1u);
                             B0 += mx;
@@ -492,7 +525,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 L.s = (int)(__ldcg(p4) & 0xffu);
                 L.sbit = (T)1 << L.s;
                 L.ps = tab.pin(L.vb + L.s);
-                L.exm = (HX || SEG) ? (T)__ldg(G.scc_exm + uscc) : (T)0;
+                if constexpr (!D2) L.exm = (HX || SEG) ? (T)__ldg(G.scc_exm + uscc) : (T)0;
                 L.S = S0;
                 L.B = B0;
                 if constexpr (SEG) {
@@ -511,13 +544,15 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     st_len = (uint32_t)depth + 2;
                     st_slot = L.vb + L.s;
                     L.rem = 0;
+                    L.cur = 0xffffu;
                     L.done = true;
                 } else {  // K_NODE: the node's own event, then its subtree
                     if (depth > 0 && L.emit) t_ext += 1;
                     const T ub = (T)1 << u;
-                    const T su = tab.sin(L.vb + u);
+                    const T su = D2 ? (T)__ldg(&tab.g[L.vb + u].sin[0]) : tab.sin(L.vb + u);
                     L.rem = su & (~L.M | L.sbit);
-                    const bool ex = ((L.exm >> u) & 1) != 0;
+                    if constexpr (D2) L.cur = d2_bytes<T>(L.rem);
+                    const bool ex = D2 ? ((__ldg(G.slot_d2 + 2 * (L.vb + u)) >> 16) & 1) != 0 : ((L.exm >> u) & 1) != 0;
                     if constexpr (SEG) {  // tail segment (succ(u) on the path) or transit segments (R8, R9)
                         st_other = ex || (su & ~L.M) == 0;
                         st_kind = ex ? EK_TRANSIT : EK_TAIL;
@@ -586,6 +621,51 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
         for (int blk = 0; blk < CNT_PASSES / RING; blk++) {
 #pragma unroll 1
             for (int t = 0; t < RING; t++) {
+              if constexpr (D2) {
+                const bool act = L.active && !L.done;
+                const uint32_t cur = L.cur;
+                const int l = L.l;
+                const uint32_t a = cur & 0xffu;  // (take) the child
+                const bool empty = a == 0xffu;
+                if (act & empty & (l == L.r)) L.done = true;  // the unit's subtree is finished
+                const bool pop = act & empty & (l > L.r);
+                TPG_DCHECK(!act || (l >= L.r && l < PLEV), "cnt: depth out of range");
+                const bool take = act & !empty;
+                const uint32_t e = lds_u16(pb + (uint32_t)l * PST);  // {path[l], the untried child of level l-1}
+                const int v = take ? (int)a : (int)(e & 0xffu);     // the child, or the vertex popped
+                const int vslot = L.vb + v;
+                uint64_t wd, mv;  // {t0 | t1 << 8 | exit << 16, mix64(gid)} of v
+                asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(wd), "=l"(mv) : "r"(tab.sb + (uint32_t)vslot * 16u) : "memory");
+                const uint64_t prod = mul64x32(mv, 2u * (uint32_t)(take ? l + 1 : l) + 1u);
+                const T vbit = (T)1 << v;
+                const T Mw = L.M | vbit;
+                const T avail = ~Mw | L.sbit;  // vertices a child of v may move to
+                const uint32_t w32 = (uint32_t)wd;
+                const uint32_t t0 = w32 & 0xffu, t1 = (w32 >> 8) & 0xffu;  // (a missing one is v: never available)
+                // straight-line (bitwise, no short-circuit branches): the availability bits of t0, t1
+                const uint32_t ok0 = (uint32_t)(avail >> t0) & 1u, ok1 = (uint32_t)(avail >> t1) & 1u;
+                const uint32_t first = ok0 ? t0 : (ok1 ? t1 : 0xffu);
+                const uint32_t cw = first | ((ok0 & ok1) ? (t1 << 8) : 0xff00u);
+                const bool clo = (int)a == L.s;
+                const bool ex = HX && ((w32 >> 16) & 1u) != 0;
+                const bool leaf = (ok0 | ok1) == 0u;
+                const bool pok = (L.ps & ~L.M) == 0;   // pred(s) within path[0..l]
+                const bool pokw = (L.ps & ~Mw) == 0;   // ... within path[0..l] + v
+                const bool pp = take & (clo | (leaf & pok & !ex));
+                const bool other = HX & take & !clo & ex & pokw;  // a head segment
+                const bool push = take & !clo & !leaf;
+                const uint64_t Sw = L.S + prod;
+                if (push) {
+                    TPG_DCHECK(l + 1 < PLEV, "cnt: path deeper than the lane's column");
+                    sts_u16(pb + (uint32_t)(l + 1) * PST, cur);  // {w, the untried child left at level l}
+                }
+                ext32 += take ? 1u : 0u;
+                L.M = (push | pop) ? (L.M ^ vbit) : L.M;
+                L.S = push ? Sw : (pop ? L.S - prod : L.S);
+                L.l = l + (push ? 1 : 0) - (pop ? 1 : 0);
+                L.cur = push ? cw : (pop ? ((e >> 8) | 0xff00u) : (take ? ((cur >> 8) | 0xff00u) : cur));
+                put_ev(pp, other, EK_HEAD, Sw, 0, (uint32_t)l + 2, vslot);
+              } else {
                 const bool act = L.active && !L.done;
                 const T rem = L.rem;
                 const int l = L.l;
@@ -595,7 +675,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 TPG_DCHECK(!act || (l >= L.r && l < PLEV), "cnt: depth out of range");
                 const bool take = act && !empty;
                 const int w = ffs_t(rem);                     // (take) the child
-                const int u = lds_u8(pb + (uint32_t)l * 32u);  // (pop) the vertex popped
+                const int u = lds_u8(pb + (uint32_t)l * PST);  // (pop) the vertex popped
                 const int v = take ? w : u;
                 const int vslot = L.vb + v;                   // (idle lanes: a valid slot of their last SCC)
                 const uint64_t mv = tab.mix(vslot);
@@ -625,7 +705,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     if (pop) rem_pop = (T)lds_u32(rb + (uint32_t)(l - 1) * 128u);
                 } else {
                     if (pop) {  // the parent's successors above u that are still open
-                        const int p = lds_u8(pb + (uint32_t)(l - 1) * 32u);
+                        const int p = lds_u8(pb + (uint32_t)(l - 1) * PST);
                         const T above = (u >= 63) ? (T)0 : ((~(T)0) << (u + 1));
                         rem_pop = tab.sin(L.vb + p) & (~(L.M & ~vbit) | L.sbit) & above;
                     }
@@ -633,7 +713,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 if (push) {
                     TPG_DCHECK(l + 1 < PLEV, "cnt: path deeper than the lane's column");
                     if constexpr (RS) sts_u32(rb + (uint32_t)l * 128u, (uint32_t)(rem & (rem - 1)));
-                    sts_u8(pb + (uint32_t)(l + 1) * 32u, w);
+                    sts_u8(pb + (uint32_t)(l + 1) * PST, w);
                 }
                 ext32 += (take && (!SEG || L.emit)) ? 1u : 0u;
                 L.M = (push || pop) ? (L.M ^ vbit) : L.M;
@@ -664,6 +744,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 }
 #endif
                 put_ev(pp, other, kind, Sw, Bw, (uint32_t)l + 2, vslot);
+              }
             }
             drain();
         }
@@ -679,14 +760,16 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 for (int j = L.l; j >= L.r; j--) {
                     T c;
                     if (j == L.l) {
-                        c = L.rem;
+                        c = D2 ? d2_mask<T>(L.cur) : L.rem;
                     } else {
-                        const int wc = lds_u8(pb + (uint32_t)(j + 1) * 32u);  // the child of level j on the path
+                        const int wc = lds_u8(pb + (uint32_t)(j + 1) * PST);  // the child of level j on the path
                         M &= ~((T)1 << wc);
-                        if constexpr (RS) {
+                        if constexpr (D2) {
+                            c = d2_mask<T>((uint32_t)lds_u8(pb + (uint32_t)(j + 1) * PST + 1u) | 0xff00u);
+                        } else if constexpr (RS) {
                             c = (T)lds_u32(rb + (uint32_t)j * 128u);
                         } else {
-                            const int p = lds_u8(pb + (uint32_t)j * 32u);
+                            const int p = lds_u8(pb + (uint32_t)j * PST);
                             const T above = (wc >= 63) ? (T)0 : ((~(T)0) << (wc + 1));
                             c = tab.sin(L.vb + p) & (~M | L.sbit) & above;
                         }
@@ -704,7 +787,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     atomicOr(A.overflow, 4u);
                 } else {
                     T M = L.M;  // the mask of path[0..j0]
-                    for (int j = j0 + 1; j <= L.l; j++) M &= ~((T)1 << lds_u8(pb + (uint32_t)j * 32u));
+                    for (int j = j0 + 1; j <= L.l; j++) M &= ~((T)1 << lds_u8(pb + (uint32_t)j * PST));
                     T c = c0;
                     for (int n = 0; n < m; n++) {
                         const int w = ffs_t(c);
@@ -715,7 +798,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                             uint32_t wv = 0;
 #pragma unroll
                             for (int b = 0; b < 4; b++)
-                                if (q * 4 + b <= j0) wv |= (uint32_t)lds_u8(pb + (uint32_t)(q * 4 + b) * 32u) << (8 * b);
+                                if (q * 4 + b <= j0) wv |= (uint32_t)lds_u8(pb + (uint32_t)(q * 4 + b) * PST) << (8 * b);
                             reinterpret_cast<uint32_t *>(U.path)[q] = wv;
                         }
                         uint64_t Mu = (uint64_t)M;

@@ -138,7 +138,7 @@ PlanImpl::~PlanImpl() {
 
 std::vector<DevBuf *> PlanImpl::all_bufs() {
     std::vector<DevBuf *> v = {&d_slots, &d_slot_gid, &d_out_gid, &d_out_pos, &d_scc_vbase, &d_scc_out_base,
-                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_v_slot, &d_slot_mix, &d_vmix, &d_scc_exm, &cheads, &tp_terms, &citems, &citems2, &icnt,
+                               &d_scc_nout, &d_scc_pair_base, &d_slot_eidx, &d_Wc, &d_Wv, &d_scc_gbase, &d_comp, &d_v_slot, &d_slot_mix, &d_vmix, &d_scc_exm, &d_slot_d2, &cheads, &tp_terms, &citems, &citems2, &icnt,
                                &qunits, &qready, &qext, &qrfirst, &qrcount, &qchead, &blk_first, &blk_count, &blk_next, &qgen, &roots, &qparent, &qnchild,
                                &scan_b, &scan_tot, &ctr, &agg, &agg_bak, &heads, &head_pool, &items, &item_pool,
                                &icum, &ivcum, &ibeg, &iend, &hcomp, &offs, &tp_tabs, &chunks, &dbgbuf, &qctr, &sscratch, &presplit_dev, &presplit_roots, &rscan,
@@ -198,6 +198,29 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
             for (int32_t i = 0; i < H.scc_size[c] && i < 64; i++)
                 if (H.slot_out_cnt[H.scc_vbase[c] + i] > 0) exm[c] |= 1ull << i;
         TPG_TRY(upload(P.d_scc_exm, exm, s));
+        // out-degree-2 table of the count kernel's D2 variant (count.cuh): per slot the local ids of
+        // its (at most 2) in-SCC successors t0 < t1 -- a missing one is the slot's OWN local id,
+        // whose bit is always on the path when the slot is the child being taken -- the exit flag
+        // (Def. 5) and the digest value mix64(gid)
+        bool d2 = H.max_scc <= 64 && H.W == 1;
+        std::vector<uint64_t> t2(2 * (size_t)std::max(H.n, 1), 0);
+        for (int32_t c = 0; c < H.n_scc && d2; c++)
+            for (int32_t i = 0; i < H.scc_size[c]; i++) {
+                const int32_t sl = H.scc_vbase[c] + i;
+                uint64_t sn = H.sin[(size_t)sl * H.W];
+                if (__builtin_popcountll(sn) > 2) {
+                    d2 = false;
+                    break;
+                }
+                const uint64_t t0 = sn ? (uint64_t)__builtin_ctzll(sn) : (uint64_t)i;
+                sn &= sn - 1;
+                const uint64_t t1 = sn ? (uint64_t)__builtin_ctzll(sn) : (uint64_t)i;
+                t2[2 * (size_t)sl] = t0 | (t1 << 8) | ((H.slot_out_cnt[sl] > 0 ? 1ull : 0ull) << 16);
+                t2[2 * (size_t)sl + 1] = sm[sl];
+            }
+        if (const char *ev = getenv("TPGEN_NO_D2")) d2 = d2 && atoi(ev) == 0;  // A/B hook
+        P.d2_ok = d2;
+        if (d2) TPG_TRY(upload(P.d_slot_d2, t2, s));
     }
     P.chead_hwm = 0;
     TPG_TRY(P.d_Wc.ensure(std::max<size_t>(H.n, 1) * 8, s));
@@ -225,6 +248,7 @@ static DevGraph dev_graph(PlanImpl &P, int32_t lo, int32_t hi) {
     G.slot_mix = P.d_slot_mix.as<uint64_t>();
     G.vmix = P.d_vmix.as<uint64_t>();
     G.scc_exm = P.d_scc_exm.as<uint64_t>();
+    G.slot_d2 = P.d2_ok ? P.d_slot_d2.as<uint64_t>() : nullptr;
     G.v_slot = P.d_v_slot.as<int32_t>();
     G.comp = P.d_comp.as<int32_t>();
     G.shard_lo = lo;
@@ -645,9 +669,13 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
                           cnt_min_blocks<CT>(seg, HSH || A.tp != nullptr);
         const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
         const bool ts = ctab <= kSmemTabMax;
-        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg);
+        // D2: the out-degree-2 prime-path kernel (count.cuh) when the plan's table allows it
+        const bool d2 = !seg && A.tp == nullptr && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8;
+        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg, d2);
         void (*k)(DfsArgs);
-        if (seg) {
+        if (d2) {
+            if constexpr (sizeof(CT) == 8) k = any_exit ? cnt_kernel<CT, true, HSH, true, P_PP, true> : cnt_kernel<CT, true, HSH, false, P_PP, true>;
+        } else if (seg) {
             k = ts ? cnt_kernel<CT, true, HSH, true, P_SEG> : cnt_kernel<CT, false, HSH, true, P_SEG>;
         } else if (A.tp != nullptr) {
             k = ts ? (any_exit ? cnt_kernel<CT, true, true, true, P_TP> : cnt_kernel<CT, true, true, false, P_TP>)

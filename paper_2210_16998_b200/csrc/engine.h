@@ -37,7 +37,9 @@ struct PlanImpl {
     double ms_plan = 0;
     // device tables
     DevBuf d_slots, d_slot_gid, d_out_gid, d_out_pos, d_scc_vbase, d_scc_out_base, d_scc_nout, d_scc_pair_base,
-        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase, d_comp, d_slot_mix, d_vmix, d_scc_exm, d_v_slot;
+        d_slot_eidx, d_Wc, d_Wv, d_scc_gbase, d_comp, d_slot_mix, d_vmix, d_scc_exm, d_v_slot,
+        d_slot_d2;  // count modes, SCCs of in-SCC out-degree <= 2: {t0 | t1 << 8 | exit << 16, mix} per slot
+    bool d2_ok = false;  // every slot has at most 2 in-SCC successors and every SCC at most 64 vertices
     DevBuf cheads;           // count modes: HeadS records of the prime-path phase
     DevBuf citems, citems2;  // count modes: ItemS records of the segment phase (as written; grouped by entry)
     DevBuf icnt;             // count modes: items per entry vertex, their scan, the scatter cursors
