@@ -49,6 +49,9 @@ namespace tpg {
 #ifndef CNT_QUEUE
 #define CNT_QUEUE 1  // 1: prime paths into a per-warp queue (ballot), hashed 32 at a time; 0: per-lane rings
 #endif
+#ifndef CNT_D2_POPS
+#define CNT_D2_POPS 0  // D2: 0 -- one move per pass (a pop or a take); k > 0 -- up to k pops, then a take, per pass
+#endif
 #ifndef CNT_PASSES
 #define CNT_PASSES 32  // passes of the step between two rounds of queue housekeeping
 #endif
@@ -265,6 +268,42 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     asm volatile("mov.b32 %0, %1;" : "=r"(qLa) : "r"((uint32_t)__cvta_generic_to_shared(sql + (CNT_QUEUE ? wid * 64 : 0))));
     uint32_t qn = 0;  // CNT_QUEUE: queued prime paths of the warp (warp-uniform, < 32 between hashes)
     const uint32_t ltm = (1u << lane) - 1u;
+    constexpr bool CQ = D2 && HSH && HX && CNT_QUEUE && !USE_RING;
+    uint32_t r_pp = 0, r_vert = 0;  // prime paths / their vertices since the last flush into t_pp / t_vert
+    // CQ: one queued event per lane (warp-uniform call): a prime path is hashed (the two finalizers,
+    // R20); a head segment (tag bit 31; bits 8-30 the slot of its last vertex, 0-7 |h|) becomes a
+    // HeadS in the warp's block of head slots
+    auto cq_flush = [&](bool valid, uint64_t z, uint32_t tag) {
+        const bool hd = valid && (tag >> 31) != 0u;
+        if (valid && !hd) {
+            const uint64_t n = tag & 0xffu;
+            t_ha += mix64(z ^ (kSeedA + n));
+            t_hb += mix64(z ^ (kSeedB + n));
+        }
+        const uint32_t hbm = __ballot_sync(kFull, hd);
+        if (hbm) {
+            const uint32_t need = __popc(hbm);
+            if (hblk + need > hblk_end) {  // a new block of 256 slots (the rest of the old one: holes)
+                for (unsigned long long q = hblk + lane; q < hblk_end; q += 32)
+                    if (q < A.head_cap) A.heads[q].x = -1;
+                unsigned long long b = 0;
+                if (lane == 0) b = atomicAdd(A.cacc + 5, 256ull);
+                b = __shfl_sync(kFull, b, 0);
+                hblk = b;
+                hblk_end = b + 256;
+                if (b + 256 > A.head_cap && lane == 0) atomicOr(A.overflow, 8u);
+            }
+            const unsigned long long q = hblk + __popc(hbm & ltm);
+            if (hd && q < A.head_cap) {
+                HeadS hr;
+                hr.S = z;
+                hr.len = (int32_t)(tag & 0xffu);
+                hr.x = (int32_t)((tag >> 8) & 0x7fffffu);
+                *reinterpret_cast<ulonglong2 *>(A.heads + q) = *reinterpret_cast<const ulonglong2 *>(&hr);
+            }
+            hblk += need;
+        }
+    };
     auto put_ev = [&](bool pp, bool other, uint32_t kind, uint64_t Sx, uint64_t Bx, uint32_t len, int slot_) {
         if ((PH == P_TP || (SEG && A.tp != nullptr)) && (pp || (other && kind == EK_HEAD))) {
             // test paths instead (R15): the prefix walk of s before the path, the suffix walk of its
@@ -276,11 +315,32 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
             if (!ok) atomicOr(A.overflow, 16u);
             if (pp) len = lt;
         }
-        if (pp) {
-            t_pp += 1;
-            t_vert += len;
+        if (pp) {  // (32-bit per round of passes; added to the 64-bit totals after the passes)
+            r_pp += 1;
+            r_vert += len;
         }
-        if constexpr (HSH && CNT_QUEUE) {
+        if constexpr (CQ) {  // D2 + digest + exits: prime paths AND head segments through the warp's queue
+            const bool ev = pp || other;
+            const uint32_t bal = __ballot_sync(kFull, ev);
+            if (ev) {
+                const uint32_t j = qn + __popc(bal & ltm);
+                TPG_DCHECK(j < 64, "cnt: warp queue overflow");
+                const uint32_t tag = other ? (0x80000000u | ((uint32_t)slot_ << 8) | len) : len;
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(qSa + j * 8u), "l"(Sx) : "memory");
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(qLa + j * 4u), "r"(tag) : "memory");
+            }
+            qn += __popc(bal);
+            if (qn >= 32) {
+                __syncwarp();
+                qn -= 32;
+                uint64_t z;
+                uint32_t tag;
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qSa + (qn + lane) * 8u) : "memory");
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tag) : "r"(qLa + (qn + lane) * 4u) : "memory");
+                __syncwarp();
+                cq_flush(true, z, tag);
+            }
+        } else if constexpr (HSH && CNT_QUEUE) {
             const uint32_t bal = __ballot_sync(kFull, pp);
             if (pp) {
                 const uint32_t j = qn + __popc(bal & ltm);
@@ -302,7 +362,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 __syncwarp();
             }
         }
-        if constexpr (HX && !SEG && !USE_RING) {  // a head segment: written at once (one HeadS per head node)
+        if constexpr (HX && !SEG && !USE_RING && !CQ) {  // a head segment: written at once (one HeadS per head node)
             const uint32_t hbm = __ballot_sync(kFull, other);
             if (hbm) {
                 const uint32_t need = __popc(hbm);
@@ -623,15 +683,27 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
             for (int t = 0; t < RING; t++) {
               if constexpr (D2) {
                 const bool act = L.active && !L.done;
+#pragma unroll
+                for (int k = 0; k < CNT_D2_POPS; k++) {  // pops first (straight-line, predicated)
+                    const bool pk = act & ((L.cur & 0xffu) == 0xffu) & (L.l > L.r);
+                    const uint32_t ek = lds_u16(pb + (uint32_t)L.l * PST);
+                    const int uk = (int)(ek & 0xffu);
+                    const uint64_t prk = mul64x32(tab.mix(L.vb + uk), 2u * (uint32_t)L.l + 1u);
+                    const T ubk = (T)1 << uk;
+                    L.M = pk ? (L.M ^ ubk) : L.M;
+                    L.S = pk ? (L.S - prk) : L.S;
+                    L.l -= pk ? 1 : 0;
+                    L.cur = pk ? ((ek >> 8) | 0xff00u) : L.cur;
+                }
                 const uint32_t cur = L.cur;
                 const int l = L.l;
                 const uint32_t a = cur & 0xffu;  // (take) the child
                 const bool empty = a == 0xffu;
                 if (act & empty & (l == L.r)) L.done = true;  // the unit's subtree is finished
-                const bool pop = act & empty & (l > L.r);
+                const bool pop = (CNT_D2_POPS == 0) & act & empty & (l > L.r);
                 TPG_DCHECK(!act || (l >= L.r && l < PLEV), "cnt: depth out of range");
                 const bool take = act & !empty;
-                const uint32_t e = lds_u16(pb + (uint32_t)l * PST);  // {path[l], the untried child of level l-1}
+                const uint32_t e = CNT_D2_POPS == 0 ? lds_u16(pb + (uint32_t)l * PST) : 0u;  // {path[l], the untried child of level l-1}
                 const int v = take ? (int)a : (int)(e & 0xffu);     // the child, or the vertex popped
                 const int vslot = L.vb + v;
                 uint64_t wd, mv;  // {t0 | t1 << 8 | exit << 16, mix64(gid)} of v
@@ -749,6 +821,9 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
             drain();
         }
         t_ext += ext32;
+        t_pp += r_pp;
+        t_vert += r_vert;
+        r_pp = r_vert = 0;
         if (L.active) steps += CNT_PASSES;
 
         // ---------------- donate on demand: the untried children of the shallowest open level
@@ -825,7 +900,18 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
             L.done = false;
         }
     }
-    if constexpr (HSH && CNT_QUEUE) {  // the queue's remainder
+    t_pp += r_pp;
+    t_vert += r_vert;
+    if constexpr (CQ) {  // the queue's remainder
+        __syncwarp();
+        uint64_t z = 0;
+        uint32_t tag = 0;
+        if (lane < qn) {
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(z) : "r"(qSa + lane * 8u) : "memory");
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tag) : "r"(qLa + lane * 4u) : "memory");
+        }
+        cq_flush(lane < qn, z, tag);
+    } else if constexpr (HSH && CNT_QUEUE) {  // the queue's remainder
         __syncwarp();
         if (lane < qn) {
             uint64_t z;

@@ -202,7 +202,7 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
         // its (at most 2) in-SCC successors t0 < t1 -- a missing one is the slot's OWN local id,
         // whose bit is always on the path when the slot is the child being taken -- the exit flag
         // (Def. 5) and the digest value mix64(gid)
-        bool d2 = H.max_scc <= 64 && H.W == 1;
+        bool d2 = H.max_scc <= 64 && H.W == 1 && H.n < (1 << 23);  // (slots fit the queue tag, count.cuh)
         std::vector<uint64_t> t2(2 * (size_t)std::max(H.n, 1), 0);
         for (int32_t c = 0; c < H.n_scc && d2; c++)
             for (int32_t i = 0; i < H.scc_size[c]; i++) {
