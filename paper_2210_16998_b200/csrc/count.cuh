@@ -50,7 +50,8 @@ namespace tpg {
 #define CNT_QUEUE 1  // 1: prime paths into a per-warp queue (ballot), hashed 32 at a time; 0: per-lane rings
 #endif
 #ifndef CNT_D2_POPS
-#define CNT_D2_POPS 0  // D2: 0 -- one move per pass (a pop or a take); k > 0 -- up to k pops, then a take, per pass
+#define CNT_D2_POPS 2  // D2: 0 -- one move per pass (a pop or a take); k > 0 -- up to k pops, then a take, per pass
+                       // (config 5 cnt_kernel, one box: k = 0 / 1 / 2 / 3 / 4 -> 123.8 / 118.1 / 112.0 / 118.7 / 130.1 ms)
 #endif
 #ifndef CNT_PASSES
 #define CNT_PASSES 32  // passes of the step between two rounds of queue housekeeping
@@ -182,7 +183,7 @@ constexpr int cnt_min_blocks(bool seg, bool hsh) {
 // with ONE shared load instead of recomputing them from the parent's successor set.
 template <class T, bool TS, bool HSH, bool HX, int PH, bool D2 = false>
 __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_SEG, HSH)) cnt_kernel(DfsArgs A) {
-    static_assert(!D2 || (TS && PH == P_PP), "D2: prime-path phase with the table in shared memory");
+    static_assert(!D2 || (TS && PH != P_TP), "D2: prime-path or segment phase with the table in shared memory");
     constexpr uint32_t PST = D2 ? 64u : 32u;  // bytes per path level of a warp's column block
     constexpr bool SEG = PH == P_SEG;
     constexpr bool TRACK_B = PH != P_PP;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     asm volatile("mov.b32 %0, %1;" : "=r"(qLa) : "r"((uint32_t)__cvta_generic_to_shared(sql + (CNT_QUEUE ? wid * 64 : 0))));
     uint32_t qn = 0;  // CNT_QUEUE: queued prime paths of the warp (warp-uniform, < 32 between hashes)
     const uint32_t ltm = (1u << lane) - 1u;
-    constexpr bool CQ = D2 && HSH && HX && CNT_QUEUE && !USE_RING;
+    constexpr bool CQ = D2 && PH == P_PP && HSH && HX && CNT_QUEUE && !USE_RING;
     uint32_t r_pp = 0, r_vert = 0;  // prime paths / their vertices since the last flush into t_pp / t_vert
     // CQ: one queued event per lane (warp-uniform call): a prime path is hashed (the two finalizers,
     // R20); a head segment (tag bit 31; bits 8-30 the slot of its last vertex, 0-7 |h|) becomes a
@@ -688,10 +689,12 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     const bool pk = act & ((L.cur & 0xffu) == 0xffu) & (L.l > L.r);
                     const uint32_t ek = lds_u16(pb + (uint32_t)L.l * PST);
                     const int uk = (int)(ek & 0xffu);
-                    const uint64_t prk = mul64x32(tab.mix(L.vb + uk), 2u * (uint32_t)L.l + 1u);
+                    const uint64_t mk = tab.mix(L.vb + uk);
+                    const uint64_t prk = mul64x32(mk, 2u * (uint32_t)L.l + 1u);
                     const T ubk = (T)1 << uk;
                     L.M = pk ? (L.M ^ ubk) : L.M;
                     L.S = pk ? (L.S - prk) : L.S;
+                    if constexpr (TRACK_B) L.B = pk ? (L.B - mk) : L.B;
                     L.l -= pk ? 1 : 0;
                     L.cur = pk ? ((ek >> 8) | 0xff00u) : L.cur;
                 }
@@ -723,20 +726,29 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 const bool leaf = (ok0 | ok1) == 0u;
                 const bool pok = (L.ps & ~L.M) == 0;   // pred(s) within path[0..l]
                 const bool pokw = (L.ps & ~Mw) == 0;   // ... within path[0..l] + v
-                const bool pp = take & (clo | (leaf & pok & !ex));
-                const bool other = HX & take & !clo & ex & pokw;  // a head segment
+                bool pp, other;
+                if constexpr (SEG) {  // cycles are prime paths; tail / transit segments become items (R8, R9)
+                    const uint32_t in0 = (uint32_t)(Mw >> t0) & 1u, in1 = (uint32_t)(Mw >> t1) & 1u;
+                    pp = take & clo & L.emit;
+                    other = take & !clo & (ex | ((in0 & in1) != 0u));
+                } else {
+                    pp = take & (clo | (leaf & pok & !ex));
+                    other = HX & take & !clo & ex & pokw;  // a head segment
+                }
                 const bool push = take & !clo & !leaf;
                 const uint64_t Sw = L.S + prod;
+                const uint64_t Bw = L.B + mv;
                 if (push) {
                     TPG_DCHECK(l + 1 < PLEV, "cnt: path deeper than the lane's column");
                     sts_u16(pb + (uint32_t)(l + 1) * PST, cur);  // {w, the untried child left at level l}
                 }
-                ext32 += take ? 1u : 0u;
+                ext32 += (take && (!SEG || L.emit)) ? 1u : 0u;
                 L.M = (push | pop) ? (L.M ^ vbit) : L.M;
                 L.S = push ? Sw : (pop ? L.S - prod : L.S);
+                if constexpr (TRACK_B) L.B = push ? Bw : (pop ? L.B - mv : L.B);
                 L.l = l + (push ? 1 : 0) - (pop ? 1 : 0);
                 L.cur = push ? cw : (pop ? ((e >> 8) | 0xff00u) : (take ? ((cur >> 8) | 0xff00u) : cur));
-                put_ev(pp, other, EK_HEAD, Sw, 0, (uint32_t)l + 2, vslot);
+                put_ev(pp, other, SEG ? (ex ? EK_TRANSIT : EK_TAIL) : EK_HEAD, Sw, Bw, (uint32_t)l + 2, vslot);
               } else {
                 const bool act = L.active && !L.done;
                 const T rem = L.rem;

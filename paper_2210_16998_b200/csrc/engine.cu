@@ -671,10 +671,13 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         const bool ts = ctab <= kSmemTabMax;
         // D2: the out-degree-2 prime-path kernel (count.cuh) when the plan's table allows it
         const bool d2 = !seg && A.tp == nullptr && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8;
-        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg, d2);
+        const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg, d2 || (seg && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8));
         void (*k)(DfsArgs);
+        const bool d2seg = seg && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8;
         if (d2) {
             if constexpr (sizeof(CT) == 8) k = any_exit ? cnt_kernel<CT, true, HSH, true, P_PP, true> : cnt_kernel<CT, true, HSH, false, P_PP, true>;
+        } else if (d2seg) {
+            if constexpr (sizeof(CT) == 8) k = cnt_kernel<CT, true, HSH, true, P_SEG, true>;
         } else if (seg) {
             k = ts ? cnt_kernel<CT, true, HSH, true, P_SEG> : cnt_kernel<CT, false, HSH, true, P_SEG>;
         } else if (A.tp != nullptr) {
