@@ -53,6 +53,9 @@ namespace tpg {
 #define CNT_D2_POPS 2  // D2: 0 -- one move per pass (a pop or a take); k > 0 -- up to k pops, then a take, per pass
                        // (config 5 cnt_kernel, one box: k = 0 / 1 / 2 / 3 / 4 -> 123.8 / 118.1 / 112.0 / 118.7 / 130.1 ms)
 #endif
+#ifndef CNT_D2_SELFREE
+#define CNT_D2_SELFREE 0  // D2 pops: predicates folded into the multiplier / shift instead of 64-bit selects
+#endif
 #ifndef CNT_PASSES
 #define CNT_PASSES 32  // passes of the step between two rounds of queue housekeeping
 #endif
@@ -690,10 +693,21 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     const uint32_t ek = lds_u16(pb + (uint32_t)L.l * PST);
                     const int uk = (int)(ek & 0xffu);
                     const uint64_t mk = tab.mix(L.vb + uk);
+#if CNT_D2_SELFREE
+                    // predicate folded into the operands (no 64-bit selects on the ALU pipe, the kernel's
+                    // limiting pipe): the multiplier is 0 and the shift 64 (PTX clamps: a zero bit) when
+                    // this lane does not pop
+                    const uint64_t prk = mul64x32(mk, pk ? 2u * (uint32_t)L.l + 1u : 0u);
+                    uint64_t ubk;
+                    asm("shl.b64 %0, %1, %2;" : "=l"(ubk) : "l"(1ull), "r"(pk ? (uint32_t)uk : 64u));
+                    L.M ^= (T)ubk;
+                    L.S -= prk;
+#else
                     const uint64_t prk = mul64x32(mk, 2u * (uint32_t)L.l + 1u);
                     const T ubk = (T)1 << uk;
                     L.M = pk ? (L.M ^ ubk) : L.M;
                     L.S = pk ? (L.S - prk) : L.S;
+#endif
                     if constexpr (TRACK_B) L.B = pk ? (L.B - mk) : L.B;
                     L.l -= pk ? 1 : 0;
                     L.cur = pk ? ((ek >> 8) | 0xff00u) : L.cur;

@@ -399,9 +399,51 @@ __device__ __forceinline__ int lean_node_event(uint32_t c, uint32_t ps, uint32_t
     return (emit && c == 0u && (ps & ~Mp) == 0u) ? (EV_PP | ((l + 1) << 8)) : 0;
 }
 
+#ifndef LEAN_PRED
+#define LEAN_PRED 0  // 1: the LEAN step as one straight-line predicated stream (pops, then the take)
+#endif
 template <bool TS, bool CNT>
 __device__ __forceinline__ int lean_step(const TabView<1, TS> &tab, const MixTab<TS> &mt, Lane<uint32_t> &L,
                                          uint32_t mp, uint32_t rp, uint32_t &ext) {
+#if LEAN_PRED
+    // the same moves as below, without branches: every lane executes every instruction, the
+    // predicates select (the walk order, hence the record stream, is unchanged)
+#pragma unroll
+    for (int x = 0; x < LEAN_POPS; x++) {
+        const bool pk = (L.sin == 0u) & (L.l > L.r);
+        const int u = lds_u8(mp + pidx(L.l));
+        if (CNT) L.S -= pk ? mt(L.vb + u) * pos_weight((uint32_t)L.l) : 0ull;
+        const int lp = pk ? L.l - 1 : L.l;
+        const uint32_t rem = lane_rem(rp, lp);
+        L.sin = pk ? rem : L.sin;
+        L.M &= pk ? ~(1u << u) : ~0u;
+        L.base = pk ? min(L.base, lp + 1) : L.base;
+        L.l = lp;
+    }
+    const bool empty = L.sin == 0u;
+    if (empty & (L.l == L.r)) L.done = true;
+    const bool take = !empty;
+    const int w = __ffs(L.sin) - 1;  // (take)
+    const int wv = take ? w : 0;     // (lanes that do not take read local vertex 0: a valid slot)
+    const uint32_t rest = L.sin & (L.sin - 1u);
+    ext += (take & L.emit) ? 1u : 0u;
+    const bool clo = take & (w == L.s);
+    const bool push = take & !clo;
+    if (push) {
+        sts_u32(rp + ((uint32_t)L.l << 7), rest);
+        sts_u8(mp + pidx(L.l + 1), w);
+    }
+    if (CNT) L.S += push ? mt(L.vb + wv) * pos_weight((uint32_t)(L.l + 1)) : 0ull;
+    const uint32_t Mp = L.M;
+    const uint32_t Mn = Mp | (1u << wv);
+    const uint32_t cw = tab.template sin<uint32_t>(L.vb + wv) & (~Mn | L.sbit);
+    L.M = push ? Mn : Mp;
+    L.l += push ? 1 : 0;
+    L.sin = push ? cw : (take ? rest : L.sin);
+    const int evc = L.emit ? (EV_PP | EV_CLO | ((L.l + 2) << 8)) : 0;
+    const int evn = lean_node_event(cw, L.ps, Mp, L.l, L.emit);
+    return clo ? evc : (push ? evn : 0);
+#endif
     const bool pop = L.sin == 0u;
     const bool fin = pop && L.l == L.r;  // the unit's subtree is exhausted
     if (pop && !fin) {                   // back to the parent and its untried children
