@@ -132,6 +132,18 @@ typedef struct {
                                   and device tables per device and reuse them when the next call passes a
                                   byte-identical CSR; 1 = always plan and upload anew (what an end-to-end timing of a
                                   fresh graph measures).  Ignored by the tpgen_plan_* calls. */
+    int32_t shard_prefix;      /* 1: with shard_count > 1, shards are contiguous ranges of PREFIX UNITS instead of
+                                  start vertices ("(start, depth-k prefix) for heavy starts"):
+                                  a heavy start vertex's path trie is cut at its depth-k prefixes (each unit the
+                                  subtree under path[0..k], or the closing arc of a cycle) until no unit holds
+                                  more than 1/(16 count) of the Knuth-estimated work, so a graph with fewer start
+                                  vertices than shards (config 3: 22 starts) still balances.  Units keep the
+                                  canonical order, so shard r's output is still block r of the global list
+                                  (tpgen_shard_units gives the split).  Applies to graphs with one mask word (SCCs
+                                  of <= 32 vertices) and no arc leaving an SCC on the DFS engine (materialize
+                                  additionally needs the LEAN table in shared memory: n_vertices <= 1024);
+                                  elsewhere the start-vertex split is used and stats.unit_lo = unit_hi = -1.
+                                  Other engines: TPGEN_ERR_INVALID_ARGUMENT.  0 (default): start-vertex shards. */
 } tpgen_options;
 
 typedef struct {
@@ -157,6 +169,8 @@ typedef struct {
     double ms_linearize;     /* device: linearization of the unit forest (canonical offsets) */
     double ms_dominant;      /* device time of the prime-path phase's enumeration kernel (the dominant launch) */
     int64_t ext_dominant;    /* extensions (E_canon terms) that launch made */
+    int64_t unit_lo, unit_hi;  /* shard_prefix: this shard's prefix-unit range [unit_lo, unit_hi) of the
+                                  split (tpgen_shard_units); -1 / -1 otherwise */
 } tpgen_stats;
 
 void tpgen_options_init(tpgen_options *opt);
@@ -204,6 +218,18 @@ tpgen_status tpgen_components(const int64_t *csr_offsets, const int32_t *csr_tar
  */
 tpgen_status tpgen_shard_range(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
                                int32_t rank, int32_t count, int32_t *lo, int32_t *hi);
+
+/*
+ * Prefix-unit shard of a graph (host only; tpgen_options.shard_prefix): the split
+ * has *n_units units in canonical order; shard `rank` of `count` takes [*unit_lo, *unit_hi) and
+ * touches start vertices [*lo, *hi) (its first / last unit's start; neighbouring shards may share
+ * one).  *applies = 0 when the graph does not qualify (SCCs of > 32 vertices or arcs leaving SCCs):
+ * the unit outputs are then 0 and lo / hi are tpgen_shard_range's.  Any output pointer may be NULL
+ * except applies.  Same validation and errors as tpgen_components.
+ */
+tpgen_status tpgen_shard_units(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                               int32_t rank, int32_t count, int32_t *applies, int64_t *unit_lo,
+                               int64_t *unit_hi, int64_t *n_units, int32_t *lo, int32_t *hi);
 
 /* Structure metrics of a CFG (Table 1; host only). */
 typedef struct {

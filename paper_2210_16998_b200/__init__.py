@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _abi
 
-__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "metrics", "shard_range",
+__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "metrics", "shard_range", "shard_units",
            "library", "version"]
 
 
@@ -135,7 +135,7 @@ class _TorchAllocator:
 def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest: bool, max_paths: int,
              max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None,
              start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
-             plan_cache: bool = True) -> _abi.Options:
+             plan_cache: bool = True, shard_prefix: bool = False) -> _abi.Options:
     lib = library()
     o = _abi.Options()
     lib.tpgen_options_init(ctypes.byref(o))
@@ -151,6 +151,7 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
     o.compute_digest = 1 if digest else 0
     o.engine = _engine(engine)
     o.no_plan_cache = 0 if plan_cache else 1
+    o.shard_prefix = 1 if shard_prefix else 0
     if alloc is not None:
         o.device_alloc = alloc.alloc_fn
         o.device_free = alloc.free_fn
@@ -218,7 +219,7 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
                 shard: Tuple[int, int] = (0, 1), digest: bool = False, max_paths: int = 0,
                 max_extensions: int = 0, stream=None, host_out=None,
                 start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
-                plan_cache: bool = True) -> PathSet:
+                plan_cache: bool = True, shard_prefix: bool = False) -> PathSet:
     """All prime paths of ``graph`` (Def. 1), canonical order.
 
     ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host).
@@ -226,13 +227,15 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
     include/tpgen.h TPGEN_ENGINE_FRONTIER) or "alg3" (the paper's vertex-centric
     self-stabilizing Alg. 3 as a comparison engine, ``mode="count"``, <= 128 vertices;
     TPGEN_ENGINE_ALG3).  ``plan_cache=False``: plan and upload the graph
-    anew even if the previous call passed the same CSR (tpgen_options.no_plan_cache)."""
+    anew even if the previous call passed the same CSR (tpgen_options.no_plan_cache).
+    ``shard_prefix=True``: ``shard`` splits prefix units of heavy start vertices, not whole
+    start vertices (tpgen_options.shard_prefix; see ``shard_units``)."""
     lib = library()
     _engine(engine)
     so, st, n = _csr(graph)
     alloc = None  # outputs come from the library's device memory pool (no Python callback while timing)
     o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
-                 alloc, host_out, start_range, engine, plan_cache)
+                 alloc, host_out, start_range, engine, plan_cache, shard_prefix)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_prime_paths(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc, host_out)
@@ -313,6 +316,20 @@ def shard_range(graph, rank: int, count: int) -> Tuple[int, int]:
     return int(lo.value), int(hi.value)
 
 
+def shard_units(graph, rank: int, count: int) -> Dict[str, Any]:
+    """Prefix-unit shard ``rank`` of ``count`` (``tpgen_shard_units``, host; what
+    ``shard=(rank, count), shard_prefix=True`` selects): ``applies``, the unit range
+    ``[unit_lo, unit_hi)`` of ``n_units`` and the start vertices ``[lo, hi)`` it touches."""
+    lib = library()
+    so, st, n = _csr(graph)
+    ap, lo, hi = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    ul, uh, nu = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.tpgen_shard_units(_p64(so), _p32(st), n, rank, count, ctypes.byref(ap), ctypes.byref(ul),
+                                 ctypes.byref(uh), ctypes.byref(nu), ctypes.byref(lo), ctypes.byref(hi)))
+    return {"applies": bool(ap.value), "unit_lo": int(ul.value), "unit_hi": int(uh.value),
+            "n_units": int(nu.value), "lo": int(lo.value), "hi": int(hi.value)}
+
+
 def release_cache() -> None:
     """Frees what one-shot calls keep between calls (``tpgen_release_cache``): the cached plan and
     its device workspaces per device, the cached output blocks; trims the device memory pool."""
@@ -387,11 +404,12 @@ class Plan:
 
     def prime_paths(self, *, output: str = "device", mode: str = "materialize", shard: Tuple[int, int] = (0, 1),
                     digest: bool = False, max_paths: int = 0, stream=None, host_out=None,
-                    start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs") -> PathSet:
+                    start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
+                    shard_prefix: bool = False) -> PathSet:
         lib = library()
         alloc = None
         o = _options(self.device, output, mode, shard, digest, max_paths, 0, _stream_handle(self.device, stream),
-                     alloc, host_out, start_range, engine)
+                     alloc, host_out, start_range, engine, shard_prefix=shard_prefix)
         paths, stats = _abi.Paths(), _abi.Stats()
         _check(lib.tpgen_plan_prime_paths(self._h, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
         return _wrap(paths, stats, alloc, host_out)

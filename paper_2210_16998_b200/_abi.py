@@ -41,7 +41,7 @@ class Options(Structure):
                 ("max_paths", c_int64), ("max_extensions", c_int64), ("tp_mode", c_int32),
                 ("compute_digest", c_int32), ("device_alloc", ALLOC_FN), ("device_free", FREE_FN),
                 ("alloc_ctx", c_void_p), ("host_out", c_void_p), ("host_out_bytes", c_size_t),
-                ("engine", c_int32), ("no_plan_cache", c_int32)]
+                ("engine", c_int32), ("no_plan_cache", c_int32), ("shard_prefix", c_int32)]
 
 
 class Metrics(Structure):
@@ -59,7 +59,7 @@ class Stats(Structure):
                 ("ms_plan", c_double), ("ms_count", c_double), ("ms_write", c_double), ("ms_stitch", c_double),
                 ("ms_device", c_double), ("ms_total", c_double), ("ms_dfs_write", c_double),
                 ("ms_dfs_count", c_double), ("ms_linearize", c_double), ("ms_dominant", c_double),
-                ("ext_dominant", c_int64)]
+                ("ext_dominant", c_int64), ("unit_lo", c_int64), ("unit_hi", c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -79,6 +79,9 @@ SYMBOLS = {
     "tpgen_components": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, POINTER(c_int32), POINTER(c_int32),
                                  POINTER(c_int32)]),
     "tpgen_shard_range": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32, POINTER(c_int32),
+                                  POINTER(c_int32)]),
+    "tpgen_shard_units": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32, POINTER(c_int32),
+                                  POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32),
                                   POINTER(c_int32)]),
     "tpgen_metrics_compute": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32,
                                       POINTER(Metrics)]),

@@ -48,6 +48,14 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("the Alg. 3 engine has no start-vertex shards (every vertex list is global)");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
+    if (o.shard_prefix != 0 && o.shard_prefix != 1) {
+        tpg::set_error("bad shard_prefix");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    if (o.shard_prefix && o.engine != TPGEN_ENGINE_DFS) {
+        tpg::set_error("prefix-unit shards are a DFS-engine option");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
     if (o.tp_mode != TPGEN_TP_PER_PP && o.tp_mode != TPGEN_TP_UNIQUE && o.tp_mode != TPGEN_TP_GREEDY) {
         tpg::set_error("bad tp_mode");
         return TPGEN_ERR_INVALID_ARGUMENT;
@@ -336,6 +344,38 @@ tpgen_status tpgen_shard_range(const int64_t *so, const int32_t *st, int32_t n, 
         return s;
     }
     tpg::shard_range(P, rank, count, *lo, *hi);
+    return TPGEN_OK;
+}
+
+tpgen_status tpgen_shard_units(const int64_t *so, const int32_t *st, int32_t n, int32_t rank, int32_t count,
+                               int32_t *applies, int64_t *unit_lo, int64_t *unit_hi, int64_t *n_units, int32_t *lo,
+                               int32_t *hi) {
+    if (n < 0 || !applies || count < 1 || rank < 0 || rank >= count) {
+        tpg::set_error("bad shard spec, NULL applies pointer or n < 0");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    tpg::HostPlan P;
+    std::string msg;
+    tpgen_status s = tpg::build_plan(so, st, n, P, msg, true);
+    if (s != TPGEN_OK) {
+        tpg::set_error(msg);
+        return s;
+    }
+    int32_t l = 0, h = 0;
+    int64_t ul = 0, uh = 0, nu = 0;
+    *applies = tpg::prefix_shard_applies(P) ? 1 : 0;
+    if (*applies) {
+        tpg::PrefixShard ps;
+        tpg::prefix_shard(P, rank, count, ps);
+        l = ps.lo, h = ps.hi, ul = ps.ulo, uh = ps.uhi, nu = ps.n_units;
+    } else {
+        tpg::shard_range(P, rank, count, l, h);
+    }
+    if (unit_lo) *unit_lo = ul;
+    if (unit_hi) *unit_hi = uh;
+    if (n_units) *n_units = nu;
+    if (lo) *lo = l;
+    if (hi) *hi = h;
     return TPGEN_OK;
 }
 

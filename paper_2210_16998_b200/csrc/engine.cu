@@ -162,6 +162,7 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
         memcpy(r + 16 * W, meta, 16);
     }
     P.presplit_lo = P.presplit_hi = -1;  // a new graph: the cached pre-split roots are stale
+    P.presplit_key = P.pfx_key = -1;
     P.presplit_n = 0;
     P.presplit_roots_n = -1;
     P.f_tab_ok = false;  // frontier engine: slot table, roots and record high-water mark belong to the old graph
@@ -590,48 +591,71 @@ static tpgen_status put_roots(PlanImpl &P, RootSpan<W> roots, uint64_t qbase, cu
 // that have children carry no event (an internal prime path has no child,
 // Def. 1 / R3) but each is one extension (E_canon): counted here.  Cached per
 // plan and start range; the device copy is reused by every call.
+// With a prefix-unit shard (`ps`, tpgen_options.shard_prefix) the expansion
+// starts from the shard's units instead of one unit per start vertex; the
+// extensions of the shard split's own expanded nodes come with it (ps->ext).
 template <int W>
 static void presplit_roots(PlanImpl &P, int32_t lo, int32_t hi, int64_t target, std::vector<Unit<W>> &units,
-                           std::vector<int32_t> &gids, uint64_t &ext) {
+                           std::vector<int32_t> &gids, uint64_t &ext, const PrefixShard *ps = nullptr) {
     const HostPlan &H = P.hp;
     units.clear();
     gids.clear();
     ext = 0;
-    for (int32_t v = lo; v < hi; v++) {
-        const int32_t slot = H.v_slot[v], c = H.comp[v];
-        Unit<W> u;
-        memset(&u, 0, sizeof(u));
-        const int loc = slot - H.scc_vbase[c];
-        u.M[0] = 1ull << loc;
-        u.scc = c;
-        u.e = -1;
-        u.kind = K_NODE;
-        u.path[0] = (uint8_t)loc;
-        units.push_back(u);
-        gids.push_back(v);
+    if (ps) {
+        for (const PrefixUnit &pu : ps->units) {
+            Unit<W> u;
+            memset(&u, 0, sizeof(u));
+            u.M[0] = pu.M;
+            u.scc = pu.scc;
+            u.e = -1;
+            u.kind = pu.closure ? K_CLOSURE : K_NODE;
+            u.depth = pu.depth;
+            memcpy(u.path, pu.path, (size_t)pu.depth + 1);
+            units.push_back(u);
+            gids.push_back(pu.gid);
+        }
+        ext = ps->ext;
+    } else {
+        for (int32_t v = lo; v < hi; v++) {
+            const int32_t slot = H.v_slot[v], c = H.comp[v];
+            Unit<W> u;
+            memset(&u, 0, sizeof(u));
+            const int loc = slot - H.scc_vbase[c];
+            u.M[0] = 1ull << loc;
+            u.scc = c;
+            u.e = -1;
+            u.kind = K_NODE;
+            u.path[0] = (uint8_t)loc;
+            units.push_back(u);
+            gids.push_back(v);
+        }
     }
-    for (int depth = 0; depth < 30 && (int64_t)units.size() < target; depth++) {
+    auto children = [&](const Unit<W> &u) -> uint64_t {
+        return H.sin[(size_t)(H.scc_vbase[u.scc] + u.path[u.depth]) * W] & (~u.M[0] | (1ull << u.path[0]));
+    };
+    while ((int64_t)units.size() < target) {
+        int depth = 1 << 30;  // the shallowest expandable level (every unit starts there without a shard)
+        for (const Unit<W> &u : units)
+            if (u.kind == K_NODE && children(u)) depth = std::min(depth, (int)u.depth);
+        if (depth >= 30) break;
         size_t grown = 0;  // size of the next level (bounded: a dense SCC can branch 31 ways)
         for (const Unit<W> &u : units) {
-            const uint64_t ch = H.sin[(size_t)(H.scc_vbase[u.scc] + u.path[u.depth]) * W] & (~u.M[0] | (1ull << u.path[0]));
+            const uint64_t ch = children(u);
             grown += (u.kind == K_NODE && u.depth == depth && ch) ? (size_t)__builtin_popcountll(ch) : 1;
         }
         if ((int64_t)grown > 16 * target) break;
         std::vector<Unit<W>> next;
         std::vector<int32_t> ngid;
         next.reserve(grown);
-        bool grew = false;
         for (size_t i = 0; i < units.size(); i++) {
             const Unit<W> &u = units[i];
-            const int vb = H.scc_vbase[u.scc], s0 = u.path[0], x = u.path[u.depth];
-            const uint64_t sbit = 1ull << s0;
-            const uint64_t ch = H.sin[(size_t)(vb + x) * W] & (~u.M[0] | sbit);
+            const int s0 = u.path[0];
+            const uint64_t ch = children(u);
             if (u.kind != K_NODE || u.depth != depth || ch == 0) {  // terminal: kept as it is
                 next.push_back(u);
                 ngid.push_back(gids[i]);
                 continue;
             }
-            grew = true;
             if (depth > 0) ext++;  // this node's own extension (its unit is replaced by its children)
             for (uint64_t cc = ch; cc; cc &= cc - 1) {
                 const int w = __builtin_ctzll(cc);
@@ -649,8 +673,24 @@ static void presplit_roots(PlanImpl &P, int32_t lo, int32_t hi, int64_t target, 
         }
         units.swap(next);
         gids.swap(ngid);
-        if (!grew) break;
     }
+}
+
+// tpgen_options.shard_prefix: this call's prefix-unit shard, when it applies (the pre-split path:
+// one mask word, no arc leaving an SCC); lo / hi become the start vertices it touches and *key
+// the pre-split cache key.  The split is cached per plan and (rank, count).
+static const PrefixShard *prefix_shard_call(PlanImpl &P, const tpgen_options &o, bool presplit_ok, int32_t &lo,
+                                            int32_t &hi, int64_t &key) {
+    key = -1;
+    if (!o.shard_prefix || o.shard_count <= 1 || !presplit_ok || !prefix_shard_applies(P.hp)) return nullptr;
+    key = ((int64_t)o.shard_rank << 32) | (uint32_t)o.shard_count;
+    if (P.pfx_key != key) {
+        prefix_shard(P.hp, o.shard_rank, o.shard_count, P.pfx);
+        P.pfx_key = key;
+    }
+    lo = P.pfx.lo;
+    hi = P.pfx.hi;
+    return &P.pfx;
 }
 
 // One phase of the persistent DFS (seg = SCC-entry starts, else prime-path
@@ -976,6 +1016,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     memset(out, 0, sizeof(*out));
     int64_t launches = 0;
     const HostPlan &H = P.hp;
@@ -986,6 +1027,14 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
         lo = std::max(0, o.start_lo);
         hi = std::min(H.n, o.start_hi);
     }
+    // LEAN calls start from host pre-split tries (below); with shard_prefix the shard is a range of them
+    const bool presplit_ok = std::is_same<T, uint32_t>::value && !P.any_exit &&
+                             (size_t)H.n * sizeof(Slot<W>) <= kSmemTabLean && !getenv("TPGEN_NO_LEAN") &&
+                             !getenv("TPGEN_NO_PRESPLIT");
+    int64_t pfx_key = -1;
+    const PrefixShard *pfx = prefix_shard_call(P, o, presplit_ok, lo, hi, pfx_key);
+    st.unit_lo = pfx ? pfx->ulo : -1;
+    st.unit_hi = pfx ? pfx->uhi : -1;
     st.shard_lo = lo;
     st.shard_hi = hi;
     st.n_scc = H.n_scc;
@@ -1051,14 +1100,13 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
     bool presplit_ext_used = false;
     RootSpan<W> pp_span(pp_roots);
     const std::vector<int32_t> *pp_gid_p = &pp_gid;
-    if (std::is_same<T, uint32_t>::value && seg_roots.empty() && !P.any_exit &&
-        (size_t)H.n * sizeof(Slot<W>) <= kSmemTabLean && !getenv("TPGEN_NO_LEAN") && !getenv("TPGEN_NO_PRESPLIT")) {
-        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_dev.p)) {
+    if (presplit_ok && seg_roots.empty()) {
+        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_key == pfx_key && P.presplit_dev.p)) {
             const int64_t lanes = (int64_t)P.num_sms * DfsCfg<W>::min_blocks * DfsCfg<W>::threads;
             std::vector<Unit<W>> units;
             int64_t target = lanes;  // measured: lanes/4 4.98, lanes 4.92, 2 lanes 5.00 ms per config-3 call
             if (const char *ev = getenv("TPGEN_PRESPLIT_TARGET")) target = atoll(ev);  // tuning knob
-            presplit_roots<W>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext);
+            presplit_roots<W>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext, pfx);
             P.presplit_host.assign(reinterpret_cast<const uint8_t *>(units.data()),
                                    reinterpret_cast<const uint8_t *>(units.data() + units.size()));
             P.presplit_n = (int64_t)units.size();
@@ -1066,6 +1114,7 @@ static tpgen_status run_pp(PlanImpl &P, const tpgen_options &o, tpgen_paths *out
             TPG_TRY(upload(P.presplit_dev, P.presplit_host, s));
             P.presplit_lo = lo;
             P.presplit_hi = hi;
+            P.presplit_key = pfx_key;
         }
         pp_span = RootSpan<W>(reinterpret_cast<const Unit<W> *>(P.presplit_host.data()), (size_t)P.presplit_n);
         pp_gid_p = &P.presplit_gid;
@@ -1611,6 +1660,7 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     int64_t launches = 0;
     const HostPlan &H = P.hp;
     cudaStream_t s = (cudaStream_t)o.stream;
@@ -1620,6 +1670,13 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
         lo = std::max(0, o.start_lo);
         hi = std::min(H.n, o.start_hi);
     }
+    // graphs with no arc leaving any SCC start from host pre-split tries (below); with shard_prefix the
+    // shard is a range of them
+    const bool presplit_ok = std::is_same<T, uint32_t>::value && !P.any_exit && !getenv("TPGEN_NO_PRESPLIT");
+    int64_t pfx_key = -1;
+    const PrefixShard *pfx = prefix_shard_call(P, o, presplit_ok, lo, hi, pfx_key);
+    st.unit_lo = pfx ? pfx->ulo : -1;
+    st.unit_hi = pfx ? pfx->uhi : -1;
     st.shard_lo = lo;
     st.shard_hi = hi;
     st.n_scc = H.n_scc;
@@ -1666,13 +1723,13 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
     // graphs with no arc leaving any SCC: the host pre-split trie tops (cached per plan and range)
     RootSpan<1> pp_span(pp_roots);
     uint64_t presplit_ext = 0;
-    if (std::is_same<T, uint32_t>::value && seg_roots.empty() && !P.any_exit && !getenv("TPGEN_NO_PRESPLIT")) {
-        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_dev.p)) {
+    if (presplit_ok && seg_roots.empty()) {
+        if (!(P.presplit_lo == lo && P.presplit_hi == hi && P.presplit_key == pfx_key && P.presplit_dev.p)) {
             const int64_t lanes = (int64_t)P.num_sms * CntCfg<uint32_t>::min_blocks * CntCfg<uint32_t>::threads;
             std::vector<Unit<1>> units;
             int64_t target = lanes;
             if (const char *ev = getenv("TPGEN_PRESPLIT_TARGET")) target = atoll(ev);
-            presplit_roots<1>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext);
+            presplit_roots<1>(P, lo, hi, target, units, P.presplit_gid, P.presplit_ext, pfx);
             P.presplit_host.assign(reinterpret_cast<const uint8_t *>(units.data()),
                                    reinterpret_cast<const uint8_t *>(units.data() + units.size()));
             P.presplit_n = (int64_t)units.size();
@@ -1680,6 +1737,7 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
             TPG_TRY(upload(P.presplit_dev, P.presplit_host, s));
             P.presplit_lo = lo;
             P.presplit_hi = hi;
+            P.presplit_key = pfx_key;
         }
         pp_span = RootSpan<1>(reinterpret_cast<const Unit<1> *>(P.presplit_host.data()), (size_t)P.presplit_n);
         presplit_ext = P.presplit_ext;
@@ -1726,6 +1784,7 @@ static tpgen_status run_frontier(PlanImpl &P, const tpgen_options &o, tpgen_stat
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     const HostPlan &H = P.hp;
     if (H.max_scc > 64 || H.W != 1 || H.n >= (1 << 21)) {
         set_error("the frontier engine needs SCCs of <= 64 vertices (use the DFS engine)");
@@ -2299,6 +2358,7 @@ static tpgen_status run_frontier_seg(PlanImpl &P, const tpgen_options &o, tpgen_
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     const HostPlan &H = P.hp;
     cudaStream_t s = (cudaStream_t)o.stream;
     int32_t lo = 0, hi = H.n;
@@ -2367,6 +2427,7 @@ static tpgen_status run_alg3(PlanImpl &P, const tpgen_options &o, tpgen_stats *s
     const double t0 = now_ms();
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     const HostPlan &H = P.hp;
     const int32_t n = H.n;
     cudaStream_t s = (cudaStream_t)o.stream;
@@ -2636,6 +2697,7 @@ static tpgen_status run_test_paths_count(PlanImpl &P, const tpgen_paths *pp_in, 
     // the prime paths as a list (given, or computed), then one thread per path
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     tpgen_paths own;
     memset(&own, 0, sizeof(own));
     const tpgen_paths *pp = pp_in;
@@ -2716,6 +2778,7 @@ tpgen_status run_test_paths(PlanImpl &P, const tpgen_paths *pp_in, int32_t entry
     cudaStream_t s = (cudaStream_t)o.stream;
     tpgen_stats st;
     memset(&st, 0, sizeof(st));
+    st.unit_lo = st.unit_hi = -1;
     tpgen_paths own;
     memset(&own, 0, sizeof(own));
     const tpgen_paths *pp = pp_in;

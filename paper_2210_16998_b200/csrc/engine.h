@@ -79,6 +79,9 @@ struct PlanImpl {
     int64_t presplit_n = 0;
     uint64_t presplit_ext = 0;
     int32_t presplit_lo = -1, presplit_hi = -1;
+    int64_t presplit_key = -1;  // prefix-unit shard (rank << 32 | count) the cached pre-split belongs to; -1: none
+    PrefixShard pfx;              // the last prefix-unit split computed (tpgen_options.shard_prefix) ...
+    int64_t pfx_key = -1;         // ... and its (rank << 32 | count)
     bool presplit_active = false;
     DevBuf presplit_roots, rscan;  // pre-split root table (cached); root-scan scratch
     int64_t presplit_roots_n = -1, presplit_roots_tail = -1;  // the running PP phase's roots are the cached pre-split units  // some arc leaves its SCC (head / segment events possible; no LEAN DFS)

@@ -80,6 +80,33 @@ tpgen_status build_plan(const int64_t *so, const int32_t *st, int32_t n, HostPla
 // Start-vertex range [lo, hi) of a shard (contiguous, cost balanced).
 void shard_range(const HostPlan &plan, int32_t rank, int32_t count, int32_t &lo, int32_t &hi);
 
+// Prefix-unit shards ("Unit = (SCC, start vertex), or (start,
+// depth-k prefix) for heavy starts"; tpgen_options.shard_prefix).  A unit is a
+// node of a start vertex's path trie (the subtree under path[0..depth]) or the
+// closing arc of one (a cyclic prime path); the list stays in canonical
+// (preorder) order, so a contiguous range of units is a contiguous block of the
+// canonical prime-path list.
+struct PrefixUnit {
+    uint64_t M;         // visited local bits of path[0..depth]
+    int32_t scc, gid;   // component, global id of the start vertex
+    uint8_t depth, closure;
+    uint8_t path[32];   // local ids
+};
+struct PrefixShard {
+    int64_t ulo = 0, uhi = 0, n_units = 0;  // this shard's unit range / units of the whole split
+    int32_t lo = 0, hi = 0;                 // start vertices the range touches, [lo, hi)
+    uint64_t ext = 0;  // extensions of the expanded interior trie nodes (depth >= 1) credited to the range
+                       // (each to the shard holding its first descendant unit)
+    std::vector<PrefixUnit> units;          // units [ulo, uhi)
+};
+// Graphs the split applies to: one mask word (SCCs <= 32 vertices) and no arc leaving an SCC
+// (prime paths then never leave their SCC; the LEAN / pre-split DFS path).
+bool prefix_shard_applies(const HostPlan &plan);
+// Heavy units (Knuth estimate above total / (16 count)) are replaced by their children, round
+// by round, until none is heavy; then contiguous unit ranges balanced by cost.  Deterministic:
+// every rank computes the same split.
+void prefix_shard(const HostPlan &plan, int32_t rank, int32_t count, PrefixShard &out);
+
 // Completion-count DP over the component DAG:
 //   W(x) = #tails(x) + sum_arcs cnt(x,e) W(y_e),  V(x) = vertices of all completions.
 // Inputs are the per-entry tail aggregates and per-(entry, out-arc) transit

@@ -258,6 +258,131 @@ void shard_range(const HostPlan &P, int32_t rank, int32_t count, int32_t &lo, in
     if (hi < lo) hi = lo;
 }
 
+bool prefix_shard_applies(const HostPlan &P) {
+    if (P.W != 1 || P.max_scc > 32) return false;
+    for (size_t i = 0; i < P.slot_flags.size(); i++)
+        if (P.slot_out_cnt[i] > 0 || (P.slot_flags[i] & (F_EXIT | F_ENTRY))) return false;
+    return true;
+}
+
+void prefix_shard(const HostPlan &P, int32_t rank, int32_t count, PrefixShard &out) {
+    out = PrefixShard();
+    std::vector<PrefixUnit> units;
+    std::vector<double> cost;
+    std::vector<uint32_t> credit;  // expanded interior nodes credited to the unit (its first descendant)
+    for (int32_t v = 0; v < P.n; v++) {
+        const int32_t slot = P.v_slot[v], c = P.comp[v];
+        PrefixUnit u;
+        memset(&u, 0, sizeof(u));
+        const int loc = slot - P.scc_vbase[c];
+        u.M = 1ull << loc;
+        u.scc = c;
+        u.gid = v;
+        u.path[0] = (uint8_t)loc;
+        units.push_back(u);
+        cost.push_back(P.cost[v]);
+        credit.push_back(0);
+    }
+    // Knuth's estimator of the subtree under a unit (its own node included), fixed seed
+    uint64_t rng = 0x13198A2E03707344ull;
+    auto next = [&rng]() {
+        rng ^= rng << 13;
+        rng ^= rng >> 7;
+        rng ^= rng << 17;
+        return rng;
+    };
+    auto knuth = [&](const PrefixUnit &u) {
+        if (u.closure) return 1.0;
+        const uint64_t *S = &P.sin[(size_t)P.scc_vbase[u.scc]];
+        const uint64_t sbit = 1ull << u.path[0];
+        const int probes = 48;
+        double acc = 0;
+        for (int p = 0; p < probes; p++) {
+            uint64_t M = u.M;
+            int32_t x = u.path[u.depth];
+            double prod = 1, est = 1;
+            while (true) {
+                const uint64_t ch = S[x] & (~M | sbit);
+                const int d = __builtin_popcountll(ch);
+                if (!d) break;
+                prod *= d;
+                est += prod;
+                uint64_t cand = ch;
+                for (int q = (int)(next() % (uint64_t)d); q > 0; q--) cand &= cand - 1;
+                x = __builtin_ctzll(cand);
+                if (x == u.path[0]) break;  // the closing arc: a leaf
+                M |= 1ull << x;
+            }
+            acc += est;
+        }
+        return acc / probes;
+    };
+    for (int round = 0; count > 1 && round < 32; round++) {  // (one shard: nothing to cut)
+        double total = 0;
+        for (double c : cost) total += c;
+        const double heavy = total / (16.0 * std::max(count, 1));
+        std::vector<PrefixUnit> nu;
+        std::vector<double> nc;
+        std::vector<uint32_t> ncr;
+        bool grew = false;
+        for (size_t i = 0; i < units.size(); i++) {
+            const PrefixUnit &u = units[i];
+            const uint64_t sbit = 1ull << u.path[0];
+            const uint64_t ch = u.closure ? 0 : (P.sin[(size_t)(P.scc_vbase[u.scc] + u.path[u.depth])] & (~u.M | sbit));
+            if (cost[i] <= heavy || ch == 0 || u.depth >= 30) {
+                nu.push_back(u);
+                nc.push_back(cost[i]);
+                ncr.push_back(credit[i]);
+                continue;
+            }
+            grew = true;
+            uint32_t cr = credit[i] + (u.depth > 0 ? 1u : 0u);  // the expanded node's own extension
+            for (uint64_t cc = ch; cc; cc &= cc - 1) {
+                const int w = __builtin_ctzll(cc);
+                PrefixUnit k = u;
+                if (w == u.path[0]) {
+                    k.closure = 1;
+                } else {
+                    k.depth = (uint8_t)(u.depth + 1);
+                    k.path[k.depth] = (uint8_t)w;
+                    k.M |= 1ull << w;
+                }
+                nu.push_back(k);
+                nc.push_back(knuth(k));
+                ncr.push_back(cr);
+                cr = 0;
+            }
+        }
+        units.swap(nu);
+        cost.swap(nc);
+        credit.swap(ncr);
+        if (!grew) break;
+    }
+    const int64_t nu = (int64_t)units.size();
+    out.n_units = nu;
+    double total = 0;
+    for (double c : cost) total += c;
+    auto boundary = [&](int32_t r) -> int64_t {  // first unit whose prefix cost reaches r / count of the total
+        if (r <= 0) return 0;
+        if (r >= count) return nu;
+        const double target = total * r / count;
+        double acc = 0;
+        for (int64_t i = 0; i < nu; i++) {
+            if (acc + 0.5 * cost[i] >= target) return i;
+            acc += cost[i];
+        }
+        return nu;
+    };
+    out.ulo = boundary(rank);
+    out.uhi = std::max(out.ulo, boundary(rank + 1));
+    out.units.assign(units.begin() + out.ulo, units.begin() + out.uhi);
+    for (int64_t i = out.ulo; i < out.uhi; i++) out.ext += credit[i];
+    if (out.uhi > out.ulo) {
+        out.lo = units[out.ulo].gid;
+        out.hi = units[out.uhi - 1].gid + 1;
+    }
+}
+
 static inline bool add_ov(uint64_t a, uint64_t b, uint64_t &r) {
     r = a + b;
     return r < a || r >= (1ull << 62);

@@ -71,12 +71,15 @@ def _gather_blocks(ps: PathSet, rows, rank: int, world: int, group, dev):
 
 def sharded_prime_paths(graph, group=None, *, device: Optional[int] = None, mode: str = "materialize",
                         digest: bool = True, compute: Optional[Callable[[int, int], PathSet]] = None,
-                        engine: str = "dfs", gather: bool = False) -> ShardResult:
+                        engine: str = "dfs", gather: bool = False, shard_prefix: bool = False) -> ShardResult:
     """This rank's prime paths plus their place in the global list.
 
     ``engine="frontier"`` (with ``mode="count"``) runs the level-synchronous engine on
     this rank's start vertices; the exchange is the same.
     ``gather=True`` (materialize mode): rank 0 also gets the whole list in ``whole`` (C4).
+    ``shard_prefix=True``: the ranks split prefix units of heavy start vertices
+    (tpgen_options.shard_prefix; a graph with fewer start vertices than ranks still balances);
+    the blocks are still contiguous in rank order, so the exchange is the same.
     ``compute(rank, world)`` replaces the GPU call (a test seam: the gloo tests run
     the collective logic on CPU with the oracle's shards)."""
     import torch
@@ -85,7 +88,8 @@ def sharded_prime_paths(graph, group=None, *, device: Optional[int] = None, mode
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     if compute is None:
         dev = torch.cuda.current_device() if device is None else device
-        ps = prime_paths(graph, device=dev, shard=(rank, world), mode=mode, digest=digest, engine=engine)
+        ps = prime_paths(graph, device=dev, shard=(rank, world), mode=mode, digest=digest, engine=engine,
+                         shard_prefix=shard_prefix)
     else:
         ps = compute(rank, world)
     st = ps.stats

@@ -49,8 +49,9 @@ def test_abi_struct_sizes_match_header():
 #include <stdio.h>
 #include <stddef.h>
 #include "tpgen.h"
-int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
- offsetof(tpgen_stats, ms_plan), offsetof(tpgen_options, host_out), offsetof(tpgen_options, engine));return 0;}
+int main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
+ offsetof(tpgen_stats, ms_plan), offsetof(tpgen_options, host_out), offsetof(tpgen_options, engine),
+ offsetof(tpgen_options, shard_prefix), offsetof(tpgen_stats, unit_lo));return 0;}
 '''
     tmpd = os.path.join(ROOT, "build")
     os.makedirs(tmpd, exist_ok=True)
@@ -60,7 +61,8 @@ int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
     vals = [int(x) for x in subprocess.check_output([exe]).split()]
     assert vals == [ctypes.sizeof(_abi.Options), ctypes.sizeof(_abi.Stats), ctypes.sizeof(_abi.Paths),
-                    _abi.Stats.ms_plan.offset, _abi.Options.host_out.offset, _abi.Options.engine.offset]
+                    _abi.Stats.ms_plan.offset, _abi.Options.host_out.offset, _abi.Options.engine.offset,
+                    _abi.Options.shard_prefix.offset, _abi.Stats.unit_lo.offset]
 
 
 def _corpus(count, seed0):
@@ -139,6 +141,16 @@ def test_frontier_engine_option_checks():
         assert paths.n_paths == 0
     with pytest.raises(ValueError):
         tp.prime_paths(g, mode="count", engine="bfs")
+    for engine in (_abi.ENGINE_FRONTIER, _abi.ENGINE_ALG3):  # prefix-unit shards: a DFS-engine option
+        o = _abi.Options()
+        lib.tpgen_options_init(ctypes.byref(o))
+        assert o.shard_prefix == 0
+        o.engine, o.output_mode, o.shard_prefix, o.shard_count = engine, _abi.OUT_COUNT_HASH, 1, 2
+        paths, stats = _abi.Paths(), _abi.Stats()
+        r = lib.tpgen_prime_paths(so.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  st.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), g.n, ctypes.byref(o),
+                                  ctypes.byref(paths), ctypes.byref(stats))
+        assert r == 1
 
 
 def test_metrics_fig1b_and_loops():
@@ -183,3 +195,33 @@ def test_shard_range_partitions_the_starts():
         cuts = [tp.shard_range(g, r, world) for r in range(world)]
         assert cuts[0][0] == 0 and cuts[-1][1] == g.n
         assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+
+
+def test_shard_units_tile_the_split():
+    """Prefix-unit shards (tpgen_shard_units): on graphs with no arc leaving an SCC
+    and SCCs of <= 32 vertices the ranks' unit ranges tile [0, n_units) in rank order, heavy start
+    vertices are cut into prefix units (more units than start vertices, every rank non-empty even
+    when there are more ranks than start vertices), the start ranges are monotone; elsewhere the
+    split is the start-vertex one."""
+    g = gen.config3()
+    for world in (1, 2, 8, 40):
+        cuts = [tp.shard_units(g, r, world) for r in range(world)]
+        assert all(c["applies"] for c in cuts)
+        n_units = cuts[0]["n_units"]
+        assert all(c["n_units"] == n_units for c in cuts)
+        assert cuts[0]["unit_lo"] == 0 and cuts[-1]["unit_hi"] == n_units
+        assert all(a["unit_hi"] == b["unit_lo"] for a, b in zip(cuts, cuts[1:]))
+        assert all(c["unit_hi"] > c["unit_lo"] for c in cuts)
+        assert all(a["lo"] <= b["lo"] and a["hi"] <= b["hi"] and a["hi"] - 1 <= b["lo"]
+                   for a, b in zip(cuts, cuts[1:]))
+        assert cuts[0]["lo"] == 0 and cuts[-1]["hi"] == g.n
+        if world > 1:
+            assert n_units > g.n
+    assert tp.shard_units(g, 0, 1)["n_units"] == g.n  # one shard: nothing is heavy enough to cut
+    g5 = gen.config5()  # 56-vertex SCCs with arcs leaving them: the start-vertex split
+    for r in range(4):
+        c = tp.shard_units(g5, r, 4)
+        assert not c["applies"] and (c["lo"], c["hi"]) == tp.shard_range(g5, r, 4)
+        assert c["unit_lo"] == c["unit_hi"] == c["n_units"] == 0
+    with pytest.raises(tp.TpgenError):
+        tp.shard_units(g, 3, 3)
