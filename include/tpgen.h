@@ -144,6 +144,16 @@ typedef struct {
                                   additionally needs the LEAN table in shared memory: n_vertices <= 1024);
                                   elsewhere the start-vertex split is used and stats.unit_lo = unit_hi = -1.
                                   Other engines: TPGEN_ERR_INVALID_ARGUMENT.  0 (default): start-vertex shards. */
+    int32_t prune;             /* 1: reachability pruning (not in the paper) in the COUNT_HASH
+                                  prime-path phase of the DFS engine: a child w is not entered when w is not a
+                                  predecessor of the start s, some predecessor of s is off the path, and no
+                                  predecessor of s off the path is reachable from w in the SCC minus the path
+                                  (bitset BFS) -- its subtree holds no closure, internal prime path or head
+                                  segment (Def. 1; Def. 6).  Counts, vertices and digest are
+                                  unchanged; stats.n_extensions then counts the extensions MADE (<= E_canon).
+                                  Graphs with SCCs of > 64 vertices and the segment / test-path phases do not
+                                  prune.  Requires output_mode = TPGEN_OUT_COUNT_HASH and the DFS engine, else
+                                  TPGEN_ERR_INVALID_ARGUMENT.  0 (default): off (measured slower). */
 } tpgen_options;
 
 typedef struct {

@@ -135,7 +135,7 @@ class _TorchAllocator:
 def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest: bool, max_paths: int,
              max_extensions: int, stream, alloc: Optional[_TorchAllocator], host_out=None,
              start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
-             plan_cache: bool = True, shard_prefix: bool = False) -> _abi.Options:
+             plan_cache: bool = True, shard_prefix: bool = False, prune: bool = False) -> _abi.Options:
     lib = library()
     o = _abi.Options()
     lib.tpgen_options_init(ctypes.byref(o))
@@ -152,6 +152,7 @@ def _options(device: int, output: str, mode: str, shard: Tuple[int, int], digest
     o.engine = _engine(engine)
     o.no_plan_cache = 0 if plan_cache else 1
     o.shard_prefix = 1 if shard_prefix else 0
+    o.prune = 1 if prune else 0
     if alloc is not None:
         o.device_alloc = alloc.alloc_fn
         o.device_free = alloc.free_fn
@@ -219,7 +220,7 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
                 shard: Tuple[int, int] = (0, 1), digest: bool = False, max_paths: int = 0,
                 max_extensions: int = 0, stream=None, host_out=None,
                 start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
-                plan_cache: bool = True, shard_prefix: bool = False) -> PathSet:
+                plan_cache: bool = True, shard_prefix: bool = False, prune: bool = False) -> PathSet:
     """All prime paths of ``graph`` (Def. 1), canonical order.
 
     ``graph``: a ``workloads.Graph`` or ``(offsets, targets)`` successor CSR (host).
@@ -229,13 +230,15 @@ def prime_paths(graph, *, device: int = 0, output: str = "device", mode: str = "
     TPGEN_ENGINE_ALG3).  ``plan_cache=False``: plan and upload the graph
     anew even if the previous call passed the same CSR (tpgen_options.no_plan_cache).
     ``shard_prefix=True``: ``shard`` splits prefix units of heavy start vertices, not whole
-    start vertices (tpgen_options.shard_prefix; see ``shard_units``)."""
+    start vertices (tpgen_options.shard_prefix; see ``shard_units``).  ``prune=True``
+    (``mode="count"``): NEXT #2 reachability pruning (tpgen_options.prune; n_extensions
+    then counts the extensions made)."""
     lib = library()
     _engine(engine)
     so, st, n = _csr(graph)
     alloc = None  # outputs come from the library's device memory pool (no Python callback while timing)
     o = _options(device, output, mode, shard, digest, max_paths, max_extensions, _stream_handle(device, stream),
-                 alloc, host_out, start_range, engine, plan_cache, shard_prefix)
+                 alloc, host_out, start_range, engine, plan_cache, shard_prefix, prune)
     paths, stats = _abi.Paths(), _abi.Stats()
     _check(lib.tpgen_prime_paths(_p64(so), _p32(st), n, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
     return _wrap(paths, stats, alloc, host_out)
@@ -405,11 +408,11 @@ class Plan:
     def prime_paths(self, *, output: str = "device", mode: str = "materialize", shard: Tuple[int, int] = (0, 1),
                     digest: bool = False, max_paths: int = 0, stream=None, host_out=None,
                     start_range: Optional[Tuple[int, int]] = None, engine: str = "dfs",
-                    shard_prefix: bool = False) -> PathSet:
+                    shard_prefix: bool = False, prune: bool = False) -> PathSet:
         lib = library()
         alloc = None
         o = _options(self.device, output, mode, shard, digest, max_paths, 0, _stream_handle(self.device, stream),
-                     alloc, host_out, start_range, engine, shard_prefix=shard_prefix)
+                     alloc, host_out, start_range, engine, shard_prefix=shard_prefix, prune=prune)
         paths, stats = _abi.Paths(), _abi.Stats()
         _check(lib.tpgen_plan_prime_paths(self._h, ctypes.byref(o), ctypes.byref(paths), ctypes.byref(stats)))
         return _wrap(paths, stats, alloc, host_out)

@@ -41,7 +41,8 @@ class Options(Structure):
                 ("max_paths", c_int64), ("max_extensions", c_int64), ("tp_mode", c_int32),
                 ("compute_digest", c_int32), ("device_alloc", ALLOC_FN), ("device_free", FREE_FN),
                 ("alloc_ctx", c_void_p), ("host_out", c_void_p), ("host_out_bytes", c_size_t),
-                ("engine", c_int32), ("no_plan_cache", c_int32), ("shard_prefix", c_int32)]
+                ("engine", c_int32), ("no_plan_cache", c_int32), ("shard_prefix", c_int32),
+                ("prune", c_int32)]
 
 
 class Metrics(Structure):

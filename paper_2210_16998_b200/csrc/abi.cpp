@@ -52,6 +52,10 @@ tpgen_status check_options(const tpgen_options &o) {
         tpg::set_error("bad shard_prefix");
         return TPGEN_ERR_INVALID_ARGUMENT;
     }
+    if (o.prune != 0 && (o.prune != 1 || o.engine != TPGEN_ENGINE_DFS || o.output_mode != TPGEN_OUT_COUNT_HASH)) {
+        tpg::set_error("prune: 0 or 1, DFS engine, COUNT_HASH output only");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
     if (o.shard_prefix && o.engine != TPGEN_ENGINE_DFS) {
         tpg::set_error("prefix-unit shards are a DFS-engine option");
         return TPGEN_ERR_INVALID_ARGUMENT;

@@ -169,7 +169,8 @@ constexpr size_t cnt_smem_block(bool seg, bool d2 = false) {
 // segment phase -- the trees of the SCC entry vertices: their cycles are prime paths (when the
 // entry lies in the call's start range; their test paths when A.tp is set), their tail and
 // transit segments (R8/R9) become ItemS records for the completion DP and the stitch.
-enum CntPhase : int { P_PP = 0, P_TP = 1, P_SEG = 2 };
+// P_PRUNE: P_PP with NEXT #2's reachability pruning (tpgen_options.prune).
+enum CntPhase : int { P_PP = 0, P_TP = 1, P_SEG = 2, P_PRUNE = 3 };
 #ifndef CNT_MINB_SEG
 #define CNT_MINB_SEG 3
 #endif
@@ -186,10 +187,10 @@ constexpr int cnt_min_blocks(bool seg, bool hsh) {
 // with ONE shared load instead of recomputing them from the parent's successor set.
 template <class T, bool TS, bool HSH, bool HX, int PH, bool D2 = false>
 __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_SEG, HSH)) cnt_kernel(DfsArgs A) {
-    static_assert(!D2 || (TS && PH != P_TP), "D2: prime-path or segment phase with the table in shared memory");
+    static_assert(!D2 || (TS && PH != P_TP && PH != P_PRUNE), "D2: prime-path or segment phase with the table in shared memory");
     constexpr uint32_t PST = D2 ? 64u : 32u;  // bytes per path level of a warp's column block
     constexpr bool SEG = PH == P_SEG;
-    constexpr bool TRACK_B = PH != P_PP;
+    constexpr bool TRACK_B = PH == P_TP || PH == P_SEG;
     using C = CntCfg<T>;
     constexpr bool RS = C::RS;
     constexpr int WARPS = C::warps;
@@ -796,7 +797,31 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     other = HX && take && !clo && ex && (L.ps & ~Mw) == 0;  // a head segment
                     kind = EK_HEAD;
                 }
-                const bool push = take && cw != 0;
+                bool push = take && cw != 0;
+                if constexpr (PH == P_PRUNE) {
+                    // NEXT #2 (not in the paper): a child w whose subtree can hold no prime
+                    // path is not entered.  Every event below w ends at a vertex x reachable from w in
+                    // C \ path: a closure needs x in pred(s), an internal prime path or a head segment
+                    // needs pred(s) on the path (Def. 1 / R3, Def. 6).  So when w is not in pred(s),
+                    // some of pred(s) is off the path, and no vertex of pred(s) off the path is
+                    // reachable from w in C \ path (bitset BFS), the subtree is empty of events.
+                    if (push && ((L.ps >> v) & 1) == 0) {
+                        const T need = L.ps & ~Mw;
+                        if (need != 0) {
+                            T R = Mw | cw, F = cw;
+                            bool hit = (cw & need) != 0;
+                            while (!hit && F != 0) {
+                                T N = 0;
+                                for (T f = F; f != 0; f &= f - 1) N |= tab.sin(L.vb + ffs_t(f));
+                                N &= ~R;
+                                hit = (N & need) != 0;
+                                R |= N;
+                                F = N;
+                            }
+                            push = hit;
+                        }
+                    }
+                }
                 const uint64_t Sw = L.S + prod;  // (take) the digest sum of path + w
                 T rem_pop = 0;
                 if constexpr (RS) {

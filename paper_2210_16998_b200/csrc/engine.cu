@@ -710,7 +710,7 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         const size_t ctab = (size_t)A.n_slots * 16;  // {sin, mix} per slot
         const bool ts = ctab <= kSmemTabMax;
         // D2: the out-degree-2 prime-path kernel (count.cuh) when the plan's table allows it
-        const bool d2 = !seg && A.tp == nullptr && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8;
+        const bool d2 = !seg && A.tp == nullptr && !A.prune && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8;
         const size_t cdyn = (ts ? ctab : 0) + cnt_smem_block<CT>(seg, d2 || (seg && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8));
         void (*k)(DfsArgs);
         const bool d2seg = seg && ts && A.G.slot_d2 != nullptr && sizeof(CT) == 8;
@@ -723,6 +723,9 @@ static tpgen_status launch_dfs(bool lean, size_t tab_bytes, int grid, const DfsA
         } else if (A.tp != nullptr) {
             k = ts ? (any_exit ? cnt_kernel<CT, true, true, true, P_TP> : cnt_kernel<CT, true, true, false, P_TP>)
                    : (any_exit ? cnt_kernel<CT, false, true, true, P_TP> : cnt_kernel<CT, false, true, false, P_TP>);
+        } else if (A.prune) {  // NEXT #2: the prime-path phase with reachability pruning
+            k = ts ? (any_exit ? cnt_kernel<CT, true, HSH, true, P_PRUNE> : cnt_kernel<CT, true, HSH, false, P_PRUNE>)
+                   : (any_exit ? cnt_kernel<CT, false, HSH, true, P_PRUNE> : cnt_kernel<CT, false, HSH, false, P_PRUNE>);
         } else {
             k = ts ? (any_exit ? cnt_kernel<CT, true, HSH, true, P_PP> : cnt_kernel<CT, true, HSH, false, P_PP>)
                    : (any_exit ? cnt_kernel<CT, false, HSH, true, P_PP> : cnt_kernel<CT, false, HSH, false, P_PP>);
@@ -857,6 +860,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.head_cap = (mode != M_REC && !seg) ? std::min<uint64_t>(hlim, P.cheads.cap / sizeof(HeadS)) : 0;
         A.items = P.citems.as<ItemS>();
         A.tp = (mode != M_REC) ? P.cur_tp : nullptr;
+        A.prune = (mode != M_REC && !seg) ? P.cur_prune : 0;
         A.item_cap = (mode != M_REC && seg) ? std::min<uint64_t>(hlim, P.citems.cap / sizeof(ItemS)) : 0;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
         // LEAN: 32-bit masks, prime-path phase, no arc leaves any SCC (no head / segment
@@ -1686,6 +1690,7 @@ static tpgen_status run_count(PlanImpl &P, const tpgen_options &o, tpgen_stats *
     P.overflow = false;
     P.tp_unreachable = false;
     P.maxgen = 0;
+    P.cur_prune = o.prune;
     const int mode = o.compute_digest ? M_CNT : M_CNT_NOHASH;
     const bool hdbg = getenv("TPGEN_DEBUG") != nullptr;  // host stage marks, synchronised
     auto HT = [&](const char *what) {

@@ -44,6 +44,7 @@ struct PlanImpl {
     DevBuf citems, citems2;  // count modes: ItemS records of the segment phase (as written; grouped by entry)
     DevBuf icnt;             // count modes: items per entry vertex, their scan, the scatter cursors
     DevBuf tp_terms;         // count modes, test paths: TpTerm per slot
+    int32_t cur_prune = 0;           // the running count-mode call prunes (tpgen_options.prune)
     const TpTerm *cur_tp = nullptr;  // the running count-mode call hashes test paths with these terms
     bool tp_unreachable = false;     // ... and found a path whose end vertices have no walk
     uint64_t chead_hwm = 0;  // most head slots any count-mode call of this plan reserved

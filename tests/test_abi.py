@@ -49,9 +49,9 @@ def test_abi_struct_sizes_match_header():
 #include <stdio.h>
 #include <stddef.h>
 #include "tpgen.h"
-int main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
+int main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options), sizeof(tpgen_stats), sizeof(tpgen_paths),
  offsetof(tpgen_stats, ms_plan), offsetof(tpgen_options, host_out), offsetof(tpgen_options, engine),
- offsetof(tpgen_options, shard_prefix), offsetof(tpgen_stats, unit_lo));return 0;}
+ offsetof(tpgen_options, shard_prefix), offsetof(tpgen_stats, unit_lo), offsetof(tpgen_options, prune));return 0;}
 '''
     tmpd = os.path.join(ROOT, "build")
     os.makedirs(tmpd, exist_ok=True)
@@ -62,7 +62,7 @@ int main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(tpgen_options)
     vals = [int(x) for x in subprocess.check_output([exe]).split()]
     assert vals == [ctypes.sizeof(_abi.Options), ctypes.sizeof(_abi.Stats), ctypes.sizeof(_abi.Paths),
                     _abi.Stats.ms_plan.offset, _abi.Options.host_out.offset, _abi.Options.engine.offset,
-                    _abi.Options.shard_prefix.offset, _abi.Stats.unit_lo.offset]
+                    _abi.Options.shard_prefix.offset, _abi.Stats.unit_lo.offset, _abi.Options.prune.offset]
 
 
 def _corpus(count, seed0):
@@ -141,6 +141,16 @@ def test_frontier_engine_option_checks():
         assert paths.n_paths == 0
     with pytest.raises(ValueError):
         tp.prime_paths(g, mode="count", engine="bfs")
+    for engine, mode in ((_abi.ENGINE_DFS, _abi.OUT_MATERIALIZE), (_abi.ENGINE_FRONTIER, _abi.OUT_COUNT_HASH)):
+        o = _abi.Options()  # pruning (NEXT #2): the DFS engine's COUNT_HASH mode only
+        lib.tpgen_options_init(ctypes.byref(o))
+        assert o.prune == 0
+        o.engine, o.output_mode, o.prune = engine, mode, 1
+        paths, stats = _abi.Paths(), _abi.Stats()
+        r = lib.tpgen_prime_paths(so.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  st.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), g.n, ctypes.byref(o),
+                                  ctypes.byref(paths), ctypes.byref(stats))
+        assert r == 1
     for engine in (_abi.ENGINE_FRONTIER, _abi.ENGINE_ALG3):  # prefix-unit shards: a DFS-engine option
         o = _abi.Options()
         lib.tpgen_options_init(ctypes.byref(o))
