@@ -136,6 +136,34 @@ __device__ __forceinline__ uint64_t mul64x32(uint64_t m, uint32_t w) {
     return lo + ((uint64_t)((uint32_t)(m >> 32) * w) << 32);
 }
 
+// NEXT #2 (not in the paper): may the subtree under the path node w (path mask Mw,
+// w included; untried children cw) hold an event?  Every event below w ends at a vertex x
+// reachable from w in C \ path: a closure needs x in pred(s), an internal prime path or a head
+// segment needs pred(s) on the path (Def. 1 / R3, Def. 6).  No when w is not in pred(s), some of
+// pred(s) is off the path, and none of that part is reachable from w in C \ path (bitset BFS).
+// CNT_PRUNE_MAXD: the deepest path position tested (a subtree a shallow test did not cut is still
+// cut where a deeper test fires; deep subtrees are small, the test's cost is not).
+#ifndef CNT_PRUNE_MAXD
+#define CNT_PRUNE_MAXD 64
+#endif
+template <class T, class Tab>
+__device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, T Mw, T cw) {
+    if ((ps >> w) & 1) return true;
+    const T need = ps & ~Mw;
+    if (need == 0) return true;
+    T R = Mw | cw, F = cw;
+    bool hit = (cw & need) != 0;
+    while (!hit && F != 0) {
+        T N = 0;
+        for (T f = F; f != 0; f &= f - 1) N |= tab.sin(vb + ffs_t(f));
+        N &= ~R;
+        hit = (N & need) != 0;
+        R |= N;
+        F = N;
+    }
+    return hit;
+}
+
 template <class T>
 struct CntCfg {
     static constexpr bool RS = sizeof(T) == 4;  // untried children on a shared-memory stack
@@ -616,6 +644,10 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     const T ub = (T)1 << u;
                     const T su = D2 ? (T)__ldg(&tab.g[L.vb + u].sin[0]) : tab.sin(L.vb + u);
                     L.rem = su & (~L.M | L.sbit);
+                    if constexpr (PH == P_PRUNE) {  // NEXT #2: the root of a donated unit, as at a push
+                        if (depth > 0 && depth <= CNT_PRUNE_MAXD && L.rem != 0 && !prune_keep<T>(tab, L.vb, L.ps, u, L.M, L.rem))
+                            L.rem = 0;
+                    }
                     if constexpr (D2) L.cur = d2_bytes<T>(L.rem);
                     const bool ex = D2 ? ((__ldg(G.slot_d2 + 2 * (L.vb + u)) >> 16) & 1) != 0 : ((L.exm >> u) & 1) != 0;
                     if constexpr (SEG) {  // tail segment (succ(u) on the path) or transit segments (R8, R9)
@@ -805,22 +837,9 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     // needs pred(s) on the path (Def. 1 / R3, Def. 6).  So when w is not in pred(s),
                     // some of pred(s) is off the path, and no vertex of pred(s) off the path is
                     // reachable from w in C \ path (bitset BFS), the subtree is empty of events.
-                    if (push && ((L.ps >> v) & 1) == 0) {
-                        const T need = L.ps & ~Mw;
-                        if (need != 0) {
-                            T R = Mw | cw, F = cw;
-                            bool hit = (cw & need) != 0;
-                            while (!hit && F != 0) {
-                                T N = 0;
-                                for (T f = F; f != 0; f &= f - 1) N |= tab.sin(L.vb + ffs_t(f));
-                                N &= ~R;
-                                hit = (N & need) != 0;
-                                R |= N;
-                                F = N;
-                            }
-                            push = hit;
-                        }
-                    }
+                    // (a donated unit's root gets the same test when it starts: the extensions made
+                    // do not depend on the donation pattern)
+                    if (push && l + 1 <= CNT_PRUNE_MAXD) push = prune_keep<T>(tab, L.vb, L.ps, v, Mw, cw);
                 }
                 const uint64_t Sw = L.S + prod;  // (take) the digest sum of path + w
                 T rem_pop = 0;
