@@ -131,9 +131,20 @@ __device__ __forceinline__ uint32_t d2_bytes(T m) {
     return b0 | (b1 << 8);
 }
 // m * w mod 2^64 for a 32-bit w: one wide multiply of the low word, one of the high word
+#ifndef CNT_MUL_PTX
+#define CNT_MUL_PTX 0  // 1: the product as two PTX multiplies (mul.wide.u32 + mad.lo.u32 into the high word)
+#endif
 __device__ __forceinline__ uint64_t mul64x32(uint64_t m, uint32_t w) {
+#if CNT_MUL_PTX
+    uint32_t lo, hi;
+    asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %4;\n\tmov.b64 {%0, %1}, t;\n\tmad.lo.u32 %1, %3, %4, %1;\n\t}"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)m), "r"((uint32_t)(m >> 32)), "r"(w));
+    return ((uint64_t)hi << 32) | lo;
+#else
     const uint64_t lo = (uint64_t)(uint32_t)m * w;
     return lo + ((uint64_t)((uint32_t)(m >> 32) * w) << 32);
+#endif
 }
 
 // NEXT #2 (not in the paper): may the subtree under the path node w (path mask Mw,
