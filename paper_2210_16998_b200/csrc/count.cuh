@@ -132,7 +132,7 @@ __device__ __forceinline__ uint32_t d2_bytes(T m) {
 }
 // m * w mod 2^64 for a 32-bit w: one wide multiply of the low word, one of the high word
 #ifndef CNT_MUL_PTX
-#define CNT_MUL_PTX 0  // 1: the product as two PTX multiplies (mul.wide.u32 + mad.lo.u32 into the high word)
+#define CNT_MUL_PTX 1  // 1 (measured: config 5 cnt_kernel 111.95 -> 110.87 ms): the product as two PTX multiplies (mul.wide.u32 + mad.lo.u32 into the high word)
 #endif
 __device__ __forceinline__ uint64_t mul64x32(uint64_t m, uint32_t w) {
 #if CNT_MUL_PTX
@@ -173,6 +173,33 @@ __device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, 
         F = N;
     }
     return hit;
+}
+
+// 2 x + 1, the digest weight of path position x (R20), as one multiply-add (the FMA pipe; the
+// compiler's shift-or form takes an ALU-pipe LOP3, the pipe the D2 pass is bound on)
+#ifndef CNT_ODD_MAD
+#define CNT_ODD_MAD 1
+#endif
+// CNT_OPAQUE_K: the D2 pass's constant multipliers (2 for the weight, 16 for the table stride)
+// come from blockDim.x (= 256, unknown to ptxas), so the products stay IMADs (FMA pipe) instead
+// of being strength-reduced to LEA / shift-or (ALU pipe)
+#ifndef CNT_OPAQUE_K
+#define CNT_OPAQUE_K 1
+#endif
+__device__ __forceinline__ uint32_t odd2(uint32_t x, uint32_t k2 = 2u) {
+#if CNT_ODD_MAD
+    uint32_t r;
+    if (CNT_OPAQUE_K) asm("mad.lo.u32 %0, %1, %2, 1;" : "=r"(r) : "r"(x), "r"(k2));
+    else asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(r) : "r"(x));
+    return r;
+#else
+    return 2u * x + 1u;
+#endif
+}
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
 }
 
 template <class T>
@@ -257,6 +284,8 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     asm volatile("mov.b32 %0, %1;" : "=r"(rb) : "r"((uint32_t)__cvta_generic_to_shared(srem + (RS ? wid * 32 * 32 : 0)) + (RS ? lane * 4 : 0)));
     asm volatile("mov.b32 %0, %1;" : "=r"(qb) : "r"((uint32_t)__cvta_generic_to_shared(sring + wid * RSLOTS * 32) + lane * 8));
     asm volatile("mov.b32 %0, %1;" : "=r"(lb) : "r"((uint32_t)__cvta_generic_to_shared(sringt + wid * RSLOTS * 32) + lane * 4));
+#define k2 A.k2    // 2 and 16 as kernel parameters (CNT_OPAQUE_K): constant-bank operands of the IMADs
+#define k16 A.k16
     CntTab<T, TS> tab;
     tab.g = reinterpret_cast<const Slot<1> *>(G.slots);
     tab.gm = G.slot_mix;
@@ -736,7 +765,11 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     const bool pk = act & ((L.cur & 0xffu) == 0xffu) & (L.l > L.r);
                     const uint32_t ek = lds_u16(pb + (uint32_t)L.l * PST);
                     const int uk = (int)(ek & 0xffu);
-                    const uint64_t mk = tab.mix(L.vb + uk);
+                    uint64_t mk;
+                    if (CNT_OPAQUE_K)
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(mk) : "r"(mad_u32((uint32_t)(L.vb + uk), k16, tab.sb + 8u)) : "memory");
+                    else
+                        mk = tab.mix(L.vb + uk);
 #if CNT_D2_SELFREE
                     // predicate folded into the operands (no 64-bit selects on the ALU pipe, the kernel's
                     // limiting pipe): the multiplier is 0 and the shift 64 (PTX clamps: a zero bit) when
@@ -747,7 +780,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                     L.M ^= (T)ubk;
                     L.S -= prk;
 #else
-                    const uint64_t prk = mul64x32(mk, 2u * (uint32_t)L.l + 1u);
+                    const uint64_t prk = mul64x32(mk, odd2((uint32_t)L.l, k2));
                     const T ubk = (T)1 << uk;
                     L.M = pk ? (L.M ^ ubk) : L.M;
                     L.S = pk ? (L.S - prk) : L.S;
@@ -768,8 +801,9 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 const int v = take ? (int)a : (int)(e & 0xffu);     // the child, or the vertex popped
                 const int vslot = L.vb + v;
                 uint64_t wd, mv;  // {t0 | t1 << 8 | exit << 16, mix64(gid)} of v
-                asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(wd), "=l"(mv) : "r"(tab.sb + (uint32_t)vslot * 16u) : "memory");
-                const uint64_t prod = mul64x32(mv, 2u * (uint32_t)(take ? l + 1 : l) + 1u);
+                asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(wd), "=l"(mv)
+                             : "r"(CNT_OPAQUE_K ? mad_u32((uint32_t)vslot, k16, tab.sb) : tab.sb + (uint32_t)vslot * 16u) : "memory");
+                const uint64_t prod = mul64x32(mv, odd2((uint32_t)(take ? l + 1 : l), k2));
                 const T vbit = (T)1 << v;
                 const T Mw = L.M | vbit;
                 const T avail = ~Mw | L.sbit;  // vertices a child of v may move to
@@ -1029,5 +1063,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     }
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(A.overflow, 1u);
 }
+#undef k2
+#undef k16
 
 }  // namespace tpg

@@ -861,6 +861,8 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.items = P.citems.as<ItemS>();
         A.tp = (mode != M_REC) ? P.cur_tp : nullptr;
         A.prune = (mode != M_REC && !seg) ? P.cur_prune : 0;
+        A.k2 = 2;
+        A.k16 = 16;
         A.item_cap = (mode != M_REC && seg) ? std::min<uint64_t>(hlim, P.citems.cap / sizeof(ItemS)) : 0;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);
         // LEAN: 32-bit masks, prime-path phase, no arc leaves any SCC (no head / segment
