@@ -183,6 +183,9 @@ __device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, 
 // CNT_OPAQUE_K: the D2 pass's constant multipliers (2 for the weight, 16 for the table stride)
 // come from blockDim.x (= 256, unknown to ptxas), so the products stay IMADs (FMA pipe) instead
 // of being strength-reduced to LEA / shift-or (ALU pipe)
+#ifndef CNT_BIT_TAB
+#define CNT_BIT_TAB 1  // D2: one-bit masks from a 512-byte shared table (no SHF / SEL on the ALU pipe)
+#endif
 #ifndef CNT_OPAQUE_K
 #define CNT_OPAQUE_K 1
 #endif
@@ -286,6 +289,13 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
     asm volatile("mov.b32 %0, %1;" : "=r"(lb) : "r"((uint32_t)__cvta_generic_to_shared(sringt + wid * RSLOTS * 32) + lane * 4));
 #define k2 A.k2    // 2 and 16 as kernel parameters (CNT_OPAQUE_K): constant-bank operands of the IMADs
 #define k16 A.k16
+#define k8 A.k8
+    uint32_t bitb = 0;  // CNT_BIT_TAB (D2): shared table of the 64 one-bit masks 1 << i
+    if constexpr (D2 && CNT_BIT_TAB) {
+        __shared__ uint64_t s_bits[64];
+        if (threadIdx.x < 64) s_bits[threadIdx.x] = 1ull << threadIdx.x;
+        asm volatile("mov.b32 %0, %1;" : "=r"(bitb) : "r"((uint32_t)__cvta_generic_to_shared(s_bits)));
+    }
     CntTab<T, TS> tab;
     tab.g = reinterpret_cast<const Slot<1> *>(G.slots);
     tab.gm = G.slot_mix;
@@ -770,7 +780,16 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(mk) : "r"(mad_u32((uint32_t)(L.vb + uk), k16, tab.sb + 8u)) : "memory");
                     else
                         mk = tab.mix(L.vb + uk);
-#if CNT_D2_SELFREE
+#if CNT_BIT_TAB
+                    // the popped vertex's bit from the shared bit table by a predicated load (0 when this
+                    // lane does not pop), the weight 0 when it does not: no shifts, no 64-bit selects
+                    uint64_t ubk;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tmov.b64 %0, 0;\n\t@p ld.shared.u64 %0, [%1];\n\t}"
+                                 : "=l"(ubk) : "r"(mad_u32((uint32_t)uk, k8, bitb)), "r"((uint32_t)pk) : "memory");
+                    const uint64_t prk = mul64x32(mk, pk ? odd2((uint32_t)L.l, k2) : 0u);
+                    L.M ^= (T)ubk;
+                    L.S -= prk;
+#elif CNT_D2_SELFREE
                     // predicate folded into the operands (no 64-bit selects on the ALU pipe, the kernel's
                     // limiting pipe): the multiplier is 0 and the shift 64 (PTX clamps: a zero bit) when
                     // this lane does not pop
@@ -804,7 +823,12 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(wd), "=l"(mv)
                              : "r"(CNT_OPAQUE_K ? mad_u32((uint32_t)vslot, k16, tab.sb) : tab.sb + (uint32_t)vslot * 16u) : "memory");
                 const uint64_t prod = mul64x32(mv, odd2((uint32_t)(take ? l + 1 : l), k2));
+#if CNT_BIT_TAB
+                T vbit;
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(vbit) : "r"(mad_u32((uint32_t)v, k8, bitb)) : "memory");
+#else
                 const T vbit = (T)1 << v;
+#endif
                 const T Mw = L.M | vbit;
                 const T avail = ~Mw | L.sbit;  // vertices a child of v may move to
                 const uint32_t w32 = (uint32_t)wd;
@@ -1065,5 +1089,6 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
 }
 #undef k2
 #undef k16
+#undef k8
 
 }  // namespace tpg

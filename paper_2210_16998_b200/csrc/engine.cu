@@ -862,6 +862,7 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.tp = (mode != M_REC) ? P.cur_tp : nullptr;
         A.prune = (mode != M_REC && !seg) ? P.cur_prune : 0;
         A.k2 = 2;
+        A.k8 = 8;
         A.k16 = 16;
         A.item_cap = (mode != M_REC && seg) ? std::min<uint64_t>(hlim, P.citems.cap / sizeof(ItemS)) : 0;
         const size_t tab_bytes = (size_t)H.n * sizeof(Slot<W>);

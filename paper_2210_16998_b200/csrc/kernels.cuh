@@ -263,7 +263,7 @@ struct DfsArgs {
     unsigned long long item_cap;  //   (cacc[7] = item slots reserved)
     const TpTerm *tp;             // count modes: non-null = hash the prime paths' TEST PATHS (per slot)
     int32_t prune;                // count modes, prime-path phase: NEXT #2 reachability pruning (P_PRUNE)
-    uint32_t k2, k16;             // = 2, 16: multipliers the count kernel keeps opaque to ptxas (count.cuh)
+    uint32_t k2, k8, k16;         // = 2, 8, 16: multipliers the count kernel keeps opaque to ptxas (count.cuh)
 };
 
 // 256 threads per block for W <= 2; 128 for W = 4 (the per-lane path needs 64*W bytes of smem)
