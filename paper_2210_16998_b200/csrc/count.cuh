@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                             L.rem = 0;
                     }
                     if constexpr (D2) L.cur = d2_bytes<T>(L.rem);
-                    const bool ex = D2 ? ((__ldg(G.slot_d2 + 2 * (L.vb + u)) >> 16) & 1) != 0 : ((L.exm >> u) & 1) != 0;
+                    const bool ex = D2 ? ((__ldg(G.slot_d2 + 2 * (L.vb + u)) >> 40) & 1) != 0 : ((L.exm >> u) & 1) != 0;
                     if constexpr (SEG) {  // tail segment (succ(u) on the path) or transit segments (R8, R9)
                         st_other = ex || (su & ~L.M) == 0;
                         st_kind = ex ? EK_TRANSIT : EK_TAIL;
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 const bool act = L.active && !L.done;
 #pragma unroll
                 for (int k = 0; k < CNT_D2_POPS; k++) {  // pops first (straight-line, predicated)
-                    const bool pk = act & ((L.cur & 0xffu) == 0xffu) & (L.l > L.r);
+                    const bool pk = act & (((~L.cur) & 0xffu) == 0u) & (L.l > L.r);
                     const uint32_t ek = lds_u16(pb + (uint32_t)L.l * PST);
                     const int uk = (int)(ek & 0xffu);
                     uint64_t mk;
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 const uint32_t cur = L.cur;
                 const int l = L.l;
                 const uint32_t a = cur & 0xffu;  // (take) the child
-                const bool empty = a == 0xffu;
+                const bool empty = ((~cur) & 0xffu) == 0u;
                 if (act & empty & (l == L.r)) L.done = true;  // the unit's subtree is finished
                 const bool pop = (CNT_D2_POPS == 0) & act & empty & (l > L.r);
                 TPG_DCHECK(!act || (l >= L.r && l < PLEV), "cnt: depth out of range");
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 const uint32_t e = CNT_D2_POPS == 0 ? lds_u16(pb + (uint32_t)l * PST) : 0u;  // {path[l], the untried child of level l-1}
                 const int v = take ? (int)a : (int)(e & 0xffu);     // the child, or the vertex popped
                 const int vslot = L.vb + v;
-                uint64_t wd, mv;  // {t0 | t1 << 8 | exit << 16, mix64(gid)} of v
+                uint64_t wd, mv;  // {t0 | t1 << 32 | exit << 40, mix64(gid)} of v
                 asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(wd), "=l"(mv)
                              : "r"(CNT_OPAQUE_K ? mad_u32((uint32_t)vslot, k16, tab.sb) : tab.sb + (uint32_t)vslot * 16u) : "memory");
                 const uint64_t prod = mul64x32(mv, odd2((uint32_t)(take ? l + 1 : l), k2));
@@ -831,14 +831,14 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
 #endif
                 const T Mw = L.M | vbit;
                 const T avail = ~Mw | L.sbit;  // vertices a child of v may move to
-                const uint32_t w32 = (uint32_t)wd;
-                const uint32_t t0 = w32 & 0xffu, t1 = (w32 >> 8) & 0xffu;  // (a missing one is v: never available)
+                const uint32_t w1 = (uint32_t)(wd >> 32);
+                const uint32_t t0 = (uint32_t)wd, t1 = w1 & 0xffu;  // (a missing one is v: never available)
                 // straight-line (bitwise, no short-circuit branches): the availability bits of t0, t1
                 const uint32_t ok0 = (uint32_t)(avail >> t0) & 1u, ok1 = (uint32_t)(avail >> t1) & 1u;
                 const uint32_t first = ok0 ? t0 : (ok1 ? t1 : 0xffu);
                 const uint32_t cw = first | ((ok0 & ok1) ? (t1 << 8) : 0xff00u);
                 const bool clo = (int)a == L.s;
-                const bool ex = HX && ((w32 >> 16) & 1u) != 0;
+                const bool ex = HX && (w1 & 0x100u) != 0;
                 const bool leaf = (ok0 | ok1) == 0u;
                 const bool pok = (L.ps & ~L.M) == 0;   // pred(s) within path[0..l]
                 const bool pokw = (L.ps & ~Mw) == 0;   // ... within path[0..l] + v

@@ -216,7 +216,8 @@ tpgen_status plan_upload(PlanImpl &P, cudaStream_t s) {
                 const uint64_t t0 = sn ? (uint64_t)__builtin_ctzll(sn) : (uint64_t)i;
                 sn &= sn - 1;
                 const uint64_t t1 = sn ? (uint64_t)__builtin_ctzll(sn) : (uint64_t)i;
-                t2[2 * (size_t)sl] = t0 | (t1 << 8) | ((H.slot_out_cnt[sl] > 0 ? 1ull : 0ull) << 16);
+                // t0 and t1 in words of their own (shift amounts without masking), exit next to t1
+                t2[2 * (size_t)sl] = t0 | (t1 << 32) | ((H.slot_out_cnt[sl] > 0 ? 1ull : 0ull) << 40);
                 t2[2 * (size_t)sl + 1] = sm[sl];
             }
         if (const char *ev = getenv("TPGEN_NO_D2")) d2 = d2 && atoi(ev) == 0;  // A/B hook

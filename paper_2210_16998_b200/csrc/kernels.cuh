@@ -158,7 +158,7 @@ struct DevGraph {
     const uint64_t *slot_mix;  // per slot: mix64(global id), the vertex's digest value (R20)
     const uint64_t *vmix;      // per global vertex id: mix64(id)
     const uint64_t *scc_exm;   // per SCC (<= 64 vertices): local bits of its exit vertices (Def. 5)
-    const uint64_t *slot_d2;   // in-SCC out-degree <= 2 everywhere: {t0 | t1 << 8 | exit << 16, mix} per slot, else null
+    const uint64_t *slot_d2;   // in-SCC out-degree <= 2 everywhere: {t0 | t1 << 32 | exit << 40, mix} per slot, else null
     const int32_t *v_slot;     // per global vertex id: its slot
     const int32_t *comp;       // per global vertex id: its SCC
     int32_t shard_lo, shard_hi;
