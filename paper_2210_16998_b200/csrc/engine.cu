@@ -840,6 +840,10 @@ static tpgen_status dfs_phase(PlanImpl &P, const DevGraph &G, RootSpan<MT<T>::W>
         A.eager_gens = P.presplit_active ? 1 : kEagerGens;
         if (const char *ev = getenv("TPGEN_SPLIT_MIN")) A.split_min = (uint32_t)atoi(ev);  // tuning knobs
         if (const char *ev = getenv("TPGEN_EAGER_GENS")) A.eager_gens = atoi(ev);
+        if (seg) {  // the segment phase starts from the SCC entries alone (config 5: 16 roots)
+            if (const char *ev = getenv("TPGEN_SEG_EAGER_GENS")) A.eager_gens = atoi(ev);
+            if (const char *ev = getenv("TPGEN_SEG_SPLIT_MIN")) A.split_min = (uint32_t)atoi(ev);
+        }
         A.dbg = nullptr;
         if (getenv("TPGEN_DEBUG")) {
             TPG_TRY(P.dbgbuf.ensure(160 * 8, s));
