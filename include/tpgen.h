@@ -241,6 +241,20 @@ tpgen_status tpgen_shard_units(const int64_t *csr_offsets, const int32_t *csr_ta
                                int32_t rank, int32_t count, int32_t *applies, int64_t *unit_lo,
                                int64_t *unit_hi, int64_t *n_units, int32_t *lo, int32_t *hi);
 
+/*
+ * The units of prefix-unit shard `rank` of `count` (host only; what tpgen_shard_units counts):
+ * unit i is the path vertices[offsets[i] .. offsets[i+1]) (global ids, the start first); closure[i]
+ * = 1: the unit is the closing arc of that path back to its start (one cyclic prime path), 0: the
+ * trie subtree under the path (every prime path that has it as a prefix).  Two-call pattern:
+ * *n_units_out / *n_vertices_out are always set; the arrays (n_units + 1 offsets, n_units closure
+ * flags, n_vertices ids) are written when every pointer is non-NULL and the capacities suffice,
+ * else TPGEN_ERR_INVALID_ARGUMENT (graphs the split does not apply to: 0 units).
+ */
+tpgen_status tpgen_shard_unit_paths(const int64_t *csr_offsets, const int32_t *csr_targets, int32_t n_vertices,
+                                    int32_t rank, int32_t count, int64_t *offsets, int32_t *vertices,
+                                    int32_t *closure, int64_t cap_units, int64_t cap_vertices,
+                                    int64_t *n_units_out, int64_t *n_vertices_out);
+
 /* Structure metrics of a CFG (Table 1; host only). */
 typedef struct {
     int64_t nodes, edges;      /* V, E */

@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _abi
 
-__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "metrics", "shard_range", "shard_units",
+__all__ = ["TpgenError", "PathSet", "Plan", "prime_paths", "test_paths", "components", "metrics", "shard_range", "shard_units", "shard_unit_paths",
            "library", "version"]
 
 
@@ -331,6 +331,23 @@ def shard_units(graph, rank: int, count: int) -> Dict[str, Any]:
                                  ctypes.byref(uh), ctypes.byref(nu), ctypes.byref(lo), ctypes.byref(hi)))
     return {"applies": bool(ap.value), "unit_lo": int(ul.value), "unit_hi": int(uh.value),
             "n_units": int(nu.value), "lo": int(lo.value), "hi": int(hi.value)}
+
+
+def shard_unit_paths(graph, rank: int, count: int):
+    """The prefix units of shard ``rank`` of ``count`` (``tpgen_shard_unit_paths``, host): a list of
+    ``(path, closure)`` -- ``path`` the unit's global vertex ids (start first); ``closure`` True:
+    the cyclic prime path path + [start], False: every prime path with ``path`` as a prefix."""
+    lib = library()
+    so, st, n = _csr(graph)
+    nu, nv = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.tpgen_shard_unit_paths(_p64(so), _p32(st), n, rank, count, None, None, None, 0, 0,
+                                      ctypes.byref(nu), ctypes.byref(nv)))
+    off = np.zeros(nu.value + 1, dtype=np.int64)
+    vert = np.zeros(max(nv.value, 1), dtype=np.int32)
+    clo = np.zeros(max(nu.value, 1), dtype=np.int32)
+    _check(lib.tpgen_shard_unit_paths(_p64(so), _p32(st), n, rank, count, _p64(off), _p32(vert), _p32(clo),
+                                      nu.value, nv.value, ctypes.byref(nu), ctypes.byref(nv)))
+    return [(tuple(vert[off[i]:off[i + 1]].tolist()), bool(clo[i])) for i in range(nu.value)]
 
 
 def release_cache() -> None:

@@ -84,6 +84,9 @@ SYMBOLS = {
     "tpgen_shard_units": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32, POINTER(c_int32),
                                   POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32),
                                   POINTER(c_int32)]),
+    "tpgen_shard_unit_paths": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32,
+                                       POINTER(c_int64), POINTER(c_int32), POINTER(c_int32), c_int64, c_int64,
+                                       POINTER(c_int64), POINTER(c_int64)]),
     "tpgen_metrics_compute": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, c_int32, c_int32,
                                       POINTER(Metrics)]),
     "tpgen_normalize_outdeg2": (c_int, [POINTER(c_int64), POINTER(c_int32), c_int32, POINTER(c_int32),

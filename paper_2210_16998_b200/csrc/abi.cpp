@@ -383,6 +383,43 @@ tpgen_status tpgen_shard_units(const int64_t *so, const int32_t *st, int32_t n, 
     return TPGEN_OK;
 }
 
+tpgen_status tpgen_shard_unit_paths(const int64_t *so, const int32_t *st, int32_t n, int32_t rank, int32_t count,
+                                    int64_t *offsets, int32_t *vertices, int32_t *closure, int64_t cap_units,
+                                    int64_t cap_vertices, int64_t *n_units_out, int64_t *n_vertices_out) {
+    if (n < 0 || !n_units_out || !n_vertices_out || count < 1 || rank < 0 || rank >= count) {
+        tpg::set_error("bad shard spec, NULL count pointers or n < 0");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    tpg::HostPlan P;
+    std::string msg;
+    tpgen_status s = tpg::build_plan(so, st, n, P, msg, true);
+    if (s != TPGEN_OK) {
+        tpg::set_error(msg);
+        return s;
+    }
+    tpg::PrefixShard ps;
+    if (tpg::prefix_shard_applies(P)) tpg::prefix_shard(P, rank, count, ps);
+    int64_t nv = 0;
+    for (const tpg::PrefixUnit &u : ps.units) nv += u.depth + 1;
+    *n_units_out = (int64_t)ps.units.size();
+    *n_vertices_out = nv;
+    if (!offsets || !vertices || !closure) return TPGEN_OK;
+    if (cap_units < (int64_t)ps.units.size() || cap_vertices < nv) {
+        tpg::set_error("unit arrays too small");
+        return TPGEN_ERR_INVALID_ARGUMENT;
+    }
+    int64_t o = 0;
+    for (size_t i = 0; i < ps.units.size(); i++) {
+        const tpg::PrefixUnit &u = ps.units[i];
+        offsets[i] = o;
+        closure[i] = u.closure ? 1 : 0;
+        const int32_t vb = P.scc_vbase[u.scc];
+        for (int d = 0; d <= u.depth; d++) vertices[o++] = P.slot_gid[vb + u.path[d]];
+    }
+    offsets[ps.units.size()] = o;
+    return TPGEN_OK;
+}
+
 tpgen_status tpgen_metrics_compute(const int64_t *so, const int32_t *st, int32_t n, int32_t start, int32_t end,
                                    tpgen_metrics *m) {
     if (n < 0 || !m || (n > 0 && (start < 0 || start >= n || end < 0 || end >= n))) {

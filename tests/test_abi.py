@@ -235,3 +235,35 @@ def test_shard_units_tile_the_split():
         assert c["unit_lo"] == c["unit_hi"] == c["n_units"] == 0
     with pytest.raises(tp.TpgenError):
         tp.shard_units(g, 3, 3)
+
+
+def _unit_of(pp, units):
+    """Index of the prefix unit a prime path belongs to (tpgen_shard_unit_paths semantics)."""
+    hits = [i for i, (path, clo) in enumerate(units)
+            if (clo and pp == path + (path[0],)) or (not clo and pp[:len(path)] == path)]
+    assert len(hits) == 1, (pp, hits)
+    return hits[0]
+
+
+@pytest.mark.parametrize("world", [2, 5, 16])
+def test_prefix_units_partition_the_oracle_list(world):
+    """The prefix-unit split on the host, pinned by the oracle: the units of all shards, in rank
+    order, partition the oracle's canonical prime-path list into contiguous runs in unit order
+    (so shard r's output is block r of the global list), and each shard's units are the
+    [unit_lo, unit_hi) range tpgen_shard_units reports."""
+    for g in (gen.dense_scc(12, 3, 7), gen.dense_scc(9, 4, 3),
+              gen.disjoint_union([gen.dense_scc(10, 3, 1), gen.dense_scc(7, 3, 2)], name="pfx_union")):
+        units, bounds = [], []
+        for r in range(world):
+            u = tp.shard_unit_paths(g, r, world)
+            c = tp.shard_units(g, r, world)
+            assert c["applies"] and len(u) == c["unit_hi"] - c["unit_lo"] and c["unit_lo"] == len(units)
+            if u:
+                assert (u[0][0][0], u[-1][0][0] + 1) == (c["lo"], c["hi"])
+            units += u
+            bounds.append(len(units))
+        assert len(units) == tp.shard_units(g, 0, world)["n_units"]
+        off, vert = oracle.prime_paths(g)
+        idx = [_unit_of(tuple(vert[off[i]:off[i + 1]].tolist()), units) for i in range(len(off) - 1)]
+        assert idx == sorted(idx), g.name  # canonical order = unit order
+    assert tp.shard_unit_paths(gen.config5(), 0, 4) == []  # arcs leave its SCCs: no prefix split

@@ -188,3 +188,78 @@ def test_sharded_prime_paths_gloo():
     # C4: rank 0 holds the whole canonical list, element by element
     assert np.array_equal(np.asarray(whole[0], dtype=np.int64), off)
     assert np.array_equal(np.asarray(whole[1], dtype=np.int32), vert)
+
+
+def _worker_prefix(rank: int, world: int, port: int, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2210_16998_b200 as tp
+    from paper_2210_16998_b200 import PathSet
+    from paper_2210_16998_b200.distributed import sharded_prime_paths
+    from workloads import generators as gen
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = gen.dense_scc(9, 4, 3)  # 9 start vertices, one SCC: prefix units cut the heavy starts
+
+        def compute(r, w):  # the oracle's prime paths of this rank's prefix units (the host split)
+            units = tp.shard_unit_paths(g, r, w)
+            off, vert = oracle.prime_paths(g)
+            keep = []
+            for i in range(len(off) - 1):
+                pp = tuple(vert[off[i]:off[i + 1]].tolist())
+                if any((c and pp == p + (p[0],)) or (not c and pp[:len(p)] == p) for p, c in units):
+                    keep.append(pp)
+            o = np.zeros(len(keep) + 1, dtype=np.int64)
+            o[1:] = np.cumsum([len(p) for p in keep])
+            v = np.asarray([x for p in keep for x in p], dtype=np.int32)
+            lo, hi = oracle.digest(o, v)
+            st = {"n_paths": len(keep), "total_vertices": int(o[-1]), "n_extensions": 0,
+                  "hash_lo": lo, "hash_hi": hi}
+            return PathSet(o, v, len(keep), False, st)
+
+        res = sharded_prime_paths(g, compute=compute, gather=True, shard_prefix=True)
+        q.put(dict(rank=rank, pp_base=res.pp_base, n_paths=res.n_paths, digest=res.digest,
+                   local=len(res.paths.offsets) - 1,
+                   whole=(res.whole[0].tolist(), res.whole[1].tolist()) if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_prefix_shards_gloo():
+    """Prefix-unit shards (tpgen_options.shard_prefix) through the same exchange: each rank's
+    block is its units' prime paths, the blocks' global offsets tile the list, and the C4 gather
+    on rank 0 equals the oracle's whole canonical list element by element."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    from workloads import generators as gen
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_prefix, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=240), q.get(timeout=240)], key=lambda x: x["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = gen.dense_scc(9, 4, 3)
+    off, vert = oracle.prime_paths(g)
+    assert got[0]["pp_base"] == 0 and got[1]["pp_base"] == got[0]["local"]
+    assert got[0]["local"] > 0 and got[1]["local"] > 0
+    assert got[0]["local"] + got[1]["local"] == len(off) - 1 == got[1]["n_paths"]
+    assert tuple(got[1]["digest"]) == oracle.digest(off, vert)
+    whole = got[0]["whole"]
+    assert np.array_equal(np.asarray(whole[0], dtype=np.int64), off)
+    assert np.array_equal(np.asarray(whole[1], dtype=np.int32), vert)
