@@ -183,6 +183,10 @@ __device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, 
 // CNT_OPAQUE_K: the D2 pass's constant multipliers (2 for the weight, 16 for the table stride)
 // come from blockDim.x (= 256, unknown to ptxas), so the products stay IMADs (FMA pipe) instead
 // of being strength-reduced to LEA / shift-or (ALU pipe)
+#ifndef CNT_PASS_UNROLL
+#define CNT_PASS_UNROLL 2  // passes per iteration of the pass loop (config 5 cnt_kernel 103.46 -> 102.78 ms at 2)
+#endif
+constexpr int kCntPassUnroll = CNT_PASS_UNROLL;
 #ifndef CNT_BIT_TAB
 #define CNT_BIT_TAB 1  // D2: one-bit masks from a 512-byte shared table (no SHF / SEL on the ALU pipe)
 #endif
@@ -766,7 +770,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
         uint32_t ext32 = 0;
 #pragma unroll 1
         for (int blk = 0; blk < CNT_PASSES / RING; blk++) {
-#pragma unroll 1
+#pragma unroll kCntPassUnroll
             for (int t = 0; t < RING; t++) {
               if constexpr (D2) {
                 const bool act = L.active && !L.done;
