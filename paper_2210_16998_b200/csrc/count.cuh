@@ -187,6 +187,9 @@ __device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, 
 #define CNT_PASS_UNROLL 2  // passes per iteration of the pass loop (config 5 cnt_kernel 103.46 -> 102.78 ms at 2)
 #endif
 constexpr int kCntPassUnroll = CNT_PASS_UNROLL;
+#ifndef CNT_BIT_TAB_TAKE
+#define CNT_BIT_TAB_TAKE 1  // the take's bit from the table too (0: two shifts on the ALU pipe instead)
+#endif
 #ifndef CNT_BIT_TAB
 #define CNT_BIT_TAB 1  // D2: one-bit masks from a 512-byte shared table (no SHF / SEL on the ALU pipe)
 #endif
@@ -828,7 +831,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(wd), "=l"(mv)
                              : "r"(CNT_OPAQUE_K ? mad_u32((uint32_t)vslot, k16, tab.sb) : tab.sb + (uint32_t)vslot * 16u) : "memory");
                 const uint64_t prod = mul64x32(mv, odd2((uint32_t)(take ? l + 1 : l), k2));
-#if CNT_BIT_TAB
+#if CNT_BIT_TAB && CNT_BIT_TAB_TAKE
                 T vbit;
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(vbit) : "r"(mad_u32((uint32_t)v, k8, bitb)) : "memory");
 #else
