@@ -187,6 +187,9 @@ __device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, 
 #define CNT_PASS_UNROLL 2  // passes per iteration of the pass loop (config 5 cnt_kernel 103.46 -> 102.78 ms at 2)
 #endif
 constexpr int kCntPassUnroll = CNT_PASS_UNROLL;
+#ifndef CNT_ACT_REG
+#define CNT_ACT_REG 1  // (config 5 cnt_kernel 102.79 -> 101.07 ms) D2: the lane's stepping flag kept across the passes, L.done written after them
+#endif
 #ifndef CNT_BIT_TAB_TAKE
 #define CNT_BIT_TAB_TAKE 1  // the take's bit from the table too (0: two shifts on the ALU pipe instead)
 #endif
@@ -772,12 +775,13 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
         // (the popped one or the child), its digest term mix(v)*(2 pos+1), the visited-bit
         // toggle and the depth change are the same operations either way
         uint32_t ext32 = 0;
+        bool actp = L.active && !L.done;  // (D2, CNT_ACT_REG) stepping, kept across the passes; L.done after them
 #pragma unroll 1
         for (int blk = 0; blk < CNT_PASSES / RING; blk++) {
 #pragma unroll PASS_UNROLL
             for (int t = 0; t < RING; t++) {
               if constexpr (D2) {
-                const bool act = L.active && !L.done;
+                const bool act = CNT_ACT_REG ? actp : (L.active && !L.done);
 #pragma unroll
                 for (int k = 0; k < CNT_D2_POPS; k++) {  // pops first (straight-line, predicated)
                     const bool pk = act & (((~L.cur) & 0xffu) == 0u) & (L.l > L.r);
@@ -820,7 +824,8 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                 const int l = L.l;
                 const uint32_t a = cur & 0xffu;  // (take) the child
                 const bool empty = ((~cur) & 0xffu) == 0u;
-                if (act & empty & (l == L.r)) L.done = true;  // the unit's subtree is finished
+                if (CNT_ACT_REG) actp = act & !(empty & (l == L.r));  // the unit's subtree is finished
+                else if (act & empty & (l == L.r)) L.done = true;
                 const bool pop = (CNT_D2_POPS == 0) & act & empty & (l > L.r);
                 TPG_DCHECK(!act || (l >= L.r && l < PLEV), "cnt: depth out of range");
                 const bool take = act & !empty;
@@ -967,6 +972,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
             }
             drain();
         }
+        if (D2 && CNT_ACT_REG && L.active && !actp) L.done = true;
         t_ext += ext32;
         t_pp += r_pp;
         t_vert += r_vert;
