@@ -187,6 +187,9 @@ __device__ __forceinline__ bool prune_keep(const Tab &tab, int vb, T ps, int w, 
 #define CNT_PASS_UNROLL 2  // passes per iteration of the pass loop (config 5 cnt_kernel 103.46 -> 102.78 ms at 2)
 #endif
 constexpr int kCntPassUnroll = CNT_PASS_UNROLL;
+#ifndef CNT_POP_PRED
+#define CNT_POP_PRED 0  // D2: the pops' shared loads predicated on the pop (see the pass)
+#endif
 #ifndef CNT_ACT_REG
 #define CNT_ACT_REG 1  // (config 5 cnt_kernel 102.79 -> 101.07 ms) D2: the lane's stepping flag kept across the passes, L.done written after them
 #endif
@@ -785,6 +788,17 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
 #pragma unroll
                 for (int k = 0; k < CNT_D2_POPS; k++) {  // pops first (straight-line, predicated)
                     const bool pk = act & (((~L.cur) & 0xffu) == 0u) & (L.l > L.r);
+#if CNT_POP_PRED
+                    // only popping lanes touch shared memory (the LSU pipe is the busiest: 85 %); the
+                    // others read 0 (vertex 0, weight 0)
+                    uint32_t ek;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tmov.u32 %0, 0;\n\t@p ld.shared.u16 %0, [%1];\n\t}"
+                                 : "=r"(ek) : "r"(pb + (uint32_t)L.l * PST), "r"((uint32_t)pk) : "memory");
+                    const int uk = (int)(ek & 0xffu);
+                    uint64_t mk;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tmov.b64 %0, 0;\n\t@p ld.shared.u64 %0, [%1];\n\t}"
+                                 : "=l"(mk) : "r"(mad_u32((uint32_t)(L.vb + uk), k16, tab.sb + 8u)), "r"((uint32_t)pk) : "memory");
+#else
                     const uint32_t ek = lds_u16(pb + (uint32_t)L.l * PST);
                     const int uk = (int)(ek & 0xffu);
                     uint64_t mk;
@@ -792,6 +806,7 @@ __global__ void __launch_bounds__(CntCfg<T>::threads, cnt_min_blocks<T>(PH == P_
                         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(mk) : "r"(mad_u32((uint32_t)(L.vb + uk), k16, tab.sb + 8u)) : "memory");
                     else
                         mk = tab.mix(L.vb + uk);
+#endif
 #if CNT_BIT_TAB
                     // the popped vertex's bit from the shared bit table by a predicated load (0 when this
                     // lane does not pop), the weight 0 when it does not: no shifts, no 64-bit selects
